@@ -1,0 +1,1190 @@
+// capi.cu — the device layer of the C ABI declared in include/flz.h.
+//
+// Everything here runs on the GPU; there is no CPU fallback (flz_ctx_create fails with
+// FLZ_ENODEV when no sm_100 device is present).  Host code in this file only builds
+// data structures (SELL-C-sigma conversion, halo plan) and sequences kernel launches.
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <numeric>
+
+#include "flz_internal.hpp"
+
+using namespace flz;
+
+namespace flz {
+namespace {
+thread_local std::string g_last_error;
+std::atomic<uint64_t> g_matvecs{0};
+}  // namespace
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+}  // namespace flz
+
+namespace {
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return FLZ_OK;
+  } catch (const ApiError& e) {
+    set_last_error(e.what());
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    set_last_error("out of host memory");
+    return FLZ_ENOMEM;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return FLZ_EINVAL;
+  }
+}
+
+void use(const flz_ctx* ctx) { FLZ_CUDA(cudaSetDevice(ctx->device)); }
+
+struct Pinned {  // small RAII pinned host array
+  double* p = nullptr;
+  explicit Pinned(size_t count) { FLZ_CUDA(cudaMallocHost(&p, count * sizeof(double))); }
+  ~Pinned() { if (p) cudaFreeHost(p); }
+  Pinned(const Pinned&) = delete;
+  Pinned& operator=(const Pinned&) = delete;
+};
+
+void allreduce(flz_ctx* ctx, double* buf, size_t count) {
+  if (ctx->nranks == 1 || count == 0) return;
+  FLZ_NCCL(ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, ctx->comm, ctx->stream));
+}
+
+SellView view_all(const flz_matrix* A) {
+  return SellView{A->slice_ptr.p, A->slice_len.p, A->row_len.p, A->col.p,
+                  A->val.p,       nullptr,        A->nslices,   A->nl};
+}
+SellView view_list(const flz_matrix* A, const int32_t* ids, int64_t count) {
+  return SellView{A->slice_ptr.p, A->slice_len.p, A->row_len.p, A->col.p,
+                  A->val.p,       ids,            count,        A->nl};
+}
+
+void ensure_workspaces(const flz_matrix* A) {
+  flz_ctx* ctx = A->ctx;
+  const size_t need = (size_t)(A->nl + A->nhalo) * kMaxFuse + 8;
+  if (A->y1.count < need) {
+    A->y1.reserve_zero(need, ctx->stream);
+    A->y2.reserve_zero(need, ctx->stream);
+  }
+}
+
+// Halo exchange of the gather source Y1 (interleaved, R doubles per row): pack the rows
+// the peers reference, send/recv on the comm stream, leave ev_halo_done for the boundary
+// launch.  The caller launches the interior slices in between.
+void halo_begin(const flz_matrix* A, int R, double* Y1) {
+  flz_ctx* ctx = A->ctx;
+  launch_pack_rows(ctx, ctx->stream, A->n_send, R, A->send_rows.p, Y1, A->send_buf.p);
+  FLZ_CUDA(cudaEventRecord(ctx->ev_halo_ready, ctx->stream));
+  FLZ_CUDA(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_halo_ready, 0));
+  FLZ_NCCL(ncclGroupStart());
+  for (const auto& p : A->peers) {
+    if (p.send_count)
+      FLZ_NCCL(ncclSend(A->send_buf.p + p.send_off * R, (size_t)p.send_count * R, ncclDouble,
+                        p.rank, ctx->comm, ctx->comm_stream));
+    if (p.recv_count)
+      FLZ_NCCL(ncclRecv(Y1 + (A->nl + p.recv_off) * R, (size_t)p.recv_count * R, ncclDouble,
+                        p.rank, ctx->comm, ctx->comm_stream));
+  }
+  FLZ_NCCL(ncclGroupEnd());
+  FLZ_CUDA(cudaEventRecord(ctx->ev_halo_done, ctx->comm_stream));
+}
+
+// One fused step over the whole local matrix, with the halo exchange overlapped with the
+// interior slices when the context is distributed.
+void sell_step(const flz_matrix* A, int R, StepMode mode, double s1, double s2, double b,
+               double* Y1, double* Y2, const double* X, int64_t ldx, double* Out, int64_t ldo) {
+  flz_ctx* ctx = A->ctx;
+  if (ctx->nranks == 1 || A->peers.empty()) {
+    launch_clenshaw_step(ctx, view_all(A), R, mode, ctx->exact, s1, s2, b, Y1, Y2, X, ldx, Out,
+                         ldo);
+    return;
+  }
+  halo_begin(A, R, Y1);
+  launch_clenshaw_step(ctx, view_list(A, A->interior.p, A->n_interior), R, mode, ctx->exact, s1,
+                       s2, b, Y1, Y2, X, ldx, Out, ldo);
+  FLZ_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_halo_done, 0));
+  launch_clenshaw_step(ctx, view_list(A, A->boundary.p, A->n_boundary), R, mode, ctx->exact, s1,
+                       s2, b, Y1, Y2, X, ldx, Out, ldo);
+}
+
+// Z[:, 0..ncols) = A X[:, 0..ncols), device-resident column-major blocks (permuted rows).
+void spmm_device(const flz_matrix* A, const double* X, int64_t ldx, int ncols, double* Z,
+                 int64_t ldz, bool counted) {
+  flz_ctx* ctx = A->ctx;
+  ensure_workspaces(A);
+  for (int c0 = 0; c0 < ncols; c0 += kMaxFuse) {
+    const int R = std::min(kMaxFuse, ncols - c0);
+    launch_interleave(ctx, A->nl, R, 1.0, X + (int64_t)c0 * ldx, ldx, A->y1.p);
+    sell_step(A, R, StepMode::plain, 1.0, 0.0, 0.0, A->y1.p, A->y2.p, nullptr, 0,
+              Z + (int64_t)c0 * ldz, ldz);
+  }
+  if (counted) g_matvecs.fetch_add((uint64_t)ncols, std::memory_order_relaxed);
+}
+
+// Z = p((A - cI)/e) X by block Clenshaw (filter.cpp:122-155), device-resident blocks.
+void filter_device(const flz_matrix* A, const double* coeffs, int m, double c, double e,
+                   const double* X, int64_t ldx, int ncols, double* Z, int64_t ldz) {
+  flz_ctx* ctx = A->ctx;
+  ensure_workspaces(A);
+  const double inv_e = 1.0 / e;                                  // filter.cpp:128
+  const double s1 = 2.0 * inv_e, s2 = -2.0 * c * inv_e;          // filter.cpp:148
+  const double f1 = inv_e, f2 = -c * inv_e;                      // filter.cpp:153
+  for (int c0 = 0; c0 < ncols; c0 += kMaxFuse) {
+    const int R = std::min(kMaxFuse, ncols - c0);
+    const double* Xc = X + (int64_t)c0 * ldx;
+    double* Zc = Z + (int64_t)c0 * ldz;
+    if (m == 0) {  // Y = b_0 X, no products (filter.cpp:133-136)
+      for (int k = 0; k < R; ++k)
+        launch_interleave(ctx, A->nl, 1, coeffs[0], Xc + (int64_t)k * ldx, ldx,
+                          Zc + (int64_t)k * ldz);
+      continue;
+    }
+    double* Y1 = A->y1.p;
+    double* Y2 = A->y2.p;
+    launch_interleave(ctx, A->nl, R, coeffs[m], Xc, ldx, Y1);                  // :144
+    FLZ_CUDA(cudaMemsetAsync(Y2, 0, (size_t)A->nl * R * sizeof(double), ctx->stream));
+    for (int j = m - 1; j >= 1; --j) {                                          // :146-151
+      sell_step(A, R, StepMode::step, s1, s2, coeffs[j], Y1, Y2, Xc, ldx, nullptr, 0);
+      std::swap(Y1, Y2);
+    }
+    sell_step(A, R, StepMode::final, f1, f2, coeffs[0], Y1, Y2, Xc, ldx, Zc, ldz);  // :152-154
+    g_matvecs.fetch_add((uint64_t)R * (uint64_t)m, std::memory_order_relaxed);
+  }
+}
+
+// host (n_local x ncols, column-major, ld = nl, original row order) -> device block in the
+// matrix's permuted order (ld = A->ld, pad rows untouched)
+void upload_block(const flz_matrix* A, const double* host, int ncols, double* dst) {
+  flz_ctx* ctx = A->ctx;
+  if (A->nl == 0 || ncols == 0) return;
+  if (A->sigma <= 1) {
+    FLZ_CUDA(cudaMemcpy2DAsync(dst, A->ld * sizeof(double), host, A->nl * sizeof(double),
+                               A->nl * sizeof(double), ncols, cudaMemcpyHostToDevice,
+                               ctx->stream));
+    return;
+  }
+  ctx->stage.reserve((size_t)A->nl * ncols);
+  FLZ_CUDA(cudaMemcpyAsync(ctx->stage.p, host, (size_t)A->nl * ncols * sizeof(double),
+                           cudaMemcpyHostToDevice, ctx->stream));
+  launch_permute_in(ctx, ctx->stage.p, A->nl, dst, A->ld, ncols, A->nl, A->perm.p);
+}
+
+void download_block(const flz_matrix* A, const double* src, int ncols, double* host) {
+  flz_ctx* ctx = A->ctx;
+  if (A->nl == 0 || ncols == 0) return;
+  if (A->sigma <= 1) {
+    FLZ_CUDA(cudaMemcpy2DAsync(host, A->nl * sizeof(double), src, A->ld * sizeof(double),
+                               A->nl * sizeof(double), ncols, cudaMemcpyDeviceToHost,
+                               ctx->stream));
+  } else {
+    ctx->stage2.reserve((size_t)A->nl * ncols);
+    launch_permute_out(ctx, src, A->ld, ctx->stage2.p, A->nl, ncols, A->nl, A->perm.p);
+    FLZ_CUDA(cudaMemcpyAsync(host, ctx->stage2.p, (size_t)A->nl * ncols * sizeof(double),
+                             cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  FLZ_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+void ensure_xz(const flz_matrix* A, int ncols) {
+  flz_ctx* ctx = A->ctx;
+  const size_t need = (size_t)A->ld * ncols;
+  if (A->xs.count < need) A->xs.reserve_zero(need, ctx->stream);
+  if (A->zs.count < need) A->zs.reserve_zero(need, ctx->stream);
+}
+
+// layout of ctx->small during a block step
+struct SmallLayout {
+  int64_t capC;     // doubles per coefficient block (cols x ldc)
+  int ldc;          // row stride of C1/C2 (multiple of 8 covering r)
+  int64_t C1, C2, gram, Sk, t1, t2, normsq, inv, dead, scale, total;
+};
+constexpr int kRMax = 16;
+SmallLayout small_layout(int64_t max_cols, int r) {
+  SmallLayout L;
+  L.ldc = (int)round_up(r, 8);
+  L.capC = (max_cols + 2 * kRMax) * L.ldc;
+  L.C1 = 0;
+  L.C2 = L.C1 + L.capC;
+  L.gram = L.C2 + L.capC;
+  L.Sk = L.gram + kRMax * kRMax;
+  L.t1 = L.Sk + kRMax * kRMax;                 // [r][kRMax rows][8]
+  L.t2 = L.t1 + kRMax * kRMax * 8;
+  L.normsq = L.t2 + kRMax * kRMax * 8;
+  L.inv = L.normsq + kRMax;
+  L.dead = L.inv + kRMax;
+  L.scale = L.dead + kRMax;
+  L.total = L.scale + 8;
+  return L;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* flz_last_error(void) { return g_last_error.c_str(); }
+const char* flz_version(void) { return "flz 0.1 (sm_100a; SELL-32-sigma Clenshaw SpMM; DMMA GEMMs)"; }
+
+// ---------------------------------------------------------------- context
+
+static int ctx_create_common(int device, int rank, int nranks, const void* uid, flz_ctx** out) {
+  return guarded([&] {
+    FLZ_REQUIRE(out != nullptr, FLZ_EINVAL, "ctx_create: null output");
+    int count = 0;
+    cudaError_t err = cudaGetDeviceCount(&count);
+    if (err != cudaSuccess || count == 0)
+      throw ApiError(FLZ_ENODEV,
+                     std::string("no CUDA device available (") + cudaGetErrorString(err) +
+                         "); libflz has no CPU fallback");
+    if (device < 0) FLZ_CUDA(cudaGetDevice(&device));
+    FLZ_REQUIRE(device < count, FLZ_EINVAL, "ctx_create: device index out of range");
+    cudaDeviceProp prop;
+    FLZ_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+      throw ApiError(FLZ_ENODEV, std::string("device '") + prop.name +
+                                     "' is not sm_100 (this library is built for sm_100a only)");
+    FLZ_CUDA(cudaSetDevice(device));
+    auto* ctx = new flz_ctx;
+    ctx->device = device;
+    ctx->sm_count = prop.multiProcessorCount;
+    ctx->rank = rank;
+    ctx->nranks = nranks;
+    FLZ_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    FLZ_CUDA(cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking));
+    FLZ_CUDA(cudaEventCreateWithFlags(&ctx->ev_halo_ready, cudaEventDisableTiming));
+    FLZ_CUDA(cudaEventCreateWithFlags(&ctx->ev_halo_done, cudaEventDisableTiming));
+    for (int i = 0; i < 16; ++i) {
+      FLZ_CUDA(cudaEventCreate(&ctx->t0[i]));
+      FLZ_CUDA(cudaEventCreate(&ctx->t1[i]));
+    }
+    if (nranks > 1) {
+      FLZ_REQUIRE(uid != nullptr, FLZ_EINVAL, "ctx_create_dist: null NCCL unique id");
+      ncclUniqueId id;
+      static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
+      std::memcpy(&id, uid, sizeof(id));
+      FLZ_NCCL(ncclCommInitRank(&ctx->comm, nranks, id, rank));
+    }
+    *out = ctx;
+  });
+}
+
+int flz_ctx_create(int device, flz_ctx** out) {
+  return ctx_create_common(device, 0, 1, nullptr, out);
+}
+int flz_ctx_create_dist(int device, int rank, int nranks, const void* uid, flz_ctx** out) {
+  if (nranks < 1 || rank < 0 || rank >= nranks) {
+    set_last_error("ctx_create_dist: bad rank/nranks");
+    return FLZ_EINVAL;
+  }
+  return ctx_create_common(device, rank, nranks, uid, out);
+}
+int flz_nccl_unique_id(void* out128) {
+  return guarded([&] {
+    ncclUniqueId id;
+    FLZ_NCCL(ncclGetUniqueId(&id));
+    std::memcpy(out128, &id, sizeof(id));
+  });
+}
+void flz_ctx_destroy(flz_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  cudaStreamSynchronize(ctx->comm_stream);
+  if (ctx->comm) ncclCommDestroy(ctx->comm);
+  for (int i = 0; i < 16; ++i) {
+    cudaEventDestroy(ctx->t0[i]);
+    cudaEventDestroy(ctx->t1[i]);
+  }
+  cudaEventDestroy(ctx->ev_halo_ready);
+  cudaEventDestroy(ctx->ev_halo_done);
+  ctx->partial.release();
+  ctx->small.release();
+  ctx->stage.release();
+  ctx->stage2.release();
+  ctx->flush.release();
+  cudaStreamDestroy(ctx->stream);
+  cudaStreamDestroy(ctx->comm_stream);
+  delete ctx;
+}
+int flz_ctx_sync(flz_ctx* ctx) {
+  return guarded([&] {
+    use(ctx);
+    FLZ_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+int flz_ctx_rank(const flz_ctx* ctx) { return ctx->rank; }
+int flz_ctx_nranks(const flz_ctx* ctx) { return ctx->nranks; }
+uint64_t flz_ctx_launch_count(const flz_ctx* ctx) { return ctx->launches; }
+int flz_timer_start(flz_ctx* ctx, int slot) {
+  return guarded([&] {
+    FLZ_REQUIRE(slot >= 0 && slot < 16, FLZ_EINVAL, "timer slot out of range");
+    use(ctx);
+    FLZ_CUDA(cudaEventRecord(ctx->t0[slot], ctx->stream));
+  });
+}
+int flz_timer_stop(flz_ctx* ctx, int slot, double* elapsed_ms) {
+  return guarded([&] {
+    FLZ_REQUIRE(slot >= 0 && slot < 16, FLZ_EINVAL, "timer slot out of range");
+    use(ctx);
+    FLZ_CUDA(cudaEventRecord(ctx->t1[slot], ctx->stream));
+    FLZ_CUDA(cudaEventSynchronize(ctx->t1[slot]));
+    float ms = 0.f;
+    FLZ_CUDA(cudaEventElapsedTime(&ms, ctx->t0[slot], ctx->t1[slot]));
+    if (elapsed_ms) *elapsed_ms = ms;
+  });
+}
+int flz_flush_l2(flz_ctx* ctx, size_t bytes) {
+  return guarded([&] {
+    use(ctx);
+    ctx->flush.reserve(bytes);
+    FLZ_CUDA(cudaMemsetAsync(ctx->flush.p, 0, bytes, ctx->stream));
+  });
+}
+int flz_ctx_set_exact(flz_ctx* ctx, int exact) {
+  ctx->exact = exact != 0;
+  return FLZ_OK;
+}
+int flz_host_alloc(size_t bytes, void** out) {
+  return guarded([&] { FLZ_CUDA(cudaMallocHost(out, bytes)); });
+}
+void flz_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+int flz_mem_info(flz_ctx* ctx, size_t* free_bytes, size_t* total_bytes) {
+  return guarded([&] {
+    use(ctx);
+    FLZ_CUDA(cudaMemGetInfo(free_bytes, total_bytes));
+  });
+}
+
+uint64_t flz_matvec_count(void) { return g_matvecs.load(std::memory_order_relaxed); }
+void flz_reset_matvec_count(void) { g_matvecs.store(0, std::memory_order_relaxed); }
+
+// ----------------------------------------------------------------- matrix
+
+static int64_t padded_entries(const std::vector<int32_t>& lens_new) {
+  int64_t total = 0;
+  for (size_t s = 0; s < lens_new.size(); s += kSliceRows) {
+    int32_t mx = 0;
+    for (size_t i = s; i < std::min(lens_new.size(), s + kSliceRows); ++i)
+      mx = std::max(mx, lens_new[i]);
+    total += (int64_t)mx * kSliceRows;
+  }
+  return total;
+}
+
+static void sort_windows(const std::vector<int32_t>& len, int64_t sigma,
+                         std::vector<int32_t>& perm) {
+  const int64_t nl = (int64_t)len.size();
+  perm.resize(nl);
+  std::iota(perm.begin(), perm.end(), 0);
+  if (sigma <= 1) return;
+  for (int64_t w0 = 0; w0 < nl; w0 += sigma) {
+    const int64_t w1 = std::min(nl, w0 + sigma);
+    std::stable_sort(perm.begin() + w0, perm.begin() + w1,
+                     [&](int32_t a, int32_t b) { return len[a] > len[b]; });
+  }
+}
+
+int flz_matrix_upload(flz_ctx* ctx, int64_t n_global, int64_t row_begin, int64_t row_end,
+                      const int64_t* row_ptr, const int32_t* col_idx, const double* values,
+                      int sigma, flz_matrix** out) {
+  return guarded([&] {
+    FLZ_REQUIRE(ctx && out && row_ptr, FLZ_EINVAL, "matrix_upload: null argument");
+    FLZ_REQUIRE(0 <= row_begin && row_begin <= row_end && row_end <= n_global, FLZ_EINVAL,
+                "matrix_upload: bad row range");
+    FLZ_REQUIRE(ctx->nranks > 1 || (row_begin == 0 && row_end == n_global), FLZ_EINVAL,
+                "matrix_upload: a single-GPU context owns all rows");
+    use(ctx);
+    const int64_t nl = row_end - row_begin;
+    FLZ_REQUIRE(nl < (int64_t)1 << 31, FLZ_EINVAL, "matrix_upload: too many local rows");
+    const int64_t nnz = row_ptr[nl] - row_ptr[0];
+    const int64_t p0 = row_ptr[0];
+    auto A = std::make_unique<flz_matrix>();
+    A->ctx = ctx;
+    A->n_global = n_global;
+    A->row_begin = row_begin;
+    A->row_end = row_end;
+    A->nl = nl;
+    A->ld = std::max<int64_t>(round_up(nl, kLdAlign), kLdAlign);
+    A->nnz = nnz;
+
+    std::vector<int32_t> len(nl);
+    for (int64_t i = 0; i < nl; ++i) {
+      const int64_t l = row_ptr[i + 1] - row_ptr[i];
+      FLZ_REQUIRE(l >= 0 && l < (int64_t)1 << 31, FLZ_EINVAL, "matrix_upload: bad row_ptr");
+      len[i] = (int32_t)l;
+    }
+    for (int64_t p = 0; p < nnz; ++p)
+      FLZ_REQUIRE(col_idx[p0 + p] >= 0 && col_idx[p0 + p] < n_global, FLZ_EINVAL,
+                  "matrix_upload: column index out of range");
+
+    // ---- choose sigma: smallest window whose padding overhead is <= 5 %
+    std::vector<int32_t> perm;
+    auto fill_for = [&](int64_t sg) {
+      sort_windows(len, sg, perm);
+      std::vector<int32_t> ln(nl);
+      for (int64_t i = 0; i < nl; ++i) ln[i] = len[perm[i]];
+      return padded_entries(ln);
+    };
+    int64_t chosen = sigma;
+    if (sigma <= 0) {
+      const int64_t cands[] = {1, 256, 4096, 65536, std::max<int64_t>(nl, 1)};
+      int64_t best_sg = 1, best_fill = -1;
+      for (int64_t sg : cands) {
+        if (sg > 1 && sg > nl && sg != cands[4]) continue;
+        const int64_t f = fill_for(sg);
+        if (best_fill < 0 || f < best_fill) {
+          best_fill = f;
+          best_sg = sg;
+        }
+        if ((double)f <= 1.05 * (double)std::max<int64_t>(nnz, 1)) {
+          best_sg = sg;
+          break;
+        }
+      }
+      chosen = best_sg;
+    }
+    sort_windows(len, chosen, perm);
+    A->sigma = (int)std::min<int64_t>(chosen, 1 << 30);
+    bool identity = true;
+    for (int64_t i = 0; i < nl && identity; ++i) identity = perm[i] == i;
+    if (identity) A->sigma = 1;
+    std::vector<int32_t> iperm(nl);
+    for (int64_t i = 0; i < nl; ++i) iperm[perm[i]] = (int32_t)i;
+
+    // ---- halo columns (distributed): sorted unique remote global ids
+    std::vector<int64_t> halo;
+    if (ctx->nranks > 1) {
+      for (int64_t p = 0; p < nnz; ++p) {
+        const int64_t g = col_idx[p0 + p];
+        if (g < row_begin || g >= row_end) halo.push_back(g);
+      }
+      std::sort(halo.begin(), halo.end());
+      halo.erase(std::unique(halo.begin(), halo.end()), halo.end());
+    }
+    A->nhalo = (int64_t)halo.size();
+    FLZ_REQUIRE(nl + A->nhalo < (int64_t)1 << 31, FLZ_EINVAL, "matrix_upload: index overflow");
+
+    // ---- SELL-32 storage
+    const int64_t nslices = (nl + kSliceRows - 1) / kSliceRows;
+    A->nslices = nslices;
+    std::vector<int64_t> slice_ptr(nslices + 1, 0);
+    std::vector<int32_t> slice_len(nslices, 0), row_len(nslices * kSliceRows, 0);
+    for (int64_t s = 0; s < nslices; ++s) {
+      int32_t mx = 0;
+      for (int l = 0; l < kSliceRows; ++l) {
+        const int64_t inew = s * kSliceRows + l;
+        if (inew >= nl) break;
+        row_len[inew] = len[perm[inew]];
+        mx = std::max(mx, row_len[inew]);
+      }
+      slice_len[s] = mx;
+      slice_ptr[s + 1] = slice_ptr[s] + (int64_t)mx * kSliceRows;
+    }
+    const int64_t stored = slice_ptr[nslices];
+    A->stored = stored;
+    std::vector<int32_t> col(std::max<int64_t>(stored, 1));
+    std::vector<double> val(std::max<int64_t>(stored, 1), 0.0);
+    std::vector<uint8_t> slice_boundary(nslices, 0);
+    for (int64_t s = 0; s < nslices; ++s)
+      for (int l = 0; l < kSliceRows; ++l) {
+        const int64_t inew = s * kSliceRows + l;
+        const int64_t base = slice_ptr[s] + l;
+        const int32_t self = (int32_t)std::min<int64_t>(inew, std::max<int64_t>(nl - 1, 0));
+        int32_t cnt = 0;
+        if (inew < nl) {
+          const int64_t iold = perm[inew];
+          for (int64_t p = row_ptr[iold]; p < row_ptr[iold + 1]; ++p, ++cnt) {
+            const int64_t g = col_idx[p];
+            int32_t c;
+            if (g >= row_begin && g < row_end) {
+              c = iperm[g - row_begin];
+            } else {
+              const int64_t slot = std::lower_bound(halo.begin(), halo.end(), g) - halo.begin();
+              c = (int32_t)(nl + slot);
+              slice_boundary[s] = 1;
+            }
+            col[base + (int64_t)cnt * kSliceRows] = c;
+            val[base + (int64_t)cnt * kSliceRows] = values[p];
+          }
+        }
+        for (; cnt < slice_len[s]; ++cnt) {  // padding: zero value, harmless in-range column
+          col[base + (int64_t)cnt * kSliceRows] = self;
+          val[base + (int64_t)cnt * kSliceRows] = 0.0;
+        }
+      }
+    std::vector<int32_t> interior, boundary;
+    for (int64_t s = 0; s < nslices; ++s)
+      (slice_boundary[s] ? boundary : interior).push_back((int32_t)s);
+    A->n_interior = (int64_t)interior.size();
+    A->n_boundary = (int64_t)boundary.size();
+
+    auto up = [&](auto& buf, const auto& host) {
+      buf.reserve(std::max<size_t>(host.size(), 1));
+      if (!host.empty())
+        FLZ_CUDA(cudaMemcpyAsync(buf.p, host.data(), host.size() * sizeof(host[0]),
+                                 cudaMemcpyHostToDevice, ctx->stream));
+    };
+    up(A->slice_ptr, slice_ptr);
+    up(A->slice_len, slice_len);
+    up(A->row_len, row_len);
+    up(A->col, col);
+    up(A->val, val);
+    up(A->perm, perm);
+    up(A->iperm, iperm);
+    up(A->interior, interior);
+    up(A->boundary, boundary);
+    A->h_perm = perm;
+    A->h_iperm = iperm;
+
+    // ---- halo plan: tell every owner which of its rows we gather
+    if (ctx->nranks > 1) {
+      const int P = ctx->nranks;
+      // all ranks' row ranges
+      DevBuf<int64_t> d_begin;
+      d_begin.reserve(2 * (size_t)P + 2);
+      std::vector<int64_t> starts(P + 1, 0), mine = {row_begin};
+      FLZ_CUDA(cudaMemcpyAsync(d_begin.p + P, mine.data(), sizeof(int64_t),
+                               cudaMemcpyHostToDevice, ctx->stream));
+      FLZ_NCCL(ncclAllGather(d_begin.p + P, d_begin.p, 1, ncclInt64, ctx->comm, ctx->stream));
+      FLZ_CUDA(cudaMemcpyAsync(starts.data(), d_begin.p, P * sizeof(int64_t),
+                               cudaMemcpyDeviceToHost, ctx->stream));
+      FLZ_CUDA(cudaStreamSynchronize(ctx->stream));
+      starts[P] = n_global;
+      for (int p = 0; p + 1 <= P; ++p)
+        FLZ_REQUIRE(starts[p] <= starts[p + 1], FLZ_EINVAL,
+                    "matrix_upload: rank row ranges must be ascending and contiguous");
+      // what we need from each peer (contiguous runs of the sorted halo list)
+      std::vector<int64_t> need_cnt(P, 0), need_off(P, 0);
+      {
+        size_t h = 0;
+        for (int p = 0; p < P; ++p) {
+          need_off[p] = (int64_t)h;
+          while (h < halo.size() && halo[h] < starts[p + 1]) ++h;
+          need_cnt[p] = (int64_t)h - need_off[p];
+        }
+      }
+      // exchange counts
+      DevBuf<int64_t> d_cnt;
+      d_cnt.reserve(2 * (size_t)P);
+      FLZ_CUDA(cudaMemcpyAsync(d_cnt.p, need_cnt.data(), P * sizeof(int64_t),
+                               cudaMemcpyHostToDevice, ctx->stream));
+      FLZ_NCCL(ncclGroupStart());
+      for (int p = 0; p < P; ++p) {
+        if (p == ctx->rank) continue;
+        FLZ_NCCL(ncclSend(d_cnt.p + p, 1, ncclInt64, p, ctx->comm, ctx->stream));
+        FLZ_NCCL(ncclRecv(d_cnt.p + P + p, 1, ncclInt64, p, ctx->comm, ctx->stream));
+      }
+      FLZ_NCCL(ncclGroupEnd());
+      std::vector<int64_t> give_cnt(P, 0);
+      FLZ_CUDA(cudaMemcpyAsync(give_cnt.data(), d_cnt.p + P, P * sizeof(int64_t),
+                               cudaMemcpyDeviceToHost, ctx->stream));
+      FLZ_CUDA(cudaStreamSynchronize(ctx->stream));
+      give_cnt[ctx->rank] = 0;
+      // exchange the row lists (global ids)
+      std::vector<int64_t> give_off(P, 0);
+      int64_t give_total = 0;
+      for (int p = 0; p < P; ++p) {
+        give_off[p] = give_total;
+        give_total += give_cnt[p];
+      }
+      DevBuf<int64_t> d_need, d_give;
+      d_need.reserve(std::max<size_t>(halo.size(), 1));
+      d_give.reserve(std::max<size_t>((size_t)give_total, 1));
+      if (!halo.empty())
+        FLZ_CUDA(cudaMemcpyAsync(d_need.p, halo.data(), halo.size() * sizeof(int64_t),
+                                 cudaMemcpyHostToDevice, ctx->stream));
+      FLZ_NCCL(ncclGroupStart());
+      for (int p = 0; p < P; ++p) {
+        if (p == ctx->rank) continue;
+        if (need_cnt[p])
+          FLZ_NCCL(ncclSend(d_need.p + need_off[p], (size_t)need_cnt[p], ncclInt64, p, ctx->comm,
+                            ctx->stream));
+        if (give_cnt[p])
+          FLZ_NCCL(ncclRecv(d_give.p + give_off[p], (size_t)give_cnt[p], ncclInt64, p, ctx->comm,
+                            ctx->stream));
+      }
+      FLZ_NCCL(ncclGroupEnd());
+      std::vector<int64_t> give(std::max<int64_t>(give_total, 1));
+      if (give_total)
+        FLZ_CUDA(cudaMemcpyAsync(give.data(), d_give.p, give_total * sizeof(int64_t),
+                                 cudaMemcpyDeviceToHost, ctx->stream));
+      FLZ_CUDA(cudaStreamSynchronize(ctx->stream));
+      std::vector<int32_t> send_rows(std::max<int64_t>(give_total, 1));
+      for (int64_t i = 0; i < give_total; ++i) {
+        FLZ_REQUIRE(give[i] >= row_begin && give[i] < row_end, FLZ_EINVAL,
+                    "matrix_upload: peer requested a row this rank does not own");
+        send_rows[i] = iperm[give[i] - row_begin];
+      }
+      for (int p = 0; p < P; ++p) {
+        if (p == ctx->rank || (need_cnt[p] == 0 && give_cnt[p] == 0)) continue;
+        A->peers.push_back({p, give_off[p], give_cnt[p], need_off[p], need_cnt[p]});
+      }
+      A->n_send = give_total;
+      up(A->send_rows, send_rows);
+      A->send_buf.reserve(std::max<size_t>((size_t)give_total * kMaxFuse, 1));
+    }
+    FLZ_CUDA(cudaStreamSynchronize(ctx->stream));
+    *out = A.release();
+  });
+}
+
+void flz_matrix_destroy(flz_matrix* A) {
+  if (!A) return;
+  cudaSetDevice(A->ctx->device);
+  cudaStreamSynchronize(A->ctx->stream);
+  delete A;
+}
+int64_t flz_matrix_rows_local(const flz_matrix* A) { return A->nl; }
+int64_t flz_matrix_nnz_local(const flz_matrix* A) { return A->nnz; }
+int flz_matrix_stats(const flz_matrix* A, int64_t* stored_entries, int64_t* slices,
+                     int64_t* halo_rows, int64_t* boundary_slices) {
+  if (stored_entries) *stored_entries = A->stored;
+  if (slices) *slices = A->nslices;
+  if (halo_rows) *halo_rows = A->nhalo;
+  if (boundary_slices) *boundary_slices = A->n_boundary;
+  return A->sigma;
+}
+
+// ------------------------------------------------- block products & filter
+
+int flz_spmm(flz_ctx* ctx, const flz_matrix* A, const double* X, int r, double* Y, int counted) {
+  return guarded([&] {
+    FLZ_REQUIRE(ctx && A && X && Y && r >= 1, FLZ_EINVAL, "spmm: bad argument");
+    use(ctx);
+    ensure_xz(A, r);
+    upload_block(A, X, r, A->xs.p);
+    spmm_device(A, A->xs.p, A->ld, r, A->zs.p, A->ld, counted != 0);
+    download_block(A, A->zs.p, r, Y);
+  });
+}
+
+int flz_filter_apply(flz_ctx* ctx, const flz_matrix* A, const double* coeffs, int m, double c,
+                     double e, const double* X, int r, double* Y) {
+  return guarded([&] {
+    FLZ_REQUIRE(ctx && A && X && Y && coeffs && r >= 1, FLZ_EINVAL, "filter_apply: bad argument");
+    FLZ_REQUIRE(m >= 0, FLZ_EINVAL, "filter needs at least one coefficient");
+    FLZ_REQUIRE(e > 0.0, FLZ_EINTERVAL, "spectral bounds require lambda_min < lambda_max");
+    use(ctx);
+    ensure_xz(A, r);
+    upload_block(A, X, r, A->xs.p);
+    filter_device(A, coeffs, m, c, e, A->xs.p, A->ld, r, A->zs.p, A->ld);
+    download_block(A, A->zs.p, r, Y);
+  });
+}
+
+int flz_filter_bench(flz_ctx* ctx, const flz_matrix* A, const double* coeffs, int m, double c,
+                     double e, const double* X, int r, int reps, int flush_l2, double* ms_total,
+                     double* Y_last) {
+  return guarded([&] {
+    FLZ_REQUIRE(ctx && A && X && coeffs && r >= 1 && m >= 1 && reps >= 1, FLZ_EINVAL,
+                "filter_bench: bad argument");
+    use(ctx);
+    ensure_xz(A, r);
+    upload_block(A, X, r, A->xs.p);
+    if (flush_l2) {
+      ctx->flush.reserve((size_t)256 << 20);
+      FLZ_CUDA(cudaMemsetAsync(ctx->flush.p, 0, (size_t)256 << 20, ctx->stream));
+    }
+    FLZ_CUDA(cudaStreamSynchronize(ctx->stream));
+    FLZ_CUDA(cudaEventRecord(ctx->t0[15], ctx->stream));
+    for (int rep = 0; rep < reps; ++rep)
+      filter_device(A, coeffs, m, c, e, A->xs.p, A->ld, r, A->zs.p, A->ld);
+    FLZ_CUDA(cudaEventRecord(ctx->t1[15], ctx->stream));
+    FLZ_CUDA(cudaEventSynchronize(ctx->t1[15]));
+    float ms = 0.f;
+    FLZ_CUDA(cudaEventElapsedTime(&ms, ctx->t0[15], ctx->t1[15]));
+    if (ms_total) *ms_total = ms;
+    if (Y_last) download_block(A, A->zs.p, r, Y_last);
+  });
+}
+
+int flz_dot(flz_ctx* ctx, const double* x, const double* y, int64_t n, double* out) {
+  return guarded([&] {
+    use(ctx);
+    const int64_t ld = std::max<int64_t>(round_up(n, kLdAlign), kLdAlign);
+    ctx->stage.reserve_zero((size_t)ld * 2, ctx->stream);
+    ctx->small.reserve(64);
+    FLZ_CUDA(cudaMemcpyAsync(ctx->stage.p, x, n * sizeof(double), cudaMemcpyHostToDevice,
+                             ctx->stream));
+    FLZ_CUDA(cudaMemcpyAsync(ctx->stage.p + ld, y, n * sizeof(double), cudaMemcpyHostToDevice,
+                             ctx->stream));
+    launch_gemm_tn(ctx, ctx->stage.p, ld, 1, ctx->stage.p + ld, ld, 1, n, ctx->small.p, 8);
+    FLZ_CUDA(cudaMemcpyAsync(out, ctx->small.p, sizeof(double), cudaMemcpyDeviceToHost,
+                             ctx->stream));
+    FLZ_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int flz_axpy(flz_ctx* ctx, double a, const double* x, double* y, int64_t n) {
+  return guarded([&] {
+    use(ctx);
+    const int64_t ld = std::max<int64_t>(round_up(n, kLdAlign), kLdAlign);
+    ctx->stage.reserve_zero((size_t)ld * 2, ctx->stream);
+    ctx->small.reserve(64);
+    FLZ_CUDA(cudaMemcpyAsync(ctx->stage.p, x, n * sizeof(double), cudaMemcpyHostToDevice,
+                             ctx->stream));
+    FLZ_CUDA(cudaMemcpyAsync(ctx->stage.p + ld, y, n * sizeof(double), cudaMemcpyHostToDevice,
+                             ctx->stream));
+    double bs[8] = {a, 0, 0, 0, 0, 0, 0, 0};
+    FLZ_CUDA(cudaMemcpyAsync(ctx->small.p, bs, sizeof(bs), cudaMemcpyHostToDevice, ctx->stream));
+    launch_gemm_nn(ctx, ctx->stage.p, ld, 1, ctx->small.p, 8, 1, n, 1.0, true, ctx->stage.p + ld,
+                   ld);
+    FLZ_CUDA(cudaMemcpyAsync(y, ctx->stage.p + ld, n * sizeof(double), cudaMemcpyDeviceToHost,
+                             ctx->stream));
+    FLZ_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int flz_clenshaw_combine(flz_ctx* ctx, int64_t n, double s1, double s2, double b,
+                         const double* w, const double* y1, const double* y2, const double* x,
+                         double* out) {
+  return guarded([&] {
+    use(ctx);
+    ctx->stage.reserve((size_t)n * 5 + 8);
+    double* d = ctx->stage.p;
+    const double* src[4] = {w, y1, y2, x};
+    for (int i = 0; i < 4; ++i)
+      FLZ_CUDA(cudaMemcpyAsync(d + (size_t)i * n, src[i], n * sizeof(double),
+                               cudaMemcpyHostToDevice, ctx->stream));
+    launch_combine(ctx, n, ctx->exact, s1, s2, b, d, d + n, d + 2 * n, d + 3 * n, d + 4 * n);
+    FLZ_CUDA(cudaMemcpyAsync(out, d + 4 * n, n * sizeof(double), cudaMemcpyDeviceToHost,
+                             ctx->stream));
+    FLZ_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+// ------------------------------------------------- Lanczos factorization
+
+int flz_basis_create(flz_ctx* ctx, const flz_matrix* A, int64_t max_cols, int r,
+                     const double* start, flz_basis** out) {
+  return guarded([&] {
+    FLZ_REQUIRE(ctx && A && start && out, FLZ_EINVAL, "basis_create: null argument");
+    FLZ_REQUIRE(r >= 1 && r <= kRMax, FLZ_EINVAL,
+                "basis_create: block_size must lie in [1, 16] on the device path");
+    FLZ_REQUIRE(max_cols >= 2 * r, FLZ_EINVAL, "LanczosFactorization: column budget too small");
+    use(ctx);
+    auto B = std::make_unique<flz_basis>();
+    B->ctx = ctx;
+    B->A = A;
+    B->nl = A->nl;
+    B->ld = A->ld;
+    B->r = r;
+    B->max_cols = max_cols;
+    const size_t total = (size_t)B->ld * (size_t)(max_cols + r);
+    size_t free_b = 0, total_b = 0;
+    FLZ_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    if (total * sizeof(double) > free_b)
+      throw ApiError(FLZ_ENOMEM, "basis_create: basis of " +
+                                     std::to_string(total * sizeof(double) >> 20) +
+                                     " MiB does not fit in free device memory (" +
+                                     std::to_string(free_b >> 20) + " MiB); lower max_dim");
+    B->Q.reserve(total);
+    if (B->ld > B->nl)  // keep the pad rows of every column zero
+      FLZ_CUDA(cudaMemset2DAsync(B->Q.p + B->nl, B->ld * sizeof(double), 0,
+                                 (B->ld - B->nl) * sizeof(double), max_cols + r, ctx->stream));
+    B->Z.reserve_zero((size_t)B->ld * r, ctx->stream);
+    B->X.reserve_zero((size_t)B->ld * r, ctx->stream);
+    upload_block(A, start, r, B->Q.p);
+    const SmallLayout L = small_layout(max_cols, r);
+    B->small.reserve_zero((size_t)L.total, ctx->stream);
+    FLZ_CUDA(cudaMallocHost(&B->pinned, (size_t)L.total * sizeof(double)));
+    B->pinned_count = (size_t)L.total;
+    FLZ_CUDA(cudaEventCreate(&B->e0));
+    FLZ_CUDA(cudaEventCreate(&B->e1));
+    FLZ_CUDA(cudaEventCreate(&B->e2));
+    FLZ_CUDA(cudaStreamSynchronize(ctx->stream));
+    *out = B.release();
+  });
+}
+
+void flz_basis_destroy(flz_basis* B) {
+  if (!B) return;
+  cudaSetDevice(B->ctx->device);
+  cudaStreamSynchronize(B->ctx->stream);
+  if (B->e0) cudaEventDestroy(B->e0);
+  if (B->e1) cudaEventDestroy(B->e1);
+  if (B->e2) cudaEventDestroy(B->e2);
+  if (B->pinned) cudaFreeHost(B->pinned);
+  delete B;
+}
+int64_t flz_basis_blocks(const flz_basis* B) { return B->k; }
+
+int flz_basis_get(flz_ctx* ctx, const flz_basis* B, int64_t j0, int64_t count, double* out) {
+  return guarded([&] {
+    FLZ_REQUIRE(j0 >= 0 && count >= 0 && j0 + count <= B->max_cols + B->r, FLZ_EDIM,
+                "basis_get: column range out of bounds");
+    use(ctx);
+    for (int64_t c = 0; c < count; c += 64) {
+      const int nc = (int)std::min<int64_t>(64, count - c);
+      download_block(B->A, B->col(j0 + c), nc, out + (size_t)c * B->nl);
+    }
+  });
+}
+
+int flz_basis_set(flz_ctx* ctx, flz_basis* B, int64_t j, const double* col) {
+  return guarded([&] {
+    FLZ_REQUIRE(j >= 0 && j < B->max_cols + B->r, FLZ_EDIM, "basis_set: column out of bounds");
+    use(ctx);
+    upload_block(B->A, col, 1, B->col(j));
+    FLZ_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int flz_lanczos_step(flz_ctx* ctx, const flz_matrix* A, flz_basis* B, const double* coeffs,
+                     int m, double c, double e, double* Dk, double* Sk, double* op_scale,
+                     uint8_t* dead) {
+  return guarded([&] {
+    FLZ_REQUIRE(ctx && A && B && Dk && Sk && dead, FLZ_EINVAL, "lanczos_step: null argument");
+    FLZ_REQUIRE(B->A == A, FLZ_EINVAL, "lanczos_step: basis belongs to another matrix");
+    const int r = B->r;
+    FLZ_REQUIRE((B->k + 1) * r <= B->max_cols, FLZ_EDIM, "lanczos_step: column budget exhausted");
+    FLZ_REQUIRE(m < 0 || (coeffs && e > 0.0), FLZ_EINVAL, "lanczos_step: bad filter");
+    use(ctx);
+    const int64_t nl = B->nl, ld = B->ld;
+    const SmallLayout L = small_layout(B->max_cols, r);
+    double* sm = B->small.p;
+
+    B->k += 1;  // promote the pending block (lanczos.cpp:153)
+    const int64_t cols = B->k * r, newest = cols - r;
+
+    FLZ_CUDA(cudaEventRecord(B->e0, ctx->stream));
+    // Z = op(newest block); the block is staged first, as the reference copies it
+    // (lanczos.cpp:161-164) — it keeps the filter's X operand at a fixed address.
+    FLZ_CUDA(cudaMemcpyAsync(B->X.p, B->col(newest), (size_t)ld * r * sizeof(double),
+                             cudaMemcpyDeviceToDevice, ctx->stream));
+    if (m >= 0)
+      filter_device(A, coeffs, m, c, e, B->X.p, ld, r, B->Z.p, ld);
+    else
+      spmm_device(A, B->X.p, ld, r, B->Z.p, ld, true);
+    FLZ_CUDA(cudaEventRecord(B->e1, ctx->stream));
+
+    // op_scale = max(op_scale, ||Z_j||) (lanczos.cpp:169-170)
+    launch_coldot(ctx, B->Z.p, ld, B->Z.p, ld, r, nl, sm + L.normsq);
+    allreduce(ctx, sm + L.normsq, r);
+    launch_update_scale(ctx, sm + L.normsq, r, 0, sm + L.scale);
+
+    // two full Gram-Schmidt sweeps in GEMM form (lanczos.cpp:177-182)
+    launch_gemm_tn(ctx, B->Q.p, ld, cols, B->Z.p, ld, r, nl, sm + L.C1, L.ldc);
+    allreduce(ctx, sm + L.C1, (size_t)cols * L.ldc);
+    launch_gemm_nn(ctx, B->Q.p, ld, cols, sm + L.C1, L.ldc, r, nl, -1.0, true, B->Z.p, ld);
+    launch_gemm_tn(ctx, B->Q.p, ld, cols, B->Z.p, ld, r, nl, sm + L.C2, L.ldc);
+    allreduce(ctx, sm + L.C2, (size_t)cols * L.ldc);
+    launch_gemm_nn(ctx, B->Q.p, ld, cols, sm + L.C2, L.ldc, r, nl, -1.0, true, B->Z.p, ld);
+
+    // intra-block QR, two sweeps against the finished pending columns (lanczos.cpp:205-230)
+    FLZ_CUDA(cudaMemsetAsync(sm + L.Sk, 0, (size_t)(L.normsq - L.Sk) * sizeof(double),
+                             ctx->stream));
+    double* P = B->col(cols);
+    for (int j = 0; j < r; ++j) {
+      double* zj = B->Z.p + (int64_t)j * ld;
+      if (j > 0) {
+        for (int pass = 0; pass < 2; ++pass) {
+          double* t = sm + (pass == 0 ? L.t1 : L.t2) + (int64_t)j * kRMax * 8;
+          launch_gemm_tn(ctx, P, ld, j, zj, ld, 1, nl, t, 8);
+          allreduce(ctx, t, (size_t)j * 8);
+          launch_gemm_nn(ctx, P, ld, j, t, 8, 1, nl, -1.0, true, zj, ld);
+        }
+      }
+      launch_coldot(ctx, zj, ld, zj, ld, 1, nl, sm + L.normsq + j);
+      allreduce(ctx, sm + L.normsq + j, 1);
+      launch_finish_col(ctx, sm + L.normsq + j, sm + L.scale, sm + L.Sk, r, j, sm + L.inv + j,
+                        sm + L.dead + j);
+      launch_scale_copy(ctx, zj, sm + L.inv + j, P + (int64_t)j * ld, nl);
+    }
+    FLZ_CUDA(cudaEventRecord(B->e2, ctx->stream));
+
+    // small results back: D_k rows of C1, Sk + t1 + t2 + norms + flags + scale
+    double* h = B->pinned;
+    FLZ_CUDA(cudaMemcpyAsync(h, sm + L.C1 + newest * L.ldc, (size_t)r * L.ldc * sizeof(double),
+                             cudaMemcpyDeviceToHost, ctx->stream));
+    FLZ_CUDA(cudaMemcpyAsync(h + L.Sk, sm + L.Sk, (size_t)(L.total - L.Sk) * sizeof(double),
+                             cudaMemcpyDeviceToHost, ctx->stream));
+    FLZ_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (int i = 0; i < r; ++i)
+      for (int j = 0; j < r; ++j) Dk[i * r + j] = h[i * L.ldc + j];  // coeff[newest+i] of col j
+    for (int i = 0; i < r * r; ++i) Sk[i] = 0.0;
+    for (int j = 0; j < r; ++j) {
+      for (int i = 0; i < j; ++i)
+        Sk[i * r + j] = h[L.t1 + (int64_t)j * kRMax * 8 + i * 8] +
+                        h[L.t2 + (int64_t)j * kRMax * 8 + i * 8];
+      Sk[j * r + j] = h[L.Sk + j * r + j];
+      dead[j] = h[L.dead + j] != 0.0 ? 1 : 0;
+    }
+    B->op_scale = h[L.scale];
+    if (op_scale) *op_scale = B->op_scale;
+    float ms_mv = 0.f, ms_orth = 0.f;
+    FLZ_CUDA(cudaEventElapsedTime(&ms_mv, B->e0, B->e1));
+    FLZ_CUDA(cudaEventElapsedTime(&ms_orth, B->e1, B->e2));
+    B->mv_s += 1e-3 * ms_mv;
+    B->orth_s += 1e-3 * ms_orth;
+  });
+}
+
+int flz_orthogonalize_column(flz_ctx* ctx, const flz_basis* B, int64_t cols, int pending,
+                             double* v, double* norm) {
+  return guarded([&] {
+    FLZ_REQUIRE(ctx && B && v && norm, FLZ_EINVAL, "orthogonalize_column: null argument");
+    FLZ_REQUIRE(cols + pending <= B->max_cols + B->r, FLZ_EDIM,
+                "orthogonalize_column: too many columns");
+    use(ctx);
+    const int64_t nl = B->nl, ld = B->ld, M = cols + pending;
+    const SmallLayout L = small_layout(B->max_cols, B->r);
+    double* sm = B->small.p;
+    double* z = B->Z.p;  // scratch: the step that owns Z has finished
+    FLZ_CUDA(cudaMemsetAsync(z, 0, (size_t)ld * sizeof(double), ctx->stream));
+    upload_block(B->A, v, 1, z);
+    for (int pass = 0; pass < 2; ++pass) {
+      launch_gemm_tn(ctx, B->Q.p, ld, M, z, ld, 1, nl, sm + L.C1, L.ldc);
+      allreduce(ctx, sm + L.C1, (size_t)M * L.ldc);
+      launch_gemm_nn(ctx, B->Q.p, ld, M, sm + L.C1, L.ldc, 1, nl, -1.0, true, z, ld);
+    }
+    launch_coldot(ctx, z, ld, z, ld, 1, nl, sm + L.normsq);
+    allreduce(ctx, sm + L.normsq, 1);
+    FLZ_CUDA(cudaMemcpyAsync(B->pinned, sm + L.normsq, sizeof(double), cudaMemcpyDeviceToHost,
+                             ctx->stream));
+    download_block(B->A, z, 1, v);
+    *norm = std::sqrt(std::max(B->pinned[0], 0.0));
+  });
+}
+
+int flz_basis_ortho_error(flz_ctx* ctx, const flz_basis* B, const uint8_t* dead, double* out) {
+  return guarded([&] {
+    use(ctx);
+    const int64_t cols = B->k * B->r;
+    double worst = 0.0;
+    const int panel = 128;
+    DevBuf<double> G;
+    G.reserve((size_t)cols * panel + 8);
+    std::vector<double> h((size_t)cols * panel);
+    for (int64_t j0 = 0; j0 < cols; j0 += panel) {
+      const int nb = (int)std::min<int64_t>(panel, cols - j0);
+      launch_gemm_tn(ctx, B->Q.p, B->ld, cols, B->col(j0), B->ld, nb, B->nl, G.p, panel);
+      allreduce(ctx, G.p, (size_t)cols * panel);
+      FLZ_CUDA(cudaMemcpyAsync(h.data(), G.p, (size_t)cols * panel * sizeof(double),
+                               cudaMemcpyDeviceToHost, ctx->stream));
+      FLZ_CUDA(cudaStreamSynchronize(ctx->stream));
+      for (int64_t i = 0; i < cols; ++i) {
+        if (dead && dead[i]) continue;
+        for (int jj = 0; jj < nb; ++jj) {
+          const int64_t j = j0 + jj;
+          if (j < i || (dead && dead[j])) continue;
+          worst = std::max(worst, std::abs(h[i * panel + jj] - (i == j ? 1.0 : 0.0)));
+        }
+      }
+    }
+    *out = worst;
+  });
+}
+
+int flz_basis_times(const flz_basis* B, double* mv_s, double* orth_s) {
+  if (mv_s) *mv_s = B->mv_s;
+  if (orth_s) *orth_s = B->orth_s;
+  return FLZ_OK;
+}
+
+// ------------------------------------------------------- Ritz recovery
+
+int flz_ritz_lift(flz_ctx* ctx, const flz_matrix* A, const flz_basis* Bc, int64_t dim,
+                  const double* W, int w, double* vnorm, uint8_t* keep, int* w_kept, double* Bm) {
+  return guarded([&] {
+    flz_basis* B = const_cast<flz_basis*>(Bc);
+    FLZ_REQUIRE(ctx && A && B && W && vnorm && keep && w_kept && Bm, FLZ_EINVAL,
+                "ritz_lift: null argument");
+    FLZ_REQUIRE(dim == B->k * B->r, FLZ_EDIM, "ritz_lift: dim does not match the basis");
+    use(ctx);
+    *w_kept = 0;
+    B->w_kept = 0;
+    if (w == 0) return;
+    const int64_t nl = B->nl, ld = B->ld;
+    const int64_t ldw = round_up(w, 64);
+    B->V.reserve_zero((size_t)ld * w, ctx->stream);
+    B->AV.reserve_zero((size_t)ld * w, ctx->stream);
+    // W (dim x w column-major) -> row-major [dim][ldw]
+    std::vector<double> Wt((size_t)dim * ldw, 0.0);
+    for (int c = 0; c < w; ++c)
+      for (int64_t j = 0; j < dim; ++j) Wt[(size_t)j * ldw + c] = W[(size_t)c * dim + j];
+    DevBuf<double> dW;
+    dW.reserve(Wt.size() + 8);
+    FLZ_CUDA(cudaMemcpyAsync(dW.p, Wt.data(), Wt.size() * sizeof(double), cudaMemcpyHostToDevice,
+                             ctx->stream));
+    launch_gemm_nn(ctx, B->Q.p, ld, dim, dW.p, ldw, w, nl, 1.0, false, B->V.p, ld);
+    DevBuf<double> dn;
+    dn.reserve((size_t)2 * w + 8);
+    launch_coldot(ctx, B->V.p, ld, B->V.p, ld, w, nl, dn.p);
+    allreduce(ctx, dn.p, w);
+    std::vector<double> hn(w), hs(w);
+    FLZ_CUDA(cudaMemcpyAsync(hn.data(), dn.p, w * sizeof(double), cudaMemcpyDeviceToHost,
+                             ctx->stream));
+    FLZ_CUDA(cudaStreamSynchronize(ctx->stream));
+    int wk = 0;
+    for (int c = 0; c < w; ++c) {
+      vnorm[c] = std::sqrt(std::max(hn[c], 0.0));
+      keep[c] = vnorm[c] >= 0.5 ? 1 : 0;  // lanczos.cpp:430-431
+      if (!keep[c]) continue;
+      if (wk != c)
+        FLZ_CUDA(cudaMemcpyAsync(B->V.p + (size_t)wk * ld, B->V.p + (size_t)c * ld,
+                                 ld * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+      hs[wk] = 1.0 / vnorm[c];
+      ++wk;
+    }
+    *w_kept = wk;
+    B->w_kept = wk;
+    if (wk == 0) return;
+    FLZ_CUDA(cudaMemcpyAsync(dn.p + w, hs.data(), wk * sizeof(double), cudaMemcpyHostToDevice,
+                             ctx->stream));
+    launch_scale_cols(ctx, B->V.p, ld, wk, nl, dn.p + w);
+    spmm_device(A, B->V.p, ld, wk, B->AV.p, ld, false);  // uncounted (lanczos.cpp:448-449)
+    const int64_t ldb = round_up(wk, 8);
+    DevBuf<double> dB;
+    dB.reserve((size_t)wk * ldb + 8);
+    launch_gemm_tn(ctx, B->V.p, ld, wk, B->AV.p, ld, wk, nl, dB.p, ldb);
+    allreduce(ctx, dB.p, (size_t)wk * ldb);
+    std::vector<double> hB((size_t)wk * ldb);
+    FLZ_CUDA(cudaMemcpyAsync(hB.data(), dB.p, hB.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                             ctx->stream));
+    FLZ_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (int i = 0; i < wk; ++i)  // 0.5*(v_i.Av_j + v_j.Av_i) (lanczos.cpp:451-457)
+      for (int j = 0; j < wk; ++j)
+        Bm[(size_t)j * wk + i] = 0.5 * (hB[(size_t)i * ldb + j] + hB[(size_t)j * ldb + i]);
+  });
+}
+
+static void residuals_and_vectors(flz_ctx* ctx, const flz_basis* B, double* V, double* AV,
+                                  const double* lambda, int w2, double scale, bool normalize,
+                                  double* residuals, double* eigvecs) {
+  const int64_t nl = B->nl, ld = B->ld;
+  DevBuf<double> d;
+  d.reserve((size_t)3 * w2 + 8);
+  std::vector<double> h(w2), inv(w2, 1.0);
+  if (normalize) {
+    launch_coldot(ctx, V, ld, V, ld, w2, nl, d.p);
+    allreduce(ctx, d.p, w2);
+    FLZ_CUDA(cudaMemcpyAsync(h.data(), d.p, w2 * sizeof(double), cudaMemcpyDeviceToHost,
+                             ctx->stream));
+    FLZ_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (int c = 0; c < w2; ++c) inv[c] = 1.0 / std::sqrt(h[c]);  // lanczos.cpp:473-475
+  }
+  FLZ_CUDA(cudaMemcpyAsync(d.p + w2, inv.data(), w2 * sizeof(double), cudaMemcpyHostToDevice,
+                           ctx->stream));
+  FLZ_CUDA(cudaMemcpyAsync(d.p + 2 * w2, lambda, w2 * sizeof(double), cudaMemcpyHostToDevice,
+                           ctx->stream));
+  launch_residual_prep(ctx, V, AV, ld, w2, nl, d.p + w2, d.p + 2 * w2);  // :476
+  launch_coldot(ctx, AV, ld, AV, ld, w2, nl, d.p);
+  allreduce(ctx, d.p, w2);
+  FLZ_CUDA(cudaMemcpyAsync(h.data(), d.p, w2 * sizeof(double), cudaMemcpyDeviceToHost,
+                           ctx->stream));
+  FLZ_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (int c = 0; c < w2; ++c) residuals[c] = std::sqrt(std::max(h[c], 0.0)) / scale;  // :477
+  if (eigvecs)
+    for (int c = 0; c < w2; c += 64) {
+      const int nc = std::min(64, w2 - c);
+      download_block(B->A, V + (size_t)c * ld, nc, eigvecs + (size_t)c * nl);
+    }
+}
+
+int flz_ritz_rotate(flz_ctx* ctx, const flz_basis* Bc, const double* U, const double* lambda,
+                    int w2, double scale, double* residuals, double* eigvecs) {
+  return guarded([&] {
+    flz_basis* B = const_cast<flz_basis*>(Bc);
+    FLZ_REQUIRE(ctx && B && (w2 == 0 || (U && lambda && residuals)), FLZ_EINVAL,
+                "ritz_rotate: null argument");
+    use(ctx);
+    if (w2 == 0) return;
+    const int wk = B->w_kept;
+    FLZ_REQUIRE(wk > 0, FLZ_EINVAL, "ritz_rotate: call ritz_lift first");
+    const int64_t nl = B->nl, ld = B->ld;
+    const int64_t ldu = round_up(w2, 64);
+    std::vector<double> Ut((size_t)wk * ldu, 0.0);
+    for (int c = 0; c < w2; ++c)
+      for (int j = 0; j < wk; ++j) Ut[(size_t)j * ldu + c] = U[(size_t)c * wk + j];
+    DevBuf<double> dU;
+    dU.reserve(Ut.size() + 8);
+    FLZ_CUDA(cudaMemcpyAsync(dU.p, Ut.data(), Ut.size() * sizeof(double), cudaMemcpyHostToDevice,
+                             ctx->stream));
+    B->V2.reserve_zero((size_t)ld * w2, ctx->stream);
+    B->AV2.reserve_zero((size_t)ld * w2, ctx->stream);
+    launch_gemm_nn(ctx, B->V.p, ld, wk, dU.p, ldu, w2, nl, 1.0, false, B->V2.p, ld);   // :467-470
+    launch_gemm_nn(ctx, B->AV.p, ld, wk, dU.p, ldu, w2, nl, 1.0, false, B->AV2.p, ld);
+    residuals_and_vectors(ctx, B, B->V2.p, B->AV2.p, lambda, w2, scale, true, residuals, eigvecs);
+  });
+}
+
+int flz_ritz_plain(flz_ctx* ctx, const flz_matrix* A, const flz_basis* Bc, const double* lambda,
+                   int w_kept, double scale, double* residuals, double* eigvecs) {
+  return guarded([&] {
+    flz_basis* B = const_cast<flz_basis*>(Bc);
+    FLZ_REQUIRE(ctx && A && B, FLZ_EINVAL, "ritz_plain: null argument");
+    FLZ_REQUIRE(w_kept == B->w_kept, FLZ_EDIM, "ritz_plain: w_kept mismatch");
+    use(ctx);
+    if (w_kept == 0) return;
+    // V holds the normalised lifted vectors, AV = A V (lanczos.cpp:480-495)
+    residuals_and_vectors(ctx, B, B->V.p, B->AV.p, lambda, w_kept, scale, false, residuals,
+                          eigvecs);
+  });
+}
+
+// ------------------------------------------------------- spectral bounds
+
+int flz_bounds_lanczos(flz_ctx* ctx, const flz_matrix* A, int steps, const double* q0, double* d,
+                       double* e, double* beta_last, int* done) {
+  return guarded([&] {
+    FLZ_REQUIRE(ctx && A && q0 && d && e && beta_last && done, FLZ_EINVAL,
+                "bounds_lanczos: null argument");
+    FLZ_REQUIRE(steps >= 1, FLZ_EINVAL, "bounds_lanczos: steps must be >= 1");
+    use(ctx);
+    const int64_t nl = A->nl, ld = A->ld;
+    DevBuf<double> Q, w, sm;
+    Q.reserve_zero((size_t)ld * steps, ctx->stream);
+    w.reserve_zero((size_t)ld, ctx->stream);
+    sm.reserve_zero((size_t)(steps + 4) * 8 * 2 + 64, ctx->stream);
+    double* C = sm.p;                                   // [steps+..][8]
+    double* sc = sm.p + (size_t)(steps + 4) * 8;        // scalars: nw2, a, beta2, inv, dead, ...
+    double* one = sc + 16;                              // op_scale stand-in (=huge so never dead)
+    Pinned pin(64);
+    upload_block(A, q0, 1, Q.p);
+    double scale = 0.0;
+    *beta_last = 0.0;
+    *done = 0;
+    for (int s = 0; s < steps; ++s) {
+      double* qs = Q.p + (size_t)s * ld;
+      spmm_device(A, qs, ld, 1, w.p, ld, true);                          // lanczos.cpp:533
+      launch_coldot(ctx, w.p, ld, w.p, ld, 1, nl, sc + 0);               // :534
+      launch_coldot(ctx, qs, ld, w.p, ld, 1, nl, sc + 1);                // :535
+      allreduce(ctx, sc, 2);
+      for (int pass = 0; pass < 2; ++pass) {                             // :537-538
+        launch_gemm_tn(ctx, Q.p, ld, s + 1, w.p, ld, 1, nl, C, 8);
+        allreduce(ctx, C, (size_t)(s + 1) * 8);
+        launch_gemm_nn(ctx, Q.p, ld, s + 1, C, 8, 1, nl, -1.0, true, w.p, ld);
+      }
+      launch_coldot(ctx, w.p, ld, w.p, ld, 1, nl, sc + 2);               // :539
+      allreduce(ctx, sc + 2, 1);
+      // inv = 1/beta via the finish kernel (op_scale slot = 0 => dead_tol = 1e-310)
+      launch_finish_col(ctx, sc + 2, one, sc + 8, 1, 0, sc + 3, sc + 4);
+      if (s + 1 < steps) launch_scale_copy(ctx, w.p, sc + 3, Q.p + (size_t)(s + 1) * ld, nl);
+      FLZ_CUDA(cudaMemcpyAsync(pin.p, sc, 8 * sizeof(double), cudaMemcpyDeviceToHost,
+                               ctx->stream));
+      FLZ_CUDA(cudaStreamSynchronize(ctx->stream));
+      const double nw = std::sqrt(std::max(pin.p[0], 0.0));
+      scale = std::max(scale, nw);
+      d[s] = pin.p[1];
+      const double beta = std::sqrt(std::max(pin.p[2], 0.0));
+      *beta_last = beta;
+      *done = s + 1;
+      if (beta <= 1e-14 * std::max(scale, 1e-300)) {                     // :541-544
+        *beta_last = 0.0;
+        break;
+      }
+      if (s + 1 < steps) e[s] = beta;                                    // :545-549
+    }
+  });
+}
+
+}  // extern "C"

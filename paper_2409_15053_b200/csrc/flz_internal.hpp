@@ -1,0 +1,236 @@
+// flz_internal.hpp — shared declarations of the device layer behind include/flz.h.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "flz.h"
+
+namespace flz {
+
+// ---------------------------------------------------------------- errors
+struct ApiError : std::runtime_error {
+  int code;
+  ApiError(int c, const std::string& what) : std::runtime_error(what), code(c) {}
+};
+
+void set_last_error(const std::string& msg);
+
+#define FLZ_CUDA(expr)                                                                  \
+  do {                                                                                  \
+    cudaError_t err__ = (expr);                                                         \
+    if (err__ != cudaSuccess)                                                           \
+      throw ::flz::ApiError(FLZ_ECUDA, std::string(#expr) + ": " +                      \
+                                           cudaGetErrorString(err__));                  \
+  } while (0)
+
+#define FLZ_NCCL(expr)                                                                  \
+  do {                                                                                  \
+    ncclResult_t err__ = (expr);                                                        \
+    if (err__ != ncclSuccess)                                                           \
+      throw ::flz::ApiError(FLZ_ENCCL, std::string(#expr) + ": " +                      \
+                                           ncclGetErrorString(err__));                  \
+  } while (0)
+
+#define FLZ_REQUIRE(cond, code, msg)                                                    \
+  do {                                                                                  \
+    if (!(cond)) throw ::flz::ApiError((code), (msg));                                  \
+  } while (0)
+
+// ------------------------------------------------------------ device buffer
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t count = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    count = 0;
+  }
+  // grows (never shrinks); contents are NOT preserved
+  void reserve(size_t n) {
+    if (n <= count) return;
+    release();
+    FLZ_CUDA(cudaMalloc(&p, n * sizeof(T)));
+    count = n;
+  }
+  void reserve_zero(size_t n, cudaStream_t s) {
+    reserve(n);
+    FLZ_CUDA(cudaMemsetAsync(p, 0, count * sizeof(T), s));
+  }
+};
+
+inline int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+constexpr int kSliceRows = 32;   // SELL-C: C = one warp of rows per slice
+constexpr int kMaxFuse = 4;      // block columns fused per Clenshaw-step launch
+constexpr int kLdAlign = 32;     // leading dimensions are multiples of 32 doubles (256 B)
+
+}  // namespace flz
+
+// ---------------------------------------------------------------- context
+struct flz_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_halo_ready = nullptr;   // send buffer packed (compute -> comm)
+  cudaEvent_t ev_halo_done = nullptr;    // halo received (comm -> compute)
+  int rank = 0, nranks = 1;
+  ncclComm_t comm = nullptr;
+  bool exact = false;
+  int sm_count = 148;
+  uint64_t launches = 0;
+  cudaEvent_t t0[16] = {}, t1[16] = {};
+  flz::DevBuf<double> partial;   // split-K partial sums of the tall-skinny GEMMs
+  flz::DevBuf<double> small;     // small device scratch of the host-buffer test seams
+  flz::DevBuf<double> stage;     // host<->device staging of blocks
+  flz::DevBuf<double> stage2;
+  flz::DevBuf<char> flush;       // L2 flush target
+};
+
+// ----------------------------------------------------------------- matrix
+// SELL-32-sigma, rows permuted by `perm` (new -> old local row).  The whole device
+// side works in the permuted ordering; only host transfers apply perm.
+struct flz_matrix {
+  flz_ctx* ctx = nullptr;
+  int64_t n_global = 0;
+  int64_t row_begin = 0, row_end = 0;
+  int64_t nl = 0;         // local rows
+  int64_t ld = 0;         // padded local rows (multiple of kLdAlign)
+  int64_t nnz = 0;        // true local nonzeros
+  int64_t stored = 0;     // stored entries incl. padding
+  int64_t nslices = 0;
+  int64_t nhalo = 0;      // halo rows appended after the nl local rows of a gather source
+  int sigma = 1;
+  // device arrays
+  flz::DevBuf<int64_t> slice_ptr;   // [nslices+1] element offsets
+  flz::DevBuf<int32_t> slice_len;   // [nslices]
+  flz::DevBuf<int32_t> row_len;     // [nslices*32]
+  flz::DevBuf<int32_t> col;         // [stored] permuted local col or nl + halo slot
+  flz::DevBuf<double> val;          // [stored]
+  flz::DevBuf<int32_t> perm;        // [nl] new -> old
+  flz::DevBuf<int32_t> iperm;       // [nl] old -> new
+  flz::DevBuf<int32_t> interior;    // slice ids without halo references
+  flz::DevBuf<int32_t> boundary;    // slice ids with halo references
+  int64_t n_interior = 0, n_boundary = 0;
+  std::vector<int32_t> h_perm, h_iperm;
+  // halo exchange plan (distributed only)
+  struct Peer {
+    int rank;
+    int64_t send_off, send_count;   // rows of send_rows (permuted local ids) to pack
+    int64_t recv_off, recv_count;   // halo slots [recv_off, recv_off+recv_count)
+  };
+  std::vector<Peer> peers;
+  flz::DevBuf<int32_t> send_rows;   // concatenated per-peer send lists
+  int64_t n_send = 0;
+  flz::DevBuf<double> send_buf;     // n_send * kMaxFuse doubles
+  // filter workspaces (interleaved (nl+nhalo) x R), created on first use
+  mutable flz::DevBuf<double> y1, y2, xs, zs;
+};
+
+// ------------------------------------------------------------------ basis
+struct flz_basis {
+  flz_ctx* ctx = nullptr;
+  const flz_matrix* A = nullptr;
+  int64_t nl = 0, ld = 0;
+  int r = 0;
+  int64_t max_cols = 0;
+  int64_t k = 0;                       // completed blocks
+  // ld x (max_cols + r) column-major; cudaMalloc is lazy about physical pages and nothing
+  // is zero-filled up front (the reference zero-fills eagerly, lanczos.cpp:111); rows
+  // [nl, ld) of every written column are kept zero.
+  flz::DevBuf<double> Q;
+  flz::DevBuf<double> Z;               // ld x r operator output / remainder
+  flz::DevBuf<double> X;               // ld x r staged newest block
+  flz::DevBuf<double> small;           // coefficient blocks C1/C2, S_k, scalars, op_scale
+  double* pinned = nullptr;            // pinned host mirror of `small`
+  size_t pinned_count = 0;
+  // recovery storage
+  flz::DevBuf<double> V, AV, V2, AV2;
+  int w_kept = 0;
+  double op_scale = 0.0;
+  double mv_s = 0.0, orth_s = 0.0;
+  cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr;
+  double* col(int64_t j) const { return Q.p + j * ld; }
+};
+
+namespace flz {
+
+// --------------------------------------------------------- kernel launchers
+// (kernels_sell.cu)
+struct SellView {
+  const int64_t* slice_ptr;
+  const int32_t* slice_len;
+  const int32_t* row_len;
+  const int32_t* col;
+  const double* val;
+  const int32_t* slice_ids;  // nullptr: all slices [0, nslices)
+  int64_t nslices;           // number of slices this launch covers
+  int64_t nl;
+};
+
+enum class StepMode { step, final, plain };
+
+// One fused Clenshaw step (or plain SpMM) for R in [1, kMaxFuse] interleaved columns:
+//   step : Y2[i,:] = s1*(A Y1)[i,:] + s2*Y1[i,:] - Y2[i,:] + b*X[i,:]   (interleaved out)
+//   final: Out[:,k] column-major (ld = ldo) receives the same expression
+//   plain: Out[:,k] = (A Y1)[i,k]
+void launch_clenshaw_step(flz_ctx* ctx, const SellView& A, int R, StepMode mode, bool exact,
+                          double s1, double s2, double b, const double* Y1, double* Y2,
+                          const double* X, int64_t ldx, double* Out, int64_t ldo);
+// Y1[i*R+k] = scale * X[k*ldx+i]  (column-major -> interleaved); scale==1 is a pure copy
+void launch_interleave(flz_ctx* ctx, int64_t nl, int R, double scale, const double* X,
+                       int64_t ldx, double* Y1);
+// halo packing: buf[s*R+k] = Y1[rows[s]*R+k]
+void launch_pack_rows(flz_ctx* ctx, cudaStream_t stream, int64_t count, int R,
+                      const int32_t* rows, const double* Y1, double* buf);
+// out[i] = s1*w[i] + s2*y1[i] - y2[i] + b*x[i]
+void launch_combine(flz_ctx* ctx, int64_t n, bool exact, double s1, double s2, double b,
+                    const double* w, const double* y1, const double* y2, const double* x,
+                    double* out);
+
+// (kernels_dense.cu)
+// C[M x N] (row-major, row stride ldc) = A[:, 0..M)^T B[:, 0..N) over `rows` rows, A and B
+// column-major with leading dimensions lda/ldb (multiples of 8, zero padded past `rows`).
+// FP64 DMMA, deterministic split-K (partials in ctx->partial, fixed-order reduction).
+void launch_gemm_tn(flz_ctx* ctx, const double* A, int64_t lda, int64_t M, const double* B,
+                    int64_t ldb, int N, int64_t rows, double* C, int64_t ldc);
+// Out[:, 0..N) (column-major, ldo) = alpha * A[:, 0..K) * Bs (+ Out when accumulate);
+// Bs row-major [K][ldbs] with ldbs a multiple of 8 and zero padded columns.
+void launch_gemm_nn(flz_ctx* ctx, const double* A, int64_t lda, int64_t K, const double* Bs,
+                    int64_t ldbs, int N, int64_t rows, double alpha, bool accumulate, double* Out,
+                    int64_t ldo);
+// out[c] = sum_i A[i,c]*B[i,c], c < N (column-major, lda/ldb)
+void launch_coldot(flz_ctx* ctx, const double* A, int64_t lda, const double* B, int64_t ldb, int N,
+                   int64_t rows, double* out);
+// dest[i] = src[i] * (*inv) for i < rows  (inv read from device memory)
+void launch_scale_copy(flz_ctx* ctx, const double* src, const double* inv, double* dest,
+                       int64_t rows);
+// per column c: A[:,c] *= s[c]
+void launch_scale_cols(flz_ctx* ctx, double* A, int64_t lda, int N, int64_t rows, const double* s);
+// residual kernel: v = V[:,c]*inv[c]; av = AV[:,c]*inv[c] - lambda[c]*v; V[:,c] = v;
+// AV[:,c] = av   (norms via coldot afterwards)
+void launch_residual_prep(flz_ctx* ctx, double* V, double* AV, int64_t ld, int N, int64_t rows,
+                          const double* inv, const double* lambda);
+// gather/scatter rows by permutation between a host-ordered block and a device-ordered one
+// dst[perm-ordered] : dst[c*ldd + inew] = src[c*lds + perm[inew]]
+void launch_permute_in(flz_ctx* ctx, const double* src, int64_t lds, double* dst, int64_t ldd,
+                       int N, int64_t rows, const int32_t* perm);
+void launch_permute_out(flz_ctx* ctx, const double* src, int64_t lds, double* dst, int64_t ldd,
+                        int N, int64_t rows, const int32_t* perm);
+// block-step scalar logic (single thread kernels)
+void launch_update_scale(flz_ctx* ctx, const double* gram, int r, int ldg, double* op_scale);
+void launch_finish_col(flz_ctx* ctx, const double* normsq, const double* op_scale, double* Sk,
+                       int r, int j, double* inv, double* dead_flag);
+
+}  // namespace flz

@@ -1,0 +1,418 @@
+// kernels_dense.cu — K3..K9: the dense contractions of the Lanczos engine as FP64
+// tensor-core (DMMA, mma.sync.m8n8k4.f64) GEMMs, plus the small vector helpers.
+//
+// Reference call sites replaced:
+//   gemm_tn  C = A^T B  (reduction over the long dimension n):
+//            cgs_pass projections  (lanczos.cpp:35-42, :177-182)      M = k*r, N = r
+//            intra-block QR dots   (lanczos.cpp:205-230)              M < r,   N = 1
+//            B = V^T A V           (lanczos.cpp:451-457)              M = N = w
+//   gemm_nn  Out (+)= alpha A Bs  (long dimension n is the M side):
+//            cgs_pass updates      (lanczos.cpp:35-42)                K = k*r, N = r
+//            Ritz lift V = Q_k W   (lanczos.cpp:422-433)              K = dim, N = w
+//            rotation V U, AV U    (lanczos.cpp:461-472)              K = N = w
+//
+// tcgen05.mma has no f64 kind, so FP64 tensor work on sm_100a is the warp-level
+// mma.sync path (SASS: DMMA.8x8x4).  Both GEMMs are HBM-bound for N = r <= 4 (0.75
+// flop/B); the tensor pipe just takes the multiply-add issue pressure off the FP64 ALUs.
+//
+// Determinism: every reduction has a fixed order (split-K partials are combined by a
+// second kernel in chunk order), so repeated solves are bitwise identical, like the
+// reference (kernels.hpp:9-11).
+
+#include "flz_internal.hpp"
+
+namespace flz {
+
+namespace {
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile(
+      "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+
+// ---------------------------------------------------------------- gemm_tn
+// grid (ceil(M/64), nchunks, ceil(N/(8*NT))), 256 threads = 8 warps; warp w owns the 8
+// A-columns m0 = blockIdx.x*64 + 8w .. +8 and the 8*NT B-columns n0 = blockIdx.z*8*NT ..;
+// it streams `rows_per_chunk` rows (multiple of 8) and writes its 8 x 8NT partial tile.
+// Lane (g = lane>>2, t = lane&3) loads the double2 at rows k+2t, k+2t+1 of column g: the
+// .x halves of a warp form one 8x4 k-slab, the .y halves the next (the k order inside an
+// MMA is free as long as A and B agree), so every load is a full 16 B per lane.
+template <int NT>
+__global__ void __launch_bounds__(256)
+    gemm_tn_kernel(const double* __restrict__ A, int64_t lda, int64_t M,
+                   const double* __restrict__ B, int64_t ldb, int N, int64_t rows8,
+                   int64_t rows_per_chunk, double* __restrict__ part, int64_t Mpad, int Npad) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int64_t m0 = (int64_t)blockIdx.x * 64 + warp * 8;
+  if (m0 >= M) return;
+  const int n0 = blockIdx.z * 8 * NT;
+  const int64_t k0 = (int64_t)blockIdx.y * rows_per_chunk;
+  const int64_t k1 = min(k0 + rows_per_chunk, rows8);
+
+  const bool a_ok = (m0 + g) < M;
+  const double* ap = A + (a_ok ? (m0 + g) : 0) * lda + 2 * t;
+  const double* bp[NT];
+  bool b_ok[NT];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    b_ok[nt] = (n0 + 8 * nt + g) < N;
+    bp[nt] = B + (int64_t)(b_ok[nt] ? (n0 + 8 * nt + g) : 0) * ldb + 2 * t;
+  }
+  double c[NT][2];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) c[nt][0] = c[nt][1] = 0.0;
+
+#pragma unroll 4
+  for (int64_t k = k0; k < k1; k += 8) {
+    double2 a2 = a_ok ? *reinterpret_cast<const double2*>(ap + k) : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      double2 b2 = b_ok[nt] ? *reinterpret_cast<const double2*>(bp[nt] + k)
+                            : make_double2(0.0, 0.0);
+      dmma(c[nt][0], c[nt][1], a2.x, b2.x);
+      dmma(c[nt][0], c[nt][1], a2.y, b2.y);
+    }
+  }
+  // C fragment: row g, columns 2t, 2t+1 of each 8x8 tile
+  double* out = part + ((int64_t)blockIdx.y * Mpad + m0 + g) * Npad + n0 + 2 * t;
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    out[8 * nt] = c[nt][0];
+    out[8 * nt + 1] = c[nt][1];
+  }
+}
+
+// C[m][n] = sum over chunks (in chunk order) of part[chunk][m][n]
+__global__ void reduce_partials_kernel(const double* __restrict__ part, int64_t nchunks,
+                                       int64_t M, int N, int64_t Mpad, int Npad,
+                                       double* __restrict__ C, int64_t ldc) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= M * Npad) return;
+  const int64_t m = idx / Npad;
+  const int n = (int)(idx % Npad);
+  if (n >= N) return;
+  double s = 0.0;
+  for (int64_t ch = 0; ch < nchunks; ++ch) s += part[(ch * Mpad + m) * Npad + n];
+  C[m * ldc + n] = s;
+}
+
+// ---------------------------------------------------------------- gemm_nn
+// grid (ceil(rows/128), ceil(N/(8*NT))), 256 threads; warp w owns rows i0 = blockIdx.x*128
+// + 16w .. +16 as two interleaved 8-row tiles (even rows / odd rows, again so that each
+// lane loads a double2), and 8*NT output columns.  Bs (row-major [K][ldbs]) stays in L1/L2.
+template <int NT, bool ACCUM>
+__global__ void __launch_bounds__(256)
+    gemm_nn_kernel(const double* __restrict__ A, int64_t lda, int64_t K,
+                   const double* __restrict__ Bs, int64_t ldbs, int N, int64_t rows, double alpha,
+                   double* __restrict__ Out, int64_t ldo) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int64_t i0 = (int64_t)blockIdx.x * 128 + warp * 16;
+  if (i0 >= rows) return;
+  const int n0 = blockIdx.y * 8 * NT;
+
+  double ce[NT][2], co[NT][2];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) ce[nt][0] = ce[nt][1] = co[nt][0] = co[nt][1] = 0.0;
+
+  const double* ap = A + i0 + 2 * g;     // + (j0+t)*lda
+  const double* bp = Bs + n0 + g;        // + (j0+t)*ldbs + 8*nt
+  const int64_t K4 = K & ~(int64_t)3;
+#pragma unroll 4
+  for (int64_t j0 = 0; j0 < K4; j0 += 4) {
+    const double2 a2 = *reinterpret_cast<const double2*>(ap + (j0 + t) * lda);
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const double b = bp[(j0 + t) * ldbs + 8 * nt];
+      dmma(ce[nt][0], ce[nt][1], a2.x, b);
+      dmma(co[nt][0], co[nt][1], a2.y, b);
+    }
+  }
+  if (K4 < K) {
+    const bool ok = (K4 + t) < K;
+    const double2 a2 = ok ? *reinterpret_cast<const double2*>(ap + (K4 + t) * lda)
+                          : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const double b = ok ? bp[(K4 + t) * ldbs + 8 * nt] : 0.0;
+      dmma(ce[nt][0], ce[nt][1], a2.x, b);
+      dmma(co[nt][0], co[nt][1], a2.y, b);
+    }
+  }
+  // fragment (row g of the even/odd tile, columns 2t, 2t+1) -> rows i0+2g, i0+2g+1
+  const int64_t i = i0 + 2 * g;
+  if (i >= rows) return;
+  const bool second = (i + 1) < rows;
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int n = n0 + 8 * nt + 2 * t + e;
+      if (n >= N) continue;
+      double* o = Out + (int64_t)n * ldo + i;
+      double v0 = alpha * ce[nt][e], v1 = alpha * co[nt][e];
+      if constexpr (ACCUM) {
+        const double2 old = *reinterpret_cast<const double2*>(o);
+        v0 += old.x;
+        v1 += old.y;
+      }
+      if (second)
+        *reinterpret_cast<double2*>(o) = make_double2(v0, v1);
+      else
+        o[0] = v0;
+    }
+}
+
+// ---------------------------------------------------------------- helpers
+// out[c] = sum_i A[i,c]*B[i,c]: one block row-chunk per (chunk, c), fixed-order tree
+__global__ void __launch_bounds__(256)
+    coldot_partial_kernel(const double* __restrict__ A, int64_t lda, const double* __restrict__ B,
+                          int64_t ldb, int64_t rows, int64_t rows_per_chunk,
+                          double* __restrict__ part, int N) {
+  __shared__ double sm[256];
+  const int c = blockIdx.y;
+  const int64_t k0 = (int64_t)blockIdx.x * rows_per_chunk;
+  const int64_t k1 = min(k0 + rows_per_chunk, rows);
+  const double* a = A + (int64_t)c * lda;
+  const double* b = B + (int64_t)c * ldb;
+  double s = 0.0;
+  for (int64_t i = k0 + threadIdx.x; i < k1; i += 256) s = fma(a[i], b[i], s);
+  sm[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sm[threadIdx.x] += sm[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[(int64_t)blockIdx.x * N + c] = sm[0];
+}
+
+__global__ void coldot_reduce_kernel(const double* __restrict__ part, int64_t nchunks, int N,
+                                     double* __restrict__ out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= N) return;
+  double s = 0.0;
+  for (int64_t ch = 0; ch < nchunks; ++ch) s += part[ch * N + c];
+  out[c] = s;
+}
+
+__global__ void scale_copy_kernel(const double* __restrict__ src, const double* __restrict__ inv,
+                                  double* __restrict__ dest, int64_t rows) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows) return;
+  dest[i] = src[i] * (*inv);
+}
+
+__global__ void scale_cols_kernel(double* __restrict__ A, int64_t lda, int64_t rows,
+                                  const double* __restrict__ s) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows) return;
+  const int c = blockIdx.y;
+  A[(int64_t)c * lda + i] *= s[c];
+}
+
+__global__ void residual_prep_kernel(double* __restrict__ V, double* __restrict__ AV, int64_t ld,
+                                     int64_t rows, const double* __restrict__ inv,
+                                     const double* __restrict__ lambda) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows) return;
+  const int c = blockIdx.y;
+  const double s = inv[c];
+  const double v = V[(int64_t)c * ld + i] * s;
+  const double av = AV[(int64_t)c * ld + i] * s;
+  V[(int64_t)c * ld + i] = v;
+  AV[(int64_t)c * ld + i] = fma(-lambda[c], v, av);
+}
+
+__global__ void permute_in_kernel(const double* __restrict__ src, int64_t lds,
+                                  double* __restrict__ dst, int64_t ldd, int64_t rows,
+                                  const int32_t* __restrict__ perm) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows) return;
+  const int c = blockIdx.y;
+  dst[(int64_t)c * ldd + i] = src[(int64_t)c * lds + perm[i]];
+}
+
+__global__ void permute_out_kernel(const double* __restrict__ src, int64_t lds,
+                                   double* __restrict__ dst, int64_t ldd, int64_t rows,
+                                   const int32_t* __restrict__ perm) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows) return;
+  const int c = blockIdx.y;
+  dst[(int64_t)c * ldd + perm[i]] = src[(int64_t)c * lds + i];
+}
+
+// op_scale = max(op_scale, sqrt(gram[j][j])) (lanczos.cpp:169-170)
+__global__ void update_scale_kernel(const double* gram, int r, int ldg, double* op_scale) {
+  double s = *op_scale;
+  for (int j = 0; j < r; ++j) s = fmax(s, sqrt(fmax(gram[j * ldg + j], 0.0)));
+  *op_scale = s;
+}
+
+// norm = sqrt(normsq); live iff norm > 1e-10*max(op_scale,1e-300) (lanczos.cpp:201, :224-230)
+__global__ void finish_col_kernel(const double* normsq, const double* op_scale, double* Sk, int r,
+                                  int j, double* inv, double* dead_flag) {
+  const double norm = sqrt(fmax(*normsq, 0.0));
+  const double dead_tol = 1e-10 * fmax(*op_scale, 1e-300);
+  if (norm > dead_tol) {
+    Sk[j * r + j] = norm;
+    *inv = 1.0 / norm;
+    *dead_flag = 0.0;
+  } else {
+    Sk[j * r + j] = 0.0;
+    *inv = 0.0;
+    *dead_flag = 1.0;
+  }
+}
+
+}  // namespace
+
+// --------------------------------------------------------------- launchers
+
+void launch_gemm_tn(flz_ctx* ctx, const double* A, int64_t lda, int64_t M, const double* B,
+                    int64_t ldb, int N, int64_t rows, double* C, int64_t ldc) {
+  if (M <= 0 || N <= 0) return;
+  const int64_t rows8 = round_up(rows, 8);
+  FLZ_REQUIRE(rows8 <= lda && rows8 <= ldb, FLZ_EDIM, "gemm_tn: leading dimension too small");
+  const int NT = N > 16 ? 4 : (N > 8 ? 2 : 1);
+  const int64_t mblocks = (M + 63) / 64;
+  const int nblocks = (N + 8 * NT - 1) / (8 * NT);
+  // enough CTAs to fill the machine ~4x, chunks of at least 512 rows
+  int64_t want = (int64_t)ctx->sm_count * 4;
+  int64_t nchunks = (want + mblocks * nblocks - 1) / (mblocks * nblocks);
+  const int64_t max_chunks = (rows8 + 511) / 512;
+  if (nchunks > max_chunks) nchunks = max_chunks;
+  if (nchunks < 1) nchunks = 1;
+  int64_t rpc = round_up((rows8 + nchunks - 1) / nchunks, 8);
+  nchunks = (rows8 + rpc - 1) / rpc;
+  const int64_t Mpad = mblocks * 64;
+  const int Npad = nblocks * 8 * NT;
+  ctx->partial.reserve((size_t)(nchunks * Mpad * Npad));
+  dim3 grid((unsigned)mblocks, (unsigned)nchunks, (unsigned)nblocks);
+  switch (NT) {
+    case 1:
+      gemm_tn_kernel<1><<<grid, 256, 0, ctx->stream>>>(A, lda, M, B, ldb, N, rows8, rpc,
+                                                       ctx->partial.p, Mpad, Npad);
+      break;
+    case 2:
+      gemm_tn_kernel<2><<<grid, 256, 0, ctx->stream>>>(A, lda, M, B, ldb, N, rows8, rpc,
+                                                       ctx->partial.p, Mpad, Npad);
+      break;
+    default:
+      gemm_tn_kernel<4><<<grid, 256, 0, ctx->stream>>>(A, lda, M, B, ldb, N, rows8, rpc,
+                                                       ctx->partial.p, Mpad, Npad);
+      break;
+  }
+  const int64_t total = M * Npad;
+  reduce_partials_kernel<<<(unsigned)((total + 255) / 256), 256, 0, ctx->stream>>>(
+      ctx->partial.p, nchunks, M, N, Mpad, Npad, C, ldc);
+  ctx->launches += 2;
+  FLZ_CUDA(cudaGetLastError());
+}
+
+void launch_gemm_nn(flz_ctx* ctx, const double* A, int64_t lda, int64_t K, const double* Bs,
+                    int64_t ldbs, int N, int64_t rows, double alpha, bool accumulate, double* Out,
+                    int64_t ldo) {
+  if (rows <= 0 || N <= 0) return;
+  FLZ_REQUIRE(round_up(rows, 2) <= lda && round_up(rows, 2) <= ldo, FLZ_EDIM,
+              "gemm_nn: leading dimension too small");
+  const int NT = N > 32 ? 8 : (N > 16 ? 4 : (N > 8 ? 2 : 1));
+  FLZ_REQUIRE(ldbs >= round_up(N, 8 * NT), FLZ_EDIM, "gemm_nn: Bs row stride too small");
+  dim3 grid((unsigned)((rows + 127) / 128), (unsigned)((N + 8 * NT - 1) / (8 * NT)));
+#define FLZ_NN(NTV)                                                                              \
+  if (accumulate)                                                                                \
+    gemm_nn_kernel<NTV, true><<<grid, 256, 0, ctx->stream>>>(A, lda, K, Bs, ldbs, N, rows, alpha, \
+                                                             Out, ldo);                          \
+  else                                                                                           \
+    gemm_nn_kernel<NTV, false><<<grid, 256, 0, ctx->stream>>>(A, lda, K, Bs, ldbs, N, rows,      \
+                                                              alpha, Out, ldo)
+  switch (NT) {
+    case 1: FLZ_NN(1); break;
+    case 2: FLZ_NN(2); break;
+    case 4: FLZ_NN(4); break;
+    default: FLZ_NN(8); break;
+  }
+#undef FLZ_NN
+  ctx->launches++;
+  FLZ_CUDA(cudaGetLastError());
+}
+
+void launch_coldot(flz_ctx* ctx, const double* A, int64_t lda, const double* B, int64_t ldb, int N,
+                   int64_t rows, double* out) {
+  if (N <= 0) return;
+  int64_t nchunks = ((int64_t)ctx->sm_count * 8 + N - 1) / N;
+  const int64_t max_chunks = (rows + 2047) / 2048;
+  if (nchunks > max_chunks) nchunks = max_chunks;
+  if (nchunks < 1) nchunks = 1;
+  const int64_t rpc = (rows + nchunks - 1) / nchunks;
+  nchunks = rpc > 0 ? (rows + rpc - 1) / rpc : 1;
+  if (nchunks < 1) nchunks = 1;
+  ctx->partial.reserve((size_t)(nchunks * N));
+  dim3 grid((unsigned)nchunks, (unsigned)N);
+  coldot_partial_kernel<<<grid, 256, 0, ctx->stream>>>(A, lda, B, ldb, rows, rpc, ctx->partial.p,
+                                                       N);
+  coldot_reduce_kernel<<<(N + 127) / 128, 128, 0, ctx->stream>>>(ctx->partial.p, nchunks, N, out);
+  ctx->launches += 2;
+  FLZ_CUDA(cudaGetLastError());
+}
+
+void launch_scale_copy(flz_ctx* ctx, const double* src, const double* inv, double* dest,
+                       int64_t rows) {
+  if (rows <= 0) return;
+  scale_copy_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, ctx->stream>>>(src, inv, dest, rows);
+  ctx->launches++;
+  FLZ_CUDA(cudaGetLastError());
+}
+
+void launch_scale_cols(flz_ctx* ctx, double* A, int64_t lda, int N, int64_t rows,
+                       const double* s) {
+  if (rows <= 0 || N <= 0) return;
+  dim3 grid((unsigned)((rows + 255) / 256), (unsigned)N);
+  scale_cols_kernel<<<grid, 256, 0, ctx->stream>>>(A, lda, rows, s);
+  ctx->launches++;
+  FLZ_CUDA(cudaGetLastError());
+}
+
+void launch_residual_prep(flz_ctx* ctx, double* V, double* AV, int64_t ld, int N, int64_t rows,
+                          const double* inv, const double* lambda) {
+  if (rows <= 0 || N <= 0) return;
+  dim3 grid((unsigned)((rows + 255) / 256), (unsigned)N);
+  residual_prep_kernel<<<grid, 256, 0, ctx->stream>>>(V, AV, ld, rows, inv, lambda);
+  ctx->launches++;
+  FLZ_CUDA(cudaGetLastError());
+}
+
+void launch_permute_in(flz_ctx* ctx, const double* src, int64_t lds, double* dst, int64_t ldd,
+                       int N, int64_t rows, const int32_t* perm) {
+  if (rows <= 0 || N <= 0) return;
+  dim3 grid((unsigned)((rows + 255) / 256), (unsigned)N);
+  permute_in_kernel<<<grid, 256, 0, ctx->stream>>>(src, lds, dst, ldd, rows, perm);
+  ctx->launches++;
+  FLZ_CUDA(cudaGetLastError());
+}
+
+void launch_permute_out(flz_ctx* ctx, const double* src, int64_t lds, double* dst, int64_t ldd,
+                        int N, int64_t rows, const int32_t* perm) {
+  if (rows <= 0 || N <= 0) return;
+  dim3 grid((unsigned)((rows + 255) / 256), (unsigned)N);
+  permute_out_kernel<<<grid, 256, 0, ctx->stream>>>(src, lds, dst, ldd, rows, perm);
+  ctx->launches++;
+  FLZ_CUDA(cudaGetLastError());
+}
+
+void launch_update_scale(flz_ctx* ctx, const double* gram, int r, int ldg, double* op_scale) {
+  update_scale_kernel<<<1, 1, 0, ctx->stream>>>(gram, r, ldg, op_scale);
+  ctx->launches++;
+  FLZ_CUDA(cudaGetLastError());
+}
+
+void launch_finish_col(flz_ctx* ctx, const double* normsq, const double* op_scale, double* Sk,
+                       int r, int j, double* inv, double* dead_flag) {
+  finish_col_kernel<<<1, 1, 0, ctx->stream>>>(normsq, op_scale, Sk, r, j, inv, dead_flag);
+  ctx->launches++;
+  FLZ_CUDA(cudaGetLastError());
+}
+
+}  // namespace flz
