@@ -1,0 +1,130 @@
+// flz/matrix.hpp — host containers of the drop-in C++ API: errors, DenseBlock,
+// SparseSymMatrix (+ Matrix Market I/O) and the device handle behind them.
+//
+// Mirrors the reference's speig/error.hpp:9-25, speig/dense_block.hpp:11-40 and
+// speig/sparse.hpp:12-79 (same names, argument meaning and error behaviour); the
+// arithmetic entry points (spmv / spmm_block / apply_uncounted) run on the GPU
+// through the C ABI (include/flz.h) instead of kernels::csr_matvec.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+struct flz_ctx;
+struct flz_matrix;
+
+namespace flz {
+
+// ------------------------------------------------------------------ errors
+struct Error : std::runtime_error {
+  explicit Error(const std::string& what) : std::runtime_error(what) {}
+};
+struct ParseError : Error { using Error::Error; };      // malformed input file
+struct IntervalError : Error { using Error::Error; };   // invalid / empty / outside interval
+struct DimensionError : Error { using Error::Error; };  // shape mismatch
+struct DeviceError : Error { using Error::Error; };     // CUDA / NCCL / no device
+
+// Translates a C-ABI status into the exception the reference would throw.
+void throw_status(int status);
+
+// ------------------------------------------------------------------ device
+// Process-wide default GPU context used by the C++ API (created on first use; there is
+// no CPU fallback, so this throws DeviceError without an sm_100 GPU).
+class Device {
+ public:
+  static flz_ctx* context();
+  // Adopt an externally created context (e.g. a distributed one from flz_ctx_create_dist).
+  static void adopt(flz_ctx* ctx);
+  static void set_device(int index);  // before first use
+  static void shutdown();
+};
+
+// -------------------------------------------------------------- DenseBlock
+// Column-major rows x cols block, zero-initialised.
+class DenseBlock {
+ public:
+  DenseBlock() = default;
+  DenseBlock(std::size_t rows, std::size_t cols)
+      : rows_(rows), cols_(cols), data_(rows * cols, 0.0) {}
+
+  std::size_t rows() const { return rows_; }
+  std::size_t cols() const { return cols_; }
+  std::size_t size() const { return data_.size(); }
+  double* data() { return data_.data(); }
+  const double* data() const { return data_.data(); }
+  double* col(std::size_t j) { return data_.data() + j * rows_; }
+  const double* col(std::size_t j) const { return data_.data() + j * rows_; }
+  double& operator()(std::size_t i, std::size_t j) { return data_[j * rows_ + i]; }
+  double operator()(std::size_t i, std::size_t j) const { return data_[j * rows_ + i]; }
+
+  static DenseBlock identity(std::size_t n) {
+    DenseBlock I(n, n);
+    for (std::size_t i = 0; i < n; ++i) I(i, i) = 1.0;
+    return I;
+  }
+
+ private:
+  std::size_t rows_ = 0, cols_ = 0;
+  std::vector<double> data_;
+};
+
+// ---------------------------------------------------------- SparseSymMatrix
+struct Triplet {
+  std::int64_t row;
+  std::int64_t col;
+  double value;
+};
+
+// Real symmetric CSR matrix, both triangles stored, exact symmetry enforced at
+// construction, immutable afterwards.  The SELL-C-sigma device copy is created lazily on
+// first arithmetic use and shared by all copies of the object.
+class SparseSymMatrix {
+ public:
+  static SparseSymMatrix from_entries(std::size_t n, std::vector<Triplet> entries);
+  // Adopts already validated CSR arrays (sorted, duplicate-free, exactly symmetric) —
+  // used by generators that build CSR directly; `check` re-verifies symmetry.
+  static SparseSymMatrix from_csr(std::size_t n, std::vector<std::int64_t> row_ptr,
+                                  std::vector<std::int32_t> col_idx, std::vector<double> values,
+                                  bool check = true);
+
+  std::size_t dim() const { return n_; }
+  std::size_t nnz() const { return static_cast<std::size_t>(row_ptr_.back()); }
+  const std::vector<std::int64_t>& row_ptr() const { return row_ptr_; }
+  const std::vector<std::int32_t>& col_idx() const { return col_idx_; }
+  const std::vector<double>& values() const { return values_; }
+  double max_abs() const { return max_abs_; }
+
+  void spmv(const double* x, double* y) const;                      // counted (+1)
+  std::vector<double> spmv(const std::vector<double>& x) const;
+  void spmm_block(const DenseBlock& X, DenseBlock& Y) const;        // counted (+X.cols())
+  DenseBlock spmm_block(const DenseBlock& X) const;
+  void apply_uncounted(const double* x, double* y) const;
+
+  // Device handle on the default context (uploads on first call).
+  flz_matrix* device() const;
+
+ private:
+  SparseSymMatrix() = default;
+  void verify_symmetry() const;
+
+  std::size_t n_ = 0;
+  std::vector<std::int64_t> row_ptr_{0};
+  std::vector<std::int32_t> col_idx_;
+  std::vector<double> values_;
+  double max_abs_ = 0.0;
+  struct DeviceCopy;
+  mutable std::shared_ptr<DeviceCopy> dev_;
+};
+
+SparseSymMatrix load_matrix_market(const std::string& path);
+void save_matrix_market(const SparseSymMatrix& A, const std::string& path);
+void save_dense_matrix_market(const DenseBlock& X, const std::string& path);
+
+std::uint64_t matvec_count();
+void reset_matvec_count();
+
+}  // namespace flz

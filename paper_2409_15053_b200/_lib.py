@@ -106,35 +106,40 @@ _SIGS = {
     "flz_bounds_lanczos": (i32, [vp, vp, i32, f64p, f64p, f64p, dP, iP]),
 }
 
-# host-side solver entry points (csrc/host/capi_solver.cpp); bound when present
+# host-side solver entry points (include/flz_solver.h, csrc/host/capi_solver.cpp)
 _SOLVER_SIGS = {
-    "flz_solve": (i32, [vp, vp, i64, i64p, i32p, f64p, d, d, C.POINTER(FlzConfig), i32,
-                        C.POINTER(vp)]),
-    "flz_result_free": (None, [vp]),
-    "flz_result_count": (i64, [vp]),
-    "flz_result_get": (i32, [vp, vp, vp, vp, C.POINTER(FlzStats)]),
+    "flz_config_default": (None, [C.POINTER(FlzConfig)]),
+    "flz_set_default_ctx": (i32, [vp]),
+    "flz_hostmatrix_from_triplets": (i32, [i64, i64, i64p, i64p, f64p, C.POINTER(vp)]),
+    "flz_hostmatrix_from_csr": (i32, [i64, i64p, i32p, f64p, i32, C.POINTER(vp)]),
+    "flz_hostmatrix_load_mm": (i32, [C.c_char_p, C.POINTER(vp)]),
+    "flz_hostmatrix_save_mm": (i32, [vp, C.c_char_p]),
+    "flz_hostmatrix_free": (None, [vp]),
+    "flz_hostmatrix_dims": (i32, [vp, i64P, i64P]),
+    "flz_hostmatrix_csr": (i32, [vp, i64p, i32p, f64p]),
+    "flz_hostmatrix_spmm": (i32, [vp, f64p, i32, f64p]),
+    "flz_hostmatrix_filter_apply": (i32, [vp, f64p, i32, d, d, f64p, i32, f64p]),
     "flz_indicator_coefficients": (i32, [d, d, i32, f64p]),
     "flz_select_degree": (i32, [d, d, d, i32, iP]),
     "flz_clenshaw": (d, [f64p, i32, d]),
     "flz_build_filter": (i32, [d, d, d, d, i32, d, i32, vp, i32, dP, dP, iP]),
     "flz_init_block": (i32, [i64, i32, u64, f64p]),
-    "flz_estimate_bounds": (i32, [vp, vp, i32, u64, dP, dP]),
+    "flz_estimate_bounds": (i32, [vp, i32, u64, dP, dP]),
     "flz_sym_band_eig": (i32, [i64, i64, f64p, f64p, vp]),
-    "flz_band_ritz_rows": (i32, [i64, i64, f64p, i64, i64p, f64p, f64p]),
-    "flz_fact_create": (i32, [vp, vp, vp, i32, d, d, d, d, f64p, i32, i64, C.POINTER(vp)]),
+    "flz_band_ritz_rows": (i32, [i64, i64, f64p, i64, i64p, f64p, vp]),
+    "flz_band_eigenvectors": (i32, [i64, i64, f64p, f64p, i64, i64p, f64p, dP, dP]),
+    "flz_fact_create": (i32, [vp, f64p, i32, d, d, d, d, f64p, i32, i64, C.POINTER(vp)]),
     "flz_fact_free": (None, [vp]),
     "flz_fact_expand": (i32, [vp, i32]),
     "flz_fact_block_count": (i64, [vp]),
-    "flz_fact_get": (i32, [vp, vp, f64p, f64p, u8p]),
+    "flz_fact_get": (i32, [vp, vp, vp, vp, vp]),
     "flz_fact_ortho_error": (i32, [vp, dP]),
     "flz_fact_flags": (i32, [vp]),
     "flz_fact_check": (i32, [vp, d, d, d, i32, f64p, f64p, u8p, u8p]),
-    "flz_matrix_from_triplets": (i32, [i64, i64, i64p, i64p, f64p, C.POINTER(vp)]),
-    "flz_matrix_load_mm": (i32, [C.c_char_p, C.POINTER(vp)]),
-    "flz_hostmatrix_free": (None, [vp]),
-    "flz_hostmatrix_dims": (i32, [vp, i64P, i64P]),
-    "flz_hostmatrix_csr": (i32, [vp, i64p, i32p, f64p]),
-    "flz_hostmatrix_save_mm": (i32, [vp, C.c_char_p]),
+    "flz_solve": (i32, [vp, d, d, C.POINTER(FlzConfig), i32, C.POINTER(vp)]),
+    "flz_result_free": (None, [vp]),
+    "flz_result_count": (i64, [vp]),
+    "flz_result_get": (i32, [vp, vp, vp, vp, C.POINTER(FlzStats)]),
 }
 
 
@@ -160,9 +165,8 @@ def lib() -> C.CDLL:
             fn = getattr(L, name)
             fn.restype, fn.argtypes = res, args
         for name, (res, args) in _SOLVER_SIGS.items():
-            if hasattr(L, name):
-                fn = getattr(L, name)
-                fn.restype, fn.argtypes = res, args
+            fn = getattr(L, name)
+            fn.restype, fn.argtypes = res, args
         _lib = L
     return _lib
 

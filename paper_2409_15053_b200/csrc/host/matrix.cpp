@@ -1,0 +1,430 @@
+// host/matrix.cpp — SparseSymMatrix, Matrix Market I/O, default device context.
+//
+// Behavioural contract: speig/sparse.hpp + src/sparse.cpp (from_entries :27-85, spmv /
+// spmm_block / apply_uncounted :87-117, Matrix Market reader :172-291 and writers
+// :293-331) and speig/error.hpp.  Products run on the GPU via include/flz.h.
+
+#include "flz/matrix.hpp"
+
+#include <algorithm>
+#include <cctype>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <mutex>
+
+#include "flz.h"
+
+namespace flz {
+
+// ------------------------------------------------------------ status -> throw
+void throw_status(int status) {
+  if (status == FLZ_OK) return;
+  const std::string msg = flz_last_error();
+  switch (status) {
+    case FLZ_EDIM: throw DimensionError(msg);
+    case FLZ_EINTERVAL: throw IntervalError(msg);
+    case FLZ_EPARSE: throw ParseError(msg);
+    case FLZ_ECUDA:
+    case FLZ_ENODEV:
+    case FLZ_ENCCL:
+    case FLZ_ENOMEM: throw DeviceError(msg);
+    default: throw Error(msg);
+  }
+}
+
+// ------------------------------------------------------------------ Device
+namespace {
+std::mutex g_dev_mutex;
+flz_ctx* g_ctx = nullptr;
+bool g_ctx_owned = false;
+int g_dev_index = -1;
+}  // namespace
+
+flz_ctx* Device::context() {
+  std::lock_guard<std::mutex> lock(g_dev_mutex);
+  if (!g_ctx) {
+    throw_status(flz_ctx_create(g_dev_index, &g_ctx));
+    g_ctx_owned = true;
+  }
+  return g_ctx;
+}
+void Device::adopt(flz_ctx* ctx) {
+  std::lock_guard<std::mutex> lock(g_dev_mutex);
+  if (g_ctx && g_ctx_owned) flz_ctx_destroy(g_ctx);
+  g_ctx = ctx;
+  g_ctx_owned = false;
+}
+void Device::set_device(int index) {
+  std::lock_guard<std::mutex> lock(g_dev_mutex);
+  g_dev_index = index;
+}
+void Device::shutdown() {
+  std::lock_guard<std::mutex> lock(g_dev_mutex);
+  if (g_ctx && g_ctx_owned) flz_ctx_destroy(g_ctx);
+  g_ctx = nullptr;
+  g_ctx_owned = false;
+}
+
+// --------------------------------------------------------- SparseSymMatrix
+struct SparseSymMatrix::DeviceCopy {
+  flz_matrix* handle = nullptr;
+  flz_ctx* ctx = nullptr;
+  ~DeviceCopy() {
+    if (handle) flz_matrix_destroy(handle);
+  }
+};
+
+namespace {
+bool coord_less(const Triplet& a, const Triplet& b) {
+  return a.row < b.row || (a.row == b.row && a.col < b.col);
+}
+}  // namespace
+
+SparseSymMatrix SparseSymMatrix::from_entries(std::size_t n, std::vector<Triplet> entries) {
+  const auto dim = static_cast<std::int64_t>(n);
+  for (const Triplet& t : entries) {
+    if (t.row < 0 || t.col < 0 || t.row >= dim || t.col >= dim)
+      throw Error("matrix entry index out of range");
+    if (!std::isfinite(t.value)) throw Error("matrix entry is not finite");
+  }
+  std::sort(entries.begin(), entries.end(), coord_less);
+
+  SparseSymMatrix A;
+  A.n_ = n;
+  A.row_ptr_.assign(n + 1, 0);
+  A.col_idx_.reserve(entries.size());
+  A.values_.reserve(entries.size());
+  // merge runs of equal coordinates while emitting CSR
+  for (std::size_t i = 0; i < entries.size();) {
+    double sum = entries[i].value;
+    std::size_t j = i + 1;
+    while (j < entries.size() && entries[j].row == entries[i].row &&
+           entries[j].col == entries[i].col)
+      sum += entries[j++].value;
+    A.row_ptr_[entries[i].row + 1] += 1;
+    A.col_idx_.push_back(static_cast<std::int32_t>(entries[i].col));
+    A.values_.push_back(sum);
+    A.max_abs_ = std::max(A.max_abs_, std::abs(sum));
+    i = j;
+  }
+  for (std::size_t i = 0; i < n; ++i) A.row_ptr_[i + 1] += A.row_ptr_[i];
+  A.verify_symmetry();
+  return A;
+}
+
+SparseSymMatrix SparseSymMatrix::from_csr(std::size_t n, std::vector<std::int64_t> row_ptr,
+                                          std::vector<std::int32_t> col_idx,
+                                          std::vector<double> values, bool check) {
+  if (row_ptr.size() != n + 1 || row_ptr.front() != 0 ||
+      static_cast<std::size_t>(row_ptr.back()) != col_idx.size() ||
+      col_idx.size() != values.size())
+    throw Error("from_csr: inconsistent CSR arrays");
+  SparseSymMatrix A;
+  A.n_ = n;
+  A.row_ptr_ = std::move(row_ptr);
+  A.col_idx_ = std::move(col_idx);
+  A.values_ = std::move(values);
+  for (std::size_t i = 0; i < n; ++i) {
+    if (A.row_ptr_[i] > A.row_ptr_[i + 1]) throw Error("from_csr: row_ptr is not monotone");
+    for (std::int64_t p = A.row_ptr_[i]; p < A.row_ptr_[i + 1]; ++p) {
+      const std::int32_t c = A.col_idx_[p];
+      if (c < 0 || static_cast<std::size_t>(c) >= n)
+        throw Error("matrix entry index out of range");
+      if (p > A.row_ptr_[i] && A.col_idx_[p - 1] >= c)
+        throw Error("from_csr: columns must be strictly ascending within a row");
+      if (!std::isfinite(A.values_[p])) throw Error("matrix entry is not finite");
+      A.max_abs_ = std::max(A.max_abs_, std::abs(A.values_[p]));
+    }
+  }
+  if (check) A.verify_symmetry();
+  return A;
+}
+
+// exact structural + numerical symmetry (sparse.cpp:65-83)
+void SparseSymMatrix::verify_symmetry() const {
+  for (std::size_t i = 0; i < n_; ++i)
+    for (std::int64_t p = row_ptr_[i]; p < row_ptr_[i + 1]; ++p) {
+      const auto j = static_cast<std::size_t>(col_idx_[p]);
+      if (j <= i) continue;
+      const std::int32_t* first = col_idx_.data() + row_ptr_[j];
+      const std::int32_t* last = col_idx_.data() + row_ptr_[j + 1];
+      const std::int32_t* hit = std::lower_bound(first, last, static_cast<std::int32_t>(i));
+      const std::string where = "(" + std::to_string(i) + "," + std::to_string(j) + ")";
+      if (hit == last || *hit != static_cast<std::int32_t>(i))
+        throw Error("matrix is structurally asymmetric at " + where);
+      if (values_[p] != values_[row_ptr_[j] + (hit - first)])
+        throw Error("matrix is numerically asymmetric at " + where);
+    }
+}
+
+flz_matrix* SparseSymMatrix::device() const {
+  flz_ctx* ctx = Device::context();
+  if (!dev_ || dev_->ctx != ctx) {
+    auto copy = std::make_shared<DeviceCopy>();
+    copy->ctx = ctx;
+    throw_status(flz_matrix_upload(ctx, static_cast<std::int64_t>(n_), 0,
+                                   static_cast<std::int64_t>(n_), row_ptr_.data(),
+                                   col_idx_.data(), values_.data(), 0, &copy->handle));
+    dev_ = std::move(copy);
+  }
+  return dev_->handle;
+}
+
+void SparseSymMatrix::apply_uncounted(const double* x, double* y) const {
+  throw_status(flz_spmm(Device::context(), device(), x, 1, y, 0));
+}
+void SparseSymMatrix::spmv(const double* x, double* y) const {
+  throw_status(flz_spmm(Device::context(), device(), x, 1, y, 1));
+}
+std::vector<double> SparseSymMatrix::spmv(const std::vector<double>& x) const {
+  if (x.size() != n_)
+    throw DimensionError("spmv: vector length " + std::to_string(x.size()) +
+                         " does not match matrix dimension " + std::to_string(n_));
+  std::vector<double> y(n_);
+  spmv(x.data(), y.data());
+  return y;
+}
+void SparseSymMatrix::spmm_block(const DenseBlock& X, DenseBlock& Y) const {
+  if (X.rows() != n_)
+    throw DimensionError("spmm_block: block has " + std::to_string(X.rows()) +
+                         " rows, matrix dimension is " + std::to_string(n_));
+  if (Y.rows() != X.rows() || Y.cols() != X.cols()) Y = DenseBlock(X.rows(), X.cols());
+  if (X.cols() == 0) return;
+  throw_status(flz_spmm(Device::context(), device(), X.data(), static_cast<int>(X.cols()),
+                        Y.data(), 1));
+}
+DenseBlock SparseSymMatrix::spmm_block(const DenseBlock& X) const {
+  DenseBlock Y(X.rows(), X.cols());
+  spmm_block(X, Y);
+  return Y;
+}
+
+std::uint64_t matvec_count() { return flz_matvec_count(); }
+void reset_matvec_count() { flz_reset_matvec_count(); }
+
+// ------------------------------------------------------------ Matrix Market
+namespace {
+
+[[noreturn]] void parse_fail(const std::string& path, std::size_t line, const std::string& msg) {
+  throw ParseError(path + ":" + std::to_string(line) + ": " + msg);
+}
+
+std::string lowered(std::string s) {
+  for (char& ch : s) ch = static_cast<char>(std::tolower(static_cast<unsigned char>(ch)));
+  return s;
+}
+
+// Splits the file image into lines without copying (pointers into `text`).
+struct LineCursor {
+  const char* p;
+  const char* end;
+  std::size_t lineno = 0;
+  bool next(const char*& b, const char*& e) {
+    if (p >= end) return false;
+    b = p;
+    const char* nl = static_cast<const char*>(std::memchr(p, '\n', end - p));
+    e = nl ? nl : end;
+    p = nl ? nl + 1 : end;
+    ++lineno;
+    return true;
+  }
+};
+
+bool skippable(const char* b, const char* e) {
+  for (; b < e; ++b) {
+    if (*b == '%') return true;
+    if (!std::isspace(static_cast<unsigned char>(*b))) return false;
+  }
+  return true;
+}
+
+enum class Field { real, integer, pattern };
+
+}  // namespace
+
+SparseSymMatrix load_matrix_market(const std::string& path) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) throw Error("cannot open '" + path + "'");
+  std::string text((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+  text.push_back('\0');  // strto* need a terminator
+  LineCursor cur{text.data(), text.data() + text.size() - 1};
+
+  const char *b, *e;
+  if (!cur.next(b, e)) throw ParseError(path + ": empty file");
+  // banner: %%MatrixMarket matrix coordinate <field> <symmetry>
+  std::string tok[5];
+  {
+    const char* q = b;
+    for (int t = 0; t < 5; ++t) {
+      while (q < e && std::isspace(static_cast<unsigned char>(*q))) ++q;
+      const char* s = q;
+      while (q < e && !std::isspace(static_cast<unsigned char>(*q))) ++q;
+      tok[t].assign(s, q);
+    }
+  }
+  if (lowered(tok[0]) != "%%matrixmarket")
+    parse_fail(path, 1, "not a Matrix Market file (missing %%MatrixMarket banner)");
+  if (lowered(tok[1]) != "matrix") parse_fail(path, 1, "unsupported object '" + tok[1] + "'");
+  if (lowered(tok[2]) != "coordinate")
+    parse_fail(path, 1, "unsupported format '" + tok[2] + "' (expected coordinate)");
+  Field field = Field::real;
+  const std::string f = lowered(tok[3]);
+  if (f == "real") field = Field::real;
+  else if (f == "integer") field = Field::integer;
+  else if (f == "pattern") field = Field::pattern;
+  else if (f == "complex") parse_fail(path, 1, "complex matrices are not supported");
+  else parse_fail(path, 1, "unsupported field '" + tok[3] + "'");
+  bool symmetric = false;
+  const std::string s = lowered(tok[4]);
+  if (s == "symmetric") symmetric = true;
+  else if (s == "general") symmetric = false;
+  else if (s == "skew-symmetric") parse_fail(path, 1, "skew-symmetric matrices are not supported");
+  else if (s == "hermitian") parse_fail(path, 1, "hermitian matrices are not supported");
+  else parse_fail(path, 1, "unsupported symmetry '" + tok[4] + "'");
+
+  // size line
+  std::int64_t rows = -1, cols = -1, declared = -1;
+  while (cur.next(b, e)) {
+    if (skippable(b, e)) continue;
+    char* q = nullptr;
+    const std::string line(b, e);
+    const char* lp = line.c_str();
+    rows = std::strtoll(lp, &q, 10);
+    bool ok = q != lp;
+    lp = q;
+    if (ok) {
+      cols = std::strtoll(lp, &q, 10);
+      ok = q != lp;
+      lp = q;
+    }
+    if (ok) {
+      declared = std::strtoll(lp, &q, 10);
+      ok = q != lp;
+    }
+    if (!ok) parse_fail(path, cur.lineno, "malformed size line (expected: rows cols nnz)");
+    break;
+  }
+  if (rows < 0) throw ParseError(path + ": missing size line");
+  if (rows != cols)
+    throw ParseError(path + ": matrix is not square (" + std::to_string(rows) + "x" +
+                     std::to_string(cols) + ")");
+  if (declared < 0) throw ParseError(path + ": negative entry count");
+
+  std::vector<Triplet> entries;
+  entries.reserve(static_cast<std::size_t>(symmetric ? 2 * declared : declared));
+  std::int64_t seen = 0;
+  while (cur.next(b, e)) {
+    if (skippable(b, e)) continue;
+    if (seen == declared) parse_fail(path, cur.lineno, "more entries than declared in size line");
+    // the line is terminated in place for strto* (restored afterwards)
+    char* le = const_cast<char*>(e);
+    const char saved = *le;
+    *le = '\0';
+    char* q = nullptr;
+    const char* lp = b;
+    const std::int64_t i = std::strtoll(lp, &q, 10);
+    if (q == lp) parse_fail(path, cur.lineno, "malformed entry (row index)");
+    lp = q;
+    const std::int64_t j = std::strtoll(lp, &q, 10);
+    if (q == lp) parse_fail(path, cur.lineno, "malformed entry (column index)");
+    lp = q;
+    double v = 1.0;
+    if (field != Field::pattern) {
+      v = std::strtod(lp, &q);
+      if (q == lp) parse_fail(path, cur.lineno, "malformed entry (value)");
+      lp = q;
+    }
+    while (*lp != '\0' && std::isspace(static_cast<unsigned char>(*lp))) ++lp;
+    const bool trailing = *lp != '\0';
+    *le = saved;
+    if (trailing) parse_fail(path, cur.lineno, "trailing characters after entry");
+    if (i < 1 || i > rows || j < 1 || j > cols)
+      parse_fail(path, cur.lineno, "entry index out of range");
+    if (symmetric && i < j) parse_fail(path, cur.lineno, "upper-triangle entry in symmetric file");
+    if (!std::isfinite(v)) parse_fail(path, cur.lineno, "entry value is not finite");
+    entries.push_back({i - 1, j - 1, v});
+    if (symmetric && i != j) entries.push_back({j - 1, i - 1, v});
+    ++seen;
+  }
+  if (seen != declared)
+    throw ParseError(path + ": file ends after " + std::to_string(seen) + " of " +
+                     std::to_string(declared) + " entries");
+
+  if (!symmetric) {
+    // general file: merge duplicates, require |a_ij - a_ji| <= 1e-12 max|A| and a
+    // symmetric pattern, then replace both by their mean (sparse.cpp:236-287)
+    std::sort(entries.begin(), entries.end(), coord_less);
+    std::size_t out = 0;
+    for (std::size_t i = 0; i < entries.size(); ++i) {
+      if (out > 0 && entries[out - 1].row == entries[i].row &&
+          entries[out - 1].col == entries[i].col)
+        entries[out - 1].value += entries[i].value;
+      else
+        entries[out++] = entries[i];
+    }
+    entries.resize(out);
+    double max_abs = 0.0;
+    for (const Triplet& t : entries) max_abs = std::max(max_abs, std::abs(t.value));
+    const double tol = 1e-12 * max_abs;
+    auto mirror_of = [&](const Triplet& t) -> Triplet* {
+      const Triplet key{t.col, t.row, 0.0};
+      auto it = std::lower_bound(entries.begin(), entries.end(), key, coord_less);
+      return (it != entries.end() && it->row == key.row && it->col == key.col) ? &*it : nullptr;
+    };
+    for (Triplet& t : entries) {
+      if (t.row == t.col) continue;
+      Triplet* m = mirror_of(t);
+      const std::string where =
+          "(" + std::to_string(t.row + 1) + "," + std::to_string(t.col + 1) + ")";
+      if (t.row < t.col) {
+        const double other = m ? m->value : 0.0;
+        if (std::abs(t.value - other) > tol)
+          throw Error(path + ": general matrix is not symmetric at " + where + ": " +
+                      std::to_string(t.value) + " vs " + std::to_string(other));
+        if (!m) throw Error(path + ": general matrix is structurally asymmetric at " + where);
+        const double mean = 0.5 * (t.value + m->value);
+        t.value = mean;
+        m->value = mean;
+      } else if (!m) {
+        throw Error(path + ": general matrix is structurally asymmetric at " + where);
+      }
+    }
+  }
+  return SparseSymMatrix::from_entries(static_cast<std::size_t>(rows), std::move(entries));
+}
+
+void save_matrix_market(const SparseSymMatrix& A, const std::string& path) {
+  std::FILE* fp = std::fopen(path.c_str(), "w");
+  if (!fp) throw Error("cannot open '" + path + "' for writing");
+  const auto& rp = A.row_ptr();
+  const auto& ci = A.col_idx();
+  const auto& va = A.values();
+  std::int64_t lower = 0;
+  for (std::size_t i = 0; i < A.dim(); ++i)
+    for (std::int64_t p = rp[i]; p < rp[i + 1]; ++p) lower += static_cast<std::size_t>(ci[p]) <= i;
+  bool ok = std::fprintf(fp, "%%%%MatrixMarket matrix coordinate real symmetric\n%zu %zu %lld\n",
+                         A.dim(), A.dim(), static_cast<long long>(lower)) > 0;
+  // %.17g round-trips doubles exactly (sparse.cpp:293-315)
+  for (std::size_t i = 0; i < A.dim() && ok; ++i)
+    for (std::int64_t p = rp[i]; p < rp[i + 1]; ++p)
+      if (static_cast<std::size_t>(ci[p]) <= i)
+        ok = std::fprintf(fp, "%zu %d %.17g\n", i + 1, ci[p] + 1, va[p]) > 0 && ok;
+  ok = std::fclose(fp) == 0 && ok;
+  if (!ok) throw Error("write to '" + path + "' failed");
+}
+
+void save_dense_matrix_market(const DenseBlock& X, const std::string& path) {
+  std::FILE* fp = std::fopen(path.c_str(), "w");
+  if (!fp) throw Error("cannot open '" + path + "' for writing");
+  bool ok = std::fprintf(fp, "%%%%MatrixMarket matrix array real general\n%zu %zu\n", X.rows(),
+                         X.cols()) > 0;
+  for (std::size_t j = 0; j < X.cols() && ok; ++j)
+    for (std::size_t i = 0; i < X.rows(); ++i) ok = std::fprintf(fp, "%.17g\n", X(i, j)) > 0 && ok;
+  ok = std::fclose(fp) == 0 && ok;
+  if (!ok) throw Error("write to '" + path + "' failed");
+}
+
+}  // namespace flz
