@@ -1,0 +1,354 @@
+#!/usr/bin/env python
+"""bench.py — filtered-Lanczos time-to-solution + filter-SpMV roofline on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2] [--impl flz|reference]
+
+One "step" = one full filtered-Lanczos solve of the named workload (BASELINE.json configs).
+Prints ONE JSON line (rank 0).  Keys follow the driver contract:
+  value      seconds per solve with the matrix already resident in HBM (CUDA events on the
+             library's stream bracket each solve; host logic in between is included)
+  e2e        seconds per solve through the reference-facing API (flz_solve ==
+             speig::filtered_lanczos) from HOST CSR buffers: host validation, CSR->SELL, H2D,
+             solve, D2H of the eigenvectors, all inside the timed region
+  roofline   the dominant kernel (fused Clenshaw-step SpMM): algorithmic bytes per launch
+             (12*nnz + 4*(n+1) + 32*n*r) / its average device time, measured
+             live with CUDA events around every filter application of the timed solves
+  cpu_baseline  the reference CPU path on this box's host cores (1: the reference is serial),
+             timed on a bounded sample and scaled to the metric's unit
+`--impl reference` runs only the CPU reference arm and prints the same line shape.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "filtered_lanczos_time_to_solution"
+UNIT = "s"
+
+
+# --------------------------------------------------------------------------- workloads
+def workloads():
+    from paper_2409_15053_b200 import matrices as M
+    return {
+        # BASELINE.json configs[0]: the reference's own CPU-runnable case
+        "c1": dict(desc="2D Laplacian 5-point 200x200 (n=40k), [1.00,1.02], degree 50, block 1",
+                   gen=lambda: M.laplacian2d(200), interval=(1.00, 1.02),
+                   cfg=dict(block_size=1, degree=50), expect=80),
+        # configs[1]: the metric's 1-GPU configuration
+        "c2": dict(desc="3D Laplacian 7-point 100^3 (n=1M), [0.10,0.11] (82 eigenpairs), block 3, "
+                        "auto degree (clamps at 1000)",
+                   gen=lambda: M.laplacian3d(100), interval=(0.10, 0.11), cfg=dict(block_size=3),
+                   expect=82),
+        # configs[2]: PARSEC-shaped Ge99H100-like Hamiltonian
+        "c3": dict(desc="synthetic PARSEC-shaped Hamiltonian (Ge99H100-like, n~113k, ~75 nnz/row), "
+                        "degree 50, block 3",
+                   gen=lambda: M.parsec_like(), interval=(-0.65, -0.0096),
+                   cfg=dict(block_size=3, degree=50), expect=None),
+        # configs[3]: Ga41As41H72-shaped
+        "c4": dict(desc="synthetic Ga41As41H72-shaped Hamiltonian (n~268k, ~69 nnz/row), "
+                        "degree 200, block 3",
+                   gen=lambda: M.parsec_like(radius=40.0, h=0.0903, n_atoms=154, ball_radius=3.86,
+                                             seed=2),
+                   interval=(-0.64, 0.0), cfg=dict(block_size=3, degree=200), expect=None),
+        # small smoke-sized case
+        "tiny": dict(desc="2D Laplacian 30x30, [3.0,3.8]", gen=lambda: M.laplacian2d(30),
+                     interval=(3.0, 3.8), cfg=dict(), expect=124),
+    }
+
+
+def step_bytes(n, nnz, r):
+    """Algorithmic bytes of one fused Clenshaw step."""
+    return 12 * nnz + 4 * (n + 1) + 32 * n * r
+
+
+# ------------------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.tmp = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.tmp,
+                stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.tmp.flush()
+        rows = [ln.strip().split(", ") for ln in open(self.tmp.name) if ln.strip()]
+        os.unlink(self.tmp.name)
+        sm, smax, power, reasons = [], [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[0]))
+                smax.append(float(r[1]))
+                power.append(float(r[2]))
+            except (ValueError, IndexError):
+                continue
+            for name, flag in zip(names, r[3:7]):
+                if flag.strip().lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "power_w_max": max(power) if power else None, "samples": len(sm),
+                "reasons": sorted(reasons)}
+
+
+def measured_peak_gbs():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        return float(json.load(open(path))["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ------------------------------------------------------------------------ CPU baseline
+def cpu_reference_sample(csr, interval, cfg, block_steps, degree, budget_s=12.0):
+    """Times the reference CPU implementation (oracle/_ref when present, else the plain-C
+    port) on a bounded sample of the workload and scales it to one full solve.
+
+    Sample: ChebyshevFilter::apply (filter.cpp:122-155) on one n x r block at a reduced
+    degree m_s; scaled by (degree / m_s) * block_steps.  The reference's orthogonalization,
+    convergence checks and recovery are NOT added, so the figure is a lower bound of its
+    time-to-solution."""
+    import oracle
+    orc = oracle.best()
+    n, rp, ci, va = csr
+    r = cfg.get("block_size", 3)
+    A = orc.matrix_from_csr(n, rp, ci, va)
+    lo, hi = -0.1, 1.0  # any bounds: the arithmetic per step does not depend on them
+    X = np.random.default_rng(0).standard_normal((n, r))
+    t0 = time.perf_counter()
+    orc.filter_apply(A, np.ones(3), lo, hi, X)  # 2 steps: estimate the per-step cost
+    per_step = (time.perf_counter() - t0) / 2
+    m_s = int(max(2, min(degree, budget_s / max(per_step, 1e-9))))
+    t0 = time.perf_counter()
+    orc.filter_apply(A, np.ones(m_s + 1), lo, hi, X)
+    elapsed = time.perf_counter() - t0
+    per_step = elapsed / m_s
+    scaled = per_step * degree * block_steps
+    return {"value": scaled, "unit": UNIT, "cores": 1, "kind": orc.kind,
+            "sample": (f"reference ChebyshevFilter::apply on one n x {r} block, {m_s} of {degree} "
+                       f"Clenshaw steps ({elapsed:.1f} s on 1 host core, {per_step * 1e3:.2f} ms/step, "
+                       f"backend {orc.backend()}); scaled x{degree}/{m_s} x {block_steps} block steps; "
+                       "reference orthogonalization/check/recovery time not included (lower bound)"),
+            "host_cores_available": os.cpu_count(), "ms_per_clenshaw_step": per_step * 1e3}
+
+
+# -------------------------------------------------------------------------------- arms
+def run_reference(args, wl):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_2409_15053_b200 import solver as S
+    csr = wl["gen"]()
+    n, rp, ci, va = csr
+    r = wl["cfg"].get("block_size", 3)
+    # block-step count and degree come from the reference's own rules: the degree is a host
+    # scalar computation (build_filter), the block count is what the solve needs; when it
+    # cannot be run on the CPU in bounded time we use the recorded count for this workload.
+    import oracle
+    orc = oracle.best()
+    known_blocks = {"c1": 1730, "c2": None, "c3": None, "c4": None, "tiny": 110}
+    blocks_file = os.path.join(ROOT, "profiles", "block_steps.json")
+    recorded = json.load(open(blocks_file)) if os.path.exists(blocks_file) else {}
+    block_steps = recorded.get(args.workload, {}).get("block_steps") or known_blocks.get(args.workload)
+    degree = recorded.get(args.workload, {}).get("degree") or wl["cfg"].get("degree") or 1000
+    if block_steps is None:
+        block_steps = 100
+    samples = []
+    for _ in range(max(1, args.warmup and 1)):
+        pass
+    base = None
+    for _ in range(max(1, min(args.steps, 2))):
+        base = cpu_reference_sample(csr, wl["interval"], wl["cfg"], block_steps, degree,
+                                    budget_s=10.0)
+        samples.append(base["value"])
+    value = statistics.median(samples)
+    base["value"] = value
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": value * 1e3,
+            "higher_is_better": False, "scaling": "weak" if args.gpus > 1 else "n/a",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.workload}: {wl['desc']}", "n": n, "nnz": int(len(va)),
+                       "block_size": r, "degree": degree, "block_steps": block_steps},
+            "cpu_baseline": base,
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "gpu_launches": 0}
+    print(json.dumps(line))
+
+
+def run_flz(args, wl):
+    from paper_2409_15053_b200 import Context, matrices as M, solver as S
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch with torchrun")
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl")
+        uid = [Context.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        ctx = Context(local_rank, rank, world, uid[0])
+        ctx.adopt_as_default()
+    else:
+        ctx = Context.default()
+
+    csr = wl["gen"]()
+    n, rp, ci, va = csr
+    nnz = int(len(va))
+    a, b = wl["interval"]
+    cfg = S.LanczosConfig(**wl["cfg"])
+    r = cfg.block_size
+
+    def barrier():
+        ctx.sync()
+        if dist is not None:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if dist is None:
+            return x
+        import torch
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- resident arm: matrix uploaded once, W warm-up + K timed solves
+    H = S.SparseSymMatrix.from_csr(n, rp, ci, va, check_symmetry=False)
+    res = None
+    for _ in range(args.warmup):
+        res = S.filtered_lanczos(H, a, b, cfg)
+    sampler = ClockSampler(local_rank) if rank == 0 else None
+    times, mv_s, orth_s, chk_s, rec_s, launches, filter_steps = [], 0.0, 0.0, 0.0, 0.0, 0, 0
+    for _ in range(args.steps):
+        ctx.flush_l2()
+        barrier()
+        ctx.timer_start(0)
+        res = S.filtered_lanczos(H, a, b, cfg)
+        ms = ctx.timer_stop(0)
+        barrier()
+        times.append(max_over_ranks(ms * 1e-3))
+        st = res.stats
+        mv_s += st["time_mv_s"]
+        orth_s += st["time_orth_s"]
+        chk_s += st["time_check_s"]
+        rec_s += st["time_recover_s"]
+        launches += st["gpu_launches"]
+        filter_steps += st["degree"] * st["block_steps"]
+    value = sum(times) / len(times)
+    st = res.stats
+
+    # ---- e2e arm: host CSR -> validated SparseSymMatrix -> solve -> eigenvectors on the host
+    e2e_times = []
+    h2d = 12 * nnz + 8 * (n + 1) + 8 * n * r + 8 * n
+    d2h = 8 * n * len(res.eigenvalues)
+    for i in range(1 + args.steps):
+        ctx.flush_l2()
+        barrier()
+        t0 = time.perf_counter()
+        H2 = S.SparseSymMatrix.from_csr(n, rp, ci, va, check_symmetry=True)
+        r2 = S.filtered_lanczos(H2, a, b, cfg)
+        _ = float(r2.eigenvalues.sum()) if len(r2.eigenvalues) else 0.0
+        ctx.sync()
+        dt = time.perf_counter() - t0
+        del H2
+        if i > 0:  # first pass is the warm-up of this arm
+            e2e_times.append(max_over_ranks(dt))
+    clocks = sampler.stop() if sampler else None
+    e2e = sum(e2e_times) / len(e2e_times)
+
+    if rank != 0:
+        return
+    peak, peak_src = measured_peak_gbs()
+    bstep = step_bytes(n, nnz, r)
+    achieved = bstep * filter_steps / mv_s / 1e9 if mv_s > 0 else 0.0
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "k1_traffic.json")
+    if os.path.exists(prof):
+        traffic = json.load(open(prof)).get(args.workload)
+    ok = True
+    if wl["expect"] is not None:
+        ok = len(res.eigenvalues) == wl["expect"]
+    cpu = cpu_reference_sample(csr, wl["interval"], wl["cfg"], st["block_steps"], st["degree"]) \
+        if world == 1 and not args.no_cpu_baseline else None
+    os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": value * 1e3, "higher_is_better": False,
+        "scaling": "strong" if world > 1 else "n/a", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"{args.workload}: {wl['desc']}", "n": n, "nnz": nnz,
+                   "interval": [a, b], "block_size": r, "degree": st["degree"],
+                   "degree_clamped": bool(st["degree_clamped"]), "block_steps": st["block_steps"],
+                   "basis_vectors": st["basis_vectors"], "eigenpairs": int(len(res.eigenvalues)),
+                   "expected_eigenpairs": wl["expect"], "count_ok": ok,
+                   "converged": bool(st["converged"]), "max_residual": float(res.residuals.max())
+                   if len(res.residuals) else 0.0,
+                   "l2": "per-step inputs exceed the 126 MB L2 where the matrix does; a 256 MB "
+                         "flush is written between timed solves"},
+        "breakdown_s": {"filter_mv": mv_s / args.steps, "orth": orth_s / args.steps,
+                        "host_check": chk_s / args.steps, "recover": rec_s / args.steps,
+                        "preproc": st["time_preproc_s"]},
+        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": int(launches),
+        "roofline": {"kernel": "clenshaw_step_sell (fused Clenshaw-step SpMM, K1)", "bound": "hbm",
+                     "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "peak_source": peak_src, "bytes_per_launch": bstep,
+                     "launches_timed": int(filter_steps),
+                     "avg_launch_us": mv_s / max(filter_steps, 1) * 1e6, "traffic": traffic},
+        "filter_gbs": achieved,
+        "clocks": clocks,
+    }
+    if cpu is not None:
+        line["cpu_baseline"] = cpu
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default=None)
+    ap.add_argument("--impl", default="flz", choices=["flz", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.workload is None:
+        args.workload = "c2"
+    wl = workloads()[args.workload]
+    if args.impl == "reference":
+        run_reference(args, wl)
+    else:
+        run_flz(args, wl)
+
+
+if __name__ == "__main__":
+    main()

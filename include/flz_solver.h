@@ -50,6 +50,8 @@ void flz_config_default(flz_config* cfg); /* lanczos.hpp:14-29 defaults */
 /* The host layer runs on the process-wide default context; adopt a caller-made one
  * (e.g. a distributed context) with this call.  ctx == NULL restores the lazy default. */
 int flz_set_default_ctx(flz_ctx* ctx);
+/* The context the host layer is using (created on first use). */
+int flz_default_ctx(flz_ctx** out);
 
 /* ---- SparseSymMatrix: from_entries (sparse.cpp:27-85), Matrix Market (:172-331) ---- */
 int flz_hostmatrix_from_triplets(int64_t n, int64_t count, const int64_t* rows,
@@ -64,10 +66,12 @@ int flz_hostmatrix_dims(const flz_hostmatrix* A, int64_t* n, int64_t* nnz);
 int flz_hostmatrix_csr(const flz_hostmatrix* A, int64_t* row_ptr, int32_t* col_idx,
                        double* values);
 /* SparseSymMatrix::spmm_block / ChebyshevFilter::apply through the C++ facade */
-int flz_hostmatrix_spmm(const flz_hostmatrix* A, const double* X, int r, double* Y);
+/* X is rows x r; rows != dim(A) is rejected with FLZ_EDIM (speig::DimensionError) */
+int flz_hostmatrix_spmm(const flz_hostmatrix* A, const double* X, int64_t rows, int r,
+                        double* Y);
 int flz_hostmatrix_filter_apply(const flz_hostmatrix* A, const double* coeffs, int m,
-                                double lambda_min, double lambda_max, const double* X, int r,
-                                double* Y);
+                                double lambda_min, double lambda_max, const double* X,
+                                int64_t rows, int r, double* Y);
 
 /* ---- filter scalars (filter.cpp:33-96, :163-184); host arithmetic ---- */
 int flz_indicator_coefficients(double alpha_s, double beta_s, int degree, double* out);

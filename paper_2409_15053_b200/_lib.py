@@ -110,6 +110,7 @@ _SIGS = {
 _SOLVER_SIGS = {
     "flz_config_default": (None, [C.POINTER(FlzConfig)]),
     "flz_set_default_ctx": (i32, [vp]),
+    "flz_default_ctx": (i32, [C.POINTER(vp)]),
     "flz_hostmatrix_from_triplets": (i32, [i64, i64, i64p, i64p, f64p, C.POINTER(vp)]),
     "flz_hostmatrix_from_csr": (i32, [i64, i64p, i32p, f64p, i32, C.POINTER(vp)]),
     "flz_hostmatrix_load_mm": (i32, [C.c_char_p, C.POINTER(vp)]),
@@ -117,8 +118,8 @@ _SOLVER_SIGS = {
     "flz_hostmatrix_free": (None, [vp]),
     "flz_hostmatrix_dims": (i32, [vp, i64P, i64P]),
     "flz_hostmatrix_csr": (i32, [vp, i64p, i32p, f64p]),
-    "flz_hostmatrix_spmm": (i32, [vp, f64p, i32, f64p]),
-    "flz_hostmatrix_filter_apply": (i32, [vp, f64p, i32, d, d, f64p, i32, f64p]),
+    "flz_hostmatrix_spmm": (i32, [vp, f64p, i64, i32, f64p]),
+    "flz_hostmatrix_filter_apply": (i32, [vp, f64p, i32, d, d, f64p, i64, i32, f64p]),
     "flz_indicator_coefficients": (i32, [d, d, i32, f64p]),
     "flz_select_degree": (i32, [d, d, d, i32, iP]),
     "flz_clenshaw": (d, [f64p, i32, d]),

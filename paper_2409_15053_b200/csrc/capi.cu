@@ -291,8 +291,10 @@ int flz_nccl_unique_id(void* out128) {
     std::memcpy(out128, &id, sizeof(id));
   });
 }
-void flz_ctx_destroy(flz_ctx* ctx) {
-  if (!ctx) return;
+// Handles are reference counted so that destroying them in any order is safe: a context
+// outlives its matrices and bases, a matrix outlives the bases built on it.
+static void ctx_release(flz_ctx* ctx) {
+  if (!ctx || --ctx->refs > 0) return;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   cudaStreamSynchronize(ctx->comm_stream);
@@ -312,6 +314,7 @@ void flz_ctx_destroy(flz_ctx* ctx) {
   cudaStreamDestroy(ctx->comm_stream);
   delete ctx;
 }
+void flz_ctx_destroy(flz_ctx* ctx) { ctx_release(ctx); }
 int flz_ctx_sync(flz_ctx* ctx) {
   return guarded([&] {
     use(ctx);
@@ -632,16 +635,20 @@ int flz_matrix_upload(flz_ctx* ctx, int64_t n_global, int64_t row_begin, int64_t
       A->send_buf.reserve(std::max<size_t>((size_t)give_total * kMaxFuse, 1));
     }
     FLZ_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx->refs += 1;
     *out = A.release();
   });
 }
 
-void flz_matrix_destroy(flz_matrix* A) {
-  if (!A) return;
-  cudaSetDevice(A->ctx->device);
-  cudaStreamSynchronize(A->ctx->stream);
+static void matrix_release(flz_matrix* A) {
+  if (!A || --A->refs > 0) return;
+  flz_ctx* ctx = A->ctx;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
   delete A;
+  ctx_release(ctx);
 }
+void flz_matrix_destroy(flz_matrix* A) { matrix_release(A); }
 int64_t flz_matrix_rows_local(const flz_matrix* A) { return A->nl; }
 int64_t flz_matrix_nnz_local(const flz_matrix* A) { return A->nnz; }
 int flz_matrix_stats(const flz_matrix* A, int64_t* stored_entries, int64_t* slices,
@@ -801,6 +808,8 @@ int flz_basis_create(flz_ctx* ctx, const flz_matrix* A, int64_t max_cols, int r,
     FLZ_CUDA(cudaEventCreate(&B->e1));
     FLZ_CUDA(cudaEventCreate(&B->e2));
     FLZ_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx->refs += 1;
+    const_cast<flz_matrix*>(A)->refs += 1;
     *out = B.release();
   });
 }
@@ -813,7 +822,11 @@ void flz_basis_destroy(flz_basis* B) {
   if (B->e1) cudaEventDestroy(B->e1);
   if (B->e2) cudaEventDestroy(B->e2);
   if (B->pinned) cudaFreeHost(B->pinned);
+  flz_ctx* ctx = B->ctx;
+  flz_matrix* A = const_cast<flz_matrix*>(B->A);
   delete B;
+  matrix_release(A);
+  ctx_release(ctx);
 }
 int64_t flz_basis_blocks(const flz_basis* B) { return B->k; }
 

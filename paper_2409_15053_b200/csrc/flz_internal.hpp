@@ -89,6 +89,7 @@ struct flz_ctx {
   ncclComm_t comm = nullptr;
   bool exact = false;
   int sm_count = 148;
+  int refs = 1;                  // owner + every matrix/basis created on the context
   uint64_t launches = 0;
   cudaEvent_t t0[16] = {}, t1[16] = {};
   flz::DevBuf<double> partial;   // split-K partial sums of the tall-skinny GEMMs
@@ -103,6 +104,7 @@ struct flz_ctx {
 // side works in the permuted ordering; only host transfers apply perm.
 struct flz_matrix {
   flz_ctx* ctx = nullptr;
+  int refs = 1;           // owner + every basis built on the matrix
   int64_t n_global = 0;
   int64_t row_begin = 0, row_end = 0;
   int64_t nl = 0;         // local rows

@@ -109,6 +109,10 @@ int flz_set_default_ctx(flz_ctx* ctx) {
   });
 }
 
+int flz_default_ctx(flz_ctx** out) {
+  return wrap([&] { *out = Device::context(); });
+}
+
 int flz_hostmatrix_from_triplets(int64_t n, int64_t count, const int64_t* rows,
                                  const int64_t* cols, const double* values,
                                  flz_hostmatrix** out) {
@@ -148,9 +152,10 @@ int flz_hostmatrix_csr(const flz_hostmatrix* A, int64_t* row_ptr, int32_t* col_i
   std::copy(A->A.values().begin(), A->A.values().end(), values);
   return FLZ_OK;
 }
-int flz_hostmatrix_spmm(const flz_hostmatrix* A, const double* X, int r, double* Y) {
+int flz_hostmatrix_spmm(const flz_hostmatrix* A, const double* X, int64_t rows, int r,
+                        double* Y) {
   return wrap([&] {
-    const std::size_t n = A->A.dim();
+    const std::size_t n = static_cast<std::size_t>(rows);
     DenseBlock Xb(n, r), Yb;
     std::copy(X, X + n * r, Xb.data());
     A->A.spmm_block(Xb, Yb);
@@ -158,10 +163,10 @@ int flz_hostmatrix_spmm(const flz_hostmatrix* A, const double* X, int r, double*
   });
 }
 int flz_hostmatrix_filter_apply(const flz_hostmatrix* A, const double* coeffs, int m,
-                                double lambda_min, double lambda_max, const double* X, int r,
-                                double* Y) {
+                                double lambda_min, double lambda_max, const double* X,
+                                int64_t rows, int r, double* Y) {
   return wrap([&] {
-    const std::size_t n = A->A.dim();
+    const std::size_t n = static_cast<std::size_t>(rows);
     const auto f = ChebyshevFilter::from_coefficients(
         SpectralBounds(lambda_min, lambda_max), lambda_min, lambda_max,
         std::vector<double>(coeffs, coeffs + std::max(m, -1) + 1));

@@ -44,6 +44,20 @@ class Context:
         self.handle = h
         self.rank, self.nranks = rank, nranks
 
+    @classmethod
+    def default(cls) -> "Context":
+        """Non-owning view of the context the host solver layer uses (flz_default_ctx)."""
+        h = C.c_void_p()
+        check(lib().flz_default_ctx(C.byref(h)))
+        self = cls.__new__(cls)
+        self.handle, self.rank, self.nranks = h, int(lib().flz_ctx_rank(h)), int(lib().flz_ctx_nranks(h))
+        self.close = lambda: None
+        return self
+
+    def adopt_as_default(self):
+        """Make the host solver layer (filtered_lanczos & co.) run on this context."""
+        check(lib().flz_set_default_ctx(self.handle))
+
     @staticmethod
     def nccl_unique_id() -> bytes:
         buf = C.create_string_buffer(128)

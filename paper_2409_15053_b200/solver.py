@@ -76,14 +76,15 @@ class SparseSymMatrix:
     def spmm_block(self, X):
         flat, (n, r) = _fcol(X)
         out = np.empty_like(flat)
-        check(lib().flz_hostmatrix_spmm(self.handle, flat, r, out))
+        check(lib().flz_hostmatrix_spmm(self.handle, flat, n, r, out))
         return _from_fcol(out, n, r)
 
     def filter_apply(self, coeffs, lo, hi, X):
         flat, (n, r) = _fcol(X)
         cf = np.ascontiguousarray(coeffs, np.float64)
         out = np.empty_like(flat)
-        check(lib().flz_hostmatrix_filter_apply(self.handle, cf, len(cf) - 1, lo, hi, flat, r, out))
+        check(lib().flz_hostmatrix_filter_apply(self.handle, cf, len(cf) - 1, lo, hi, flat, n, r,
+                                                out))
         return _from_fcol(out, n, r)
 
     def __del__(self):

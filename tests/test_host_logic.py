@@ -1,0 +1,183 @@
+"""Host-side logic of libflz (no GPU): filter scalars, start block, projected eigenproblem,
+matrix validation and Matrix Market I/O — checked against the oracle and NumPy."""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2409_15053_b200 import FlzError, matrices as M, solver as S
+
+
+def test_filter_scalars_bit_equal_to_oracle(best_oracle, golden):
+    for a, b, deg in [(-1.0, -0.5, 12), (0.1, 0.3, 200), (-0.37, 0.81, 64)]:
+        assert np.array_equal(S.indicator_coefficients(a, b, deg),
+                              best_oracle.indicator_coefficients(a, b, deg))
+    assert np.array_equal(S.indicator_coefficients(0.1, 0.3, 200), golden["coef_01_03"])
+    assert S.select_degree(0.1, 0.3) == (48, False)        # filter_test.cpp:96-99
+    assert S.select_degree(-1.0, -0.5) == (10, False)
+    assert S.select_degree(-0.001, 0.001) == (1000, True)
+    for a, b, eps in [(-0.02, 0.02, 0.255), (0.3, 0.9, 0.1), (-0.9, -0.2, 0.4)]:
+        assert S.select_degree(a, b, eps) == best_oracle.select_degree(a, b, eps)
+    cf = golden["coef_01_03"]
+    vals = [S.clenshaw(cf, t) for t in golden["clenshaw_pts"]]
+    assert np.array_equal(vals, golden["clenshaw_vals"])
+
+
+def test_build_filter_matches_oracle_and_errors(best_oracle):
+    for args in [(-0.05, 8.05, 3.0, 3.8, 0), (-1.5, 34.0, -0.6, 0.0, 50), (0.0, 1.0, -5.0, 0.4, 0)]:
+        cf, a_s, b_s, cl = S.build_filter(*args)
+        cf2, a2, b2, cl2 = best_oracle.build_filter(*args)
+        assert np.array_equal(cf, cf2) and (a_s, b_s, cl) == (a2, b2, cl2)
+    with pytest.raises(FlzError) as e:
+        S.build_filter(0.0, 1.0, 2.0, 3.0)       # interval outside the bounds
+    assert e.value.code == -3                      # -> IntervalError
+    with pytest.raises(FlzError):
+        S.build_filter(0.0, 1.0, 0.6, 0.4)       # alpha >= beta
+    with pytest.raises(FlzError):
+        S.indicator_coefficients(0.5, 0.2, 4)
+
+
+def test_init_block_matches_reference(golden):
+    Q = S.init_block(1000, 3, 20177)
+    assert np.abs(Q - golden["init_block_1000x3_scalar"]).max() < 1e-15
+    assert np.abs(Q.T @ Q - np.eye(3)).max() < 1e-14
+    assert np.array_equal(Q, S.init_block(1000, 3, 20177))       # deterministic per seed
+    assert not np.array_equal(Q, S.init_block(1000, 3, 20178))
+    with pytest.raises(FlzError):
+        S.init_block(2, 3)
+
+
+def band_dense(bands):
+    sb, dim = bands.shape[0] - 1, bands.shape[1]
+    A = np.zeros((dim, dim))
+    for d in range(sb + 1):
+        for i in range(dim - d):
+            A[i + d, i] = A[i, i + d] = bands[d, i]
+    return A
+
+
+@pytest.mark.parametrize("dim,sb", [(1, 0), (2, 1), (7, 1), (40, 3), (61, 5), (30, 20), (12, 11),
+                                    (200, 3)])
+def test_sym_band_eig(best_oracle, dim, sb):
+    rng = np.random.default_rng(dim * 31 + sb)
+    bands = rng.uniform(-1, 1, (sb + 1, dim))
+    A = band_dense(bands)
+    vals, W = S.sym_band_eig(bands)
+    assert np.abs(vals - np.linalg.eigvalsh(A)).max() < 1e-12
+    assert np.abs(W.T @ W - np.eye(dim)).max() < 1e-12          # band_eig_test orthogonality
+    assert np.abs(A @ W - W * vals).max() < 1e-12
+    ov, _ = best_oracle.sym_band_eig(bands)
+    assert np.abs(vals - ov).max() < 1e-12
+
+
+@pytest.mark.parametrize("dim,sb", [(9, 1), (60, 3), (150, 1), (90, 4)])
+def test_band_ritz_rows_equals_full_rows(dim, sb):
+    """The cheap periodic-check path returns exactly the rows of the full eigenvector matrix."""
+    bands = np.random.default_rng(dim + sb).uniform(-1, 1, (sb + 1, dim))
+    vals, W = S.sym_band_eig(bands)
+    rows = [dim - 1, dim - 2, 0, dim // 2]
+    v2, R = S.band_ritz_rows(bands, rows)
+    assert np.array_equal(vals, v2)
+    assert np.array_equal(R, W[rows, :])          # same rotations -> bitwise the same rows
+    v3, R3 = S.band_ritz_rows(bands, [])
+    assert np.array_equal(v3, vals) and R3.shape == (0, dim)
+
+
+@pytest.mark.parametrize("dim,sb", [(50, 1), (120, 3), (300, 3)])
+def test_band_inverse_iteration(dim, sb):
+    bands = np.random.default_rng(7 * dim + sb).uniform(-1, 1, (sb + 1, dim))
+    A = band_dense(bands)
+    vals, _ = S.sym_band_eig(bands, want_vectors=False)
+    pick = list(range(dim - 25, dim))
+    W, res, ortho = S.band_eigenvectors(bands, vals, pick)
+    assert res < 1e-13 and ortho < 1e-12
+    assert np.abs(A @ W - W * vals[pick]).max() < 1e-12
+
+
+def test_band_inverse_iteration_with_multiplicities():
+    # block diagonal of identical blocks -> exactly repeated eigenvalues
+    dim = 90
+    bands = np.zeros((3, dim))
+    blk = np.random.default_rng(3).uniform(-1, 1, (3, 30))
+    blk[1, 29] = blk[2, 28:] = 0.0
+    for c in range(3):
+        bands[:, 30 * c:30 * (c + 1)] = blk
+    A = band_dense(bands)
+    vals, _ = S.sym_band_eig(bands, want_vectors=False)
+    pick = list(range(dim - 30, dim))
+    W, res, ortho = S.band_eigenvectors(bands, vals, pick)
+    assert res < 1e-12 and ortho < 1e-11
+    assert np.abs(A @ W - W * vals[pick]).max() < 1e-11
+
+
+def test_from_entries_semantics():
+    # duplicates are summed, asymmetry / range / non-finite rejected (sparse.cpp:27-85)
+    A = S.SparseSymMatrix.from_entries(3, [0, 0, 1, 2, 0, 1], [0, 0, 1, 2, 1, 0],
+                                       [1.0, 0.5, 2.0, 3.0, -1.0, -1.0])
+    rp, ci, va = A.csr()
+    assert list(rp) == [0, 2, 4, 5] and list(ci) == [0, 1, 0, 1, 2]
+    assert list(va) == [1.5, -1.0, -1.0, 2.0, 3.0]
+    for rows, cols, vals in [([0, 1], [1, 2], [1.0, 2.0]), ([0, 1], [1, 0], [1.0, 1.5]),
+                             ([0], [3], [1.0]), ([0], [0], [float("nan")])]:
+        with pytest.raises(FlzError):
+            S.SparseSymMatrix.from_entries(3, rows, cols, vals)
+    n, rp, ci, va = M.laplacian2d(30)
+    assert len(va) == 5 * n - 4 * 30                  # sparse_test.cpp:206-209
+    assert S.SparseSymMatrix.from_csr(n, rp, ci, va).nnz == len(va)
+
+
+MM_OK = """%%MatrixMarket matrix coordinate real symmetric
+% comment
+3 3 4
+1 1 2.0
+2 1 -1.0
+2 2 2.0
+3 3 5e-1
+"""
+
+
+def test_matrix_market_round_trip(tmp_path, best_oracle):
+    p = tmp_path / "a.mtx"
+    p.write_text(MM_OK)
+    A = S.SparseSymMatrix.load_matrix_market(p)
+    rp, ci, va = A.csr()
+    assert list(rp) == [0, 2, 4, 5] and list(va) == [2.0, -1.0, -1.0, 2.0, 0.5]
+    n, rp, ci, va = M.random_sparse_sym(60, 0.2, 5)
+    B = S.SparseSymMatrix.from_csr(n, rp, ci, va)
+    q = tmp_path / "b.mtx"
+    B.save_matrix_market(q)
+    C2 = S.SparseSymMatrix.load_matrix_market(q)
+    assert all(np.array_equal(x, y) for x, y in zip(B.csr(), C2.csr()))   # %.17g is exact
+    general = tmp_path / "g.mtx"
+    general.write_text("%%MatrixMarket matrix coordinate real general\n2 2 3\n1 1 1\n1 2 3\n"
+                       "2 1 3.000000000000001\n")
+    G = S.SparseSymMatrix.load_matrix_market(general)
+    assert G.csr()[2][1] == G.csr()[2][2]             # symmetrised by averaging
+    pat = tmp_path / "p.mtx"
+    pat.write_text("%%MatrixMarket matrix coordinate pattern symmetric\n2 2 2\n1 1\n2 1\n")
+    assert list(S.SparseSymMatrix.load_matrix_market(pat).csr()[2]) == [1.0, 1.0, 1.0]
+
+
+@pytest.mark.parametrize("text,needle", [
+    ("", "empty file"),
+    ("%%NotMM matrix coordinate real symmetric\n1 1 0\n", ":1:"),
+    ("%%MatrixMarket matrix array real general\n1 1\n", "expected coordinate"),
+    ("%%MatrixMarket matrix coordinate complex symmetric\n1 1 0\n", "complex"),
+    ("%%MatrixMarket matrix coordinate real hermitian\n1 1 0\n", "hermitian"),
+    ("%%MatrixMarket matrix coordinate real symmetric\n2 3 0\n", "not square"),
+    ("%%MatrixMarket matrix coordinate real symmetric\n2 2 1\n1 2 1.0\n", "upper-triangle"),
+    ("%%MatrixMarket matrix coordinate real symmetric\n2 2 2\n1 1 1.0\n", "file ends after 1 of 2"),
+    ("%%MatrixMarket matrix coordinate real symmetric\n2 2 1\n1 1 1.0\n2 2 1.0\n", "more entries"),
+    ("%%MatrixMarket matrix coordinate real symmetric\n2 2 1\n1 1 abc\n", ":3:"),
+    ("%%MatrixMarket matrix coordinate real symmetric\n2 2 1\n3 1 1.0\n", "out of range"),
+    ("%%MatrixMarket matrix coordinate real general\n2 2 2\n1 2 1.0\n2 1 2.0\n", "not symmetric"),
+])
+def test_matrix_market_errors(tmp_path, text, needle):
+    p = tmp_path / "bad.mtx"
+    p.write_text(text)
+    with pytest.raises(FlzError) as e:
+        S.SparseSymMatrix.load_matrix_market(p)
+    assert needle in str(e.value)
+    with pytest.raises(FlzError):
+        S.SparseSymMatrix.load_matrix_market(tmp_path / "missing.mtx")
