@@ -12,7 +12,7 @@ import subprocess
 import numpy as np
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG_DIR, "libflz.so")
+LIB_PATH = os.environ.get("FLZ_LIB", os.path.join(PKG_DIR, "libflz.so"))  # FLZ_LIB: kernel-variant A/B runs
 CSRC = os.path.join(PKG_DIR, "csrc")
 
 FLZ_OK = 0

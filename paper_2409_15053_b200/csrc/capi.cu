@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <numeric>
@@ -58,12 +59,40 @@ void allreduce(flz_ctx* ctx, double* buf, size_t count) {
 }
 
 SellView view_all(const flz_matrix* A) {
-  return SellView{A->slice_ptr.p, A->slice_len.p, A->row_len.p, A->col.p,
-                  A->val.p,       nullptr,        A->nslices,   A->nl};
+  return SellView{A->tasks_all.p, A->nt_all, A->short_rows, A->slice_ptr.p, A->slice_len.p, A->row_len.p,
+                  A->col.p,       A->val.p,  nullptr,        A->nslices,     A->nl};
 }
-SellView view_list(const flz_matrix* A, const int32_t* ids, int64_t count) {
-  return SellView{A->slice_ptr.p, A->slice_len.p, A->row_len.p, A->col.p,
-                  A->val.p,       ids,            count,        A->nl};
+SellView view_interior(const flz_matrix* A) {
+  return SellView{A->tasks_interior.p, A->nt_interior, A->short_rows, A->slice_ptr.p, A->slice_len.p,
+                  A->row_len.p,        A->col.p,       A->val.p,       A->interior.p,
+                  A->n_interior,       A->nl};
+}
+SellView view_boundary(const flz_matrix* A) {
+  return SellView{A->tasks_boundary.p, A->nt_boundary, A->short_rows, A->slice_ptr.p, A->slice_len.p,
+                  A->row_len.p,        A->col.p,       A->val.p,       A->boundary.p,
+                  A->n_boundary,       A->nl};
+}
+
+// Groups slices (in list order) into CTA tasks: long slices get several warps each.
+std::vector<SliceTask> build_tasks(const std::vector<int32_t>& ids,
+                                   const std::vector<int32_t>& slice_len) {
+  #ifndef FLZ_K1_T
+#define FLZ_K1_T 24   // target entries per warp before a slice is split further
+#endif
+  auto warps_for = [](int32_t len) {
+    return len <= FLZ_K1_T ? 1 : (len <= 2 * FLZ_K1_T ? 2 : (len <= 4 * FLZ_K1_T ? 4 : 8));
+  };
+  std::vector<SliceTask> tasks;
+  size_t i = 0;
+  while (i < ids.size()) {
+    SliceTask t{};
+    t.warps_per_slice = warps_for(slice_len[ids[i]]);
+    const int cap = kTaskWarps / t.warps_per_slice;
+    while (i < ids.size() && t.count < cap && warps_for(slice_len[ids[i]]) == t.warps_per_slice)
+      t.slice[t.count++] = ids[i++];
+    tasks.push_back(t);
+  }
+  return tasks;
 }
 
 void ensure_workspaces(const flz_matrix* A) {
@@ -78,9 +107,10 @@ void ensure_workspaces(const flz_matrix* A) {
 // Halo exchange of the gather source Y1 (interleaved, R doubles per row): pack the rows
 // the peers reference, send/recv on the comm stream, leave ev_halo_done for the boundary
 // launch.  The caller launches the interior slices in between.
-void halo_begin(const flz_matrix* A, int R, double* Y1) {
+void halo_begin(const flz_matrix* A, int S, double* Y1) {
   flz_ctx* ctx = A->ctx;
-  launch_pack_rows(ctx, ctx->stream, A->n_send, R, A->send_rows.p, Y1, A->send_buf.p);
+  const int R = S;  // whole (padded) rows travel
+  launch_pack_rows(ctx, ctx->stream, A->n_send, S, A->send_rows.p, Y1, A->send_buf.p);
   FLZ_CUDA(cudaEventRecord(ctx->ev_halo_ready, ctx->stream));
   FLZ_CUDA(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_halo_ready, 0));
   FLZ_NCCL(ncclGroupStart());
@@ -98,20 +128,28 @@ void halo_begin(const flz_matrix* A, int R, double* Y1) {
 
 // One fused step over the whole local matrix, with the halo exchange overlapped with the
 // interior slices when the context is distributed.
-void sell_step(const flz_matrix* A, int R, StepMode mode, double s1, double s2, double b,
+void sell_step(const flz_matrix* A, int R, int S, StepMode mode, double s1, double s2, double b,
                double* Y1, double* Y2, const double* X, int64_t ldx, double* Out, int64_t ldo) {
   flz_ctx* ctx = A->ctx;
   if (ctx->nranks == 1 || A->peers.empty()) {
-    launch_clenshaw_step(ctx, view_all(A), R, mode, ctx->exact, s1, s2, b, Y1, Y2, X, ldx, Out,
-                         ldo);
+    launch_clenshaw_step(ctx, view_all(A), R, S, mode, ctx->exact, s1, s2, b, Y1, Y2, X, ldx,
+                         Out, ldo);
     return;
   }
-  halo_begin(A, R, Y1);
-  launch_clenshaw_step(ctx, view_list(A, A->interior.p, A->n_interior), R, mode, ctx->exact, s1,
-                       s2, b, Y1, Y2, X, ldx, Out, ldo);
+  halo_begin(A, S, Y1);
+  launch_clenshaw_step(ctx, view_interior(A), R, S, mode, ctx->exact, s1, s2, b, Y1, Y2, X, ldx,
+                       Out, ldo);
   FLZ_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_halo_done, 0));
-  launch_clenshaw_step(ctx, view_list(A, A->boundary.p, A->n_boundary), R, mode, ctx->exact, s1,
-                       s2, b, Y1, Y2, X, ldx, Out, ldo);
+  launch_clenshaw_step(ctx, view_boundary(A), R, S, mode, ctx->exact, s1, s2, b, Y1, Y2, X, ldx,
+                       Out, ldo);
+}
+
+// Row stride of the interleaved workspaces for R fused columns: 3 columns are padded to 4
+// (one aligned 32-byte sector per gathered row) when the matrix is gather dominated
+// (>= 16 entries per row); the exact-mode kernel always uses S == R.
+int row_stride(const flz_matrix* A, int R) {
+  if (R != 3 || A->ctx->exact || A->nl == 0) return R;
+  return (A->nnz >= 16 * A->nl) ? 4 : 3;
 }
 
 // Z[:, 0..ncols) = A X[:, 0..ncols), device-resident column-major blocks (permuted rows).
@@ -121,8 +159,9 @@ void spmm_device(const flz_matrix* A, const double* X, int64_t ldx, int ncols, d
   ensure_workspaces(A);
   for (int c0 = 0; c0 < ncols; c0 += kMaxFuse) {
     const int R = std::min(kMaxFuse, ncols - c0);
-    launch_interleave(ctx, A->nl, R, 1.0, X + (int64_t)c0 * ldx, ldx, A->y1.p);
-    sell_step(A, R, StepMode::plain, 1.0, 0.0, 0.0, A->y1.p, A->y2.p, nullptr, 0,
+    const int S = row_stride(A, R);
+    launch_interleave(ctx, A->nl, R, S, 1.0, X + (int64_t)c0 * ldx, ldx, A->y1.p);
+    sell_step(A, R, S, StepMode::plain, 1.0, 0.0, 0.0, A->y1.p, A->y2.p, nullptr, 0,
               Z + (int64_t)c0 * ldz, ldz);
   }
   if (counted) g_matvecs.fetch_add((uint64_t)ncols, std::memory_order_relaxed);
@@ -138,23 +177,24 @@ void filter_device(const flz_matrix* A, const double* coeffs, int m, double c, d
   const double f1 = inv_e, f2 = -c * inv_e;                      // filter.cpp:153
   for (int c0 = 0; c0 < ncols; c0 += kMaxFuse) {
     const int R = std::min(kMaxFuse, ncols - c0);
+    const int S = row_stride(A, R);
     const double* Xc = X + (int64_t)c0 * ldx;
     double* Zc = Z + (int64_t)c0 * ldz;
     if (m == 0) {  // Y = b_0 X, no products (filter.cpp:133-136)
       for (int k = 0; k < R; ++k)
-        launch_interleave(ctx, A->nl, 1, coeffs[0], Xc + (int64_t)k * ldx, ldx,
+        launch_interleave(ctx, A->nl, 1, 1, coeffs[0], Xc + (int64_t)k * ldx, ldx,
                           Zc + (int64_t)k * ldz);
       continue;
     }
     double* Y1 = A->y1.p;
     double* Y2 = A->y2.p;
-    launch_interleave(ctx, A->nl, R, coeffs[m], Xc, ldx, Y1);                  // :144
-    FLZ_CUDA(cudaMemsetAsync(Y2, 0, (size_t)A->nl * R * sizeof(double), ctx->stream));
+    launch_interleave(ctx, A->nl, R, S, coeffs[m], Xc, ldx, Y1);               // :144
+    FLZ_CUDA(cudaMemsetAsync(Y2, 0, (size_t)A->nl * S * sizeof(double), ctx->stream));
     for (int j = m - 1; j >= 1; --j) {                                          // :146-151
-      sell_step(A, R, StepMode::step, s1, s2, coeffs[j], Y1, Y2, Xc, ldx, nullptr, 0);
+      sell_step(A, R, S, StepMode::step, s1, s2, coeffs[j], Y1, Y2, Xc, ldx, nullptr, 0);
       std::swap(Y1, Y2);
     }
-    sell_step(A, R, StepMode::final, f1, f2, coeffs[0], Y1, Y2, Xc, ldx, Zc, ldz);  // :152-154
+    sell_step(A, R, S, StepMode::final, f1, f2, coeffs[0], Y1, Y2, Xc, ldx, Zc, ldz);  // :152-154
     g_matvecs.fetch_add((uint64_t)R * (uint64_t)m, std::memory_order_relaxed);
   }
 }
@@ -544,6 +584,20 @@ int flz_matrix_upload(flz_ctx* ctx, int64_t n_global, int64_t row_begin, int64_t
     up(A->iperm, iperm);
     up(A->interior, interior);
     up(A->boundary, boundary);
+    {
+      std::vector<int32_t> all(nslices);
+      std::iota(all.begin(), all.end(), 0);
+      const auto ta = build_tasks(all, slice_len), ti = build_tasks(interior, slice_len),
+                 tb = build_tasks(boundary, slice_len);
+      A->short_rows = std::all_of(ta.begin(), ta.end(),
+                                  [](const SliceTask& t) { return t.warps_per_slice == 1; });
+      A->nt_all = (int64_t)ta.size();
+      A->nt_interior = (int64_t)ti.size();
+      A->nt_boundary = (int64_t)tb.size();
+      up(A->tasks_all, ta);
+      up(A->tasks_interior, ti);
+      up(A->tasks_boundary, tb);
+    }
     A->h_perm = perm;
     A->h_iperm = iperm;
 

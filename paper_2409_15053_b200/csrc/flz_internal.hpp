@@ -76,6 +76,15 @@ constexpr int kSliceRows = 32;   // SELL-C: C = one warp of rows per slice
 constexpr int kMaxFuse = 4;      // block columns fused per Clenshaw-step launch
 constexpr int kLdAlign = 32;     // leading dimensions are multiples of 32 doubles (256 B)
 
+// Work item of the multi-warp Clenshaw-step kernel: one CTA of kTaskWarps warps processes
+// `count` slices with `warps_per_slice` warps each (count * warps_per_slice <= kTaskWarps).
+constexpr int kTaskWarps = 8;
+struct SliceTask {
+  int32_t warps_per_slice;
+  int32_t count;
+  int32_t slice[kTaskWarps];
+};
+
 }  // namespace flz
 
 // ---------------------------------------------------------------- context
@@ -125,6 +134,9 @@ struct flz_matrix {
   flz::DevBuf<int32_t> interior;    // slice ids without halo references
   flz::DevBuf<int32_t> boundary;    // slice ids with halo references
   int64_t n_interior = 0, n_boundary = 0;
+  flz::DevBuf<flz::SliceTask> tasks_all, tasks_interior, tasks_boundary;
+  int64_t nt_all = 0, nt_interior = 0, nt_boundary = 0;
+  bool short_rows = false;          // max slice length <= 24: single-warp tasks only
   std::vector<int32_t> h_perm, h_iperm;
   // halo exchange plan (distributed only)
   struct Peer {
@@ -171,6 +183,9 @@ namespace flz {
 // --------------------------------------------------------- kernel launchers
 // (kernels_sell.cu)
 struct SellView {
+  const SliceTask* tasks;    // task list of the fast kernel (nullptr: one warp per slice)
+  int64_t ntasks;
+  bool short_rows;           // every slice fits one warp: the one-warp-per-slice kernel is best
   const int64_t* slice_ptr;
   const int32_t* slice_len;
   const int32_t* row_len;
@@ -183,18 +198,19 @@ struct SellView {
 
 enum class StepMode { step, final, plain };
 
-// One fused Clenshaw step (or plain SpMM) for R in [1, kMaxFuse] interleaved columns:
+// One fused Clenshaw step (or plain SpMM) for R in [1, kMaxFuse] interleaved columns with
+// row stride S (S == R, or S == 4 for R == 3 on long-row matrices):
 //   step : Y2[i,:] = s1*(A Y1)[i,:] + s2*Y1[i,:] - Y2[i,:] + b*X[i,:]   (interleaved out)
 //   final: Out[:,k] column-major (ld = ldo) receives the same expression
 //   plain: Out[:,k] = (A Y1)[i,k]
-void launch_clenshaw_step(flz_ctx* ctx, const SellView& A, int R, StepMode mode, bool exact,
+void launch_clenshaw_step(flz_ctx* ctx, const SellView& A, int R, int S, StepMode mode, bool exact,
                           double s1, double s2, double b, const double* Y1, double* Y2,
                           const double* X, int64_t ldx, double* Out, int64_t ldo);
-// Y1[i*R+k] = scale * X[k*ldx+i]  (column-major -> interleaved); scale==1 is a pure copy
-void launch_interleave(flz_ctx* ctx, int64_t nl, int R, double scale, const double* X,
+// Y1[i*S+k] = scale * X[k*ldx+i]  (column-major -> interleaved with row stride S >= R)
+void launch_interleave(flz_ctx* ctx, int64_t nl, int R, int S, double scale, const double* X,
                        int64_t ldx, double* Y1);
-// halo packing: buf[s*R+k] = Y1[rows[s]*R+k]
-void launch_pack_rows(flz_ctx* ctx, cudaStream_t stream, int64_t count, int R,
+// halo packing: buf[s*S+k] = Y1[rows[s]*S+k]
+void launch_pack_rows(flz_ctx* ctx, cudaStream_t stream, int64_t count, int S,
                       const int32_t* rows, const double* Y1, double* buf);
 // out[i] = s1*w[i] + s2*y1[i] - y2[i] + b*x[i]
 void launch_combine(flz_ctx* ctx, int64_t n, bool exact, double s1, double s2, double b,

@@ -33,9 +33,10 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 }
 
 // ---------------------------------------------------------------- gemm_tn
-// grid (ceil(M/64), nchunks, ceil(N/(8*NT))), 256 threads = 8 warps; warp w owns the 8
-// A-columns m0 = blockIdx.x*64 + 8w .. +8 and the 8*NT B-columns n0 = blockIdx.z*8*NT ..;
-// it streams `rows_per_chunk` rows (multiple of 8) and writes its 8 x 8NT partial tile.
+// Work item = (8-column tile of A, k-chunk): one warp each, 8 warps per CTA, items ordered so
+// that the warps of a CTA share the k-chunk (the B rows they read are the same -> L1).  The
+// k-chunking adapts to M: a 3-column projection (first Lanczos steps, intra-block QR) is split
+// into hundreds of chunks, a 3000-column one into a few, always ~32 warps per SM.
 // Lane (g = lane>>2, t = lane&3) loads the double2 at rows k+2t, k+2t+1 of column g: the
 // .x halves of a warp form one 8x4 k-slab, the .y halves the next (the k order inside an
 // MMA is free as long as A and B agree), so every load is a full 16 B per lane.
@@ -43,13 +44,16 @@ template <int NT>
 __global__ void __launch_bounds__(256)
     gemm_tn_kernel(const double* __restrict__ A, int64_t lda, int64_t M,
                    const double* __restrict__ B, int64_t ldb, int N, int64_t rows8,
-                   int64_t rows_per_chunk, double* __restrict__ part, int64_t Mpad, int Npad) {
+                   int64_t rows_per_chunk, int64_t mtiles, int64_t nitems,
+                   double* __restrict__ part, int64_t Mpad, int Npad) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
-  const int64_t m0 = (int64_t)blockIdx.x * 64 + warp * 8;
-  if (m0 >= M) return;
-  const int n0 = blockIdx.z * 8 * NT;
-  const int64_t k0 = (int64_t)blockIdx.y * rows_per_chunk;
+  const int64_t item = (int64_t)blockIdx.x * 8 + warp;
+  if (item >= nitems) return;
+  const int64_t chunk = item / mtiles;
+  const int64_t m0 = (item - chunk * mtiles) * 8;
+  const int n0 = blockIdx.y * 8 * NT;
+  const int64_t k0 = chunk * rows_per_chunk;
   const int64_t k1 = min(k0 + rows_per_chunk, rows8);
 
   const bool a_ok = (m0 + g) < M;
@@ -77,7 +81,7 @@ __global__ void __launch_bounds__(256)
     }
   }
   // C fragment: row g, columns 2t, 2t+1 of each 8x8 tile
-  double* out = part + ((int64_t)blockIdx.y * Mpad + m0 + g) * Npad + n0 + 2 * t;
+  double* out = part + (chunk * Mpad + m0 + g) * Npad + n0 + 2 * t;
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt) {
     out[8 * nt] = c[nt][0];
@@ -85,18 +89,21 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// C[m][n] = sum over chunks (in chunk order) of part[chunk][m][n]
-__global__ void reduce_partials_kernel(const double* __restrict__ part, int64_t nchunks,
-                                       int64_t M, int N, int64_t Mpad, int Npad,
-                                       double* __restrict__ C, int64_t ldc) {
-  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= M * Npad) return;
-  const int64_t m = idx / Npad;
-  const int n = (int)(idx % Npad);
-  if (n >= N) return;
+// C[m][n] = sum over chunks of part[chunk][m][n]: one warp per output element, lanes stride
+// over the chunks, fixed shuffle tree -> the summation order never changes between runs.
+__global__ void __launch_bounds__(256)
+    reduce_partials_kernel(const double* __restrict__ part, int64_t nchunks, int64_t M, int N,
+                           int64_t Mpad, int Npad, double* __restrict__ C, int64_t ldc) {
+  const int lane = threadIdx.x & 31;
+  const int64_t idx = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (idx >= M * N) return;
+  const int64_t m = idx / N;
+  const int n = (int)(idx - m * N);
   double s = 0.0;
-  for (int64_t ch = 0; ch < nchunks; ++ch) s += part[(ch * Mpad + m) * Npad + n];
-  C[m * ldc + n] = s;
+  for (int64_t ch = lane; ch < nchunks; ch += 32) s += part[(ch * Mpad + m) * Npad + n];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off);
+  if (lane == 0) C[m * ldc + n] = s;
 }
 
 // ---------------------------------------------------------------- gemm_nn
@@ -277,36 +284,37 @@ void launch_gemm_tn(flz_ctx* ctx, const double* A, int64_t lda, int64_t M, const
   const int64_t rows8 = round_up(rows, 8);
   FLZ_REQUIRE(rows8 <= lda && rows8 <= ldb, FLZ_EDIM, "gemm_tn: leading dimension too small");
   const int NT = N > 16 ? 4 : (N > 8 ? 2 : 1);
-  const int64_t mblocks = (M + 63) / 64;
+  const int64_t mtiles = (M + 7) / 8;
   const int nblocks = (N + 8 * NT - 1) / (8 * NT);
-  // enough CTAs to fill the machine ~4x, chunks of at least 512 rows
-  int64_t want = (int64_t)ctx->sm_count * 4;
-  int64_t nchunks = (want + mblocks * nblocks - 1) / (mblocks * nblocks);
-  const int64_t max_chunks = (rows8 + 511) / 512;
+  // ~32 warps per SM over the whole grid, chunks of at least 256 rows
+  const int64_t want_warps = (int64_t)ctx->sm_count * 32;
+  int64_t nchunks = (want_warps + mtiles * nblocks - 1) / (mtiles * nblocks);
+  const int64_t max_chunks = (rows8 + 255) / 256;
   if (nchunks > max_chunks) nchunks = max_chunks;
   if (nchunks < 1) nchunks = 1;
-  int64_t rpc = round_up((rows8 + nchunks - 1) / nchunks, 8);
+  const int64_t rpc = round_up((rows8 + nchunks - 1) / nchunks, 8);
   nchunks = (rows8 + rpc - 1) / rpc;
-  const int64_t Mpad = mblocks * 64;
+  const int64_t Mpad = mtiles * 8;
   const int Npad = nblocks * 8 * NT;
+  const int64_t nitems = mtiles * nchunks;
   ctx->partial.reserve((size_t)(nchunks * Mpad * Npad));
-  dim3 grid((unsigned)mblocks, (unsigned)nchunks, (unsigned)nblocks);
+  dim3 grid((unsigned)((nitems + 7) / 8), (unsigned)nblocks);
   switch (NT) {
     case 1:
-      gemm_tn_kernel<1><<<grid, 256, 0, ctx->stream>>>(A, lda, M, B, ldb, N, rows8, rpc,
-                                                       ctx->partial.p, Mpad, Npad);
+      gemm_tn_kernel<1><<<grid, 256, 0, ctx->stream>>>(A, lda, M, B, ldb, N, rows8, rpc, mtiles,
+                                                       nitems, ctx->partial.p, Mpad, Npad);
       break;
     case 2:
-      gemm_tn_kernel<2><<<grid, 256, 0, ctx->stream>>>(A, lda, M, B, ldb, N, rows8, rpc,
-                                                       ctx->partial.p, Mpad, Npad);
+      gemm_tn_kernel<2><<<grid, 256, 0, ctx->stream>>>(A, lda, M, B, ldb, N, rows8, rpc, mtiles,
+                                                       nitems, ctx->partial.p, Mpad, Npad);
       break;
     default:
-      gemm_tn_kernel<4><<<grid, 256, 0, ctx->stream>>>(A, lda, M, B, ldb, N, rows8, rpc,
-                                                       ctx->partial.p, Mpad, Npad);
+      gemm_tn_kernel<4><<<grid, 256, 0, ctx->stream>>>(A, lda, M, B, ldb, N, rows8, rpc, mtiles,
+                                                       nitems, ctx->partial.p, Mpad, Npad);
       break;
   }
-  const int64_t total = M * Npad;
-  reduce_partials_kernel<<<(unsigned)((total + 255) / 256), 256, 0, ctx->stream>>>(
+  const int64_t total = M * N;
+  reduce_partials_kernel<<<(unsigned)((total + 7) / 8), 256, 0, ctx->stream>>>(
       ctx->partial.p, nchunks, M, N, Mpad, Npad, C, ldc);
   ctx->launches += 2;
   FLZ_CUDA(cudaGetLastError());

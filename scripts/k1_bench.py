@@ -1,0 +1,42 @@
+"""K1 (fused Clenshaw-step SpMM) timing + fast-vs-exact agreement on the bench shapes."""
+import sys, time, os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+from paper_2409_15053_b200 import Context, DeviceMatrix, matrices as M, solver as S
+
+ctx = Context()
+rng = np.random.default_rng(0)
+PEAK = 6533.2
+
+def bench(name, csr, r, m=50, sigma=0, check=True):
+    n, rp, ci, va = csr
+    A = DeviceMatrix(ctx, n, rp, ci, va, sigma=sigma)
+    cf = S.indicator_coefficients(-0.3, -0.25, m)
+    X = rng.standard_normal((n, r))
+    if check:
+        ctx.set_exact(True); _, Ye = A.filter_bench(cf, 1.0, 2.0, X, reps=1, want_output=True)
+        ctx.set_exact(False); _, Yf = A.filter_bench(cf, 1.0, 2.0, X, reps=1, want_output=True)
+        err = np.abs(Yf - Ye).max() / np.abs(Ye).max()
+    else:
+        err = float('nan')
+    A.filter_bench(cf, 1.0, 2.0, X, reps=1)
+    ms, _ = A.filter_bench(cf, 1.0, 2.0, X, reps=4)
+    nnz = len(va)
+    bytes_step = 12 * nnz + 4 * (n + 1) + 32 * n * r
+    gbs = 4 * m * bytes_step / (ms * 1e-3) / 1e9
+    st = A.stats()
+    print(f"{name:28s} n={n:8d} nnz/row={nnz/n:5.1f} r={r} fill={st['fill']:.3f} sigma={st['sigma']:6d} "
+          f"{ms/4/m*1e3:7.1f} us/step {gbs:7.0f} GB/s ({100*gbs/PEAK:5.1f}% of measured peak) fast-vs-exact {err:.1e}", flush=True)
+
+which = sys.argv[1] if len(sys.argv) > 1 else "all"
+lap = M.laplacian3d(100)
+bench("lap3d-100 r=3", lap, 3)
+bench("lap3d-100 r=1", lap, 1)
+bench("lap3d-100 r=4", lap, 4)
+pk = M.parsec_like()
+bench("parsec r=3", pk, 3)
+bench("parsec r=1", pk, 1)
+bench("lap2d-200 r=1", M.laplacian2d(200), 1)
+if which == "all":
+    bench("lap3d-160 r=3", M.laplacian3d(160), 3, m=20, check=False)
+    bench("parsec-c4 r=3", M.parsec_like(radius=40.0, h=0.0903, n_atoms=154, ball_radius=3.86, seed=2), 3, m=20, check=False)
