@@ -95,6 +95,28 @@ int64_t flz_matrix_nnz_local(const flz_matrix* A);
 int flz_matrix_stats(const flz_matrix* A, int64_t* stored_entries, int64_t* slices,
                      int64_t* halo_rows, int64_t* boundary_slices);
 
+/* Host-only half of flz_matrix_upload (no GPU, no NCCL): the SELL-32-sigma layout of this
+ * rank's rows and its halo plan.  Exists so that the multi-GPU logic can be exercised on
+ * CPUs; flz_matrix_upload runs exactly this code and then exchanges the need lists by NCCL.
+ *   starts[nranks+1]: first row of every rank (+ n_global).
+ *   info[10] = {rows_local, halo_rows, slices, stored_entries, interior_slices,
+ *               boundary_slices, send_rows, sigma, nnz_local, short_rows}
+ *   need(peer): global rows of `peer` this rank gathers (sorted); returns the count.
+ *   set_give(peer): the rows `peer` needs from this rank (its need list), once per peer.
+ *   arrays: any pointer may be NULL; sizes follow info[] (give/need offsets: nranks each). */
+typedef struct flz_plan flz_plan;
+int flz_plan_create(int64_t n_global, int rank, int nranks, const int64_t* starts,
+                    const int64_t* row_ptr, const int32_t* col_idx, const double* values,
+                    int sigma, flz_plan** out);
+void flz_plan_destroy(flz_plan* plan);
+int flz_plan_info(const flz_plan* plan, int64_t* info);
+int64_t flz_plan_need(const flz_plan* plan, int peer, int64_t* rows);
+int flz_plan_set_give(flz_plan* plan, int peer, int64_t count, const int64_t* rows);
+int flz_plan_arrays(const flz_plan* plan, int32_t* perm, int64_t* slice_ptr, int32_t* slice_len,
+                    int32_t* row_len, int32_t* col, double* val, int32_t* interior,
+                    int32_t* boundary, int32_t* send_rows, int64_t* give_off, int64_t* give_cnt,
+                    int64_t* need_off);
+
 /* Global matvec counter: speig::matvec_count()/reset (sparse.hpp:74-79).  One count per
  * vector-column product, so a fused r-column block product adds r. */
 uint64_t flz_matvec_count(void);

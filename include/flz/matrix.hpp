@@ -5,6 +5,10 @@
 // speig/sparse.hpp:12-79 (same names, argument meaning and error behaviour); the
 // arithmetic entry points (spmv / spmm_block / apply_uncounted) run on the GPU
 // through the C ABI (include/flz.h) instead of kernels::csr_matvec.
+//
+// Multi-GPU: on a distributed context (flz_ctx_create_dist + Device::adopt) every n-vector
+// argument of the block-level seams (spmm_block, ChebyshevFilter::apply, basis columns,
+// EigenResult::eigenvectors) holds this rank's LOCAL rows only.
 #pragma once
 
 #include <cstddef>
@@ -41,6 +45,11 @@ class Device {
   static void adopt(flz_ctx* ctx);
   static void set_device(int index);  // before first use
   static void shutdown();
+  // Multi-GPU (one process per GPU): rank / size of the active context and the contiguous
+  // block of rows this rank owns, [n*rank/size, n*(rank+1)/size).
+  static int rank();
+  static int nranks();
+  static void row_range(std::size_t n, std::size_t& begin, std::size_t& end);
 };
 
 // -------------------------------------------------------------- DenseBlock
@@ -91,6 +100,16 @@ class SparseSymMatrix {
                                   std::vector<std::int32_t> col_idx, std::vector<double> values,
                                   bool check = true);
 
+  // Distributed construction: this rank's rows [row_begin, row_begin + row_ptr.size() - 1) of
+  // an n_global x n_global matrix (global column ids).  Symmetry cannot be verified locally
+  // and is the caller's responsibility; dim() is the global dimension.
+  static SparseSymMatrix from_local_rows(std::size_t n_global, std::size_t row_begin,
+                                         std::vector<std::int64_t> row_ptr,
+                                         std::vector<std::int32_t> col_idx,
+                                         std::vector<double> values);
+  bool is_local_slab() const { return slab_; }
+  std::size_t local_begin() const { return row_begin_; }
+
   std::size_t dim() const { return n_; }
   std::size_t nnz() const { return static_cast<std::size_t>(row_ptr_.back()); }
   const std::vector<std::int64_t>& row_ptr() const { return row_ptr_; }
@@ -112,6 +131,8 @@ class SparseSymMatrix {
   void verify_symmetry() const;
 
   std::size_t n_ = 0;
+  std::size_t row_begin_ = 0;  // first row held (slab mode)
+  bool slab_ = false;
   std::vector<std::int64_t> row_ptr_{0};
   std::vector<std::int32_t> col_idx_;
   std::vector<double> values_;

@@ -59,6 +59,11 @@ int flz_hostmatrix_from_triplets(int64_t n, int64_t count, const int64_t* rows,
                                  flz_hostmatrix** out);
 int flz_hostmatrix_from_csr(int64_t n, const int64_t* row_ptr, const int32_t* col_idx,
                             const double* values, int check_symmetry, flz_hostmatrix** out);
+/* Distributed construction: this rank's rows [row_begin,row_end) (row_ptr starts at 0, global
+ * column ids); the row range must be the context's block n*rank/size .. n*(rank+1)/size. */
+int flz_hostmatrix_from_local_rows(int64_t n_global, int64_t row_begin, int64_t row_end,
+                                   const int64_t* row_ptr, const int32_t* col_idx,
+                                   const double* values, flz_hostmatrix** out);
 int flz_hostmatrix_load_mm(const char* path, flz_hostmatrix** out);
 int flz_hostmatrix_save_mm(const flz_hostmatrix* A, const char* path);
 void flz_hostmatrix_free(flz_hostmatrix* A);

@@ -83,6 +83,12 @@ _SIGS = {
     "flz_matrix_rows_local": (i64, [vp]),
     "flz_matrix_nnz_local": (i64, [vp]),
     "flz_matrix_stats": (i32, [vp, i64P, i64P, i64P, i64P]),
+    "flz_plan_create": (i32, [i64, i32, i32, i64p, i64p, i32p, f64p, i32, C.POINTER(vp)]),
+    "flz_plan_destroy": (None, [vp]),
+    "flz_plan_info": (i32, [vp, i64p]),
+    "flz_plan_need": (i64, [vp, i32, vp]),
+    "flz_plan_set_give": (i32, [vp, i32, i64, i64p]),
+    "flz_plan_arrays": (i32, [vp] + [vp] * 12),
     "flz_matvec_count": (u64, []),
     "flz_reset_matvec_count": (None, []),
     "flz_spmm": (i32, [vp, vp, vp, i32, vp, i32]),
@@ -113,6 +119,7 @@ _SOLVER_SIGS = {
     "flz_default_ctx": (i32, [C.POINTER(vp)]),
     "flz_hostmatrix_from_triplets": (i32, [i64, i64, i64p, i64p, f64p, C.POINTER(vp)]),
     "flz_hostmatrix_from_csr": (i32, [i64, i64p, i32p, f64p, i32, C.POINTER(vp)]),
+    "flz_hostmatrix_from_local_rows": (i32, [i64, i64, i64, i64p, i32p, f64p, C.POINTER(vp)]),
     "flz_hostmatrix_load_mm": (i32, [C.c_char_p, C.POINTER(vp)]),
     "flz_hostmatrix_save_mm": (i32, [vp, C.c_char_p]),
     "flz_hostmatrix_free": (None, [vp]),

@@ -13,6 +13,7 @@
 #include <numeric>
 
 #include "flz_internal.hpp"
+#include "host/plan.hpp"
 
 using namespace flz;
 
@@ -71,28 +72,6 @@ SellView view_boundary(const flz_matrix* A) {
   return SellView{A->tasks_boundary.p, A->nt_boundary, A->short_rows, A->slice_ptr.p, A->slice_len.p,
                   A->row_len.p,        A->col.p,       A->val.p,       A->boundary.p,
                   A->n_boundary,       A->nl};
-}
-
-// Groups slices (in list order) into CTA tasks: long slices get several warps each.
-std::vector<SliceTask> build_tasks(const std::vector<int32_t>& ids,
-                                   const std::vector<int32_t>& slice_len) {
-  #ifndef FLZ_K1_T
-#define FLZ_K1_T 24   // target entries per warp before a slice is split further
-#endif
-  auto warps_for = [](int32_t len) {
-    return len <= FLZ_K1_T ? 1 : (len <= 2 * FLZ_K1_T ? 2 : (len <= 4 * FLZ_K1_T ? 4 : 8));
-  };
-  std::vector<SliceTask> tasks;
-  size_t i = 0;
-  while (i < ids.size()) {
-    SliceTask t{};
-    t.warps_per_slice = warps_for(slice_len[ids[i]]);
-    const int cap = kTaskWarps / t.warps_per_slice;
-    while (i < ids.size() && t.count < cap && warps_for(slice_len[ids[i]]) == t.warps_per_slice)
-      t.slice[t.count++] = ids[i++];
-    tasks.push_back(t);
-  }
-  return tasks;
 }
 
 void ensure_workspaces(const flz_matrix* A) {
@@ -411,28 +390,63 @@ void flz_reset_matvec_count(void) { g_matvecs.store(0, std::memory_order_relaxed
 
 // ----------------------------------------------------------------- matrix
 
-static int64_t padded_entries(const std::vector<int32_t>& lens_new) {
-  int64_t total = 0;
-  for (size_t s = 0; s < lens_new.size(); s += kSliceRows) {
-    int32_t mx = 0;
-    for (size_t i = s; i < std::min(lens_new.size(), s + kSliceRows); ++i)
-      mx = std::max(mx, lens_new[i]);
-    total += (int64_t)mx * kSliceRows;
-  }
-  return total;
-}
+static_assert(sizeof(PlanTask) == sizeof(SliceTask), "PlanTask mirrors SliceTask");
 
-static void sort_windows(const std::vector<int32_t>& len, int64_t sigma,
-                         std::vector<int32_t>& perm) {
-  const int64_t nl = (int64_t)len.size();
-  perm.resize(nl);
-  std::iota(perm.begin(), perm.end(), 0);
-  if (sigma <= 1) return;
-  for (int64_t w0 = 0; w0 < nl; w0 += sigma) {
-    const int64_t w1 = std::min(nl, w0 + sigma);
-    std::stable_sort(perm.begin() + w0, perm.begin() + w1,
-                     [&](int32_t a, int32_t b) { return len[a] > len[b]; });
+// Device copy of a finished host plan (give lists set).
+static void upload_plan(flz_ctx* ctx, const HostPlan& P, flz_matrix* A) {
+  A->ctx = ctx;
+  A->n_global = P.n_global;
+  A->row_begin = P.row_begin;
+  A->row_end = P.row_end;
+  A->nl = P.nl;
+  A->ld = std::max<int64_t>(round_up(P.nl, kLdAlign), kLdAlign);
+  A->nnz = P.nnz;
+  A->stored = P.stored;
+  A->nslices = P.nslices;
+  A->nhalo = (int64_t)P.halo.size();
+  A->sigma = P.sigma;
+  A->short_rows = P.short_rows;
+  A->n_interior = (int64_t)P.interior.size();
+  A->n_boundary = (int64_t)P.boundary.size();
+  A->nt_all = (int64_t)P.tasks_all.size();
+  A->nt_interior = (int64_t)P.tasks_interior.size();
+  A->nt_boundary = (int64_t)P.tasks_boundary.size();
+  auto up = [&](auto& buf, const auto& host) {
+    buf.reserve(std::max<size_t>(host.size(), 1));
+    if (!host.empty())
+      FLZ_CUDA(cudaMemcpyAsync(buf.p, host.data(), host.size() * sizeof(host[0]),
+                               cudaMemcpyHostToDevice, ctx->stream));
+  };
+  up(A->slice_ptr, P.slice_ptr);
+  up(A->slice_len, P.slice_len);
+  up(A->row_len, P.row_len);
+  up(A->col, P.col);
+  up(A->val, P.val);
+  up(A->perm, P.perm);
+  up(A->iperm, P.iperm);
+  up(A->interior, P.interior);
+  up(A->boundary, P.boundary);
+  A->tasks_all.reserve(std::max<size_t>(P.tasks_all.size(), 1));
+  A->tasks_interior.reserve(std::max<size_t>(P.tasks_interior.size(), 1));
+  A->tasks_boundary.reserve(std::max<size_t>(P.tasks_boundary.size(), 1));
+  auto up_tasks = [&](DevBuf<SliceTask>& buf, const std::vector<PlanTask>& host) {
+    if (!host.empty())
+      FLZ_CUDA(cudaMemcpyAsync(buf.p, host.data(), host.size() * sizeof(PlanTask),
+                               cudaMemcpyHostToDevice, ctx->stream));
+  };
+  up_tasks(A->tasks_all, P.tasks_all);
+  up_tasks(A->tasks_interior, P.tasks_interior);
+  up_tasks(A->tasks_boundary, P.tasks_boundary);
+  A->h_perm = P.perm;
+  A->h_iperm = P.iperm;
+  for (int p = 0; p < P.nranks; ++p) {
+    if (p == P.rank || (P.need_cnt[p] == 0 && P.give_cnt[p] == 0)) continue;
+    A->peers.push_back({p, P.give_off[p], P.give_cnt[p], P.need_off[p], P.need_cnt[p]});
   }
+  A->n_send = (int64_t)P.send_rows.size();
+  up(A->send_rows, P.send_rows);
+  A->send_buf.reserve(std::max<size_t>(P.send_rows.size() * kMaxFuse, 1));
+  FLZ_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
 int flz_matrix_upload(flz_ctx* ctx, int64_t n_global, int64_t row_begin, int64_t row_end,
@@ -445,193 +459,34 @@ int flz_matrix_upload(flz_ctx* ctx, int64_t n_global, int64_t row_begin, int64_t
     FLZ_REQUIRE(ctx->nranks > 1 || (row_begin == 0 && row_end == n_global), FLZ_EINVAL,
                 "matrix_upload: a single-GPU context owns all rows");
     use(ctx);
-    const int64_t nl = row_end - row_begin;
-    FLZ_REQUIRE(nl < (int64_t)1 << 31, FLZ_EINVAL, "matrix_upload: too many local rows");
-    const int64_t nnz = row_ptr[nl] - row_ptr[0];
-    const int64_t p0 = row_ptr[0];
-    auto A = std::make_unique<flz_matrix>();
-    A->ctx = ctx;
-    A->n_global = n_global;
-    A->row_begin = row_begin;
-    A->row_end = row_end;
-    A->nl = nl;
-    A->ld = std::max<int64_t>(round_up(nl, kLdAlign), kLdAlign);
-    A->nnz = nnz;
-
-    std::vector<int32_t> len(nl);
-    for (int64_t i = 0; i < nl; ++i) {
-      const int64_t l = row_ptr[i + 1] - row_ptr[i];
-      FLZ_REQUIRE(l >= 0 && l < (int64_t)1 << 31, FLZ_EINVAL, "matrix_upload: bad row_ptr");
-      len[i] = (int32_t)l;
-    }
-    for (int64_t p = 0; p < nnz; ++p)
-      FLZ_REQUIRE(col_idx[p0 + p] >= 0 && col_idx[p0 + p] < n_global, FLZ_EINVAL,
-                  "matrix_upload: column index out of range");
-
-    // ---- choose sigma: smallest window whose padding overhead is <= 5 %
-    std::vector<int32_t> perm;
-    auto fill_for = [&](int64_t sg) {
-      sort_windows(len, sg, perm);
-      std::vector<int32_t> ln(nl);
-      for (int64_t i = 0; i < nl; ++i) ln[i] = len[perm[i]];
-      return padded_entries(ln);
-    };
-    int64_t chosen = sigma;
-    if (sigma <= 0) {
-      const int64_t cands[] = {1, 256, 4096, 65536, std::max<int64_t>(nl, 1)};
-      int64_t best_sg = 1, best_fill = -1;
-      for (int64_t sg : cands) {
-        if (sg > 1 && sg > nl && sg != cands[4]) continue;
-        const int64_t f = fill_for(sg);
-        if (best_fill < 0 || f < best_fill) {
-          best_fill = f;
-          best_sg = sg;
-        }
-        if ((double)f <= 1.05 * (double)std::max<int64_t>(nnz, 1)) {
-          best_sg = sg;
-          break;
-        }
-      }
-      chosen = best_sg;
-    }
-    sort_windows(len, chosen, perm);
-    A->sigma = (int)std::min<int64_t>(chosen, 1 << 30);
-    bool identity = true;
-    for (int64_t i = 0; i < nl && identity; ++i) identity = perm[i] == i;
-    if (identity) A->sigma = 1;
-    std::vector<int32_t> iperm(nl);
-    for (int64_t i = 0; i < nl; ++i) iperm[perm[i]] = (int32_t)i;
-
-    // ---- halo columns (distributed): sorted unique remote global ids
-    std::vector<int64_t> halo;
-    if (ctx->nranks > 1) {
-      for (int64_t p = 0; p < nnz; ++p) {
-        const int64_t g = col_idx[p0 + p];
-        if (g < row_begin || g >= row_end) halo.push_back(g);
-      }
-      std::sort(halo.begin(), halo.end());
-      halo.erase(std::unique(halo.begin(), halo.end()), halo.end());
-    }
-    A->nhalo = (int64_t)halo.size();
-    FLZ_REQUIRE(nl + A->nhalo < (int64_t)1 << 31, FLZ_EINVAL, "matrix_upload: index overflow");
-
-    // ---- SELL-32 storage
-    const int64_t nslices = (nl + kSliceRows - 1) / kSliceRows;
-    A->nslices = nslices;
-    std::vector<int64_t> slice_ptr(nslices + 1, 0);
-    std::vector<int32_t> slice_len(nslices, 0), row_len(nslices * kSliceRows, 0);
-    for (int64_t s = 0; s < nslices; ++s) {
-      int32_t mx = 0;
-      for (int l = 0; l < kSliceRows; ++l) {
-        const int64_t inew = s * kSliceRows + l;
-        if (inew >= nl) break;
-        row_len[inew] = len[perm[inew]];
-        mx = std::max(mx, row_len[inew]);
-      }
-      slice_len[s] = mx;
-      slice_ptr[s + 1] = slice_ptr[s] + (int64_t)mx * kSliceRows;
-    }
-    const int64_t stored = slice_ptr[nslices];
-    A->stored = stored;
-    std::vector<int32_t> col(std::max<int64_t>(stored, 1));
-    std::vector<double> val(std::max<int64_t>(stored, 1), 0.0);
-    std::vector<uint8_t> slice_boundary(nslices, 0);
-    for (int64_t s = 0; s < nslices; ++s)
-      for (int l = 0; l < kSliceRows; ++l) {
-        const int64_t inew = s * kSliceRows + l;
-        const int64_t base = slice_ptr[s] + l;
-        const int32_t self = (int32_t)std::min<int64_t>(inew, std::max<int64_t>(nl - 1, 0));
-        int32_t cnt = 0;
-        if (inew < nl) {
-          const int64_t iold = perm[inew];
-          for (int64_t p = row_ptr[iold]; p < row_ptr[iold + 1]; ++p, ++cnt) {
-            const int64_t g = col_idx[p];
-            int32_t c;
-            if (g >= row_begin && g < row_end) {
-              c = iperm[g - row_begin];
-            } else {
-              const int64_t slot = std::lower_bound(halo.begin(), halo.end(), g) - halo.begin();
-              c = (int32_t)(nl + slot);
-              slice_boundary[s] = 1;
-            }
-            col[base + (int64_t)cnt * kSliceRows] = c;
-            val[base + (int64_t)cnt * kSliceRows] = values[p];
-          }
-        }
-        for (; cnt < slice_len[s]; ++cnt) {  // padding: zero value, harmless in-range column
-          col[base + (int64_t)cnt * kSliceRows] = self;
-          val[base + (int64_t)cnt * kSliceRows] = 0.0;
-        }
-      }
-    std::vector<int32_t> interior, boundary;
-    for (int64_t s = 0; s < nslices; ++s)
-      (slice_boundary[s] ? boundary : interior).push_back((int32_t)s);
-    A->n_interior = (int64_t)interior.size();
-    A->n_boundary = (int64_t)boundary.size();
-
-    auto up = [&](auto& buf, const auto& host) {
-      buf.reserve(std::max<size_t>(host.size(), 1));
-      if (!host.empty())
-        FLZ_CUDA(cudaMemcpyAsync(buf.p, host.data(), host.size() * sizeof(host[0]),
-                                 cudaMemcpyHostToDevice, ctx->stream));
-    };
-    up(A->slice_ptr, slice_ptr);
-    up(A->slice_len, slice_len);
-    up(A->row_len, row_len);
-    up(A->col, col);
-    up(A->val, val);
-    up(A->perm, perm);
-    up(A->iperm, iperm);
-    up(A->interior, interior);
-    up(A->boundary, boundary);
-    {
-      std::vector<int32_t> all(nslices);
-      std::iota(all.begin(), all.end(), 0);
-      const auto ta = build_tasks(all, slice_len), ti = build_tasks(interior, slice_len),
-                 tb = build_tasks(boundary, slice_len);
-      A->short_rows = std::all_of(ta.begin(), ta.end(),
-                                  [](const SliceTask& t) { return t.warps_per_slice == 1; });
-      A->nt_all = (int64_t)ta.size();
-      A->nt_interior = (int64_t)ti.size();
-      A->nt_boundary = (int64_t)tb.size();
-      up(A->tasks_all, ta);
-      up(A->tasks_interior, ti);
-      up(A->tasks_boundary, tb);
-    }
-    A->h_perm = perm;
-    A->h_iperm = iperm;
-
-    // ---- halo plan: tell every owner which of its rows we gather
-    if (ctx->nranks > 1) {
-      const int P = ctx->nranks;
-      // all ranks' row ranges
-      DevBuf<int64_t> d_begin;
-      d_begin.reserve(2 * (size_t)P + 2);
-      std::vector<int64_t> starts(P + 1, 0), mine = {row_begin};
-      FLZ_CUDA(cudaMemcpyAsync(d_begin.p + P, mine.data(), sizeof(int64_t),
-                               cudaMemcpyHostToDevice, ctx->stream));
-      FLZ_NCCL(ncclAllGather(d_begin.p + P, d_begin.p, 1, ncclInt64, ctx->comm, ctx->stream));
-      FLZ_CUDA(cudaMemcpyAsync(starts.data(), d_begin.p, P * sizeof(int64_t),
-                               cudaMemcpyDeviceToHost, ctx->stream));
+    const int P = ctx->nranks;
+    std::vector<int64_t> starts(P + 1, 0);
+    starts[P] = n_global;
+    if (P > 1) {  // every rank's first row
+      DevBuf<int64_t> d;
+      d.reserve(2 * (size_t)P + 2);
+      FLZ_CUDA(cudaMemcpyAsync(d.p + P, &row_begin, sizeof(int64_t), cudaMemcpyHostToDevice,
+                               ctx->stream));
+      FLZ_NCCL(ncclAllGather(d.p + P, d.p, 1, ncclInt64, ctx->comm, ctx->stream));
+      FLZ_CUDA(cudaMemcpyAsync(starts.data(), d.p, P * sizeof(int64_t), cudaMemcpyDeviceToHost,
+                               ctx->stream));
       FLZ_CUDA(cudaStreamSynchronize(ctx->stream));
-      starts[P] = n_global;
-      for (int p = 0; p + 1 <= P; ++p)
-        FLZ_REQUIRE(starts[p] <= starts[p + 1], FLZ_EINVAL,
-                    "matrix_upload: rank row ranges must be ascending and contiguous");
-      // what we need from each peer (contiguous runs of the sorted halo list)
-      std::vector<int64_t> need_cnt(P, 0), need_off(P, 0);
-      {
-        size_t h = 0;
-        for (int p = 0; p < P; ++p) {
-          need_off[p] = (int64_t)h;
-          while (h < halo.size() && halo[h] < starts[p + 1]) ++h;
-          need_cnt[p] = (int64_t)h - need_off[p];
-        }
-      }
-      // exchange counts
-      DevBuf<int64_t> d_cnt;
+      FLZ_REQUIRE(starts[ctx->rank] == row_begin && (ctx->rank + 1 == P ? n_global
+                                                                         : starts[ctx->rank + 1]) ==
+                                                        row_end,
+                  FLZ_EINVAL, "matrix_upload: rank row ranges must be ascending and contiguous");
+    }
+    HostPlan plan;
+    try {
+      plan = build_plan(n_global, ctx->rank, P, starts, row_ptr, col_idx, values, sigma);
+    } catch (const std::invalid_argument& e) {
+      throw ApiError(FLZ_EINVAL, std::string("matrix_upload: ") + e.what());
+    }
+    if (P > 1) {
+      // tell every owner which of its rows we gather: counts first, then the row lists
+      DevBuf<int64_t> d_cnt, d_need, d_give;
       d_cnt.reserve(2 * (size_t)P);
-      FLZ_CUDA(cudaMemcpyAsync(d_cnt.p, need_cnt.data(), P * sizeof(int64_t),
+      FLZ_CUDA(cudaMemcpyAsync(d_cnt.p, plan.need_cnt.data(), P * sizeof(int64_t),
                                cudaMemcpyHostToDevice, ctx->stream));
       FLZ_NCCL(ncclGroupStart());
       for (int p = 0; p < P; ++p) {
@@ -640,30 +495,27 @@ int flz_matrix_upload(flz_ctx* ctx, int64_t n_global, int64_t row_begin, int64_t
         FLZ_NCCL(ncclRecv(d_cnt.p + P + p, 1, ncclInt64, p, ctx->comm, ctx->stream));
       }
       FLZ_NCCL(ncclGroupEnd());
-      std::vector<int64_t> give_cnt(P, 0);
+      std::vector<int64_t> give_cnt(P, 0), give_off(P, 0);
       FLZ_CUDA(cudaMemcpyAsync(give_cnt.data(), d_cnt.p + P, P * sizeof(int64_t),
                                cudaMemcpyDeviceToHost, ctx->stream));
       FLZ_CUDA(cudaStreamSynchronize(ctx->stream));
       give_cnt[ctx->rank] = 0;
-      // exchange the row lists (global ids)
-      std::vector<int64_t> give_off(P, 0);
       int64_t give_total = 0;
       for (int p = 0; p < P; ++p) {
         give_off[p] = give_total;
         give_total += give_cnt[p];
       }
-      DevBuf<int64_t> d_need, d_give;
-      d_need.reserve(std::max<size_t>(halo.size(), 1));
+      d_need.reserve(std::max<size_t>(plan.halo.size(), 1));
       d_give.reserve(std::max<size_t>((size_t)give_total, 1));
-      if (!halo.empty())
-        FLZ_CUDA(cudaMemcpyAsync(d_need.p, halo.data(), halo.size() * sizeof(int64_t),
+      if (!plan.halo.empty())
+        FLZ_CUDA(cudaMemcpyAsync(d_need.p, plan.halo.data(), plan.halo.size() * sizeof(int64_t),
                                  cudaMemcpyHostToDevice, ctx->stream));
       FLZ_NCCL(ncclGroupStart());
       for (int p = 0; p < P; ++p) {
         if (p == ctx->rank) continue;
-        if (need_cnt[p])
-          FLZ_NCCL(ncclSend(d_need.p + need_off[p], (size_t)need_cnt[p], ncclInt64, p, ctx->comm,
-                            ctx->stream));
+        if (plan.need_cnt[p])
+          FLZ_NCCL(ncclSend(d_need.p + plan.need_off[p], (size_t)plan.need_cnt[p], ncclInt64, p,
+                            ctx->comm, ctx->stream));
         if (give_cnt[p])
           FLZ_NCCL(ncclRecv(d_give.p + give_off[p], (size_t)give_cnt[p], ncclInt64, p, ctx->comm,
                             ctx->stream));
@@ -674,24 +526,89 @@ int flz_matrix_upload(flz_ctx* ctx, int64_t n_global, int64_t row_begin, int64_t
         FLZ_CUDA(cudaMemcpyAsync(give.data(), d_give.p, give_total * sizeof(int64_t),
                                  cudaMemcpyDeviceToHost, ctx->stream));
       FLZ_CUDA(cudaStreamSynchronize(ctx->stream));
-      std::vector<int32_t> send_rows(std::max<int64_t>(give_total, 1));
-      for (int64_t i = 0; i < give_total; ++i) {
-        FLZ_REQUIRE(give[i] >= row_begin && give[i] < row_end, FLZ_EINVAL,
-                    "matrix_upload: peer requested a row this rank does not own");
-        send_rows[i] = iperm[give[i] - row_begin];
+      try {
+        for (int p = 0; p < P; ++p)
+          if (p != ctx->rank && give_cnt[p])
+            plan_set_give(plan, p, give_cnt[p], give.data() + give_off[p]);
+      } catch (const std::invalid_argument& e) {
+        throw ApiError(FLZ_EINVAL, std::string("matrix_upload: ") + e.what());
       }
-      for (int p = 0; p < P; ++p) {
-        if (p == ctx->rank || (need_cnt[p] == 0 && give_cnt[p] == 0)) continue;
-        A->peers.push_back({p, give_off[p], give_cnt[p], need_off[p], need_cnt[p]});
-      }
-      A->n_send = give_total;
-      up(A->send_rows, send_rows);
-      A->send_buf.reserve(std::max<size_t>((size_t)give_total * kMaxFuse, 1));
     }
-    FLZ_CUDA(cudaStreamSynchronize(ctx->stream));
+    auto A = std::make_unique<flz_matrix>();
+    upload_plan(ctx, plan, A.get());
     ctx->refs += 1;
     *out = A.release();
   });
+}
+
+// ---- host-only view of the plan (no GPU needed): used to test the multi-GPU logic on CPUs
+struct flz_plan {
+  HostPlan P;
+};
+
+int flz_plan_create(int64_t n_global, int rank, int nranks, const int64_t* starts,
+                    const int64_t* row_ptr, const int32_t* col_idx, const double* values,
+                    int sigma, flz_plan** out) {
+  return guarded([&] {
+    FLZ_REQUIRE(starts && row_ptr && out, FLZ_EINVAL, "plan_create: null argument");
+    try {
+      auto plan = std::make_unique<flz_plan>();
+      plan->P = build_plan(n_global, rank, nranks,
+                           std::vector<int64_t>(starts, starts + nranks + 1), row_ptr, col_idx,
+                           values, sigma);
+      *out = plan.release();
+    } catch (const std::invalid_argument& e) {
+      throw ApiError(FLZ_EINVAL, e.what());
+    }
+  });
+}
+void flz_plan_destroy(flz_plan* plan) { delete plan; }
+int flz_plan_info(const flz_plan* plan, int64_t* info) {
+  const HostPlan& P = plan->P;
+  const int64_t v[10] = {P.nl, (int64_t)P.halo.size(), P.nslices, P.stored,
+                         (int64_t)P.interior.size(), (int64_t)P.boundary.size(),
+                         (int64_t)P.send_rows.size(), P.sigma, P.nnz, P.short_rows ? 1 : 0};
+  std::copy(v, v + 10, info);
+  return FLZ_OK;
+}
+int64_t flz_plan_need(const flz_plan* plan, int peer, int64_t* rows) {
+  const HostPlan& P = plan->P;
+  if (peer < 0 || peer >= P.nranks) return -1;
+  if (rows)
+    std::copy(P.halo.begin() + P.need_off[peer],
+              P.halo.begin() + P.need_off[peer] + P.need_cnt[peer], rows);
+  return P.need_cnt[peer];
+}
+int flz_plan_set_give(flz_plan* plan, int peer, int64_t count, const int64_t* rows) {
+  return guarded([&] {
+    try {
+      plan_set_give(plan->P, peer, count, rows);
+    } catch (const std::invalid_argument& e) {
+      throw ApiError(FLZ_EINVAL, e.what());
+    }
+  });
+}
+int flz_plan_arrays(const flz_plan* plan, int32_t* perm, int64_t* slice_ptr, int32_t* slice_len,
+                    int32_t* row_len, int32_t* col, double* val, int32_t* interior,
+                    int32_t* boundary, int32_t* send_rows, int64_t* give_off, int64_t* give_cnt,
+                    int64_t* need_off) {
+  const HostPlan& P = plan->P;
+  auto cp = [](const auto& v, auto* dst) {
+    if (dst) std::copy(v.begin(), v.end(), dst);
+  };
+  cp(P.perm, perm);
+  cp(P.slice_ptr, slice_ptr);
+  cp(P.slice_len, slice_len);
+  cp(P.row_len, row_len);
+  if (col) std::copy(P.col.begin(), P.col.begin() + P.stored, col);
+  if (val) std::copy(P.val.begin(), P.val.begin() + P.stored, val);
+  cp(P.interior, interior);
+  cp(P.boundary, boundary);
+  cp(P.send_rows, send_rows);
+  cp(P.give_off, give_off);
+  cp(P.give_cnt, give_cnt);
+  cp(P.need_off, need_off);
+  return FLZ_OK;
 }
 
 static void matrix_release(flz_matrix* A) {

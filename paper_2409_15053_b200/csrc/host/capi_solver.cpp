@@ -133,6 +133,19 @@ int flz_hostmatrix_from_csr(int64_t n, const int64_t* row_ptr, const int32_t* co
         std::vector<double>(values, values + nnz), check_symmetry != 0)};
   });
 }
+int flz_hostmatrix_from_local_rows(int64_t n_global, int64_t row_begin, int64_t row_end,
+                                   const int64_t* row_ptr, const int32_t* col_idx,
+                                   const double* values, flz_hostmatrix** out) {
+  return wrap([&] {
+    const int64_t nl = row_end - row_begin;
+    const std::size_t nnz = static_cast<std::size_t>(row_ptr[nl]);
+    *out = new flz_hostmatrix{SparseSymMatrix::from_local_rows(
+        static_cast<std::size_t>(n_global), static_cast<std::size_t>(row_begin),
+        std::vector<std::int64_t>(row_ptr, row_ptr + nl + 1),
+        std::vector<std::int32_t>(col_idx, col_idx + nnz),
+        std::vector<double>(values, values + nnz))};
+  });
+}
 int flz_hostmatrix_load_mm(const char* path, flz_hostmatrix** out) {
   return wrap([&] { *out = new flz_hostmatrix{load_matrix_market(path)}; });
 }

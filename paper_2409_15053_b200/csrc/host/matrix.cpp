@@ -61,6 +61,14 @@ void Device::set_device(int index) {
   std::lock_guard<std::mutex> lock(g_dev_mutex);
   g_dev_index = index;
 }
+int Device::rank() { return flz_ctx_rank(context()); }
+int Device::nranks() { return flz_ctx_nranks(context()); }
+void Device::row_range(std::size_t n, std::size_t& begin, std::size_t& end) {
+  const auto r = static_cast<std::size_t>(rank()), p = static_cast<std::size_t>(nranks());
+  begin = n * r / p;
+  end = n * (r + 1) / p;
+}
+
 void Device::shutdown() {
   std::lock_guard<std::mutex> lock(g_dev_mutex);
   if (g_ctx && g_ctx_owned) flz_ctx_destroy(g_ctx);
@@ -143,6 +151,30 @@ SparseSymMatrix SparseSymMatrix::from_csr(std::size_t n, std::vector<std::int64_
   return A;
 }
 
+SparseSymMatrix SparseSymMatrix::from_local_rows(std::size_t n_global, std::size_t row_begin,
+                                                 std::vector<std::int64_t> row_ptr,
+                                                 std::vector<std::int32_t> col_idx,
+                                                 std::vector<double> values) {
+  if (row_ptr.empty() || row_ptr.front() != 0 ||
+      static_cast<std::size_t>(row_ptr.back()) != col_idx.size() ||
+      col_idx.size() != values.size() || row_begin + row_ptr.size() - 1 > n_global)
+    throw Error("from_local_rows: inconsistent CSR arrays");
+  SparseSymMatrix A;
+  A.n_ = n_global;
+  A.row_begin_ = row_begin;
+  A.slab_ = true;
+  A.row_ptr_ = std::move(row_ptr);
+  A.col_idx_ = std::move(col_idx);
+  A.values_ = std::move(values);
+  for (std::size_t p = 0; p < A.values_.size(); ++p) {
+    if (A.col_idx_[p] < 0 || static_cast<std::size_t>(A.col_idx_[p]) >= n_global)
+      throw Error("matrix entry index out of range");
+    if (!std::isfinite(A.values_[p])) throw Error("matrix entry is not finite");
+    A.max_abs_ = std::max(A.max_abs_, std::abs(A.values_[p]));
+  }
+  return A;
+}
+
 // exact structural + numerical symmetry (sparse.cpp:65-83)
 void SparseSymMatrix::verify_symmetry() const {
   for (std::size_t i = 0; i < n_; ++i)
@@ -165,8 +197,17 @@ flz_matrix* SparseSymMatrix::device() const {
   if (!dev_ || dev_->ctx != ctx) {
     auto copy = std::make_shared<DeviceCopy>();
     copy->ctx = ctx;
-    throw_status(flz_matrix_upload(ctx, static_cast<std::int64_t>(n_), 0,
-                                   static_cast<std::int64_t>(n_), row_ptr_.data(),
+    std::size_t b = 0, e = n_;
+    Device::row_range(n_, b, e);
+    const std::int64_t* rp = row_ptr_.data();
+    if (slab_) {
+      if (b != row_begin_ || e - b != row_ptr_.size() - 1)
+        throw Error("SparseSymMatrix: the local row slab does not match this rank's row range");
+    } else {
+      rp += b;  // replicated global matrix: this rank's rows, absolute offsets
+    }
+    throw_status(flz_matrix_upload(ctx, static_cast<std::int64_t>(n_),
+                                   static_cast<std::int64_t>(b), static_cast<std::int64_t>(e), rp,
                                    col_idx_.data(), values_.data(), 0, &copy->handle));
     dev_ = std::move(copy);
   }
@@ -180,15 +221,19 @@ void SparseSymMatrix::spmv(const double* x, double* y) const {
   throw_status(flz_spmm(Device::context(), device(), x, 1, y, 1));
 }
 std::vector<double> SparseSymMatrix::spmv(const std::vector<double>& x) const {
-  if (x.size() != n_)
+  std::size_t b = 0, e = n_;
+  Device::row_range(n_, b, e);
+  if (x.size() != e - b)
     throw DimensionError("spmv: vector length " + std::to_string(x.size()) +
                          " does not match matrix dimension " + std::to_string(n_));
-  std::vector<double> y(n_);
+  std::vector<double> y(x.size());
   spmv(x.data(), y.data());
   return y;
 }
 void SparseSymMatrix::spmm_block(const DenseBlock& X, DenseBlock& Y) const {
-  if (X.rows() != n_)
+  std::size_t b = 0, e = n_;
+  Device::row_range(n_, b, e);
+  if (X.rows() != e - b)
     throw DimensionError("spmm_block: block has " + std::to_string(X.rows()) +
                          " rows, matrix dimension is " + std::to_string(n_));
   if (Y.rows() != X.rows() || Y.cols() != X.cols()) Y = DenseBlock(X.rows(), X.cols());

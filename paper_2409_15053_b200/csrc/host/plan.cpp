@@ -1,0 +1,220 @@
+// host/plan.cpp — see plan.hpp.  Pure host code, no CUDA.
+
+#include "plan.hpp"
+
+#include <algorithm>
+#include <numeric>
+#include <stdexcept>
+#include <string>
+
+namespace flz {
+
+namespace {
+
+#ifndef FLZ_K1_T
+#define FLZ_K1_T 24  // target entries per warp before a slice is split over more warps
+#endif
+
+int warps_for(int32_t len) {
+  return len <= FLZ_K1_T ? 1 : (len <= 2 * FLZ_K1_T ? 2 : (len <= 4 * FLZ_K1_T ? 4 : 8));
+}
+
+// Groups slices (in list order) into CTA tasks: long slices get several warps each.
+std::vector<PlanTask> build_tasks(const std::vector<int32_t>& ids,
+                                  const std::vector<int32_t>& slice_len) {
+  std::vector<PlanTask> tasks;
+  size_t i = 0;
+  while (i < ids.size()) {
+    PlanTask t{};
+    t.warps_per_slice = warps_for(slice_len[ids[i]]);
+    const int cap = kPlanTaskWarps / t.warps_per_slice;
+    while (i < ids.size() && t.count < cap && warps_for(slice_len[ids[i]]) == t.warps_per_slice)
+      t.slice[t.count++] = ids[i++];
+    tasks.push_back(t);
+  }
+  return tasks;
+}
+
+// stable sort by descending row length inside windows of `sigma` rows
+void sort_windows(const std::vector<int32_t>& len, int64_t sigma, std::vector<int32_t>& perm) {
+  const int64_t nl = (int64_t)len.size();
+  perm.resize(nl);
+  std::iota(perm.begin(), perm.end(), 0);
+  if (sigma <= 1) return;
+  for (int64_t w0 = 0; w0 < nl; w0 += sigma) {
+    const int64_t w1 = std::min(nl, w0 + sigma);
+    std::stable_sort(perm.begin() + w0, perm.begin() + w1,
+                     [&](int32_t a, int32_t b) { return len[a] > len[b]; });
+  }
+}
+
+int64_t padded_entries(const std::vector<int32_t>& len, const std::vector<int32_t>& perm) {
+  int64_t total = 0;
+  for (size_t s = 0; s < perm.size(); s += kPlanSliceRows) {
+    int32_t mx = 0;
+    for (size_t i = s; i < std::min(perm.size(), s + kPlanSliceRows); ++i)
+      mx = std::max(mx, len[perm[i]]);
+    total += (int64_t)mx * kPlanSliceRows;
+  }
+  return total;
+}
+
+void require(bool ok, const char* msg) {
+  if (!ok) throw std::invalid_argument(msg);
+}
+
+}  // namespace
+
+HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<int64_t>& starts,
+                    const int64_t* row_ptr, const int32_t* col_idx, const double* values,
+                    int sigma) {
+  require(nranks >= 1 && rank >= 0 && rank < nranks, "plan: bad rank/nranks");
+  require((int)starts.size() == nranks + 1 && starts.front() == 0 && starts.back() == n_global,
+          "plan: rank row ranges must cover [0, n)");
+  for (int p = 0; p < nranks; ++p)
+    require(starts[p] <= starts[p + 1], "plan: rank row ranges must be ascending and contiguous");
+  HostPlan P;
+  P.rank = rank;
+  P.nranks = nranks;
+  P.n_global = n_global;
+  P.starts = starts;
+  P.row_begin = starts[rank];
+  P.row_end = starts[rank + 1];
+  const int64_t nl = P.nl = P.row_end - P.row_begin;
+  require(nl < ((int64_t)1 << 31), "plan: too many local rows");
+  P.nnz = nl > 0 ? row_ptr[nl] - row_ptr[0] : 0;
+
+  std::vector<int32_t> len(nl);
+  for (int64_t i = 0; i < nl; ++i) {
+    const int64_t l = row_ptr[i + 1] - row_ptr[i];
+    require(l >= 0 && l < ((int64_t)1 << 31), "plan: bad row_ptr");
+    len[i] = (int32_t)l;
+  }
+  const int64_t p0 = nl > 0 ? row_ptr[0] : 0;
+  for (int64_t p = 0; p < P.nnz; ++p)
+    require(col_idx[p0 + p] >= 0 && col_idx[p0 + p] < n_global,
+            "plan: column index out of range");
+
+  // ---- sigma: smallest window whose padding overhead is <= 5 %
+  int64_t chosen = sigma;
+  if (sigma <= 0) {
+    const int64_t cands[] = {1, 256, 4096, 65536, std::max<int64_t>(nl, 1)};
+    int64_t best_fill = -1;
+    chosen = 1;
+    for (int64_t sg : cands) {
+      if (sg > 1 && sg > nl && sg != cands[4]) continue;
+      sort_windows(len, sg, P.perm);
+      const int64_t f = padded_entries(len, P.perm);
+      if (best_fill < 0 || f < best_fill) {
+        best_fill = f;
+        chosen = sg;
+      }
+      if ((double)f <= 1.05 * (double)std::max<int64_t>(P.nnz, 1)) {
+        chosen = sg;
+        break;
+      }
+    }
+  }
+  sort_windows(len, chosen, P.perm);
+  P.sigma = (int)std::min<int64_t>(chosen, 1 << 30);
+  bool identity = true;
+  for (int64_t i = 0; i < nl && identity; ++i) identity = P.perm[i] == i;
+  if (identity) P.sigma = 1;
+  P.iperm.resize(nl);
+  for (int64_t i = 0; i < nl; ++i) P.iperm[P.perm[i]] = (int32_t)i;
+
+  // ---- halo columns: sorted unique remote global ids, grouped by owner
+  if (nranks > 1) {
+    for (int64_t p = 0; p < P.nnz; ++p) {
+      const int64_t g = col_idx[p0 + p];
+      if (g < P.row_begin || g >= P.row_end) P.halo.push_back(g);
+    }
+    std::sort(P.halo.begin(), P.halo.end());
+    P.halo.erase(std::unique(P.halo.begin(), P.halo.end()), P.halo.end());
+  }
+  require(nl + (int64_t)P.halo.size() < ((int64_t)1 << 31), "plan: index overflow");
+  P.need_off.assign(nranks, 0);
+  P.need_cnt.assign(nranks, 0);
+  {
+    size_t h = 0;
+    for (int p = 0; p < nranks; ++p) {
+      P.need_off[p] = (int64_t)h;
+      while (h < P.halo.size() && P.halo[h] < starts[p + 1]) ++h;
+      P.need_cnt[p] = (int64_t)h - P.need_off[p];
+    }
+  }
+  P.give_off.assign(nranks, 0);
+  P.give_cnt.assign(nranks, 0);
+
+  // ---- SELL-32 storage
+  const int64_t nslices = P.nslices = (nl + kPlanSliceRows - 1) / kPlanSliceRows;
+  P.slice_ptr.assign(nslices + 1, 0);
+  P.slice_len.assign(nslices, 0);
+  P.row_len.assign(nslices * kPlanSliceRows, 0);
+  for (int64_t s = 0; s < nslices; ++s) {
+    int32_t mx = 0;
+    for (int l = 0; l < kPlanSliceRows; ++l) {
+      const int64_t inew = s * kPlanSliceRows + l;
+      if (inew >= nl) break;
+      P.row_len[inew] = len[P.perm[inew]];
+      mx = std::max(mx, P.row_len[inew]);
+    }
+    P.slice_len[s] = mx;
+    P.slice_ptr[s + 1] = P.slice_ptr[s] + (int64_t)mx * kPlanSliceRows;
+  }
+  P.stored = P.slice_ptr[nslices];
+  P.col.assign(std::max<int64_t>(P.stored, 1), 0);
+  P.val.assign(std::max<int64_t>(P.stored, 1), 0.0);
+  std::vector<uint8_t> is_boundary(nslices, 0);
+  for (int64_t s = 0; s < nslices; ++s)
+    for (int l = 0; l < kPlanSliceRows; ++l) {
+      const int64_t inew = s * kPlanSliceRows + l;
+      const int64_t base = P.slice_ptr[s] + l;
+      const int32_t self = (int32_t)std::min<int64_t>(inew, std::max<int64_t>(nl - 1, 0));
+      int32_t cnt = 0;
+      if (inew < nl) {
+        const int64_t iold = P.perm[inew];
+        for (int64_t p = row_ptr[iold]; p < row_ptr[iold + 1]; ++p, ++cnt) {  // CSR order kept
+          const int64_t g = col_idx[p];
+          int32_t c;
+          if (g >= P.row_begin && g < P.row_end) {
+            c = P.iperm[g - P.row_begin];
+          } else {
+            const int64_t slot = std::lower_bound(P.halo.begin(), P.halo.end(), g) - P.halo.begin();
+            c = (int32_t)(nl + slot);
+            is_boundary[s] = 1;
+          }
+          P.col[base + (int64_t)cnt * kPlanSliceRows] = c;
+          P.val[base + (int64_t)cnt * kPlanSliceRows] = values[p];
+        }
+      }
+      for (; cnt < P.slice_len[s]; ++cnt) {  // padding: zero value, harmless in-range column
+        P.col[base + (int64_t)cnt * kPlanSliceRows] = self;
+        P.val[base + (int64_t)cnt * kPlanSliceRows] = 0.0;
+      }
+    }
+  std::vector<int32_t> all(nslices);
+  std::iota(all.begin(), all.end(), 0);
+  for (int64_t s = 0; s < nslices; ++s)
+    (is_boundary[s] ? P.boundary : P.interior).push_back((int32_t)s);
+  P.tasks_all = build_tasks(all, P.slice_len);
+  P.tasks_interior = build_tasks(P.interior, P.slice_len);
+  P.tasks_boundary = build_tasks(P.boundary, P.slice_len);
+  P.short_rows = std::all_of(P.tasks_all.begin(), P.tasks_all.end(),
+                             [](const PlanTask& t) { return t.warps_per_slice == 1; });
+  return P;
+}
+
+void plan_set_give(HostPlan& P, int peer, int64_t count, const int64_t* global_rows) {
+  require(peer >= 0 && peer < P.nranks && peer != P.rank, "plan: bad peer");
+  require(P.give_cnt[peer] == 0, "plan: give list of this peer was already set");
+  P.give_off[peer] = (int64_t)P.send_rows.size();
+  P.give_cnt[peer] = count;
+  for (int64_t i = 0; i < count; ++i) {
+    require(global_rows[i] >= P.row_begin && global_rows[i] < P.row_end,
+            "plan: peer requested a row this rank does not own");
+    P.send_rows.push_back(P.iperm[global_rows[i] - P.row_begin]);
+  }
+}
+
+}  // namespace flz

@@ -1,0 +1,58 @@
+// host/plan.hpp — host-only construction of the device matrix layout and the halo plan.
+//
+// Everything flz_matrix_upload() decides on the host lives here so that the multi-GPU logic
+// (row partition, halo lists, interior/boundary split) can be unit-tested on CPUs
+// (tests/test_dist_plan.py drives it over gloo, world_size 2): SELL-32-sigma conversion of
+// the local rows of a CSR matrix (reference layout: sparse.hpp:28-33), renumbering of remote
+// columns to halo slots, per-peer "need" lists and, once the peers' requests are known,
+// the rows to pack for them.
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+namespace flz {
+
+constexpr int kPlanSliceRows = 32;
+constexpr int kPlanTaskWarps = 8;
+
+struct PlanTask {  // mirrors SliceTask (flz_internal.hpp)
+  int32_t warps_per_slice;
+  int32_t count;
+  int32_t slice[kPlanTaskWarps];
+};
+
+struct HostPlan {
+  // partition
+  int rank = 0, nranks = 1;
+  int64_t n_global = 0, row_begin = 0, row_end = 0, nl = 0, nnz = 0;
+  std::vector<int64_t> starts;  // nranks + 1 row offsets
+  // SELL-32-sigma of the local rows (columns: permuted local id, or nl + halo slot)
+  int sigma = 1;
+  int64_t nslices = 0, stored = 0;
+  std::vector<int32_t> perm, iperm;      // new -> old, old -> new (local rows)
+  std::vector<int64_t> slice_ptr;
+  std::vector<int32_t> slice_len, row_len, col;
+  std::vector<double> val;
+  std::vector<int32_t> interior, boundary;  // slice ids
+  std::vector<PlanTask> tasks_all, tasks_interior, tasks_boundary;
+  bool short_rows = false;
+  // halo: sorted unique remote global columns; slot h lives at row nl + h of a gather source
+  std::vector<int64_t> halo;
+  std::vector<int64_t> need_off, need_cnt;  // per owner rank: run of `halo` it must send us
+  // filled by set_give(): rows (permuted local ids) to pack for each peer
+  std::vector<int64_t> give_off, give_cnt;
+  std::vector<int32_t> send_rows;
+};
+
+// row_ptr holds absolute offsets into col_idx/values for local rows [row_begin,row_end);
+// col_idx are GLOBAL column ids.  sigma <= 0 selects the sorting window automatically.
+// Throws std::invalid_argument on malformed input.
+HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<int64_t>& starts,
+                    const int64_t* row_ptr, const int32_t* col_idx, const double* values,
+                    int sigma);
+
+// Peer `p` asks for `count` of our rows (global ids); call once per peer, any order.
+void plan_set_give(HostPlan& plan, int peer, int64_t count, const int64_t* global_rows);
+
+}  // namespace flz

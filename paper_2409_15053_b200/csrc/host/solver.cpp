@@ -58,6 +58,16 @@ void host_mgs(const DenseBlock& Q, std::size_t cols, double* z, std::size_t n) {
   }
 }
 
+// Rows [b, e) of a column-major block (identity when the context owns all rows).
+DenseBlock local_rows(const DenseBlock& X, std::size_t n_global) {
+  std::size_t b = 0, e = n_global;
+  Device::row_range(n_global, b, e);
+  if (b == 0 && e == X.rows()) return X;
+  DenseBlock L(e - b, X.cols());
+  for (std::size_t j = 0; j < X.cols(); ++j) std::copy(X.col(j) + b, X.col(j) + e, L.col(j));
+  return L;
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------ config
@@ -128,8 +138,12 @@ LanczosFactorization::LanczosFactorization(const BlockOperator& op, DenseBlock s
       rng_state_(mix_seed(0xD1B54A32D192ED03ULL, max_cols)) {
   if (r_ == 0 || n_ == 0) throw Error("LanczosFactorization: empty start block");
   if (max_cols_ < 2 * r_) throw Error("LanczosFactorization: column budget too small");
-  if (n_ != op.matrix().dim())
-    throw DimensionError("LanczosFactorization: start block rows do not match the matrix");
+  {
+    std::size_t b = 0, e = op.matrix().dim();
+    Device::row_range(op.matrix().dim(), b, e);
+    if (n_ != e - b)
+      throw DimensionError("LanczosFactorization: start block rows do not match the matrix");
+  }
   throw_status(flz_basis_create(Device::context(), op.matrix().device(),
                                 static_cast<std::int64_t>(max_cols_), static_cast<int>(r_),
                                 start.data(), &dev_));
@@ -160,7 +174,11 @@ double LanczosFactorization::ortho_error() const {
 }
 
 int expand(LanczosFactorization& st, int nblocks, ExpandTimes* times) {
-  const std::size_t n = st.n_, r = st.r_;
+  // n: global dimension (random replacement vectors are drawn for all n rows on every rank so
+  // that the stream equals the single-GPU one; each rank keeps its slab)
+  const std::size_t n = st.op_->matrix().dim(), r = st.r_;
+  std::size_t row_b = 0, row_e = n;
+  Device::row_range(n, row_b, row_e);
   flz_ctx* ctx = Device::context();
   const BlockOperator& op = *st.op_;
   const ChebyshevFilter* f = op.filter();
@@ -215,13 +233,13 @@ int expand(LanczosFactorization& st, int nblocks, ExpandTimes* times) {
         for (int attempt = 0; attempt < 5 && !replaced; ++attempt) {
           for (std::size_t i = 0; i < n; ++i) fresh[i] = gauss(rng);
           double rn = 0.0;
+          double* mine = fresh.data() + row_b;  // this rank's rows; rn is the global norm
           throw_status(flz_orthogonalize_column(ctx, st.dev_, static_cast<std::int64_t>(cols),
-                                                static_cast<int>(j), fresh.data(), &rn));
+                                                static_cast<int>(j), mine, &rn));
           if (rn > 1e-4) {
             const double inv = 1.0 / rn;
-            for (std::size_t i = 0; i < n; ++i) fresh[i] *= inv;
-            throw_status(flz_basis_set(ctx, st.dev_, static_cast<std::int64_t>(cols + j),
-                                       fresh.data()));
+            for (std::size_t i = 0; i < row_e - row_b; ++i) mine[i] *= inv;
+            throw_status(flz_basis_set(ctx, st.dev_, static_cast<std::int64_t>(cols + j), mine));
             replaced = true;
           }
         }
@@ -469,8 +487,10 @@ SpectralBounds estimate_spectral_bounds(const SparseSymMatrix& A, int steps, std
   std::vector<double> d(s_max, 0.0), e(s_max, 0.0);
   double beta_last = 0.0;
   int done = 0;
+  std::size_t row_b = 0, row_e = n;
+  Device::row_range(n, row_b, row_e);
   throw_status(flz_bounds_lanczos(Device::context(), A.device(), static_cast<int>(s_max),
-                                  q0.data(), d.data(), e.data(), &beta_last, &done));
+                                  q0.data() + row_b, d.data(), e.data(), &beta_last, &done));
   const auto s_done = static_cast<std::size_t>(done);
   d.resize(s_done);
   e.resize(s_done > 0 ? s_done - 1 : 0);
@@ -525,7 +545,7 @@ EigenResult run_solve(const SparseSymMatrix& A, double alpha, double beta,
 
   const auto r = static_cast<std::size_t>(cfg.block_size);
   const auto max_cols = static_cast<std::size_t>(cfg.resolved_max_dim(A.dim()));
-  LanczosFactorization st(op, init_block(A.dim(), r, cfg.seed), max_cols);
+  LanczosFactorization st(op, local_rows(init_block(A.dim(), r, cfg.seed), A.dim()), max_cols);
   const double norm_est = std::max(std::abs(bounds.lambda_min()), std::abs(bounds.lambda_max()));
 
   ExpandTimes times;

@@ -1,0 +1,85 @@
+"""Row-partition helpers for the multi-GPU path (one process per GPU).
+
+``HaloPlan`` wraps the host-only ``flz_plan_*`` entry points: the code flz_matrix_upload runs
+before it touches the GPU (SELL-32-sigma layout of the local rows, halo slots, per-peer need /
+give lists, interior / boundary slices).  It exists so that the N>1 logic is testable on CPUs
+(tests/test_dist_plan.py, gloo) — it performs no arithmetic of the hot path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from ._lib import check, lib
+
+
+def uniform_starts(n: int, nranks: int) -> np.ndarray:
+    """Contiguous row blocks: rank p owns [n*p//P, n*(p+1)//P) — the split the C++ facade uses."""
+    return np.array([n * p // nranks for p in range(nranks + 1)], dtype=np.int64)
+
+
+class HaloPlan:
+    INFO = ("rows_local", "halo_rows", "slices", "stored", "interior_slices", "boundary_slices",
+            "send_rows", "sigma", "nnz_local", "short_rows")
+
+    def __init__(self, n_global, rank, nranks, starts, row_ptr, col_idx, values, sigma=0):
+        """row_ptr/col_idx/values: the GLOBAL CSR arrays or this rank's slab with absolute
+        offsets (row_ptr[i] indexes col_idx/values directly); col_idx are global ids."""
+        self.rank, self.nranks = rank, nranks
+        starts = np.ascontiguousarray(starts, np.int64)
+        rp = np.ascontiguousarray(row_ptr, np.int64)
+        if len(rp) == n_global + 1 and nranks > 1:      # global array given: view of our rows
+            rp = np.ascontiguousarray(rp[starts[rank]:starts[rank + 1] + 1])
+        self._keep = (rp, np.ascontiguousarray(col_idx, np.int32),
+                      np.ascontiguousarray(values, np.float64))
+        h = C.c_void_p()
+        check(lib().flz_plan_create(n_global, rank, nranks, starts, *self._keep, sigma,
+                                    C.byref(h)))
+        self.handle = h
+        self._refresh()
+
+    def _refresh(self):
+        info = np.zeros(10, np.int64)
+        check(lib().flz_plan_info(self.handle, info))
+        self.info = dict(zip(self.INFO, (int(v) for v in info)))
+
+    def need(self, peer: int) -> np.ndarray:
+        cnt = lib().flz_plan_need(self.handle, peer, None)
+        out = np.zeros(max(cnt, 1), np.int64)
+        lib().flz_plan_need(self.handle, peer, out.ctypes.data_as(C.c_void_p))
+        return out[:cnt]
+
+    def set_give(self, peer: int, rows):
+        rows = np.ascontiguousarray(rows, np.int64)
+        check(lib().flz_plan_set_give(self.handle, peer, len(rows), rows))
+        self._refresh()
+
+    def arrays(self):
+        i, P = self.info, self.nranks
+        a = dict(perm=np.zeros(max(i["rows_local"], 1), np.int32),
+                 slice_ptr=np.zeros(i["slices"] + 1, np.int64),
+                 slice_len=np.zeros(max(i["slices"], 1), np.int32),
+                 row_len=np.zeros(max(i["slices"] * 32, 1), np.int32),
+                 col=np.zeros(max(i["stored"], 1), np.int32),
+                 val=np.zeros(max(i["stored"], 1), np.float64),
+                 interior=np.zeros(max(i["interior_slices"], 1), np.int32),
+                 boundary=np.zeros(max(i["boundary_slices"], 1), np.int32),
+                 send_rows=np.zeros(max(i["send_rows"], 1), np.int32),
+                 give_off=np.zeros(P, np.int64), give_cnt=np.zeros(P, np.int64),
+                 need_off=np.zeros(P, np.int64))
+        order = ("perm", "slice_ptr", "slice_len", "row_len", "col", "val", "interior", "boundary",
+                 "send_rows", "give_off", "give_cnt", "need_off")
+        check(lib().flz_plan_arrays(self.handle, *[a[k].ctypes.data_as(C.c_void_p) for k in order]))
+        a["perm"] = a["perm"][: i["rows_local"]]
+        a["interior"] = a["interior"][: i["interior_slices"]]
+        a["boundary"] = a["boundary"][: i["boundary_slices"]]
+        a["send_rows"] = a["send_rows"][: i["send_rows"]]
+        a["col"], a["val"] = a["col"][: i["stored"]], a["val"][: i["stored"]]
+        return a
+
+    def __del__(self):
+        try:
+            lib().flz_plan_destroy(self.handle)
+        except Exception:
+            pass

@@ -58,6 +58,16 @@ class SparseSymMatrix:
         return cls(h)
 
     @classmethod
+    def from_local_rows(cls, n_global, row_begin, row_end, row_ptr, col_idx, values):
+        """Distributed construction: this rank's row slab (row_ptr starts at 0)."""
+        h = C.c_void_p()
+        check(lib().flz_hostmatrix_from_local_rows(
+            n_global, row_begin, row_end, np.ascontiguousarray(row_ptr, np.int64),
+            np.ascontiguousarray(col_idx, np.int32), np.ascontiguousarray(values, np.float64),
+            C.byref(h)))
+        return cls(h)
+
+    @classmethod
     def load_matrix_market(cls, path):
         h = C.c_void_p()
         check(lib().flz_hostmatrix_load_mm(str(path).encode(), C.byref(h)))
