@@ -6,7 +6,9 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -44,12 +46,37 @@ int guarded(F&& f) {
   }
 }
 
+// FLZ_TRACE=1: per-phase device timings on stderr (synchronises the stream; diagnostics only)
+struct Trace {
+  flz_ctx* ctx;
+  const char* what;
+  std::chrono::steady_clock::time_point t0;
+  static bool on() {
+    static const bool v = std::getenv("FLZ_TRACE") != nullptr;
+    return v;
+  }
+  Trace(flz_ctx* c, const char* w) : ctx(c), what(w) {
+    if (on()) {
+      cudaStreamSynchronize(ctx->stream);
+      t0 = std::chrono::steady_clock::now();
+    }
+  }
+  ~Trace() {
+    if (on()) {
+      cudaStreamSynchronize(ctx->stream);
+      const double ms =
+          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+      std::fprintf(stderr, "[flz]   dev %-24s %9.3f ms\n", what, ms);
+    }
+  }
+};
+
 void use(const flz_ctx* ctx) { FLZ_CUDA(cudaSetDevice(ctx->device)); }
 
 struct Pinned {  // small RAII pinned host array
   double* p = nullptr;
-  explicit Pinned(size_t count) { FLZ_CUDA(cudaMallocHost(&p, count * sizeof(double))); }
-  ~Pinned() { if (p) cudaFreeHost(p); }
+  explicit Pinned(size_t count) { p = static_cast<double*>(pinned_alloc(count * sizeof(double))); }
+  ~Pinned() { pinned_free(p); }
   Pinned(const Pinned&) = delete;
   Pinned& operator=(const Pinned&) = delete;
 };
@@ -329,6 +356,7 @@ static void ctx_release(flz_ctx* ctx) {
   ctx->stage.release();
   ctx->stage2.release();
   ctx->flush.release();
+  pool_trim();  // cached blocks go back to the driver with the last user of the device
   cudaStreamDestroy(ctx->stream);
   cudaStreamDestroy(ctx->comm_stream);
   delete ctx;
@@ -382,6 +410,7 @@ int flz_mem_info(flz_ctx* ctx, size_t* free_bytes, size_t* total_bytes) {
   return guarded([&] {
     use(ctx);
     FLZ_CUDA(cudaMemGetInfo(free_bytes, total_bytes));
+    *free_bytes += pool_cached_bytes();  // cached blocks are reusable (and trimmed on demand)
   });
 }
 
@@ -773,7 +802,7 @@ int flz_basis_create(flz_ctx* ctx, const flz_matrix* A, int64_t max_cols, int r,
     upload_block(A, start, r, B->Q.p);
     const SmallLayout L = small_layout(max_cols, r);
     B->small.reserve_zero((size_t)L.total, ctx->stream);
-    FLZ_CUDA(cudaMallocHost(&B->pinned, (size_t)L.total * sizeof(double)));
+    B->pinned = static_cast<double*>(pinned_alloc((size_t)L.total * sizeof(double)));
     B->pinned_count = (size_t)L.total;
     FLZ_CUDA(cudaEventCreate(&B->e0));
     FLZ_CUDA(cudaEventCreate(&B->e1));
@@ -792,7 +821,7 @@ void flz_basis_destroy(flz_basis* B) {
   if (B->e0) cudaEventDestroy(B->e0);
   if (B->e1) cudaEventDestroy(B->e1);
   if (B->e2) cudaEventDestroy(B->e2);
-  if (B->pinned) cudaFreeHost(B->pinned);
+  pinned_free(B->pinned);
   flz_ctx* ctx = B->ctx;
   flz_matrix* A = const_cast<flz_matrix*>(B->A);
   delete B;
@@ -989,8 +1018,10 @@ int flz_ritz_lift(flz_ctx* ctx, const flz_matrix* A, const flz_basis* Bc, int64_
     if (w == 0) return;
     const int64_t nl = B->nl, ld = B->ld;
     const int64_t ldw = round_up(w, 64);
+    { Trace tr(ctx, "lift: reserve V, AV");
     B->V.reserve_zero((size_t)ld * w, ctx->stream);
-    B->AV.reserve_zero((size_t)ld * w, ctx->stream);
+    B->AV.reserve_zero((size_t)ld * w, ctx->stream); }
+    Trace* tr1 = new Trace(ctx, "lift: W transpose + H2D");
     // W (dim x w column-major) -> row-major [dim][ldw]
     std::vector<double> Wt((size_t)dim * ldw, 0.0);
     for (int c = 0; c < w; ++c)
@@ -999,7 +1030,9 @@ int flz_ritz_lift(flz_ctx* ctx, const flz_matrix* A, const flz_basis* Bc, int64_
     dW.reserve(Wt.size() + 8);
     FLZ_CUDA(cudaMemcpyAsync(dW.p, Wt.data(), Wt.size() * sizeof(double), cudaMemcpyHostToDevice,
                              ctx->stream));
-    launch_gemm_nn(ctx, B->Q.p, ld, dim, dW.p, ldw, w, nl, 1.0, false, B->V.p, ld);
+    delete tr1;
+    { Trace tr(ctx, "lift: V = Q W (gemm_nn)");
+    launch_gemm_nn(ctx, B->Q.p, ld, dim, dW.p, ldw, w, nl, 1.0, false, B->V.p, ld); }
     DevBuf<double> dn;
     dn.reserve((size_t)2 * w + 8);
     launch_coldot(ctx, B->V.p, ld, B->V.p, ld, w, nl, dn.p);
@@ -1025,11 +1058,13 @@ int flz_ritz_lift(flz_ctx* ctx, const flz_matrix* A, const flz_basis* Bc, int64_
     FLZ_CUDA(cudaMemcpyAsync(dn.p + w, hs.data(), wk * sizeof(double), cudaMemcpyHostToDevice,
                              ctx->stream));
     launch_scale_cols(ctx, B->V.p, ld, wk, nl, dn.p + w);
-    spmm_device(A, B->V.p, ld, wk, B->AV.p, ld, false);  // uncounted (lanczos.cpp:448-449)
+    { Trace tr(ctx, "lift: AV = A V");
+    spmm_device(A, B->V.p, ld, wk, B->AV.p, ld, false); }  // uncounted (lanczos.cpp:448-449)
     const int64_t ldb = round_up(wk, 8);
     DevBuf<double> dB;
     dB.reserve((size_t)wk * ldb + 8);
-    launch_gemm_tn(ctx, B->V.p, ld, wk, B->AV.p, ld, wk, nl, dB.p, ldb);
+    { Trace tr(ctx, "lift: V'AV (gemm_tn)");
+    launch_gemm_tn(ctx, B->V.p, ld, wk, B->AV.p, ld, wk, nl, dB.p, ldb); }
     allreduce(ctx, dB.p, (size_t)wk * ldb);
     std::vector<double> hB((size_t)wk * ldb);
     FLZ_CUDA(cudaMemcpyAsync(hB.data(), dB.p, hB.size() * sizeof(double), cudaMemcpyDeviceToHost,
@@ -1067,6 +1102,7 @@ static void residuals_and_vectors(flz_ctx* ctx, const flz_basis* B, double* V, d
                            ctx->stream));
   FLZ_CUDA(cudaStreamSynchronize(ctx->stream));
   for (int c = 0; c < w2; ++c) residuals[c] = std::sqrt(std::max(h[c], 0.0)) / scale;  // :477
+  Trace tr(ctx, "eigenvectors D2H");
   if (eigvecs)
     for (int c = 0; c < w2; c += 64) {
       const int nc = std::min(64, w2 - c);
@@ -1095,8 +1131,9 @@ int flz_ritz_rotate(flz_ctx* ctx, const flz_basis* Bc, const double* U, const do
                              ctx->stream));
     B->V2.reserve_zero((size_t)ld * w2, ctx->stream);
     B->AV2.reserve_zero((size_t)ld * w2, ctx->stream);
+    { Trace tr(ctx, "rotate: V U, AV U");
     launch_gemm_nn(ctx, B->V.p, ld, wk, dU.p, ldu, w2, nl, 1.0, false, B->V2.p, ld);   // :467-470
-    launch_gemm_nn(ctx, B->AV.p, ld, wk, dU.p, ldu, w2, nl, 1.0, false, B->AV2.p, ld);
+    launch_gemm_nn(ctx, B->AV.p, ld, wk, dU.p, ldu, w2, nl, 1.0, false, B->AV2.p, ld); }
     residuals_and_vectors(ctx, B, B->V2.p, B->AV2.p, lambda, w2, scale, true, residuals, eigvecs);
   });
 }

@@ -44,6 +44,15 @@ void set_last_error(const std::string& msg);
   } while (0)
 
 // ------------------------------------------------------------ device buffer
+// Caching allocator (pool.cu): device blocks of the current device and pinned host blocks
+// are kept for reuse after they are freed; pool_trim() returns everything to the driver.
+void* pool_alloc(size_t bytes);
+void pool_free(void* p);
+void pool_trim();
+size_t pool_cached_bytes();
+void* pinned_alloc(size_t bytes);
+void pinned_free(void* p);
+
 template <class T>
 struct DevBuf {
   T* p = nullptr;
@@ -53,7 +62,7 @@ struct DevBuf {
   DevBuf& operator=(const DevBuf&) = delete;
   ~DevBuf() { release(); }
   void release() {
-    if (p) cudaFree(p);
+    if (p) pool_free(p);
     p = nullptr;
     count = 0;
   }
@@ -61,7 +70,7 @@ struct DevBuf {
   void reserve(size_t n) {
     if (n <= count) return;
     release();
-    FLZ_CUDA(cudaMalloc(&p, n * sizeof(T)));
+    p = static_cast<T*>(pool_alloc(n * sizeof(T)));
     count = n;
   }
   void reserve_zero(size_t n, cudaStream_t s) {

@@ -16,6 +16,8 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <random>
 
 #include "flz.h"
@@ -34,6 +36,15 @@ class WallClock {
  private:
   std::chrono::steady_clock::time_point t0_;
 };
+
+// FLZ_TRACE=1: phase timings of the host driver on stderr (diagnostics only)
+bool trace_on() {
+  static const bool on = std::getenv("FLZ_TRACE") != nullptr;
+  return on;
+}
+void trace(const char* what, const WallClock& clk) {
+  if (trace_on()) std::fprintf(stderr, "[flz] %-28s %9.3f ms\n", what, clk.seconds() * 1e3);
+}
 
 // splitmix64 finaliser; same stream derivation as the reference (lanczos.cpp:25-30)
 std::uint64_t mix_seed(std::uint64_t seed, std::uint64_t salt) {
@@ -387,6 +398,7 @@ EigenResult recover_eigenpairs(const LanczosFactorization& st, const SparseSymMa
   }
 
   // Ritz vectors of T_k for the candidates only.
+  const WallClock t_w;
   DenseBlock W(dim, w);
   if (ritz.vectors.size() == dim * dim && dim > 0) {
     for (std::size_t t = 0; t < w; ++t)
@@ -413,12 +425,15 @@ EigenResult recover_eigenpairs(const LanczosFactorization& st, const SparseSymMa
     }
   }
 
+  trace("recover: T_k eigenvectors", t_w);
   std::vector<double> vnorm(w), Bm(w * w);
   std::vector<std::uint8_t> keep(w);
   int w_kept = 0;
+  const WallClock t_lift;
   throw_status(flz_ritz_lift(ctx, A.device(), st.device(), static_cast<std::int64_t>(dim),
                              W.data(), static_cast<int>(w), vnorm.data(), keep.data(), &w_kept,
                              Bm.data()));
+  trace("recover: lift + A V + V'AV", t_lift);
   std::vector<std::size_t> kept_src;
   for (std::size_t t = 0; t < w; ++t)
     if (keep[t]) kept_src.push_back(candidates[t]);
@@ -430,7 +445,9 @@ EigenResult recover_eigenpairs(const LanczosFactorization& st, const SparseSymMa
     SymBandMatrix B(wk, wk > 1 ? wk - 1 : 0);
     for (std::size_t i = 0; i < wk; ++i)
       for (std::size_t j = i; j < wk; ++j) B.set(j, i, Bm[i * wk + j]);
+    const WallClock t_b;
     const SymEig small = sym_band_eig(B);
+    trace("recover: eig of V'AV", t_b);
     std::vector<std::size_t> sel;
     for (std::size_t c = 0; c < wk; ++c)
       if (small.values[c] >= alpha && small.values[c] <= beta) sel.push_back(c);
@@ -442,10 +459,12 @@ EigenResult recover_eigenpairs(const LanczosFactorization& st, const SparseSymMa
     out.eigenvalues = lambdas;  // already ascending
     out.residuals.assign(sel.size(), 0.0);
     out.eigenvectors = DenseBlock(n, sel.size());
+    const WallClock t_rot;
     if (!sel.empty())
       throw_status(flz_ritz_rotate(ctx, st.device(), U.data(), lambdas.data(),
                                    static_cast<int>(sel.size()), scale, out.residuals.data(),
                                    out.eigenvectors.data()));
+    trace("recover: rotate + residuals + D2H", t_rot);
   } else if (wk > 0) {
     // plain mode: Ritz values are the eigenvalue estimates (:480-495)
     std::vector<double> lam(wk), res(wk);

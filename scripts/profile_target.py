@@ -10,5 +10,9 @@ wl = bench.workloads()[name]
 n, rp, ci, va = wl["gen"]()
 H = S.SparseSymMatrix.from_csr(n, rp, ci, va, check_symmetry=False)
 cfg = S.LanczosConfig(max_dim=max_dim, **wl["cfg"])
-res = S.filtered_lanczos(H, *wl["interval"], cfg, want_vectors=False)
+reps = int(sys.argv[3]) if len(sys.argv) > 3 else 1
+want = len(sys.argv) > 4 and sys.argv[4] == "vectors"
+for rep in range(reps):
+    print(f"--- solve {rep}", file=sys.stderr, flush=True)
+    res = S.filtered_lanczos(H, *wl["interval"], cfg, want_vectors=want)
 print(name, len(res.eigenvalues), res.stats["block_steps"], res.stats["converged"], res.stats["time_total_s"])
