@@ -94,6 +94,13 @@ int64_t flz_matrix_nnz_local(const flz_matrix* A);
 /* storage statistics: stored (padded) entries, slices, halo rows received per SpMV */
 int flz_matrix_stats(const flz_matrix* A, int64_t* stored_entries, int64_t* slices,
                      int64_t* halo_rows, int64_t* boundary_slices);
+/* index-compressed layout the fast kernels stream: matrix bytes read per product and the
+ * number of true nonzeros held at uniform-offset positions (8 instead of 12 bytes each) */
+int flz_matrix_layout(const flz_matrix* A, int64_t* matrix_bytes, int64_t* uniform_entries);
+/* launch-shape knobs of the fused Clenshaw-step kernels (0 = built-in default): slices per
+ * CTA of the one-warp-per-slice kernel, tasks per CTA of the multi-warp kernel, positions
+ * per pipeline stage of the one-warp-per-slice kernel (4 or 8) */
+int flz_ctx_set_tuning(flz_ctx* ctx, int slices_per_cta, int tasks_per_cta, int batch);
 
 /* Host-only half of flz_matrix_upload (no GPU, no NCCL): the SELL-32-sigma layout of this
  * rank's rows and its halo plan.  Exists so that the multi-GPU logic can be exercised on
@@ -116,6 +123,12 @@ int flz_plan_arrays(const flz_plan* plan, int32_t* perm, int64_t* slice_ptr, int
                     int32_t* row_len, int32_t* col, double* val, int32_t* interior,
                     int32_t* boundary, int32_t* send_rows, int64_t* give_off, int64_t* give_cnt,
                     int64_t* need_off);
+/* index-compressed layout of the plan (what the fast kernels stream), for host-side checks:
+ * sizes[5] = {slices, values, general columns, uniform offsets, uniform true entries};
+ * descriptors: 16 int32 per slice {val_ptr lo/hi, col_ptr lo/hi, uoff_ptr, nu, ng, 0,
+ * first 8 offsets}.  Any pointer may be NULL. */
+int flz_plan_ug(const flz_plan* plan, int64_t* sizes, int32_t* descriptors, double* ug_val,
+                int32_t* ug_col, int32_t* ug_uoff);
 
 /* Global matvec counter: speig::matvec_count()/reset (sparse.hpp:74-79).  One count per
  * vector-column product, so a fused r-column block product adds r. */

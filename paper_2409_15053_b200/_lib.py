@@ -83,12 +83,15 @@ _SIGS = {
     "flz_matrix_rows_local": (i64, [vp]),
     "flz_matrix_nnz_local": (i64, [vp]),
     "flz_matrix_stats": (i32, [vp, i64P, i64P, i64P, i64P]),
+    "flz_matrix_layout": (i32, [vp, i64P, i64P]),
+    "flz_ctx_set_tuning": (i32, [vp, i32, i32, i32]),
     "flz_plan_create": (i32, [i64, i32, i32, i64p, i64p, i32p, f64p, i32, C.POINTER(vp)]),
     "flz_plan_destroy": (None, [vp]),
     "flz_plan_info": (i32, [vp, i64p]),
     "flz_plan_need": (i64, [vp, i32, vp]),
     "flz_plan_set_give": (i32, [vp, i32, i64, i64p]),
     "flz_plan_arrays": (i32, [vp] + [vp] * 12),
+    "flz_plan_ug": (i32, [vp, vp, vp, vp, vp, vp]),
     "flz_matvec_count": (u64, []),
     "flz_reset_matvec_count": (None, []),
     "flz_spmm": (i32, [vp, vp, vp, i32, vp, i32]),

@@ -86,47 +86,84 @@ void allreduce(flz_ctx* ctx, double* buf, size_t count) {
   FLZ_NCCL(ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, ctx->comm, ctx->stream));
 }
 
+// The CSR-order SELL arrays serve the exact-mode kernel only: they stay on the host until
+// the first exact-mode product on this matrix.
+void ensure_exact_arrays(const flz_matrix* A) {
+  flz_ctx* ctx = A->ctx;
+  if (!ctx->exact || A->col.p) return;
+  A->col.reserve(std::max<size_t>(A->h_col.size(), 1));
+  A->val.reserve(std::max<size_t>(A->h_val.size(), 1));
+  if (!A->h_col.empty()) {
+    FLZ_CUDA(cudaMemcpyAsync(A->col.p, A->h_col.data(), A->h_col.size() * sizeof(int32_t),
+                             cudaMemcpyHostToDevice, ctx->stream));
+    FLZ_CUDA(cudaMemcpyAsync(A->val.p, A->h_val.data(), A->h_val.size() * sizeof(double),
+                             cudaMemcpyHostToDevice, ctx->stream));
+    FLZ_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  std::vector<int32_t>().swap(A->h_col);
+  std::vector<double>().swap(A->h_val);
+}
+
+SellView make_view(const flz_matrix* A, const SliceTask* tasks, int64_t ntasks,
+                   const int32_t* slice_ids, int64_t nslices) {
+  ensure_exact_arrays(A);
+  return SellView{tasks,        ntasks,     A->short_rows, A->slice_ptr.p, A->slice_len.p,
+                  A->row_len.p, A->col.p,   A->val.p,      slice_ids,      nslices,
+                  A->nl,        A->ug.p,    A->ug_val.p,   A->ug_col.p,    A->ug_uoff.p,
+                  A->nl + A->nhalo};
+}
 SellView view_all(const flz_matrix* A) {
-  return SellView{A->tasks_all.p, A->nt_all, A->short_rows, A->slice_ptr.p, A->slice_len.p, A->row_len.p,
-                  A->col.p,       A->val.p,  nullptr,        A->nslices,     A->nl};
+  return make_view(A, A->tasks_all.p, A->nt_all, nullptr, A->nslices);
 }
 SellView view_interior(const flz_matrix* A) {
-  return SellView{A->tasks_interior.p, A->nt_interior, A->short_rows, A->slice_ptr.p, A->slice_len.p,
-                  A->row_len.p,        A->col.p,       A->val.p,       A->interior.p,
-                  A->n_interior,       A->nl};
+  return make_view(A, A->tasks_interior.p, A->nt_interior, A->interior.p, A->n_interior);
 }
 SellView view_boundary(const flz_matrix* A) {
-  return SellView{A->tasks_boundary.p, A->nt_boundary, A->short_rows, A->slice_ptr.p, A->slice_len.p,
-                  A->row_len.p,        A->col.p,       A->val.p,       A->boundary.p,
-                  A->n_boundary,       A->nl};
+  return make_view(A, A->tasks_boundary.p, A->nt_boundary, A->boundary.p, A->n_boundary);
 }
+
+// leading dimension of the planar filter workspaces (local rows + halo rows, padded)
+int64_t planar_ld(const flz_matrix* A) { return round_up(A->nl + A->nhalo, kLdAlign); }
 
 void ensure_workspaces(const flz_matrix* A) {
   flz_ctx* ctx = A->ctx;
-  const size_t need = (size_t)(A->nl + A->nhalo) * kMaxFuse + 8;
+  const size_t need = (size_t)planar_ld(A) * kMaxFuse + 8;
   if (A->y1.count < need) {
     A->y1.reserve_zero(need, ctx->stream);
     A->y2.reserve_zero(need, ctx->stream);
   }
 }
 
-// Halo exchange of the gather source Y1 (interleaved, R doubles per row): pack the rows
-// the peers reference, send/recv on the comm stream, leave ev_halo_done for the boundary
-// launch.  The caller launches the interior slices in between.
-void halo_begin(const flz_matrix* A, int S, double* Y1) {
+// Halo exchange of the gather source Y1: pack the rows the peers reference, send/recv on the
+// comm stream, leave ev_halo_done for the boundary launch.  The caller launches the interior
+// slices in between.  Interleaved blocks (S > 0) travel as whole padded rows; planar blocks
+// (S == 0) as R contiguous runs per peer, received straight into the tail of each column.
+void halo_begin(const flz_matrix* A, int R, int S, double* Y1) {
   flz_ctx* ctx = A->ctx;
-  const int R = S;  // whole (padded) rows travel
-  launch_pack_rows(ctx, ctx->stream, A->n_send, S, A->send_rows.p, Y1, A->send_buf.p);
+  const int64_t ldy = planar_ld(A);
+  launch_pack_rows(ctx, ctx->stream, A->n_send, R, S, ldy, A->send_rows.p, Y1, A->send_buf.p);
   FLZ_CUDA(cudaEventRecord(ctx->ev_halo_ready, ctx->stream));
   FLZ_CUDA(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_halo_ready, 0));
   FLZ_NCCL(ncclGroupStart());
   for (const auto& p : A->peers) {
-    if (p.send_count)
-      FLZ_NCCL(ncclSend(A->send_buf.p + p.send_off * R, (size_t)p.send_count * R, ncclDouble,
-                        p.rank, ctx->comm, ctx->comm_stream));
-    if (p.recv_count)
-      FLZ_NCCL(ncclRecv(Y1 + (A->nl + p.recv_off) * R, (size_t)p.recv_count * R, ncclDouble,
-                        p.rank, ctx->comm, ctx->comm_stream));
+    if (S > 0) {
+      if (p.send_count)
+        FLZ_NCCL(ncclSend(A->send_buf.p + p.send_off * S, (size_t)p.send_count * S, ncclDouble,
+                          p.rank, ctx->comm, ctx->comm_stream));
+      if (p.recv_count)
+        FLZ_NCCL(ncclRecv(Y1 + (A->nl + p.recv_off) * S, (size_t)p.recv_count * S, ncclDouble,
+                          p.rank, ctx->comm, ctx->comm_stream));
+    } else {
+      for (int k = 0; k < R; ++k) {
+        if (p.send_count)
+          FLZ_NCCL(ncclSend(A->send_buf.p + (int64_t)k * A->n_send + p.send_off,
+                            (size_t)p.send_count, ncclDouble, p.rank, ctx->comm,
+                            ctx->comm_stream));
+        if (p.recv_count)
+          FLZ_NCCL(ncclRecv(Y1 + (int64_t)k * ldy + A->nl + p.recv_off, (size_t)p.recv_count,
+                            ncclDouble, p.rank, ctx->comm, ctx->comm_stream));
+      }
+    }
   }
   FLZ_NCCL(ncclGroupEnd());
   FLZ_CUDA(cudaEventRecord(ctx->ev_halo_done, ctx->comm_stream));
@@ -137,24 +174,32 @@ void halo_begin(const flz_matrix* A, int S, double* Y1) {
 void sell_step(const flz_matrix* A, int R, int S, StepMode mode, double s1, double s2, double b,
                double* Y1, double* Y2, const double* X, int64_t ldx, double* Out, int64_t ldo) {
   flz_ctx* ctx = A->ctx;
+  const int64_t ldy = planar_ld(A);
   if (ctx->nranks == 1 || A->peers.empty()) {
-    launch_clenshaw_step(ctx, view_all(A), R, S, mode, ctx->exact, s1, s2, b, Y1, Y2, X, ldx,
+    launch_clenshaw_step(ctx, view_all(A), R, S, mode, ctx->exact, s1, s2, b, Y1, Y2, ldy, X, ldx,
                          Out, ldo);
     return;
   }
-  halo_begin(A, S, Y1);
-  launch_clenshaw_step(ctx, view_interior(A), R, S, mode, ctx->exact, s1, s2, b, Y1, Y2, X, ldx,
-                       Out, ldo);
+  halo_begin(A, R, S, Y1);
+  launch_clenshaw_step(ctx, view_interior(A), R, S, mode, ctx->exact, s1, s2, b, Y1, Y2, ldy, X,
+                       ldx, Out, ldo);
   FLZ_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_halo_done, 0));
-  launch_clenshaw_step(ctx, view_boundary(A), R, S, mode, ctx->exact, s1, s2, b, Y1, Y2, X, ldx,
-                       Out, ldo);
+  launch_clenshaw_step(ctx, view_boundary(A), R, S, mode, ctx->exact, s1, s2, b, Y1, Y2, ldy, X,
+                       ldx, Out, ldo);
 }
 
-// Row stride of the interleaved workspaces for R fused columns: 3 columns are padded to 4
-// (one aligned 32-byte sector per gathered row) when the matrix is gather dominated
-// (>= 16 entries per row); the exact-mode kernel always uses S == R.
+// Layout of the filter workspaces for R fused columns (see launch_clenshaw_step):
+// interleaved rows, 3 columns padded to 4 (one aligned 32-byte sector per gathered row) when
+// the matrix is gather dominated (>= 16 entries per row).  The planar layout (0) is kept as
+// an experiment (FLZ_K1_LAYOUT=planar): measured on B200 it is slower than interleaved rows
+// even for pure stencils (100^3 Laplacian, 3 columns: 84 % vs 96 % of the copy bandwidth).
+// The exact-mode kernel always reads interleaved rows of stride R.
 int row_stride(const flz_matrix* A, int R) {
-  if (R != 3 || A->ctx->exact || A->nl == 0) return R;
+  if (A->ctx->exact || A->nl == 0) return R;
+  static const char* force = std::getenv("FLZ_K1_LAYOUT");  // experiments: planar | interleaved
+  const bool planar = force && force[0] == 'p';
+  if (planar) return 0;
+  if (R != 3) return R;
   return (A->nnz >= 16 * A->nl) ? 4 : 3;
 }
 
@@ -166,7 +211,7 @@ void spmm_device(const flz_matrix* A, const double* X, int64_t ldx, int ncols, d
   for (int c0 = 0; c0 < ncols; c0 += kMaxFuse) {
     const int R = std::min(kMaxFuse, ncols - c0);
     const int S = row_stride(A, R);
-    launch_interleave(ctx, A->nl, R, S, 1.0, X + (int64_t)c0 * ldx, ldx, A->y1.p);
+    launch_interleave(ctx, A->nl, R, S, 1.0, X + (int64_t)c0 * ldx, ldx, A->y1.p, planar_ld(A));
     sell_step(A, R, S, StepMode::plain, 1.0, 0.0, 0.0, A->y1.p, A->y2.p, nullptr, 0,
               Z + (int64_t)c0 * ldz, ldz);
   }
@@ -189,13 +234,14 @@ void filter_device(const flz_matrix* A, const double* coeffs, int m, double c, d
     if (m == 0) {  // Y = b_0 X, no products (filter.cpp:133-136)
       for (int k = 0; k < R; ++k)
         launch_interleave(ctx, A->nl, 1, 1, coeffs[0], Xc + (int64_t)k * ldx, ldx,
-                          Zc + (int64_t)k * ldz);
+                          Zc + (int64_t)k * ldz, 0);
       continue;
     }
     double* Y1 = A->y1.p;
     double* Y2 = A->y2.p;
-    launch_interleave(ctx, A->nl, R, S, coeffs[m], Xc, ldx, Y1);               // :144
-    FLZ_CUDA(cudaMemsetAsync(Y2, 0, (size_t)A->nl * S * sizeof(double), ctx->stream));
+    launch_interleave(ctx, A->nl, R, S, coeffs[m], Xc, ldx, Y1, planar_ld(A));   // :144
+    FLZ_CUDA(cudaMemsetAsync(Y2, 0, (S > 0 ? (size_t)A->nl * S : (size_t)planar_ld(A) * R) *
+                                            sizeof(double), ctx->stream));
     for (int j = m - 1; j >= 1; --j) {                                          // :146-151
       sell_step(A, R, S, StepMode::step, s1, s2, coeffs[j], Y1, Y2, Xc, ldx, nullptr, 0);
       std::swap(Y1, Y2);
@@ -422,7 +468,7 @@ void flz_reset_matvec_count(void) { g_matvecs.store(0, std::memory_order_relaxed
 static_assert(sizeof(PlanTask) == sizeof(SliceTask), "PlanTask mirrors SliceTask");
 
 // Device copy of a finished host plan (give lists set).
-static void upload_plan(flz_ctx* ctx, const HostPlan& P, flz_matrix* A) {
+static void upload_plan(flz_ctx* ctx, HostPlan& P, flz_matrix* A) {
   A->ctx = ctx;
   A->n_global = P.n_global;
   A->row_begin = P.row_begin;
@@ -449,8 +495,19 @@ static void upload_plan(flz_ctx* ctx, const HostPlan& P, flz_matrix* A) {
   up(A->slice_ptr, P.slice_ptr);
   up(A->slice_len, P.slice_len);
   up(A->row_len, P.row_len);
-  up(A->col, P.col);
-  up(A->val, P.val);
+  A->h_col = std::move(P.col);  // exact-mode arrays: uploaded on first use
+  A->h_val = std::move(P.val);
+  static_assert(sizeof(PlanUgSlice) == sizeof(UgSlice), "PlanUgSlice mirrors UgSlice");
+  A->ug.reserve(std::max<size_t>(P.ug_slice.size(), 1));
+  if (!P.ug_slice.empty())
+    FLZ_CUDA(cudaMemcpyAsync(A->ug.p, P.ug_slice.data(), P.ug_slice.size() * sizeof(UgSlice),
+                             cudaMemcpyHostToDevice, ctx->stream));
+  up(A->ug_val, P.ug_val);
+  up(A->ug_col, P.ug_col);
+  up(A->ug_uoff, P.ug_uoff);
+  A->ug_bytes = (int64_t)(P.ug_val.size() * 8 + P.ug_col.size() * 4 + P.ug_uoff.size() * 4 +
+                          P.ug_slice.size() * sizeof(UgSlice));
+  A->ug_uniform_entries = P.ug_uniform_entries;
   up(A->perm, P.perm);
   up(A->iperm, P.iperm);
   up(A->interior, P.interior);
@@ -640,6 +697,25 @@ int flz_plan_arrays(const flz_plan* plan, int32_t* perm, int64_t* slice_ptr, int
   return FLZ_OK;
 }
 
+int flz_plan_ug(const flz_plan* plan, int64_t* sizes, int32_t* descriptors, double* ug_val,
+                int32_t* ug_col, int32_t* ug_uoff) {
+  if (!plan) return FLZ_EINVAL;
+  const HostPlan& P = plan->P;
+  if (sizes) {
+    sizes[0] = (int64_t)P.ug_slice.size();
+    sizes[1] = (int64_t)P.ug_val.size();
+    sizes[2] = (int64_t)P.ug_col.size();
+    sizes[3] = (int64_t)P.ug_uoff.size();
+    sizes[4] = P.ug_uniform_entries;
+  }
+  if (descriptors && !P.ug_slice.empty())
+    std::memcpy(descriptors, P.ug_slice.data(), P.ug_slice.size() * sizeof(PlanUgSlice));
+  if (ug_val) std::copy(P.ug_val.begin(), P.ug_val.end(), ug_val);
+  if (ug_col) std::copy(P.ug_col.begin(), P.ug_col.end(), ug_col);
+  if (ug_uoff) std::copy(P.ug_uoff.begin(), P.ug_uoff.end(), ug_uoff);
+  return FLZ_OK;
+}
+
 static void matrix_release(flz_matrix* A) {
   if (!A || --A->refs > 0) return;
   flz_ctx* ctx = A->ctx;
@@ -658,6 +734,20 @@ int flz_matrix_stats(const flz_matrix* A, int64_t* stored_entries, int64_t* slic
   if (halo_rows) *halo_rows = A->nhalo;
   if (boundary_slices) *boundary_slices = A->n_boundary;
   return A->sigma;
+}
+
+int flz_matrix_layout(const flz_matrix* A, int64_t* matrix_bytes, int64_t* uniform_entries) {
+  if (!A) return FLZ_EINVAL;
+  if (matrix_bytes) *matrix_bytes = A->ug_bytes;
+  if (uniform_entries) *uniform_entries = A->ug_uniform_entries;
+  return FLZ_OK;
+}
+int flz_ctx_set_tuning(flz_ctx* ctx, int slices_per_cta, int tasks_per_cta, int batch) {
+  if (!ctx || slices_per_cta < 0 || tasks_per_cta < 0 || batch < 0) return FLZ_EINVAL;
+  ctx->k1_slices_per_cta = slices_per_cta;
+  ctx->k1_tasks_per_cta = tasks_per_cta;
+  ctx->k1_batch = batch;
+  return FLZ_OK;
 }
 
 // ------------------------------------------------- block products & filter

@@ -88,10 +88,23 @@ constexpr int kLdAlign = 32;     // leading dimensions are multiples of 32 doubl
 // Work item of the multi-warp Clenshaw-step kernel: one CTA of kTaskWarps warps processes
 // `count` slices with `warps_per_slice` warps each (count * warps_per_slice <= kTaskWarps).
 constexpr int kTaskWarps = 8;
+constexpr int kUgInline = 8;     // uniform offsets repeated inside a slice descriptor
 struct SliceTask {
   int32_t warps_per_slice;
   int32_t count;
   int32_t slice[kTaskWarps];
+};
+
+// Per-slice header of the index-compressed ("UG") layout of the fast kernels; mirrors
+// PlanUgSlice (host/plan.hpp).  Positions [0, nu) are uniform (column = row + uoff[p]),
+// positions [nu, nu + ng) are general (one column per lane).
+struct UgSlice {
+  int64_t val_ptr;
+  int64_t col_ptr;
+  int32_t uoff_ptr;
+  int32_t nu, ng;
+  int32_t reserved;
+  int32_t inline_off[8];  // the first offsets again: one 64-byte load serves short slices
 };
 
 }  // namespace flz
@@ -109,6 +122,7 @@ struct flz_ctx {
   int sm_count = 148;
   int refs = 1;                  // owner + every matrix/basis created on the context
   uint64_t launches = 0;
+  int k1_slices_per_cta = 0, k1_tasks_per_cta = 0, k1_batch = 0;  // 0: defaults (tuning knobs)
   cudaEvent_t t0[16] = {}, t1[16] = {};
   flz::DevBuf<double> partial;   // split-K partial sums of the tall-skinny GEMMs
   flz::DevBuf<double> small;     // small device scratch of the host-buffer test seams
@@ -136,8 +150,18 @@ struct flz_matrix {
   flz::DevBuf<int64_t> slice_ptr;   // [nslices+1] element offsets
   flz::DevBuf<int32_t> slice_len;   // [nslices]
   flz::DevBuf<int32_t> row_len;     // [nslices*32]
-  flz::DevBuf<int32_t> col;         // [stored] permuted local col or nl + halo slot
-  flz::DevBuf<double> val;          // [stored]
+  // CSR-order SELL arrays: read only by the exact-mode kernel, uploaded on its first use
+  // from the host copies below
+  mutable flz::DevBuf<int32_t> col; // [stored] permuted local col or nl + halo slot
+  mutable flz::DevBuf<double> val;  // [stored]
+  mutable std::vector<int32_t> h_col;
+  mutable std::vector<double> h_val;
+  // index-compressed layout read by the fast kernels
+  flz::DevBuf<flz::UgSlice> ug;     // [nslices]
+  flz::DevBuf<double> ug_val;
+  flz::DevBuf<int32_t> ug_col, ug_uoff;
+  int64_t ug_bytes = 0;             // matrix bytes one fast step streams
+  int64_t ug_uniform_entries = 0;
   flz::DevBuf<int32_t> perm;        // [nl] new -> old
   flz::DevBuf<int32_t> iperm;       // [nl] old -> new
   flz::DevBuf<int32_t> interior;    // slice ids without halo references
@@ -203,23 +227,31 @@ struct SellView {
   const int32_t* slice_ids;  // nullptr: all slices [0, nslices)
   int64_t nslices;           // number of slices this launch covers
   int64_t nl;
+  // index-compressed layout (fast kernels)
+  const UgSlice* ug;
+  const double* ug_val;
+  const int32_t* ug_col;
+  const int32_t* ug_uoff;
+  int64_t ncols;             // rows of a gather source: local rows + halo rows
 };
 
 enum class StepMode { step, final, plain };
 
-// One fused Clenshaw step (or plain SpMM) for R in [1, kMaxFuse] interleaved columns with
-// row stride S (S == R, or S == 4 for R == 3 on long-row matrices):
+// One fused Clenshaw step (or plain SpMM) for R in [1, kMaxFuse] block columns.  Layout of
+// the blocks Y1/Y2: S > 0 interleaved with row stride S (S == R, or S == 4 for R == 3 on
+// long-row matrices); S == 0 planar, column k at Y + k*ldy (best when the matrix is mostly
+// uniform-offset positions: every gather is then a contiguous 256-byte warp load):
 //   step : Y2[i,:] = s1*(A Y1)[i,:] + s2*Y1[i,:] - Y2[i,:] + b*X[i,:]   (interleaved out)
 //   final: Out[:,k] column-major (ld = ldo) receives the same expression
 //   plain: Out[:,k] = (A Y1)[i,k]
 void launch_clenshaw_step(flz_ctx* ctx, const SellView& A, int R, int S, StepMode mode, bool exact,
                           double s1, double s2, double b, const double* Y1, double* Y2,
-                          const double* X, int64_t ldx, double* Out, int64_t ldo);
-// Y1[i*S+k] = scale * X[k*ldx+i]  (column-major -> interleaved with row stride S >= R)
+                          int64_t ldy, const double* X, int64_t ldx, double* Out, int64_t ldo);
+// Y1 = scale * X  (column-major -> interleaved with row stride S >= R, or planar for S == 0)
 void launch_interleave(flz_ctx* ctx, int64_t nl, int R, int S, double scale, const double* X,
-                       int64_t ldx, double* Y1);
-// halo packing: buf[s*S+k] = Y1[rows[s]*S+k]
-void launch_pack_rows(flz_ctx* ctx, cudaStream_t stream, int64_t count, int S,
+                       int64_t ldx, double* Y1, int64_t ldy);
+// halo packing: buf[s*S+k] = Y1[rows[s]*S+k]; planar (S == 0): buf[k*count+s] = Y1[k*ldy+rows[s]]
+void launch_pack_rows(flz_ctx* ctx, cudaStream_t stream, int64_t count, int R, int S, int64_t ldy,
                       const int32_t* rows, const double* Y1, double* buf);
 // out[i] = s1*w[i] + s2*y1[i] - y2[i] + b*x[i]
 void launch_combine(flz_ctx* ctx, int64_t n, bool exact, double s1, double s2, double b,

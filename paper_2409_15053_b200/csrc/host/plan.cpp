@@ -59,6 +59,133 @@ int64_t padded_entries(const std::vector<int32_t>& len, const std::vector<int32_
   return total;
 }
 
+// ---- UG layout -------------------------------------------------------------------------
+// A diagonal offset d = col - row that at least kUgMinLanes of a slice's 32 lanes hold is
+// stored as ONE uniform position: 32 values + one int32, the lanes without it get a zero.
+// Break-even against a general position (12 bytes per true entry) is 22 of 32 lanes.
+constexpr int kUgMinLanes = 22;
+
+struct OffsetCounter {  // open-addressing counter of the offsets of one slice
+  std::vector<int64_t> key;
+  std::vector<int32_t> cnt;
+  std::vector<int32_t> used;
+  size_t mask;
+  explicit OffsetCounter(size_t cap_pow2) : key(cap_pow2), cnt(cap_pow2, 0), mask(cap_pow2 - 1) {}
+  void add(int64_t d) {
+    size_t h = (size_t)((uint64_t)d * 0x9E3779B97F4A7C15ULL >> 40) & mask;
+    while (cnt[h] != 0 && key[h] != d) h = (h + 1) & mask;
+    if (cnt[h] == 0) {
+      key[h] = d;
+      used.push_back((int32_t)h);
+    }
+    ++cnt[h];
+  }
+  void clear() {
+    for (int32_t h : used) cnt[h] = 0;
+    used.clear();
+  }
+};
+
+void build_ug(HostPlan& P) {
+  const int64_t nslices = P.nslices, nl = P.nl;
+  P.ug_slice.assign(nslices, PlanUgSlice{});
+  P.ug_val.clear();
+  P.ug_col.clear();
+  P.ug_uoff.clear();
+  P.ug_val.reserve(P.stored);
+  P.ug_uniform_entries = 0;
+  int32_t max_len = 0;
+  for (int64_t s = 0; s < nslices; ++s) max_len = std::max(max_len, P.slice_len[s]);
+  size_t cap = 64;
+  while (cap < (size_t)max_len * kPlanSliceRows * 2) cap <<= 1;
+  OffsetCounter counter(cap);
+  std::vector<int64_t> uni;            // chosen offsets of the slice, ascending
+  std::vector<int32_t> glen(kPlanSliceRows);
+  // identical offset lists (every interior slice of a stencil) share one copy
+  std::vector<int64_t> last_uni;
+  int32_t last_uoff_ptr = -1;
+  for (int64_t s = 0; s < nslices; ++s) {
+    const int32_t L = P.slice_len[s];
+    const int64_t base = P.slice_ptr[s];
+    counter.clear();
+    for (int l = 0; l < kPlanSliceRows; ++l) {
+      const int64_t row = s * kPlanSliceRows + l;
+      const int32_t len = row < nl ? P.row_len[row] : 0;
+      for (int32_t p = 0; p < len; ++p)
+        counter.add((int64_t)P.col[base + (int64_t)p * kPlanSliceRows + l] - row);
+    }
+    uni.clear();
+    for (int32_t h : counter.used)
+      if (counter.cnt[h] >= kUgMinLanes) uni.push_back(counter.key[h]);
+    std::sort(uni.begin(), uni.end());
+    // general part: what every lane keeps after its uniform entries are taken out
+    int32_t ng = 0;
+    if (!uni.empty()) {
+      for (int l = 0; l < kPlanSliceRows; ++l) {
+        const int64_t row = s * kPlanSliceRows + l;
+        const int32_t len = row < nl ? P.row_len[row] : 0;
+        int32_t g = 0;
+        for (int32_t p = 0; p < len; ++p) {
+          const int64_t d = (int64_t)P.col[base + (int64_t)p * kPlanSliceRows + l] - row;
+          if (!std::binary_search(uni.begin(), uni.end(), d)) ++g;
+        }
+        glen[l] = g;
+        ng = std::max(ng, g);
+      }
+      // keep the split only when it moves fewer bytes than the plain slice
+      const int64_t bytes_plain = (int64_t)12 * kPlanSliceRows * L;
+      const int64_t bytes_ug = (int64_t)8 * kPlanSliceRows * ((int64_t)uni.size() + ng) +
+                               4 * (int64_t)uni.size() + (int64_t)4 * kPlanSliceRows * ng;
+      if (bytes_ug >= bytes_plain) uni.clear();
+    }
+    if (uni.empty()) ng = L;
+    const int32_t nu = (int32_t)uni.size();
+    PlanUgSlice& H = P.ug_slice[s];
+    H.val_ptr = (int64_t)P.ug_val.size();
+    H.col_ptr = (int64_t)P.ug_col.size();
+    H.nu = nu;
+    H.ng = ng;
+    if (nu > 0 && uni == last_uni) {
+      H.uoff_ptr = last_uoff_ptr;
+    } else {
+      H.uoff_ptr = (int32_t)P.ug_uoff.size();
+      for (int64_t d : uni) P.ug_uoff.push_back((int32_t)d);
+      if (nu > 0) {
+        last_uni = uni;
+        last_uoff_ptr = H.uoff_ptr;
+      }
+    }
+    for (int i = 0; i < 8; ++i) H.inline_off[i] = i < nu ? (int32_t)uni[i] : 0;
+    P.ug_val.resize(P.ug_val.size() + (size_t)(nu + ng) * kPlanSliceRows, 0.0);
+    P.ug_col.resize(P.ug_col.size() + (size_t)ng * kPlanSliceRows, 0);
+    double* v = P.ug_val.data() + H.val_ptr;
+    int32_t* c = P.ug_col.data() + H.col_ptr;
+    for (int l = 0; l < kPlanSliceRows; ++l) {
+      const int64_t row = s * kPlanSliceRows + l;
+      const int32_t len = row < nl ? P.row_len[row] : 0;
+      const int32_t self = (int32_t)std::min<int64_t>(row, std::max<int64_t>(nl - 1, 0));
+      int32_t g = 0;
+      for (int32_t p = 0; p < len; ++p) {
+        const int64_t e = base + (int64_t)p * kPlanSliceRows + l;
+        const int64_t d = (int64_t)P.col[e] - row;
+        const auto it = std::lower_bound(uni.begin(), uni.end(), d);
+        if (it != uni.end() && *it == d) {
+          v[(int64_t)(it - uni.begin()) * kPlanSliceRows + l] += P.val[e];
+          if (P.val[e] != 0.0) ++P.ug_uniform_entries;
+        } else {  // general entries keep their CSR order
+          v[(int64_t)(nu + g) * kPlanSliceRows + l] = P.val[e];
+          c[(int64_t)g * kPlanSliceRows + l] = P.col[e];
+          ++g;
+        }
+      }
+      for (; g < ng; ++g) c[(int64_t)g * kPlanSliceRows + l] = self;
+    }
+  }
+  if (P.ug_val.empty()) P.ug_val.push_back(0.0);
+  if (P.ug_col.empty()) P.ug_col.push_back(0);
+  if (P.ug_uoff.empty()) P.ug_uoff.push_back(0);
+}
+
 void require(bool ok, const char* msg) {
   if (!ok) throw std::invalid_argument(msg);
 }
@@ -197,9 +324,12 @@ HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<in
   std::iota(all.begin(), all.end(), 0);
   for (int64_t s = 0; s < nslices; ++s)
     (is_boundary[s] ? P.boundary : P.interior).push_back((int32_t)s);
-  P.tasks_all = build_tasks(all, P.slice_len);
-  P.tasks_interior = build_tasks(P.interior, P.slice_len);
-  P.tasks_boundary = build_tasks(P.boundary, P.slice_len);
+  build_ug(P);
+  std::vector<int32_t> ug_len(nslices);  // the fast kernels walk the compressed slices
+  for (int64_t s = 0; s < nslices; ++s) ug_len[s] = P.ug_slice[s].nu + P.ug_slice[s].ng;
+  P.tasks_all = build_tasks(all, ug_len);
+  P.tasks_interior = build_tasks(P.interior, ug_len);
+  P.tasks_boundary = build_tasks(P.boundary, ug_len);
   P.short_rows = std::all_of(P.tasks_all.begin(), P.tasks_all.end(),
                              [](const PlanTask& t) { return t.warps_per_slice == 1; });
   return P;

@@ -22,6 +22,19 @@ struct PlanTask {  // mirrors SliceTask (flz_internal.hpp)
   int32_t slice[kPlanTaskWarps];
 };
 
+// Per-slice header of the index-compressed ("UG") layout the fast kernels read: the first
+// `nu` positions of a slice are UNIFORM (every lane's column is its own row + uoff[p], one
+// int32 per position instead of 32), the remaining `ng` positions are GENERAL (one int32 per
+// lane).  Values are [nu + ng][32] doubles; padding entries have value 0 and are skipped.
+struct PlanUgSlice {
+  int64_t val_ptr;   // element offset into ug_val
+  int64_t col_ptr;   // element offset into ug_col (general positions only)
+  int32_t uoff_ptr;  // offset into ug_uoff
+  int32_t nu, ng;
+  int32_t reserved;
+  int32_t inline_off[8];  // the first offsets again: one 64-byte load serves short slices
+};
+
 struct HostPlan {
   // partition
   int rank = 0, nranks = 1;
@@ -37,6 +50,11 @@ struct HostPlan {
   std::vector<int32_t> interior, boundary;  // slice ids
   std::vector<PlanTask> tasks_all, tasks_interior, tasks_boundary;
   bool short_rows = false;
+  // index-compressed copy of the same slices (same rows, same permutation)
+  std::vector<PlanUgSlice> ug_slice;
+  std::vector<double> ug_val;
+  std::vector<int32_t> ug_col, ug_uoff;
+  int64_t ug_uniform_entries = 0;   // true nonzeros stored at uniform positions
   // halo: sorted unique remote global columns; slot h lives at row nl + h of a gather source
   std::vector<int64_t> halo;
   std::vector<int64_t> need_off, need_cnt;  // per owner rank: run of `halo` it must send us

@@ -74,7 +74,13 @@ __device__ __forceinline__ int ld_stream_s32(const int* p) {
 // sm_100: a whole padded row = one sector = ONE L1 tag lookup per lane instead of three),
 // otherwise scalar 8-byte loads.
 template <int R, int S, bool READONLY>
-__device__ __forceinline__ void load_row(const double* Y, int64_t row, double (&out)[R]) {
+__device__ __forceinline__ void load_row(const double* Y, int64_t ldy, int64_t row,
+                                         double (&out)[R]) {
+  if constexpr (S == 0) {  // planar: column k of the block is Y + k*ldy
+#pragma unroll
+    for (int k = 0; k < R; ++k) out[k] = READONLY ? __ldg(Y + k * ldy + row) : Y[k * ldy + row];
+    return;
+  }
   const double* p = Y + row * S;
   if constexpr (S == 4) {
     double a, b, c, d;
@@ -102,8 +108,13 @@ __device__ __forceinline__ void load_row(const double* Y, int64_t row, double (&
 // Predicated gather of one block row: zeros when !on (no branch, so the loads of a batch
 // stay independent and in flight together).
 template <int R, int S>
-__device__ __forceinline__ void gather_row(const double* __restrict__ Y, int64_t row, bool on,
-                                           double (&out)[R]) {
+__device__ __forceinline__ void gather_row(const double* __restrict__ Y, int64_t ldy, int64_t row,
+                                           bool on, double (&out)[R]) {
+  if constexpr (S == 0) {
+#pragma unroll
+    for (int k = 0; k < R; ++k) out[k] = on ? __ldg(Y + k * ldy + row) : 0.0;
+    return;
+  }
   const double* p = Y + row * S;
   if constexpr (S == 4) {
     double a, b, c, d;
@@ -129,7 +140,13 @@ __device__ __forceinline__ void gather_row(const double* __restrict__ Y, int64_t
 }
 
 template <int R, int S>
-__device__ __forceinline__ void store_row(double* Y, int64_t row, const double (&v)[R]) {
+__device__ __forceinline__ void store_row(double* Y, int64_t ldy, int64_t row,
+                                          const double (&v)[R]) {
+  if constexpr (S == 0) {
+#pragma unroll
+    for (int k = 0; k < R; ++k) Y[k * ldy + row] = v[k];
+    return;
+  }
   double* p = Y + row * S;
   if constexpr (S == 4) {
     double w[4] = {0.0, 0.0, 0.0, 0.0};
@@ -145,33 +162,46 @@ __device__ __forceinline__ void store_row(double* Y, int64_t row, const double (
   }
 }
 
-// acc[k] += sum_{p in [p0,p1), p < len} val[p] * Y1[col[p]*S + k] for one lane (= one row).
-// Software pipelined: the (val, col) pairs of batch b+1 are requested before the gathers of
-// batch b are consumed, so a row of L entries costs about 1 + ceil(L/U) memory latencies
-// instead of 2*ceil(L/U); all loads of a batch are independent.
+// acc[k] += sum over positions [p0, p1) of one compressed slice for one lane (= one row).
+// Positions [0, nu) are uniform: the column is row + uoff[p] (offsets fetched 32 at a time,
+// one per lane, and broadcast by shuffle), clamped into the block because lanes that do not
+// hold the offset carry a zero value there; positions [nu, nu + ng) are general (padding: zero
+// value, own row as column).  The gathers depend only on the index stream, never on the
+// values.  Software pipelined: the values (and columns) of batch b+1 are requested before the
+// gathers of batch b are consumed; all loads of a batch are independent.
 template <int R, int S, int U>
-__device__ __forceinline__ void accumulate_range(const double* __restrict__ val,
-                                                 const int* __restrict__ col, int len, int p0,
-                                                 int p1, const double* __restrict__ Y1,
-                                                 double (&acc)[R]) {
+__device__ __forceinline__ void ug_accumulate(const SellView& A, const UgSlice& H, int lane,
+                                              int64_t row, int p0, int p1,
+                                              const double* __restrict__ Y1, int64_t ldy,
+                                              double (&acc)[R]) {
+  const double* __restrict__ val = A.ug_val + H.val_ptr + lane;
+  const int32_t* __restrict__ col = A.ug_col + H.col_ptr + lane - (int64_t)H.nu * kSliceRows;
+  const int32_t* __restrict__ uoff = A.ug_uoff + H.uoff_ptr;
+  const int nu = H.nu;
+  const int cmax = (int)A.ncols - 1;
+  int myoff = p0 + lane < nu ? __ldg(uoff + p0 + lane) : 0;
+  // (value, column) of position `pos`; pos is warp-uniform
+  auto fetch = [&](int pos, double& v, int& c) {
+    const bool ok = pos < p1;
+    v = ok ? ld_stream_f64(val + (int64_t)pos * kSliceRows) : 0.0;
+    if (pos < nu) {
+      const int q = pos - p0;
+      if (q > 0 && (q & 31) == 0) myoff = pos + lane < nu ? __ldg(uoff + pos + lane) : 0;
+      c = min(max((int)row + __shfl_sync(0xffffffffu, myoff, q & 31), 0), cmax);
+    } else {
+      c = ok ? ld_stream_s32(col + (int64_t)pos * kSliceRows) : 0;
+    }
+  };
   double v[U], vn[U];
   int c[U], cn[U];
 #pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const bool ok = p0 + u < p1;
-    v[u] = ok ? ld_stream_f64(val + (int64_t)(p0 + u) * kSliceRows) : 0.0;
-    c[u] = ok ? ld_stream_s32(col + (int64_t)(p0 + u) * kSliceRows) : 0;
-  }
+  for (int u = 0; u < U; ++u) fetch(p0 + u, v[u], c[u]);
   for (int p = p0; p < p1; p += U) {
 #pragma unroll
-    for (int u = 0; u < U; ++u) {  // next batch of the matrix stream
-      const bool ok = p + U + u < p1;
-      vn[u] = ok ? ld_stream_f64(val + (int64_t)(p + U + u) * kSliceRows) : 0.0;
-      cn[u] = ok ? ld_stream_s32(col + (int64_t)(p + U + u) * kSliceRows) : 0;
-    }
+    for (int u = 0; u < U; ++u) fetch(p + U + u, vn[u], cn[u]);
     double g[U][R];
 #pragma unroll
-    for (int u = 0; u < U; ++u) gather_row<R, S>(Y1, c[u], p + u < len && p + u < p1, g[u]);
+    for (int u = 0; u < U; ++u) gather_row<R, S>(Y1, ldy, c[u], p + u < p1, g[u]);
 #pragma unroll
     for (int u = 0; u < U; ++u)
 #pragma unroll
@@ -182,6 +212,19 @@ __device__ __forceinline__ void accumulate_range(const double* __restrict__ val,
       c[u] = cn[u];
     }
   }
+}
+
+__device__ __forceinline__ UgSlice load_ug_header(const UgSlice* __restrict__ h) {
+  const int4 a = __ldg(reinterpret_cast<const int4*>(h));
+  const int4 b = __ldg(reinterpret_cast<const int4*>(h) + 1);
+  UgSlice H{};
+  H.val_ptr = (int64_t)(((uint64_t)(uint32_t)a.y << 32) | (uint32_t)a.x);
+  H.col_ptr = (int64_t)(((uint64_t)(uint32_t)a.w << 32) | (uint32_t)a.z);
+  H.uoff_ptr = b.x;
+  H.nu = b.y;
+  H.ng = b.z;
+  H.reserved = b.w;
+  return H;
 }
 
 // ---------------------------------------------------------------- exact / simple kernel
@@ -206,30 +249,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 #pragma unroll
   for (int k = 0; k < R; ++k) acc[k] = 0.0;
   int p = 0;
-  if constexpr (!EXACT) {
-    // short-row fast path (stencils, <= 24 entries per row): four entries of every row in
-    // flight before the dependent gathers; measured best for 5..7-point stencils
-    for (; p + 4 <= L; p += 4) {
-      double v[4];
-      int c[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        v[u] = ld_stream_f64(val + (int64_t)(p + u) * kSliceRows);
-        c[u] = ld_stream_s32(col + (int64_t)(p + u) * kSliceRows);
-      }
-      double g[4][R];
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int k = 0; k < R; ++k) g[u][k] = (p + u < len) ? Y1[(int64_t)c[u] * R + k] : 0.0;
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (p + u < len) {
-#pragma unroll
-          for (int k = 0; k < R; ++k) acc[k] = fma(v[u], g[u][k], acc[k]);
-        }
-    }
-  }
   for (; p < L; ++p) {
     const double v = ld_stream_f64(val + (int64_t)p * kSliceRows);
     const int c = ld_stream_s32(col + (int64_t)p * kSliceRows);
@@ -257,55 +276,33 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
   }
 }
 
-// ------------------------------------------------------------------------ fast kernel
+// ----------------------------------------------------------------------- fast kernels
+// Epilogue shared by the fast kernels: own-row operands were requested before the matrix
+// stream so that they are in flight together with it.
 template <int R, int S, int MODE>
-__global__ void __launch_bounds__(kTaskWarps * 32, 4)
-    clenshaw_step_tasks(SellView A, double s1, double s2, double b,
-                        const double* __restrict__ Y1, double* __restrict__ Y2,
-                        const double* __restrict__ X, int64_t ldx, double* __restrict__ Out,
-                        int64_t ldo) {
-  __shared__ double part[kTaskWarps][R][32];
-  const SliceTask task = A.tasks[blockIdx.x];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int W = task.warps_per_slice;
-  const int sub = warp / W, piece = warp - sub * W;
-  const bool active = sub < task.count;
+__device__ __forceinline__ void load_own(const SellView& A, int64_t row, const double* Y1,
+                                         const double* Y2, int64_t ldy,
+                                         const double* __restrict__ X,
+                                         int64_t ldx, double (&y1o)[R], double (&y2o)[R],
+                                         double (&xo)[R]) {
+#pragma unroll
+  for (int k = 0; k < R; ++k) y1o[k] = y2o[k] = xo[k] = 0.0;
+  if constexpr (MODE != 2) {
+    if (row < A.nl) {
+      load_row<R, S, true>(Y1, ldy, row, y1o);
+      load_row<R, S, false>(Y2, ldy, row, y2o);
+#pragma unroll
+      for (int k = 0; k < R; ++k) xo[k] = __ldg(X + (int64_t)k * ldx + row);
+    }
+  }
+}
 
-  double acc[R], y1o[R], y2o[R], xo[R];
-#pragma unroll
-  for (int k = 0; k < R; ++k) acc[k] = y1o[k] = y2o[k] = xo[k] = 0.0;
-  int64_t row = 0;
-  if (active) {
-    const int64_t slice = task.slice[sub];
-    row = slice * kSliceRows + lane;
-    if constexpr (MODE != 2) {  // own-row operands of the epilogue: requested up front
-      if (piece == 0 && row < A.nl) {
-        load_row<R, S, true>(Y1, row, y1o);
-        load_row<R, S, false>(Y2, row, y2o);
-#pragma unroll
-        for (int k = 0; k < R; ++k) xo[k] = __ldg(X + (int64_t)k * ldx + row);
-      }
-    }
-    const int len = A.row_len[row];
-    const int L = A.slice_len[slice];
-    const int chunk = (L + W - 1) / W;
-    const int p0 = piece * chunk, p1 = min(L, p0 + chunk);
-    const int64_t base = A.slice_ptr[slice] + lane;
-    accumulate_range<R, S, kBatch>(A.val + base, A.col + base, len, p0, p1, Y1, acc);
-  }
-  if (W > 1) {  // uniform across the CTA
-    if (active && piece > 0) {
-#pragma unroll
-      for (int k = 0; k < R; ++k) part[warp][k][lane] = acc[k];
-    }
-    __syncthreads();
-    if (active && piece == 0) {
-      for (int q = 1; q < W; ++q)
-#pragma unroll
-        for (int k = 0; k < R; ++k) acc[k] += part[warp + q][k][lane];
-    }
-  }
-  if (!active || piece != 0 || row >= A.nl) return;
+template <int R, int S, int MODE>
+__device__ __forceinline__ void finish_row(int64_t row, double s1, double s2, double b,
+                                           const double (&acc)[R], const double (&y1o)[R],
+                                           const double (&y2o)[R], const double (&xo)[R],
+                                           double* Y2, int64_t ldy, double* __restrict__ Out,
+                                           int64_t ldo) {
   if constexpr (MODE == 2) {
 #pragma unroll
     for (int k = 0; k < R; ++k) Out[(int64_t)k * ldo + row] = acc[k];
@@ -314,7 +311,7 @@ __global__ void __launch_bounds__(kTaskWarps * 32, 4)
 #pragma unroll
     for (int k = 0; k < R; ++k) o[k] = combine<false>(s1, acc[k], s2, y1o[k], y2o[k], b, xo[k]);
     if constexpr (MODE == 0) {
-      store_row<R, S>(Y2, row, o);
+      store_row<R, S>(Y2, ldy, row, o);
     } else {
 #pragma unroll
       for (int k = 0; k < R; ++k) Out[(int64_t)k * ldo + row] = o[k];
@@ -322,16 +319,127 @@ __global__ void __launch_bounds__(kTaskWarps * 32, 4)
   }
 }
 
+// Short slices (stencils): one warp per slice; a CTA walks a contiguous range of slices so
+// that the block rows gathered by one slice are still in L1 for its neighbours.  The slice
+// descriptor (header + the first kUgInline uniform offsets) is one coalesced 64-byte load;
+// values and gathers of a batch are then all independent, so a slice costs two dependent
+// memory round trips (descriptor, then everything else).
+template <int R, int S, int MODE, int U>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+    clenshaw_step_ug_warp(SellView A, int slices_per_cta, double s1, double s2, double b,
+                          const double* __restrict__ Y1, double* __restrict__ Y2, int64_t ldy,
+                          const double* __restrict__ X, int64_t ldx, double* __restrict__ Out,
+                          int64_t ldo) {
+  static_assert(sizeof(UgSlice) == 64, "descriptor is 16 words");
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t first = (int64_t)blockIdx.x * slices_per_cta;
+  const int64_t last = min(A.nslices, first + slices_per_cta);
+  const int cmax = (int)A.ncols - 1;
+  for (int64_t w = first + warp; w < last; w += kWarpsPerBlock) {
+    const int64_t slice = A.slice_ids ? (int64_t)A.slice_ids[w] : w;
+    const int word = __ldg(reinterpret_cast<const int*>(A.ug + slice) + (lane & 15));
+    const int64_t row = slice * kSliceRows + lane;
+    double acc[R], y1o[R], y2o[R], xo[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) acc[k] = 0.0;
+    load_own<R, S, MODE>(A, row, Y1, Y2, ldy, X, ldx, y1o, y2o, xo);
+    const int64_t val_ptr = (int64_t)(((uint64_t)(uint32_t)__shfl_sync(0xffffffffu, word, 1) << 32) |
+                                      (uint32_t)__shfl_sync(0xffffffffu, word, 0));
+    const int nu = __shfl_sync(0xffffffffu, word, 5);
+    const int ng = __shfl_sync(0xffffffffu, word, 6);
+    const double* __restrict__ val = A.ug_val + val_ptr + lane;
+    int p = 0;
+    if (nu <= kUgInline) {  // offsets are in the descriptor
+      for (; p < nu; p += U) {
+        double v[U], g[U][R];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const bool ok = p + u < nu;
+          v[u] = ok ? ld_stream_f64(val + (int64_t)(p + u) * kSliceRows) : 0.0;
+          const int d = __shfl_sync(0xffffffffu, word, 8 + ((p + u) & (kUgInline - 1)));
+          gather_row<R, S>(Y1, ldy, min(max((int)row + d, 0), cmax), ok, g[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int k = 0; k < R; ++k) acc[k] = fma(v[u], g[u][k], acc[k]);
+      }
+      p = nu;  // the last batch was predicated, not overrun
+    }
+    if (p < nu + ng) {  // long offset lists and general positions
+      UgSlice H{};
+      H.val_ptr = val_ptr;
+      H.col_ptr = (int64_t)(((uint64_t)(uint32_t)__shfl_sync(0xffffffffu, word, 3) << 32) |
+                            (uint32_t)__shfl_sync(0xffffffffu, word, 2));
+      H.uoff_ptr = __shfl_sync(0xffffffffu, word, 4);
+      H.nu = nu;
+      H.ng = ng;
+      ug_accumulate<R, S, 4>(A, H, lane, row, p, nu + ng, Y1, ldy, acc);
+    }
+    if (row < A.nl) finish_row<R, S, MODE>(row, s1, s2, b, acc, y1o, y2o, xo, Y2, ldy, Out, ldo);
+  }
+}
+
+// Long slices: CTAs of 8 warps walk a contiguous range of a host-built task list; a task
+// gives each of its slices 1, 2, 4 or 8 warps, whose partial sums meet in shared memory in
+// a fixed order (deterministic).
+template <int R, int S, int MODE>
+__global__ void __launch_bounds__(kTaskWarps * 32, 3)
+    clenshaw_step_ug_tasks(SellView A, int tasks_per_cta, double s1, double s2, double b,
+                           const double* __restrict__ Y1, double* __restrict__ Y2, int64_t ldy,
+                           const double* __restrict__ X, int64_t ldx, double* __restrict__ Out,
+                           int64_t ldo) {
+  __shared__ double part[kTaskWarps][R][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t t0 = (int64_t)blockIdx.x * tasks_per_cta;
+  const int64_t t1 = min(A.ntasks, t0 + tasks_per_cta);
+  for (int64_t t = t0; t < t1; ++t) {
+    const SliceTask task = A.tasks[t];
+    const int W = task.warps_per_slice;
+    const int sub = warp / W, piece = warp - sub * W;
+    const bool active = sub < task.count;
+    double acc[R], y1o[R], y2o[R], xo[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) acc[k] = y1o[k] = y2o[k] = xo[k] = 0.0;
+    int64_t row = 0;
+    if (active) {
+      const int64_t slice = task.slice[sub];
+      const UgSlice H = load_ug_header(A.ug + slice);
+      row = slice * kSliceRows + lane;
+      if (piece == 0) load_own<R, S, MODE>(A, row, Y1, Y2, ldy, X, ldx, y1o, y2o, xo);
+      const int L = H.nu + H.ng;
+      const int chunk = (((L + W - 1) / W) + kBatch - 1) / kBatch * kBatch;
+      const int p0 = piece * chunk, p1 = min(L, p0 + chunk);
+      if (p0 < p1) ug_accumulate<R, S, kBatch>(A, H, lane, row, p0, p1, Y1, ldy, acc);
+    }
+    if (W > 1) {  // uniform across the CTA
+      if (active && piece > 0) {
+#pragma unroll
+        for (int k = 0; k < R; ++k) part[warp][k][lane] = acc[k];
+      }
+      __syncthreads();
+      if (active && piece == 0) {
+        for (int q = 1; q < W; ++q)
+#pragma unroll
+          for (int k = 0; k < R; ++k) acc[k] += part[warp + q][k][lane];
+      }
+      if (t + 1 < t1) __syncthreads();  // `part` is reused by the next task
+    }
+    if (active && piece == 0 && row < A.nl)
+      finish_row<R, S, MODE>(row, s1, s2, b, acc, y1o, y2o, xo, Y2, ldy, Out, ldo);
+  }
+}
+
 // Y1[i*S+k] = scale * X[k*ldx+i], k < R; pad entries (R <= k < S) are zeroed
 template <int R, int S>
 __global__ void interleave_kernel(int64_t nl, double scale, const double* __restrict__ X,
-                                  int64_t ldx, double* __restrict__ Y1) {
+                                  int64_t ldx, double* __restrict__ Y1, int64_t ldy) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nl) return;
   double v[R];
 #pragma unroll
   for (int k = 0; k < R; ++k) v[k] = __dmul_rn(scale, X[(int64_t)k * ldx + i]);
-  store_row<R, S>(Y1, i, v);
+  store_row<R, S>(Y1, ldy, i, v);
 }
 
 template <int S>
@@ -344,6 +452,16 @@ __global__ void pack_rows_kernel(int64_t count, const int32_t* __restrict__ rows
   for (int k = 0; k < S; ++k) buf[s * S + k] = Y1[r * S + k];
 }
 
+// planar blocks: buf[k*count + s] = Y1[k*ldy + rows[s]]
+__global__ void pack_rows_planar_kernel(int64_t count, int R, const int32_t* __restrict__ rows,
+                                        const double* __restrict__ Y1, int64_t ldy,
+                                        double* __restrict__ buf) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= count) return;
+  const int64_t r = rows[s];
+  for (int k = 0; k < R; ++k) buf[(int64_t)k * count + s] = Y1[(int64_t)k * ldy + r];
+}
+
 template <bool EXACT>
 __global__ void combine_kernel(int64_t n, double s1, double s2, double b,
                                const double* __restrict__ w, const double* __restrict__ y1,
@@ -354,49 +472,70 @@ __global__ void combine_kernel(int64_t n, double s1, double s2, double b,
 }
 
 template <int R, int MODE>
-void launch_simple(flz_ctx* ctx, const SellView& A, bool exact, double s1, double s2, double b,
+void launch_simple(flz_ctx* ctx, const SellView& A, double s1, double s2, double b,
                    const double* Y1, double* Y2, const double* X, int64_t ldx, double* Out,
                    int64_t ldo) {
   const unsigned grid = (unsigned)((A.nslices + kWarpsPerBlock - 1) / kWarpsPerBlock);
   if (grid == 0) return;
-  if (exact)
-    clenshaw_step_sell<R, MODE, true><<<grid, kWarpsPerBlock * 32, 0, ctx->stream>>>(
-        A, s1, s2, b, Y1, Y2, X, ldx, Out, ldo);
-  else
-    clenshaw_step_sell<R, MODE, false><<<grid, kWarpsPerBlock * 32, 0, ctx->stream>>>(
-        A, s1, s2, b, Y1, Y2, X, ldx, Out, ldo);
+  clenshaw_step_sell<R, MODE, true><<<grid, kWarpsPerBlock * 32, 0, ctx->stream>>>(
+      A, s1, s2, b, Y1, Y2, X, ldx, Out, ldo);
   ctx->launches++;
 }
 
+#ifndef FLZ_K1_UB
+#define FLZ_K1_UB 4
+#endif
+#ifndef FLZ_K1_SLICES_PER_CTA
+#define FLZ_K1_SLICES_PER_CTA 4
+#endif
+#ifndef FLZ_K1_TASKS_PER_CTA
+#define FLZ_K1_TASKS_PER_CTA 1
+#endif
+
 template <int R, int S, int MODE>
-void launch_tasks(flz_ctx* ctx, const SellView& A, double s1, double s2, double b,
-                  const double* Y1, double* Y2, const double* X, int64_t ldx, double* Out,
-                  int64_t ldo) {
-  if (A.ntasks == 0) return;
-  clenshaw_step_tasks<R, S, MODE><<<(unsigned)A.ntasks, kTaskWarps * 32, 0, ctx->stream>>>(
-      A, s1, s2, b, Y1, Y2, X, ldx, Out, ldo);
+void launch_ug(flz_ctx* ctx, const SellView& A, double s1, double s2, double b, const double* Y1,
+               double* Y2, int64_t ldy, const double* X, int64_t ldx, double* Out, int64_t ldo) {
+  if (A.short_rows) {
+    if (A.nslices == 0) return;
+    const int spc = ctx->k1_slices_per_cta > 0 ? ctx->k1_slices_per_cta : FLZ_K1_SLICES_PER_CTA;
+    const unsigned grid = (unsigned)((A.nslices + spc - 1) / spc);
+    if ((ctx->k1_batch > 0 ? ctx->k1_batch : FLZ_K1_UB) >= 8)
+      clenshaw_step_ug_warp<R, S, MODE, 8><<<grid, kWarpsPerBlock * 32, 0, ctx->stream>>>(
+          A, spc, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo);
+    else
+      clenshaw_step_ug_warp<R, S, MODE, 4><<<grid, kWarpsPerBlock * 32, 0, ctx->stream>>>(
+          A, spc, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo);
+  } else {
+    if (A.ntasks == 0) return;
+    const int tpc = ctx->k1_tasks_per_cta > 0 ? ctx->k1_tasks_per_cta : FLZ_K1_TASKS_PER_CTA;
+    const unsigned grid = (unsigned)((A.ntasks + tpc - 1) / tpc);
+    clenshaw_step_ug_tasks<R, S, MODE>
+        <<<grid, kTaskWarps * 32, 0, ctx->stream>>>(A, tpc, s1, s2, b, Y1, Y2, ldy, X, ldx, Out,
+                                                    ldo);
+  }
   ctx->launches++;
 }
 
 template <int R, int S>
 void launch_rs(flz_ctx* ctx, const SellView& A, StepMode mode, bool exact, double s1, double s2,
-               double b, const double* Y1, double* Y2, const double* X, int64_t ldx, double* Out,
-               int64_t ldo) {
-  const bool fast = !exact && A.tasks != nullptr && !(A.short_rows && S == R);
-  if (!fast && S != R)
-    throw ApiError(FLZ_EINVAL, "clenshaw step: a padded row stride needs the fast path");
+               double b, const double* Y1, double* Y2, int64_t ldy, const double* X, int64_t ldx,
+               double* Out, int64_t ldo) {
+  if constexpr (S != R) {
+    if (exact)
+      throw ApiError(FLZ_EINVAL, "clenshaw step: exact mode needs interleaved blocks, stride R");
+  }
   switch (mode) {
     case StepMode::step:
-      if (fast) launch_tasks<R, S, 0>(ctx, A, s1, s2, b, Y1, Y2, X, ldx, Out, ldo);
-      else launch_simple<R, 0>(ctx, A, exact, s1, s2, b, Y1, Y2, X, ldx, Out, ldo);
+      if (!exact) launch_ug<R, S, 0>(ctx, A, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo);
+      else if constexpr (S == R) launch_simple<R, 0>(ctx, A, s1, s2, b, Y1, Y2, X, ldx, Out, ldo);
       break;
     case StepMode::final:
-      if (fast) launch_tasks<R, S, 1>(ctx, A, s1, s2, b, Y1, Y2, X, ldx, Out, ldo);
-      else launch_simple<R, 1>(ctx, A, exact, s1, s2, b, Y1, Y2, X, ldx, Out, ldo);
+      if (!exact) launch_ug<R, S, 1>(ctx, A, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo);
+      else if constexpr (S == R) launch_simple<R, 1>(ctx, A, s1, s2, b, Y1, Y2, X, ldx, Out, ldo);
       break;
     case StepMode::plain:
-      if (fast) launch_tasks<R, S, 2>(ctx, A, s1, s2, b, Y1, Y2, X, ldx, Out, ldo);
-      else launch_simple<R, 2>(ctx, A, exact, s1, s2, b, Y1, Y2, X, ldx, Out, ldo);
+      if (!exact) launch_ug<R, S, 2>(ctx, A, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo);
+      else if constexpr (S == R) launch_simple<R, 2>(ctx, A, s1, s2, b, Y1, Y2, X, ldx, Out, ldo);
       break;
   }
 }
@@ -405,44 +544,49 @@ void launch_rs(flz_ctx* ctx, const SellView& A, StepMode mode, bool exact, doubl
 
 void launch_clenshaw_step(flz_ctx* ctx, const SellView& A, int R, int S, StepMode mode, bool exact,
                           double s1, double s2, double b, const double* Y1, double* Y2,
-                          const double* X, int64_t ldx, double* Out, int64_t ldo) {
+                          int64_t ldy, const double* X, int64_t ldx, double* Out, int64_t ldo) {
+#define FLZ_K1_CASE(RR, SS)                                                                  \
+  case RR * 10 + SS:                                                                         \
+    launch_rs<RR, SS>(ctx, A, mode, exact, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo);        \
+    break;
   switch (R * 10 + S) {
-    case 11: launch_rs<1, 1>(ctx, A, mode, exact, s1, s2, b, Y1, Y2, X, ldx, Out, ldo); break;
-    case 22: launch_rs<2, 2>(ctx, A, mode, exact, s1, s2, b, Y1, Y2, X, ldx, Out, ldo); break;
-    case 33: launch_rs<3, 3>(ctx, A, mode, exact, s1, s2, b, Y1, Y2, X, ldx, Out, ldo); break;
-    case 34: launch_rs<3, 4>(ctx, A, mode, exact, s1, s2, b, Y1, Y2, X, ldx, Out, ldo); break;
-    case 44: launch_rs<4, 4>(ctx, A, mode, exact, s1, s2, b, Y1, Y2, X, ldx, Out, ldo); break;
+    FLZ_K1_CASE(1, 1) FLZ_K1_CASE(2, 2) FLZ_K1_CASE(3, 3) FLZ_K1_CASE(3, 4) FLZ_K1_CASE(4, 4)
+    FLZ_K1_CASE(1, 0) FLZ_K1_CASE(2, 0) FLZ_K1_CASE(3, 0) FLZ_K1_CASE(4, 0)
     default: throw ApiError(FLZ_EINVAL, "clenshaw step: unsupported (columns, stride) pair");
   }
+#undef FLZ_K1_CASE
   FLZ_CUDA(cudaGetLastError());
 }
 
 void launch_interleave(flz_ctx* ctx, int64_t nl, int R, int S, double scale, const double* X,
-                       int64_t ldx, double* Y1) {
+                       int64_t ldx, double* Y1, int64_t ldy) {
   if (nl == 0) return;
   const unsigned grid = (unsigned)((nl + 255) / 256);
+#define FLZ_IL_CASE(RR, SS)                                                                  \
+  case RR * 10 + SS:                                                                         \
+    interleave_kernel<RR, SS><<<grid, 256, 0, ctx->stream>>>(nl, scale, X, ldx, Y1, ldy);    \
+    break;
   switch (R * 10 + S) {
-    case 11: interleave_kernel<1, 1><<<grid, 256, 0, ctx->stream>>>(nl, scale, X, ldx, Y1); break;
-    case 22: interleave_kernel<2, 2><<<grid, 256, 0, ctx->stream>>>(nl, scale, X, ldx, Y1); break;
-    case 33: interleave_kernel<3, 3><<<grid, 256, 0, ctx->stream>>>(nl, scale, X, ldx, Y1); break;
-    case 34: interleave_kernel<3, 4><<<grid, 256, 0, ctx->stream>>>(nl, scale, X, ldx, Y1); break;
-    case 44: interleave_kernel<4, 4><<<grid, 256, 0, ctx->stream>>>(nl, scale, X, ldx, Y1); break;
+    FLZ_IL_CASE(1, 1) FLZ_IL_CASE(2, 2) FLZ_IL_CASE(3, 3) FLZ_IL_CASE(3, 4) FLZ_IL_CASE(4, 4)
+    FLZ_IL_CASE(1, 0) FLZ_IL_CASE(2, 0) FLZ_IL_CASE(3, 0) FLZ_IL_CASE(4, 0)
     default: throw ApiError(FLZ_EINVAL, "interleave: unsupported (columns, stride) pair");
   }
+#undef FLZ_IL_CASE
   ctx->launches++;
   FLZ_CUDA(cudaGetLastError());
 }
 
-void launch_pack_rows(flz_ctx* ctx, cudaStream_t stream, int64_t count, int S,
+void launch_pack_rows(flz_ctx* ctx, cudaStream_t stream, int64_t count, int R, int S, int64_t ldy,
                       const int32_t* rows, const double* Y1, double* buf) {
   if (count == 0) return;
   const unsigned grid = (unsigned)((count + 255) / 256);
   switch (S) {
+    case 0: pack_rows_planar_kernel<<<grid, 256, 0, stream>>>(count, R, rows, Y1, ldy, buf); break;
     case 1: pack_rows_kernel<1><<<grid, 256, 0, stream>>>(count, rows, Y1, buf); break;
     case 2: pack_rows_kernel<2><<<grid, 256, 0, stream>>>(count, rows, Y1, buf); break;
     case 3: pack_rows_kernel<3><<<grid, 256, 0, stream>>>(count, rows, Y1, buf); break;
     case 4: pack_rows_kernel<4><<<grid, 256, 0, stream>>>(count, rows, Y1, buf); break;
-    default: throw ApiError(FLZ_EINVAL, "pack: row stride must be 1..4");
+    default: throw ApiError(FLZ_EINVAL, "pack: row stride must be 0..4");
   }
   ctx->launches++;
   FLZ_CUDA(cudaGetLastError());

@@ -81,6 +81,11 @@ class Context:
     def set_exact(self, exact: bool):
         check(lib().flz_ctx_set_exact(self.handle, int(exact)))
 
+    def set_tuning(self, slices_per_cta=0, tasks_per_cta=0, batch=0):
+        """Launch-shape knobs of the fused Clenshaw-step kernels (0 = default)."""
+        check(lib().flz_ctx_set_tuning(self.handle, int(slices_per_cta), int(tasks_per_cta),
+                                       int(batch)))
+
     @property
     def launches(self) -> int:
         return int(lib().flz_ctx_launch_count(self.handle))
@@ -143,9 +148,12 @@ class DeviceMatrix:
     def stats(self):
         a, b, c, e = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
         sigma = lib().flz_matrix_stats(self.handle, C.byref(a), C.byref(b), C.byref(c), C.byref(e))
+        mb, ue = C.c_int64(), C.c_int64()
+        check(lib().flz_matrix_layout(self.handle, C.byref(mb), C.byref(ue)))
         return {"stored": a.value, "slices": b.value, "halo_rows": c.value,
                 "boundary_slices": e.value, "sigma": sigma, "nnz": self.nnz,
-                "fill": a.value / max(self.nnz, 1)}
+                "fill": a.value / max(self.nnz, 1), "matrix_bytes": mb.value,
+                "uniform_entries": ue.value}
 
     def close(self):
         if getattr(self, "handle", None):

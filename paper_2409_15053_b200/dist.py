@@ -78,6 +78,45 @@ class HaloPlan:
         a["col"], a["val"] = a["col"][: i["stored"]], a["val"][: i["stored"]]
         return a
 
+    def ug_arrays(self):
+        """Index-compressed layout (descriptors, values, general columns, uniform offsets)."""
+        sizes = np.zeros(5, np.int64)
+        vp = lambda a: a.ctypes.data_as(C.c_void_p)
+        check(lib().flz_plan_ug(self.handle, vp(sizes), None, None, None, None))
+        desc = np.zeros((max(int(sizes[0]), 1), 16), np.int32)
+        val = np.zeros(max(int(sizes[1]), 1), np.float64)
+        col = np.zeros(max(int(sizes[2]), 1), np.int32)
+        uoff = np.zeros(max(int(sizes[3]), 1), np.int32)
+        check(lib().flz_plan_ug(self.handle, vp(sizes), vp(desc), vp(val), vp(col), vp(uoff)))
+        return dict(desc=desc[: int(sizes[0])], val=val, col=col, uoff=uoff,
+                    uniform_entries=int(sizes[4]))
+
+    def ug_product(self, x):
+        """y = A x evaluated from the index-compressed layout exactly as the fast kernels walk
+        it (host-side check of the layout; x is indexed by permuted local row / halo slot)."""
+        u = self.ug_arrays()
+        nl = self.info["rows_local"]
+        ncols = nl + self.info["halo_rows"]
+        y = np.zeros(len(u["desc"]) * 32)
+        lanes = np.arange(32)
+        for s, d in enumerate(u["desc"]):
+            val_ptr = int(np.array(d[0:2]).view(np.int64)[0])
+            col_ptr = int(np.array(d[2:4]).view(np.int64)[0])
+            uoff_ptr, nu, ng = int(d[4]), int(d[5]), int(d[6])
+            rows = s * 32 + lanes
+            acc = np.zeros(32)
+            for p in range(nu):
+                off = int(u["uoff"][uoff_ptr + p])
+                if p < 8:
+                    assert off == int(d[8 + p])
+                c = np.clip(rows + off, 0, ncols - 1)
+                acc += u["val"][val_ptr + p * 32: val_ptr + p * 32 + 32] * x[c]
+            for q in range(ng):
+                c = u["col"][col_ptr + q * 32: col_ptr + q * 32 + 32]
+                acc += u["val"][val_ptr + (nu + q) * 32: val_ptr + (nu + q) * 32 + 32] * x[c]
+            y[rows] = acc
+        return y[:nl]
+
     def __del__(self):
         try:
             lib().flz_plan_destroy(self.handle)

@@ -25,10 +25,31 @@ def bench(name, csr, r, m=50, sigma=0, check=True):
     bytes_step = 12 * nnz + 4 * (n + 1) + 32 * n * r
     gbs = 4 * m * bytes_step / (ms * 1e-3) / 1e9
     st = A.stats()
+    stride = 4 if (r == 3 and nnz >= 16 * n) else r
+    if os.environ.get("FLZ_K1_LAYOUT", "")[:1] == "p":
+        stride = r
+    moved = st["matrix_bytes"] + 8 * n * (3 * stride + r)
     print(f"{name:28s} n={n:8d} nnz/row={nnz/n:5.1f} r={r} fill={st['fill']:.3f} sigma={st['sigma']:6d} "
-          f"{ms/4/m*1e3:7.1f} us/step {gbs:7.0f} GB/s ({100*gbs/PEAK:5.1f}% of measured peak) fast-vs-exact {err:.1e}", flush=True)
+          f"uniform={st['uniform_entries']/nnz:5.1%} moved/formula={moved/bytes_step:.3f} "
+          f"{ms/4/m*1e3:7.1f} us/step {gbs:7.0f} GB/s ({100*gbs/PEAK:5.1f}% of measured peak; moved bytes "
+          f"{4*m*moved/(ms*1e-3)/1e9:6.0f} GB/s) fast-vs-exact {err:.1e}", flush=True)
+    return ms / 4 / m * 1e3
 
 which = sys.argv[1] if len(sys.argv) > 1 else "all"
+if which == "sweep":
+    lap = M.laplacian3d(100)
+    pk = M.parsec_like()
+    for batch in (4, 8):
+        for spc in (4, 16, 64):
+            ctx.set_tuning(spc, 0, batch)
+            print("batch", batch, "slices_per_cta", spc, end=": ")
+            bench("lap3d-100 r=3", lap, 3, check=False)
+    ctx.set_tuning(0, 0)
+    for tpc in (1, 2, 4, 8):
+        ctx.set_tuning(0, tpc)
+        print("tasks_per_cta", tpc, end=": ")
+        bench("parsec r=3", pk, 3, check=False)
+    sys.exit(0)
 lap = M.laplacian3d(100)
 bench("lap3d-100 r=3", lap, 3)
 bench("lap3d-100 r=1", lap, 1)
