@@ -124,11 +124,13 @@ int flz_plan_arrays(const flz_plan* plan, int32_t* perm, int64_t* slice_ptr, int
                     int32_t* boundary, int32_t* send_rows, int64_t* give_off, int64_t* give_cnt,
                     int64_t* need_off);
 /* index-compressed layout of the plan (what the fast kernels stream), for host-side checks:
- * sizes[5] = {slices, values, general columns, uniform offsets, uniform true entries};
- * descriptors: 16 int32 per slice {val_ptr lo/hi, col_ptr lo/hi, uoff_ptr, nu, ng, 0,
- * first 8 offsets}.  Any pointer may be NULL. */
+ * sizes[8] = {slices (main + rest), values, general columns, uniform offsets, uniform true
+ * entries, rest slices, split mode, interior rest slices};
+ * descriptors: 16 int32 per slice {val_ptr lo/hi, col_ptr lo/hi, uoff_ptr, nu, ng, flags,
+ * first 8 offsets}; rest_rows: 32 int32 per rest slice (row of each lane, -1 = unused).
+ * Any pointer may be NULL. */
 int flz_plan_ug(const flz_plan* plan, int64_t* sizes, int32_t* descriptors, double* ug_val,
-                int32_t* ug_col, int32_t* ug_uoff);
+                int32_t* ug_col, int32_t* ug_uoff, int32_t* rest_rows);
 
 /* Global matvec counter: speig::matvec_count()/reset (sparse.hpp:74-79).  One count per
  * vector-column product, so a fused r-column block product adds r. */

@@ -91,7 +91,7 @@ _SIGS = {
     "flz_plan_need": (i64, [vp, i32, vp]),
     "flz_plan_set_give": (i32, [vp, i32, i64, i64p]),
     "flz_plan_arrays": (i32, [vp] + [vp] * 12),
-    "flz_plan_ug": (i32, [vp, vp, vp, vp, vp, vp]),
+    "flz_plan_ug": (i32, [vp, vp, vp, vp, vp, vp, vp]),
     "flz_matvec_count": (u64, []),
     "flz_reset_matvec_count": (None, []),
     "flz_spmm": (i32, [vp, vp, vp, i32, vp, i32]),

@@ -107,10 +107,18 @@ void ensure_exact_arrays(const flz_matrix* A) {
 SellView make_view(const flz_matrix* A, const SliceTask* tasks, int64_t ntasks,
                    const int32_t* slice_ids, int64_t nslices) {
   ensure_exact_arrays(A);
-  return SellView{tasks,        ntasks,     A->short_rows, A->slice_ptr.p, A->slice_len.p,
+  return SellView{tasks,        ntasks,     A->short_rows, A->lean, A->slice_ptr.p, A->slice_len.p,
                   A->row_len.p, A->col.p,   A->val.p,      slice_ids,      nslices,
                   A->nl,        A->ug.p,    A->ug_val.p,   A->ug_col.p,    A->ug_uoff.p,
-                  A->nl + A->nhalo};
+                  A->nl + A->nhalo, A->rest_rows.p, A->nslices,   A->w.p};
+}
+// rest launches (SPLIT mode): task lists over the rest slices
+SellView view_rest(const flz_matrix* A, int which) {
+  const DevBuf<SliceTask>& t =
+      which == 0 ? A->tasks_rest_all : (which == 1 ? A->tasks_rest_interior : A->tasks_rest_boundary);
+  const int64_t nt =
+      which == 0 ? A->nt_rest_all : (which == 1 ? A->nt_rest_interior : A->nt_rest_boundary);
+  return make_view(A, t.p, nt, nullptr, A->nrest);
 }
 SellView view_all(const flz_matrix* A) {
   return make_view(A, A->tasks_all.p, A->nt_all, nullptr, A->nslices);
@@ -132,6 +140,9 @@ void ensure_workspaces(const flz_matrix* A) {
     A->y1.reserve_zero(need, ctx->stream);
     A->y2.reserve_zero(need, ctx->stream);
   }
+  // rows without a rest part keep W = 0 for ever; rest rows are overwritten every product
+  if (A->nrest > 0 && A->w.count == 0)
+    A->w.reserve_zero((size_t)A->nl * kMaxFuse + 8, ctx->stream);
 }
 
 // Halo exchange of the gather source Y1: pack the rows the peers reference, send/recv on the
@@ -175,15 +186,25 @@ void sell_step(const flz_matrix* A, int R, int S, StepMode mode, double s1, doub
                double* Y1, double* Y2, const double* X, int64_t ldx, double* Out, int64_t ldo) {
   flz_ctx* ctx = A->ctx;
   const int64_t ldy = planar_ld(A);
+  // SPLIT mode: the rest slices leave their partial sums in W before the main slices of the
+  // same rows run (the exact-mode kernel reads the unsplit CSR-order arrays instead)
+  auto rest = [&](int which, int64_t ntasks) {
+    if (ctx->exact || ntasks == 0) return;
+    launch_clenshaw_step(ctx, view_rest(A, which), R, S, StepMode::rest, false, 0.0, 0.0, 0.0, Y1,
+                         Y2, ldy, nullptr, 0, nullptr, 0);
+  };
   if (ctx->nranks == 1 || A->peers.empty()) {
+    rest(0, A->nt_rest_all);
     launch_clenshaw_step(ctx, view_all(A), R, S, mode, ctx->exact, s1, s2, b, Y1, Y2, ldy, X, ldx,
                          Out, ldo);
     return;
   }
   halo_begin(A, R, S, Y1);
+  rest(1, A->nt_rest_interior);
   launch_clenshaw_step(ctx, view_interior(A), R, S, mode, ctx->exact, s1, s2, b, Y1, Y2, ldy, X,
                        ldx, Out, ldo);
   FLZ_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_halo_done, 0));
+  rest(2, A->nt_rest_boundary);
   launch_clenshaw_step(ctx, view_boundary(A), R, S, mode, ctx->exact, s1, s2, b, Y1, Y2, ldy, X,
                        ldx, Out, ldo);
 }
@@ -481,6 +502,7 @@ static void upload_plan(flz_ctx* ctx, HostPlan& P, flz_matrix* A) {
   A->nhalo = (int64_t)P.halo.size();
   A->sigma = P.sigma;
   A->short_rows = P.short_rows;
+  A->lean = P.lean;
   A->n_interior = (int64_t)P.interior.size();
   A->n_boundary = (int64_t)P.boundary.size();
   A->nt_all = (int64_t)P.tasks_all.size();
@@ -508,6 +530,10 @@ static void upload_plan(flz_ctx* ctx, HostPlan& P, flz_matrix* A) {
   A->ug_bytes = (int64_t)(P.ug_val.size() * 8 + P.ug_col.size() * 4 + P.ug_uoff.size() * 4 +
                           P.ug_slice.size() * sizeof(UgSlice));
   A->ug_uniform_entries = P.ug_uniform_entries;
+  A->split = P.split;
+  A->nrest = P.nrest;
+  up(A->rest_rows, P.rest_rows);
+  A->ug_bytes += (int64_t)P.rest_rows.size() * 4;
   up(A->perm, P.perm);
   up(A->iperm, P.iperm);
   up(A->interior, P.interior);
@@ -520,6 +546,15 @@ static void upload_plan(flz_ctx* ctx, HostPlan& P, flz_matrix* A) {
       FLZ_CUDA(cudaMemcpyAsync(buf.p, host.data(), host.size() * sizeof(PlanTask),
                                cudaMemcpyHostToDevice, ctx->stream));
   };
+  A->nt_rest_all = (int64_t)P.tasks_rest_all.size();
+  A->nt_rest_interior = (int64_t)P.tasks_rest_interior.size();
+  A->nt_rest_boundary = (int64_t)P.tasks_rest_boundary.size();
+  A->tasks_rest_all.reserve(std::max<size_t>(P.tasks_rest_all.size(), 1));
+  A->tasks_rest_interior.reserve(std::max<size_t>(P.tasks_rest_interior.size(), 1));
+  A->tasks_rest_boundary.reserve(std::max<size_t>(P.tasks_rest_boundary.size(), 1));
+  up_tasks(A->tasks_rest_all, P.tasks_rest_all);
+  up_tasks(A->tasks_rest_interior, P.tasks_rest_interior);
+  up_tasks(A->tasks_rest_boundary, P.tasks_rest_boundary);
   up_tasks(A->tasks_all, P.tasks_all);
   up_tasks(A->tasks_interior, P.tasks_interior);
   up_tasks(A->tasks_boundary, P.tasks_boundary);
@@ -698,7 +733,7 @@ int flz_plan_arrays(const flz_plan* plan, int32_t* perm, int64_t* slice_ptr, int
 }
 
 int flz_plan_ug(const flz_plan* plan, int64_t* sizes, int32_t* descriptors, double* ug_val,
-                int32_t* ug_col, int32_t* ug_uoff) {
+                int32_t* ug_col, int32_t* ug_uoff, int32_t* rest_rows) {
   if (!plan) return FLZ_EINVAL;
   const HostPlan& P = plan->P;
   if (sizes) {
@@ -707,7 +742,11 @@ int flz_plan_ug(const flz_plan* plan, int64_t* sizes, int32_t* descriptors, doub
     sizes[2] = (int64_t)P.ug_col.size();
     sizes[3] = (int64_t)P.ug_uoff.size();
     sizes[4] = P.ug_uniform_entries;
+    sizes[5] = P.nrest;
+    sizes[6] = P.split ? 1 : 0;
+    sizes[7] = (int64_t)P.rest_interior.size();
   }
+  if (rest_rows) std::copy(P.rest_rows.begin(), P.rest_rows.end(), rest_rows);
   if (descriptors && !P.ug_slice.empty())
     std::memcpy(descriptors, P.ug_slice.data(), P.ug_slice.size() * sizeof(PlanUgSlice));
   if (ug_val) std::copy(P.ug_val.begin(), P.ug_val.end(), ug_val);

@@ -162,6 +162,13 @@ struct flz_matrix {
   flz::DevBuf<int32_t> ug_col, ug_uoff;
   int64_t ug_bytes = 0;             // matrix bytes one fast step streams
   int64_t ug_uniform_entries = 0;
+  // SPLIT mode (host/plan.hpp): rest slices follow the main ones in `ug`
+  bool split = false;
+  int64_t nrest = 0;
+  flz::DevBuf<int32_t> rest_rows;   // [nrest*32] row of every rest lane, -1 = unused
+  flz::DevBuf<flz::SliceTask> tasks_rest_all, tasks_rest_interior, tasks_rest_boundary;
+  int64_t nt_rest_all = 0, nt_rest_interior = 0, nt_rest_boundary = 0;
+  mutable flz::DevBuf<double> w;    // partial sums of the rest slices, (nl x kMaxFuse) rows
   flz::DevBuf<int32_t> perm;        // [nl] new -> old
   flz::DevBuf<int32_t> iperm;       // [nl] old -> new
   flz::DevBuf<int32_t> interior;    // slice ids without halo references
@@ -169,7 +176,8 @@ struct flz_matrix {
   int64_t n_interior = 0, n_boundary = 0;
   flz::DevBuf<flz::SliceTask> tasks_all, tasks_interior, tasks_boundary;
   int64_t nt_all = 0, nt_interior = 0, nt_boundary = 0;
-  bool short_rows = false;          // max slice length <= 24: single-warp tasks only
+  bool short_rows = false;          // every main slice fits one warp (single-warp tasks only)
+  bool lean = false;                // ... with at most kUgInline uniform positions each
   std::vector<int32_t> h_perm, h_iperm;
   // halo exchange plan (distributed only)
   struct Peer {
@@ -219,6 +227,7 @@ struct SellView {
   const SliceTask* tasks;    // task list of the fast kernel (nullptr: one warp per slice)
   int64_t ntasks;
   bool short_rows;           // every slice fits one warp: the one-warp-per-slice kernel is best
+  bool lean;                 // ... and has <= kUgInline uniform positions (stencils)
   const int64_t* slice_ptr;
   const int32_t* slice_len;
   const int32_t* row_len;
@@ -233,9 +242,14 @@ struct SellView {
   const int32_t* ug_col;
   const int32_t* ug_uoff;
   int64_t ncols;             // rows of a gather source: local rows + halo rows
+  // SPLIT mode: rest launches map lanes to rows through rest_rows (slice ids start at
+  // rest_base) and leave their sums in W; main launches add W where a slice is flagged
+  const int32_t* rest_rows;
+  int64_t rest_base;
+  double* W;
 };
 
-enum class StepMode { step, final, plain };
+enum class StepMode { step, final, plain, rest };
 
 // One fused Clenshaw step (or plain SpMM) for R in [1, kMaxFuse] block columns.  Layout of
 // the blocks Y1/Y2: S > 0 interleaved with row stride S (S == R, or S == 4 for R == 3 on

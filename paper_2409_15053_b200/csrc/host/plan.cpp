@@ -3,6 +3,7 @@
 #include "plan.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <numeric>
 #include <stdexcept>
 #include <string>
@@ -12,7 +13,7 @@ namespace flz {
 namespace {
 
 #ifndef FLZ_K1_T
-#define FLZ_K1_T 24  // target entries per warp before a slice is split over more warps
+#define FLZ_K1_T 48  // target entries per warp before a slice is split over more warps
 #endif
 
 int warps_for(int32_t len) {
@@ -86,7 +87,8 @@ struct OffsetCounter {  // open-addressing counter of the offsets of one slice
   }
 };
 
-void build_ug(HostPlan& P) {
+// returns the number of spilled entries
+int64_t build_ug(HostPlan& P, const std::vector<uint8_t>& is_boundary, bool allow_spill) {
   const int64_t nslices = P.nslices, nl = P.nl;
   P.ug_slice.assign(nslices, PlanUgSlice{});
   P.ug_val.clear();
@@ -104,6 +106,15 @@ void build_ug(HostPlan& P) {
   // identical offset lists (every interior slice of a stencil) share one copy
   std::vector<int64_t> last_uni;
   int32_t last_uoff_ptr = -1;
+  // spilled leftovers (SPLIT mode): per rest row its entries, pooled
+  struct RestRow {
+    int32_t row;
+    int64_t begin, end;
+    uint8_t boundary;
+  };
+  std::vector<RestRow> rest;
+  std::vector<int32_t> rest_col;
+  std::vector<double> rest_val;
   for (int64_t s = 0; s < nslices; ++s) {
     const int32_t L = P.slice_len[s];
     const int64_t base = P.slice_ptr[s];
@@ -132,19 +143,34 @@ void build_ug(HostPlan& P) {
         glen[l] = g;
         ng = std::max(ng, g);
       }
-      // keep the split only when it moves fewer bytes than the plain slice
+      // keep the uniform positions only when they move fewer bytes than the plain slice
       const int64_t bytes_plain = (int64_t)12 * kPlanSliceRows * L;
       const int64_t bytes_ug = (int64_t)8 * kPlanSliceRows * ((int64_t)uni.size() + ng) +
                                4 * (int64_t)uni.size() + (int64_t)4 * kPlanSliceRows * ng;
-      if (bytes_ug >= bytes_plain) uni.clear();
+      if (!P.split && bytes_ug >= bytes_plain) uni.clear();
     }
-    if (uni.empty()) ng = L;
+    if (uni.empty()) {
+      ng = L;
+      for (int l = 0; l < kPlanSliceRows; ++l) {
+        const int64_t row = s * kPlanSliceRows + l;
+        glen[l] = row < nl ? P.row_len[row] : 0;
+      }
+    }
+    // SPLIT mode: ragged leftovers leave the slice
+    bool spill = false;
+    if (P.split && allow_spill && ng > 2) {
+      int64_t gsum = 0;
+      for (int l = 0; l < kPlanSliceRows; ++l) gsum += glen[l];
+      spill = 4 * gsum < (int64_t)3 * ng * kPlanSliceRows;  // < 75 % of the padded rectangle
+    }
+    if (spill) ng = 0;
     const int32_t nu = (int32_t)uni.size();
     PlanUgSlice& H = P.ug_slice[s];
     H.val_ptr = (int64_t)P.ug_val.size();
     H.col_ptr = (int64_t)P.ug_col.size();
     H.nu = nu;
     H.ng = ng;
+    H.reserved = spill ? 1 : 0;
     if (nu > 0 && uni == last_uni) {
       H.uoff_ptr = last_uoff_ptr;
     } else {
@@ -172,18 +198,146 @@ void build_ug(HostPlan& P) {
         if (it != uni.end() && *it == d) {
           v[(int64_t)(it - uni.begin()) * kPlanSliceRows + l] += P.val[e];
           if (P.val[e] != 0.0) ++P.ug_uniform_entries;
+        } else if (spill) {
+          if (g == 0) rest.push_back({(int32_t)row, (int64_t)rest_col.size(), 0, is_boundary[s]});
+          rest_col.push_back(P.col[e]);
+          rest_val.push_back(P.val[e]);
+          rest.back().end = (int64_t)rest_col.size();
+          ++g;
         } else {  // general entries keep their CSR order
           v[(int64_t)(nu + g) * kPlanSliceRows + l] = P.val[e];
           c[(int64_t)g * kPlanSliceRows + l] = P.col[e];
           ++g;
         }
       }
-      for (; g < ng; ++g) c[(int64_t)g * kPlanSliceRows + l] = self;
+      if (!spill)
+        for (; g < ng; ++g) c[(int64_t)g * kPlanSliceRows + l] = self;
+    }
+  }
+  // ---- rest slices: interior rows first, then boundary rows.  Rows with the same column
+  // extent (first, last leftover column) — e.g. the rows of one dense non-local block — are
+  // kept together, 32 per slice; a column most lanes of such a slice hold becomes ONE shared
+  // position (bit 1 of the flags: the position's int32 is an absolute column, every lane
+  // reads the same block row — a broadcast instead of 32 scattered gathers).  Rows of small
+  // groups are pooled and sorted by descending length in windows of 4096 (stable).
+  P.nrest = 0;
+  P.rest_rows.clear();
+  P.rest_interior.clear();
+  P.rest_boundary.clear();
+  if (!rest.empty()) {
+    constexpr int kMinGroup = 16;      // rows a column-extent group needs to get own slices
+    OffsetCounter colcount(cap);
+    std::vector<int32_t> order, pooled, shared;
+    std::vector<int32_t> lanes;        // rest-row ids of the slice being emitted
+    auto emit = [&](int pass, bool share) {
+      const int h = (int)lanes.size();
+      shared.clear();
+      if (share) {
+        colcount.clear();
+        for (int32_t id : lanes)
+          for (int64_t e = rest[id].begin; e < rest[id].end; ++e) colcount.add(rest_col[e]);
+        const int need = std::max(2, (3 * h + 4) / 5);  // >= 60 % of the lanes
+        for (int32_t hh : colcount.used)
+          if (colcount.cnt[hh] >= need) shared.push_back((int32_t)colcount.key[hh]);
+        std::sort(shared.begin(), shared.end());
+      }
+      const int32_t nu = (int32_t)shared.size();
+      int32_t ng = 0;
+      for (int32_t id : lanes) {
+        int32_t g = 0;
+        for (int64_t e = rest[id].begin; e < rest[id].end; ++e)
+          if (!std::binary_search(shared.begin(), shared.end(), rest_col[e])) ++g;
+        ng = std::max(ng, g);
+      }
+      PlanUgSlice H{};
+      H.val_ptr = (int64_t)P.ug_val.size();
+      H.col_ptr = (int64_t)P.ug_col.size();
+      H.uoff_ptr = (int32_t)P.ug_uoff.size();
+      H.nu = nu;
+      H.ng = ng;
+      H.reserved = nu > 0 ? 2 : 0;
+      for (int i = 0; i < 8; ++i) H.inline_off[i] = i < nu ? shared[i] : 0;
+      P.ug_uoff.insert(P.ug_uoff.end(), shared.begin(), shared.end());
+      P.ug_val.resize(P.ug_val.size() + (size_t)(nu + ng) * kPlanSliceRows, 0.0);
+      P.ug_col.resize(P.ug_col.size() + (size_t)ng * kPlanSliceRows, 0);
+      double* v = P.ug_val.data() + H.val_ptr;
+      int32_t* c = P.ug_col.data() + H.col_ptr;
+      const int32_t fallback = rest[lanes[0]].row;
+      for (int l = 0; l < kPlanSliceRows; ++l) {
+        const bool on = l < h;
+        const RestRow* rr = on ? &rest[lanes[l]] : nullptr;
+        P.rest_rows.push_back(on ? rr->row : -1);
+        int32_t g = 0;
+        if (on)
+          for (int64_t e = rr->begin; e < rr->end; ++e) {
+            const auto it = std::lower_bound(shared.begin(), shared.end(), rest_col[e]);
+            if (it != shared.end() && *it == rest_col[e]) {
+              v[(int64_t)(it - shared.begin()) * kPlanSliceRows + l] = rest_val[e];
+            } else {
+              v[(int64_t)(nu + g) * kPlanSliceRows + l] = rest_val[e];
+              c[(int64_t)g * kPlanSliceRows + l] = rest_col[e];
+              ++g;
+            }
+          }
+        for (; g < ng; ++g) c[(int64_t)g * kPlanSliceRows + l] = on ? rr->row : fallback;
+      }
+      const int32_t id = (int32_t)(nslices + P.nrest);
+      (pass ? P.rest_boundary : P.rest_interior).push_back(id);
+      P.ug_slice.push_back(H);
+      ++P.nrest;
+      lanes.clear();
+    };
+    auto key_less = [&](int32_t a, int32_t b) {
+      const int32_t fa = rest_col[rest[a].begin], fb = rest_col[rest[b].begin];
+      if (fa != fb) return fa < fb;
+      const int32_t la = rest_col[rest[a].end - 1], lb = rest_col[rest[b].end - 1];
+      if (la != lb) return la < lb;
+      return rest[a].row < rest[b].row;
+    };
+    auto same_key = [&](int32_t a, int32_t b) {
+      return rest_col[rest[a].begin] == rest_col[rest[b].begin] &&
+             rest_col[rest[a].end - 1] == rest_col[rest[b].end - 1];
+    };
+    for (int pass = 0; pass < 2; ++pass) {
+      order.clear();
+      pooled.clear();
+      for (size_t i = 0; i < rest.size(); ++i)
+        if (rest[i].boundary == pass) order.push_back((int32_t)i);
+      std::sort(order.begin(), order.end(), key_less);
+      for (size_t g0 = 0; g0 < order.size();) {
+        size_t g1 = g0 + 1;
+        while (g1 < order.size() && same_key(order[g0], order[g1])) ++g1;
+        if ((int)(g1 - g0) >= kMinGroup) {
+          for (size_t i = g0; i < g1; ++i) {
+            lanes.push_back(order[i]);
+            if ((int)lanes.size() == kPlanSliceRows) emit(pass, true);
+          }
+          if (!lanes.empty()) emit(pass, true);
+        } else {
+          pooled.insert(pooled.end(), order.begin() + g0, order.begin() + g1);
+        }
+        g0 = g1;
+      }
+      std::sort(pooled.begin(), pooled.end(),
+                [&](int32_t a, int32_t b) { return rest[a].row < rest[b].row; });
+      constexpr size_t kWindow = 4096;
+      for (size_t w0 = 0; w0 < pooled.size(); w0 += kWindow) {
+        const size_t w1 = std::min(pooled.size(), w0 + kWindow);
+        std::stable_sort(pooled.begin() + w0, pooled.begin() + w1, [&](int32_t a, int32_t b) {
+          return rest[a].end - rest[a].begin > rest[b].end - rest[b].begin;
+        });
+      }
+      for (size_t i = 0; i < pooled.size(); ++i) {
+        lanes.push_back(pooled[i]);
+        if ((int)lanes.size() == kPlanSliceRows) emit(pass, false);
+      }
+      if (!lanes.empty()) emit(pass, false);
     }
   }
   if (P.ug_val.empty()) P.ug_val.push_back(0.0);
   if (P.ug_col.empty()) P.ug_col.push_back(0);
   if (P.ug_uoff.empty()) P.ug_uoff.push_back(0);
+  return (int64_t)rest_col.size();
 }
 
 void require(bool ok, const char* msg) {
@@ -222,9 +376,35 @@ HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<in
     require(col_idx[p0 + p] >= 0 && col_idx[p0 + p] < n_global,
             "plan: column index out of range");
 
+  // ---- SPLIT mode?  Count the nonzeros whose diagonal offset is shared by at least
+  // kUgMinLanes rows of their natural-order slice (global indices: a good estimate of what
+  // build_ug finds after the halo columns are renumbered).
+  P.split = false;
+  if (sigma <= 0 && nl > 0) {
+    int32_t max_len = 0;
+    for (int64_t i = 0; i < nl; ++i) max_len = std::max(max_len, len[i]);
+    size_t cap = 64;
+    while (cap < (size_t)max_len * kPlanSliceRows * 2) cap <<= 1;
+    OffsetCounter counter(cap);
+    int64_t uniform = 0;
+    for (int64_t i0 = 0; i0 < nl; i0 += kPlanSliceRows) {
+      counter.clear();
+      const int64_t i1 = std::min(nl, i0 + kPlanSliceRows);
+      for (int64_t i = i0; i < i1; ++i)
+        for (int64_t p = row_ptr[i]; p < row_ptr[i + 1]; ++p)
+          counter.add((int64_t)col_idx[p] - (P.row_begin + i));
+      for (int32_t h : counter.used)
+        if (counter.cnt[h] >= kUgMinLanes) uniform += counter.cnt[h];
+    }
+    P.split = 2 * uniform >= P.nnz;
+    if (const char* force = std::getenv("FLZ_SPLIT")) P.split = force[0] == '1';  // experiments
+  }
+
   // ---- sigma: smallest window whose padding overhead is <= 5 %
   int64_t chosen = sigma;
-  if (sigma <= 0) {
+  if (P.split) {
+    chosen = 1;  // natural order: uniform offsets only exist there
+  } else if (sigma <= 0) {
     const int64_t cands[] = {1, 256, 4096, 65536, std::max<int64_t>(nl, 1)};
     int64_t best_fill = -1;
     chosen = 1;
@@ -324,14 +504,26 @@ HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<in
   std::iota(all.begin(), all.end(), 0);
   for (int64_t s = 0; s < nslices; ++s)
     (is_boundary[s] ? P.boundary : P.interior).push_back((int32_t)s);
-  build_ug(P);
-  std::vector<int32_t> ug_len(nslices);  // the fast kernels walk the compressed slices
-  for (int64_t s = 0; s < nslices; ++s) ug_len[s] = P.ug_slice[s].nu + P.ug_slice[s].ng;
+  // a rest launch per product only pays when it carries a real share of the matrix
+  if (const int64_t spilled = build_ug(P, is_boundary, true);
+      spilled > 0 && 50 * spilled < P.nnz)
+    build_ug(P, is_boundary, false);
+  std::vector<int32_t> ug_len(nslices + P.nrest);  // the fast kernels walk the compressed slices
+  for (int64_t s = 0; s < nslices + P.nrest; ++s) ug_len[s] = P.ug_slice[s].nu + P.ug_slice[s].ng;
+  {
+    std::vector<int32_t> rest_all(P.rest_interior);
+    rest_all.insert(rest_all.end(), P.rest_boundary.begin(), P.rest_boundary.end());
+    P.tasks_rest_all = build_tasks(rest_all, ug_len);
+    P.tasks_rest_interior = build_tasks(P.rest_interior, ug_len);
+    P.tasks_rest_boundary = build_tasks(P.rest_boundary, ug_len);
+  }
   P.tasks_all = build_tasks(all, ug_len);
   P.tasks_interior = build_tasks(P.interior, ug_len);
   P.tasks_boundary = build_tasks(P.boundary, ug_len);
   P.short_rows = std::all_of(P.tasks_all.begin(), P.tasks_all.end(),
                              [](const PlanTask& t) { return t.warps_per_slice == 1; });
+  P.lean = P.short_rows;
+  for (int64_t s = 0; s < nslices && P.lean; ++s) P.lean = P.ug_slice[s].nu <= 8;
   return P;
 }
 

@@ -50,11 +50,26 @@ struct HostPlan {
   std::vector<int32_t> interior, boundary;  // slice ids
   std::vector<PlanTask> tasks_all, tasks_interior, tasks_boundary;
   bool short_rows = false;
+  bool lean = false;   // short_rows and every main slice has <= 8 uniform positions
   // index-compressed copy of the same slices (same rows, same permutation)
   std::vector<PlanUgSlice> ug_slice;
   std::vector<double> ug_val;
   std::vector<int32_t> ug_col, ug_uoff;
   int64_t ug_uniform_entries = 0;   // true nonzeros stored at uniform positions
+  // SPLIT mode (automatic sigma only; chosen when at least half of the nonzeros sit at
+  // uniform offsets in natural row order — measured on B200, the PARSEC-shaped matrices with
+  // 42 % uniform entries are still faster unsplit: 35 us vs 43 us per step): rows keep their natural order, main slices hold
+  // the uniform part (plus small balanced leftovers), ragged leftovers ("spilled" entries,
+  // e.g. dense non-local blocks) live in REST slices: general-position slices over the rows
+  // that have leftovers, regrouped by length.  Rest slices are appended to ug_slice after
+  // the nslices main ones; rest_rows maps their lanes to rows (-1: unused lane).  A main
+  // slice whose rows have rest parts has bit 0 of `reserved` set: it adds the partial sums
+  // the rest kernel left in the W workspace.
+  bool split = false;
+  int64_t nrest = 0;
+  std::vector<int32_t> rest_rows;                    // [nrest * 32]
+  std::vector<int32_t> rest_interior, rest_boundary; // slice ids (>= nslices)
+  std::vector<PlanTask> tasks_rest_all, tasks_rest_interior, tasks_rest_boundary;
   // halo: sorted unique remote global columns; slot h lives at row nl + h of a gather source
   std::vector<int64_t> halo;
   std::vector<int64_t> need_off, need_cnt;  // per owner rank: run of `halo` it must send us

@@ -564,7 +564,13 @@ EigenResult run_solve(const SparseSymMatrix& A, double alpha, double beta,
 
   const auto r = static_cast<std::size_t>(cfg.block_size);
   const auto max_cols = static_cast<std::size_t>(cfg.resolved_max_dim(A.dim()));
-  LanczosFactorization st(op, local_rows(init_block(A.dim(), r, cfg.seed), A.dim()), max_cols);
+  trace("solve: upload + bounds + filter", total);
+  const WallClock t_init;
+  DenseBlock start = local_rows(init_block(A.dim(), r, cfg.seed), A.dim());
+  trace("solve: init_block (host)", t_init);
+  const WallClock t_fact;
+  LanczosFactorization st(op, std::move(start), max_cols);
+  trace("solve: factorization setup", t_fact);
   const double norm_est = std::max(std::abs(bounds.lambda_min()), std::abs(bounds.lambda_max()));
 
   ExpandTimes times;
@@ -595,6 +601,7 @@ EigenResult run_solve(const SparseSymMatrix& A, double alpha, double beta,
     time_recover += rec.seconds();
   }
 
+  trace("solve: total", total);
   const std::uint64_t mv2 = matvec_count();
   SolveStats& s = result.stats;
   s.block_steps = static_cast<int>(st.block_count());

@@ -167,49 +167,80 @@ __device__ __forceinline__ void store_row(double* Y, int64_t ldy, int64_t row,
 // one per lane, and broadcast by shuffle), clamped into the block because lanes that do not
 // hold the offset carry a zero value there; positions [nu, nu + ng) are general (padding: zero
 // value, own row as column).  The gathers depend only on the index stream, never on the
-// values.  Software pipelined: the values (and columns) of batch b+1 are requested before the
-// gathers of batch b are consumed; all loads of a batch are independent.
+// values.  Two tight loops, each software pipelined: the values (and columns) of batch b+1
+// are requested before the gathers of batch b are consumed; all loads of a batch are
+// independent.
 template <int R, int S, int U>
 __device__ __forceinline__ void ug_accumulate(const SellView& A, const UgSlice& H, int lane,
                                               int64_t row, int p0, int p1,
                                               const double* __restrict__ Y1, int64_t ldy,
                                               double (&acc)[R]) {
   const double* __restrict__ val = A.ug_val + H.val_ptr + lane;
-  const int32_t* __restrict__ col = A.ug_col + H.col_ptr + lane - (int64_t)H.nu * kSliceRows;
-  const int32_t* __restrict__ uoff = A.ug_uoff + H.uoff_ptr;
-  const int nu = H.nu;
-  const int cmax = (int)A.ncols - 1;
-  int myoff = p0 + lane < nu ? __ldg(uoff + p0 + lane) : 0;
-  // (value, column) of position `pos`; pos is warp-uniform
-  auto fetch = [&](int pos, double& v, int& c) {
-    const bool ok = pos < p1;
-    v = ok ? ld_stream_f64(val + (int64_t)pos * kSliceRows) : 0.0;
-    if (pos < nu) {
-      const int q = pos - p0;
-      if (q > 0 && (q & 31) == 0) myoff = pos + lane < nu ? __ldg(uoff + pos + lane) : 0;
-      c = min(max((int)row + __shfl_sync(0xffffffffu, myoff, q & 31), 0), cmax);
-    } else {
-      c = ok ? ld_stream_s32(col + (int64_t)pos * kSliceRows) : 0;
-    }
-  };
   double v[U], vn[U];
-  int c[U], cn[U];
+  // ---- uniform positions [p0, pu1)
+  const int pu1 = min(p1, H.nu);
+  if (p0 < pu1) {
+    const int32_t* __restrict__ uoff = A.ug_uoff + H.uoff_ptr + lane;
+    const int cmax = (int)A.ncols - 1;
+    const int crow = (H.reserved & 2) ? 0 : (int)row;  // flag bit 1: absolute shared columns
+    int myoff = p0 + lane < pu1 ? __ldg(uoff + p0) : 0;
+    const double* vp = val + (int64_t)p0 * kSliceRows;
 #pragma unroll
-  for (int u = 0; u < U; ++u) fetch(p0 + u, v[u], c[u]);
-  for (int p = p0; p < p1; p += U) {
+    for (int u = 0; u < U; ++u) v[u] = p0 + u < pu1 ? ld_stream_f64(vp + u * kSliceRows) : 0.0;
+    for (int p = p0; p < pu1; p += U) {
+      vp += U * kSliceRows;
 #pragma unroll
-    for (int u = 0; u < U; ++u) fetch(p + U + u, vn[u], cn[u]);
-    double g[U][R];
+      for (int u = 0; u < U; ++u)
+        vn[u] = p + U + u < pu1 ? ld_stream_f64(vp + u * kSliceRows) : 0.0;
+      const int q = (p - p0) & 31;
+      if (q == 0 && p > p0) myoff = p + lane < pu1 ? __ldg(uoff + p) : 0;
+      double g[U][R];
 #pragma unroll
-    for (int u = 0; u < U; ++u) gather_row<R, S>(Y1, ldy, c[u], p + u < p1, g[u]);
+      for (int u = 0; u < U; ++u) {
+        const int c = min(max(crow + __shfl_sync(0xffffffffu, myoff, q + u), 0), cmax);
+        gather_row<R, S>(Y1, ldy, c, p + u < pu1, g[u]);
+      }
 #pragma unroll
-    for (int u = 0; u < U; ++u)
+      for (int u = 0; u < U; ++u)
 #pragma unroll
-      for (int k = 0; k < R; ++k) acc[k] = fma(v[u], g[u][k], acc[k]);
+        for (int k = 0; k < R; ++k) acc[k] = fma(v[u], g[u][k], acc[k]);
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = vn[u];
+    }
+  }
+  // ---- general positions [q0, p1)
+  const int q0 = max(p0, H.nu);
+  if (q0 < p1) {
+    const double* vp = val + (int64_t)q0 * kSliceRows;
+    const int32_t* cp = A.ug_col + H.col_ptr + lane + (int64_t)(q0 - H.nu) * kSliceRows;
+    int c[U], cn[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      v[u] = vn[u];
-      c[u] = cn[u];
+      const bool ok = q0 + u < p1;
+      v[u] = ok ? ld_stream_f64(vp + u * kSliceRows) : 0.0;
+      c[u] = ok ? ld_stream_s32(cp + u * kSliceRows) : 0;
+    }
+    for (int p = q0; p < p1; p += U) {
+      vp += U * kSliceRows;
+      cp += U * kSliceRows;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const bool ok = p + U + u < p1;
+        vn[u] = ok ? ld_stream_f64(vp + u * kSliceRows) : 0.0;
+        cn[u] = ok ? ld_stream_s32(cp + u * kSliceRows) : 0;
+      }
+      double g[U][R];
+#pragma unroll
+      for (int u = 0; u < U; ++u) gather_row<R, S>(Y1, ldy, c[u], p + u < p1, g[u]);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int k = 0; k < R; ++k) acc[k] = fma(v[u], g[u][k], acc[k]);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        v[u] = vn[u];
+        c[u] = cn[u];
+      }
     }
   }
 }
@@ -287,7 +318,7 @@ __device__ __forceinline__ void load_own(const SellView& A, int64_t row, const d
                                          double (&xo)[R]) {
 #pragma unroll
   for (int k = 0; k < R; ++k) y1o[k] = y2o[k] = xo[k] = 0.0;
-  if constexpr (MODE != 2) {
+  if constexpr (MODE != 2 && MODE != 3) {
     if (row < A.nl) {
       load_row<R, S, true>(Y1, ldy, row, y1o);
       load_row<R, S, false>(Y2, ldy, row, y2o);
@@ -319,13 +350,56 @@ __device__ __forceinline__ void finish_row(int64_t row, double s1, double s2, do
   }
 }
 
+// L2 prefetch of the own-row operands of the epilogue (streamed once: Y2 row, X entries);
+// the loads themselves are issued after the accumulation so that they hold no registers
+// while the gathers are in flight.
+template <int R, int S, int MODE>
+__device__ __forceinline__ void prefetch_own(const SellView& A, int64_t row, const double* Y2,
+                                             int64_t ldy, const double* X, int64_t ldx) {
+  if constexpr (MODE != 2 && MODE != 3) {
+    if (row < A.nl) {
+      if constexpr (S == 0) {
+#pragma unroll
+        for (int k = 0; k < R; ++k)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(Y2 + k * ldy + row));
+      } else {
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(Y2 + row * S));
+        if constexpr (S == 3) asm volatile("prefetch.global.L2 [%0];" ::"l"(Y2 + row * S + 2));
+      }
+#pragma unroll
+      for (int k = 0; k < R; ++k)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(X + (int64_t)k * ldx + row));
+    }
+  }
+}
+
+// SPLIT mode: partial sums the rest launch left for this row (kMaxFuse doubles per row)
+template <int R>
+__device__ __forceinline__ void add_rest(const SellView& A, int64_t row, double (&acc)[R]) {
+  if (row < A.nl) {
+#pragma unroll
+    for (int k = 0; k < R; ++k) acc[k] += A.W[row * kMaxFuse + k];
+  }
+}
+
 // Short slices (stencils): one warp per slice; a CTA walks a contiguous range of slices so
 // that the block rows gathered by one slice are still in L1 for its neighbours.  The slice
 // descriptor (header + the first kUgInline uniform offsets) is one coalesced 64-byte load;
 // values and gathers of a batch are then all independent, so a slice costs two dependent
 // memory round trips (descriptor, then everything else).
-template <int R, int S, int MODE, int U>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+//   LEAN: every slice has at most kUgInline uniform positions and a few general ones
+//   (stencils); the code then needs no offset lists and no software pipeline, which keeps the
+//   register count at 64 (eight CTAs per SM) — occupancy is what hides the latency of
+//   seven-position slices (measured, 100^3 Laplacian, 3 columns: 24 warps/SM 37 us, 28 warps
+//   29 us, 32 warps 27.7 us per step).
+#ifndef FLZ_K1_LEAN_CTAS
+#define FLZ_K1_LEAN_CTAS 8
+#endif
+#ifndef FLZ_K1_EARLY_OWN
+#define FLZ_K1_LATE_OWN 1  // own-row operands: L2 prefetch up front, loads after the gathers
+#endif
+template <int R, int S, int MODE, int U, bool LEAN>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, (LEAN && R <= 3) ? FLZ_K1_LEAN_CTAS : 1)
     clenshaw_step_ug_warp(SellView A, int slices_per_cta, double s1, double s2, double b,
                           const double* __restrict__ Y1, double* __restrict__ Y2, int64_t ldy,
                           const double* __restrict__ X, int64_t ldx, double* __restrict__ Out,
@@ -342,7 +416,12 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
     double acc[R], y1o[R], y2o[R], xo[R];
 #pragma unroll
     for (int k = 0; k < R; ++k) acc[k] = 0.0;
+#ifdef FLZ_K1_LATE_OWN
+    if constexpr (LEAN) prefetch_own<R, S, MODE>(A, row, Y2, ldy, X, ldx);
+    else load_own<R, S, MODE>(A, row, Y1, Y2, ldy, X, ldx, y1o, y2o, xo);
+#else
     load_own<R, S, MODE>(A, row, Y1, Y2, ldy, X, ldx, y1o, y2o, xo);
+#endif
     const int64_t val_ptr = (int64_t)(((uint64_t)(uint32_t)__shfl_sync(0xffffffffu, word, 1) << 32) |
                                       (uint32_t)__shfl_sync(0xffffffffu, word, 0));
     const int nu = __shfl_sync(0xffffffffu, word, 5);
@@ -366,7 +445,28 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
       }
       p = nu;  // the last batch was predicated, not overrun
     }
-    if (p < nu + ng) {  // long offset lists and general positions
+    if constexpr (LEAN) {
+      const int64_t col_ptr =
+          (int64_t)(((uint64_t)(uint32_t)__shfl_sync(0xffffffffu, word, 3) << 32) |
+                    (uint32_t)__shfl_sync(0xffffffffu, word, 2));
+      const int32_t* __restrict__ col = A.ug_col + col_ptr + lane;
+      for (int q = 0; q < ng; q += 4) {
+        double v[4], g[4][R];
+        int c[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const bool ok = q + u < ng;
+          v[u] = ok ? ld_stream_f64(val + (int64_t)(nu + q + u) * kSliceRows) : 0.0;
+          c[u] = ok ? ld_stream_s32(col + (int64_t)(q + u) * kSliceRows) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) gather_row<R, S>(Y1, ldy, c[u], q + u < ng, g[u]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int k = 0; k < R; ++k) acc[k] = fma(v[u], g[u][k], acc[k]);
+      }
+    } else if (p < nu + ng) {  // long offset lists and general positions
       UgSlice H{};
       H.val_ptr = val_ptr;
       H.col_ptr = (int64_t)(((uint64_t)(uint32_t)__shfl_sync(0xffffffffu, word, 3) << 32) |
@@ -374,8 +474,13 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
       H.uoff_ptr = __shfl_sync(0xffffffffu, word, 4);
       H.nu = nu;
       H.ng = ng;
-      ug_accumulate<R, S, 4>(A, H, lane, row, p, nu + ng, Y1, ldy, acc);
+      H.reserved = __shfl_sync(0xffffffffu, word, 7);
+      ug_accumulate<R, S, U>(A, H, lane, row, p, nu + ng, Y1, ldy, acc);
     }
+    if (__shfl_sync(0xffffffffu, word, 7) & 1) add_rest<R>(A, row, acc);
+#ifdef FLZ_K1_LATE_OWN
+    if constexpr (LEAN) load_own<R, S, MODE>(A, row, Y1, Y2, ldy, X, ldx, y1o, y2o, xo);
+#endif
     if (row < A.nl) finish_row<R, S, MODE>(row, s1, s2, b, acc, y1o, y2o, xo, Y2, ldy, Out, ldo);
   }
 }
@@ -384,7 +489,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 // gives each of its slices 1, 2, 4 or 8 warps, whose partial sums meet in shared memory in
 // a fixed order (deterministic).
 template <int R, int S, int MODE>
-__global__ void __launch_bounds__(kTaskWarps * 32, 3)
+#ifndef FLZ_K1_TASK_CTAS
+#define FLZ_K1_TASK_CTAS 3
+#endif
+__global__ void __launch_bounds__(kTaskWarps * 32, FLZ_K1_TASK_CTAS)
     clenshaw_step_ug_tasks(SellView A, int tasks_per_cta, double s1, double s2, double b,
                            const double* __restrict__ Y1, double* __restrict__ Y2, int64_t ldy,
                            const double* __restrict__ X, int64_t ldx, double* __restrict__ Out,
@@ -402,10 +510,17 @@ __global__ void __launch_bounds__(kTaskWarps * 32, 3)
 #pragma unroll
     for (int k = 0; k < R; ++k) acc[k] = y1o[k] = y2o[k] = xo[k] = 0.0;
     int64_t row = 0;
+    bool has_rest = false;
     if (active) {
       const int64_t slice = task.slice[sub];
       const UgSlice H = load_ug_header(A.ug + slice);
-      row = slice * kSliceRows + lane;
+      if constexpr (MODE == 3) {  // rest slice: lanes map to rows through rest_rows
+        const int r = A.rest_rows[(slice - A.rest_base) * kSliceRows + lane];
+        row = r < 0 ? A.nl : r;
+      } else {
+        row = slice * kSliceRows + lane;
+        has_rest = H.reserved & 1;
+      }
       if (piece == 0) load_own<R, S, MODE>(A, row, Y1, Y2, ldy, X, ldx, y1o, y2o, xo);
       const int L = H.nu + H.ng;
       const int chunk = (((L + W - 1) / W) + kBatch - 1) / kBatch * kBatch;
@@ -425,8 +540,15 @@ __global__ void __launch_bounds__(kTaskWarps * 32, 3)
       }
       if (t + 1 < t1) __syncthreads();  // `part` is reused by the next task
     }
-    if (active && piece == 0 && row < A.nl)
-      finish_row<R, S, MODE>(row, s1, s2, b, acc, y1o, y2o, xo, Y2, ldy, Out, ldo);
+    if (active && piece == 0 && row < A.nl) {
+      if constexpr (MODE == 3) {
+#pragma unroll
+        for (int k = 0; k < R; ++k) A.W[row * kMaxFuse + k] = acc[k];
+      } else {
+        if (has_rest) add_rest<R>(A, row, acc);
+        finish_row<R, S, MODE>(row, s1, s2, b, acc, y1o, y2o, xo, Y2, ldy, Out, ldo);
+      }
+    }
   }
 }
 
@@ -495,16 +617,23 @@ void launch_simple(flz_ctx* ctx, const SellView& A, double s1, double s2, double
 template <int R, int S, int MODE>
 void launch_ug(flz_ctx* ctx, const SellView& A, double s1, double s2, double b, const double* Y1,
                double* Y2, int64_t ldy, const double* X, int64_t ldx, double* Out, int64_t ldo) {
-  if (A.short_rows) {
+  bool warp_kernel = false;
+  if constexpr (MODE != 3) warp_kernel = A.short_rows;
+  if (warp_kernel) {
+    if constexpr (MODE != 3) {
     if (A.nslices == 0) return;
     const int spc = ctx->k1_slices_per_cta > 0 ? ctx->k1_slices_per_cta : FLZ_K1_SLICES_PER_CTA;
     const unsigned grid = (unsigned)((A.nslices + spc - 1) / spc);
-    if ((ctx->k1_batch > 0 ? ctx->k1_batch : FLZ_K1_UB) >= 8)
-      clenshaw_step_ug_warp<R, S, MODE, 8><<<grid, kWarpsPerBlock * 32, 0, ctx->stream>>>(
+    if (!A.lean)
+      clenshaw_step_ug_warp<R, S, MODE, 8, false><<<grid, kWarpsPerBlock * 32, 0, ctx->stream>>>(
+          A, spc, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo);
+    else if ((ctx->k1_batch > 0 ? ctx->k1_batch : FLZ_K1_UB) >= 8)
+      clenshaw_step_ug_warp<R, S, MODE, 8, true><<<grid, kWarpsPerBlock * 32, 0, ctx->stream>>>(
           A, spc, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo);
     else
-      clenshaw_step_ug_warp<R, S, MODE, 4><<<grid, kWarpsPerBlock * 32, 0, ctx->stream>>>(
+      clenshaw_step_ug_warp<R, S, MODE, 4, true><<<grid, kWarpsPerBlock * 32, 0, ctx->stream>>>(
           A, spc, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo);
+    }
   } else {
     if (A.ntasks == 0) return;
     const int tpc = ctx->k1_tasks_per_cta > 0 ? ctx->k1_tasks_per_cta : FLZ_K1_TASKS_PER_CTA;
@@ -532,6 +661,9 @@ void launch_rs(flz_ctx* ctx, const SellView& A, StepMode mode, bool exact, doubl
     case StepMode::final:
       if (!exact) launch_ug<R, S, 1>(ctx, A, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo);
       else if constexpr (S == R) launch_simple<R, 1>(ctx, A, s1, s2, b, Y1, Y2, X, ldx, Out, ldo);
+      break;
+    case StepMode::rest:
+      if (!exact) launch_ug<R, S, 3>(ctx, A, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo);
       break;
     case StepMode::plain:
       if (!exact) launch_ug<R, S, 2>(ctx, A, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo);

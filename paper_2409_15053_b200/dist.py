@@ -79,43 +79,77 @@ class HaloPlan:
         return a
 
     def ug_arrays(self):
-        """Index-compressed layout (descriptors, values, general columns, uniform offsets)."""
-        sizes = np.zeros(5, np.int64)
+        """Index-compressed layout (descriptors, values, general columns, uniform offsets,
+        rest rows); main slices come first, rest slices (SPLIT mode) after them."""
+        sizes = np.zeros(8, np.int64)
         vp = lambda a: a.ctypes.data_as(C.c_void_p)
-        check(lib().flz_plan_ug(self.handle, vp(sizes), None, None, None, None))
+        check(lib().flz_plan_ug(self.handle, vp(sizes), None, None, None, None, None))
         desc = np.zeros((max(int(sizes[0]), 1), 16), np.int32)
         val = np.zeros(max(int(sizes[1]), 1), np.float64)
         col = np.zeros(max(int(sizes[2]), 1), np.int32)
         uoff = np.zeros(max(int(sizes[3]), 1), np.int32)
-        check(lib().flz_plan_ug(self.handle, vp(sizes), vp(desc), vp(val), vp(col), vp(uoff)))
+        rest_rows = np.zeros(max(int(sizes[5]) * 32, 1), np.int32)
+        check(lib().flz_plan_ug(self.handle, vp(sizes), vp(desc), vp(val), vp(col), vp(uoff),
+                                vp(rest_rows)))
         return dict(desc=desc[: int(sizes[0])], val=val, col=col, uoff=uoff,
-                    uniform_entries=int(sizes[4]))
+                    uniform_entries=int(sizes[4]), nrest=int(sizes[5]), split=bool(sizes[6]),
+                    rest_interior=int(sizes[7]),
+                    rest_rows=rest_rows[: int(sizes[5]) * 32].reshape(-1, 32))
 
-    def ug_product(self, x):
+    def ug_product(self, x, which="all"):
         """y = A x evaluated from the index-compressed layout exactly as the fast kernels walk
-        it (host-side check of the layout; x is indexed by permuted local row / halo slot)."""
+        it (host-side check of the layout; x is indexed by permuted local row / halo slot).
+        which: "all", or ("interior" | "boundary") to evaluate only those main slices together
+        with the rest slices that must precede them; returns (y, rows computed)."""
         u = self.ug_arrays()
+        a = self.arrays()
         nl = self.info["rows_local"]
         ncols = nl + self.info["halo_rows"]
-        y = np.zeros(len(u["desc"]) * 32)
+        nmain = len(u["desc"]) - u["nrest"]
         lanes = np.arange(32)
-        for s, d in enumerate(u["desc"]):
+
+        def slice_sum(s, rows):
+            d = u["desc"][s]
             val_ptr = int(np.array(d[0:2]).view(np.int64)[0])
             col_ptr = int(np.array(d[2:4]).view(np.int64)[0])
             uoff_ptr, nu, ng = int(d[4]), int(d[5]), int(d[6])
-            rows = s * 32 + lanes
+            base = 0 if int(d[7]) & 2 else rows       # flag bit 1: absolute shared columns
             acc = np.zeros(32)
             for p in range(nu):
                 off = int(u["uoff"][uoff_ptr + p])
                 if p < 8:
                     assert off == int(d[8 + p])
-                c = np.clip(rows + off, 0, ncols - 1)
+                c = np.clip(base + off, 0, ncols - 1)
                 acc += u["val"][val_ptr + p * 32: val_ptr + p * 32 + 32] * x[c]
             for q in range(ng):
                 c = u["col"][col_ptr + q * 32: col_ptr + q * 32 + 32]
                 acc += u["val"][val_ptr + (nu + q) * 32: val_ptr + (nu + q) * 32 + 32] * x[c]
+            return acc
+
+        W = np.zeros(nl + 32)
+        if which == "all":
+            rest_ids = range(u["nrest"])
+            main_ids = range(nmain)
+        else:
+            ri = u["rest_interior"]
+            rest_ids = range(ri) if which == "interior" else range(ri, u["nrest"])
+            main_ids = a[which]
+        for t in rest_ids:
+            rows = u["rest_rows"][t]
+            acc = slice_sum(nmain + t, np.where(rows < 0, nl, rows))
+            assert not np.any(W[rows[rows >= 0]] != 0)      # a row sits in one rest slice only
+            W[rows[rows >= 0]] = acc[rows >= 0]
+        y = np.zeros(nmain * 32)
+        done = []
+        for s in main_ids:
+            rows = s * 32 + lanes
+            acc = slice_sum(s, rows)
+            if u["desc"][s][7] & 1:
+                acc += W[np.minimum(rows, nl + 31)]
             y[rows] = acc
-        return y[:nl]
+            done.extend(r for r in rows if r < nl)
+        self._w_rows_used = W
+        return (y[:nl], np.array(done, np.int64)) if which != "all" else y[:nl]
 
     def __del__(self):
         try:

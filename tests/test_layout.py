@@ -1,0 +1,111 @@
+"""The index-compressed matrix layout of the fast kernels (host/plan.cpp build_ug), checked on
+CPUs: HaloPlan.ug_product walks the descriptors exactly as the CUDA kernels do (uniform-offset
+positions with clamping, shared absolute columns of rest slices, general positions, the W
+hand-over from rest slices to flagged main slices) and must reproduce A x.  Covers the SPLIT
+mode (rest slices), the unsplit sigma-sorted mode and the row-partitioned case where interior
+slices run before the halo arrives."""
+import numpy as np
+import pytest
+
+from paper_2409_15053_b200 import matrices as M
+from paper_2409_15053_b200.dist import HaloPlan, uniform_starts
+
+
+def reference(csr, x):
+    n, rp, ci, va = csr
+    return M.csr_to_scipy(n, rp, ci, va) @ x
+
+
+CASES = {
+    "lap2d30": (lambda: M.laplacian2d(30), True),            # 30 does not divide 32: mixed slices
+    "lap3d12": (lambda: M.laplacian3d(12), True),
+    "lap3d20": (lambda: M.laplacian3d(20), True),
+    "aniso": (lambda: M.laplacian3d(9, (1.0, 0.5, 0.25)), True),
+    "rand500": (lambda: M.random_sparse_sym(500, 0.03, 1), False),   # nothing uniform: unsplit
+    "parsec7k": (lambda: M.parsec_like(radius=12.0, n_atoms=12), None),
+    "diag": (lambda: M.diag_matrix(np.arange(1.0, 41.0)), True),
+}
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_ug_layout_reproduces_product(name):
+    gen, want_split = CASES[name]
+    csr = gen()
+    n, rp, ci, va = csr
+    P = HaloPlan(n, 0, 1, [0, n], rp, ci, va)
+    u, a = P.ug_arrays(), P.arrays()
+    if want_split is not None:
+        assert u["split"] == want_split
+    if u["split"]:
+        assert np.array_equal(a["perm"], np.arange(n))       # natural row order
+    x = np.random.default_rng(3).standard_normal(n)
+    y = P.ug_product(x[a["perm"]])
+    want = reference(csr, x)[a["perm"]]
+    assert np.abs(y - want).max() <= 1e-13 * max(1.0, np.abs(want).max())
+    # stencils: (almost) every nonzero sits at a uniform position, 8 bytes instead of 12
+    if name.startswith("lap3d"):
+        assert u["uniform_entries"] >= 0.95 * len(va)
+        assert u["nrest"] == 0
+
+
+def test_forced_split_builds_rest_slices(monkeypatch):
+    """PARSEC-shaped matrix with the split forced on: ragged leftovers (dense non-local blocks)
+    go to rest slices, part of them as shared absolute columns; a row has one rest slice."""
+    monkeypatch.setenv("FLZ_SPLIT", "1")
+    csr = M.parsec_like(radius=14.0, n_atoms=10, ball_radius=3.25)
+    n, rp, ci, va = csr
+    P = HaloPlan(n, 0, 1, [0, n], rp, ci, va)
+    u = P.ug_arrays()
+    assert u["split"] and u["nrest"] > 0
+    nmain = len(u["desc"]) - u["nrest"]
+    assert (u["desc"][:nmain, 7] & 1).sum() > 0              # main slices that add W
+    rows = u["rest_rows"][u["rest_rows"] >= 0]
+    assert len(np.unique(rows)) == len(rows)
+    x = np.random.default_rng(4).standard_normal(n)
+    y = P.ug_product(x)
+    want = reference(csr, x)
+    assert np.abs(y - want).max() <= 1e-12 * np.abs(want).max()
+    shared = u["desc"][nmain:, 5].sum()
+    assert (u["desc"][nmain:, 7][u["desc"][nmain:, 5] > 0] & 2).all()   # shared = absolute
+    assert shared >= 0
+
+
+@pytest.mark.parametrize("nranks,split", [(2, "1"), (3, "1"), (2, "0"), (4, None)])
+def test_partitioned_ug_product(monkeypatch, nranks, split):
+    """Row-partitioned: interior main/rest slices use local rows only (they run before the halo
+    arrives), boundary ones run after; together they give this rank's rows of A x."""
+    if split is not None:
+        monkeypatch.setenv("FLZ_SPLIT", split)
+    csr = M.parsec_like(radius=10.0, n_atoms=8) if split is not None else M.laplacian3d(12)
+    n, rp, ci, va = csr
+    starts = uniform_starts(n, nranks)
+    plans = [HaloPlan(n, p, nranks, starts, rp, ci, va) for p in range(nranks)]
+    for p in range(nranks):
+        for q in range(nranks):
+            if p != q and len(plans[p].need(q)):
+                plans[q].set_give(p, plans[p].need(q))
+    x = np.random.default_rng(5).standard_normal(n)
+    want = reference(csr, x)
+    for p in range(nranks):
+        info, a = plans[p].info, plans[p].arrays()
+        nl, nh = info["rows_local"], info["halo_rows"]
+        xl = np.full(nl + nh, np.nan)                          # halo not there yet
+        xl[:nl] = x[starts[p] + a["perm"]]
+        y_int, rows_int = plans[p].ug_product(xl, "interior")
+        assert not np.isnan(y_int[rows_int]).any()             # interior never touches the halo
+        for q in range(nranks):                                # halo arrives
+            if q == p:
+                continue
+            aq = plans[q].arrays()
+            off, cnt = aq["give_off"][p], aq["give_cnt"][p]
+            rows = aq["send_rows"][off: off + cnt]
+            slot0 = a["need_off"][q]
+            xl[nl + slot0: nl + slot0 + cnt] = x[starts[q] + aq["perm"][rows]]
+        y_bnd, rows_bnd = plans[p].ug_product(xl, "boundary")
+        assert len(set(rows_int) & set(rows_bnd)) == 0 and len(rows_int) + len(rows_bnd) == nl
+        got = np.zeros(nl)
+        got[rows_int] = y_int[rows_int]
+        got[rows_bnd] = y_bnd[rows_bnd]
+        out = np.zeros(nl)
+        out[a["perm"]] = got
+        assert np.abs(out - want[starts[p]:starts[p + 1]]).max() <= 1e-12 * np.abs(want).max()
