@@ -14,8 +14,11 @@
 #include <cstddef>
 #include <cstdint>
 #include <memory>
+#include <new>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
+#include <utility>
 #include <vector>
 
 struct flz_ctx;
@@ -54,21 +57,65 @@ class Device {
 
 // -------------------------------------------------------------- DenseBlock
 // Column-major rows x cols block, zero-initialised.
+namespace detail {
+// std::allocator whose construct() default-initialises: a vector<double, ...>(n) then leaves
+// its storage untouched (no zero fill, no page faults before the first real write).
+template <class T>
+struct DefaultInitAllocator : std::allocator<T> {
+  template <class U>
+  struct rebind {
+    using other = DefaultInitAllocator<U>;
+  };
+  using std::allocator<T>::allocator;
+  template <class U>
+  void construct(U* p) noexcept(std::is_nothrow_default_constructible_v<U>) {
+    ::new (static_cast<void*>(p)) U;
+  }
+  template <class U, class... Args>
+  void construct(U* p, Args&&... args) {
+    ::new (static_cast<void*>(p)) U(std::forward<Args>(args)...);
+  }
+};
+}  // namespace detail
+
 class DenseBlock {
  public:
   DenseBlock() = default;
   DenseBlock(std::size_t rows, std::size_t cols)
       : rows_(rows), cols_(cols), data_(rows * cols, 0.0) {}
+  // storage the caller overwrites completely (device downloads): no zero fill
+  static DenseBlock uninitialized(std::size_t rows, std::size_t cols) {
+    DenseBlock B;
+    B.rows_ = rows;
+    B.cols_ = cols;
+    B.data_ = Storage(rows * cols);
+    return B;
+  }
+  // same, in page-locked host memory from the library's pool (flz_host_alloc): device
+  // downloads then run at full PCIe rate and touch no fresh pageable pages.  Falls back to
+  // ordinary storage when pinning fails.  Copies of such a block own ordinary storage.
+  static DenseBlock pinned(std::size_t rows, std::size_t cols);
+
+  DenseBlock(const DenseBlock& o) : rows_(o.rows_), cols_(o.cols_) {
+    if (o.ext_) data_.assign(o.ext_.get(), o.ext_.get() + o.size());
+    else data_ = o.data_;
+  }
+  DenseBlock& operator=(const DenseBlock& o) {
+    if (this != &o) *this = DenseBlock(o);
+    return *this;
+  }
+  DenseBlock(DenseBlock&&) noexcept = default;
+  DenseBlock& operator=(DenseBlock&&) noexcept = default;
 
   std::size_t rows() const { return rows_; }
   std::size_t cols() const { return cols_; }
-  std::size_t size() const { return data_.size(); }
-  double* data() { return data_.data(); }
-  const double* data() const { return data_.data(); }
-  double* col(std::size_t j) { return data_.data() + j * rows_; }
-  const double* col(std::size_t j) const { return data_.data() + j * rows_; }
-  double& operator()(std::size_t i, std::size_t j) { return data_[j * rows_ + i]; }
-  double operator()(std::size_t i, std::size_t j) const { return data_[j * rows_ + i]; }
+  std::size_t size() const { return rows_ * cols_; }
+  double* data() { return ext_ ? ext_.get() : data_.data(); }
+  const double* data() const { return ext_ ? ext_.get() : data_.data(); }
+  double* col(std::size_t j) { return data() + j * rows_; }
+  const double* col(std::size_t j) const { return data() + j * rows_; }
+  double& operator()(std::size_t i, std::size_t j) { return data()[j * rows_ + i]; }
+  double operator()(std::size_t i, std::size_t j) const { return data()[j * rows_ + i]; }
 
   static DenseBlock identity(std::size_t n) {
     DenseBlock I(n, n);
@@ -77,8 +124,10 @@ class DenseBlock {
   }
 
  private:
+  using Storage = std::vector<double, detail::DefaultInitAllocator<double>>;
   std::size_t rows_ = 0, cols_ = 0;
-  std::vector<double> data_;
+  Storage data_;
+  std::shared_ptr<double> ext_;  // pinned pool block (data_ is empty then)
 };
 
 // ---------------------------------------------------------- SparseSymMatrix

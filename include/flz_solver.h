@@ -124,6 +124,10 @@ int flz_solve(const flz_hostmatrix* A, double alpha, double beta, const flz_conf
               int plain, flz_result** out);
 void flz_result_free(flz_result* R);
 int64_t flz_result_count(const flz_result* R);
+/* the result's own eigenvector storage (n x count column-major, valid until flz_result_free):
+ * lets a binding wrap the vectors without a second host copy */
+const double* flz_result_vectors(const flz_result* result);
+int64_t flz_result_rows(const flz_result* result); /* rows of that storage (local rows) */
 /* any output pointer may be NULL; eigenvectors is n x count column-major */
 int flz_result_get(const flz_result* R, double* eigenvalues, double* residuals,
                    double* eigenvectors, flz_stats* stats);

@@ -151,6 +151,8 @@ _SOLVER_SIGS = {
     "flz_result_free": (None, [vp]),
     "flz_result_count": (i64, [vp]),
     "flz_result_get": (i32, [vp, vp, vp, vp, C.POINTER(FlzStats)]),
+    "flz_result_vectors": (vp, [vp]),
+    "flz_result_rows": (i64, [vp]),
 }
 
 

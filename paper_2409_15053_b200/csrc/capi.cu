@@ -468,11 +468,9 @@ int flz_ctx_set_exact(flz_ctx* ctx, int exact) {
   return FLZ_OK;
 }
 int flz_host_alloc(size_t bytes, void** out) {
-  return guarded([&] { FLZ_CUDA(cudaMallocHost(out, bytes)); });
+  return guarded([&] { *out = pinned_alloc(bytes); });
 }
-void flz_host_free(void* p) {
-  if (p) cudaFreeHost(p);
-}
+void flz_host_free(void* p) { pinned_free(p); }
 int flz_mem_info(flz_ctx* ctx, size_t* free_bytes, size_t* total_bytes) {
   return guarded([&] {
     use(ctx);

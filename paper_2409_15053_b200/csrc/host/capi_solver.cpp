@@ -358,6 +358,10 @@ void flz_result_free(flz_result* R) { delete R; }
 int64_t flz_result_count(const flz_result* R) {
   return static_cast<int64_t>(R->R.eigenvalues.size());
 }
+const double* flz_result_vectors(const flz_result* R) { return R->R.eigenvectors.data(); }
+int64_t flz_result_rows(const flz_result* R) {
+  return static_cast<int64_t>(R->R.eigenvectors.rows());
+}
 int flz_result_get(const flz_result* Rp, double* eigenvalues, double* residuals,
                    double* eigenvectors, flz_stats* s) {
   const EigenResult& R = Rp->R;

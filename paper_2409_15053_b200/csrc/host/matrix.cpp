@@ -175,8 +175,28 @@ SparseSymMatrix SparseSymMatrix::from_local_rows(std::size_t n_global, std::size
   return A;
 }
 
-// exact structural + numerical symmetry (sparse.cpp:65-83)
+// exact structural + numerical symmetry (sparse.cpp:65-83): every upper entry (i,j) must
+// have an equal mirror (j,i) — like the reference, lower entries are not looked up.  One
+// linear pass instead of a binary search per entry: rows are visited in ascending order, so
+// the mirror of (i,j) is found by advancing a cursor through row j.  On a mismatch the
+// reference's own search runs, so the entry it would report is the one reported.
 void SparseSymMatrix::verify_symmetry() const {
+  std::vector<std::int64_t> cursor(row_ptr_.begin(), row_ptr_.end() - 1);
+  bool ok = true;
+  for (std::size_t i = 0; i < n_ && ok; ++i)
+    for (std::int64_t p = row_ptr_[i]; p < row_ptr_[i + 1]; ++p) {
+      const auto j = static_cast<std::size_t>(col_idx_[p]);
+      if (j <= i) continue;
+      std::int64_t q = cursor[j];
+      const std::int64_t end = row_ptr_[j + 1];
+      while (q < end && static_cast<std::size_t>(col_idx_[q]) < i) ++q;
+      if (q >= end || static_cast<std::size_t>(col_idx_[q]) != i || values_[q] != values_[p]) {
+        ok = false;
+        break;
+      }
+      cursor[j] = q + 1;
+    }
+  if (ok) return;
   for (std::size_t i = 0; i < n_; ++i)
     for (std::int64_t p = row_ptr_[i]; p < row_ptr_[i + 1]; ++p) {
       const auto j = static_cast<std::size_t>(col_idx_[p]);
@@ -184,12 +204,24 @@ void SparseSymMatrix::verify_symmetry() const {
       const std::int32_t* first = col_idx_.data() + row_ptr_[j];
       const std::int32_t* last = col_idx_.data() + row_ptr_[j + 1];
       const std::int32_t* hit = std::lower_bound(first, last, static_cast<std::int32_t>(i));
-      const std::string where = "(" + std::to_string(i) + "," + std::to_string(j) + ")";
       if (hit == last || *hit != static_cast<std::int32_t>(i))
-        throw Error("matrix is structurally asymmetric at " + where);
+        throw Error("matrix is structurally asymmetric at (" + std::to_string(i) + "," +
+                    std::to_string(j) + ")");
       if (values_[p] != values_[row_ptr_[j] + (hit - first)])
-        throw Error("matrix is numerically asymmetric at " + where);
+        throw Error("matrix is numerically asymmetric at (" + std::to_string(i) + "," +
+                    std::to_string(j) + ")");
     }
+}
+
+DenseBlock DenseBlock::pinned(std::size_t rows, std::size_t cols) {
+  void* p = nullptr;
+  if (rows * cols == 0 || flz_host_alloc(rows * cols * sizeof(double), &p) != FLZ_OK || !p)
+    return uninitialized(rows, cols);
+  DenseBlock B;
+  B.rows_ = rows;
+  B.cols_ = cols;
+  B.ext_ = std::shared_ptr<double>(static_cast<double*>(p), [](double* q) { flz_host_free(q); });
+  return B;
 }
 
 flz_matrix* SparseSymMatrix::device() const {

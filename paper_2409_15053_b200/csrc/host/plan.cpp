@@ -3,7 +3,12 @@
 #include "plan.hpp"
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
+#include <exception>
+#include <mutex>
+#include <thread>
 #include <numeric>
 #include <stdexcept>
 #include <string>
@@ -60,6 +65,33 @@ int64_t padded_entries(const std::vector<int32_t>& len, const std::vector<int32_
   return total;
 }
 
+// ---- host parallelism: the layout passes are independent per slice
+int worker_count() {
+  if (const char* e = std::getenv("FLZ_HOST_THREADS")) return std::max(1, std::atoi(e));
+  return (int)std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+}
+template <class F>
+void run_chunks(int nchunks, F&& body) {
+  if (nchunks <= 1) {
+    body(0);
+    return;
+  }
+  std::vector<std::thread> pool;
+  std::exception_ptr err;
+  std::mutex mu;
+  for (int t = 0; t < nchunks; ++t)
+    pool.emplace_back([&, t] {
+      try {
+        body(t);
+      } catch (...) {
+        std::lock_guard<std::mutex> lock(mu);
+        if (!err) err = std::current_exception();
+      }
+    });
+  for (auto& th : pool) th.join();
+  if (err) std::rethrow_exception(err);
+}
+
 // ---- UG layout -------------------------------------------------------------------------
 // A diagonal offset d = col - row that at least kUgMinLanes of a slice's 32 lanes hold is
 // stored as ONE uniform position: 32 values + one int32, the lanes without it get a zero.
@@ -100,119 +132,186 @@ int64_t build_ug(HostPlan& P, const std::vector<uint8_t>& is_boundary, bool allo
   for (int64_t s = 0; s < nslices; ++s) max_len = std::max(max_len, P.slice_len[s]);
   size_t cap = 64;
   while (cap < (size_t)max_len * kPlanSliceRows * 2) cap <<= 1;
-  OffsetCounter counter(cap);
-  std::vector<int64_t> uni;            // chosen offsets of the slice, ascending
-  std::vector<int32_t> glen(kPlanSliceRows);
-  // identical offset lists (every interior slice of a stencil) share one copy
-  std::vector<int64_t> last_uni;
-  int32_t last_uoff_ptr = -1;
   // spilled leftovers (SPLIT mode): per rest row its entries, pooled
   struct RestRow {
     int32_t row;
     int64_t begin, end;
     uint8_t boundary;
   };
-  std::vector<RestRow> rest;
-  std::vector<int32_t> rest_col;
-  std::vector<double> rest_val;
-  for (int64_t s = 0; s < nslices; ++s) {
-    const int32_t L = P.slice_len[s];
-    const int64_t base = P.slice_ptr[s];
-    counter.clear();
-    for (int l = 0; l < kPlanSliceRows; ++l) {
-      const int64_t row = s * kPlanSliceRows + l;
-      const int32_t len = row < nl ? P.row_len[row] : 0;
-      for (int32_t p = 0; p < len; ++p)
-        counter.add((int64_t)P.col[base + (int64_t)p * kPlanSliceRows + l] - row);
-    }
-    uni.clear();
-    for (int32_t h : counter.used)
-      if (counter.cnt[h] >= kUgMinLanes) uni.push_back(counter.key[h]);
-    std::sort(uni.begin(), uni.end());
-    // general part: what every lane keeps after its uniform entries are taken out
-    int32_t ng = 0;
-    if (!uni.empty()) {
+  // ---- phase A (parallel over chunks of slices): uniform offsets, nu, ng, spill decision
+  struct SliceInfo {
+    int32_t nu = 0, ng = 0;
+    uint8_t spill = 0;
+    int64_t uni_begin = 0;  // into the chunk's offset pool
+  };
+  struct Chunk {
+    int64_t s0 = 0, s1 = 0;
+    std::vector<int64_t> uni_pool;
+    int64_t uniform_entries = 0;
+    std::vector<RestRow> rest;
+    std::vector<int32_t> rest_col;
+    std::vector<double> rest_val;
+  };
+  const int nchunks = (int)std::max<int64_t>(1, std::min<int64_t>(worker_count(), nslices / 256));
+  std::vector<Chunk> chunks(nchunks);
+  for (int t = 0; t < nchunks; ++t) {
+    chunks[t].s0 = nslices * t / nchunks;
+    chunks[t].s1 = nslices * (t + 1) / nchunks;
+  }
+  std::vector<SliceInfo> info(nslices);
+  run_chunks(nchunks, [&](int t) {
+    Chunk& C = chunks[t];
+    OffsetCounter counter(cap);
+    std::vector<int64_t> uni;
+    int32_t glen[kPlanSliceRows];
+    for (int64_t s = C.s0; s < C.s1; ++s) {
+      const int32_t L = P.slice_len[s];
+      const int64_t base = P.slice_ptr[s];
+      counter.clear();
       for (int l = 0; l < kPlanSliceRows; ++l) {
         const int64_t row = s * kPlanSliceRows + l;
         const int32_t len = row < nl ? P.row_len[row] : 0;
-        int32_t g = 0;
-        for (int32_t p = 0; p < len; ++p) {
-          const int64_t d = (int64_t)P.col[base + (int64_t)p * kPlanSliceRows + l] - row;
-          if (!std::binary_search(uni.begin(), uni.end(), d)) ++g;
-        }
-        glen[l] = g;
-        ng = std::max(ng, g);
+        for (int32_t p = 0; p < len; ++p)
+          counter.add((int64_t)P.col[base + (int64_t)p * kPlanSliceRows + l] - row);
       }
-      // keep the uniform positions only when they move fewer bytes than the plain slice
-      const int64_t bytes_plain = (int64_t)12 * kPlanSliceRows * L;
-      const int64_t bytes_ug = (int64_t)8 * kPlanSliceRows * ((int64_t)uni.size() + ng) +
-                               4 * (int64_t)uni.size() + (int64_t)4 * kPlanSliceRows * ng;
-      if (!P.split && bytes_ug >= bytes_plain) uni.clear();
+      uni.clear();
+      for (int32_t h : counter.used)
+        if (counter.cnt[h] >= kUgMinLanes) uni.push_back(counter.key[h]);
+      std::sort(uni.begin(), uni.end());
+      // general part: what every lane keeps after its uniform entries are taken out
+      int32_t ng = 0;
+      if (!uni.empty()) {
+        for (int l = 0; l < kPlanSliceRows; ++l) {
+          const int64_t row = s * kPlanSliceRows + l;
+          const int32_t len = row < nl ? P.row_len[row] : 0;
+          int32_t g = 0;
+          for (int32_t p = 0; p < len; ++p) {
+            const int64_t d = (int64_t)P.col[base + (int64_t)p * kPlanSliceRows + l] - row;
+            if (!std::binary_search(uni.begin(), uni.end(), d)) ++g;
+          }
+          glen[l] = g;
+          ng = std::max(ng, g);
+        }
+        // keep the uniform positions only when they move fewer bytes than the plain slice
+        const int64_t bytes_plain = (int64_t)12 * kPlanSliceRows * L;
+        const int64_t bytes_ug = (int64_t)8 * kPlanSliceRows * ((int64_t)uni.size() + ng) +
+                                 4 * (int64_t)uni.size() + (int64_t)4 * kPlanSliceRows * ng;
+        if (!P.split && bytes_ug >= bytes_plain) uni.clear();
+      }
+      if (uni.empty()) {
+        ng = L;
+        for (int l = 0; l < kPlanSliceRows; ++l) {
+          const int64_t row = s * kPlanSliceRows + l;
+          glen[l] = row < nl ? P.row_len[row] : 0;
+        }
+      }
+      // SPLIT mode: ragged leftovers leave the slice
+      bool spill = false;
+      if (P.split && allow_spill && ng > 2) {
+        int64_t gsum = 0;
+        for (int l = 0; l < kPlanSliceRows; ++l) gsum += glen[l];
+        spill = 4 * gsum < (int64_t)3 * ng * kPlanSliceRows;  // < 75 % of the padded rectangle
+      }
+      if (spill) ng = 0;
+      SliceInfo& I = info[s];
+      I.nu = (int32_t)uni.size();
+      I.ng = ng;
+      I.spill = spill;
+      I.uni_begin = (int64_t)C.uni_pool.size();
+      C.uni_pool.insert(C.uni_pool.end(), uni.begin(), uni.end());
     }
-    if (uni.empty()) {
-      ng = L;
+  });
+  // ---- phase B (serial): pointers; identical consecutive offset lists (every interior slice
+  // of a stencil) share one copy
+  {
+    int64_t vptr = 0, cptr = 0;
+    const int64_t* last_uni = nullptr;
+    int32_t last_nu = -1, last_uoff_ptr = -1;
+    for (int t = 0; t < nchunks; ++t)
+      for (int64_t s = chunks[t].s0; s < chunks[t].s1; ++s) {
+        const SliceInfo& I = info[s];
+        const int64_t* uni = chunks[t].uni_pool.data() + I.uni_begin;
+        PlanUgSlice& H = P.ug_slice[s];
+        H.val_ptr = vptr;
+        H.col_ptr = cptr;
+        H.nu = I.nu;
+        H.ng = I.ng;
+        H.reserved = I.spill ? 1 : 0;
+        if (I.nu > 0 && I.nu == last_nu && std::equal(uni, uni + I.nu, last_uni)) {
+          H.uoff_ptr = last_uoff_ptr;
+        } else {
+          H.uoff_ptr = (int32_t)P.ug_uoff.size();
+          for (int32_t i = 0; i < I.nu; ++i) P.ug_uoff.push_back((int32_t)uni[i]);
+          if (I.nu > 0) {
+            last_uni = uni;
+            last_nu = I.nu;
+            last_uoff_ptr = H.uoff_ptr;
+          }
+        }
+        for (int i = 0; i < 8; ++i) H.inline_off[i] = i < I.nu ? (int32_t)uni[i] : 0;
+        vptr += (int64_t)(I.nu + I.ng) * kPlanSliceRows;
+        cptr += (int64_t)I.ng * kPlanSliceRows;
+      }
+    P.ug_val.assign((size_t)vptr, 0.0);
+    P.ug_col.assign((size_t)cptr, 0);
+  }
+  // ---- phase C (parallel): values, general columns, spilled entries
+  run_chunks(nchunks, [&](int t) {
+    Chunk& C = chunks[t];
+    for (int64_t s = C.s0; s < C.s1; ++s) {
+      const SliceInfo& I = info[s];
+      const PlanUgSlice& H = P.ug_slice[s];
+      const int64_t* uni = C.uni_pool.data() + I.uni_begin;
+      const int64_t* uni_end = uni + I.nu;
+      const int64_t base = P.slice_ptr[s];
+      const int32_t nu = I.nu, ng = I.ng;
+      const bool spill = I.spill;
+      double* v = P.ug_val.data() + H.val_ptr;
+      int32_t* c = P.ug_col.data() + H.col_ptr;
       for (int l = 0; l < kPlanSliceRows; ++l) {
         const int64_t row = s * kPlanSliceRows + l;
-        glen[l] = row < nl ? P.row_len[row] : 0;
-      }
-    }
-    // SPLIT mode: ragged leftovers leave the slice
-    bool spill = false;
-    if (P.split && allow_spill && ng > 2) {
-      int64_t gsum = 0;
-      for (int l = 0; l < kPlanSliceRows; ++l) gsum += glen[l];
-      spill = 4 * gsum < (int64_t)3 * ng * kPlanSliceRows;  // < 75 % of the padded rectangle
-    }
-    if (spill) ng = 0;
-    const int32_t nu = (int32_t)uni.size();
-    PlanUgSlice& H = P.ug_slice[s];
-    H.val_ptr = (int64_t)P.ug_val.size();
-    H.col_ptr = (int64_t)P.ug_col.size();
-    H.nu = nu;
-    H.ng = ng;
-    H.reserved = spill ? 1 : 0;
-    if (nu > 0 && uni == last_uni) {
-      H.uoff_ptr = last_uoff_ptr;
-    } else {
-      H.uoff_ptr = (int32_t)P.ug_uoff.size();
-      for (int64_t d : uni) P.ug_uoff.push_back((int32_t)d);
-      if (nu > 0) {
-        last_uni = uni;
-        last_uoff_ptr = H.uoff_ptr;
-      }
-    }
-    for (int i = 0; i < 8; ++i) H.inline_off[i] = i < nu ? (int32_t)uni[i] : 0;
-    P.ug_val.resize(P.ug_val.size() + (size_t)(nu + ng) * kPlanSliceRows, 0.0);
-    P.ug_col.resize(P.ug_col.size() + (size_t)ng * kPlanSliceRows, 0);
-    double* v = P.ug_val.data() + H.val_ptr;
-    int32_t* c = P.ug_col.data() + H.col_ptr;
-    for (int l = 0; l < kPlanSliceRows; ++l) {
-      const int64_t row = s * kPlanSliceRows + l;
-      const int32_t len = row < nl ? P.row_len[row] : 0;
-      const int32_t self = (int32_t)std::min<int64_t>(row, std::max<int64_t>(nl - 1, 0));
-      int32_t g = 0;
-      for (int32_t p = 0; p < len; ++p) {
-        const int64_t e = base + (int64_t)p * kPlanSliceRows + l;
-        const int64_t d = (int64_t)P.col[e] - row;
-        const auto it = std::lower_bound(uni.begin(), uni.end(), d);
-        if (it != uni.end() && *it == d) {
-          v[(int64_t)(it - uni.begin()) * kPlanSliceRows + l] += P.val[e];
-          if (P.val[e] != 0.0) ++P.ug_uniform_entries;
-        } else if (spill) {
-          if (g == 0) rest.push_back({(int32_t)row, (int64_t)rest_col.size(), 0, is_boundary[s]});
-          rest_col.push_back(P.col[e]);
-          rest_val.push_back(P.val[e]);
-          rest.back().end = (int64_t)rest_col.size();
-          ++g;
-        } else {  // general entries keep their CSR order
-          v[(int64_t)(nu + g) * kPlanSliceRows + l] = P.val[e];
-          c[(int64_t)g * kPlanSliceRows + l] = P.col[e];
-          ++g;
+        const int32_t len = row < nl ? P.row_len[row] : 0;
+        const int32_t self = (int32_t)std::min<int64_t>(row, std::max<int64_t>(nl - 1, 0));
+        int32_t g = 0;
+        for (int32_t p = 0; p < len; ++p) {
+          const int64_t e = base + (int64_t)p * kPlanSliceRows + l;
+          const int64_t d = (int64_t)P.col[e] - row;
+          const int64_t* it = std::lower_bound(uni, uni_end, d);
+          if (it != uni_end && *it == d) {
+            v[(int64_t)(it - uni) * kPlanSliceRows + l] += P.val[e];
+            if (P.val[e] != 0.0) ++C.uniform_entries;
+          } else if (spill) {
+            if (g == 0)
+              C.rest.push_back({(int32_t)row, (int64_t)C.rest_col.size(), 0, is_boundary[s]});
+            C.rest_col.push_back(P.col[e]);
+            C.rest_val.push_back(P.val[e]);
+            C.rest.back().end = (int64_t)C.rest_col.size();
+            ++g;
+          } else {  // general entries keep their CSR order
+            v[(int64_t)(nu + g) * kPlanSliceRows + l] = P.val[e];
+            c[(int64_t)g * kPlanSliceRows + l] = P.col[e];
+            ++g;
+          }
         }
+        if (!spill)
+          for (; g < ng; ++g) c[(int64_t)g * kPlanSliceRows + l] = self;
       }
-      if (!spill)
-        for (; g < ng; ++g) c[(int64_t)g * kPlanSliceRows + l] = self;
     }
+  });
+  // ---- phase D (serial): the chunks' spilled rows, in row order
+  std::vector<RestRow> rest;
+  std::vector<int32_t> rest_col;
+  std::vector<double> rest_val;
+  for (Chunk& C : chunks) {
+    P.ug_uniform_entries += C.uniform_entries;
+    const int64_t shift = (int64_t)rest_col.size();
+    for (RestRow r : C.rest) {
+      r.begin += shift;
+      r.end += shift;
+      rest.push_back(r);
+    }
+    rest_col.insert(rest_col.end(), C.rest_col.begin(), C.rest_col.end());
+    rest_val.insert(rest_val.end(), C.rest_val.begin(), C.rest_val.end());
   }
   // ---- rest slices: interior rows first, then boundary rows.  Rows with the same column
   // extent (first, last leftover column) — e.g. the rows of one dense non-local block — are
@@ -340,6 +439,18 @@ int64_t build_ug(HostPlan& P, const std::vector<uint8_t>& is_boundary, bool allo
   return (int64_t)rest_col.size();
 }
 
+struct PhaseTimer {  // FLZ_TRACE=1: phase timings of build_plan on stderr
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  bool on = std::getenv("FLZ_TRACE") != nullptr;
+  void lap(const char* what) {
+    if (!on) return;
+    const auto t1 = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[flz]   plan %-22s %9.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(t1 - t0).count());
+    t0 = t1;
+  }
+};
+
 void require(bool ok, const char* msg) {
   if (!ok) throw std::invalid_argument(msg);
 }
@@ -376,6 +487,8 @@ HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<in
     require(col_idx[p0 + p] >= 0 && col_idx[p0 + p] < n_global,
             "plan: column index out of range");
 
+  PhaseTimer timer;
+  timer.lap("validate");
   // ---- SPLIT mode?  Count the nonzeros whose diagonal offset is shared by at least
   // kUgMinLanes rows of their natural-order slice (global indices: a good estimate of what
   // build_ug finds after the halo columns are renumbered).
@@ -385,21 +498,29 @@ HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<in
     for (int64_t i = 0; i < nl; ++i) max_len = std::max(max_len, len[i]);
     size_t cap = 64;
     while (cap < (size_t)max_len * kPlanSliceRows * 2) cap <<= 1;
-    OffsetCounter counter(cap);
+    const int64_t nsl = (nl + kPlanSliceRows - 1) / kPlanSliceRows;
+    const int nchunks = (int)std::max<int64_t>(1, std::min<int64_t>(worker_count(), nsl / 256));
+    std::vector<int64_t> part(nchunks, 0);
+    run_chunks(nchunks, [&](int t) {
+      OffsetCounter counter(cap);
+      for (int64_t sl = nsl * t / nchunks; sl < nsl * (t + 1) / nchunks; ++sl) {
+        const int64_t i0 = sl * kPlanSliceRows;
+        counter.clear();
+        const int64_t i1 = std::min(nl, i0 + kPlanSliceRows);
+        for (int64_t i = i0; i < i1; ++i)
+          for (int64_t p = row_ptr[i]; p < row_ptr[i + 1]; ++p)
+            counter.add((int64_t)col_idx[p] - (P.row_begin + i));
+        for (int32_t h : counter.used)
+          if (counter.cnt[h] >= kUgMinLanes) part[t] += counter.cnt[h];
+      }
+    });
     int64_t uniform = 0;
-    for (int64_t i0 = 0; i0 < nl; i0 += kPlanSliceRows) {
-      counter.clear();
-      const int64_t i1 = std::min(nl, i0 + kPlanSliceRows);
-      for (int64_t i = i0; i < i1; ++i)
-        for (int64_t p = row_ptr[i]; p < row_ptr[i + 1]; ++p)
-          counter.add((int64_t)col_idx[p] - (P.row_begin + i));
-      for (int32_t h : counter.used)
-        if (counter.cnt[h] >= kUgMinLanes) uniform += counter.cnt[h];
-    }
+    for (int64_t v : part) uniform += v;
     P.split = 2 * uniform >= P.nnz;
     if (const char* force = std::getenv("FLZ_SPLIT")) P.split = force[0] == '1';  // experiments
   }
 
+  timer.lap("split estimate");
   // ---- sigma: smallest window whose padding overhead is <= 5 %
   int64_t chosen = sigma;
   if (P.split) {
@@ -430,6 +551,7 @@ HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<in
   P.iperm.resize(nl);
   for (int64_t i = 0; i < nl; ++i) P.iperm[P.perm[i]] = (int32_t)i;
 
+  timer.lap("sigma / perm");
   // ---- halo columns: sorted unique remote global ids, grouped by owner
   if (nranks > 1) {
     for (int64_t p = 0; p < P.nnz; ++p) {
@@ -453,6 +575,7 @@ HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<in
   P.give_off.assign(nranks, 0);
   P.give_cnt.assign(nranks, 0);
 
+  timer.lap("halo");
   // ---- SELL-32 storage
   const int64_t nslices = P.nslices = (nl + kPlanSliceRows - 1) / kPlanSliceRows;
   P.slice_ptr.assign(nslices + 1, 0);
@@ -473,7 +596,9 @@ HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<in
   P.col.assign(std::max<int64_t>(P.stored, 1), 0);
   P.val.assign(std::max<int64_t>(P.stored, 1), 0.0);
   std::vector<uint8_t> is_boundary(nslices, 0);
-  for (int64_t s = 0; s < nslices; ++s)
+  const int fill_chunks = (int)std::max<int64_t>(1, std::min<int64_t>(worker_count(), nslices / 256));
+  run_chunks(fill_chunks, [&](int t) {
+  for (int64_t s = nslices * t / fill_chunks; s < nslices * (t + 1) / fill_chunks; ++s)
     for (int l = 0; l < kPlanSliceRows; ++l) {
       const int64_t inew = s * kPlanSliceRows + l;
       const int64_t base = P.slice_ptr[s] + l;
@@ -500,14 +625,17 @@ HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<in
         P.val[base + (int64_t)cnt * kPlanSliceRows] = 0.0;
       }
     }
+  });
   std::vector<int32_t> all(nslices);
   std::iota(all.begin(), all.end(), 0);
   for (int64_t s = 0; s < nslices; ++s)
     (is_boundary[s] ? P.boundary : P.interior).push_back((int32_t)s);
+  timer.lap("SELL arrays");
   // a rest launch per product only pays when it carries a real share of the matrix
   if (const int64_t spilled = build_ug(P, is_boundary, true);
       spilled > 0 && 50 * spilled < P.nnz)
     build_ug(P, is_boundary, false);
+  timer.lap("UG layout");
   std::vector<int32_t> ug_len(nslices + P.nrest);  // the fast kernels walk the compressed slices
   for (int64_t s = 0; s < nslices + P.nrest; ++s) ug_len[s] = P.ug_slice[s].nu + P.ug_slice[s].ng;
   {

@@ -18,6 +18,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <future>
 #include <random>
 
 #include "flz.h"
@@ -458,7 +459,7 @@ EigenResult recover_eigenpairs(const LanczosFactorization& st, const SparseSymMa
     }
     out.eigenvalues = lambdas;  // already ascending
     out.residuals.assign(sel.size(), 0.0);
-    out.eigenvectors = DenseBlock(n, sel.size());
+    out.eigenvectors = DenseBlock::pinned(n, sel.size());
     const WallClock t_rot;
     if (!sel.empty())
       throw_status(flz_ritz_rotate(ctx, st.device(), U.data(), lambdas.data(),
@@ -469,7 +470,7 @@ EigenResult recover_eigenpairs(const LanczosFactorization& st, const SparseSymMa
     // plain mode: Ritz values are the eigenvalue estimates (:480-495)
     std::vector<double> lam(wk), res(wk);
     for (std::size_t c = 0; c < wk; ++c) lam[c] = ritz.values[kept_src[c]];
-    DenseBlock V(n, wk);
+    DenseBlock V = DenseBlock::uninitialized(n, wk);
     throw_status(flz_ritz_plain(ctx, A.device(), st.device(), lam.data(), static_cast<int>(wk),
                                 scale, res.data(), V.data()));
     std::vector<std::size_t> sel;
@@ -544,6 +545,12 @@ EigenResult run_solve(const SparseSymMatrix& A, double alpha, double beta,
   (void)A.device();  // CSR -> SELL + H2D when not resident yet
   const double time_upload = upload.seconds();
 
+  // the start block is host work (the reference's libstdc++ random stream, lanczos.cpp:78-103)
+  // that depends on nothing else: it runs beside the device-side bounds estimate
+  const auto r = static_cast<std::size_t>(cfg.block_size);
+  std::future<DenseBlock> start_block = std::async(
+      std::launch::async, [&A, r, seed = cfg.seed] { return init_block(A.dim(), r, seed); });
+
   const std::uint64_t mv0 = matvec_count();
   const WallClock pre;
   const SpectralBounds bounds = estimate_spectral_bounds(A, cfg.bounds_steps, cfg.seed);
@@ -562,11 +569,10 @@ EigenResult run_solve(const SparseSymMatrix& A, double alpha, double beta,
   const BlockOperator op =
       filter ? BlockOperator::filtered(A, *filter) : BlockOperator::plain(A);
 
-  const auto r = static_cast<std::size_t>(cfg.block_size);
   const auto max_cols = static_cast<std::size_t>(cfg.resolved_max_dim(A.dim()));
   trace("solve: upload + bounds + filter", total);
   const WallClock t_init;
-  DenseBlock start = local_rows(init_block(A.dim(), r, cfg.seed), A.dim());
+  DenseBlock start = local_rows(start_block.get(), A.dim());
   trace("solve: init_block (host)", t_init);
   const WallClock t_fact;
   LanczosFactorization st(op, std::move(start), max_cols);

@@ -27,6 +27,7 @@ struct Pool {
   std::multimap<size_t, void*> free_pinned;
   std::unordered_map<void*, size_t> live_pinned;
   size_t cached_bytes = 0;
+  size_t cached_pinned = 0;
 };
 
 Pool& pool() {
@@ -118,6 +119,7 @@ void* pinned_alloc(size_t bytes) {
   if (it != P.free_pinned.end() && it->first <= 2 * want) {
     void* p = it->second;
     P.live_pinned[p] = it->first;
+    P.cached_pinned -= it->first;
     P.free_pinned.erase(it);
     return p;
   }
@@ -136,10 +138,14 @@ void pinned_free(void* p) {
     cudaFreeHost(p);
     return;
   }
-  if (it->second > (size_t(64) << 20)) {  // large staging buffers are not worth pinning forever
+  // eigenvector blocks of consecutive solves are reused; the cache of page-locked memory is
+  // capped so that it cannot pin the host down
+  constexpr size_t kPinnedCacheCap = size_t(4) << 30;
+  if (P.cached_pinned + it->second > kPinnedCacheCap) {
     cudaFreeHost(p);
   } else {
     P.free_pinned.emplace(it->second, p);
+    P.cached_pinned += it->second;
   }
   P.live_pinned.erase(it);
 }

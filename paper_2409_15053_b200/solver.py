@@ -243,21 +243,40 @@ class LanczosFactorization:
             pass
 
 
+class _ResultOwner:
+    """Keeps a flz_result alive for as long as NumPy views of its eigenvectors exist."""
+
+    def __init__(self, handle):
+        self.handle = handle
+
+    def __del__(self):
+        try:
+            lib().flz_result_free(self.handle)
+        except Exception:
+            pass
+
+
 def _solve(A: SparseSymMatrix, alpha, beta, cfg, plain, want_vectors):
     cfg = cfg or LanczosConfig()
     h = C.c_void_p()
     check(lib().flz_solve(A.handle, alpha, beta, C.byref(cfg), int(plain), C.byref(h)))
-    try:
-        cnt = int(lib().flz_result_count(h))
-        ev, res = np.empty(cnt), np.empty(cnt)
-        vec = np.empty(A.n * cnt) if want_vectors else None
-        st = FlzStats()
-        check(lib().flz_result_get(h, _ptr(ev), _ptr(res), _ptr(vec) if want_vectors else None,
-                                   C.byref(st)))
-    finally:
-        lib().flz_result_free(h)
+    owner = _ResultOwner(h)
+    cnt = int(lib().flz_result_count(h))
+    ev, res = np.empty(cnt), np.empty(cnt)
+    st = FlzStats()
+    check(lib().flz_result_get(h, _ptr(ev), _ptr(res), None, C.byref(st)))
+    vec = None
+    if want_vectors:
+        rows = int(lib().flz_result_rows(h))
+        if cnt * rows:
+            # zero-copy view of the result's own storage; the view keeps the result alive
+            buf = (C.c_double * (rows * cnt)).from_address(lib().flz_result_vectors(h))
+            buf._owner = owner
+            vec = np.frombuffer(buf, dtype=np.float64).reshape(cnt, rows).T
+        else:
+            vec = np.empty((rows, cnt))
     stats = {k: getattr(st, k) for k, _ in FlzStats._fields_}
-    return EigenResult(ev, res, _from_fcol(vec, A.n, cnt) if want_vectors else None, stats)
+    return EigenResult(ev, res, vec, stats)
 
 
 def filtered_lanczos(A, alpha, beta, cfg=None, want_vectors=True) -> EigenResult:
