@@ -136,6 +136,8 @@ int flz_plan_ug(const flz_plan* plan, int64_t* sizes, int32_t* descriptors, doub
  * vector-column product, so a fused r-column block product adds r. */
 uint64_t flz_matvec_count(void);
 void flz_reset_matvec_count(void);
+/* takes back the counts of block steps that were rolled back (flz_basis_truncate) */
+void flz_matvec_sub(uint64_t count);
 
 /* ------------------------------------------------- block products & filter */
 /* Y = A X, r columns, host buffers.  Replaces SparseSymMatrix::spmm_block
@@ -170,6 +172,11 @@ int flz_basis_create(flz_ctx* ctx, const flz_matrix* A, int64_t max_cols, int r,
                      const double* start, flz_basis** out);
 void flz_basis_destroy(flz_basis* B);
 int64_t flz_basis_blocks(const flz_basis* B); /* k */
+/* Rolls the factorization back to its first k completed blocks (k <= current): block k
+ * becomes the pending block again — it still holds what it held when it was pending — and
+ * the running operator-output scale is reset to `op_scale`, its value at that point.  Used by
+ * the solver when block steps ran speculatively beside a host-side convergence check. */
+int flz_basis_truncate(flz_ctx* ctx, flz_basis* B, int64_t k, double op_scale);
 /* Copies basis columns [j0, j0+count) (local rows) to the host, column-major. */
 int flz_basis_get(flz_ctx* ctx, const flz_basis* B, int64_t j0, int64_t count, double* out);
 /* Overwrites one column (breakdown replacement path, lanczos.cpp:232-262). */

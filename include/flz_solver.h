@@ -68,6 +68,10 @@ int flz_hostmatrix_load_mm(const char* path, flz_hostmatrix** out);
 int flz_hostmatrix_save_mm(const flz_hostmatrix* A, const char* path);
 void flz_hostmatrix_free(flz_hostmatrix* A);
 int flz_hostmatrix_dims(const flz_hostmatrix* A, int64_t* n, int64_t* nnz);
+/* device layout of the matrix (uploads it when it is not resident yet): bytes of the
+ * index-compressed copy one fused Clenshaw step streams, true nonzeros at uniform positions */
+int flz_hostmatrix_layout(const flz_hostmatrix* A, int64_t* matrix_bytes,
+                          int64_t* uniform_entries);
 int flz_hostmatrix_csr(const flz_hostmatrix* A, int64_t* row_ptr, int32_t* col_idx,
                        double* values);
 /* SparseSymMatrix::spmm_block / ChebyshevFilter::apply through the C++ facade */

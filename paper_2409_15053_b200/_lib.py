@@ -94,6 +94,8 @@ _SIGS = {
     "flz_plan_ug": (i32, [vp, vp, vp, vp, vp, vp, vp]),
     "flz_matvec_count": (u64, []),
     "flz_reset_matvec_count": (None, []),
+    "flz_matvec_sub": (None, [u64]),
+    "flz_basis_truncate": (i32, [vp, vp, i64, d]),
     "flz_spmm": (i32, [vp, vp, vp, i32, vp, i32]),
     "flz_filter_apply": (i32, [vp, vp, f64p, i32, d, d, vp, i32, vp]),
     "flz_filter_bench": (i32, [vp, vp, f64p, i32, d, d, vp, i32, i32, i32, dP, vp]),
@@ -127,6 +129,7 @@ _SOLVER_SIGS = {
     "flz_hostmatrix_save_mm": (i32, [vp, C.c_char_p]),
     "flz_hostmatrix_free": (None, [vp]),
     "flz_hostmatrix_dims": (i32, [vp, i64P, i64P]),
+    "flz_hostmatrix_layout": (i32, [vp, i64P, i64P]),
     "flz_hostmatrix_csr": (i32, [vp, i64p, i32p, f64p]),
     "flz_hostmatrix_spmm": (i32, [vp, f64p, i64, i32, f64p]),
     "flz_hostmatrix_filter_apply": (i32, [vp, f64p, i32, d, d, f64p, i64, i32, f64p]),

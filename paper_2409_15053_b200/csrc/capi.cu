@@ -481,6 +481,7 @@ int flz_mem_info(flz_ctx* ctx, size_t* free_bytes, size_t* total_bytes) {
 
 uint64_t flz_matvec_count(void) { return g_matvecs.load(std::memory_order_relaxed); }
 void flz_reset_matvec_count(void) { g_matvecs.store(0, std::memory_order_relaxed); }
+void flz_matvec_sub(uint64_t count) { g_matvecs.fetch_sub(count, std::memory_order_relaxed); }
 
 // ----------------------------------------------------------------- matrix
 
@@ -974,6 +975,21 @@ int flz_basis_set(flz_ctx* ctx, flz_basis* B, int64_t j, const double* col) {
     FLZ_REQUIRE(j >= 0 && j < B->max_cols + B->r, FLZ_EDIM, "basis_set: column out of bounds");
     use(ctx);
     upload_block(B->A, col, 1, B->col(j));
+    FLZ_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int flz_basis_truncate(flz_ctx* ctx, flz_basis* B, int64_t k, double op_scale) {
+  return guarded([&] {
+    FLZ_REQUIRE(ctx && B, FLZ_EINVAL, "basis_truncate: null argument");
+    FLZ_REQUIRE(k >= 0 && k <= B->k, FLZ_EDIM, "basis_truncate: k exceeds the completed blocks");
+    use(ctx);
+    const SmallLayout L = small_layout(B->max_cols, B->r);
+    B->k = k;
+    B->op_scale = op_scale;
+    B->pinned[L.scale] = op_scale;
+    FLZ_CUDA(cudaMemcpyAsync(B->small.p + L.scale, B->pinned + L.scale, sizeof(double),
+                             cudaMemcpyHostToDevice, ctx->stream));
     FLZ_CUDA(cudaStreamSynchronize(ctx->stream));
   });
 }

@@ -158,6 +158,12 @@ int flz_hostmatrix_dims(const flz_hostmatrix* A, int64_t* n, int64_t* nnz) {
   if (nnz) *nnz = static_cast<int64_t>(A->A.nnz());
   return FLZ_OK;
 }
+int flz_hostmatrix_layout(const flz_hostmatrix* A, int64_t* matrix_bytes,
+                          int64_t* uniform_entries) {
+  return wrap([&] {
+    throw_status(flz_matrix_layout(A->A.device(), matrix_bytes, uniform_entries));
+  });
+}
 int flz_hostmatrix_csr(const flz_hostmatrix* A, int64_t* row_ptr, int32_t* col_idx,
                        double* values) {
   std::copy(A->A.row_ptr().begin(), A->A.row_ptr().end(), row_ptr);

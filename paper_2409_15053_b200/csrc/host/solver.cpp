@@ -18,8 +18,11 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <deque>
 #include <future>
+#include <memory>
 #include <random>
+#include <thread>
 
 #include "flz.h"
 
@@ -277,19 +280,59 @@ int expand(LanczosFactorization& st, int nblocks, ExpandTimes* times) {
   return added;
 }
 
+LanczosFactorization::Snapshot LanczosFactorization::snapshot() const {
+  Snapshot s;
+  s.r = r_;
+  s.k = k_;
+  s.D = D_;
+  s.S = S_;
+  s.dead = dead_;
+  s.kind = op_->kind();
+  s.filter = op_->filter();
+  s.exhausted = exhausted_;
+  s.breakdown = breakdown_;
+  s.max_diag_asym = max_diag_asym_;
+  s.op_scale = op_scale_;
+  s.rng_state = rng_state_;
+  return s;
+}
+
+void LanczosFactorization::rollback(const Snapshot& snap) {
+  if (snap.k > k_) throw Error("rollback: snapshot is ahead of the factorization");
+  const std::size_t undone = k_ - snap.k;
+  if (undone == 0) return;
+  throw_status(flz_basis_truncate(Device::context(), dev_, static_cast<std::int64_t>(snap.k),
+                                  snap.op_scale));
+  const ChebyshevFilter* f = op_->filter();
+  flz_matvec_sub(static_cast<std::uint64_t>(undone) * r_ * (f ? f->degree() : 1));
+  k_ = snap.k;
+  D_ = snap.D;
+  S_ = snap.S;
+  dead_ = snap.dead;
+  exhausted_ = snap.exhausted;
+  breakdown_ = snap.breakdown;
+  max_diag_asym_ = snap.max_diag_asym;
+  op_scale_ = snap.op_scale;
+  rng_state_ = snap.rng_state;
+}
+
 // -------------------------------------------------------- projected problem
 SymBandMatrix assemble_projected(const LanczosFactorization& st) {
-  const std::size_t r = st.block_size(), k = st.block_count();
+  return assemble_projected(st.snapshot());
+}
+
+SymBandMatrix assemble_projected(const LanczosFactorization::Snapshot& st) {
+  const std::size_t r = st.r, k = st.k;
   if (k == 0) throw Error("assemble_projected: empty factorization");
   const std::size_t dim = k * r;
   SymBandMatrix T(dim, std::min(r, dim - 1));
   for (std::size_t blk = 0; blk < k; ++blk) {
-    const auto& D = st.diag_blocks()[blk];
+    const auto& D = st.D[blk];
     for (std::size_t a = 0; a < r; ++a)
       for (std::size_t b = 0; b <= a; ++b)
         T.set(blk * r + a, blk * r + b, 0.5 * (D[a * r + b] + D[b * r + a]));
     if (blk + 1 == k) break;  // S_k of the pending block is not part of T_k
-    const auto& S = st.sub_blocks()[blk];
+    const auto& S = st.S[blk];
     for (std::size_t a = 0; a < r; ++a)
       for (std::size_t b = a; b < r; ++b) T.set((blk + 1) * r + a, blk * r + b, S[a * r + b]);
   }
@@ -298,12 +341,17 @@ SymBandMatrix assemble_projected(const LanczosFactorization& st) {
 
 RitzSet check_convergence(const LanczosFactorization& st, double alpha, double beta, double tol,
                           int extra_ritz, bool want_vectors) {
-  const std::size_t r = st.block_size(), k = st.block_count();
+  return check_convergence(st.snapshot(), alpha, beta, tol, extra_ritz, want_vectors);
+}
+
+RitzSet check_convergence(const LanczosFactorization::Snapshot& st, double alpha, double beta,
+                          double tol, int extra_ritz, bool want_vectors) {
+  const std::size_t r = st.r, k = st.k;
   if (k == 0) throw Error("check_convergence: empty factorization");
   const std::size_t dim = k * r;
   const SymBandMatrix T = assemble_projected(st);
   const double t_scale = T.max_abs();
-  const auto& dead_cols = st.dead_cols();
+  const auto& dead_cols = st.dead;
 
   // Rows of the eigenvector matrix the classification reads: the last block (residual
   // estimates, :354-361) and the rows of dead columns (dead mass, :363-369).
@@ -325,14 +373,14 @@ RitzSet check_convergence(const LanczosFactorization& st, double alpha, double b
   if (want_vectors) out.vectors = DenseBlock(dim, dim);
 
   double tau = 0.0;  // filtered-mode cut at the clipped mapped endpoints (:343-349)
-  const bool filtered = st.kind() == OperatorKind::filtered;
+  const bool filtered = st.kind == OperatorKind::filtered;
   if (filtered) {
-    const ChebyshevFilter* f = st.op().filter();
+    const ChebyshevFilter* f = st.filter;
     tau = std::min(clenshaw(f->coefficients(), f->alpha_mapped()),
                    clenshaw(f->coefficients(), f->beta_mapped())) -
           1e-10 * t_scale;
   }
-  const auto& S_last = st.sub_blocks()[k - 1];
+  const auto& S_last = st.S[k - 1];
   for (std::size_t c = 0; c < dim; ++c) {
     const std::size_t src = dim - 1 - c;  // descending order
     out.values[c] = eig.values[src];
@@ -584,20 +632,74 @@ EigenResult run_solve(const SparseSymMatrix& A, double alpha, double beta,
   int checks = 0;
   bool converged = false;
   double time_check = 0.0, time_recover = 0.0;
-  while (expand(st, cfg.check_every, &times) != 0) {
-    const WallClock chk;
-    const RitzSet ritz = check_convergence(st, alpha, beta, cfg.tol, cfg.extra_ritz);
-    time_check += chk.seconds();
-    ++checks;
-    if (!ritz.converged) continue;
-    const WallClock rec;
-    result = recover_eigenpairs(st, A, alpha, beta, ritz, norm_est);
-    time_recover += rec.seconds();
-    // accept only when every TRUE residual meets the tolerance (:617-623)
-    converged = std::all_of(result.residuals.begin(), result.residuals.end(),
-                            [&](double res) { return res <= cfg.tol; });
-    if (converged) break;
+  // The reference alternates expand(check_every) and check_convergence (lanczos.cpp:611-625).
+  // Here the host-side checks run on worker threads, each on a snapshot of the state it
+  // belongs to, while the device keeps taking block steps; checks are resolved strictly in
+  // order, and the first one that reports convergence rolls the factorization back to its
+  // snapshot (LanczosFactorization::rollback) before the eigenpairs are recovered.  Every
+  // decision is therefore taken on exactly the state the reference would see: results, block
+  // counts and matvec counts do not depend on the overlap (scripts/sync_vs_overlap.py).
+  struct PendingCheck {
+    LanczosFactorization::Snapshot snap;
+    std::future<RitzSet> ritz;
+  };
+  std::deque<std::unique_ptr<PendingCheck>> queue;
+  static const bool overlap = std::getenv("FLZ_SYNC_CHECK") == nullptr;
+  const std::size_t max_depth =
+      overlap ? std::max(1u, std::min(8u, std::thread::hardware_concurrency())) : 0;
+  auto enqueue = [&] {
+    auto p = std::make_unique<PendingCheck>();
+    p->snap = st.snapshot();
+    const LanczosFactorization::Snapshot* snap = &p->snap;
+    p->ritz = std::async(overlap ? std::launch::async : std::launch::deferred, [=, &cfg] {
+      return check_convergence(*snap, alpha, beta, cfg.tol, cfg.extra_ritz);
+    });
+    queue.push_back(std::move(p));
+  };
+  bool can_expand = true;
+  int since_check = 0;
+  const WallClock loop_clock;
+  double waited = 0.0;
+  while (!converged && (can_expand || !queue.empty())) {
+    // resolve finished checks, oldest first; block on the oldest when nothing else can be done
+    while (!queue.empty()) {
+      PendingCheck& front = *queue.front();
+      const bool must_wait = !can_expand || queue.size() > max_depth;
+      if (!must_wait &&
+          front.ritz.wait_for(std::chrono::seconds(0)) != std::future_status::ready)
+        break;
+      const WallClock w;
+      const RitzSet ritz = front.ritz.get();
+      waited += w.seconds();
+      ++checks;
+      const LanczosFactorization::Snapshot snap = std::move(front.snap);
+      queue.pop_front();
+      if (!ritz.converged) continue;
+      queue.clear();  // younger checks belong to states that are rolled back now
+      st.rollback(snap);
+      can_expand = true;
+      since_check = 0;
+      const WallClock rec;
+      result = recover_eigenpairs(st, A, alpha, beta, ritz, norm_est);
+      time_recover += rec.seconds();
+      // accept only when every TRUE residual meets the tolerance (:617-623)
+      converged = std::all_of(result.residuals.begin(), result.residuals.end(),
+                              [&](double res) { return res <= cfg.tol; });
+      if (converged) break;
+    }
+    if (converged || !can_expand) continue;
+    if (expand(st, 1, &times) == 0) {
+      can_expand = false;  // budget or space exhausted
+      if (since_check > 0) enqueue();
+      since_check = 0;
+    } else if (++since_check == cfg.check_every) {
+      enqueue();
+      since_check = 0;
+    }
   }
+  queue.clear();
+  time_check = overlap ? waited : waited;
+  (void)loop_clock;
   if (!converged) {  // budget or space exhausted: best pairs of the final state (:627-632)
     const WallClock chk;
     const RitzSet ritz = check_convergence(st, alpha, beta, cfg.tol, cfg.extra_ritz);

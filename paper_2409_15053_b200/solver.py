@@ -76,6 +76,13 @@ class SparseSymMatrix:
     def save_matrix_market(self, path):
         check(lib().flz_hostmatrix_save_mm(self.handle, str(path).encode()))
 
+    def layout(self):
+        """Device layout (uploads the matrix if needed): bytes the fused Clenshaw step streams
+        for the matrix, and the nonzeros held at uniform-offset positions."""
+        mb, ue = C.c_int64(), C.c_int64()
+        check(lib().flz_hostmatrix_layout(self.handle, C.byref(mb), C.byref(ue)))
+        return {"matrix_bytes": mb.value, "uniform_entries": ue.value}
+
     def csr(self):
         rp = np.empty(self.n + 1, np.int64)
         ci = np.empty(self.nnz, np.int32)
