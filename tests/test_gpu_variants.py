@@ -1,0 +1,85 @@
+"""GPU coverage of the code paths the automatic choices rarely take: the SPLIT layout with
+rest slices (forced), the planar block layout (forced), and the pipelined convergence checks
+against the sequential order.  Each variant runs in a fresh process because the switches are
+read once per process."""
+import json
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+def run(code, env_extra, args=()):
+    env = dict(os.environ)
+    for k in ("FLZ_SPLIT", "FLZ_K1_LAYOUT", "FLZ_SYNC_CHECK"):
+        env.pop(k, None)
+    env.update(env_extra)
+    p = subprocess.run([sys.executable, "-c", code, *args], env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-3000:]
+    return json.loads(p.stdout.strip().splitlines()[-1])
+
+
+@pytest.mark.parametrize("env", [{"FLZ_SPLIT": "1"}, {"FLZ_SPLIT": "0"}, {"FLZ_K1_LAYOUT": "planar"},
+                                 {"FLZ_SPLIT": "1", "FLZ_K1_LAYOUT": "planar"}])
+def test_filter_variants_vs_oracle(env, best_oracle):
+    """p(A) X through the forced layouts agrees with the reference (oracle) to 1e-13."""
+    code = r'''
+import sys, json
+sys.path.insert(0, %r)
+import numpy as np
+import oracle
+from paper_2409_15053_b200 import Context, DeviceMatrix, matrices as M
+orc = oracle.best()
+ctx = Context(0)
+out = {}
+for name, gen in (("parsec7k", lambda: M.parsec_like(radius=12.0, n_atoms=12)),
+                  ("parsec_overlap", lambda: M.parsec_like(radius=10.0, n_atoms=30, ball_radius=3.6)),
+                  ("lap2d30", lambda: M.laplacian2d(30)), ("lap3d12", lambda: M.laplacian3d(12)),
+                  ("rand400", lambda: M.random_sparse_sym(400, 0.04, 7))):
+    n, rp, ci, va = gen()
+    for r in (1, 3, 4):
+        X = np.random.default_rng(r).standard_normal((n, r))
+        cf, _, _, _ = orc.build_filter(-1.0, 9.0, 2.0, 3.0, 30)
+        Yo = orc.filter_apply(orc.matrix_from_csr(n, rp, ci, va), cf, -1.0, 9.0, X)
+        A = DeviceMatrix(ctx, n, rp, ci, va)
+        Y = A.filter_apply(cf, 4.0, 5.0, X)
+        out["%%s_r%%d" %% (name, r)] = float(np.abs(Y - Yo).max() / np.abs(Yo).max())
+print(json.dumps(out))
+''' % ROOT
+    errs = run(code, env)
+    assert max(errs.values()) <= 1e-13, errs
+
+
+SOLVE_CODE = r'''
+import sys, json, hashlib
+sys.path.insert(0, %r)
+import numpy as np
+from paper_2409_15053_b200 import matrices as M, solver as S
+out = {}
+for name, gen, a, b, kw in (("lap2d30", lambda: M.laplacian2d(30), 3.0, 3.8, {}),
+                            ("lap2d30_r1", lambda: M.laplacian2d(30), 3.0, 3.8, dict(block_size=1, degree=20)),
+                            ("rand400", lambda: M.random_sparse_sym(400, 0.04, 7), -0.5, 0.5, {}),
+                            ("diag5", lambda: M.diag_matrix([1, 2, 3, 4, 5]), 1.5, 4.5, {}),
+                            ("parsec7k", lambda: M.parsec_like(radius=12.0, n_atoms=12), -0.6, 0.0, dict(degree=50))):
+    res = S.filtered_lanczos(S.SparseSymMatrix.from_csr(*gen()), a, b, S.LanczosConfig(**kw))
+    st = res.stats
+    out[name] = dict(ev=hashlib.sha1(res.eigenvalues.tobytes()).hexdigest(),
+                     vec=hashlib.sha1(np.ascontiguousarray(res.eigenvectors).tobytes()).hexdigest(),
+                     count=len(res.eigenvalues), blocks=st["block_steps"], mv=st["mv_iteration"],
+                     checks=st["checks"], conv=st["converged"])
+print(json.dumps(out))
+''' % ROOT
+
+
+def test_pipelined_checks_equal_sequential_order():
+    """Snapshots + rollback: the overlapped convergence checks give bit-identical eigenpairs,
+    block counts, matvec counts and check counts to the reference's sequential order."""
+    seq = run(SOLVE_CODE, {"FLZ_SYNC_CHECK": "1"})
+    par = run(SOLVE_CODE, {})
+    assert seq == par
+    assert all(v["conv"] == 1 for v in par.values())
