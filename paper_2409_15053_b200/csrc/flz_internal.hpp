@@ -169,6 +169,8 @@ struct flz_matrix {
   flz::DevBuf<flz::SliceTask> tasks_rest_all, tasks_rest_interior, tasks_rest_boundary;
   int64_t nt_rest_all = 0, nt_rest_interior = 0, nt_rest_boundary = 0;
   mutable flz::DevBuf<double> w;    // partial sums of the rest slices, (nl x kMaxFuse) rows
+  flz::DevBuf<int32_t> units[6];    // sub-slice work units (host/plan.hpp)
+  int64_t nunits[6] = {};
   flz::DevBuf<int32_t> perm;        // [nl] new -> old
   flz::DevBuf<int32_t> iperm;       // [nl] old -> new
   flz::DevBuf<int32_t> interior;    // slice ids without halo references
@@ -228,6 +230,7 @@ struct SellView {
   int64_t ntasks;
   bool short_rows;           // every slice fits one warp: the one-warp-per-slice kernel is best
   bool lean;                 // ... and has <= kUgInline uniform positions (stencils)
+  bool mostly_uniform;       // SPLIT mode: the main slices are (almost) only uniform positions
   const int64_t* slice_ptr;
   const int32_t* slice_len;
   const int32_t* row_len;
@@ -247,6 +250,9 @@ struct SellView {
   const int32_t* rest_rows;
   int64_t rest_base;
   double* W;
+  // sub-slice kernel: work units (slice * 8 + row group) of this launch
+  const int32_t* units;
+  int64_t nunits;
 };
 
 enum class StepMode { step, final, plain, rest };

@@ -648,6 +648,32 @@ HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<in
   P.tasks_all = build_tasks(all, ug_len);
   P.tasks_interior = build_tasks(P.interior, ug_len);
   P.tasks_boundary = build_tasks(P.boundary, ug_len);
+  {  // sub-slice work units: position groups per slice from its length
+    static const int scale = [] {
+      const char* e = std::getenv("FLZ_K1_PG_BASE");  // experiments: positions per lane target
+      return e ? std::max(1, std::atoi(e)) : 12;
+    }();
+    for (int64_t s = 0; s < nslices + P.nrest; ++s) {
+      const int32_t L = ug_len[s];
+      const int g = L <= scale ? 0 : (L <= 2 * scale ? 1 : (L <= 4 * scale ? 2 : 3));
+      P.ug_slice[s].reserved = (P.ug_slice[s].reserved & 0xff) | (g << 8);
+    }
+    auto build_units = [&](const std::vector<int32_t>& ids, std::vector<int32_t>& out) {
+      out.clear();
+      for (int32_t s : ids) {
+        const int groups = 1 << ((P.ug_slice[s].reserved >> 8) & 3);
+        for (int rg = 0; rg < groups; ++rg) out.push_back(s * 8 + rg);
+      }
+    };
+    std::vector<int32_t> rest_all(P.rest_interior);
+    rest_all.insert(rest_all.end(), P.rest_boundary.begin(), P.rest_boundary.end());
+    build_units(all, P.units[0]);
+    build_units(P.interior, P.units[1]);
+    build_units(P.boundary, P.units[2]);
+    build_units(rest_all, P.units[3]);
+    build_units(P.rest_interior, P.units[4]);
+    build_units(P.rest_boundary, P.units[5]);
+  }
   P.short_rows = std::all_of(P.tasks_all.begin(), P.tasks_all.end(),
                              [](const PlanTask& t) { return t.warps_per_slice == 1; });
   P.lean = P.short_rows;

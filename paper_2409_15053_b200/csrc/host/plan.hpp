@@ -51,6 +51,11 @@ struct HostPlan {
   std::vector<PlanTask> tasks_all, tasks_interior, tasks_boundary;
   bool short_rows = false;
   bool lean = false;   // short_rows and every main slice has <= 8 uniform positions
+  // Work units of the sub-slice kernel: a slice with 2^g position groups (bits 8-9 of its
+  // descriptor flags, chosen from its length) is processed by 2^g warps, each taking
+  // 32 / 2^g of its rows and striding the positions 2^g-way inside the warp.  A unit is
+  // slice * 8 + row group.  Lists: 0 all main, 1 interior, 2 boundary, 3-5 the same for rest.
+  std::vector<int32_t> units[6];
   // index-compressed copy of the same slices (same rows, same permutation)
   std::vector<PlanUgSlice> ug_slice;
   std::vector<double> ug_val;

@@ -26,6 +26,8 @@
 //    accumulated left to right in CSR order with separately rounded multiply and add (the
 //    reference's scalar TU is built without FMA), the combine is ((s1*w + s2*y1) - y2) + b*x.
 
+#include <cstdlib>
+
 #include "flz_internal.hpp"
 
 namespace flz {
@@ -485,6 +487,86 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, (LEAN && R <= 3) ? FLZ_K1
   }
 }
 
+// Medium and long slices: one warp per SUB-SLICE.  A slice with G = 2^g position groups is
+// processed by G warps; each takes RW = 32 / G consecutive rows and lays its lanes out as
+// RW rows x G groups: lane (row, grp) walks positions grp, grp + G, grp + 2G, ...  The G
+// partial sums of a row meet by warp shuffles, so there is no shared memory and no barrier,
+// and a 37-position slice gives four warps of ~9 positions per lane instead of one warp of
+// 37 — the parallelism a 113k-row matrix needs to fill 148 SMs.  Per position and lane:
+// one value, one index (uniform offset — the lanes of a group read the same word — or
+// general column), one gather.
+template <int R, int S, int MODE, int U>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, 5)
+    clenshaw_step_ug_sub(SellView A, double s1, double s2, double b,
+                         const double* __restrict__ Y1, double* __restrict__ Y2, int64_t ldy,
+                         const double* __restrict__ X, int64_t ldx, double* __restrict__ Out,
+                         int64_t ldo) {
+  const int lane = threadIdx.x & 31;
+  const int64_t unit = (int64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  if (unit >= A.nunits) return;
+  const int packed = __ldg(A.units + unit);
+  const int64_t slice = packed >> 3;
+  const int rg = packed & 7;
+  const UgSlice H = load_ug_header(A.ug + slice);
+  const int glog = (H.reserved >> 8) & 3;
+  const int G = 1 << glog, RW = 32 >> glog;
+  const int lrow = lane & (RW - 1), grp = lane >> (5 - glog);
+  const int srow = rg * RW + lrow;  // row inside the slice
+  int64_t row;
+  if constexpr (MODE == 3) {
+    const int r = A.rest_rows[(slice - A.rest_base) * kSliceRows + srow];
+    row = r < 0 ? A.nl : r;
+  } else {
+    row = slice * kSliceRows + srow;
+  }
+  if constexpr (MODE != 2 && MODE != 3) {
+    if (grp == 0) prefetch_own<R, S, MODE>(A, row, Y2, ldy, X, ldx);
+  }
+  const int nu = H.nu, L = H.nu + H.ng;
+  const int cmax = (int)A.ncols - 1;
+  const int crow = (H.reserved & 2) ? 0 : (int)row;  // flag bit 1: absolute shared columns
+  const double* __restrict__ val = A.ug_val + H.val_ptr + srow;
+  const int32_t* __restrict__ col = A.ug_col + H.col_ptr + srow - (int64_t)nu * kSliceRows;
+  const int32_t* __restrict__ uoff = A.ug_uoff + H.uoff_ptr;
+  double acc[R];
+#pragma unroll
+  for (int k = 0; k < R; ++k) acc[k] = 0.0;
+  for (int p0 = grp; p0 < L; p0 += U * G) {  // p0 differs per group; the trip count may too
+    double v[U], g[U][R];
+    int c[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int p = p0 + u * G;
+      const bool ok = p < L;
+      v[u] = ok ? ld_stream_f64(val + (int64_t)p * kSliceRows) : 0.0;
+      int idx = 0;
+      if (ok) idx = p < nu ? __ldg(uoff + p) : ld_stream_s32(col + (int64_t)p * kSliceRows);
+      c[u] = p < nu ? min(max(crow + idx, 0), cmax) : idx;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) gather_row<R, S>(Y1, ldy, c[u], p0 + u * G < L, g[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int k = 0; k < R; ++k) acc[k] = fma(v[u], g[u][k], acc[k]);
+  }
+  // the G partial sums of a row sit RW lanes apart (fixed order: deterministic)
+  for (int m = RW; m < 32; m <<= 1) {
+#pragma unroll
+    for (int k = 0; k < R; ++k) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], m);
+  }
+  if (grp != 0 || row >= A.nl) return;
+  if constexpr (MODE == 3) {
+#pragma unroll
+    for (int k = 0; k < R; ++k) A.W[row * kMaxFuse + k] = acc[k];
+  } else {
+    if (H.reserved & 1) add_rest<R>(A, row, acc);
+    double y1o[R], y2o[R], xo[R];
+    load_own<R, S, MODE>(A, row, Y1, Y2, ldy, X, ldx, y1o, y2o, xo);
+    finish_row<R, S, MODE>(row, s1, s2, b, acc, y1o, y2o, xo, Y2, ldy, Out, ldo);
+  }
+}
+
 // Long slices: CTAs of 8 warps walk a contiguous range of a host-built task list; a task
 // gives each of its slices 1, 2, 4 or 8 warps, whose partial sums meet in shared memory in
 // a fixed order (deterministic).
@@ -617,23 +699,36 @@ void launch_simple(flz_ctx* ctx, const SellView& A, double s1, double s2, double
 template <int R, int S, int MODE>
 void launch_ug(flz_ctx* ctx, const SellView& A, double s1, double s2, double b, const double* Y1,
                double* Y2, int64_t ldy, const double* X, int64_t ldx, double* Out, int64_t ldo) {
-  bool warp_kernel = false;
-  if constexpr (MODE != 3) warp_kernel = A.short_rows;
-  if (warp_kernel) {
+  // kernel choice: stencils (every slice <= 8 uniform positions) -> lean one-warp-per-slice
+  // kernel; everything else -> multi-warp task kernel.  The sub-slice kernel is kept for A/B
+  // measurements (FLZ_K1_KERNEL=sub, or =mixed: sub-slice kernel for the uniform main part of
+  // a SPLIT matrix only).  Measured on the PARSEC-shaped matrix (3 columns, per step):
+  // tasks 34.9 us, sub 40.8-49.6 us (its lanes mix positions, which costs L1 wavefronts on
+  // general positions), SPLIT + mixed 40.2 us.
+  static const char kernel_choice = [] {
+    const char* e = std::getenv("FLZ_K1_KERNEL");
+    return e ? e[0] : 't';
+  }();
+  const bool use_tasks = kernel_choice == 't' || (kernel_choice == 'm' && (MODE == 3 || !A.mostly_uniform));
+  bool lean = false;
+  if constexpr (MODE != 3) lean = A.short_rows && A.lean;
+  if (lean) {
     if constexpr (MODE != 3) {
-    if (A.nslices == 0) return;
-    const int spc = ctx->k1_slices_per_cta > 0 ? ctx->k1_slices_per_cta : FLZ_K1_SLICES_PER_CTA;
-    const unsigned grid = (unsigned)((A.nslices + spc - 1) / spc);
-    if (!A.lean)
-      clenshaw_step_ug_warp<R, S, MODE, 8, false><<<grid, kWarpsPerBlock * 32, 0, ctx->stream>>>(
-          A, spc, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo);
-    else if ((ctx->k1_batch > 0 ? ctx->k1_batch : FLZ_K1_UB) >= 8)
-      clenshaw_step_ug_warp<R, S, MODE, 8, true><<<grid, kWarpsPerBlock * 32, 0, ctx->stream>>>(
-          A, spc, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo);
-    else
-      clenshaw_step_ug_warp<R, S, MODE, 4, true><<<grid, kWarpsPerBlock * 32, 0, ctx->stream>>>(
-          A, spc, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo);
+      if (A.nslices == 0) return;
+      const int spc = ctx->k1_slices_per_cta > 0 ? ctx->k1_slices_per_cta : FLZ_K1_SLICES_PER_CTA;
+      const unsigned grid = (unsigned)((A.nslices + spc - 1) / spc);
+      if ((ctx->k1_batch > 0 ? ctx->k1_batch : FLZ_K1_UB) >= 8)
+        clenshaw_step_ug_warp<R, S, MODE, 8, true><<<grid, kWarpsPerBlock * 32, 0, ctx->stream>>>(
+            A, spc, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo);
+      else
+        clenshaw_step_ug_warp<R, S, MODE, 4, true><<<grid, kWarpsPerBlock * 32, 0, ctx->stream>>>(
+            A, spc, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo);
     }
+  } else if (!use_tasks) {
+    if (A.nunits == 0) return;
+    const unsigned grid = (unsigned)((A.nunits + kWarpsPerBlock - 1) / kWarpsPerBlock);
+    clenshaw_step_ug_sub<R, S, MODE, 4><<<grid, kWarpsPerBlock * 32, 0, ctx->stream>>>(
+        A, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo);
   } else {
     if (A.ntasks == 0) return;
     const int tpc = ctx->k1_tasks_per_cta > 0 ? ctx->k1_tasks_per_cta : FLZ_K1_TASKS_PER_CTA;
