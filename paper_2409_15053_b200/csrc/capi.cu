@@ -105,13 +105,13 @@ void ensure_exact_arrays(const flz_matrix* A) {
 }
 
 SellView make_view(const flz_matrix* A, const SliceTask* tasks, int64_t ntasks,
-                   const int32_t* slice_ids, int64_t nslices, int unit_list) {
+                   const int32_t* slice_ids, int64_t nslices) {
   ensure_exact_arrays(A);
   return SellView{tasks,        ntasks,     A->short_rows, A->lean, A->split, A->slice_ptr.p, A->slice_len.p,
                   A->row_len.p, A->col.p,   A->val.p,      slice_ids,      nslices,
                   A->nl,        A->ug.p,    A->ug_val.p,   A->ug_col.p,    A->ug_uoff.p,
                   A->nl + A->nhalo, A->rest_rows.p, A->nslices,   A->w.p,
-                  A->units[unit_list].p, A->nunits[unit_list]};
+                  A->uv_pairs.p};
 }
 // rest launches (SPLIT mode): task lists over the rest slices
 SellView view_rest(const flz_matrix* A, int which) {
@@ -119,16 +119,16 @@ SellView view_rest(const flz_matrix* A, int which) {
       which == 0 ? A->tasks_rest_all : (which == 1 ? A->tasks_rest_interior : A->tasks_rest_boundary);
   const int64_t nt =
       which == 0 ? A->nt_rest_all : (which == 1 ? A->nt_rest_interior : A->nt_rest_boundary);
-  return make_view(A, t.p, nt, nullptr, A->nrest, 3 + which);
+  return make_view(A, t.p, nt, nullptr, A->nrest);
 }
 SellView view_all(const flz_matrix* A) {
-  return make_view(A, A->tasks_all.p, A->nt_all, nullptr, A->nslices, 0);
+  return make_view(A, A->tasks_all.p, A->nt_all, nullptr, A->nslices);
 }
 SellView view_interior(const flz_matrix* A) {
-  return make_view(A, A->tasks_interior.p, A->nt_interior, A->interior.p, A->n_interior, 1);
+  return make_view(A, A->tasks_interior.p, A->nt_interior, A->interior.p, A->n_interior);
 }
 SellView view_boundary(const flz_matrix* A) {
-  return make_view(A, A->tasks_boundary.p, A->nt_boundary, A->boundary.p, A->n_boundary, 2);
+  return make_view(A, A->tasks_boundary.p, A->nt_boundary, A->boundary.p, A->n_boundary);
 }
 
 // leading dimension of the planar filter workspaces (local rows + halo rows, padded)
@@ -222,6 +222,7 @@ int row_stride(const flz_matrix* A, int R) {
   const bool planar = force && force[0] == 'p';
   if (planar) return 0;
   if (R != 3) return R;
+  if (force && force[0] == '4') return 4;  // experiments: padded rows for every matrix
   return (A->nnz >= 16 * A->nl) ? 4 : 3;
 }
 
@@ -527,15 +528,12 @@ static void upload_plan(flz_ctx* ctx, HostPlan& P, flz_matrix* A) {
   up(A->ug_val, P.ug_val);
   up(A->ug_col, P.ug_col);
   up(A->ug_uoff, P.ug_uoff);
+  up(A->uv_pairs, P.uv_pairs);
   A->ug_bytes = (int64_t)(P.ug_val.size() * 8 + P.ug_col.size() * 4 + P.ug_uoff.size() * 4 +
                           P.ug_slice.size() * sizeof(UgSlice));
   A->ug_uniform_entries = P.ug_uniform_entries;
   A->split = P.split;
   A->nrest = P.nrest;
-  for (int i = 0; i < 6; ++i) {
-    A->nunits[i] = (int64_t)P.units[i].size();
-    up(A->units[i], P.units[i]);
-  }
   up(A->rest_rows, P.rest_rows);
   A->ug_bytes += (int64_t)P.rest_rows.size() * 4;
   up(A->perm, P.perm);

@@ -160,6 +160,7 @@ struct flz_matrix {
   flz::DevBuf<flz::UgSlice> ug;     // [nslices]
   flz::DevBuf<double> ug_val;
   flz::DevBuf<int32_t> ug_col, ug_uoff;
+  flz::DevBuf<double> uv_pairs;     // lean matrices: 16 doubles per slice (host/plan.hpp)
   int64_t ug_bytes = 0;             // matrix bytes one fast step streams
   int64_t ug_uniform_entries = 0;
   // SPLIT mode (host/plan.hpp): rest slices follow the main ones in `ug`
@@ -169,8 +170,6 @@ struct flz_matrix {
   flz::DevBuf<flz::SliceTask> tasks_rest_all, tasks_rest_interior, tasks_rest_boundary;
   int64_t nt_rest_all = 0, nt_rest_interior = 0, nt_rest_boundary = 0;
   mutable flz::DevBuf<double> w;    // partial sums of the rest slices, (nl x kMaxFuse) rows
-  flz::DevBuf<int32_t> units[6];    // sub-slice work units (host/plan.hpp)
-  int64_t nunits[6] = {};
   flz::DevBuf<int32_t> perm;        // [nl] new -> old
   flz::DevBuf<int32_t> iperm;       // [nl] old -> new
   flz::DevBuf<int32_t> interior;    // slice ids without halo references
@@ -250,9 +249,7 @@ struct SellView {
   const int32_t* rest_rows;
   int64_t rest_base;
   double* W;
-  // sub-slice kernel: work units (slice * 8 + row group) of this launch
-  const int32_t* units;
-  int64_t nunits;
+  const double* uv_pairs;    // lean matrices: (value, mask) pairs, 16 doubles per slice
 };
 
 enum class StepMode { step, final, plain, rest };

@@ -6,6 +6,7 @@
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <exception>
 #include <mutex>
 #include <thread>
@@ -92,6 +93,12 @@ void run_chunks(int nchunks, F&& body) {
   if (err) std::rethrow_exception(err);
 }
 
+// Doubles the (value, mask) pairs of nuv uniform-value positions occupy in front of the
+// per-lane value rows of a slice (mirrors ug_header_doubles in kernels_sell.cu)
+int64_t ug_header_doubles(int nuv, int lane_rows) {
+  return lane_rows > 0 ? (2 * nuv + 15) / 16 * 16 : 2 * nuv;
+}
+
 // ---- UG layout -------------------------------------------------------------------------
 // A diagonal offset d = col - row that at least kUgMinLanes of a slice's 32 lanes hold is
 // stored as ONE uniform position: 32 values + one int32, the lanes without it get a zero.
@@ -120,7 +127,8 @@ struct OffsetCounter {  // open-addressing counter of the offsets of one slice
 };
 
 // returns the number of spilled entries
-int64_t build_ug(HostPlan& P, const std::vector<uint8_t>& is_boundary, bool allow_spill) {
+int64_t build_ug(HostPlan& P, const std::vector<uint8_t>& is_boundary, bool allow_spill,
+                 bool allow_uv) {
   const int64_t nslices = P.nslices, nl = P.nl;
   P.ug_slice.assign(nslices, PlanUgSlice{});
   P.ug_val.clear();
@@ -140,13 +148,15 @@ int64_t build_ug(HostPlan& P, const std::vector<uint8_t>& is_boundary, bool allo
   };
   // ---- phase A (parallel over chunks of slices): uniform offsets, nu, ng, spill decision
   struct SliceInfo {
-    int32_t nu = 0, ng = 0;
-    uint8_t spill = 0;
-    int64_t uni_begin = 0;  // into the chunk's offset pool
+    int32_t nu = 0, ng = 0, nuv = 0;
+    uint8_t spill = 0, own_first = 0;
+    int64_t uni_begin = 0;  // into the chunk's offset pool (UV offsets first, each run sorted)
   };
   struct Chunk {
     int64_t s0 = 0, s1 = 0;
     std::vector<int64_t> uni_pool;
+    std::vector<double> uv_value;   // per pooled offset: the common value (UV offsets only)
+    std::vector<uint32_t> uv_mask;  // per pooled offset: lanes that hold the entry
     int64_t uniform_entries = 0;
     std::vector<RestRow> rest;
     std::vector<int32_t> rest_col;
@@ -162,7 +172,10 @@ int64_t build_ug(HostPlan& P, const std::vector<uint8_t>& is_boundary, bool allo
   run_chunks(nchunks, [&](int t) {
     Chunk& C = chunks[t];
     OffsetCounter counter(cap);
-    std::vector<int64_t> uni;
+    std::vector<int64_t> uni, uni_sorted;
+    std::vector<double> uval;
+    std::vector<uint32_t> umask;
+    std::vector<uint8_t> usame;
     int32_t glen[kPlanSliceRows];
     for (int64_t s = C.s0; s < C.s1; ++s) {
       const int32_t L = P.slice_len[s];
@@ -180,14 +193,26 @@ int64_t build_ug(HostPlan& P, const std::vector<uint8_t>& is_boundary, bool allo
       std::sort(uni.begin(), uni.end());
       // general part: what every lane keeps after its uniform entries are taken out
       int32_t ng = 0;
+      uval.assign(uni.size(), 0.0);
+      umask.assign(uni.size(), 0u);
+      usame.assign(uni.size(), 1);
       if (!uni.empty()) {
         for (int l = 0; l < kPlanSliceRows; ++l) {
           const int64_t row = s * kPlanSliceRows + l;
           const int32_t len = row < nl ? P.row_len[row] : 0;
           int32_t g = 0;
           for (int32_t p = 0; p < len; ++p) {
-            const int64_t d = (int64_t)P.col[base + (int64_t)p * kPlanSliceRows + l] - row;
-            if (!std::binary_search(uni.begin(), uni.end(), d)) ++g;
+            const int64_t e = base + (int64_t)p * kPlanSliceRows + l;
+            const int64_t d = (int64_t)P.col[e] - row;
+            const auto it = std::lower_bound(uni.begin(), uni.end(), d);
+            if (it == uni.end() || *it != d) {
+              ++g;
+              continue;
+            }
+            const size_t i = (size_t)(it - uni.begin());  // one value for the whole position?
+            if (umask[i] == 0u) uval[i] = P.val[e];
+            else if (uval[i] != P.val[e]) usame[i] = 0;
+            umask[i] |= 1u << l;
           }
           glen[l] = g;
           ng = std::max(ng, g);
@@ -218,7 +243,24 @@ int64_t build_ug(HostPlan& P, const std::vector<uint8_t>& is_boundary, bool allo
       I.ng = ng;
       I.spill = spill;
       I.uni_begin = (int64_t)C.uni_pool.size();
-      C.uni_pool.insert(C.uni_pool.end(), uni.begin(), uni.end());
+      // uniform-value offsets first (at most 255), then the per-lane-value ones
+      {
+        std::vector<size_t> head, tail;
+        for (size_t i = 0; i < uni.size(); ++i)
+          (allow_uv && usame[i] && head.size() < 255 ? head : tail).push_back(i);
+        I.nuv = (int32_t)head.size();
+        I.own_first = 0;  // offsets stay ascending: the summation order of a row is its CSR order
+        for (size_t i : head) {
+          C.uni_pool.push_back(uni[i]);
+          C.uv_value.push_back(uval[i]);
+          C.uv_mask.push_back(umask[i]);
+        }
+        for (size_t i : tail) {
+          C.uni_pool.push_back(uni[i]);
+          C.uv_value.push_back(0.0);
+          C.uv_mask.push_back(0u);
+        }
+      }
     }
   });
   // ---- phase B (serial): pointers; identical consecutive offset lists (every interior slice
@@ -236,7 +278,7 @@ int64_t build_ug(HostPlan& P, const std::vector<uint8_t>& is_boundary, bool allo
         H.col_ptr = cptr;
         H.nu = I.nu;
         H.ng = I.ng;
-        H.reserved = I.spill ? 1 : 0;
+        H.reserved = (I.spill ? 1 : 0) | (I.own_first ? 4 : 0) | (I.nuv << 16);
         if (I.nu > 0 && I.nu == last_nu && std::equal(uni, uni + I.nu, last_uni)) {
           H.uoff_ptr = last_uoff_ptr;
         } else {
@@ -249,7 +291,8 @@ int64_t build_ug(HostPlan& P, const std::vector<uint8_t>& is_boundary, bool allo
           }
         }
         for (int i = 0; i < 8; ++i) H.inline_off[i] = i < I.nu ? (int32_t)uni[i] : 0;
-        vptr += (int64_t)(I.nu + I.ng) * kPlanSliceRows;
+        vptr += ug_header_doubles(I.nuv, I.nu + I.ng - I.nuv) +
+                (int64_t)(I.nu - I.nuv + I.ng) * kPlanSliceRows;
         cptr += (int64_t)I.ng * kPlanSliceRows;
       }
     P.ug_val.assign((size_t)vptr, 0.0);
@@ -262,11 +305,19 @@ int64_t build_ug(HostPlan& P, const std::vector<uint8_t>& is_boundary, bool allo
       const SliceInfo& I = info[s];
       const PlanUgSlice& H = P.ug_slice[s];
       const int64_t* uni = C.uni_pool.data() + I.uni_begin;
+      const int64_t* uv_end = uni + I.nuv;   // runs: [uni, uv_end) (diagonal first) and [uv_end, uni_end)
       const int64_t* uni_end = uni + I.nu;
       const int64_t base = P.slice_ptr[s];
-      const int32_t nu = I.nu, ng = I.ng;
+      const int32_t nu = I.nu, ng = I.ng, nuv = I.nuv;
       const bool spill = I.spill;
-      double* v = P.ug_val.data() + H.val_ptr;
+      double* hdr = P.ug_val.data() + H.val_ptr;
+      for (int32_t i = 0; i < nuv; ++i) {  // (value, lane mask) pairs
+        hdr[2 * i] = C.uv_value[I.uni_begin + i];
+        const uint64_t bits = C.uv_mask[I.uni_begin + i];
+        std::memcpy(&hdr[2 * i + 1], &bits, sizeof(double));
+      }
+      // per-lane value rows: position p >= nuv lives at row p - nuv behind the header
+      double* v = hdr + ug_header_doubles(nuv, nu + ng - nuv) - (int64_t)nuv * kPlanSliceRows;
       int32_t* c = P.ug_col.data() + H.col_ptr;
       for (int l = 0; l < kPlanSliceRows; ++l) {
         const int64_t row = s * kPlanSliceRows + l;
@@ -276,8 +327,13 @@ int64_t build_ug(HostPlan& P, const std::vector<uint8_t>& is_boundary, bool allo
         for (int32_t p = 0; p < len; ++p) {
           const int64_t e = base + (int64_t)p * kPlanSliceRows + l;
           const int64_t d = (int64_t)P.col[e] - row;
-          const int64_t* it = std::lower_bound(uni, uni_end, d);
-          if (it != uni_end && *it == d) {
+          const int64_t* uv_sorted = uni + (I.own_first ? 1 : 0);  // the diagonal may lead the run
+          const int64_t* it = std::lower_bound(uv_sorted, uv_end, d);
+          bool is_uv = (I.own_first && d == 0) || (it != uv_end && *it == d);
+          if (!is_uv) it = std::lower_bound(uv_end, uni_end, d);
+          if (is_uv) {
+            if (P.val[e] != 0.0) ++C.uniform_entries;   // value and lane bit are in the header
+          } else if (it != uni_end && *it == d) {
             v[(int64_t)(it - uni) * kPlanSliceRows + l] += P.val[e];
             if (P.val[e] != 0.0) ++C.uniform_entries;
           } else if (spill) {
@@ -632,9 +688,17 @@ HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<in
     (is_boundary[s] ? P.boundary : P.interior).push_back((int32_t)s);
   timer.lap("SELL arrays");
   // a rest launch per product only pays when it carries a real share of the matrix
-  if (const int64_t spilled = build_ug(P, is_boundary, true);
-      spilled > 0 && 50 * spilled < P.nnz)
-    build_ug(P, is_boundary, false);
+  // uniform-value positions are read by the stencil ("lean") kernel only: try them when the
+  // slices are short, and fall back when the matrix does not qualify for that kernel after all
+  int32_t longest = 0;
+  for (int64_t s = 0; s < nslices; ++s) longest = std::max(longest, P.slice_len[s]);
+  bool allow_uv = longest <= 16;
+  bool allow_spill = true;
+  if (const int64_t spilled = build_ug(P, is_boundary, allow_spill, allow_uv);
+      spilled > 0 && 50 * spilled < P.nnz) {
+    allow_spill = false;
+    build_ug(P, is_boundary, allow_spill, allow_uv);
+  }
   timer.lap("UG layout");
   std::vector<int32_t> ug_len(nslices + P.nrest);  // the fast kernels walk the compressed slices
   for (int64_t s = 0; s < nslices + P.nrest; ++s) ug_len[s] = P.ug_slice[s].nu + P.ug_slice[s].ng;
@@ -648,36 +712,38 @@ HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<in
   P.tasks_all = build_tasks(all, ug_len);
   P.tasks_interior = build_tasks(P.interior, ug_len);
   P.tasks_boundary = build_tasks(P.boundary, ug_len);
-  {  // sub-slice work units: position groups per slice from its length
-    static const int scale = [] {
-      const char* e = std::getenv("FLZ_K1_PG_BASE");  // experiments: positions per lane target
-      return e ? std::max(1, std::atoi(e)) : 12;
-    }();
-    for (int64_t s = 0; s < nslices + P.nrest; ++s) {
-      const int32_t L = ug_len[s];
-      const int g = L <= scale ? 0 : (L <= 2 * scale ? 1 : (L <= 4 * scale ? 2 : 3));
-      P.ug_slice[s].reserved = (P.ug_slice[s].reserved & 0xff) | (g << 8);
-    }
-    auto build_units = [&](const std::vector<int32_t>& ids, std::vector<int32_t>& out) {
-      out.clear();
-      for (int32_t s : ids) {
-        const int groups = 1 << ((P.ug_slice[s].reserved >> 8) & 3);
-        for (int rg = 0; rg < groups; ++rg) out.push_back(s * 8 + rg);
-      }
-    };
-    std::vector<int32_t> rest_all(P.rest_interior);
-    rest_all.insert(rest_all.end(), P.rest_boundary.begin(), P.rest_boundary.end());
-    build_units(all, P.units[0]);
-    build_units(P.interior, P.units[1]);
-    build_units(P.boundary, P.units[2]);
-    build_units(rest_all, P.units[3]);
-    build_units(P.rest_interior, P.units[4]);
-    build_units(P.rest_boundary, P.units[5]);
-  }
   P.short_rows = std::all_of(P.tasks_all.begin(), P.tasks_all.end(),
                              [](const PlanTask& t) { return t.warps_per_slice == 1; });
-  P.lean = P.short_rows;
-  for (int64_t s = 0; s < nslices && P.lean; ++s) P.lean = P.ug_slice[s].nu <= 8;
+  auto is_lean = [&] {
+    bool lean = P.short_rows;
+    for (int64_t s = 0; s < nslices && lean; ++s) lean = P.ug_slice[s].nu <= 8;
+    return lean;
+  };
+  P.lean = is_lean();
+  if (!P.lean && allow_uv) {  // rare: short slices, but not a stencil — redo without pairs
+    build_ug(P, is_boundary, allow_spill, false);
+    std::vector<int32_t> len2(nslices + P.nrest);
+    for (int64_t s = 0; s < nslices + P.nrest; ++s) len2[s] = P.ug_slice[s].nu + P.ug_slice[s].ng;
+    std::vector<int32_t> rest_all(P.rest_interior);
+    rest_all.insert(rest_all.end(), P.rest_boundary.begin(), P.rest_boundary.end());
+    P.tasks_rest_all = build_tasks(rest_all, len2);
+    P.tasks_rest_interior = build_tasks(P.rest_interior, len2);
+    P.tasks_rest_boundary = build_tasks(P.rest_boundary, len2);
+    P.tasks_all = build_tasks(all, len2);
+    P.tasks_interior = build_tasks(P.interior, len2);
+    P.tasks_boundary = build_tasks(P.boundary, len2);
+    P.short_rows = std::all_of(P.tasks_all.begin(), P.tasks_all.end(),
+                               [](const PlanTask& t) { return t.warps_per_slice == 1; });
+    P.lean = false;
+  }
+  P.uv_pairs.clear();
+  if (P.lean) {
+    P.uv_pairs.assign((size_t)nslices * 16, 0.0);
+    for (int64_t s = 0; s < nslices; ++s) {
+      const int nuv = (P.ug_slice[s].reserved >> 16) & 0xff;
+      std::copy_n(P.ug_val.data() + P.ug_slice[s].val_ptr, 2 * nuv, P.uv_pairs.data() + s * 16);
+    }
+  }
   return P;
 }
 

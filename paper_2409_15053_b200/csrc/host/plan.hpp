@@ -25,7 +25,14 @@ struct PlanTask {  // mirrors SliceTask (flz_internal.hpp)
 // Per-slice header of the index-compressed ("UG") layout the fast kernels read: the first
 // `nu` positions of a slice are UNIFORM (every lane's column is its own row + uoff[p], one
 // int32 per position instead of 32), the remaining `ng` positions are GENERAL (one int32 per
-// lane).  Values are [nu + ng][32] doubles; padding entries have value 0 and are skipped.
+// lane).  The first `nuv` (flags bits 16-23) uniform positions also have a UNIFORM VALUE:
+// every lane that holds the entry holds the same number (constant-coefficient stencils), and
+// the slice stores one (value, 32-bit lane mask) pair for the position instead of 32 values.
+// Value block of a slice: nuv pairs (padded to 16 doubles when rows follow), then
+// [nu - nuv + ng][32] doubles; padding entries have value 0 and a harmless column.
+// flags (`reserved`): bit 0 the slice adds rest partial sums, bit 1 the uniform int32 are
+// absolute columns (rest slices), bit 2 position 0 is the diagonal offset 0 with a uniform
+// value (its gather is the slice's own rows), bits 16-23 nuv.
 struct PlanUgSlice {
   int64_t val_ptr;   // element offset into ug_val
   int64_t col_ptr;   // element offset into ug_col (general positions only)
@@ -51,11 +58,10 @@ struct HostPlan {
   std::vector<PlanTask> tasks_all, tasks_interior, tasks_boundary;
   bool short_rows = false;
   bool lean = false;   // short_rows and every main slice has <= 8 uniform positions
-  // Work units of the sub-slice kernel: a slice with 2^g position groups (bits 8-9 of its
-  // descriptor flags, chosen from its length) is processed by 2^g warps, each taking
-  // 32 / 2^g of its rows and striding the positions 2^g-way inside the warp.  A unit is
-  // slice * 8 + row group.  Lists: 0 all main, 1 interior, 2 boundary, 3-5 the same for rest.
-  std::vector<int32_t> units[6];
+  // lean matrices: the (value, mask) pairs of every main slice again, at a fixed stride of 16
+  // doubles per slice, so that the stencil kernel can fetch them without waiting for the
+  // slice descriptor (one dependent memory round trip less per slice)
+  std::vector<double> uv_pairs;
   // index-compressed copy of the same slices (same rows, same permutation)
   std::vector<PlanUgSlice> ug_slice;
   std::vector<double> ug_val;

@@ -27,6 +27,7 @@
 //    reference's scalar TU is built without FMA), the combine is ((s1*w + s2*y1) - y2) + b*x.
 
 #include <cstdlib>
+#include <type_traits>
 
 #include "flz_internal.hpp"
 
@@ -164,38 +165,48 @@ __device__ __forceinline__ void store_row(double* Y, int64_t ldy, int64_t row,
   }
 }
 
+// Doubles the (value, mask) pairs of nuv uniform-value positions occupy in front of the
+// per-lane value rows of a slice: padded to a 128-byte line when per-lane rows follow.
+__host__ __device__ __forceinline__ int ug_header_doubles(int nuv, int lane_rows) {
+  return lane_rows > 0 ? (2 * nuv + 15) / 16 * 16 : 2 * nuv;
+}
+
 // acc[k] += sum over positions [p0, p1) of one compressed slice for one lane (= one row).
-// Positions [0, nu) are uniform: the column is row + uoff[p] (offsets fetched 32 at a time,
-// one per lane, and broadcast by shuffle), clamped into the block because lanes that do not
-// hold the offset carry a zero value there; positions [nu, nu + ng) are general (padding: zero
-// value, own row as column).  The gathers depend only on the index stream, never on the
-// values.  Two tight loops, each software pipelined: the values (and columns) of batch b+1
-// are requested before the gathers of batch b are consumed; all loads of a batch are
-// independent.
+// Position classes, in this order (see host/plan.hpp):
+//   [0, nu)    uniform offset, per-lane values
+//   [nu, L)    general: per-lane value and column (padding: zero value, own row as column)
+// Uniform columns are row + uoff[p] (or the absolute column uoff[p] when flag bit 1 is set),
+// clamped into the block because lanes that do not hold the offset carry a zero there; the
+// offsets are fetched 32 at a time, one per lane, and broadcast by shuffle.
+// The gathers depend only on the index stream, never on the values.  The per-lane loops are
+// software pipelined: the values (and columns) of batch b+1 are requested before the gathers
+// of batch b are consumed; all loads of a batch are independent.
 template <int R, int S, int U>
 __device__ __forceinline__ void ug_accumulate(const SellView& A, const UgSlice& H, int lane,
                                               int64_t row, int p0, int p1,
                                               const double* __restrict__ Y1, int64_t ldy,
                                               double (&acc)[R]) {
+  // (slices with uniform-value pairs only occur in matrices the stencil kernel handles)
   const double* __restrict__ val = A.ug_val + H.val_ptr + lane;
+  constexpr int nuv = 0;
+  const int32_t* __restrict__ uoff = A.ug_uoff + H.uoff_ptr + lane;
+  const int cmax = (int)A.ncols - 1;
+  const int crow = (H.reserved & 2) ? 0 : (int)row;  // flag bit 1: absolute shared columns
   double v[U], vn[U];
-  // ---- uniform positions [p0, pu1)
-  const int pu1 = min(p1, H.nu);
-  if (p0 < pu1) {
-    const int32_t* __restrict__ uoff = A.ug_uoff + H.uoff_ptr + lane;
-    const int cmax = (int)A.ncols - 1;
-    const int crow = (H.reserved & 2) ? 0 : (int)row;  // flag bit 1: absolute shared columns
-    int myoff = p0 + lane < pu1 ? __ldg(uoff + p0) : 0;
-    const double* vp = val + (int64_t)p0 * kSliceRows;
+  // ---- uniform positions with per-lane values [pu0, pu1)
+  const int pu0 = max(p0, nuv), pu1 = min(p1, H.nu);
+  if (pu0 < pu1) {
+    int myoff = pu0 + lane < pu1 ? __ldg(uoff + pu0) : 0;
+    const double* vp = val + (int64_t)pu0 * kSliceRows;
 #pragma unroll
-    for (int u = 0; u < U; ++u) v[u] = p0 + u < pu1 ? ld_stream_f64(vp + u * kSliceRows) : 0.0;
-    for (int p = p0; p < pu1; p += U) {
+    for (int u = 0; u < U; ++u) v[u] = pu0 + u < pu1 ? ld_stream_f64(vp + u * kSliceRows) : 0.0;
+    for (int p = pu0; p < pu1; p += U) {
       vp += U * kSliceRows;
 #pragma unroll
       for (int u = 0; u < U; ++u)
         vn[u] = p + U + u < pu1 ? ld_stream_f64(vp + u * kSliceRows) : 0.0;
-      const int q = (p - p0) & 31;
-      if (q == 0 && p > p0) myoff = p + lane < pu1 ? __ldg(uoff + p) : 0;
+      const int q = (p - pu0) & 31;
+      if (q == 0 && p > pu0) myoff = p + lane < pu1 ? __ldg(uoff + p) : 0;
       double g[U][R];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -389,8 +400,8 @@ __device__ __forceinline__ void add_rest(const SellView& A, int64_t row, double 
 // descriptor (header + the first kUgInline uniform offsets) is one coalesced 64-byte load;
 // values and gathers of a batch are then all independent, so a slice costs two dependent
 // memory round trips (descriptor, then everything else).
-//   LEAN: every slice has at most kUgInline uniform positions and a few general ones
-//   (stencils); the code then needs no offset lists and no software pipeline, which keeps the
+//   Every slice has at most kUgInline uniform positions and a few general ones (stencils);
+//   the code then needs no offset lists and no software pipeline, which keeps the
 //   register count at 64 (eight CTAs per SM) — occupancy is what hides the latency of
 //   seven-position slices (measured, 100^3 Laplacian, 3 columns: 24 warps/SM 37 us, 28 warps
 //   29 us, 32 warps 27.7 us per step).
@@ -400,8 +411,8 @@ __device__ __forceinline__ void add_rest(const SellView& A, int64_t row, double 
 #ifndef FLZ_K1_EARLY_OWN
 #define FLZ_K1_LATE_OWN 1  // own-row operands: L2 prefetch up front, loads after the gathers
 #endif
-template <int R, int S, int MODE, int U, bool LEAN>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, (LEAN && R <= 3) ? FLZ_K1_LEAN_CTAS : 1)
+template <int R, int S, int MODE, int U>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, R <= 3 ? FLZ_K1_LEAN_CTAS : 1)
     clenshaw_step_ug_warp(SellView A, int slices_per_cta, double s1, double s2, double b,
                           const double* __restrict__ Y1, double* __restrict__ Y2, int64_t ldy,
                           const double* __restrict__ X, int64_t ldx, double* __restrict__ Out,
@@ -414,13 +425,14 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, (LEAN && R <= 3) ? FLZ_K1
   for (int64_t w = first + warp; w < last; w += kWarpsPerBlock) {
     const int64_t slice = A.slice_ids ? (int64_t)A.slice_ids[w] : w;
     const int word = __ldg(reinterpret_cast<const int*>(A.ug + slice) + (lane & 15));
+    // (value, mask) pairs of the uniform-value positions: fixed stride, no descriptor needed
+    const double pair = ld_stream_f64(A.uv_pairs + slice * 16 + (lane & 15));
     const int64_t row = slice * kSliceRows + lane;
     double acc[R], y1o[R], y2o[R], xo[R];
 #pragma unroll
     for (int k = 0; k < R; ++k) acc[k] = 0.0;
 #ifdef FLZ_K1_LATE_OWN
-    if constexpr (LEAN) prefetch_own<R, S, MODE>(A, row, Y2, ldy, X, ldx);
-    else load_own<R, S, MODE>(A, row, Y1, Y2, ldy, X, ldx, y1o, y2o, xo);
+    prefetch_own<R, S, MODE>(A, row, Y2, ldy, X, ldx);
 #else
     load_own<R, S, MODE>(A, row, Y1, Y2, ldy, X, ldx, y1o, y2o, xo);
 #endif
@@ -428,26 +440,53 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, (LEAN && R <= 3) ? FLZ_K1
                                       (uint32_t)__shfl_sync(0xffffffffu, word, 0));
     const int nu = __shfl_sync(0xffffffffu, word, 5);
     const int ng = __shfl_sync(0xffffffffu, word, 6);
-    const double* __restrict__ val = A.ug_val + val_ptr + lane;
-    int p = 0;
-    if (nu <= kUgInline) {  // offsets are in the descriptor
-      for (; p < nu; p += U) {
-        double v[U], g[U][R];
+    const int nuv = (__shfl_sync(0xffffffffu, word, 7) >> 16) & 0xff;
+    const double* __restrict__ vbase = A.ug_val + val_ptr;
+    // ---- uniform-value positions: batches of 4, 2, 1 — no predicated loads, no zero fills
+    {
+      const int maskword = __double2loint(pair);  // lanes 2i+1 hold the lane mask of position i
+      auto uv_batch = [&](auto count, int p) {
+        constexpr int N = decltype(count)::value;
+        double g[N][R];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const bool ok = p + u < nu;
-          v[u] = ok ? ld_stream_f64(val + (int64_t)(p + u) * kSliceRows) : 0.0;
-          const int d = __shfl_sync(0xffffffffu, word, 8 + ((p + u) & (kUgInline - 1)));
-          gather_row<R, S>(Y1, ldy, min(max((int)row + d, 0), cmax), ok, g[u]);
+        for (int u = 0; u < N; ++u) {  // the gathers need the descriptor only
+          const int d = __shfl_sync(0xffffffffu, word, 8 + p + u);
+          gather_row<R, S>(Y1, ldy, min(max((int)row + d, 0), cmax), true, g[u]);
         }
+
 #pragma unroll
-        for (int u = 0; u < U; ++u)
+        for (int u = 0; u < N; ++u) {
+          const double value = __shfl_sync(0xffffffffu, pair, 2 * (p + u));
+          const int mask = __shfl_sync(0xffffffffu, maskword, 2 * (p + u) + 1);
+          const double v = ((mask >> lane) & 1) ? value : 0.0;
 #pragma unroll
-          for (int k = 0; k < R; ++k) acc[k] = fma(v[u], g[u][k], acc[k]);
-      }
-      p = nu;  // the last batch was predicated, not overrun
+          for (int k = 0; k < R; ++k) acc[k] = fma(v, g[u][k], acc[k]);
+        }
+      };
+      int p = 0;
+      if (p + 4 <= nuv) { uv_batch(std::integral_constant<int, 4>{}, p); p += 4; }
+      if (p + 4 <= nuv) { uv_batch(std::integral_constant<int, 4>{}, p); p += 4; }
+      if (p + 2 <= nuv) { uv_batch(std::integral_constant<int, 2>{}, p); p += 2; }
+      if (p < nuv) uv_batch(std::integral_constant<int, 1>{}, p);
     }
-    if constexpr (LEAN) {
+    // ---- uniform positions with per-lane values
+    const double* __restrict__ val = vbase + ug_header_doubles(nuv, nu + ng - nuv) + lane;
+    for (int p = nuv; p < nu; p += U) {
+      double v[U], g[U][R];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const bool ok = p + u < nu;
+        v[u] = ok ? ld_stream_f64(val + (int64_t)(p + u - nuv) * kSliceRows) : 0.0;
+        const int d = __shfl_sync(0xffffffffu, word, 8 + ((p + u) & (kUgInline - 1)));
+        gather_row<R, S>(Y1, ldy, min(max((int)row + d, 0), cmax), ok, g[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int k = 0; k < R; ++k) acc[k] = fma(v[u], g[u][k], acc[k]);
+    }
+    // ---- the few general positions of a stencil slice
+    if (ng > 0) {
       const int64_t col_ptr =
           (int64_t)(((uint64_t)(uint32_t)__shfl_sync(0xffffffffu, word, 3) << 32) |
                     (uint32_t)__shfl_sync(0xffffffffu, word, 2));
@@ -458,7 +497,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, (LEAN && R <= 3) ? FLZ_K1
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const bool ok = q + u < ng;
-          v[u] = ok ? ld_stream_f64(val + (int64_t)(nu + q + u) * kSliceRows) : 0.0;
+          v[u] = ok ? ld_stream_f64(val + (int64_t)(nu - nuv + q + u) * kSliceRows) : 0.0;
           c[u] = ok ? ld_stream_s32(col + (int64_t)(q + u) * kSliceRows) : 0;
         }
 #pragma unroll
@@ -468,102 +507,12 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, (LEAN && R <= 3) ? FLZ_K1
 #pragma unroll
           for (int k = 0; k < R; ++k) acc[k] = fma(v[u], g[u][k], acc[k]);
       }
-    } else if (p < nu + ng) {  // long offset lists and general positions
-      UgSlice H{};
-      H.val_ptr = val_ptr;
-      H.col_ptr = (int64_t)(((uint64_t)(uint32_t)__shfl_sync(0xffffffffu, word, 3) << 32) |
-                            (uint32_t)__shfl_sync(0xffffffffu, word, 2));
-      H.uoff_ptr = __shfl_sync(0xffffffffu, word, 4);
-      H.nu = nu;
-      H.ng = ng;
-      H.reserved = __shfl_sync(0xffffffffu, word, 7);
-      ug_accumulate<R, S, U>(A, H, lane, row, p, nu + ng, Y1, ldy, acc);
     }
     if (__shfl_sync(0xffffffffu, word, 7) & 1) add_rest<R>(A, row, acc);
 #ifdef FLZ_K1_LATE_OWN
-    if constexpr (LEAN) load_own<R, S, MODE>(A, row, Y1, Y2, ldy, X, ldx, y1o, y2o, xo);
+    load_own<R, S, MODE>(A, row, Y1, Y2, ldy, X, ldx, y1o, y2o, xo);
 #endif
     if (row < A.nl) finish_row<R, S, MODE>(row, s1, s2, b, acc, y1o, y2o, xo, Y2, ldy, Out, ldo);
-  }
-}
-
-// Medium and long slices: one warp per SUB-SLICE.  A slice with G = 2^g position groups is
-// processed by G warps; each takes RW = 32 / G consecutive rows and lays its lanes out as
-// RW rows x G groups: lane (row, grp) walks positions grp, grp + G, grp + 2G, ...  The G
-// partial sums of a row meet by warp shuffles, so there is no shared memory and no barrier,
-// and a 37-position slice gives four warps of ~9 positions per lane instead of one warp of
-// 37 — the parallelism a 113k-row matrix needs to fill 148 SMs.  Per position and lane:
-// one value, one index (uniform offset — the lanes of a group read the same word — or
-// general column), one gather.
-template <int R, int S, int MODE, int U>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, 5)
-    clenshaw_step_ug_sub(SellView A, double s1, double s2, double b,
-                         const double* __restrict__ Y1, double* __restrict__ Y2, int64_t ldy,
-                         const double* __restrict__ X, int64_t ldx, double* __restrict__ Out,
-                         int64_t ldo) {
-  const int lane = threadIdx.x & 31;
-  const int64_t unit = (int64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
-  if (unit >= A.nunits) return;
-  const int packed = __ldg(A.units + unit);
-  const int64_t slice = packed >> 3;
-  const int rg = packed & 7;
-  const UgSlice H = load_ug_header(A.ug + slice);
-  const int glog = (H.reserved >> 8) & 3;
-  const int G = 1 << glog, RW = 32 >> glog;
-  const int lrow = lane & (RW - 1), grp = lane >> (5 - glog);
-  const int srow = rg * RW + lrow;  // row inside the slice
-  int64_t row;
-  if constexpr (MODE == 3) {
-    const int r = A.rest_rows[(slice - A.rest_base) * kSliceRows + srow];
-    row = r < 0 ? A.nl : r;
-  } else {
-    row = slice * kSliceRows + srow;
-  }
-  if constexpr (MODE != 2 && MODE != 3) {
-    if (grp == 0) prefetch_own<R, S, MODE>(A, row, Y2, ldy, X, ldx);
-  }
-  const int nu = H.nu, L = H.nu + H.ng;
-  const int cmax = (int)A.ncols - 1;
-  const int crow = (H.reserved & 2) ? 0 : (int)row;  // flag bit 1: absolute shared columns
-  const double* __restrict__ val = A.ug_val + H.val_ptr + srow;
-  const int32_t* __restrict__ col = A.ug_col + H.col_ptr + srow - (int64_t)nu * kSliceRows;
-  const int32_t* __restrict__ uoff = A.ug_uoff + H.uoff_ptr;
-  double acc[R];
-#pragma unroll
-  for (int k = 0; k < R; ++k) acc[k] = 0.0;
-  for (int p0 = grp; p0 < L; p0 += U * G) {  // p0 differs per group; the trip count may too
-    double v[U], g[U][R];
-    int c[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int p = p0 + u * G;
-      const bool ok = p < L;
-      v[u] = ok ? ld_stream_f64(val + (int64_t)p * kSliceRows) : 0.0;
-      int idx = 0;
-      if (ok) idx = p < nu ? __ldg(uoff + p) : ld_stream_s32(col + (int64_t)p * kSliceRows);
-      c[u] = p < nu ? min(max(crow + idx, 0), cmax) : idx;
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) gather_row<R, S>(Y1, ldy, c[u], p0 + u * G < L, g[u]);
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-#pragma unroll
-      for (int k = 0; k < R; ++k) acc[k] = fma(v[u], g[u][k], acc[k]);
-  }
-  // the G partial sums of a row sit RW lanes apart (fixed order: deterministic)
-  for (int m = RW; m < 32; m <<= 1) {
-#pragma unroll
-    for (int k = 0; k < R; ++k) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], m);
-  }
-  if (grp != 0 || row >= A.nl) return;
-  if constexpr (MODE == 3) {
-#pragma unroll
-    for (int k = 0; k < R; ++k) A.W[row * kMaxFuse + k] = acc[k];
-  } else {
-    if (H.reserved & 1) add_rest<R>(A, row, acc);
-    double y1o[R], y2o[R], xo[R];
-    load_own<R, S, MODE>(A, row, Y1, Y2, ldy, X, ldx, y1o, y2o, xo);
-    finish_row<R, S, MODE>(row, s1, s2, b, acc, y1o, y2o, xo, Y2, ldy, Out, ldo);
   }
 }
 
@@ -700,16 +649,10 @@ template <int R, int S, int MODE>
 void launch_ug(flz_ctx* ctx, const SellView& A, double s1, double s2, double b, const double* Y1,
                double* Y2, int64_t ldy, const double* X, int64_t ldx, double* Out, int64_t ldo) {
   // kernel choice: stencils (every slice <= 8 uniform positions) -> lean one-warp-per-slice
-  // kernel; everything else -> multi-warp task kernel.  The sub-slice kernel is kept for A/B
-  // measurements (FLZ_K1_KERNEL=sub, or =mixed: sub-slice kernel for the uniform main part of
-  // a SPLIT matrix only).  Measured on the PARSEC-shaped matrix (3 columns, per step):
-  // tasks 34.9 us, sub 40.8-49.6 us (its lanes mix positions, which costs L1 wavefronts on
-  // general positions), SPLIT + mixed 40.2 us.
-  static const char kernel_choice = [] {
-    const char* e = std::getenv("FLZ_K1_KERNEL");
-    return e ? e[0] : 't';
-  }();
-  const bool use_tasks = kernel_choice == 't' || (kernel_choice == 'm' && (MODE == 3 || !A.mostly_uniform));
+  // kernel; everything else -> multi-warp task kernel.  (A "sub-slice" kernel — rows x position
+  // groups inside a warp, shuffle reduction, no shared memory — was measured and dropped: on
+  // the PARSEC-shaped matrix it took 40.8-49.6 us per step against 34.9 us, because lanes that
+  // mix positions touch more L1 lines on general positions.)
   bool lean = false;
   if constexpr (MODE != 3) lean = A.short_rows && A.lean;
   if (lean) {
@@ -718,17 +661,12 @@ void launch_ug(flz_ctx* ctx, const SellView& A, double s1, double s2, double b, 
       const int spc = ctx->k1_slices_per_cta > 0 ? ctx->k1_slices_per_cta : FLZ_K1_SLICES_PER_CTA;
       const unsigned grid = (unsigned)((A.nslices + spc - 1) / spc);
       if ((ctx->k1_batch > 0 ? ctx->k1_batch : FLZ_K1_UB) >= 8)
-        clenshaw_step_ug_warp<R, S, MODE, 8, true><<<grid, kWarpsPerBlock * 32, 0, ctx->stream>>>(
+        clenshaw_step_ug_warp<R, S, MODE, 8><<<grid, kWarpsPerBlock * 32, 0, ctx->stream>>>(
             A, spc, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo);
       else
-        clenshaw_step_ug_warp<R, S, MODE, 4, true><<<grid, kWarpsPerBlock * 32, 0, ctx->stream>>>(
+        clenshaw_step_ug_warp<R, S, MODE, 4><<<grid, kWarpsPerBlock * 32, 0, ctx->stream>>>(
             A, spc, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo);
     }
-  } else if (!use_tasks) {
-    if (A.nunits == 0) return;
-    const unsigned grid = (unsigned)((A.nunits + kWarpsPerBlock - 1) / kWarpsPerBlock);
-    clenshaw_step_ug_sub<R, S, MODE, 4><<<grid, kWarpsPerBlock * 32, 0, ctx->stream>>>(
-        A, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo);
   } else {
     if (A.ntasks == 0) return;
     const int tpc = ctx->k1_tasks_per_cta > 0 ? ctx->k1_tasks_per_cta : FLZ_K1_TASKS_PER_CTA;

@@ -114,16 +114,27 @@ class HaloPlan:
             col_ptr = int(np.array(d[2:4]).view(np.int64)[0])
             uoff_ptr, nu, ng = int(d[4]), int(d[5]), int(d[6])
             base = 0 if int(d[7]) & 2 else rows       # flag bit 1: absolute shared columns
+            nuv = (int(d[7]) >> 16) & 0xff            # uniform-value positions come first
+            hdr = (2 * nuv + 15) // 16 * 16 if nu + ng - nuv > 0 else 2 * nuv
+            lane_rows = val_ptr + hdr                 # per-lane value rows start here
             acc = np.zeros(32)
             for p in range(nu):
                 off = int(u["uoff"][uoff_ptr + p])
                 if p < 8:
                     assert off == int(d[8 + p])
                 c = np.clip(base + off, 0, ncols - 1)
-                acc += u["val"][val_ptr + p * 32: val_ptr + p * 32 + 32] * x[c]
+                if p < nuv:                           # one (value, lane mask) pair
+                    value = u["val"][val_ptr + 2 * p]
+                    mask = int(u["val"][val_ptr + 2 * p + 1: val_ptr + 2 * p + 2].view(np.uint64)[0])
+                    v = np.where((mask >> lanes) & 1, value, 0.0)
+                else:
+                    q = lane_rows + (p - nuv) * 32
+                    v = u["val"][q: q + 32]
+                acc += v * x[c]
             for q in range(ng):
                 c = u["col"][col_ptr + q * 32: col_ptr + q * 32 + 32]
-                acc += u["val"][val_ptr + (nu + q) * 32: val_ptr + (nu + q) * 32 + 32] * x[c]
+                k = lane_rows + (nu - nuv + q) * 32
+                acc += u["val"][k: k + 32] * x[c]
             return acc
 
         W = np.zeros(nl + 32)

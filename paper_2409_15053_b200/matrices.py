@@ -105,6 +105,23 @@ def random_sparse_sym(n: int, density: float, seed: int):
 _FD12 = np.array([-5369 / 1800, 12 / 7, -15 / 56, 10 / 189, -1 / 112, 2 / 1925, -1 / 16632])
 
 
+def stencil3d(grid: int, h: float = 0.567, potential=None, seed: int = 1):
+    """-1/2 Laplacian with the 12th-order stencil (radius 6 per axis, 37 points) on the full
+    grid^3 box (Dirichlet, x fastest) plus an optional random local potential: the kinetic
+    part of a PARSEC Hamiltonian without the non-local blocks — every row has the same 37
+    diagonal offsets (fewer at the faces)."""
+    g = grid
+    kin = -0.5 / (h * h)
+    offs = np.arange(-6, 7)
+    T = sp.diags([np.full(g - abs(k), kin * _FD12[abs(k)]) for k in offs], offs)
+    I = sp.identity(g)
+    A = sp.kron(I, sp.kron(I, T)) + sp.kron(I, sp.kron(T, I)) + sp.kron(T, sp.kron(I, I))
+    if potential is not None:
+        rng = np.random.default_rng(seed)
+        A = A + sp.diags(rng.uniform(potential[0], potential[1], g ** 3))
+    return _to_csr(A)
+
+
 def parsec_like(radius: float = 30.0, h: float = 0.567, n_atoms: int = 199,
                 ball_radius: float = 3.25, v_range=(-1.2, 0.3), nonlocal_strength: float = 0.35,
                 seed: int = 1):

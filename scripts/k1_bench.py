@@ -28,6 +28,8 @@ def bench(name, csr, r, m=50, sigma=0, check=True):
     stride = 4 if (r == 3 and nnz >= 16 * n) else r
     if os.environ.get("FLZ_K1_LAYOUT", "")[:1] == "p":
         stride = r
+    if os.environ.get("FLZ_K1_LAYOUT", "")[:1] == "4" and r == 3:
+        stride = 4
     moved = st["matrix_bytes"] + 8 * n * (3 * stride + r)
     print(f"{name:28s} n={n:8d} nnz/row={nnz/n:5.1f} r={r} fill={st['fill']:.3f} sigma={st['sigma']:6d} "
           f"uniform={st['uniform_entries']/nnz:5.1%} moved/formula={moved/bytes_step:.3f} "
@@ -36,6 +38,11 @@ def bench(name, csr, r, m=50, sigma=0, check=True):
     return ms / 4 / m * 1e3
 
 which = sys.argv[1] if len(sys.argv) > 1 else "all"
+if which == "stencil":
+    st = M.stencil3d(48, potential=(-1.2, 0.3))
+    for r in (3, 1):
+        bench("stencil37-48^3 r=%d" % r, st, r)
+    sys.exit(0)
 if which == "sweep":
     lap = M.laplacian3d(100)
     pk = M.parsec_like()
