@@ -24,6 +24,7 @@ CASES = {
     "rand500": (lambda: M.random_sparse_sym(500, 0.03, 1), False),   # nothing uniform: unsplit
     "parsec7k": (lambda: M.parsec_like(radius=12.0, n_atoms=12), None),
     "diag": (lambda: M.diag_matrix(np.arange(1.0, 41.0)), True),
+    "stencil37": (lambda: M.stencil3d(14, potential=(-1.2, 0.3)), True),   # 37 offsets per row
 }
 
 
@@ -46,6 +47,13 @@ def test_ug_layout_reproduces_product(name):
     if name.startswith("lap3d"):
         assert u["uniform_entries"] >= 0.95 * len(va)
         assert u["nrest"] == 0
+        # constant coefficients: the positions are (value, lane mask) pairs, not 32 values
+        nuv = (u["desc"][:, 7] >> 16) & 0xFF
+        assert nuv.sum() >= 0.95 * u["desc"][:, 5].sum()
+        assert len(u["val"]) * 8 < 0.25 * 8 * len(va)
+    if name == "stencil37":      # long slices: no pairs (the task kernel reads per-lane values)
+        assert ((u["desc"][:, 7] >> 16) & 0xFF).sum() == 0
+        assert u["uniform_entries"] >= 0.85 * len(va)
 
 
 def test_forced_split_builds_rest_slices(monkeypatch):
