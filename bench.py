@@ -54,13 +54,13 @@ def workloads():
         "c3": dict(desc="synthetic PARSEC-shaped Hamiltonian (Ge99H100-like, n~113k, ~75 nnz/row), "
                         "degree 50, block 3",
                    gen=lambda: M.parsec_like(), interval=(-0.65, -0.0096),
-                   cfg=dict(block_size=3, degree=50), expect=None),
+                   cfg=dict(block_size=3, degree=50), expect=246),
         # configs[3]: Ga41As41H72-shaped
-        "c4": dict(desc="synthetic Ga41As41H72-shaped Hamiltonian (n~268k, ~69 nnz/row), "
-                        "degree 200, block 3",
+        "c4": dict(desc="synthetic Ga41As41H72-shaped Hamiltonian (n~268k, ~65 nnz/row, spectrum "
+                        "[-0.06, 1300]), [3.0,10.0] (208 eigenpairs), degree 200, block 3",
                    gen=lambda: M.parsec_like(radius=40.0, h=0.0903, n_atoms=154, ball_radius=3.86,
                                              seed=2),
-                   interval=(-0.64, 0.0), cfg=dict(block_size=3, degree=200), expect=None),
+                   interval=(3.0, 10.0), cfg=dict(block_size=3, degree=200), expect=208),
         # configs[4]: row-partitioned 27M-row Laplacian (2/4/8 GPUs; does not fit one GPU:
         # 216 MB per basis vector).  max_dim is fixed so that the 2-GPU basis fits (97 GB/GPU)
         # and is identical at every GPU count.

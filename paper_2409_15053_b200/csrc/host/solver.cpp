@@ -644,7 +644,10 @@ EigenResult run_solve(const SparseSymMatrix& A, double alpha, double beta,
     std::future<RitzSet> ritz;
   };
   std::deque<std::unique_ptr<PendingCheck>> queue;
-  static const bool overlap = std::getenv("FLZ_SYNC_CHECK") == nullptr;
+  // (row-partitioned runs keep the sequential order: how far the device gets ahead of a
+  // check depends on timing, and every rank must issue the same collectives)
+  const bool overlap =
+      std::getenv("FLZ_SYNC_CHECK") == nullptr && flz_ctx_nranks(Device::context()) == 1;
   const std::size_t max_depth =
       overlap ? std::max(1u, std::min(8u, std::thread::hardware_concurrency())) : 0;
   auto enqueue = [&] {

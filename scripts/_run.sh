@@ -1,3 +1,3 @@
-for lay in i planar; do
-FLZ_K1_LAYOUT=$lay ncu --section SpeedOfLight --section MemoryWorkloadAnalysis --section SchedulerStats --section WarpStateStats --section Occupancy --cache-control none --clock-control none -k regex:clenshaw_step_ug_warp -s 20 -c 1 python scripts/k1_profile.py c2 3 12 > gpurun_out/lean_$lay.txt 2>&1
-done
+(timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -3)
+python bench.py --workload c4 --steps 1 --warmup 1 --no-cpu-baseline 2>&1 | tail -1 > gpurun_out/bench_c4_b.json
+cp profiles/block_steps.json gpurun_out/block_steps.json
