@@ -167,3 +167,50 @@ def test_full_size_linearity_and_symmetry(ctx):
     # against SciPy's CSR product on one plain block product
     As = M.csr_to_scipy(n, rp, ci, va)
     assert np.abs(A.spmm(X) - As @ X).max() <= 1e-13 * np.abs(X).max() * 12
+
+
+def test_full_size_eigenvector_invariance(ctx):
+    """C2 shape: an analytic eigenvector v of the 100^3 Laplacian satisfies p(A) v = p(lambda) v
+    (the reference's eigenvector-invariance test, filter_test.cpp:268-283, at BASELINE size)."""
+    g = 100
+    n, rp, ci, va = M.laplacian3d(g)
+    A = DeviceMatrix(ctx, n, rp, ci, va)
+    idx = np.arange(1, g + 1)
+    modes = ((3, 5, 7), (1, 1, 1), (40, 2, 17))
+    V = np.empty((n, 3))
+    lam = []
+    for k, (a, b, c) in enumerate(modes):
+        sx, sy, sz = (np.sin(m * np.pi * idx / (g + 1)) for m in (a, b, c))
+        V[:, k] = (sz[:, None, None] * sy[None, :, None] * sx[None, None, :]).ravel()
+        V[:, k] /= np.linalg.norm(V[:, k])
+        lam.append(sum(2.0 * (1.0 - np.cos(m * np.pi / (g + 1))) for m in (a, b, c)))
+    lo, hi = -0.05, 12.05
+    cf = S.indicator_coefficients(-0.9, -0.8, 150)
+    Y = A.filter_apply(cf, 0.5 * (lo + hi), 0.5 * (hi - lo), V)
+    for k in range(3):
+        t = (lam[k] - 0.5 * (lo + hi)) / (0.5 * (hi - lo))
+        assert np.abs(Y[:, k] - S.clenshaw(cf, t) * V[:, k]).max() <= 1e-12
+
+
+def test_full_size_parsec_shape_properties(ctx):
+    """C3 shape (PARSEC-like, n = 113k, long ragged rows): product against SciPy, linearity and
+    symmetry of p(A) — size-independent checks of the long-row kernel at BASELINE size."""
+    n, rp, ci, va = M.parsec_like()
+    A = DeviceMatrix(ctx, n, rp, ci, va)
+    As = M.csr_to_scipy(n, rp, ci, va)
+    X, Z = block(n, 3, 11), block(n, 3, 12)
+    ref = As @ X
+    assert np.abs(A.spmm(X) - ref).max() <= 1e-13 * np.abs(ref).max()
+    cf = S.indicator_coefficients(-0.95, -0.9, 40)
+    c, e = 16.0, 17.5
+    FX, FZ = A.filter_apply(cf, c, e, X), A.filter_apply(cf, c, e, Z)
+    F2 = A.filter_apply(cf, c, e, X + 3.0 * Z)
+    scale = np.abs(FX).max() + np.abs(FZ).max()
+    assert np.abs(F2 - (FX + 3.0 * FZ)).max() <= 1e-12 * scale
+    assert abs(np.sum(Z * FX) - np.sum(X * FZ)) <= 1e-10 * abs(np.sum(Z * FX)) + 1e-9
+    ctx.set_exact(True)
+    try:
+        Fe = A.filter_apply(cf, c, e, X)
+    finally:
+        ctx.set_exact(False)
+    assert np.abs(FX - Fe).max() <= 1e-13 * np.abs(Fe).max()      # fast vs reference-order mode
