@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -22,8 +23,31 @@ namespace {
 #define FLZ_K1_T 48  // target entries per warp before a slice is split over more warps
 #endif
 
+// Entries per warp before a slice is split over more warps.  Splitting costs (shared-memory
+// reduction, barriers, more index traffic per entry), so the target is the LARGEST one that
+// keeps the launch balanced: measured on B200, 3 columns — PARSEC-shaped n = 113k:
+// T = 48 32.9 us, 96 30.9 us, 128 35.9 us; n = 268k: 48 65.0 us, 96 64.0 us, 192 61.6 us.
+thread_local int g_task_target = FLZ_K1_T;
 int warps_for(int32_t len) {
-  return len <= FLZ_K1_T ? 1 : (len <= 2 * FLZ_K1_T ? 2 : (len <= 4 * FLZ_K1_T ? 4 : 8));
+  const int T = g_task_target;
+  return len <= T ? 1 : (len <= 2 * T ? 2 : (len <= 4 * T ? 4 : 8));
+}
+void choose_task_target(const std::vector<int32_t>& slice_len) {
+  if (const char* e = std::getenv("FLZ_K1_T")) {  // experiments
+    g_task_target = std::max(1, std::atoi(e));
+    return;
+  }
+  // the longest warp must not outlast the average warp slot by much (24 resident warps on
+  // each of 148 SMs): largest target whose critical path stays within 1.5x of that average
+  int64_t total = 0;
+  for (int32_t L : slice_len) total += L;
+  const double slot_average = (double)total / (148.0 * 24.0);
+  for (int T : {256, 192, 128, 96, 64, 48}) {
+    g_task_target = T;
+    int32_t longest = 0;
+    for (int32_t L : slice_len) longest = std::max(longest, (L + warps_for(L) - 1) / warps_for(L));
+    if ((double)longest <= 1.5 * slot_average) return;
+  }
 }
 
 // Groups slices (in list order) into CTA tasks: long slices get several warps each.
@@ -39,19 +63,38 @@ std::vector<PlanTask> build_tasks(const std::vector<int32_t>& ids,
       t.slice[t.count++] = ids[i++];
     tasks.push_back(t);
   }
+  // longest tasks first: CTAs are dispatched in order, so the short ones fill the tail of the
+  // launch (a 113k-row matrix is only ~3 waves of CTAs)
+  static const bool lpt = std::getenv("FLZ_K1_NO_LPT") == nullptr;
+  if (lpt)
+    std::stable_sort(tasks.begin(), tasks.end(), [&](const PlanTask& a, const PlanTask& b) {
+      const int32_t ca = (slice_len[a.slice[0]] + a.warps_per_slice - 1) / a.warps_per_slice;
+      const int32_t cb = (slice_len[b.slice[0]] + b.warps_per_slice - 1) / b.warps_per_slice;
+      return ca > cb;
+    });
   return tasks;
 }
 
-// stable sort by descending row length inside windows of `sigma` rows
+// Stable sort by descending row-length CLASS inside windows of `sigma` rows.  Classes are
+// geometric (ratio 1.2): rows of similar length stay in their natural order, i.e. the lanes
+// of a slice are mostly neighbouring rows whose entries reference neighbouring columns — on
+// the PARSEC-shaped matrix a warp-level gather then touches 12.2 instead of 15.9 128-byte lines
+// (scripts/analysis/gather_lines.py) for 3 % more padding than sorting by exact length.
+int32_t length_class(int32_t len) {
+  if (len <= 8) return len;
+  return 8 + (int32_t)std::ceil(std::log((double)len / 8.0) / std::log(1.2));
+}
 void sort_windows(const std::vector<int32_t>& len, int64_t sigma, std::vector<int32_t>& perm) {
   const int64_t nl = (int64_t)len.size();
   perm.resize(nl);
   std::iota(perm.begin(), perm.end(), 0);
   if (sigma <= 1) return;
+  std::vector<int32_t> cls(nl);
+  for (int64_t i = 0; i < nl; ++i) cls[i] = length_class(len[i]);
   for (int64_t w0 = 0; w0 < nl; w0 += sigma) {
     const int64_t w1 = std::min(nl, w0 + sigma);
     std::stable_sort(perm.begin() + w0, perm.begin() + w1,
-                     [&](int32_t a, int32_t b) { return len[a] > len[b]; });
+                     [&](int32_t a, int32_t b) { return cls[a] > cls[b]; });
   }
 }
 
@@ -577,7 +620,7 @@ HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<in
   }
 
   timer.lap("split estimate");
-  // ---- sigma: smallest window whose padding overhead is <= 5 %
+  // ---- sigma: smallest window whose padding overhead is <= 8 %
   int64_t chosen = sigma;
   if (P.split) {
     chosen = 1;  // natural order: uniform offsets only exist there
@@ -593,7 +636,7 @@ HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<in
         best_fill = f;
         chosen = sg;
       }
-      if ((double)f <= 1.05 * (double)std::max<int64_t>(P.nnz, 1)) {
+      if ((double)f <= 1.08 * (double)std::max<int64_t>(P.nnz, 1)) {
         chosen = sg;
         break;
       }
@@ -702,6 +745,7 @@ HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<in
   timer.lap("UG layout");
   std::vector<int32_t> ug_len(nslices + P.nrest);  // the fast kernels walk the compressed slices
   for (int64_t s = 0; s < nslices + P.nrest; ++s) ug_len[s] = P.ug_slice[s].nu + P.ug_slice[s].ng;
+  choose_task_target(ug_len);
   {
     std::vector<int32_t> rest_all(P.rest_interior);
     rest_all.insert(rest_all.end(), P.rest_boundary.begin(), P.rest_boundary.end());
