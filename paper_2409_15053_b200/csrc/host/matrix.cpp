@@ -13,7 +13,9 @@
 #include <cstdlib>
 #include <cstring>
 #include <fstream>
+#include <atomic>
 #include <mutex>
+#include <thread>
 
 #include "flz.h"
 
@@ -123,6 +125,34 @@ SparseSymMatrix SparseSymMatrix::from_entries(std::size_t n, std::vector<Triplet
   return A;
 }
 
+namespace {
+// rows [0, n) in contiguous chunks on up to 16 threads; the first exception is rethrown
+template <class F>
+void parallel_rows(std::size_t n, F&& body) {
+  unsigned workers = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  if (const char* e = std::getenv("FLZ_HOST_THREADS")) workers = std::max(1, std::atoi(e));
+  workers = (unsigned)std::min<std::size_t>(workers, n / 4096 + 1);
+  if (workers <= 1) {
+    body(std::size_t(0), n);
+    return;
+  }
+  std::vector<std::thread> pool;
+  std::exception_ptr err;
+  std::mutex mu;
+  for (unsigned t = 0; t < workers; ++t)
+    pool.emplace_back([&, t] {
+      try {
+        body(n * t / workers, n * (t + 1) / workers);
+      } catch (...) {
+        std::lock_guard<std::mutex> lock(mu);
+        if (!err) err = std::current_exception();
+      }
+    });
+  for (auto& th : pool) th.join();
+  if (err) std::rethrow_exception(err);
+}
+}  // namespace
+
 SparseSymMatrix SparseSymMatrix::from_csr(std::size_t n, std::vector<std::int64_t> row_ptr,
                                           std::vector<std::int32_t> col_idx,
                                           std::vector<double> values, bool check) {
@@ -135,18 +165,40 @@ SparseSymMatrix SparseSymMatrix::from_csr(std::size_t n, std::vector<std::int64_
   A.row_ptr_ = std::move(row_ptr);
   A.col_idx_ = std::move(col_idx);
   A.values_ = std::move(values);
-  for (std::size_t i = 0; i < n; ++i) {
-    if (A.row_ptr_[i] > A.row_ptr_[i + 1]) throw Error("from_csr: row_ptr is not monotone");
-    for (std::int64_t p = A.row_ptr_[i]; p < A.row_ptr_[i + 1]; ++p) {
-      const std::int32_t c = A.col_idx_[p];
-      if (c < 0 || static_cast<std::size_t>(c) >= n)
-        throw Error("matrix entry index out of range");
-      if (p > A.row_ptr_[i] && A.col_idx_[p - 1] >= c)
-        throw Error("from_csr: columns must be strictly ascending within a row");
-      if (!std::isfinite(A.values_[p])) throw Error("matrix entry is not finite");
-      A.max_abs_ = std::max(A.max_abs_, std::abs(A.values_[p]));
+  // First bad row (if any) is reported exactly as a sequential scan would report it.
+  std::mutex mu;
+  std::size_t bad_row = n;
+  const char* bad_msg = nullptr;
+  double max_abs = 0.0;
+  parallel_rows(n, [&](std::size_t r0, std::size_t r1) {
+    double local_max = 0.0;
+    for (std::size_t i = r0; i < r1; ++i) {
+      const char* msg = nullptr;
+      if (A.row_ptr_[i] > A.row_ptr_[i + 1] || A.row_ptr_[i] < 0 ||
+          static_cast<std::size_t>(A.row_ptr_[i + 1]) > A.col_idx_.size())
+        msg = "from_csr: row_ptr is not monotone";
+      for (std::int64_t p = A.row_ptr_[i]; !msg && p < A.row_ptr_[i + 1]; ++p) {
+        const std::int32_t c = A.col_idx_[p];
+        if (c < 0 || static_cast<std::size_t>(c) >= n) msg = "matrix entry index out of range";
+        else if (p > A.row_ptr_[i] && A.col_idx_[p - 1] >= c)
+          msg = "from_csr: columns must be strictly ascending within a row";
+        else if (!std::isfinite(A.values_[p])) msg = "matrix entry is not finite";
+        else local_max = std::max(local_max, std::abs(A.values_[p]));
+      }
+      if (msg) {
+        std::lock_guard<std::mutex> lock(mu);
+        if (i < bad_row) {
+          bad_row = i;
+          bad_msg = msg;
+        }
+        break;
+      }
     }
-  }
+    std::lock_guard<std::mutex> lock(mu);
+    max_abs = std::max(max_abs, local_max);
+  });
+  if (bad_msg) throw Error(bad_msg);
+  A.max_abs_ = max_abs;
   if (check) A.verify_symmetry();
   return A;
 }
@@ -176,26 +228,26 @@ SparseSymMatrix SparseSymMatrix::from_local_rows(std::size_t n_global, std::size
 }
 
 // exact structural + numerical symmetry (sparse.cpp:65-83): every upper entry (i,j) must
-// have an equal mirror (j,i) — like the reference, lower entries are not looked up.  One
-// linear pass instead of a binary search per entry: rows are visited in ascending order, so
-// the mirror of (i,j) is found by advancing a cursor through row j.  On a mismatch the
-// reference's own search runs, so the entry it would report is the one reported.
+// have an equal mirror (j,i) — like the reference, lower entries are not looked up.  The
+// reference's binary search per entry, threaded over rows; on a mismatch the sequential scan
+// runs, so the entry the reference would report is the one reported.
 void SparseSymMatrix::verify_symmetry() const {
-  std::vector<std::int64_t> cursor(row_ptr_.begin(), row_ptr_.end() - 1);
-  bool ok = true;
-  for (std::size_t i = 0; i < n_ && ok; ++i)
-    for (std::int64_t p = row_ptr_[i]; p < row_ptr_[i + 1]; ++p) {
-      const auto j = static_cast<std::size_t>(col_idx_[p]);
-      if (j <= i) continue;
-      std::int64_t q = cursor[j];
-      const std::int64_t end = row_ptr_[j + 1];
-      while (q < end && static_cast<std::size_t>(col_idx_[q]) < i) ++q;
-      if (q >= end || static_cast<std::size_t>(col_idx_[q]) != i || values_[q] != values_[p]) {
-        ok = false;
-        break;
+  std::atomic<bool> ok{true};
+  parallel_rows(n_, [&](std::size_t r0, std::size_t r1) {
+    for (std::size_t i = r0; i < r1 && ok.load(std::memory_order_relaxed); ++i)
+      for (std::int64_t p = row_ptr_[i]; p < row_ptr_[i + 1]; ++p) {
+        const auto j = static_cast<std::size_t>(col_idx_[p]);
+        if (j <= i) continue;
+        const std::int32_t* first = col_idx_.data() + row_ptr_[j];
+        const std::int32_t* last = col_idx_.data() + row_ptr_[j + 1];
+        const std::int32_t* hit = std::lower_bound(first, last, static_cast<std::int32_t>(i));
+        if (hit == last || *hit != static_cast<std::int32_t>(i) ||
+            values_[p] != values_[row_ptr_[j] + (hit - first)]) {
+          ok.store(false, std::memory_order_relaxed);
+          break;
+        }
       }
-      cursor[j] = q + 1;
-    }
+  });
   if (ok) return;
   for (std::size_t i = 0; i < n_; ++i)
     for (std::int64_t p = row_ptr_[i]; p < row_ptr_[i + 1]; ++p) {
