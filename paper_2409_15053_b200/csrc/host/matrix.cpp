@@ -267,7 +267,9 @@ void SparseSymMatrix::verify_symmetry() const {
 
 DenseBlock DenseBlock::pinned(std::size_t rows, std::size_t cols) {
   void* p = nullptr;
-  if (rows * cols == 0 || flz_host_alloc(rows * cols * sizeof(double), &p) != FLZ_OK || !p)
+  constexpr std::size_t kMaxPinned = std::size_t(2) << 30;  // larger blocks stay pageable
+  const std::size_t bytes = rows * cols * sizeof(double);
+  if (bytes == 0 || bytes > kMaxPinned || flz_host_alloc(bytes, &p) != FLZ_OK || !p)
     return uninitialized(rows, cols);
   DenseBlock B;
   B.rows_ = rows;
