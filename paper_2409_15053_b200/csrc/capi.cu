@@ -321,6 +321,7 @@ struct SmallLayout {
   int64_t C1, C2, gram, Sk, t1, t2, normsq, inv, dead, scale, total;
 };
 constexpr int kRMax = 16;
+constexpr int kRecoverChunk = 64;  // columns of A V / rotated blocks held at a time
 SmallLayout small_layout(int64_t max_cols, int r) {
   SmallLayout L;
   L.ldc = (int)round_up(r, 8);
@@ -1164,9 +1165,12 @@ int flz_ritz_lift(flz_ctx* ctx, const flz_matrix* A, const flz_basis* Bc, int64_
     if (w == 0) return;
     const int64_t nl = B->nl, ld = B->ld;
     const int64_t ldw = round_up(w, 64);
-    { Trace tr(ctx, "lift: reserve V, AV");
+    // V is the only n x w block of the recovery; A V and the rotated blocks are produced in
+    // chunks of kRecoverChunk columns (memory: the 27M-row Laplacian with 345 wanted pairs
+    // needs 37 GB per n x w block on each of 2 GPUs, next to a 97 GB basis)
+    { Trace tr(ctx, "lift: reserve V, AV chunk");
     B->V.reserve_zero((size_t)ld * w, ctx->stream);
-    B->AV.reserve_zero((size_t)ld * w, ctx->stream); }
+    B->AV.reserve_zero((size_t)ld * std::min(w, kRecoverChunk), ctx->stream); }
     Trace* tr1 = new Trace(ctx, "lift: W transpose + H2D");
     // W (dim x w column-major) -> row-major [dim][ldw]
     std::vector<double> Wt((size_t)dim * ldw, 0.0);
@@ -1204,13 +1208,16 @@ int flz_ritz_lift(flz_ctx* ctx, const flz_matrix* A, const flz_basis* Bc, int64_
     FLZ_CUDA(cudaMemcpyAsync(dn.p + w, hs.data(), wk * sizeof(double), cudaMemcpyHostToDevice,
                              ctx->stream));
     launch_scale_cols(ctx, B->V.p, ld, wk, nl, dn.p + w);
-    { Trace tr(ctx, "lift: AV = A V");
-    spmm_device(A, B->V.p, ld, wk, B->AV.p, ld, false); }  // uncounted (lanczos.cpp:448-449)
     const int64_t ldb = round_up(wk, 8);
     DevBuf<double> dB;
     dB.reserve((size_t)wk * ldb + 8);
-    { Trace tr(ctx, "lift: V'AV (gemm_tn)");
-    launch_gemm_tn(ctx, B->V.p, ld, wk, B->AV.p, ld, wk, nl, dB.p, ldb); }
+    { Trace tr(ctx, "lift: A V, V'AV by chunks");
+    for (int c0 = 0; c0 < wk; c0 += kRecoverChunk) {
+      const int nc = std::min(kRecoverChunk, wk - c0);
+      // uncounted products (lanczos.cpp:448-449); columns c0.. of V^T (A V) (:451-457)
+      spmm_device(A, B->V.p + (size_t)c0 * ld, ld, nc, B->AV.p, ld, false);
+      launch_gemm_tn(ctx, B->V.p, ld, wk, B->AV.p, ld, nc, nl, dB.p + c0, ldb);
+    } }
     allreduce(ctx, dB.p, (size_t)wk * ldb);
     std::vector<double> hB((size_t)wk * ldb);
     FLZ_CUDA(cudaMemcpyAsync(hB.data(), dB.p, hB.size() * sizeof(double), cudaMemcpyDeviceToHost,
@@ -1275,12 +1282,19 @@ int flz_ritz_rotate(flz_ctx* ctx, const flz_basis* Bc, const double* U, const do
     dU.reserve(Ut.size() + 8);
     FLZ_CUDA(cudaMemcpyAsync(dU.p, Ut.data(), Ut.size() * sizeof(double), cudaMemcpyHostToDevice,
                              ctx->stream));
-    B->V2.reserve_zero((size_t)ld * w2, ctx->stream);
-    B->AV2.reserve_zero((size_t)ld * w2, ctx->stream);
-    { Trace tr(ctx, "rotate: V U, AV U");
-    launch_gemm_nn(ctx, B->V.p, ld, wk, dU.p, ldu, w2, nl, 1.0, false, B->V2.p, ld);   // :467-470
-    launch_gemm_nn(ctx, B->AV.p, ld, wk, dU.p, ldu, w2, nl, 1.0, false, B->AV2.p, ld); }
-    residuals_and_vectors(ctx, B, B->V2.p, B->AV2.p, lambda, w2, scale, true, residuals, eigvecs);
+    const int cmax = std::min(w2, kRecoverChunk);
+    B->V2.reserve_zero((size_t)ld * cmax, ctx->stream);
+    B->AV2.reserve_zero((size_t)ld * cmax, ctx->stream);
+    Trace tr(ctx, "rotate: V U, A (V U), residuals, D2H by chunks");
+    for (int c0 = 0; c0 < w2; c0 += kRecoverChunk) {
+      const int nc = std::min(kRecoverChunk, w2 - c0);
+      // v = V u (:467-470); A v is formed from v (the reference rotates A V: the same vector
+      // up to rounding) so that no second n x w block has to be kept
+      launch_gemm_nn(ctx, B->V.p, ld, wk, dU.p + c0, ldu, nc, nl, 1.0, false, B->V2.p, ld);
+      spmm_device(B->A, B->V2.p, ld, nc, B->AV2.p, ld, false);
+      residuals_and_vectors(ctx, B, B->V2.p, B->AV2.p, lambda + c0, nc, scale, true,
+                            residuals + c0, eigvecs ? eigvecs + (size_t)c0 * nl : nullptr);
+    }
   });
 }
 
@@ -1292,9 +1306,15 @@ int flz_ritz_plain(flz_ctx* ctx, const flz_matrix* A, const flz_basis* Bc, const
     FLZ_REQUIRE(w_kept == B->w_kept, FLZ_EDIM, "ritz_plain: w_kept mismatch");
     use(ctx);
     if (w_kept == 0) return;
-    // V holds the normalised lifted vectors, AV = A V (lanczos.cpp:480-495)
-    residuals_and_vectors(ctx, B, B->V.p, B->AV.p, lambda, w_kept, scale, false, residuals,
-                          eigvecs);
+    // V holds the normalised lifted vectors; A V by chunks (lanczos.cpp:480-495)
+    B->AV.reserve_zero((size_t)B->ld * std::min(w_kept, kRecoverChunk), ctx->stream);
+    for (int c0 = 0; c0 < w_kept; c0 += kRecoverChunk) {
+      const int nc = std::min(kRecoverChunk, w_kept - c0);
+      double* Vc = B->V.p + (size_t)c0 * B->ld;
+      spmm_device(A, Vc, B->ld, nc, B->AV.p, B->ld, false);
+      residuals_and_vectors(ctx, B, Vc, B->AV.p, lambda + c0, nc, scale, false, residuals + c0,
+                            eigvecs ? eigvecs + (size_t)c0 * B->nl : nullptr);
+    }
   });
 }
 
