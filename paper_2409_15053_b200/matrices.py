@@ -84,6 +84,17 @@ def laplacian3d_eigenvalues_in(grid: int, lo: float, hi: float):
     return np.sort(np.concatenate(out)) if out else np.zeros(0)
 
 
+def laplacian3d_lowest(grid: int, about: int):
+    """(upper, count): an interval end in the widest gap near the `about` lowest eigenvalues of
+    laplacian3d(grid), and the exact number of eigenvalues below it."""
+    t = 2.0 * (1.0 - np.cos(np.arange(1, grid + 1) * np.pi / (grid + 1)))
+    m = min(grid, 64)
+    s = np.sort((t[:m, None, None] + t[None, :m, None] + t[None, None, :m]).ravel())
+    gaps = np.diff(s[about - 20:about + 20])
+    count = about - 20 + int(np.argmax(gaps)) + 1
+    return 0.5 * (s[count - 1] + s[count]), count
+
+
 def diag_matrix(values):
     n = len(values)
     return (n, np.arange(n + 1, dtype=np.int64), np.arange(n, dtype=np.int32),
