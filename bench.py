@@ -66,14 +66,15 @@ def workloads():
         # and is identical at every GPU count.  With 900 basis vectors and the reference's
         # degree cap (1000) an interior interval of this matrix cannot converge (its filter
         # would need degree ~23000), and 500 pairs need ~1400 vectors; the workload is
-        # therefore the LOWEST 329 eigenpairs: on the 100^3 scale model with an equally blunt
-        # filter (degree 333) this converges in 240 block steps (scripts/explore_c5.py).
-        "c5": dict(desc="3D Laplacian 7-point 300^3 (n=27M) row-partitioned, lowest 329 eigenpairs "
+        # therefore the LOWEST 284 eigenpairs: on the 100^3 scale model with an equally blunt
+        # filter (degree 333) this converges in 200 block steps, 329 pairs on 150^3 (degree 500) in 260
+        # (scripts/explore_c5.py).
+        "c5": dict(desc="3D Laplacian 7-point 300^3 (n=27M) row-partitioned, lowest 284 eigenpairs "
                         "([-0.001, %.6f]), block 3, auto degree (clamps at 1000), max_dim 900"
-                        % M.laplacian3d_lowest(300, 330)[0],
+                        % M.laplacian3d_lowest(300, 285)[0],
                    gen=lambda: M.laplacian3d(300), gen_rows=lambda b, e: M.laplacian3d_rows(300, b, e),
-                   n=27000000, interval=(-0.001, M.laplacian3d_lowest(300, 330)[0]),
-                   cfg=dict(block_size=3, max_dim=900), expect=M.laplacian3d_lowest(300, 330)[1]),
+                   n=27000000, interval=(-0.001, M.laplacian3d_lowest(300, 285)[0]),
+                   cfg=dict(block_size=3, max_dim=900), expect=M.laplacian3d_lowest(300, 285)[1]),
         # small smoke-sized case
         "tiny": dict(desc="2D Laplacian 30x30, [3.0,3.8]", gen=lambda: M.laplacian2d(30),
                      interval=(3.0, 3.8), cfg=dict(), expect=124),
