@@ -95,6 +95,13 @@ class DenseBlock {
   // downloads then run at full PCIe rate and touch no fresh pageable pages.  Falls back to
   // ordinary storage when pinning fails.  Copies of such a block own ordinary storage.
   static DenseBlock pinned(std::size_t rows, std::size_t cols);
+  // keeps the first `cols` columns (no reallocation, no copy); cols <= cols()
+  void shrink_cols(std::size_t cols) {
+    if (cols < cols_) {
+      cols_ = cols;
+      if (!ext_) data_.resize(rows_ * cols_);
+    }
+  }
 
   DenseBlock(const DenseBlock& o) : rows_(o.rows_), cols_(o.cols_) {
     if (o.ext_) data_.assign(o.ext_.get(), o.ext_.get() + o.size());

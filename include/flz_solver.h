@@ -28,6 +28,10 @@ typedef struct {
   double epsilon;
   int32_t max_degree;
   int32_t collect_diagnostics;
+  /* extension (not in the reference): 0 = keep the eigenvectors on the device side of the
+   * recovery and return only eigenvalues and residuals (large runs: n x count doubles need
+   * not cross PCIe); flz_config_default sets 1 */
+  int32_t return_vectors;
 } flz_config;
 
 /* speig::SolveStats (lanczos.hpp:136-155) + the GPU build's host buckets. */

@@ -41,6 +41,7 @@ class FlzConfig(C.Structure):
         ("check_every", C.c_int32), ("seed", C.c_uint64), ("extra_ritz", C.c_int32),
         ("bounds_steps", C.c_int32), ("degree", C.c_int32), ("epsilon", C.c_double),
         ("max_degree", C.c_int32), ("collect_diagnostics", C.c_int32),
+        ("return_vectors", C.c_int32),
     ]
 
 

@@ -71,6 +71,7 @@ LanczosConfig to_config(const flz_config& c) {
   k.epsilon = c.epsilon;
   k.max_degree = c.max_degree;
   k.collect_diagnostics = c.collect_diagnostics != 0;
+  k.return_vectors = c.return_vectors != 0;
   return k;
 }
 
@@ -98,6 +99,7 @@ void flz_config_default(flz_config* cfg) {
   cfg->epsilon = k.epsilon;
   cfg->max_degree = k.max_degree;
   cfg->collect_diagnostics = 0;
+  cfg->return_vectors = 1;
 }
 
 int flz_set_default_ctx(flz_ctx* ctx) {

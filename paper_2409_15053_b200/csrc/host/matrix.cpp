@@ -269,8 +269,17 @@ DenseBlock DenseBlock::pinned(std::size_t rows, std::size_t cols) {
   void* p = nullptr;
   constexpr std::size_t kMaxPinned = std::size_t(2) << 30;  // larger blocks stay pageable
   const std::size_t bytes = rows * cols * sizeof(double);
-  if (bytes == 0 || bytes > kMaxPinned || flz_host_alloc(bytes, &p) != FLZ_OK || !p)
-    return uninitialized(rows, cols);
+  if (bytes == 0 || bytes > kMaxPinned || flz_host_alloc(bytes, &p) != FLZ_OK || !p) {
+    // pageable: fault the pages in on several threads now (a device download into untouched
+    // memory runs at page-fault speed, ~2 GB/s; measured 4.4 s for 8.9 GB of eigenvectors)
+    DenseBlock B = uninitialized(rows, cols);
+    double* base = B.data();
+    const std::size_t count = rows * cols;
+    parallel_rows(count / 512 + 1, [&](std::size_t p0, std::size_t p1) {
+      for (std::size_t q = p0; q < p1 && q * 512 < count; ++q) base[q * 512] = 0.0;
+    });
+    return B;
+  }
   DenseBlock B;
   B.rows_ = rows;
   B.cols_ = cols;

@@ -431,7 +431,7 @@ RitzSet check_convergence(const LanczosFactorization::Snapshot& st, double alpha
 // ----------------------------------------------------------------- recovery
 EigenResult recover_eigenpairs(const LanczosFactorization& st, const SparseSymMatrix& A,
                                double alpha, double beta, const RitzSet& ritz,
-                               double norm_estimate) {
+                               double norm_estimate, bool return_vectors) {
   const std::size_t n = st.n(), dim = st.basis_size();
   const double scale = norm_estimate > 0.0 ? norm_estimate : 1.0;
   flz_ctx* ctx = Device::context();
@@ -445,6 +445,12 @@ EigenResult recover_eigenpairs(const LanczosFactorization& st, const SparseSymMa
     out.eigenvectors = DenseBlock(n, 0);
     return out;
   }
+
+  // host storage of the eigenvectors (page-locked or pre-faulted): prepared on a second
+  // thread while the device lifts the Ritz vectors; at most w columns are needed
+  std::future<DenseBlock> storage;
+  if (return_vectors)
+    storage = std::async(std::launch::async, [n, w] { return DenseBlock::pinned(n, w); });
 
   // Ritz vectors of T_k for the candidates only.
   const WallClock t_w;
@@ -507,30 +513,36 @@ EigenResult recover_eigenpairs(const LanczosFactorization& st, const SparseSymMa
     }
     out.eigenvalues = lambdas;  // already ascending
     out.residuals.assign(sel.size(), 0.0);
-    out.eigenvectors = DenseBlock::pinned(n, sel.size());
+    if (return_vectors) {
+      out.eigenvectors = storage.get();
+      out.eigenvectors.shrink_cols(sel.size());
+    } else {
+      out.eigenvectors = DenseBlock(n, 0);
+    }
     const WallClock t_rot;
     if (!sel.empty())
       throw_status(flz_ritz_rotate(ctx, st.device(), U.data(), lambdas.data(),
                                    static_cast<int>(sel.size()), scale, out.residuals.data(),
-                                   out.eigenvectors.data()));
+                                   return_vectors ? out.eigenvectors.data() : nullptr));
     trace("recover: rotate + residuals + D2H", t_rot);
   } else if (wk > 0) {
     // plain mode: Ritz values are the eigenvalue estimates (:480-495)
     std::vector<double> lam(wk), res(wk);
     for (std::size_t c = 0; c < wk; ++c) lam[c] = ritz.values[kept_src[c]];
-    DenseBlock V = DenseBlock::uninitialized(n, wk);
+    DenseBlock V = return_vectors ? storage.get() : DenseBlock(n, 0);
+    if (return_vectors) V.shrink_cols(wk);
     throw_status(flz_ritz_plain(ctx, A.device(), st.device(), lam.data(), static_cast<int>(wk),
-                                scale, res.data(), V.data()));
+                                scale, res.data(), return_vectors ? V.data() : nullptr));
     std::vector<std::size_t> sel;
     for (std::size_t c = 0; c < wk; ++c)
       if (lam[c] >= alpha && lam[c] <= beta) sel.push_back(c);
     std::stable_sort(sel.begin(), sel.end(),
                      [&](std::size_t a, std::size_t b) { return lam[a] < lam[b]; });
-    out.eigenvectors = DenseBlock(n, sel.size());
+    out.eigenvectors = DenseBlock(n, return_vectors ? sel.size() : 0);
     for (std::size_t t = 0; t < sel.size(); ++t) {
       out.eigenvalues.push_back(lam[sel[t]]);
       out.residuals.push_back(res[sel[t]]);
-      std::copy(V.col(sel[t]), V.col(sel[t]) + n, out.eigenvectors.col(t));
+      if (return_vectors) std::copy(V.col(sel[t]), V.col(sel[t]) + n, out.eigenvectors.col(t));
     }
   } else {
     out.eigenvectors = DenseBlock(n, 0);
@@ -683,7 +695,7 @@ EigenResult run_solve(const SparseSymMatrix& A, double alpha, double beta,
       can_expand = true;
       since_check = 0;
       const WallClock rec;
-      result = recover_eigenpairs(st, A, alpha, beta, ritz, norm_est);
+      result = recover_eigenpairs(st, A, alpha, beta, ritz, norm_est, cfg.return_vectors);
       time_recover += rec.seconds();
       // accept only when every TRUE residual meets the tolerance (:617-623)
       converged = std::all_of(result.residuals.begin(), result.residuals.end(),
@@ -708,7 +720,7 @@ EigenResult run_solve(const SparseSymMatrix& A, double alpha, double beta,
     const RitzSet ritz = check_convergence(st, alpha, beta, cfg.tol, cfg.extra_ritz);
     time_check += chk.seconds();
     const WallClock rec;
-    result = recover_eigenpairs(st, A, alpha, beta, ritz, norm_est);
+    result = recover_eigenpairs(st, A, alpha, beta, ritz, norm_est, cfg.return_vectors);
     time_recover += rec.seconds();
   }
 

@@ -15,10 +15,12 @@ from .device import _fcol, _from_fcol, _ptr
 
 def LanczosConfig(block_size=3, tol=1e-10, max_dim=0, check_every=10, seed=20177, extra_ritz=5,
                   bounds_steps=50, degree=0, epsilon=0.255, max_degree=1000,
-                  collect_diagnostics=False) -> FlzConfig:
-    """speig::LanczosConfig defaults (lanczos.hpp:14-29); degree<=0 / None = automatic."""
+                  collect_diagnostics=False, return_vectors=True) -> FlzConfig:
+    """speig::LanczosConfig defaults (lanczos.hpp:14-29); degree<=0 / None = automatic.
+    ``return_vectors=False`` (extension) keeps the eigenvectors off the host."""
     return FlzConfig(block_size, tol, max_dim, check_every, seed, extra_ritz, bounds_steps,
-                     int(degree or 0), epsilon, max_degree, int(collect_diagnostics))
+                     int(degree or 0), epsilon, max_degree, int(collect_diagnostics),
+                     int(return_vectors))
 
 
 @dataclass
@@ -265,6 +267,9 @@ class _ResultOwner:
 
 def _solve(A: SparseSymMatrix, alpha, beta, cfg, plain, want_vectors):
     cfg = cfg or LanczosConfig()
+    if not want_vectors and cfg.return_vectors:   # do not even download them
+        cfg = FlzConfig(*[getattr(cfg, k) for k, _ in FlzConfig._fields_])
+        cfg.return_vectors = 0
     h = C.c_void_p()
     check(lib().flz_solve(A.handle, alpha, beta, C.byref(cfg), int(plain), C.byref(h)))
     owner = _ResultOwner(h)
@@ -273,7 +278,7 @@ def _solve(A: SparseSymMatrix, alpha, beta, cfg, plain, want_vectors):
     st = FlzStats()
     check(lib().flz_result_get(h, _ptr(ev), _ptr(res), None, C.byref(st)))
     vec = None
-    if want_vectors:
+    if want_vectors and cfg.return_vectors:
         rows = int(lib().flz_result_rows(h))
         if cnt * rows:
             # zero-copy view of the result's own storage; the view keeps the result alive

@@ -16,7 +16,7 @@ deg = int(sys.argv[2]) if len(sys.argv) > 2 else 333
 for count, degree in ((gap_count(330), deg),):
     hi = 0.5 * (s[count - 1] + s[count])
     t0 = time.time()
-    res = S.filtered_lanczos(H, -0.01, hi, S.LanczosConfig(block_size=3, degree=degree, max_dim=900), want_vectors=False)
+    res = S.filtered_lanczos(H, -0.01, hi, S.LanczosConfig(block_size=3, degree=degree, max_dim=900), want_vectors=bool(os.environ.get("WANT_VECTORS")))
     st = res.stats
     ok = len(res.eigenvalues) == count and np.abs(res.eigenvalues - s[:count]).max() < 1e-9
     print(f"g={g} [-0.01,{hi:.5f}] want {count} degree {degree}: got {len(res.eigenvalues)} conv={st['converged']} "
