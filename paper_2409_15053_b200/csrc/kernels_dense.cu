@@ -32,11 +32,31 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
       : "d"(a), "d"(b));
 }
 
+// 16-byte streaming load, volatile so that the loads of a group are all issued before the
+// (volatile) DMMAs that consume them — left to itself the compiler interleaves load and DMMA
+// pairs to save registers, which leaves one load in flight per warp
+__device__ __forceinline__ double2 ld_stream_f64x2(const double* p) {
+  double2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double2 ld_cached_f64x2(const double* p) {
+  double2 v;
+  asm volatile("ld.global.nc.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
+
 // ---------------------------------------------------------------- gemm_tn
-// Work item = (8-column tile of A, k-chunk): one warp each, 8 warps per CTA, items ordered so
-// that the warps of a CTA share the k-chunk (the B rows they read are the same -> L1).  The
-// k-chunking adapts to M: a 3-column projection (first Lanczos steps, intra-block QR) is split
-// into hundreds of chunks, a 3000-column one into a few, always ~32 warps per SM.
+// Work item = (8-column tile of A, k-chunk): one CTA of 8 warps each.  The warps of a CTA
+// interleave over the chunk's rows in groups of 64 (eight 8-row MMA steps, all loads of a
+// group in flight together), so that at any moment a CTA reads 4 KB of CONTIGUOUS memory from
+// each of its 8 columns: DRAM pages are
+// used whole.  (The first version gave every warp its own column tile and a private row
+// range: ~38k concurrent 64-byte streams, 2.2 TB/s on a 3.4M x 600 basis.)  The eight partial
+// fragments meet in shared memory in warp order; chunk partials are combined by
+// reduce_partials_kernel in chunk order: deterministic.
+// The k-chunking adapts to M: a 3-column projection (first Lanczos steps, intra-block QR) is
+// split into hundreds of chunks, a 3000-column one into a few.
 // Lane (g = lane>>2, t = lane&3) loads the double2 at rows k+2t, k+2t+1 of column g: the
 // .x halves of a warp form one 8x4 k-slab, the .y halves the next (the k order inside an
 // MMA is free as long as A and B agree), so every load is a full 16 B per lane.
@@ -46,9 +66,10 @@ __global__ void __launch_bounds__(256)
                    const double* __restrict__ B, int64_t ldb, int N, int64_t rows8,
                    int64_t rows_per_chunk, int64_t mtiles, int64_t nitems,
                    double* __restrict__ part, int64_t Mpad, int Npad) {
+  __shared__ double frag[8][NT][2][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
-  const int64_t item = (int64_t)blockIdx.x * 8 + warp;
+  const int64_t item = blockIdx.x;
   if (item >= nitems) return;
   const int64_t chunk = item / mtiles;
   const int64_t m0 = (item - chunk * mtiles) * 8;
@@ -69,17 +90,39 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt) c[nt][0] = c[nt][1] = 0.0;
 
-#pragma unroll 4
-  for (int64_t k = k0; k < k1; k += 8) {
-    double2 a2 = a_ok ? *reinterpret_cast<const double2*>(ap + k) : make_double2(0.0, 0.0);
+  constexpr int U = NT >= 4 ? 4 : 8;  // 8-row MMA steps per group: 16 B x 2U loads in flight
+  for (int64_t kb = k0 + warp * (8 * U); kb < k1; kb += 8 * (8 * U)) {
+    double2 a2[U], b2[U][NT];
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      double2 b2 = b_ok[nt] ? *reinterpret_cast<const double2*>(bp[nt] + k)
-                            : make_double2(0.0, 0.0);
-      dmma(c[nt][0], c[nt][1], a2.x, b2.x);
-      dmma(c[nt][0], c[nt][1], a2.y, b2.y);
+    for (int u = 0; u < U; ++u) {  // all loads of the group first
+      const int64_t k = kb + 8 * u;
+      const bool in = k < k1;
+      a2[u] = (a_ok && in) ? ld_stream_f64x2(ap + k) : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+        b2[u][nt] = (b_ok[nt] && in) ? ld_cached_f64x2(bp[nt] + k) : make_double2(0.0, 0.0);
     }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        dmma(c[nt][0], c[nt][1], a2[u].x, b2[u][nt].x);
+        dmma(c[nt][0], c[nt][1], a2[u].y, b2[u][nt].y);
+      }
   }
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    frag[warp][nt][0][lane] = c[nt][0];
+    frag[warp][nt][1][lane] = c[nt][1];
+  }
+  __syncthreads();
+  if (warp != 0) return;
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt)
+    for (int w = 1; w < 8; ++w) {
+      c[nt][0] += frag[w][nt][0][lane];
+      c[nt][1] += frag[w][nt][1][lane];
+    }
   // C fragment: row g, columns 2t, 2t+1 of each 8x8 tile
   double* out = part + (chunk * Mpad + m0 + g) * Npad + n0 + 2 * t;
 #pragma unroll
@@ -286,19 +329,19 @@ void launch_gemm_tn(flz_ctx* ctx, const double* A, int64_t lda, int64_t M, const
   const int NT = N > 16 ? 4 : (N > 8 ? 2 : 1);
   const int64_t mtiles = (M + 7) / 8;
   const int nblocks = (N + 8 * NT - 1) / (8 * NT);
-  // ~32 warps per SM over the whole grid, chunks of at least 256 rows
-  const int64_t want_warps = (int64_t)ctx->sm_count * 32;
-  int64_t nchunks = (want_warps + mtiles * nblocks - 1) / (mtiles * nblocks);
-  const int64_t max_chunks = (rows8 + 255) / 256;
+  // ~4 CTAs (32 warps) per SM over the whole grid, chunks of at least 2048 rows
+  const int64_t want_ctas = (int64_t)ctx->sm_count * 6;
+  int64_t nchunks = (want_ctas + mtiles * nblocks - 1) / (mtiles * nblocks);
+  const int64_t max_chunks = (rows8 + 2047) / 2048;
   if (nchunks > max_chunks) nchunks = max_chunks;
   if (nchunks < 1) nchunks = 1;
-  const int64_t rpc = round_up((rows8 + nchunks - 1) / nchunks, 8);
+  const int64_t rpc = round_up((rows8 + nchunks - 1) / nchunks, 512);
   nchunks = (rows8 + rpc - 1) / rpc;
   const int64_t Mpad = mtiles * 8;
   const int Npad = nblocks * 8 * NT;
   const int64_t nitems = mtiles * nchunks;
   ctx->partial.reserve((size_t)(nchunks * Mpad * Npad));
-  dim3 grid((unsigned)((nitems + 7) / 8), (unsigned)nblocks);
+  dim3 grid((unsigned)nitems, (unsigned)nblocks);
   switch (NT) {
     case 1:
       gemm_tn_kernel<1><<<grid, 256, 0, ctx->stream>>>(A, lda, M, B, ldb, N, rows8, rpc, mtiles,
