@@ -331,7 +331,7 @@ def run_flz(args, wl):
     # what the kernel really streams: the index-compressed matrix (8 bytes per entry at
     # uniform-offset positions) + the block vectors (row stride 4 for 3 columns on long rows)
     lay = H.layout() if world == 1 else None
-    stride = 4 if (r == 3 and nnz >= 16 * n) else r
+    stride = 4 if (r == 3 and nnz >= 16 * n) else r   # planar or interleaved: R doubles per row
     moved = lay["matrix_bytes"] + 8 * n * (3 * stride + r) if lay else None
     traffic = None
     prof = os.path.join(ROOT, "profiles", "k1_traffic.json")

@@ -212,14 +212,16 @@ void sell_step(const flz_matrix* A, int R, int S, StepMode mode, double s1, doub
 
 // Layout of the filter workspaces for R fused columns (see launch_clenshaw_step):
 // interleaved rows, 3 columns padded to 4 (one aligned 32-byte sector per gathered row) when
-// the matrix is gather dominated (>= 16 entries per row).  The planar layout (0) is kept as
-// an experiment (FLZ_K1_LAYOUT=planar): measured on B200 it is slower than interleaved rows
-// even for pure stencils (100^3 Laplacian, 3 columns: 84 % vs 96 % of the copy bandwidth).
+// the matrix is gather dominated (>= 16 entries per row); planar (0) for stencil matrices
+// with 3 columns.  FLZ_K1_LAYOUT=planar|interleaved|4 forces a layout (experiments).
 // The exact-mode kernel always reads interleaved rows of stride R.
 int row_stride(const flz_matrix* A, int R) {
   if (A->ctx->exact || A->nl == 0) return R;
   static const char* force = std::getenv("FLZ_K1_LAYOUT");  // experiments: planar | interleaved
-  const bool planar = force && force[0] == 'p';
+  // planar blocks pay for stencil matrices with 3 columns on one GPU (100^3 Laplacian: 23.0 vs
+  // 25.0 us per step: a coalesced 8-byte warp load touches 2-3 lines, a 24-byte-stride one 7);
+  // with 4 columns the 32-byte rows win (37.3 vs 39.4 us)
+  const bool planar = force ? force[0] == 'p' : (A->lean && R == 3 && A->ctx->nranks == 1);
   if (planar) return 0;
   if (R != 3) return R;
   if (force && force[0] == '4') return 4;  // experiments: padded rows for every matrix

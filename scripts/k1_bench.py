@@ -26,7 +26,7 @@ def bench(name, csr, r, m=50, sigma=0, check=True):
     gbs = 4 * m * bytes_step / (ms * 1e-3) / 1e9
     st = A.stats()
     stride = 4 if (r == 3 and nnz >= 16 * n) else r
-    if os.environ.get("FLZ_K1_LAYOUT", "")[:1] == "p":
+    if os.environ.get("FLZ_K1_LAYOUT", "")[:1] == "p" or (not os.environ.get("FLZ_K1_LAYOUT") and r == 3 and nnz < 16 * n):
         stride = r
     if os.environ.get("FLZ_K1_LAYOUT", "")[:1] == "4" and r == 3:
         stride = 4
