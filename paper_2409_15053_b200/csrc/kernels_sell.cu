@@ -412,7 +412,8 @@ __device__ __forceinline__ void add_rest(const SellView& A, int64_t row, double 
 #define FLZ_K1_LATE_OWN 1  // own-row operands: L2 prefetch up front, loads after the gathers
 #endif
 template <int R, int S, int MODE, int U>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, R <= 3 ? FLZ_K1_LEAN_CTAS : 1)
+__global__ void __launch_bounds__(kWarpsPerBlock * 32,
+                                  R == 1 ? 12 : (R <= 3 ? FLZ_K1_LEAN_CTAS : 1))  // R = 1 fits 40 registers
     clenshaw_step_ug_warp(SellView A, int slices_per_cta, double s1, double s2, double b,
                           const double* __restrict__ Y1, double* __restrict__ Y2, int64_t ldy,
                           const double* __restrict__ X, int64_t ldx, double* __restrict__ Out,
