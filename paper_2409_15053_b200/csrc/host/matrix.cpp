@@ -267,7 +267,10 @@ void SparseSymMatrix::verify_symmetry() const {
 
 DenseBlock DenseBlock::pinned(std::size_t rows, std::size_t cols) {
   void* p = nullptr;
-  constexpr std::size_t kMaxPinned = std::size_t(2) << 30;  // larger blocks stay pageable
+  // Larger blocks stay pageable: page-locking hundreds of MB takes ~0.25 s and stalls every
+  // other CUDA call of the process meanwhile (measured on the first solves of C2), whereas
+  // pre-faulted pageable memory downloads at ~19 GB/s.
+  constexpr std::size_t kMaxPinned = std::size_t(64) << 20;
   const std::size_t bytes = rows * cols * sizeof(double);
   if (bytes == 0 || bytes > kMaxPinned || flz_host_alloc(bytes, &p) != FLZ_OK || !p) {
     // pageable: fault the pages in on several threads now (a device download into untouched
