@@ -131,6 +131,11 @@ int flz_plan_arrays(const flz_plan* plan, int32_t* perm, int64_t* slice_ptr, int
  * Any pointer may be NULL. */
 int flz_plan_ug(const flz_plan* plan, int64_t* sizes, int32_t* descriptors, double* ug_val,
                 int32_t* ug_col, int32_t* ug_uoff, int32_t* rest_rows);
+/* paired layout of the plan (long ragged rows; host/plan.hpp), for host-side checks:
+ * sizes[4] = {used, 64-row slices, positions, interior slices}; ptr[slices + 1] first position
+ * of every slice; col[positions * 32]; val[positions * 64] (two values per lane and position).
+ * Any pointer may be NULL. */
+int flz_plan_p2(const flz_plan* plan, int64_t* sizes, int64_t* ptr, int32_t* col, double* val);
 
 /* Global matvec counter: speig::matvec_count()/reset (sparse.hpp:74-79).  One count per
  * vector-column product, so a fused r-column block product adds r. */

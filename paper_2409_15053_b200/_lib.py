@@ -93,6 +93,7 @@ _SIGS = {
     "flz_plan_set_give": (i32, [vp, i32, i64, i64p]),
     "flz_plan_arrays": (i32, [vp] + [vp] * 12),
     "flz_plan_ug": (i32, [vp, vp, vp, vp, vp, vp, vp]),
+    "flz_plan_p2": (i32, [vp, vp, vp, vp, vp]),
     "flz_matvec_count": (u64, []),
     "flz_reset_matvec_count": (None, []),
     "flz_matvec_sub": (None, [u64]),

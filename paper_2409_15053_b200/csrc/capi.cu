@@ -111,7 +111,15 @@ SellView make_view(const flz_matrix* A, const SliceTask* tasks, int64_t ntasks,
                   A->row_len.p, A->col.p,   A->val.p,      slice_ids,      nslices,
                   A->nl,        A->ug.p,    A->ug_val.p,   A->ug_col.p,    A->ug_uoff.p,
                   A->nl + A->nhalo, A->rest_rows.p, A->nslices,   A->w.p,
-                  A->uv_pairs.p};
+                  A->uv_pairs.p,    false,          A->p2_ptr.p,  A->p2_col.p, A->p2_val.p};
+}
+// fast mode on a matrix with the paired layout: the launch walks the paired task lists
+SellView paired(const flz_matrix* A, SellView v, int which) {
+  if (!A->p2 || A->ctx->exact) return v;
+  v.p2 = true;
+  v.tasks = which == 0 ? A->p2_tasks_all.p : (which == 1 ? A->p2_tasks_interior.p : A->p2_tasks_boundary.p);
+  v.ntasks = which == 0 ? A->p2_nt_all : (which == 1 ? A->p2_nt_interior : A->p2_nt_boundary);
+  return v;
 }
 // rest launches (SPLIT mode): task lists over the rest slices
 SellView view_rest(const flz_matrix* A, int which) {
@@ -121,14 +129,15 @@ SellView view_rest(const flz_matrix* A, int which) {
       which == 0 ? A->nt_rest_all : (which == 1 ? A->nt_rest_interior : A->nt_rest_boundary);
   return make_view(A, t.p, nt, nullptr, A->nrest);
 }
+SellView paired(const flz_matrix* A, SellView v, int which);
 SellView view_all(const flz_matrix* A) {
-  return make_view(A, A->tasks_all.p, A->nt_all, nullptr, A->nslices);
+  return paired(A, make_view(A, A->tasks_all.p, A->nt_all, nullptr, A->nslices), 0);
 }
 SellView view_interior(const flz_matrix* A) {
-  return make_view(A, A->tasks_interior.p, A->nt_interior, A->interior.p, A->n_interior);
+  return paired(A, make_view(A, A->tasks_interior.p, A->nt_interior, A->interior.p, A->n_interior), 1);
 }
 SellView view_boundary(const flz_matrix* A) {
-  return make_view(A, A->tasks_boundary.p, A->nt_boundary, A->boundary.p, A->n_boundary);
+  return paired(A, make_view(A, A->tasks_boundary.p, A->nt_boundary, A->boundary.p, A->n_boundary), 2);
 }
 
 // leading dimension of the planar filter workspaces (local rows + halo rows, padded)
@@ -532,6 +541,23 @@ static void upload_plan(flz_ctx* ctx, HostPlan& P, flz_matrix* A) {
   up(A->ug_col, P.ug_col);
   up(A->ug_uoff, P.ug_uoff);
   up(A->uv_pairs, P.uv_pairs);
+  A->p2 = P.p2;
+  if (P.p2) {
+    up(A->p2_ptr, P.p2_ptr);
+    up(A->p2_col, P.p2_col);
+    up(A->p2_val, P.p2_val);
+    auto up_p2 = [&](DevBuf<SliceTask>& buf, const std::vector<PlanTask>& host, int64_t& count) {
+      count = (int64_t)host.size();
+      buf.reserve(std::max<size_t>(host.size(), 1));
+      if (!host.empty())
+        FLZ_CUDA(cudaMemcpyAsync(buf.p, host.data(), host.size() * sizeof(PlanTask),
+                                 cudaMemcpyHostToDevice, ctx->stream));
+    };
+    up_p2(A->p2_tasks_all, P.p2_tasks_all, A->p2_nt_all);
+    up_p2(A->p2_tasks_interior, P.p2_tasks_interior, A->p2_nt_interior);
+    up_p2(A->p2_tasks_boundary, P.p2_tasks_boundary, A->p2_nt_boundary);
+    A->p2_bytes = (int64_t)(P.p2_col.size() * 4 + P.p2_val.size() * 8 + P.p2_ptr.size() * 8);
+  }
   A->ug_bytes = (int64_t)(P.ug_val.size() * 8 + P.ug_col.size() * 4 + P.ug_uoff.size() * 4 +
                           P.ug_slice.size() * sizeof(UgSlice));
   A->ug_uniform_entries = P.ug_uniform_entries;
@@ -760,6 +786,22 @@ int flz_plan_ug(const flz_plan* plan, int64_t* sizes, int32_t* descriptors, doub
   return FLZ_OK;
 }
 
+int flz_plan_p2(const flz_plan* plan, int64_t* sizes, int64_t* ptr, int32_t* col, double* val) {
+  if (!plan) return FLZ_EINVAL;
+  const HostPlan& P = plan->P;
+  if (sizes) {
+    sizes[0] = P.p2 ? 1 : 0;
+    sizes[1] = P.p2_slices;
+    sizes[2] = P.p2 ? P.p2_ptr.back() : 0;   // positions
+    sizes[3] = (int64_t)P.p2_interior.size();
+  }
+  if (!P.p2) return FLZ_OK;
+  if (ptr) std::copy(P.p2_ptr.begin(), P.p2_ptr.end(), ptr);
+  if (col) std::copy(P.p2_col.begin(), P.p2_col.end(), col);
+  if (val) std::copy(P.p2_val.begin(), P.p2_val.end(), val);
+  return FLZ_OK;
+}
+
 static void matrix_release(flz_matrix* A) {
   if (!A || --A->refs > 0) return;
   flz_ctx* ctx = A->ctx;
@@ -782,7 +824,7 @@ int flz_matrix_stats(const flz_matrix* A, int64_t* stored_entries, int64_t* slic
 
 int flz_matrix_layout(const flz_matrix* A, int64_t* matrix_bytes, int64_t* uniform_entries) {
   if (!A) return FLZ_EINVAL;
-  if (matrix_bytes) *matrix_bytes = A->ug_bytes;
+  if (matrix_bytes) *matrix_bytes = A->p2 ? A->p2_bytes : A->ug_bytes;
   if (uniform_entries) *uniform_entries = A->ug_uniform_entries;
   return FLZ_OK;
 }

@@ -161,6 +161,14 @@ struct flz_matrix {
   flz::DevBuf<double> ug_val;
   flz::DevBuf<int32_t> ug_col, ug_uoff;
   flz::DevBuf<double> uv_pairs;     // lean matrices: 16 doubles per slice (host/plan.hpp)
+  // paired layout (host/plan.hpp)
+  bool p2 = false;
+  flz::DevBuf<int64_t> p2_ptr;
+  flz::DevBuf<int32_t> p2_col;
+  flz::DevBuf<double> p2_val;
+  flz::DevBuf<flz::SliceTask> p2_tasks_all, p2_tasks_interior, p2_tasks_boundary;
+  int64_t p2_nt_all = 0, p2_nt_interior = 0, p2_nt_boundary = 0;
+  int64_t p2_bytes = 0;
   int64_t ug_bytes = 0;             // matrix bytes one fast step streams
   int64_t ug_uniform_entries = 0;
   // SPLIT mode (host/plan.hpp): rest slices follow the main ones in `ug`
@@ -250,6 +258,12 @@ struct SellView {
   int64_t rest_base;
   double* W;
   const double* uv_pairs;    // lean matrices: (value, mask) pairs, 16 doubles per slice
+  // paired layout (host/plan.hpp): 64-row slices, two adjacent rows per lane; `tasks` then
+  // lists paired slices
+  bool p2;
+  const int64_t* p2_ptr;
+  const int32_t* p2_col;
+  const double* p2_val;
 };
 
 enum class StepMode { step, final, plain, rest };

@@ -84,13 +84,18 @@ int32_t length_class(int32_t len) {
   if (len <= 8) return len;
   return 8 + (int32_t)std::ceil(std::log((double)len / 8.0) / std::log(1.2));
 }
-void sort_windows(const std::vector<int32_t>& len, int64_t sigma, std::vector<int32_t>& perm) {
+// `key` (optional) replaces the row length as the sorting key: the paired layout sorts PAIRS
+// of adjacent rows by the length of their merged column list — both rows of a pair carry the
+// same key, windows hold an even number of rows, so a stable sort keeps every pair adjacent
+// and on an even position.
+void sort_windows(const std::vector<int32_t>& len, int64_t sigma, std::vector<int32_t>& perm,
+                  const std::vector<int32_t>* key = nullptr) {
   const int64_t nl = (int64_t)len.size();
   perm.resize(nl);
   std::iota(perm.begin(), perm.end(), 0);
   if (sigma <= 1) return;
   std::vector<int32_t> cls(nl);
-  for (int64_t i = 0; i < nl; ++i) cls[i] = length_class(len[i]);
+  for (int64_t i = 0; i < nl; ++i) cls[i] = length_class(key ? (*key)[i] : len[i]);
   for (int64_t w0 = 0; w0 < nl; w0 += sigma) {
     const int64_t w1 = std::min(nl, w0 + sigma);
     std::stable_sort(perm.begin() + w0, perm.begin() + w1,
@@ -538,6 +543,101 @@ int64_t build_ug(HostPlan& P, const std::vector<uint8_t>& is_boundary, bool allo
   return (int64_t)rest_col.size();
 }
 
+// ---- paired layout (plan.hpp) ------------------------------------------------------------
+void build_p2(HostPlan& P, const std::vector<uint8_t>& is_boundary32) {
+  const int64_t nl = P.nl;
+  const int64_t ns = P.p2_slices = (nl + 63) / 64;
+  P.p2_ptr.assign(ns + 1, 0);
+  std::vector<int32_t> len(ns, 0);
+  const int nchunks = (int)std::max<int64_t>(1, std::min<int64_t>(worker_count(), ns / 64));
+  // merged (column, value A, value B) list of one lane, ascending column
+  struct Entry {
+    int32_t col;
+    double a, b;
+  };
+  auto merge_lane = [&](int64_t rowA, std::vector<Entry>& out, std::vector<Entry>& tmp) {
+    out.clear();
+    for (int which = 0; which < 2; ++which) {
+      const int64_t row = rowA + which;
+      if (row >= nl) continue;
+      const int64_t s32 = row / kPlanSliceRows, l32 = row % kPlanSliceRows;
+      const int64_t base = P.slice_ptr[s32] + l32;
+      tmp.clear();
+      for (int32_t p = 0; p < P.row_len[row]; ++p) {
+        const int64_t e = base + (int64_t)p * kPlanSliceRows;
+        tmp.push_back({P.col[e], which == 0 ? P.val[e] : 0.0, which == 1 ? P.val[e] : 0.0});
+      }
+      std::sort(tmp.begin(), tmp.end(), [](const Entry& x, const Entry& y) { return x.col < y.col; });
+      if (which == 0) {
+        out = tmp;
+      } else {  // merge into out
+        std::vector<Entry> merged;
+        merged.reserve(out.size() + tmp.size());
+        size_t i = 0, j = 0;
+        while (i < out.size() || j < tmp.size()) {
+          if (j == tmp.size() || (i < out.size() && out[i].col < tmp[j].col)) merged.push_back(out[i++]);
+          else if (i == out.size() || tmp[j].col < out[i].col) merged.push_back(tmp[j++]);
+          else {
+            merged.push_back({out[i].col, out[i].a, tmp[j].b});
+            ++i;
+            ++j;
+          }
+        }
+        out.swap(merged);
+      }
+    }
+  };
+  // pass 1: slice lengths
+  run_chunks(nchunks, [&](int t) {
+    std::vector<Entry> lane, tmp;
+    for (int64_t s = ns * t / nchunks; s < ns * (t + 1) / nchunks; ++s) {
+      int32_t L = 0;
+      for (int l = 0; l < 32; ++l) {
+        merge_lane(s * 64 + 2 * l, lane, tmp);
+        L = std::max<int32_t>(L, (int32_t)lane.size());
+      }
+      len[s] = L;
+    }
+  });
+  for (int64_t s = 0; s < ns; ++s) P.p2_ptr[s + 1] = P.p2_ptr[s] + len[s];
+  const int64_t positions = P.p2_ptr[ns];
+  P.p2_entries = positions * 32;
+  P.p2_col.assign(std::max<int64_t>(positions * 32, 1), 0);
+  P.p2_val.assign(std::max<int64_t>(positions * 64, 2), 0.0);
+  // pass 2: fill
+  run_chunks(nchunks, [&](int t) {
+    std::vector<Entry> lane, tmp;
+    for (int64_t s = ns * t / nchunks; s < ns * (t + 1) / nchunks; ++s) {
+      int32_t* c = P.p2_col.data() + P.p2_ptr[s] * 32;
+      double* v = P.p2_val.data() + P.p2_ptr[s] * 64;
+      for (int l = 0; l < 32; ++l) {
+        const int64_t rowA = s * 64 + 2 * l;
+        merge_lane(rowA, lane, tmp);
+        const int32_t self = (int32_t)std::min<int64_t>(rowA, std::max<int64_t>(nl - 1, 0));
+        for (int32_t p = 0; p < len[s]; ++p) {
+          const bool on = p < (int32_t)lane.size();
+          c[(int64_t)p * 32 + l] = on ? lane[p].col : self;
+          v[((int64_t)p * 32 + l) * 2] = on ? lane[p].a : 0.0;
+          v[((int64_t)p * 32 + l) * 2 + 1] = on ? lane[p].b : 0.0;
+        }
+      }
+    }
+  });
+  // interior / boundary: a 64-row slice covers two 32-row slices
+  P.p2_interior.clear();
+  P.p2_boundary.clear();
+  std::vector<int32_t> all(ns);
+  for (int64_t s = 0; s < ns; ++s) {
+    all[s] = (int32_t)s;
+    const bool b = is_boundary32[2 * s] || (2 * s + 1 < (int64_t)is_boundary32.size() && is_boundary32[2 * s + 1]);
+    (b ? P.p2_boundary : P.p2_interior).push_back((int32_t)s);
+  }
+  choose_task_target(len);
+  P.p2_tasks_all = build_tasks(all, len);
+  P.p2_tasks_interior = build_tasks(P.p2_interior, len);
+  P.p2_tasks_boundary = build_tasks(P.p2_boundary, len);
+}
+
 struct PhaseTimer {  // FLZ_TRACE=1: phase timings of build_plan on stderr
   std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
   bool on = std::getenv("FLZ_TRACE") != nullptr;
@@ -620,17 +720,52 @@ HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<in
   }
 
   timer.lap("split estimate");
+  // ---- paired layout ahead?  Then rows are sorted as pairs (see sort_windows): key = size of
+  // the merged column list of rows (2k, 2k+1), half of it per row so that classes stay
+  // comparable with row lengths
+  static const bool want_p2_sort = [] {
+    const char* e = std::getenv("FLZ_P2");
+    return !(e && e[0] == '0');
+  }();
+  std::vector<int32_t> pair_key;
+  {
+    int32_t longest = 0;
+    for (int64_t i = 0; i < nl; ++i) longest = std::max(longest, len[i]);
+    if (want_p2_sort && !P.split && longest > 24) {
+      pair_key.assign(nl, 0);
+      for (int64_t i = 0; i < nl; i += 2) {
+        int64_t a = row_ptr[i], a1 = row_ptr[i + 1];
+        int64_t b = i + 1 < nl ? row_ptr[i + 1] : 0, b1 = i + 1 < nl ? row_ptr[i + 2] : 0;
+        int32_t u = 0;
+        while (a < a1 || b < b1) {
+          if (b == b1 || (a < a1 && col_idx[a] < col_idx[b])) ++a;
+          else if (a == a1 || col_idx[b] < col_idx[a]) ++b;
+          else {
+            ++a;
+            ++b;
+          }
+          ++u;
+        }
+        pair_key[i] = (u + 1) / 2;
+        if (i + 1 < nl) pair_key[i + 1] = (u + 1) / 2;
+      }
+    }
+  }
+  const std::vector<int32_t>* sort_key = pair_key.empty() ? nullptr : &pair_key;
+
   // ---- sigma: smallest window whose padding overhead is <= 8 %
   int64_t chosen = sigma;
   if (P.split) {
     chosen = 1;  // natural order: uniform offsets only exist there
+  } else if (sigma <= 0 && sort_key) {
+    chosen = 16384;  // pairs: measured gathers/nnz 0.83 (1024), 0.77 (4096), 0.76 (16384), 0.75 (n)
   } else if (sigma <= 0) {
     const int64_t cands[] = {1, 256, 4096, 65536, std::max<int64_t>(nl, 1)};
     int64_t best_fill = -1;
     chosen = 1;
     for (int64_t sg : cands) {
       if (sg > 1 && sg > nl && sg != cands[4]) continue;
-      sort_windows(len, sg, P.perm);
+      sort_windows(len, sg, P.perm, sort_key);
       const int64_t f = padded_entries(len, P.perm);
       if (best_fill < 0 || f < best_fill) {
         best_fill = f;
@@ -642,7 +777,7 @@ HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<in
       }
     }
   }
-  sort_windows(len, chosen, P.perm);
+  sort_windows(len, chosen, P.perm, sort_key);
   P.sigma = (int)std::min<int64_t>(chosen, 1 << 30);
   bool identity = true;
   for (int64_t i = 0; i < nl && identity; ++i) identity = P.perm[i] == i;
@@ -780,6 +915,14 @@ HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<in
                                [](const PlanTask& t) { return t.warps_per_slice == 1; });
     P.lean = false;
   }
+  // long ragged rows: the paired layout feeds the fast kernel (FLZ_P2=0 keeps the UG tasks)
+  static const bool want_p2 = [] {
+    const char* e = std::getenv("FLZ_P2");
+    return !(e && e[0] == '0');
+  }();
+  P.p2 = want_p2 && !P.split && !P.lean && nl > 0;
+  if (P.p2) build_p2(P, is_boundary);
+  timer.lap("paired layout");
   P.uv_pairs.clear();
   if (P.lean) {
     P.uv_pairs.assign((size_t)nslices * 16, 0.0);

@@ -81,6 +81,21 @@ struct HostPlan {
   std::vector<int32_t> rest_rows;                    // [nrest * 32]
   std::vector<int32_t> rest_interior, rest_boundary; // slice ids (>= nslices)
   std::vector<PlanTask> tasks_rest_all, tasks_rest_interior, tasks_rest_boundary;
+  // PAIRED layout ("P2") for matrices with long ragged rows (not SPLIT, not lean): slices of
+  // 64 consecutive rows, lane l owns the ADJACENT rows 64 s + 2 l and + 1, and a position
+  // holds one column and TWO values (one per row, zero where a row lacks the entry).  The
+  // columns of a lane are the sorted union of its two rows' columns: neighbouring rows of the
+  // same dense block share almost all of them, so one 32-byte gather serves two matrix
+  // entries — the gathers, not HBM, bound this kernel.  p2_ptr[s] = first position
+  // of slice s (positions are [32 lanes] columns and [32 lanes][2] values).
+  bool p2 = false;
+  int64_t p2_slices = 0;
+  std::vector<int64_t> p2_ptr;                  // [p2_slices + 1]
+  std::vector<int32_t> p2_col;                  // [positions * 32]
+  std::vector<double> p2_val;                   // [positions * 64]
+  std::vector<int32_t> p2_interior, p2_boundary;
+  std::vector<PlanTask> p2_tasks_all, p2_tasks_interior, p2_tasks_boundary;
+  int64_t p2_entries = 0;                       // positions * 32 (gathers per product)
   // halo: sorted unique remote global columns; slot h lives at row nl + h of a gather source
   std::vector<int64_t> halo;
   std::vector<int64_t> need_off, need_cnt;  // per owner rank: run of `halo` it must send us

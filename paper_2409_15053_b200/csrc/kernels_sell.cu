@@ -584,6 +584,91 @@ __global__ void __launch_bounds__(kTaskWarps * 32, FLZ_K1_TASK_CTAS)
   }
 }
 
+// Paired layout (host/plan.hpp): slices of 64 rows, lane l owns the adjacent rows 2l and
+// 2l+1 of the slice; a position is one column and two values.  One gathered block row feeds
+// two rows of the product: on the PARSEC-shaped matrices, where neighbouring rows of a dense
+// non-local block share their columns, this needs 25 % fewer gathers than entries — and the
+// gathers (L1 wavefronts), not HBM, bound this kernel.  Task list and multi-warp split as in
+// clenshaw_step_ug_tasks.
+template <int R, int S, int MODE>
+__global__ void __launch_bounds__(kTaskWarps * 32, FLZ_K1_TASK_CTAS)
+    clenshaw_step_p2_tasks(SellView A, double s1, double s2, double b,
+                           const double* __restrict__ Y1, double* __restrict__ Y2, int64_t ldy,
+                           const double* __restrict__ X, int64_t ldx, double* __restrict__ Out,
+                           int64_t ldo) {
+  __shared__ double part[kTaskWarps][2 * R][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const SliceTask task = A.tasks[blockIdx.x];
+  const int W = task.warps_per_slice;
+  const int sub = warp / W, piece = warp - sub * W;
+  const bool active = sub < task.count;
+  double acc[2][R];
+#pragma unroll
+  for (int k = 0; k < R; ++k) acc[0][k] = acc[1][k] = 0.0;
+  int64_t row = 0;
+  if (active) {
+    const int64_t slice = task.slice[sub];
+    row = slice * 64 + 2 * lane;
+    const int64_t pos0 = __ldg(A.p2_ptr + slice);
+    const int L = (int)(__ldg(A.p2_ptr + slice + 1) - pos0);
+    const int chunk = (((L + W - 1) / W) + kBatch - 1) / kBatch * kBatch;
+    const int p0 = piece * chunk, p1 = min(L, p0 + chunk);
+    const int32_t* __restrict__ col = A.p2_col + (pos0 + p0) * 32 + lane;
+    const double* __restrict__ val = A.p2_val + ((pos0 + p0) * 32 + lane) * 2;
+    for (int p = p0; p < p1; p += kBatch) {
+      int c[kBatch];
+      double va[kBatch], vb[kBatch], g[kBatch][R];
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u) {
+        const bool ok = p + u < p1;
+        c[u] = ok ? ld_stream_s32(col + u * 32) : 0;
+        va[u] = vb[u] = 0.0;
+        if (ok)
+          asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];"
+                       : "=d"(va[u]), "=d"(vb[u]) : "l"(val + u * 64));
+      }
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u) gather_row<R, S>(Y1, ldy, c[u], p + u < p1, g[u]);
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u)
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+          acc[0][k] = fma(va[u], g[u][k], acc[0][k]);
+          acc[1][k] = fma(vb[u], g[u][k], acc[1][k]);
+        }
+      col += kBatch * 32;
+      val += kBatch * 64;
+    }
+  }
+  if (W > 1) {  // uniform across the CTA
+    if (active && piece > 0) {
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        part[warp][k][lane] = acc[0][k];
+        part[warp][R + k][lane] = acc[1][k];
+      }
+    }
+    __syncthreads();
+    if (active && piece == 0) {
+      for (int q = 1; q < W; ++q)
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+          acc[0][k] += part[warp + q][k][lane];
+          acc[1][k] += part[warp + q][R + k][lane];
+        }
+    }
+  }
+  if (!active || piece != 0) return;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int64_t r = row + h;
+    if (r >= A.nl) break;
+    double y1o[R], y2o[R], xo[R];
+    load_own<R, S, MODE>(A, r, Y1, Y2, ldy, X, ldx, y1o, y2o, xo);
+    finish_row<R, S, MODE>(r, s1, s2, b, acc[h], y1o, y2o, xo, Y2, ldy, Out, ldo);
+  }
+}
+
 // Y1[i*S+k] = scale * X[k*ldx+i], k < R; pad entries (R <= k < S) are zeroed
 template <int R, int S>
 __global__ void interleave_kernel(int64_t nl, double scale, const double* __restrict__ X,
@@ -654,6 +739,15 @@ void launch_ug(flz_ctx* ctx, const SellView& A, double s1, double s2, double b, 
   // groups inside a warp, shuffle reduction, no shared memory — was measured and dropped: on
   // the PARSEC-shaped matrix it took 40.8-49.6 us per step against 34.9 us, because lanes that
   // mix positions touch more L1 lines on general positions.)
+  if constexpr (MODE != 3) {
+    if (A.p2) {
+      if (A.ntasks == 0) return;
+      clenshaw_step_p2_tasks<R, S, MODE><<<(unsigned)A.ntasks, kTaskWarps * 32, 0, ctx->stream>>>(
+          A, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo);
+      ctx->launches++;
+      return;
+    }
+  }
   bool lean = false;
   if constexpr (MODE != 3) lean = A.short_rows && A.lean;
   if (lean) {

@@ -162,6 +162,37 @@ class HaloPlan:
         self._w_rows_used = W
         return (y[:nl], np.array(done, np.int64)) if which != "all" else y[:nl]
 
+    def p2_arrays(self):
+        """Paired layout (64-row slices, two rows per lane), or None when the plan has none."""
+        sizes = np.zeros(4, np.int64)
+        vp = lambda a: a.ctypes.data_as(C.c_void_p)
+        check(lib().flz_plan_p2(self.handle, vp(sizes), None, None, None))
+        if not sizes[0]:
+            return None
+        ptr = np.zeros(int(sizes[1]) + 1, np.int64)
+        col = np.zeros(max(int(sizes[2]) * 32, 1), np.int32)
+        val = np.zeros(max(int(sizes[2]) * 64, 2), np.float64)
+        check(lib().flz_plan_p2(self.handle, vp(sizes), vp(ptr), vp(col), vp(val)))
+        return dict(ptr=ptr, col=col, val=val, slices=int(sizes[1]), positions=int(sizes[2]),
+                    interior=int(sizes[3]))
+
+    def p2_product(self, x):
+        """y = A x evaluated from the paired layout as the kernel walks it."""
+        p2 = self.p2_arrays()
+        nl = self.info["rows_local"]
+        y = np.zeros(p2["slices"] * 64)
+        lanes = np.arange(32)
+        for s in range(p2["slices"]):
+            accA, accB = np.zeros(32), np.zeros(32)
+            for p in range(int(p2["ptr"][s]), int(p2["ptr"][s + 1])):
+                g = x[p2["col"][p * 32: p * 32 + 32]]
+                v = p2["val"][p * 64: p * 64 + 64].reshape(32, 2)
+                accA += v[:, 0] * g
+                accB += v[:, 1] * g
+            y[s * 64 + 2 * lanes] = accA
+            y[s * 64 + 2 * lanes + 1] = accB
+        return y[:nl]
+
     def __del__(self):
         try:
             lib().flz_plan_destroy(self.handle)

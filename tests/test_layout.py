@@ -117,3 +117,33 @@ def test_partitioned_ug_product(monkeypatch, nranks, split):
         out = np.zeros(nl)
         out[a["perm"]] = got
         assert np.abs(out - want[starts[p]:starts[p + 1]]).max() <= 1e-12 * np.abs(want).max()
+
+
+@pytest.mark.parametrize("gen", [lambda: M.parsec_like(radius=12.0, n_atoms=12),
+                                 lambda: M.parsec_like(radius=10.0, n_atoms=30, ball_radius=3.6),
+                                 lambda: M.random_sparse_sym(700, 0.06, 5)])
+def test_paired_layout_reproduces_product(gen):
+    """Long ragged rows: 64-row slices, two adjacent rows per lane, one column and two values
+    per position (host/plan.hpp).  The emulation walks it as clenshaw_step_p2_tasks does."""
+    csr = gen()
+    n, rp, ci, va = csr
+    P = HaloPlan(n, 0, 1, [0, n], rp, ci, va)
+    p2 = P.p2_arrays()
+    assert p2 is not None and p2["slices"] == (n + 63) // 64
+    a = P.arrays()
+    # pairs of adjacent rows stay adjacent (and even-aligned) under the permutation
+    perm = a["perm"]
+    even = perm[0:len(perm) - 1:2]
+    assert np.all((even % 2 == 0) & (perm[1::2] == even + 1)[: len(even)])
+    x = np.random.default_rng(9).standard_normal(n)
+    y = P.p2_product(x[perm])
+    want = reference(csr, x)[perm]
+    assert np.abs(y - want).max() <= 1e-12 * np.abs(want).max()
+    assert p2["positions"] * 32 <= 1.15 * len(va)       # at most the entries plus slice padding
+
+
+def test_paired_layout_saves_gathers_on_dense_blocks():
+    csr = M.parsec_like(radius=14.0, n_atoms=20, ball_radius=3.25)
+    n, rp, ci, va = csr
+    p2 = HaloPlan(n, 0, 1, [0, n], rp, ci, va).p2_arrays()
+    assert p2["positions"] * 32 <= 0.9 * len(va)
