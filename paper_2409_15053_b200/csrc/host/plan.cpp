@@ -544,7 +544,8 @@ int64_t build_ug(HostPlan& P, const std::vector<uint8_t>& is_boundary, bool allo
 }
 
 // ---- paired layout (plan.hpp) ------------------------------------------------------------
-void build_p2(HostPlan& P, const std::vector<uint8_t>& is_boundary32) {
+void build_p2(HostPlan& P, const std::vector<uint8_t>& is_boundary32,
+              const std::vector<int32_t>& pair_ulen) {
   const int64_t nl = P.nl;
   const int64_t ns = P.p2_slices = (nl + 63) / 64;
   P.p2_ptr.assign(ns + 1, 0);
@@ -587,18 +588,31 @@ void build_p2(HostPlan& P, const std::vector<uint8_t>& is_boundary32) {
       }
     }
   };
-  // pass 1: slice lengths
-  run_chunks(nchunks, [&](int t) {
+  // slice lengths: the merged list sizes of the pairs were counted before the rows were sorted
+  // (pair_ulen, indexed by the pair's first row in the original order)
+  // — valid where the sort kept the pair together on an even position; a lone last row sorted
+  // in front of the others shifts the pairing, and those lanes are merged here instead
+  {
     std::vector<Entry> lane, tmp;
-    for (int64_t s = ns * t / nchunks; s < ns * (t + 1) / nchunks; ++s) {
+    for (int64_t s = 0; s < ns; ++s) {
       int32_t L = 0;
       for (int l = 0; l < 32; ++l) {
-        merge_lane(s * 64 + 2 * l, lane, tmp);
-        L = std::max<int32_t>(L, (int32_t)lane.size());
+        const int64_t rowA = s * 64 + 2 * l;
+        if (rowA >= nl) break;
+        const int32_t origA = P.perm[rowA];
+        const bool lone = origA + 1 >= nl;
+        const bool kept = (origA % 2 == 0) &&
+                          (lone ? rowA + 1 >= nl : (rowA + 1 < nl && P.perm[rowA + 1] == origA + 1));
+        if (kept) {
+          L = std::max(L, pair_ulen[origA]);
+        } else {
+          merge_lane(rowA, lane, tmp);
+          L = std::max<int32_t>(L, (int32_t)lane.size());
+        }
       }
       len[s] = L;
     }
-  });
+  }
   for (int64_t s = 0; s < ns; ++s) P.p2_ptr[s + 1] = P.p2_ptr[s] + len[s];
   const int64_t positions = P.p2_ptr[ns];
   P.p2_entries = positions * 32;
@@ -727,12 +741,13 @@ HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<in
     const char* e = std::getenv("FLZ_P2");
     return !(e && e[0] == '0');
   }();
-  std::vector<int32_t> pair_key;
+  std::vector<int32_t> pair_key, pair_ulen;
   {
     int32_t longest = 0;
     for (int64_t i = 0; i < nl; ++i) longest = std::max(longest, len[i]);
     if (want_p2_sort && !P.split && longest > 24) {
       pair_key.assign(nl, 0);
+      pair_ulen.assign(nl, 0);
       for (int64_t i = 0; i < nl; i += 2) {
         int64_t a = row_ptr[i], a1 = row_ptr[i + 1];
         int64_t b = i + 1 < nl ? row_ptr[i + 1] : 0, b1 = i + 1 < nl ? row_ptr[i + 2] : 0;
@@ -748,6 +763,7 @@ HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<in
         }
         pair_key[i] = (u + 1) / 2;
         if (i + 1 < nl) pair_key[i + 1] = (u + 1) / 2;
+        pair_ulen[i] = u;
       }
     }
   }
@@ -920,8 +936,8 @@ HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<in
     const char* e = std::getenv("FLZ_P2");
     return !(e && e[0] == '0');
   }();
-  P.p2 = want_p2 && !P.split && !P.lean && nl > 0;
-  if (P.p2) build_p2(P, is_boundary);
+  P.p2 = want_p2 && !P.split && !P.lean && nl > 0 && !pair_ulen.empty();
+  if (P.p2) build_p2(P, is_boundary, pair_ulen);
   timer.lap("paired layout");
   P.uv_pairs.clear();
   if (P.lean) {

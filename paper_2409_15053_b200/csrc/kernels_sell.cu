@@ -41,6 +41,41 @@ constexpr int kWarpsPerBlock = 4;
 #endif
 constexpr int kBatch = FLZ_K1_BATCH;  // matrix entries per row requested per pipeline stage
 
+// Programmatic dependent launch: consecutive Clenshaw steps depend on each other through Y1/Y2
+// only, so step j+1 may be scheduled while step j drains and read its (immutable) matrix
+// stream; pdl_wait() orders everything after it behind the complete previous grid.  Both are
+// no-ops for a launch without the attribute.
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// FLZ_K1_PDL=0 restores plain stream-ordered launches (experiments)
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("FLZ_K1_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+template <class... KArgs, class... Args>
+void launch_k1(flz_ctx* ctx, void (*kernel)(KArgs...), unsigned grid, unsigned block,
+               Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  const bool pdl = pdl_enabled() && ctx->nranks == 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  FLZ_CUDA(cudaLaunchKernelEx(&cfg, kernel, KArgs(std::forward<Args>(args))...));
+}
+
 template <bool EXACT>
 __device__ __forceinline__ double mul_add(double a, double b, double c) {
   if constexpr (EXACT)
@@ -423,6 +458,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32,
   const int64_t first = (int64_t)blockIdx.x * slices_per_cta;
   const int64_t last = min(A.nslices, first + slices_per_cta);
   const int cmax = (int)A.ncols - 1;
+  pdl_launch_dependents();
   for (int64_t w = first + warp; w < last; w += kWarpsPerBlock) {
     const int64_t slice = A.slice_ids ? (int64_t)A.slice_ids[w] : w;
     const int word = __ldg(reinterpret_cast<const int*>(A.ug + slice) + (lane & 15));
@@ -432,6 +468,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32,
     double acc[R], y1o[R], y2o[R], xo[R];
 #pragma unroll
     for (int k = 0; k < R; ++k) acc[k] = 0.0;
+    if (w == first + warp) pdl_wait();  // matrix words above are requested before the wait
 #ifdef FLZ_K1_LATE_OWN
     prefetch_own<R, S, MODE>(A, row, Y2, ldy, X, ldx);
 #else
@@ -533,6 +570,8 @@ __global__ void __launch_bounds__(kTaskWarps * 32, FLZ_K1_TASK_CTAS)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t t0 = (int64_t)blockIdx.x * tasks_per_cta;
   const int64_t t1 = min(A.ntasks, t0 + tasks_per_cta);
+  pdl_launch_dependents();
+  pdl_wait();
   for (int64_t t = t0; t < t1; ++t) {
     const SliceTask task = A.tasks[t];
     const int W = task.warps_per_slice;
@@ -598,6 +637,7 @@ __global__ void __launch_bounds__(kTaskWarps * 32, FLZ_K1_TASK_CTAS)
                            int64_t ldo) {
   __shared__ double part[kTaskWarps][2 * R][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  pdl_launch_dependents();
   const SliceTask task = A.tasks[blockIdx.x];
   const int W = task.warps_per_slice;
   const int sub = warp / W, piece = warp - sub * W;
@@ -615,6 +655,7 @@ __global__ void __launch_bounds__(kTaskWarps * 32, FLZ_K1_TASK_CTAS)
     const int p0 = piece * chunk, p1 = min(L, p0 + chunk);
     const int32_t* __restrict__ col = A.p2_col + (pos0 + p0) * 32 + lane;
     const double* __restrict__ val = A.p2_val + ((pos0 + p0) * 32 + lane) * 2;
+    pdl_wait();
     for (int p = p0; p < p1; p += kBatch) {
       int c[kBatch];
       double va[kBatch], vb[kBatch], g[kBatch][R];
@@ -742,8 +783,8 @@ void launch_ug(flz_ctx* ctx, const SellView& A, double s1, double s2, double b, 
   if constexpr (MODE != 3) {
     if (A.p2) {
       if (A.ntasks == 0) return;
-      clenshaw_step_p2_tasks<R, S, MODE><<<(unsigned)A.ntasks, kTaskWarps * 32, 0, ctx->stream>>>(
-          A, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo);
+      launch_k1(ctx, clenshaw_step_p2_tasks<R, S, MODE>, (unsigned)A.ntasks, kTaskWarps * 32, A, s1,
+                s2, b, Y1, Y2, ldy, X, ldx, Out, ldo);
       ctx->launches++;
       return;
     }
@@ -756,19 +797,18 @@ void launch_ug(flz_ctx* ctx, const SellView& A, double s1, double s2, double b, 
       const int spc = ctx->k1_slices_per_cta > 0 ? ctx->k1_slices_per_cta : FLZ_K1_SLICES_PER_CTA;
       const unsigned grid = (unsigned)((A.nslices + spc - 1) / spc);
       if ((ctx->k1_batch > 0 ? ctx->k1_batch : FLZ_K1_UB) >= 8)
-        clenshaw_step_ug_warp<R, S, MODE, 8><<<grid, kWarpsPerBlock * 32, 0, ctx->stream>>>(
-            A, spc, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo);
+        launch_k1(ctx, clenshaw_step_ug_warp<R, S, MODE, 8>, grid, kWarpsPerBlock * 32, A, spc, s1,
+                  s2, b, Y1, Y2, ldy, X, ldx, Out, ldo);
       else
-        clenshaw_step_ug_warp<R, S, MODE, 4><<<grid, kWarpsPerBlock * 32, 0, ctx->stream>>>(
-            A, spc, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo);
+        launch_k1(ctx, clenshaw_step_ug_warp<R, S, MODE, 4>, grid, kWarpsPerBlock * 32, A, spc, s1,
+                  s2, b, Y1, Y2, ldy, X, ldx, Out, ldo);
     }
   } else {
     if (A.ntasks == 0) return;
     const int tpc = ctx->k1_tasks_per_cta > 0 ? ctx->k1_tasks_per_cta : FLZ_K1_TASKS_PER_CTA;
     const unsigned grid = (unsigned)((A.ntasks + tpc - 1) / tpc);
-    clenshaw_step_ug_tasks<R, S, MODE>
-        <<<grid, kTaskWarps * 32, 0, ctx->stream>>>(A, tpc, s1, s2, b, Y1, Y2, ldy, X, ldx, Out,
-                                                    ldo);
+    launch_k1(ctx, clenshaw_step_ug_tasks<R, S, MODE>, grid, kTaskWarps * 32, A, tpc, s1, s2, b,
+              Y1, Y2, ldy, X, ldx, Out, ldo);
   }
   ctx->launches++;
 }

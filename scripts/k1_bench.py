@@ -43,6 +43,15 @@ if which == "stencil":
     for r in (3, 1):
         bench("stencil37-48^3 r=%d" % r, st, r)
     sys.exit(0)
+if which == "parsec":   # long ragged rows only (C3 with the Ge99H100 nonzero count, C3 old, C4)
+    bench("parsec-c3 8.44M r=3", M.parsec_like(ball_radius=3.384), 3, check=False)
+    bench("parsec-c3 7.41M r=3", M.parsec_like(), 3, check=False)
+    bench("parsec-c4 r=3", M.parsec_like(radius=40.0, h=0.0903, n_atoms=154, ball_radius=3.86, seed=2), 3, m=20, check=False)
+    sys.exit(0)
+if which == "lap":
+    bench("lap3d-100 r=3", M.laplacian3d(100), 3, check=False)
+    bench("lap3d-100 r=1", M.laplacian3d(100), 1, check=False)
+    sys.exit(0)
 if which == "sweep":
     lap = M.laplacian3d(100)
     pk = M.parsec_like()

@@ -142,6 +142,33 @@ def test_paired_layout_reproduces_product(gen):
     assert p2["positions"] * 32 <= 1.15 * len(va)       # at most the entries plus slice padding
 
 
+def test_paired_layout_odd_row_count_lone_row_longest():
+    """An odd number of rows whose lone last row is the longest: the length sort moves it in
+    front of the pairs, every later pair then straddles two lanes — the product must still be
+    right (regression: slice lengths were taken from the pre-sort pair counts)."""
+    rng = np.random.default_rng(3)
+    n = 257
+    dense = np.zeros((n, n))
+    for i in range(n - 1):
+        if i % 7 == 3:
+            continue
+        cols = rng.choice(n - 1, int(rng.integers(25, 40)), replace=False)
+        dense[i, cols] = rng.uniform(-1, 1, len(cols))
+    dense[n - 1, rng.choice(n, 200, replace=False)] = 1.5
+    dense = dense + dense.T
+    import scipy.sparse as sp
+    csr = M._to_csr(sp.csr_matrix(dense))
+    n, rp, ci, va = csr
+    P = HaloPlan(n, 0, 1, [0, n], rp, ci, va)
+    p2 = P.p2_arrays()
+    assert p2 is not None
+    perm = P.arrays()["perm"]
+    x = rng.standard_normal(n)
+    y = P.p2_product(x[perm])
+    want = (dense @ x)[perm]
+    assert np.abs(y[:n] - want).max() <= 1e-12 * np.abs(want).max()
+
+
 def test_paired_layout_saves_gathers_on_dense_blocks():
     csr = M.parsec_like(radius=14.0, n_atoms=20, ball_radius=3.25)
     n, rp, ci, va = csr
