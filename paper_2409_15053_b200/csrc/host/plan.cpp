@@ -42,12 +42,35 @@ void choose_task_target(const std::vector<int32_t>& slice_len) {
   int64_t total = 0;
   for (int32_t L : slice_len) total += L;
   const double slot_average = (double)total / (148.0 * 24.0);
-  for (int T : {256, 192, 128, 96, 64, 48}) {
+  // ... and the launch must be more than one wave of CTAs (3 resident per SM): with a single
+  // wave every SM keeps the two or three unequal tasks it was dealt; from ~1.5 waves on the
+  // hardware scheduler evens the SMs out (PARSEC-shaped n = 113k: 468 tasks 32.3 us, 805 tasks
+  // 29.1 us per step)
+  auto task_count = [&] {
+    int64_t tasks = 0;
+    size_t i = 0;
+    while (i < slice_len.size()) {
+      const int W = warps_for(slice_len[i]);
+      int count = 0;
+      while (i < slice_len.size() && count < kPlanTaskWarps / W && warps_for(slice_len[i]) == W) {
+        ++i;
+        ++count;
+      }
+      ++tasks;
+    }
+    return tasks;
+  };
+  bool balanced = false;
+  for (int T : {256, 192, 128, 96, 64, 48, 32}) {
     g_task_target = T;
-    int32_t longest = 0;
-    for (int32_t L : slice_len) longest = std::max(longest, (L + warps_for(L) - 1) / warps_for(L));
-    if ((double)longest <= 1.5 * slot_average) return;
+    if (!balanced) {
+      int32_t longest = 0;
+      for (int32_t L : slice_len) longest = std::max(longest, (L + warps_for(L) - 1) / warps_for(L));
+      balanced = (double)longest <= 1.5 * slot_average;
+    }
+    if (balanced && task_count() >= 666) return;
   }
+  if (!balanced) g_task_target = 48;
 }
 
 // Groups slices (in list order) into CTA tasks: long slices get several warps each.
@@ -619,20 +642,59 @@ void build_p2(HostPlan& P, const std::vector<uint8_t>& is_boundary32,
   P.p2_col.assign(std::max<int64_t>(positions * 32, 1), 0);
   P.p2_val.assign(std::max<int64_t>(positions * 64, 2), 0.0);
   // pass 2: fill
+  // Entry order inside a lane: columns that at least 8 lanes of the slice hold come first, most
+  // frequent first (ties ascending), the others follow in ascending order.  In a slice whose
+  // lanes sit in one dense block every lane then asks for the SAME column at the same position
+  // — one L1 line per warp-level gather instead of one per lane.  (Fast mode sums in layout
+  // order; the exact-mode kernel reads the CSR-order arrays.)  Padding entries repeat the
+  // column the lane below them asked for, so they add no line either.
+  constexpr int kSharedLanes = 8;
   run_chunks(nchunks, [&](int t) {
-    std::vector<Entry> lane, tmp;
+    std::vector<Entry> lanes[32], tmp;
+    std::vector<int32_t> all, ucol, ucnt;
     for (int64_t s = ns * t / nchunks; s < ns * (t + 1) / nchunks; ++s) {
       int32_t* c = P.p2_col.data() + P.p2_ptr[s] * 32;
       double* v = P.p2_val.data() + P.p2_ptr[s] * 64;
+      all.clear();
       for (int l = 0; l < 32; ++l) {
-        const int64_t rowA = s * 64 + 2 * l;
-        merge_lane(rowA, lane, tmp);
-        const int32_t self = (int32_t)std::min<int64_t>(rowA, std::max<int64_t>(nl - 1, 0));
-        for (int32_t p = 0; p < len[s]; ++p) {
-          const bool on = p < (int32_t)lane.size();
-          c[(int64_t)p * 32 + l] = on ? lane[p].col : self;
-          v[((int64_t)p * 32 + l) * 2] = on ? lane[p].a : 0.0;
-          v[((int64_t)p * 32 + l) * 2 + 1] = on ? lane[p].b : 0.0;
+        merge_lane(s * 64 + 2 * l, lanes[l], tmp);
+        for (const Entry& e : lanes[l]) all.push_back(e.col);
+      }
+      std::sort(all.begin(), all.end());
+      ucol.clear();
+      ucnt.clear();
+      bool any_shared = false;
+      for (size_t i = 0; i < all.size();) {
+        size_t j = i;
+        while (j < all.size() && all[j] == all[i]) ++j;
+        ucol.push_back(all[i]);
+        ucnt.push_back((int32_t)(j - i));
+        any_shared = any_shared || (j - i) >= (size_t)kSharedLanes;
+        i = j;
+      }
+      if (any_shared) {
+        auto freq = [&](int32_t col) {
+          const int32_t f = ucnt[std::lower_bound(ucol.begin(), ucol.end(), col) - ucol.begin()];
+          return f >= kSharedLanes ? f : 0;
+        };
+        for (int l = 0; l < 32; ++l)
+          std::stable_sort(lanes[l].begin(), lanes[l].end(), [&](const Entry& x, const Entry& y) {
+            return freq(x.col) > freq(y.col);   // stable: ascending column inside a frequency
+          });
+      }
+      for (int32_t p = 0; p < len[s]; ++p) {
+        int32_t fill = (int32_t)std::min<int64_t>(s * 64, std::max<int64_t>(nl - 1, 0));
+        for (int l = 0; l < 32; ++l)
+          if (p < (int32_t)lanes[l].size()) {
+            fill = lanes[l][p].col;
+            break;
+          }
+        for (int l = 0; l < 32; ++l) {
+          const bool on = p < (int32_t)lanes[l].size();
+          if (on) fill = lanes[l][p].col;
+          c[(int64_t)p * 32 + l] = fill;
+          v[((int64_t)p * 32 + l) * 2] = on ? lanes[l][p].a : 0.0;
+          v[((int64_t)p * 32 + l) * 2 + 1] = on ? lanes[l][p].b : 0.0;
         }
       }
     }
@@ -768,6 +830,113 @@ HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<in
     }
   }
   const std::vector<int32_t>* sort_key = pair_key.empty() ? nullptr : &pair_key;
+  // ---- clustered order for dense blocks (PARSEC non-local projectors: a ball of grid points
+  // coupled all-to-all).  Rows much longer than the median are "long"; a long pair's cluster is
+  // the min-hash of its long COLUMNS (columns whose own row is long: the block's members, not
+  // the stencil neighbours), so the rows of one dense block meet in one cluster.  Long pairs are
+  // sorted by (cluster, length class, row), short pairs keep the window sort.  With the lanes
+  // of a slice inside one block, build_p2 lines the block's columns up across the lanes and a
+  // warp-level gather touches ONE line instead of ~20 (scripts/analysis/p2_lines.py).
+  std::vector<int32_t> cluster_perm;
+  // Measured on B200 (PARSEC-shaped n = 113k): lines per gather 18.8 -> 12.8, time per step
+  // unchanged (28.2 vs 28.3 us): the kernel is bound by the BYTES a gather returns through the
+  // LSU data pipe (32 B per lane = 16 wavefronts even when every lane reads the same line),
+  // not by the lines it touches.  The order is therefore opt-in (FLZ_P2_CLUSTER=1): it is the
+  // groundwork for a kernel that stages a block's rows in shared memory once per slice.
+  static const bool want_cluster = [] {
+    const char* e = std::getenv("FLZ_P2_CLUSTER");
+    return e && e[0] == '1';
+  }();
+  if (sort_key && want_cluster && nl >= 4096) {
+    std::vector<int32_t> tmp(len);
+    std::nth_element(tmp.begin(), tmp.begin() + nl / 2, tmp.end());
+    const int32_t long_min = std::max<int32_t>(48, tmp[nl / 2] + tmp[nl / 2] / 2);
+    std::vector<uint8_t> is_long(nl, 0);
+    int64_t long_entries = 0;
+    for (int64_t i = 0; i < nl; ++i)
+      if (len[i] > long_min) {
+        is_long[i] = 1;
+        long_entries += len[i];
+      }
+    if (5 * long_entries >= P.nnz) {
+      const int64_t npairs = (nl + 1) / 2;
+      auto mix = [](int64_t c) { return ((uint64_t)c * 0x9E3779B97F4A7C15ull) >> 20; };
+      std::vector<int64_t> key(npairs, -1);
+      const int kc = (int)std::max<int64_t>(1, std::min<int64_t>(worker_count(), npairs / 1024));
+      run_chunks(kc, [&](int t) {
+        for (int64_t q = npairs * t / kc; q < npairs * (t + 1) / kc; ++q) {
+          const int64_t i0 = 2 * q, i1 = std::min(nl, i0 + 2);
+          bool any_long = false;
+          for (int64_t i = i0; i < i1; ++i) any_long = any_long || is_long[i];
+          if (!any_long) continue;
+          uint64_t best = ~0ull;
+          int64_t arg = -1;
+          for (int64_t i = i0; i < i1; ++i)
+            for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
+              const int64_t c = (int64_t)col_idx[e] - P.row_begin;
+              if (c < 0 || c >= nl || !is_long[c]) continue;
+              const uint64_t hsh = mix(c);
+              if (hsh < best) {
+                best = hsh;
+                arg = c;
+              }
+            }
+          key[q] = arg;
+        }
+      });
+      std::vector<int32_t> long_pairs, short_pairs;
+      const bool odd = nl % 2 != 0;  // the lone last row stays last: pairs keep even positions
+      for (int64_t q = 0; q < npairs - (odd ? 1 : 0); ++q)
+        (key[q] >= 0 ? long_pairs : short_pairs).push_back((int32_t)q);
+      std::vector<int32_t> cls(npairs);
+      for (int64_t q = 0; q < npairs; ++q) cls[q] = length_class(pair_key[2 * q]);
+      std::sort(long_pairs.begin(), long_pairs.end(), [&](int32_t a, int32_t b) {
+        if (key[a] != key[b]) return key[a] < key[b];
+        if (cls[a] != cls[b]) return cls[a] > cls[b];
+        return a < b;
+      });
+      // every second cluster runs shortest-first: a slice that straddles two clusters then
+      // holds the short ends (or the long ends) of both, which pads less
+      for (size_t i = 0, k = 0; i < long_pairs.size(); ++k) {
+        size_t j = i;
+        while (j < long_pairs.size() && key[long_pairs[j]] == key[long_pairs[i]]) ++j;
+        if (k % 2 == 1) std::reverse(long_pairs.begin() + i, long_pairs.begin() + j);
+        i = j;
+      }
+      const int64_t window = 8192;  // pairs (= the 16384-row window of the unclustered sort)
+      for (size_t w0 = 0; w0 < short_pairs.size(); w0 += window)
+        std::stable_sort(short_pairs.begin() + w0,
+                         short_pairs.begin() + std::min(short_pairs.size(), w0 + (size_t)window),
+                         [&](int32_t a, int32_t b) { return cls[a] > cls[b]; });
+      std::vector<int32_t> order(long_pairs);
+      order.insert(order.end(), short_pairs.begin(), short_pairs.end());
+      if (odd) order.push_back((int32_t)(npairs - 1));
+      // padded positions of this order against the window sort: clusters of unrelated long rows
+      // (no block structure) would only add padding
+      auto padded = [&](auto&& pair_at) {
+        int64_t total = 0;
+        for (int64_t s = 0; s < npairs; s += 32) {
+          int32_t mx = 0;
+          for (int64_t l = s; l < std::min(npairs, s + 32); ++l) mx = std::max(mx, pair_ulen[2 * pair_at(l)]);
+          total += mx;
+        }
+        return total;
+      };
+      sort_windows(len, 16384, P.perm, sort_key);
+      const int64_t base = padded([&](int64_t l) { return (int64_t)(P.perm[2 * l] / 2); });
+      const int64_t clustered = padded([&](int64_t l) { return (int64_t)order[l]; });
+      if (std::getenv("FLZ_TRACE"))
+        std::fprintf(stderr, "[flz]   plan clusters: %zu long pairs, positions %lld clustered vs %lld window-sorted\n",
+                     long_pairs.size(), (long long)clustered, (long long)base);
+      if ((double)clustered <= 1.1 * (double)base && long_pairs.size() >= 64) {
+        cluster_perm.reserve(nl);
+        for (int32_t q : order) {
+          cluster_perm.push_back(2 * q);
+          if (2 * (int64_t)q + 1 < nl) cluster_perm.push_back(2 * q + 1);
+        }
+      }
+    }
+  }
 
   // ---- sigma: smallest window whose padding overhead is <= 8 %
   int64_t chosen = sigma;
@@ -793,7 +962,12 @@ HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<in
       }
     }
   }
-  sort_windows(len, chosen, P.perm, sort_key);
+  if (!cluster_perm.empty() && sigma <= 0) {
+    P.perm = cluster_perm;
+    chosen = std::max<int64_t>(nl, 2);
+  } else {
+    sort_windows(len, chosen, P.perm, sort_key);
+  }
   P.sigma = (int)std::min<int64_t>(chosen, 1 << 30);
   bool identity = true;
   for (int64_t i = 0; i < nl && identity; ++i) identity = P.perm[i] == i;

@@ -7,7 +7,7 @@ from paper_2409_15053_b200 import Context, DeviceMatrix, matrices as M, solver a
 name = sys.argv[1] if len(sys.argv) > 1 else "c3"
 r = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 m = int(sys.argv[3]) if len(sys.argv) > 3 else 12
-csr = {"c2": lambda: M.laplacian3d(100), "c3": lambda: M.parsec_like(),
+csr = {"c2": lambda: M.laplacian3d(100), "c3": lambda: M.parsec_like(ball_radius=3.384),
        "c4": lambda: M.parsec_like(radius=40.0, h=0.0903, n_atoms=154, ball_radius=3.86, seed=2)}[name]()
 n, rp, ci, va = csr
 ctx = Context()
