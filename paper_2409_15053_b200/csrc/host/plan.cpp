@@ -568,7 +568,7 @@ int64_t build_ug(HostPlan& P, const std::vector<uint8_t>& is_boundary, bool allo
 
 // ---- paired layout (plan.hpp) ------------------------------------------------------------
 void build_p2(HostPlan& P, const std::vector<uint8_t>& is_boundary32,
-              const std::vector<int32_t>& pair_ulen) {
+              const std::vector<int32_t>& pair_ulen, bool frequency_order) {
   const int64_t nl = P.nl;
   const int64_t ns = P.p2_slices = (nl + 63) / 64;
   P.p2_ptr.assign(ns + 1, 0);
@@ -642,7 +642,8 @@ void build_p2(HostPlan& P, const std::vector<uint8_t>& is_boundary32,
   P.p2_col.assign(std::max<int64_t>(positions * 32, 1), 0);
   P.p2_val.assign(std::max<int64_t>(positions * 64, 2), 0.0);
   // pass 2: fill
-  // Entry order inside a lane: columns that at least 8 lanes of the slice hold come first, most
+  // Entry order inside a lane, clustered row order only (frequency_order; otherwise ascending
+  // columns): columns that at least 8 lanes of the slice hold come first, most
   // frequent first (ties ascending), the others follow in ascending order.  In a slice whose
   // lanes sit in one dense block every lane then asks for the SAME column at the same position
   // — one L1 line per warp-level gather instead of one per lane.  (Fast mode sums in layout
@@ -658,7 +659,8 @@ void build_p2(HostPlan& P, const std::vector<uint8_t>& is_boundary32,
       all.clear();
       for (int l = 0; l < 32; ++l) {
         merge_lane(s * 64 + 2 * l, lanes[l], tmp);
-        for (const Entry& e : lanes[l]) all.push_back(e.col);
+        if (frequency_order)
+          for (const Entry& e : lanes[l]) all.push_back(e.col);
       }
       std::sort(all.begin(), all.end());
       ucol.clear();
@@ -672,7 +674,7 @@ void build_p2(HostPlan& P, const std::vector<uint8_t>& is_boundary32,
         any_shared = any_shared || (j - i) >= (size_t)kSharedLanes;
         i = j;
       }
-      if (any_shared) {
+      if (any_shared && frequency_order) {
         auto freq = [&](int32_t col) {
           const int32_t f = ucnt[std::lower_bound(ucol.begin(), ucol.end(), col) - ucol.begin()];
           return f >= kSharedLanes ? f : 0;
@@ -962,7 +964,8 @@ HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<in
       }
     }
   }
-  if (!cluster_perm.empty() && sigma <= 0) {
+  const bool clustered_order = !cluster_perm.empty() && sigma <= 0;
+  if (clustered_order) {
     P.perm = cluster_perm;
     chosen = std::max<int64_t>(nl, 2);
   } else {
@@ -1111,7 +1114,7 @@ HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<in
     return !(e && e[0] == '0');
   }();
   P.p2 = want_p2 && !P.split && !P.lean && nl > 0 && !pair_ulen.empty();
-  if (P.p2) build_p2(P, is_boundary, pair_ulen);
+  if (P.p2) build_p2(P, is_boundary, pair_ulen, clustered_order);
   timer.lap("paired layout");
   P.uv_pairs.clear();
   if (P.lean) {

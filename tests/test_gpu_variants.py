@@ -15,7 +15,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def run(code, env_extra, args=()):
     env = dict(os.environ)
-    for k in ("FLZ_SPLIT", "FLZ_K1_LAYOUT", "FLZ_SYNC_CHECK"):
+    for k in ("FLZ_SPLIT", "FLZ_K1_LAYOUT", "FLZ_SYNC_CHECK", "FLZ_K1_TMA", "FLZ_K1_PDL",
+              "FLZ_P2_CLUSTER"):
         env.pop(k, None)
     env.update(env_extra)
     p = subprocess.run([sys.executable, "-c", code, *args], env=env, capture_output=True,
@@ -25,7 +26,10 @@ def run(code, env_extra, args=()):
 
 
 @pytest.mark.parametrize("env", [{"FLZ_SPLIT": "1"}, {"FLZ_SPLIT": "0"}, {"FLZ_K1_LAYOUT": "planar"},
-                                 {"FLZ_SPLIT": "1", "FLZ_K1_LAYOUT": "planar"}])
+                                 {"FLZ_SPLIT": "1", "FLZ_K1_LAYOUT": "planar"},
+                                 {"FLZ_K1_TMA": "1"},          # paired layout, TMA-staged matrix stream
+                                 {"FLZ_K1_PDL": "0"},          # plain stream-ordered launches
+                                 {"FLZ_P2_CLUSTER": "1"}])     # dense-block row clustering
 def test_filter_variants_vs_oracle(env, best_oracle):
     """p(A) X through the forced layouts agrees with the reference (oracle) to 1e-13."""
     code = r'''

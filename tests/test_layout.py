@@ -169,6 +169,44 @@ def test_paired_layout_odd_row_count_lone_row_longest():
     assert np.abs(y[:n] - want).max() <= 1e-12 * np.abs(want).max()
 
 
+def test_clustered_pair_order_lines_up_dense_blocks():
+    """FLZ_P2_CLUSTER=1 (read once per process, hence the subprocess): long pairs sorted by the
+    min-hash of their long columns, lanes ordered by column frequency.  The product is unchanged,
+    pairs stay adjacent, and the lanes of a slice ask for far fewer distinct 128-byte lines."""
+    import json, os, subprocess, sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = r'''
+import sys, json
+sys.path.insert(0, %r)
+import numpy as np
+from paper_2409_15053_b200 import matrices as M
+from paper_2409_15053_b200.dist import HaloPlan
+n, rp, ci, va = M.parsec_like(radius=14.0, n_atoms=24, ball_radius=3.4)
+P = HaloPlan(n, 0, 1, [0, n], rp, ci, va)
+p2 = P.p2_arrays(); perm = P.arrays()["perm"]
+x = np.random.default_rng(2).standard_normal(n)
+import scipy.sparse as sp
+want = (sp.csr_matrix((va, ci, rp), shape=(n, n)) @ x)[perm]
+y = P.p2_product(x[perm])[:n]
+col = p2["col"].reshape(-1, 32)
+lines = 1 + (np.diff(np.sort(col // 4, axis=1), axis=1) != 0).sum(1)
+even = perm[0:len(perm) - 1:2]
+print(json.dumps(dict(err=float(np.abs(y - want).max() / np.abs(want).max()), lines=float(lines.mean()),
+                      positions=int(p2["positions"]),
+                      paired=bool(np.all((even %% 2 == 0) & (perm[1::2] == even + 1)[: len(even)])))))
+''' % root
+    out = {}
+    for flag in ("0", "1"):
+        env = dict(os.environ, FLZ_P2_CLUSTER=flag)
+        p = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+        assert p.returncode == 0, p.stderr[-2000:]
+        out[flag] = json.loads(p.stdout.strip().splitlines()[-1])
+    assert out["0"]["err"] <= 1e-12 and out["1"]["err"] <= 1e-12
+    assert out["0"]["paired"] and out["1"]["paired"]
+    assert out["1"]["lines"] <= 0.8 * out["0"]["lines"]
+    assert out["1"]["positions"] <= 1.1 * out["0"]["positions"]
+
+
 def test_paired_layout_saves_gathers_on_dense_blocks():
     csr = M.parsec_like(radius=14.0, n_atoms=20, ball_radius=3.25)
     n, rp, ci, va = csr
