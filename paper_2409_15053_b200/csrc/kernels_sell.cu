@@ -165,25 +165,6 @@ __device__ __forceinline__ void gather_row(const double* __restrict__ Y, int64_t
     return;
   }
   const double* p = Y + row * S;
-#ifdef FLZ_K1_GATHER_SPLIT
-  // 3 useful doubles of a 32-byte row as 16 + 8 bytes: 24 instead of 32 bytes per lane
-  // through the LSU data pipe (12 instead of 16 wavefronts per warp-level gather)
-  if constexpr (S == 4 && R == 3) {
-    double a, b, c;
-    asm volatile(
-        "{\n\t.reg .pred q;\n\tsetp.ne.s32 q, %4, 0;\n\t"
-        "mov.f64 %0, 0d0000000000000000;\n\tmov.f64 %1, 0d0000000000000000;\n\t"
-        "mov.f64 %2, 0d0000000000000000;\n\t"
-        "@q ld.global.nc.v2.f64 {%0,%1}, [%3];\n\t"
-        "@q ld.global.nc.f64 %2, [%3+16];\n\t}"
-        : "=d"(a), "=d"(b), "=d"(c)
-        : "l"(p), "r"((int)on));
-    out[0] = a;
-    out[1] = b;
-    out[2] = c;
-    return;
-  }
-#endif
   if constexpr (S == 4) {
     double a, b, c, d;
     asm volatile(
