@@ -15,10 +15,35 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <limits>
 #include <numeric>
+#include <thread>
 
 namespace flz {
+
+namespace {
+// Rows of an accumulator are independent under column transformations (rotations, reflectors):
+// a recorded sequence applied to disjoint row ranges on several threads gives bit-identical
+// results to the sequential order.  body(r0, r1) handles rows [r0, r1).
+template <class F>
+void parallel_rows(std::size_t rows, std::size_t work_per_row, F&& body) {
+  unsigned threads = 1;
+  if (rows >= 32 && rows * work_per_row >= (std::size_t)1 << 21) {
+    unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    if (const char* e = std::getenv("FLZ_HOST_THREADS")) hw = (unsigned)std::max(1, std::atoi(e));
+    threads = (unsigned)std::min<std::size_t>(hw, rows / 8);
+  }
+  if (threads <= 1) {
+    body((std::size_t)0, rows);
+    return;
+  }
+  std::vector<std::thread> pool;
+  for (unsigned t = 0; t < threads; ++t)
+    pool.emplace_back([&, t] { body(rows * t / threads, rows * (t + 1) / threads); });
+  for (auto& th : pool) th.join();
+}
+}  // namespace
 
 // ------------------------------------------------------------ SymBandMatrix
 SymBandMatrix::SymBandMatrix(std::size_t dim, std::size_t semi_bandwidth)
@@ -134,7 +159,9 @@ void reduce_householder(const SymBandMatrix& M, std::vector<double>& d, std::vec
                         DenseBlock& G) {
   const std::size_t n = M.dim();
   DenseBlock A = M.to_dense();
-  std::vector<double> v(n), p(n), w(n), gv(G.rows());
+  std::vector<double> v(n), p(n), w(n), vstore;
+  std::vector<std::size_t> reflectors;
+  vstore.reserve(n * n / 2 + n);
   for (std::size_t k = 0; k + 2 < n; ++k) {
     const std::size_t len = n - k - 1;
     double sq = 0.0;
@@ -154,7 +181,9 @@ void reduce_householder(const SymBandMatrix& M, std::vector<double>& d, std::vec
     // trailing block: A22 <- H A22 H with H = I - 2 v v^T
     for (std::size_t i = 0; i < len; ++i) {
       double acc = 0.0;
-      for (std::size_t j = 0; j < len; ++j) acc += A(k + 1 + i, k + 1 + j) * v[j];
+      // A22 stays bitwise symmetric under the rank-2 update below, so row i is read as the
+      // (contiguous) column i: same values, same summation order
+      for (std::size_t j = 0; j < len; ++j) acc += A(k + 1 + j, k + 1 + i) * v[j];
       p[i] = acc;
     }
     double vp = 0.0;
@@ -165,18 +194,31 @@ void reduce_householder(const SymBandMatrix& M, std::vector<double>& d, std::vec
         A(k + 1 + i, k + 1 + j) -= 2.0 * (v[i] * w[j] + w[i] * v[j]);
     A(k + 1, k) = A(k, k + 1) = alpha;
     for (std::size_t i = k + 2; i < n; ++i) A(i, k) = A(k, i) = 0.0;
-    // accumulator: G <- G diag(I, H)
+    // accumulator: G <- G diag(I, H), applied after the loop (rows in parallel)
+    reflectors.push_back(k);
+    vstore.insert(vstore.end(), v.begin(), v.begin() + len);
+  }
+  {
     const std::size_t rows = G.rows();
-    std::fill(gv.begin(), gv.end(), 0.0);
-    for (std::size_t j = 0; j < len; ++j) {
-      const double* gc = G.col(k + 1 + j);
-      for (std::size_t i = 0; i < rows; ++i) gv[i] += gc[i] * v[j];
-    }
-    for (std::size_t j = 0; j < len; ++j) {
-      double* gc = G.col(k + 1 + j);
-      const double f = 2.0 * v[j];
-      for (std::size_t i = 0; i < rows; ++i) gc[i] -= gv[i] * f;
-    }
+    parallel_rows(rows, n * n, [&](std::size_t r0, std::size_t r1) {
+      std::vector<double> gv(r1 - r0);
+      std::size_t off = 0;
+      for (std::size_t k : reflectors) {
+        const std::size_t len = n - k - 1;
+        const double* vk = vstore.data() + off;
+        off += len;
+        std::fill(gv.begin(), gv.end(), 0.0);
+        for (std::size_t j = 0; j < len; ++j) {
+          const double* gc = G.col(k + 1 + j);
+          for (std::size_t i = r0; i < r1; ++i) gv[i - r0] += gc[i] * vk[j];
+        }
+        for (std::size_t j = 0; j < len; ++j) {
+          double* gc = G.col(k + 1 + j);
+          const double f = 2.0 * vk[j];
+          for (std::size_t i = r0; i < r1; ++i) gc[i] -= gv[i - r0] * f;
+        }
+      }
+    });
   }
   d.resize(n);
   e.assign(n > 1 ? n - 1 : 0, 0.0);
@@ -229,6 +271,31 @@ void tridiag_eig(std::vector<double>& d, std::vector<double>& e, DenseBlock& G) 
   std::copy(e.begin(), e.begin() + std::min(e.size(), n - 1), off.begin());
   const double eps = std::numeric_limits<double>::epsilon();
 
+  // Tall accumulators (full eigenvector computations): the rotations are recorded and applied
+  // to disjoint row ranges on several threads, in the recorded order — bit-identical to the
+  // inline update.  Short ones (the periodic checks' few rows) are updated inline.
+  struct Rot {
+    std::size_t i;
+    double c, s;
+  };
+  const bool defer = G.rows() >= 64;
+  constexpr std::size_t kFlush = (std::size_t)1 << 17;
+  std::vector<Rot> pending;
+  auto flush = [&] {
+    if (pending.empty()) return;
+    parallel_rows(G.rows(), pending.size() * 4, [&](std::size_t r0, std::size_t r1) {
+      for (const Rot& q : pending) {
+        double* gi = G.col(q.i);
+        double* gi1 = G.col(q.i + 1);
+        for (std::size_t t = r0; t < r1; ++t) {
+          const double hi = gi1[t];
+          gi1[t] = q.s * gi[t] + q.c * hi;
+          gi[t] = q.c * gi[t] - q.s * hi;
+        }
+      }
+    });
+    pending.clear();
+  };
   for (std::size_t l = 0; l < n; ++l) {
     int sweeps = 0;
     while (true) {
@@ -264,15 +331,20 @@ void tridiag_eig(std::vector<double>& d, std::vector<double>& e, DenseBlock& G) 
         d[i + 1] = g + p;
         g = c * r - b;
         // columns (i, i+1) of the accumulator: [gi, gi1] <- [c gi - s gi1, s gi + c gi1]
-        double* gi = G.col(i);
-        double* gi1 = G.col(i + 1);
-        const std::size_t rows = G.rows();
-        for (std::size_t t = 0; t < rows; ++t) {
-          const double hi = gi1[t];
-          gi1[t] = s * gi[t] + c * hi;
-          gi[t] = c * gi[t] - s * hi;
+        if (defer) {
+          pending.push_back(Rot{i, c, s});
+        } else {
+          double* gi = G.col(i);
+          double* gi1 = G.col(i + 1);
+          const std::size_t rows = G.rows();
+          for (std::size_t t = 0; t < rows; ++t) {
+            const double hi = gi1[t];
+            gi1[t] = s * gi[t] + c * hi;
+            gi[t] = c * gi[t] - s * hi;
+          }
         }
       }
+      if (pending.size() >= kFlush) flush();
       if (deflated_early) continue;
       d[l] -= p;
       off[l] = g;
@@ -280,6 +352,7 @@ void tridiag_eig(std::vector<double>& d, std::vector<double>& e, DenseBlock& G) 
     }
   }
 
+  flush();
   std::vector<std::size_t> order(n);
   std::iota(order.begin(), order.end(), 0);
   std::sort(order.begin(), order.end(), [&d](std::size_t a, std::size_t b) { return d[a] < d[b]; });
@@ -329,21 +402,30 @@ DenseBlock band_eigenvectors(const SymBandMatrix& M, const std::vector<double>& 
   const double eps = std::numeric_limits<double>::epsilon();
   const double cluster_tol = 1e-3 * scale;
   const std::size_t kl = b, ku = b, ldab = 2 * kl + ku + 1;  // LAPACK-style band LU storage
+  // clusters are independent of each other (only the vectors inside one are orthogonalised
+  // against their predecessors): they are spread over host threads, each with its own
+  // factorization buffers and a start-vector stream seeded by the cluster's first index, so the
+  // result does not depend on the number of threads
+  std::vector<std::size_t> cluster_start;
+  for (std::size_t t = 0; t < w; ++t)
+    if (t == 0 || std::abs(values[pick[t]] - values[pick[t - 1]]) > cluster_tol)
+      cluster_start.push_back(t);
+  cluster_start.push_back(w);
+  auto run_clusters = [&](std::size_t c0, std::size_t c1) {
   std::vector<double> ab(ldab * n), rhs(n);
   std::vector<std::size_t> piv(n);
-  std::uint64_t lcg = 0x9E3779B97F4A7C15ULL;
+  auto AB = [&](std::size_t i, std::size_t j) -> double& {  // entry (i,j), |i-j| within band
+    return ab[j * ldab + (kl + ku + i - j)];
+  };
+  for (std::size_t cl = c0; cl < c1; ++cl) {
+  const std::size_t cluster_begin = cluster_start[cl];
+  std::uint64_t lcg = 0x9E3779B97F4A7C15ULL * (cluster_begin + 1);
   auto next_unit = [&lcg]() {
     lcg = lcg * 6364136223846793005ULL + 1442695040888963407ULL;
     return (static_cast<double>(lcg >> 11) / 9007199254740992.0) - 0.5;
   };
-  auto AB = [&](std::size_t i, std::size_t j) -> double& {  // entry (i,j), |i-j| within band
-    return ab[j * ldab + (kl + ku + i - j)];
-  };
-
-  std::size_t cluster_begin = 0;
-  for (std::size_t t = 0; t < w; ++t) {
+  for (std::size_t t = cluster_begin; t < cluster_start[cl + 1]; ++t) {
     const double theta = values[pick[t]];
-    if (t > 0 && std::abs(theta - values[pick[t - 1]]) > cluster_tol) cluster_begin = t;
     // perturb the shift slightly inside a cluster so that the factorization differs
     const double shift = theta + (t - cluster_begin) * 10.0 * eps * scale;
     // factor M - shift*I
@@ -412,6 +494,32 @@ DenseBlock band_eigenvectors(const SymBandMatrix& M, const std::vector<double>& 
       if (std::sqrt(res) <= 50.0 * eps * scale && it >= 1) break;
     }
   }
+  }
+  };
+  {
+    const std::size_t nclusters = cluster_start.size() - 1;
+    unsigned threads = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    if (const char* e = std::getenv("FLZ_HOST_THREADS")) threads = (unsigned)std::max(1, std::atoi(e));
+    threads = (unsigned)std::min<std::size_t>(threads, nclusters);
+    if (threads <= 1 || w * n < 4096) {
+      run_clusters(0, nclusters);
+    } else {
+      // contiguous cluster ranges of about equal vector counts
+      std::vector<std::size_t> cut{0};
+      for (unsigned th = 1; th < threads; ++th) {
+        const std::size_t want = w * th / threads;
+        std::size_t c = cut.back();
+        while (c < nclusters && cluster_start[c] < want) ++c;
+        cut.push_back(c);
+      }
+      cut.push_back(nclusters);
+      std::vector<std::thread> pool;
+      for (unsigned th = 0; th < threads; ++th)
+        if (cut[th] < cut[th + 1])
+          pool.emplace_back([&, th] { run_clusters(cut[th], cut[th + 1]); });
+      for (auto& th : pool) th.join();
+    }
+  }
   // verification figures for the caller's fallback decision
   double worst_res = 0.0, worst_ortho = 0.0;
   for (std::size_t t = 0; t < w; ++t) {
@@ -426,12 +534,22 @@ DenseBlock band_eigenvectors(const SymBandMatrix& M, const std::vector<double>& 
     }
     worst_res = std::max(worst_res, std::sqrt(res) / scale);
   }
-  for (std::size_t t = 0; t < w; ++t)
-    for (std::size_t u = 0; u <= t; ++u) {
-      double dot = 0.0;
-      for (std::size_t i = 0; i < n; ++i) dot += W(i, t) * W(i, u);
-      worst_ortho = std::max(worst_ortho, std::abs(dot - (t == u ? 1.0 : 0.0)));
-    }
+  {
+    std::vector<double> worst(64, 0.0);  // per chunk; a max is order independent
+    const std::size_t chunks = worst.size();
+    parallel_rows(chunks, w * w * n / chunks + 1, [&](std::size_t c0, std::size_t c1) {
+      for (std::size_t c = c0; c < c1; ++c)
+        for (std::size_t t = c; t < w; t += chunks)   // interleaved: equal work per chunk
+          for (std::size_t u = 0; u <= t; ++u) {
+            const double* x = W.col(t);
+            const double* y = W.col(u);
+            double dot = 0.0;
+            for (std::size_t i = 0; i < n; ++i) dot += x[i] * y[i];
+            worst[c] = std::max(worst[c], std::abs(dot - (t == u ? 1.0 : 0.0)));
+          }
+    });
+    for (double v : worst) worst_ortho = std::max(worst_ortho, v);
+  }
   if (max_residual) *max_residual = worst_res;
   if (max_ortho) *max_ortho = worst_ortho;
   return W;

@@ -95,6 +95,28 @@ def test_band_inverse_iteration(dim, sb):
     assert np.abs(A @ W - W * vals[pick]).max() < 1e-12
 
 
+@pytest.mark.parametrize("dim,sb", [(260, 259), (400, 3)])
+def test_host_eigensolvers_do_not_depend_on_thread_count(dim, sb, monkeypatch):
+    """Recorded rotations/reflectors applied to disjoint row ranges, and independent clusters
+    of the inverse iteration, on 1 or 8 host threads: bit-identical results (dense 260 x 260 is
+    the recovery's V'AV problem, the band is T_k)."""
+    bands = np.random.default_rng(dim + sb).uniform(-1, 1, (sb + 1, dim))
+    out = {}
+    for threads in ("1", "8"):
+        monkeypatch.setenv("FLZ_HOST_THREADS", threads)
+        vals, W = S.sym_band_eig(bands)
+        pick = list(range(dim - 120, dim))
+        V, res, ortho = S.band_eigenvectors(bands, vals, pick)
+        out[threads] = (vals, W, V, res, ortho)
+    A = band_dense(bands)
+    vals, W, V, res, ortho = out["8"]
+    assert np.abs(vals - np.linalg.eigvalsh(A)).max() < 1e-11
+    assert np.abs(W.T @ W - np.eye(dim)).max() < 1e-12 and np.abs(A @ W - W * vals).max() < 1e-11
+    assert res < 1e-12 and ortho < 1e-11
+    for a, b in zip(out["1"], out["8"]):
+        assert np.array_equal(a, b)
+
+
 def test_band_inverse_iteration_with_multiplicities():
     # block diagonal of identical blocks -> exactly repeated eigenvalues
     dim = 90
