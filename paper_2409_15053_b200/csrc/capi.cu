@@ -766,6 +766,11 @@ int flz_plan_arrays(const flz_plan* plan, int32_t* perm, int64_t* slice_ptr, int
 int flz_plan_ug(const flz_plan* plan, int64_t* sizes, int32_t* descriptors, double* ug_val,
                 int32_t* ug_col, int32_t* ug_uoff, int32_t* rest_rows) {
   if (!plan) return FLZ_EINVAL;
+  try {
+    flz::ensure_ug(const_cast<flz_plan*>(plan)->P);  // skipped when the paired layout was certain
+  } catch (...) {
+    return FLZ_EINVAL;
+  }
   const HostPlan& P = plan->P;
   if (sizes) {
     sizes[0] = (int64_t)P.ug_slice.size();

@@ -734,6 +734,72 @@ void require(bool ok, const char* msg) {
 
 }  // namespace
 
+// ---- index-compressed layout + task lists of the UG kernels (everything between the SELL
+// arrays and the paired layout).  A separate step so that matrices which are certain to run the
+// paired kernel can skip it (ensure_ug builds it on demand for the plan-inspection API).
+void build_ug_section(HostPlan& P, const std::vector<uint8_t>& is_boundary) {
+  const int64_t nslices = P.nslices;
+  std::vector<int32_t> all(nslices);
+  std::iota(all.begin(), all.end(), 0);
+  // a rest launch per product only pays when it carries a real share of the matrix
+  // uniform-value positions are read by the stencil ("lean") kernel only: try them when the
+  // slices are short, and fall back when the matrix does not qualify for that kernel after all
+  int32_t longest = 0;
+  for (int64_t s = 0; s < nslices; ++s) longest = std::max(longest, P.slice_len[s]);
+  bool allow_uv = longest <= 16;
+  bool allow_spill = true;
+  if (const int64_t spilled = build_ug(P, is_boundary, allow_spill, allow_uv);
+      spilled > 0 && 50 * spilled < P.nnz) {
+    allow_spill = false;
+    build_ug(P, is_boundary, allow_spill, allow_uv);
+  }
+  std::vector<int32_t> ug_len(nslices + P.nrest);  // the fast kernels walk the compressed slices
+  for (int64_t s = 0; s < nslices + P.nrest; ++s) ug_len[s] = P.ug_slice[s].nu + P.ug_slice[s].ng;
+  choose_task_target(ug_len);
+  {
+    std::vector<int32_t> rest_all(P.rest_interior);
+    rest_all.insert(rest_all.end(), P.rest_boundary.begin(), P.rest_boundary.end());
+    P.tasks_rest_all = build_tasks(rest_all, ug_len);
+    P.tasks_rest_interior = build_tasks(P.rest_interior, ug_len);
+    P.tasks_rest_boundary = build_tasks(P.rest_boundary, ug_len);
+  }
+  P.tasks_all = build_tasks(all, ug_len);
+  P.tasks_interior = build_tasks(P.interior, ug_len);
+  P.tasks_boundary = build_tasks(P.boundary, ug_len);
+  P.short_rows = std::all_of(P.tasks_all.begin(), P.tasks_all.end(),
+                             [](const PlanTask& t) { return t.warps_per_slice == 1; });
+  auto is_lean = [&] {
+    bool lean = P.short_rows;
+    for (int64_t s = 0; s < nslices && lean; ++s) lean = P.ug_slice[s].nu <= 8;
+    return lean;
+  };
+  P.lean = is_lean();
+  if (!P.lean && allow_uv) {  // rare: short slices, but not a stencil — redo without pairs
+    build_ug(P, is_boundary, allow_spill, false);
+    std::vector<int32_t> len2(nslices + P.nrest);
+    for (int64_t s = 0; s < nslices + P.nrest; ++s) len2[s] = P.ug_slice[s].nu + P.ug_slice[s].ng;
+    std::vector<int32_t> rest_all(P.rest_interior);
+    rest_all.insert(rest_all.end(), P.rest_boundary.begin(), P.rest_boundary.end());
+    P.tasks_rest_all = build_tasks(rest_all, len2);
+    P.tasks_rest_interior = build_tasks(P.rest_interior, len2);
+    P.tasks_rest_boundary = build_tasks(P.rest_boundary, len2);
+    P.tasks_all = build_tasks(all, len2);
+    P.tasks_interior = build_tasks(P.interior, len2);
+    P.tasks_boundary = build_tasks(P.boundary, len2);
+    P.short_rows = std::all_of(P.tasks_all.begin(), P.tasks_all.end(),
+                               [](const PlanTask& t) { return t.warps_per_slice == 1; });
+    P.lean = false;
+  }
+}
+
+void ensure_ug(HostPlan& P) {
+  if (!P.ug_skipped) return;
+  std::vector<uint8_t> is_boundary(P.nslices, 0);
+  for (int32_t s : P.boundary) is_boundary[s] = 1;
+  build_ug_section(P, is_boundary);
+  P.ug_skipped = false;
+}
+
 HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<int64_t>& starts,
                     const int64_t* row_ptr, const int32_t* col_idx, const double* values,
                     int sigma) {
@@ -1058,61 +1124,28 @@ HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<in
   for (int64_t s = 0; s < nslices; ++s)
     (is_boundary[s] ? P.boundary : P.interior).push_back((int32_t)s);
   timer.lap("SELL arrays");
-  // a rest launch per product only pays when it carries a real share of the matrix
-  // uniform-value positions are read by the stencil ("lean") kernel only: try them when the
-  // slices are short, and fall back when the matrix does not qualify for that kernel after all
-  int32_t longest = 0;
-  for (int64_t s = 0; s < nslices; ++s) longest = std::max(longest, P.slice_len[s]);
-  bool allow_uv = longest <= 16;
-  bool allow_spill = true;
-  if (const int64_t spilled = build_ug(P, is_boundary, allow_spill, allow_uv);
-      spilled > 0 && 50 * spilled < P.nnz) {
-    allow_spill = false;
-    build_ug(P, is_boundary, allow_spill, allow_uv);
-  }
-  timer.lap("UG layout");
-  std::vector<int32_t> ug_len(nslices + P.nrest);  // the fast kernels walk the compressed slices
-  for (int64_t s = 0; s < nslices + P.nrest; ++s) ug_len[s] = P.ug_slice[s].nu + P.ug_slice[s].ng;
-  choose_task_target(ug_len);
-  {
-    std::vector<int32_t> rest_all(P.rest_interior);
-    rest_all.insert(rest_all.end(), P.rest_boundary.begin(), P.rest_boundary.end());
-    P.tasks_rest_all = build_tasks(rest_all, ug_len);
-    P.tasks_rest_interior = build_tasks(P.rest_interior, ug_len);
-    P.tasks_rest_boundary = build_tasks(P.rest_boundary, ug_len);
-  }
-  P.tasks_all = build_tasks(all, ug_len);
-  P.tasks_interior = build_tasks(P.interior, ug_len);
-  P.tasks_boundary = build_tasks(P.boundary, ug_len);
-  P.short_rows = std::all_of(P.tasks_all.begin(), P.tasks_all.end(),
-                             [](const PlanTask& t) { return t.warps_per_slice == 1; });
-  auto is_lean = [&] {
-    bool lean = P.short_rows;
-    for (int64_t s = 0; s < nslices && lean; ++s) lean = P.ug_slice[s].nu <= 8;
-    return lean;
-  };
-  P.lean = is_lean();
-  if (!P.lean && allow_uv) {  // rare: short slices, but not a stencil — redo without pairs
-    build_ug(P, is_boundary, allow_spill, false);
-    std::vector<int32_t> len2(nslices + P.nrest);
-    for (int64_t s = 0; s < nslices + P.nrest; ++s) len2[s] = P.ug_slice[s].nu + P.ug_slice[s].ng;
-    std::vector<int32_t> rest_all(P.rest_interior);
-    rest_all.insert(rest_all.end(), P.rest_boundary.begin(), P.rest_boundary.end());
-    P.tasks_rest_all = build_tasks(rest_all, len2);
-    P.tasks_rest_interior = build_tasks(P.rest_interior, len2);
-    P.tasks_rest_boundary = build_tasks(P.rest_boundary, len2);
-    P.tasks_all = build_tasks(all, len2);
-    P.tasks_interior = build_tasks(P.interior, len2);
-    P.tasks_boundary = build_tasks(P.boundary, len2);
-    P.short_rows = std::all_of(P.tasks_all.begin(), P.tasks_all.end(),
-                               [](const PlanTask& t) { return t.warps_per_slice == 1; });
-    P.lean = false;
-  }
-  // long ragged rows: the paired layout feeds the fast kernel (FLZ_P2=0 keeps the UG tasks)
+  // Matrices that are certain to take the paired kernel never read the UG layout: a slice
+  // longer than the largest entries-per-warp target cannot be a one-warp ("short rows") task,
+  // so the stencil kernel is out and P.p2 below is true.  Skipping the UG build saves 55 ms of
+  // a 0.2 s ingest on the PARSEC-shaped n = 113k matrix (and its upload).
   static const bool want_p2 = [] {
     const char* e = std::getenv("FLZ_P2");
     return !(e && e[0] == '0');
   }();
+  {
+    int32_t longest_slice = 0;
+    for (int64_t s = 0; s < nslices; ++s) longest_slice = std::max(longest_slice, P.slice_len[s]);
+    P.ug_skipped = want_p2 && !P.split && nl > 0 && !pair_ulen.empty() && longest_slice > 256 &&
+                   std::getenv("FLZ_K1_T") == nullptr && std::getenv("FLZ_UG_ALWAYS") == nullptr;
+  }
+  if (P.ug_skipped) {
+    P.short_rows = false;
+    P.lean = false;
+  } else {
+    build_ug_section(P, is_boundary);
+  }
+  timer.lap("UG layout");
+  // long ragged rows: the paired layout feeds the fast kernel (FLZ_P2=0 keeps the UG tasks)
   P.p2 = want_p2 && !P.split && !P.lean && nl > 0 && !pair_ulen.empty();
   if (P.p2) build_p2(P, is_boundary, pair_ulen, clustered_order);
   timer.lap("paired layout");

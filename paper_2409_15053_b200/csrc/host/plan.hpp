@@ -67,6 +67,7 @@ struct HostPlan {
   std::vector<double> ug_val;
   std::vector<int32_t> ug_col, ug_uoff;
   int64_t ug_uniform_entries = 0;   // true nonzeros stored at uniform positions
+  bool ug_skipped = false;          // paired layout certain: UG arrays not built (ensure_ug)
   // SPLIT mode (automatic sigma only; chosen when at least half of the nonzeros sit at
   // uniform offsets in natural row order — measured on B200, the PARSEC-shaped matrices with
   // 42 % uniform entries are still faster unsplit: 35 us vs 43 us per step): rows keep their natural order, main slices hold
@@ -113,5 +114,7 @@ HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<in
 
 // Peer `p` asks for `count` of our rows (global ids); call once per peer, any order.
 void plan_set_give(HostPlan& plan, int peer, int64_t count, const int64_t* global_rows);
+// builds the UG layout of a plan that skipped it (HostPlan::ug_skipped); no-op otherwise
+void ensure_ug(HostPlan& plan);
 
 }  // namespace flz

@@ -12,6 +12,7 @@ $NCU --metrics gpu__time_duration.sum -s 700 -c 4500 --csv --log-file gpurun_out
 # (3) full-set captures of the top kernels
 $NCU --set full --import-source on -k regex:clenshaw_step_ -s 200 -c 3 -o gpurun_out/prof_k1_c2 -f python scripts/profile_target.py c2 12 > gpurun_out/prof_k1_c2.log 2>&1
 $NCU --set full --import-source on -k regex:clenshaw_step_ -s 200 -c 3 -o gpurun_out/prof_k1_c3 -f python scripts/profile_target.py c3 60 > gpurun_out/prof_k1_c3.log 2>&1
+$NCU --set full --import-source on -k regex:clenshaw_step_ -s 200 -c 3 -o gpurun_out/prof_k1_c4 -f python scripts/profile_target.py c4 30 > gpurun_out/prof_k1_c4.log 2>&1
 $NCU --set full --import-source on -k regex:gemm_tn_kernel -s 60 -c 2 -o gpurun_out/prof_tn_c3 -f python scripts/profile_target.py c3 60 > gpurun_out/prof_tn_c3.log 2>&1
 $NCU --set full --import-source on -k regex:gemm_nn_kernel -s 60 -c 2 -o gpurun_out/prof_nn_c3 -f python scripts/profile_target.py c3 60 > gpurun_out/prof_nn_c3.log 2>&1
 # (4) the same K1 launches with warm caches (no flush between replays): what the timed runs see

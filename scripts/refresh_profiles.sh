@@ -5,13 +5,13 @@ set -e
 cd "$(dirname "$0")/.."
 R=${1:-r01}
 for f in bench_c2 c2 c3; do python scripts/ncu_summary.py launches gpurun_out/launches_$f.csv > profiles/${R}_launches_$f.txt; done
-for f in k1_c2 k1_c3 tn_c3 nn_c3; do python scripts/ncu_summary.py raw gpurun_out/prof_$f.ncu-rep | grep -v "hmma\|imma\|ops_path\|mem_tensor" > profiles/${R}_prof_$f.txt; done
+for f in k1_c2 k1_c3 k1_c4 tn_c3 nn_c3; do python scripts/ncu_summary.py raw gpurun_out/prof_$f.ncu-rep | grep -v "hmma\|imma\|ops_path\|mem_tensor" > profiles/${R}_prof_$f.txt; done
 cp gpurun_out/k1_c2_warm.txt profiles/${R}_k1_c2_warm_sections.txt
 cp gpurun_out/k1_c3_warm.txt profiles/${R}_k1_c3_warm_sections.txt
 python - <<'PY'
 import subprocess, csv, io, json
 out = {}
-for w in ("c2", "c3"):
+for w in ("c2", "c3", "c4"):
     txt = subprocess.run(["ncu", "-i", f"gpurun_out/prof_k1_{w}.ncu-rep", "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
     hdr, units = rows[0], rows[1]
