@@ -335,6 +335,10 @@ def run_flz(args, wl):
     lay = H.layout() if world == 1 else None
     stride = 4 if (r == 3 and nnz >= 16 * n) else r   # planar or interleaved: R doubles per row
     moved = lay["matrix_bytes"] + 8 * n * (3 * stride + r) if lay else None
+    # stencils on one GPU: TMA-staged tile kernel; long ragged rows: paired-layout task kernel;
+    # row-partitioned stencils: one warp per slice
+    k1_name = ("clenshaw_step_p2_tasks" if nnz >= 16 * n else
+               ("clenshaw_step_stencil_tma" if world == 1 else "clenshaw_step_ug_warp"))
     traffic = None
     prof = os.path.join(ROOT, "profiles", "k1_traffic.json")
     if os.path.exists(prof):
@@ -371,7 +375,7 @@ def run_flz(args, wl):
                         "preproc": st["time_preproc_s"]},
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": int(launches),
-        "roofline": {"kernel": "clenshaw_step_ug_warp / clenshaw_step_ug_tasks (fused Clenshaw-step SpMM, K1)", "bound": "hbm",
+        "roofline": {"kernel": k1_name + " (fused Clenshaw-step SpMM, K1)", "bound": "hbm",
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "peak_source": peak_src, "bytes_per_launch": bstep,
                      "launches_timed": int(filter_steps),

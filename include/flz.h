@@ -94,8 +94,9 @@ int64_t flz_matrix_nnz_local(const flz_matrix* A);
 /* storage statistics: stored (padded) entries, slices, halo rows received per SpMV */
 int flz_matrix_stats(const flz_matrix* A, int64_t* stored_entries, int64_t* slices,
                      int64_t* halo_rows, int64_t* boundary_slices);
-/* index-compressed layout the fast kernels stream: matrix bytes read per product and the
- * number of true nonzeros held at uniform-offset positions (8 instead of 12 bytes each) */
+/* index-compressed layout the fast kernels stream: matrix bytes read per product (paired
+ * layout for long ragged rows; the (value, mask) pairs alone for stencils with a tile plan)
+ * and the number of true nonzeros held at uniform-offset positions */
 int flz_matrix_layout(const flz_matrix* A, int64_t* matrix_bytes, int64_t* uniform_entries);
 /* launch-shape knobs of the fused Clenshaw-step kernels (0 = built-in default): slices per
  * CTA of the one-warp-per-slice kernel, tasks per CTA of the multi-warp kernel, positions
@@ -136,6 +137,14 @@ int flz_plan_ug(const flz_plan* plan, int64_t* sizes, int32_t* descriptors, doub
  * of every slice; col[positions * 32]; val[positions * 64] (two values per lane and position).
  * Any pointer may be NULL. */
 int flz_plan_p2(const flz_plan* plan, int64_t* sizes, int64_t* ptr, int32_t* col, double* val);
+/* tile plan of the TMA-staged stencil kernel (constant-coefficient stencils on one rank;
+ * host/plan.hpp), for host-side checks: info[30] = {tile_rows, segments, seg_base[8],
+ * seg_len[8], seg_start[8], staged elements per column, staged element of offset 0,
+ * doubles in pairs, 0}; info[1] == 0: the matrix has no tile plan.  pairs: 16 doubles per
+ * slice, padded to whole tiles — (value, mask word) per position, mask word = lane mask |
+ * 8 * staged element << 32 | (position 0 only) position count << 52 | (position 0 only,
+ * slice also has per-lane positions) 1 << 56.  pairs may be NULL. */
+int flz_plan_tiles(const flz_plan* plan, int64_t* info, double* pairs);
 
 /* Global matvec counter: speig::matvec_count()/reset (sparse.hpp:74-79).  One count per
  * vector-column product, so a fused r-column block product adds r. */

@@ -94,6 +94,7 @@ _SIGS = {
     "flz_plan_arrays": (i32, [vp] + [vp] * 12),
     "flz_plan_ug": (i32, [vp, vp, vp, vp, vp, vp, vp]),
     "flz_plan_p2": (i32, [vp, vp, vp, vp, vp]),
+    "flz_plan_tiles": (i32, [vp, vp, vp]),
     "flz_matvec_count": (u64, []),
     "flz_reset_matvec_count": (None, []),
     "flz_matvec_sub": (None, [u64]),

@@ -111,7 +111,9 @@ SellView make_view(const flz_matrix* A, const SliceTask* tasks, int64_t ntasks,
                   A->row_len.p, A->col.p,   A->val.p,      slice_ids,      nslices,
                   A->nl,        A->ug.p,    A->ug_val.p,   A->ug_col.p,    A->ug_uoff.p,
                   A->nl + A->nhalo, A->rest_rows.p, A->nslices,   A->w.p,
-                  A->uv_pairs.p,    false,          A->p2_ptr.p,  A->p2_col.p, A->p2_val.p};
+                  A->uv_pairs.p,    false,          A->p2_ptr.p,  A->p2_col.p, A->p2_val.p,
+                  // the tile kernel covers whole-matrix launches only
+                  (slice_ids == nullptr && nslices == A->nslices) ? A->tiles : StencilTiles{}};
 }
 // fast mode on a matrix with the paired layout: the launch walks the paired task lists
 SellView paired(const flz_matrix* A, SellView v, int which) {
@@ -541,6 +543,8 @@ static void upload_plan(flz_ctx* ctx, HostPlan& P, flz_matrix* A) {
   up(A->ug_col, P.ug_col);
   up(A->ug_uoff, P.ug_uoff);
   up(A->uv_pairs, P.uv_pairs);
+  static_assert(sizeof(PlanStencilTiles) == sizeof(StencilTiles), "PlanStencilTiles mirrors StencilTiles");
+  std::memcpy(static_cast<void*>(&A->tiles), &P.tiles, sizeof(StencilTiles));
   A->p2 = P.p2;
   if (P.p2) {
     up(A->p2_ptr, P.p2_ptr);
@@ -807,6 +811,25 @@ int flz_plan_p2(const flz_plan* plan, int64_t* sizes, int64_t* ptr, int32_t* col
   return FLZ_OK;
 }
 
+int flz_plan_tiles(const flz_plan* plan, int64_t* info, double* pairs) {
+  if (!plan || !info) return FLZ_EINVAL;
+  const HostPlan& P = plan->P;
+  const PlanStencilTiles& G = P.tiles;
+  std::fill(info, info + 30, (int64_t)0);
+  info[0] = G.tile_rows;
+  info[1] = G.nseg;
+  for (int j = 0; j < kPlanMaxSegs; ++j) {
+    info[2 + j] = G.seg_base[j];
+    info[10 + j] = G.seg_len[j];
+    info[18 + j] = G.seg_start[j];
+  }
+  info[26] = G.y1_elems;
+  info[27] = G.own_e;
+  info[28] = G.nseg ? (int64_t)P.uv_pairs.size() : 0;
+  if (G.nseg && pairs) std::copy(P.uv_pairs.begin(), P.uv_pairs.end(), pairs);
+  return FLZ_OK;
+}
+
 static void matrix_release(flz_matrix* A) {
   if (!A || --A->refs > 0) return;
   flz_ctx* ctx = A->ctx;
@@ -829,7 +852,10 @@ int flz_matrix_stats(const flz_matrix* A, int64_t* stored_entries, int64_t* slic
 
 int flz_matrix_layout(const flz_matrix* A, int64_t* matrix_bytes, int64_t* uniform_entries) {
   if (!A) return FLZ_EINVAL;
-  if (matrix_bytes) *matrix_bytes = A->p2 ? A->p2_bytes : A->ug_bytes;
+  // stencils with a tile plan: the TMA-staged kernel streams the (value, mask) pairs only
+  if (matrix_bytes)
+    *matrix_bytes = A->p2 ? A->p2_bytes
+                          : (A->tiles.nseg > 0 ? (int64_t)A->uv_pairs.count * 8 : A->ug_bytes);
   if (uniform_entries) *uniform_entries = A->ug_uniform_entries;
   return FLZ_OK;
 }

@@ -98,6 +98,13 @@ struct SliceTask {
 // Per-slice header of the index-compressed ("UG") layout of the fast kernels; mirrors
 // PlanUgSlice (host/plan.hpp).  Positions [0, nu) are uniform (column = row + uoff[p]),
 // positions [nu, nu + ng) are general (one column per lane).
+// Tile plan of the TMA-staged stencil kernel (mirrors PlanStencilTiles, host/plan.hpp)
+struct StencilTiles {
+  int32_t tile_rows = 0, nseg = 0;
+  int32_t seg_base[8] = {}, seg_len[8] = {}, seg_start[8] = {};
+  int32_t y1_elems = 0, own_e = 0;
+};
+
 struct UgSlice {
   int64_t val_ptr;
   int64_t col_ptr;
@@ -161,6 +168,7 @@ struct flz_matrix {
   flz::DevBuf<double> ug_val;
   flz::DevBuf<int32_t> ug_col, ug_uoff;
   flz::DevBuf<double> uv_pairs;     // lean matrices: 16 doubles per slice (host/plan.hpp)
+  flz::StencilTiles tiles;          // nseg > 0: the TMA-staged stencil kernel applies
   // paired layout (host/plan.hpp)
   bool p2 = false;
   flz::DevBuf<int64_t> p2_ptr;
@@ -264,6 +272,7 @@ struct SellView {
   const int64_t* p2_ptr;
   const int32_t* p2_col;
   const double* p2_val;
+  StencilTiles tiles;        // nseg > 0: tile plan of the TMA-staged stencil kernel
 };
 
 enum class StepMode { step, final, plain, rest };

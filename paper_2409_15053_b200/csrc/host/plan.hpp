@@ -42,6 +42,25 @@ struct PlanUgSlice {
   int32_t inline_off[8];  // the first offsets again: one 64-byte load serves short slices
 };
 
+// TILE plan of a constant-coefficient stencil on one rank (every position of every slice is
+// a uniform offset with a uniform value): the TMA-staged stencil kernel walks tiles of
+// `tile_rows` consecutive rows and bulk-copies, per tile, the contiguous runs of the gather
+// source its offsets reach.  Offsets closer than a tile are merged into one SEGMENT
+// [base, base + tile_rows + extra) (base even: 16-byte aligned bulk copies); seg_start is the
+// segment's first element inside the staged Y1 column (y1_elems per column).  Position p of a
+// slice with offset d reads staged element seg_start[j] + (d - seg_base[j]) + (row - tile row 0);
+// that number times 8 (a byte offset) sits in bits 32-51 of the position's mask word in
+// uv_pairs, the slice's position count in bits 52-55 of position 0, and bit 56 of position 0
+// flags a slice that also has
+// per-lane positions (the kernel adds them from global memory).  nseg == 0: not applicable.
+constexpr int kPlanMaxSegs = 8;
+struct PlanStencilTiles {
+  int32_t tile_rows = 0, nseg = 0;
+  int32_t seg_base[kPlanMaxSegs] = {}, seg_len[kPlanMaxSegs] = {}, seg_start[kPlanMaxSegs] = {};
+  int32_t y1_elems = 0;  // staged elements per block column (sum of the segment lengths)
+  int32_t own_e = 0;     // staged element of offset 0 (the tile's own rows)
+};
+
 struct HostPlan {
   // partition
   int rank = 0, nranks = 1;
@@ -62,6 +81,7 @@ struct HostPlan {
   // doubles per slice, so that the stencil kernel can fetch them without waiting for the
   // slice descriptor (one dependent memory round trip less per slice)
   std::vector<double> uv_pairs;
+  PlanStencilTiles tiles;   // stencil tile plan (nseg == 0: none); uv_pairs is padded to whole tiles
   // index-compressed copy of the same slices (same rows, same permutation)
   std::vector<PlanUgSlice> ug_slice;
   std::vector<double> ug_val;

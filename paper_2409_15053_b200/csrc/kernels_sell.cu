@@ -26,6 +26,8 @@
 //    accumulated left to right in CSR order with separately rounded multiply and add (the
 //    reference's scalar TU is built without FMA), the combine is ((s1*w + s2*y1) - y2) + b*x.
 
+#include <algorithm>
+#include <cstdint>
 #include <cstdlib>
 #include <type_traits>
 
@@ -869,6 +871,222 @@ __global__ void __launch_bounds__(kTaskWarps * 32, FLZ_K1_TASK_CTAS)
   }
 }
 
+
+// ------------------------------------------------------------ TMA-staged stencil kernel
+// Constant-coefficient stencils on one GPU, planar blocks (host/plan.hpp, PlanStencilTiles).
+// A persistent CTA of T = tile_rows threads walks tiles of T consecutive rows.  Everything a
+// tile touches is CONTIGUOUS in global memory — per block column the runs of Y1 its offsets
+// reach (offsets closer than a tile share one run), its own rows of Y2 and X, and its slices'
+// (value, mask) pairs — so warp 0 requests the whole tile with a handful of cp.async.bulk
+// copies into a ring of shared-memory stages (mbarrier complete_tx), `nstages` tiles ahead.
+// The consumers then need no global load at all: a position costs one broadcast 16-byte
+// shared load (value, lane mask, staged element) and R conflict-free 8-byte shared loads, no
+// shuffles, no address clamps; only the results are written to global memory.  Memory-level
+// parallelism comes from the ring (stages x CTAs per SM x ~20 KB in flight), not from
+// occupancy and registers as in clenshaw_step_ug_warp.
+// Runs of a tile that leave [0, y_rows) are clipped; warp 0 zero-fills the clipped part (the
+// lanes that would read it carry a zero mask bit, but 0 * stale bits must stay finite).
+// The positions of a stencil slice that are not uniform-value pairs (rows next to a domain
+// boundary: per-lane values at uniform offsets, then general positions), gathered from global
+// memory in the order clenshaw_step_ug_warp adds them.  Rare: a few slices per matrix.
+template <int R>
+struct SliceAcc {
+  double v[R];
+};
+template <int R>
+__device__ __noinline__ SliceAcc<R> stencil_slice_rest(const SellView& A, int64_t slice, int lane,
+                                                       int64_t row, const double* __restrict__ Y1,
+                                                       int64_t ldy, SliceAcc<R> acc) {
+  const UgSlice H = load_ug_header(A.ug + slice);
+  const int* __restrict__ desc = reinterpret_cast<const int*>(A.ug + slice);
+  const int nuv = (H.reserved >> 16) & 0xff;
+  const int cmax = (int)A.ncols - 1;
+  const double* __restrict__ val =
+      A.ug_val + H.val_ptr + ug_header_doubles(nuv, H.nu + H.ng - nuv) + lane;
+  for (int p = nuv; p < H.nu; ++p) {
+    const double v = ld_stream_f64(val + (int64_t)(p - nuv) * kSliceRows);
+    const int c = min(max((int)row + __ldg(desc + 8 + p), 0), cmax);
+#pragma unroll
+    for (int k = 0; k < R; ++k) acc.v[k] = fma(v, __ldg(Y1 + (int64_t)k * ldy + c), acc.v[k]);
+  }
+  const int32_t* __restrict__ col = A.ug_col + H.col_ptr + lane;
+  for (int q = 0; q < H.ng; ++q) {
+    const double v = ld_stream_f64(val + (int64_t)(H.nu - nuv + q) * kSliceRows);
+    const int c = ld_stream_s32(col + (int64_t)q * kSliceRows);
+#pragma unroll
+    for (int k = 0; k < R; ++k) acc.v[k] = fma(v, __ldg(Y1 + (int64_t)k * ldy + c), acc.v[k]);
+  }
+  return acc;
+}
+
+template <int R, int MODE>
+__global__ void __launch_bounds__(768)
+    clenshaw_step_stencil_tma(const __grid_constant__ SellView A,
+                              const __grid_constant__ StencilTiles G,
+                              const double* __restrict__ pairs, int64_t nl,
+                              int64_t ntiles, int nstages, int nprod, int64_t y_rows,
+                              int64_t x_rows,
+                              double s1, double s2, double b, const double* __restrict__ Y1,
+                              double* __restrict__ Y2, int64_t ldy, const double* __restrict__ X,
+                              int64_t ldx, double* __restrict__ Out, int64_t ldo) {
+  extern __shared__ __align__(128) unsigned char st_smem[];
+  constexpr bool kOwn = MODE != 2;
+  // consumer threads = rows of a tile; the last nprod warps produce (a warp issues its bulk
+  // copies one after the other, ~150 cycles each on B200: one producer warp cannot keep up)
+  const int T = (int)blockDim.x - 32 * nprod;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int spt = T >> 5;
+  const int pair_d = spt * 16;
+  const int y1e = G.y1_elems;
+  const int y1_d = R * y1e;
+  const int stage_d = pair_d + y1_d + (kOwn ? 2 * R * T : 0);  // doubles per stage
+  double* const ring = reinterpret_cast<double*>(st_smem);
+  const uint32_t ring_s = smem_addr(ring);
+  const uint32_t full_bars = ring_s + (uint32_t)nstages * stage_d * 8;  // tile has landed
+  const uint32_t empty_bars = full_bars + (uint32_t)nstages * 8;        // all warps consumed it
+  pdl_launch_dependents();
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < nstages; ++st) {
+      mbar_init(full_bars + st * 8, nprod);
+      mbar_init(empty_bars + st * 8, spt);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
+  pdl_wait();  // Y1/Y2 belong to the previous step until here
+
+  if (warp >= spt) {
+    // ---------------------------------------------------------------- producer warps
+    // Lane l of producer warp pw owns copy c = l*nprod + pw of EVERY tile (the launcher makes
+    // 32*nprod >= copies per tile): what does not depend on the tile is set up once.
+    const int pw = warp - spt;
+    const int c = lane * nprod + pw;
+    const int ncopy = 1 + G.nseg * R + (kOwn ? 2 * R : 0);
+    int dst = 0, full = 0, off = 0;   // staged element, run length, first row relative to the tile
+    int64_t lim = 0;                  // readable rows of the source column
+    const double* base = nullptr;
+    if (c == 0) {
+      full = pair_d;
+    } else if (c < 1 + G.nseg * R) {
+      const int q = c - 1, j = q / R, k = q - j * R;
+      dst = pair_d + k * y1e + G.seg_start[j];
+      full = G.seg_len[j];
+      off = G.seg_base[j];
+      lim = y_rows;
+      base = Y1 + (int64_t)k * ldy;
+    } else if (c < ncopy) {
+      const int q = c - 1 - G.nseg * R, which = q / R, k = q - which * R;
+      dst = pair_d + y1_d + q * T;
+      full = T;
+      lim = which ? x_rows : y_rows;
+      base = which ? X + (int64_t)k * ldx : Y2 + (int64_t)k * ldy;
+    }
+    int st = 0;
+    uint32_t parity = 1;  // first pass over the ring: the stages are empty (wait falls through)
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      mbar_wait(empty_bars + st * 8, parity);
+      double* sb = ring + (int64_t)st * stage_d;
+      const uint32_t bar = full_bars + st * 8;
+      int lead = 0, count = full;
+      const double* src = pairs + t * pair_d;
+      if (base) {
+        const int64_t g0 = t * T + off;
+        const int64_t a0 = max(g0, (int64_t)0), a1 = min(g0 + full, lim);
+        lead = (int)min(a0 - g0, (int64_t)full);
+        count = (int)max(a1 - a0, (int64_t)0);
+        src = base + a0;
+      }
+      // clipped runs (first and last tiles): all lanes zero the part no copy fills
+      unsigned clipped = __ballot_sync(0xffffffffu, count < full);
+      while (clipped) {
+        const int l = __ffs(clipped) - 1;
+        clipped &= clipped - 1;
+        const int zd = __shfl_sync(0xffffffffu, dst, l), zf = __shfl_sync(0xffffffffu, full, l);
+        const int zl = __shfl_sync(0xffffffffu, lead, l), zc = __shfl_sync(0xffffffffu, count, l);
+        for (int i = lane; i < zl; i += 32) sb[zd + i] = 0.0;
+        for (int i = zl + zc + lane; i < zf; i += 32) sb[zd + i] = 0.0;
+      }
+      const uint32_t bytes = (uint32_t)count * 8u;
+      const uint32_t total = __reduce_add_sync(0xffffffffu, bytes);
+      // release: the zero fills above are visible to whoever sees the phase flip
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                     "r"(total) : "memory");
+      __syncwarp();
+      if (count > 0)
+        bulk_g2s(ring_s + (uint32_t)(st * stage_d + dst + lead) * 8u, src, bytes, bar);
+      if (++st == nstages) { st = 0; parity ^= 1u; }
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------------ consumer warps
+  int st = 0;
+  uint32_t parity = 0;
+  const uint32_t y1e8 = (uint32_t)y1e * 8u;
+  const uint32_t lanebit = 1u << lane;
+  const uint32_t own8 = (uint32_t)G.own_e * 8u;
+  int64_t row = ((int64_t)blockIdx.x * spt + warp) * 32 + lane;
+  const int64_t row_step = (int64_t)gridDim.x * T;
+  double* dst = (MODE == 0 ? Y2 : Out) + row;
+  const int64_t ldd = MODE == 0 ? ldy : ldo;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, row += row_step, dst += row_step) {
+    mbar_wait(full_bars + st * 8, parity);
+    const double* sb = ring + (int64_t)st * stage_d;
+    const double2* sP = reinterpret_cast<const double2*>(sb + warp * 16);
+    const unsigned char* sY1 = reinterpret_cast<const unsigned char*>(sb + pair_d + threadIdx.x);
+    double acc[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) acc[k] = 0.0;
+    double2 pr[8];
+#pragma unroll
+    for (int p = 0; p < 8; ++p) pr[p] = sP[p];  // unused positions: value 0, mask 0, element 0
+    const uint32_t word0 = (uint32_t)__double2hiint(pr[0].y);
+    const int nuv = (word0 >> 20) & 0xf;
+    auto position = [&](int p) {
+      const uint32_t e8 = (uint32_t)__double2hiint(pr[p].y) & 0xfffffu;  // staged BYTE offset
+      const double v = ((uint32_t)__double2loint(pr[p].y) & lanebit) ? pr[p].x : 0.0;
+#pragma unroll
+      for (int k = 0; k < R; ++k)
+        acc[k] = fma(v, *reinterpret_cast<const double*>(sY1 + k * y1e8 + e8), acc[k]);
+    };
+    position(0); position(1); position(2); position(3);
+    if (nuv > 4) { position(4); position(5); }
+    if (nuv > 6) { position(6); position(7); }
+    if ((word0 >> 24) & 1) {  // rare: the slice also has per-lane positions
+      SliceAcc<R> tmp;
+#pragma unroll
+      for (int k = 0; k < R; ++k) tmp.v[k] = acc[k];
+      tmp = stencil_slice_rest<R>(A, t * spt + warp, lane, row, Y1, ldy, tmp);
+#pragma unroll
+      for (int k = 0; k < R; ++k) acc[k] = tmp.v[k];
+    }
+    double o[R];
+    if constexpr (MODE == 2) {
+#pragma unroll
+      for (int k = 0; k < R; ++k) o[k] = acc[k];
+    } else {
+      const double* sY2 = sb + pair_d + y1_d + threadIdx.x;
+      const double* sX = sY2 + R * T;
+#pragma unroll
+      for (int k = 0; k < R; ++k)
+        o[k] = combine<false>(s1, acc[k], s2,
+                              *reinterpret_cast<const double*>(sY1 + k * y1e8 + own8), sY2[k * T],
+                              b, sX[k * T]);
+    }
+    __syncwarp();
+    if (lane == 0)  // this warp is done with the stage
+      asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(empty_bars + st * 8)
+                   : "memory");
+    if (row < nl) {
+#pragma unroll
+      for (int k = 0; k < R; ++k) dst[(int64_t)k * ldd] = o[k];
+    }
+    if (++st == nstages) { st = 0; parity ^= 1u; }
+  }
+}
+
 // Y1[i*S+k] = scale * X[k*ldx+i], k < R; pad entries (R <= k < S) are zeroed
 template <int R, int S>
 __global__ void interleave_kernel(int64_t nl, double scale, const double* __restrict__ X,
@@ -931,6 +1149,58 @@ void launch_simple(flz_ctx* ctx, const SellView& A, double s1, double s2, double
 #define FLZ_K1_TASKS_PER_CTA 1
 #endif
 
+
+// FLZ_ST_STAGES / FLZ_ST_CTAS: ring depth and CTAs per SM of the TMA-staged stencil kernel
+inline int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e && *e ? std::atoi(e) : dflt;
+}
+
+// Launches the TMA-staged stencil kernel when the matrix has a tile plan and the operands
+// allow 16-byte bulk copies; false: the caller falls back to the one-warp-per-slice kernel.
+template <int R, int MODE>
+bool launch_stencil_tma(flz_ctx* ctx, const SellView& A, double s1, double s2, double b,
+                        const double* Y1, double* Y2, int64_t ldy, const double* X, int64_t ldx,
+                        double* Out, int64_t ldo) {
+  const StencilTiles& G = A.tiles;
+  if (G.nseg == 0 || A.nslices == 0) return false;
+  auto aligned = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if (!aligned(Y1) || (ldy & 1) || ldy < A.nl) return false;
+  if (MODE != 2 && (!aligned(Y2) || !aligned(X) || (ldx & 1) || ldx < A.nl)) return false;
+  const int T = G.tile_rows;
+  const int64_t y_rows = ldy, x_rows = ldx;   // readable rows of a block column
+  const size_t stage_bytes =
+      8 * ((size_t)(T / 32) * 16 + (size_t)R * G.y1_elems + (MODE != 2 ? 2 * (size_t)R * T : 0));
+  static const int want_stages = std::clamp(env_int("FLZ_ST_STAGES", 3), 1, 8);
+  static const int want_ctas = std::clamp(env_int("FLZ_ST_CTAS", 2), 1, 8);
+  static const int want_prod = std::clamp(env_int("FLZ_ST_PRODUCERS", 4), 1, 8);
+  const int ncopy = 1 + G.nseg * R + (MODE != 2 ? 2 * R : 0);
+  const int nprod = std::max(want_prod, (ncopy + 31) / 32);
+  static const int sms = [] {
+    int dev = 0, n = 0;
+    FLZ_CUDA(cudaGetDevice(&dev));
+    FLZ_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+    return n;
+  }();
+  constexpr size_t kSmemPerSm = 227 * 1024, kMaxCta = 227 * 1024;
+  int ctas = want_ctas, stages = want_stages;
+  while (stages > 2 && (stages * (stage_bytes + 16) + 1024) * ctas > kSmemPerSm) --stages;
+  while (ctas > 1 && (stages * (stage_bytes + 16) + 1024) * ctas > kSmemPerSm) --ctas;
+  const size_t smem = stages * (stage_bytes + 16);
+  if (smem > kMaxCta) return false;
+  static const bool configured = [] {
+    FLZ_CUDA(cudaFuncSetAttribute(clenshaw_step_stencil_tma<R, MODE>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxCta));
+    return true;
+  }();
+  (void)configured;
+  const int64_t ntiles = (A.nslices + T / 32 - 1) / (T / 32);
+  const unsigned grid = (unsigned)std::min<int64_t>(ntiles, (int64_t)sms * ctas);
+  launch_k1_smem(ctx, clenshaw_step_stencil_tma<R, MODE>, grid, (unsigned)(T + 32 * nprod), smem, A, G,
+                 A.uv_pairs, A.nl, ntiles, stages, nprod, y_rows, x_rows, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo);
+  return true;
+}
+
 template <int R, int S, int MODE>
 void launch_ug(flz_ctx* ctx, const SellView& A, double s1, double s2, double b, const double* Y1,
                double* Y2, int64_t ldy, const double* X, int64_t ldx, double* Out, int64_t ldo) {
@@ -972,6 +1242,12 @@ void launch_ug(flz_ctx* ctx, const SellView& A, double s1, double s2, double b, 
   if (lean) {
     if constexpr (MODE != 3) {
       if (A.nslices == 0) return;
+      if constexpr (S == 0 || (S == 1 && R == 1)) {
+        if (launch_stencil_tma<R, MODE>(ctx, A, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo)) {
+          ctx->launches++;
+          return;
+        }
+      }
       const int spc = ctx->k1_slices_per_cta > 0 ? ctx->k1_slices_per_cta : FLZ_K1_SLICES_PER_CTA;
       const unsigned grid = (unsigned)((A.nslices + spc - 1) / spc);
       if ((ctx->k1_batch > 0 ? ctx->k1_batch : FLZ_K1_UB) >= 8)

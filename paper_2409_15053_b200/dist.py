@@ -176,6 +176,80 @@ class HaloPlan:
         return dict(ptr=ptr, col=col, val=val, slices=int(sizes[1]), positions=int(sizes[2]),
                     interior=int(sizes[3]))
 
+    def tile_plan(self):
+        """Tile plan of the TMA-staged stencil kernel (flz_plan_tiles), or None."""
+        info = np.zeros(30, np.int64)
+        vp = lambda a: a.ctypes.data_as(C.c_void_p)
+        check(lib().flz_plan_tiles(self.handle, vp(info), None))
+        if not info[1]:
+            return None
+        pairs = np.zeros(int(info[28]), np.float64)
+        check(lib().flz_plan_tiles(self.handle, vp(info), vp(pairs)))
+        ns = int(info[1])
+        return dict(tile_rows=int(info[0]), nseg=ns, seg_base=info[2:2 + ns].copy(),
+                    seg_len=info[10:10 + ns].copy(), seg_start=info[18:18 + ns].copy(),
+                    y1_elems=int(info[26]), own_e=int(info[27]), pairs=pairs)
+
+    def tile_product(self, x, y_rows=None):
+        """y = A x evaluated tile by tile as clenshaw_step_stencil_tma does: the runs of x a
+        tile's segments reach are staged (clipped to [0, y_rows), zero filled), every position
+        reads staged element + row-in-tile, masked by its lane bit."""
+        G = self.tile_plan()
+        u = self.ug_arrays()
+        nl = self.info["rows_local"]
+        T = G["tile_rows"]
+        y_rows = y_rows or (nl + 31) // 32 * 32
+        xs = np.zeros(y_rows)
+        xs[:nl] = x
+        words = G["pairs"].view(np.uint64)
+        ntiles = len(G["pairs"]) // 16 // (T // 32)
+        y = np.zeros(ntiles * T)
+        lanes = np.arange(32)
+        for t in range(ntiles):
+            r0 = t * T
+            stage = np.full(G["y1_elems"], np.nan)     # unfilled elements must never be read
+            for j in range(G["nseg"]):
+                g0 = r0 + int(G["seg_base"][j]); g1 = g0 + int(G["seg_len"][j])
+                a0, a1 = max(g0, 0), min(g1, y_rows)
+                seg = np.zeros(g1 - g0)
+                if a1 > a0:
+                    seg[a0 - g0:a1 - g0] = xs[a0:a1]
+                assert g0 % 2 == 0 and len(seg) % 2 == 0 and int(G["seg_start"][j]) % 2 == 0
+                stage[int(G["seg_start"][j]):int(G["seg_start"][j]) + len(seg)] = seg
+            for w in range(T // 32):
+                s = t * (T // 32) + w
+                nuv = int(words[s * 16 + 1] >> np.uint64(52)) & 0xf
+                acc = np.zeros(32)
+                for p in range(8):
+                    value = G["pairs"][s * 16 + 2 * p]
+                    word = int(words[s * 16 + 2 * p + 1])
+                    if p >= nuv:
+                        assert value == 0.0 and (word & 0xffffffff) == 0
+                    e = ((word >> 32) & 0xfffff) // 8
+                    on = ((word & 0xffffffff) >> lanes) & 1
+                    acc += np.where(on == 1, value, 0.0) * stage[e + w * 32 + lanes]
+                if (int(words[s * 16 + 1]) >> 56) & 1:   # per-lane positions, from "global" x
+                    d = u["desc"][s]
+                    val_ptr = int(np.array(d[0:2]).view(np.int64)[0])
+                    col_ptr = int(np.array(d[2:4]).view(np.int64)[0])
+                    nu, ng = int(d[5]), int(d[6])
+                    assert nuv == (int(d[7]) >> 16) & 0xff and nu <= 8
+                    lane_rows = val_ptr + (2 * nuv + 15) // 16 * 16
+                    rows = s * 32 + lanes
+                    for p in range(nuv, nu):
+                        c = np.clip(rows + int(d[8 + p]), 0, nl - 1)
+                        q = lane_rows + (p - nuv) * 32
+                        acc += u["val"][q: q + 32] * xs[c]
+                    for q in range(ng):
+                        c = u["col"][col_ptr + q * 32: col_ptr + q * 32 + 32]
+                        k = lane_rows + (nu - nuv + q) * 32
+                        acc += u["val"][k: k + 32] * xs[c]
+                elif s < len(u["desc"]):
+                    d = u["desc"][s]
+                    assert int(d[6]) == 0 and int(d[5]) == nuv
+                y[s * 32 + lanes] = acc
+        return y[:nl]
+
     def p2_product(self, x):
         """y = A x evaluated from the paired layout as the kernel walks it."""
         p2 = self.p2_arrays()

@@ -16,7 +16,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def run(code, env_extra, args=()):
     env = dict(os.environ)
     for k in ("FLZ_SPLIT", "FLZ_K1_LAYOUT", "FLZ_SYNC_CHECK", "FLZ_K1_TMA", "FLZ_K1_PDL",
-              "FLZ_P2_CLUSTER"):
+              "FLZ_P2_CLUSTER", "FLZ_ST_TILE", "FLZ_ST_STAGES", "FLZ_ST_CTAS"):
         env.pop(k, None)
     env.update(env_extra)
     p = subprocess.run([sys.executable, "-c", code, *args], env=env, capture_output=True,
@@ -29,7 +29,11 @@ def run(code, env_extra, args=()):
                                  {"FLZ_SPLIT": "1", "FLZ_K1_LAYOUT": "planar"},
                                  {"FLZ_K1_TMA": "1"},          # paired layout, TMA-staged matrix stream
                                  {"FLZ_K1_PDL": "0"},          # plain stream-ordered launches
-                                 {"FLZ_P2_CLUSTER": "1"}])     # dense-block row clustering
+                                 {"FLZ_P2_CLUSTER": "1"},      # dense-block row clustering
+                                 {"FLZ_ST_TILE": "0"},         # stencils: one-warp-per-slice kernel
+                                 {"FLZ_ST_TILE": "64", "FLZ_ST_STAGES": "2", "FLZ_ST_CTAS": "3"},
+                                 {"FLZ_ST_TILE": "256", "FLZ_ST_STAGES": "4", "FLZ_ST_CTAS": "1"},
+                                 {"FLZ_ST_TILE": "512", "FLZ_K1_LAYOUT": "planar"}])
 def test_filter_variants_vs_oracle(env, best_oracle):
     """p(A) X through the forced layouts agrees with the reference (oracle) to 1e-13."""
     code = r'''
@@ -87,3 +91,36 @@ def test_pipelined_checks_equal_sequential_order():
     par = run(SOLVE_CODE, {})
     assert seq == par
     assert all(v["conv"] == 1 for v in par.values())
+
+
+TILE_CODE = r'''
+import sys, json, hashlib
+sys.path.insert(0, %r)
+import numpy as np
+from paper_2409_15053_b200 import Context, DeviceMatrix, matrices as M, solver as S
+ctx = Context(0)
+out = {}
+for name, gen in (("lap3d33", lambda: M.laplacian3d(33)), ("lap2d77", lambda: M.laplacian2d(77)),
+                  ("lap3d12", lambda: M.laplacian3d(12)), ("lap3d64", lambda: M.laplacian3d(64))):
+    n, rp, ci, va = gen()
+    A = DeviceMatrix(ctx, n, rp, ci, va)
+    cf = S.indicator_coefficients(-0.3, 0.25, 40)
+    for r in (1, 3, 6):
+        X = np.random.default_rng(r).standard_normal((n, r))
+        Y = A.filter_apply(cf, 4.0, 4.5, X)
+        Z = A.spmm(X) if hasattr(A, "spmm") else Y
+        out["%%s_r%%d" %% (name, r)] = [hashlib.sha1(np.ascontiguousarray(Y).tobytes()).hexdigest(),
+                                      hashlib.sha1(np.ascontiguousarray(Z).tobytes()).hexdigest()]
+print(json.dumps(out))
+''' % ROOT
+
+
+def test_tile_kernel_bit_identical_to_warp_kernel():
+    """The TMA-staged stencil kernel adds the positions of a row in the same order as the
+    one-warp-per-slice kernel: filter outputs and plain products are bit-identical, for every
+    tile size / ring depth (boundary tiles: clipped runs, slices with per-lane positions)."""
+    warp = run(TILE_CODE, {"FLZ_ST_TILE": "0", "FLZ_K1_LAYOUT": "planar"})
+    for env in ({"FLZ_K1_LAYOUT": "planar"},
+                {"FLZ_ST_TILE": "32", "FLZ_ST_STAGES": "2", "FLZ_K1_LAYOUT": "planar"},
+                {"FLZ_ST_TILE": "256", "FLZ_ST_STAGES": "5", "FLZ_ST_CTAS": "1", "FLZ_K1_LAYOUT": "planar"}):
+        assert run(TILE_CODE, env) == warp, env

@@ -212,3 +212,34 @@ def test_paired_layout_saves_gathers_on_dense_blocks():
     n, rp, ci, va = csr
     p2 = HaloPlan(n, 0, 1, [0, n], rp, ci, va).p2_arrays()
     assert p2["positions"] * 32 <= 0.9 * len(va)
+
+
+@pytest.mark.parametrize("tile", [32, 128, 512])
+@pytest.mark.parametrize("gen", [lambda: M.laplacian3d(20), lambda: M.laplacian2d(50),
+                                 lambda: M.laplacian3d(40), lambda: M.laplacian2d(33)])
+def test_stencil_tile_plan_reproduces_product(monkeypatch, gen, tile):
+    """Tile plan of the TMA-staged stencil kernel: staging the segments of every tile (clipped
+    at the ends of the vector, 16-byte aligned runs) and reading `staged element + row in
+    tile` per position reproduces A x; elements no copy or zero fill defines are never read
+    (the emulation poisons them with NaN)."""
+    monkeypatch.setenv("FLZ_ST_TILE", str(tile))
+    n, rp, ci, va = gen()
+    P = HaloPlan(n, 0, 1, uniform_starts(n, 1), rp, ci, va)
+    G = P.tile_plan()
+    assert G is not None and G["tile_rows"] == tile and 1 <= G["nseg"] <= 8
+    assert len(G["pairs"]) % (16 * tile // 32) == 0
+    x = np.random.default_rng(3).standard_normal(n)
+    y = P.tile_product(x)
+    assert np.abs(y - reference((n, rp, ci, va), x)).max() <= 1e-13 * np.abs(y).max()
+
+
+def test_stencil_tile_plan_absent_where_it_does_not_apply(monkeypatch):
+    """No tile plan for ragged matrices, for row-partitioned stencils (halo rows are not
+    contiguous runs) or when switched off."""
+    n, rp, ci, va = M.parsec_like(radius=10.0, n_atoms=8)
+    assert HaloPlan(n, 0, 1, uniform_starts(n, 1), rp, ci, va).tile_plan() is None
+    n, rp, ci, va = M.laplacian3d(16)
+    st = uniform_starts(n, 2)
+    assert HaloPlan(n, 0, 2, st, rp[: st[1] + 1], ci, va).tile_plan() is None
+    monkeypatch.setenv("FLZ_ST_TILE", "0")
+    assert HaloPlan(n, 0, 1, uniform_starts(n, 1), rp, ci, va).tile_plan() is None
