@@ -232,7 +232,10 @@ int row_stride(const flz_matrix* A, int R) {
   // planar blocks pay for stencil matrices with 3 columns on one GPU (100^3 Laplacian: 23.0 vs
   // 25.0 us per step: a coalesced 8-byte warp load touches 2-3 lines, a 24-byte-stride one 7);
   // with 4 columns the 32-byte rows win (37.3 vs 39.4 us)
-  const bool planar = force ? force[0] == 'p' : (A->lean && R == 3 && A->ctx->nranks == 1);
+  // ... and for every column count when the TMA-staged tile kernel applies (it reads planar
+  // blocks only: contiguous runs per column)
+  const bool planar = force ? force[0] == 'p'
+                            : (A->lean && A->ctx->nranks == 1 && (R == 3 || A->tiles.nseg > 0));
   if (planar) return 0;
   if (R != 3) return R;
   if (force && force[0] == '4') return 4;  // experiments: padded rows for every matrix

@@ -763,6 +763,15 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
       ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
 }
 
+// the same with an L2 eviction-priority policy (createpolicy) for the lines the copy touches
+__device__ __forceinline__ void bulk_g2s_hint(uint32_t dst, const void* src, uint32_t bytes,
+                                              uint32_t bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;"
+      ::"r"(dst), "l"(src), "r"(bytes), "r"(bar), "l"(policy) : "memory");
+}
+
 template <int R, int S, int MODE>
 __global__ void __launch_bounds__(kTaskWarps * 32, FLZ_K1_TASK_CTAS)
     clenshaw_step_p2_tma(SellView A, double s1, double s2, double b,
@@ -874,18 +883,25 @@ __global__ void __launch_bounds__(kTaskWarps * 32, FLZ_K1_TASK_CTAS)
 
 // ------------------------------------------------------------ TMA-staged stencil kernel
 // Constant-coefficient stencils on one GPU, planar blocks (host/plan.hpp, PlanStencilTiles).
-// A persistent CTA of T = tile_rows threads walks tiles of T consecutive rows.  Everything a
-// tile touches is CONTIGUOUS in global memory — per block column the runs of Y1 its offsets
-// reach (offsets closer than a tile share one run), its own rows of Y2 and X, and its slices'
-// (value, mask) pairs — so warp 0 requests the whole tile with a handful of cp.async.bulk
-// copies into a ring of shared-memory stages (mbarrier complete_tx), `nstages` tiles ahead.
-// The consumers then need no global load at all: a position costs one broadcast 16-byte
-// shared load (value, lane mask, staged element) and R conflict-free 8-byte shared loads, no
-// shuffles, no address clamps; only the results are written to global memory.  Memory-level
-// parallelism comes from the ring (stages x CTAs per SM x ~20 KB in flight), not from
-// occupancy and registers as in clenshaw_step_ug_warp.
-// Runs of a tile that leave [0, y_rows) are clipped; warp 0 zero-fills the clipped part (the
-// lanes that would read it carry a zero mask bit, but 0 * stale bits must stay finite).
+// A persistent CTA walks tiles of T = tile_rows consecutive rows (tile t, t + grid, ...).
+// Everything a tile touches is CONTIGUOUS in global memory — per block column the runs of Y1
+// its offsets reach (offsets closer than a tile share one run), its own rows of Y2 and X,
+// and its slices' (value, mask) pairs — so the tile is requested with a handful of
+// cp.async.bulk copies into a ring of shared-memory stages (full/empty mbarriers,
+// complete_tx), `nstages` tiles ahead of the consumers.
+//   * T consumer threads (one row each, T/32 warps = the tile's slices) need no global load at
+//     all: a position costs one broadcast 16-byte shared load (value, lane mask, staged byte
+//     offset) and R conflict-free 8-byte shared loads — no shuffles, no address clamps, no
+//     dependent global round trips; only the results go back to global memory.
+//   * nprod producer warps: lane l of producer warp w owns copy l*nprod + w of every tile.
+//     A warp issues its bulk copies one after the other (UBLKCP takes uniform operands, the
+//     compiler loops over the lanes; ~150 cycles per copy on B200), so ONE producer warp
+//     cannot feed the ring (measured: 34 us per step with one, 16.4 us with four).
+// Memory-level parallelism comes from the ring (stages x CTAs per SM x ~36 KB in flight), not
+// from occupancy and registers as in clenshaw_step_ug_warp.  Runs that leave [0, rows) are
+// clipped and the producers zero-fill the clipped part (the lanes that would read it carry a
+// zero mask bit, but 0 * stale bits must stay finite).  Positions are added in the order of
+// clenshaw_step_ug_warp: results are bit-identical (tests/test_gpu_variants.py).
 // The positions of a stencil slice that are not uniform-value pairs (rows next to a domain
 // boundary: per-lane values at uniform offsets, then general positions), gathered from global
 // memory in the order clenshaw_step_ug_warp adds them.  Rare: a few slices per matrix.
@@ -924,7 +940,7 @@ __global__ void __launch_bounds__(768)
     clenshaw_step_stencil_tma(const __grid_constant__ SellView A,
                               const __grid_constant__ StencilTiles G,
                               const double* __restrict__ pairs, int64_t nl,
-                              int64_t ntiles, int nstages, int nprod, int64_t y_rows,
+                              int64_t ntiles, int nstages, int nprod, int l2hint, int64_t y_rows,
                               int64_t x_rows,
                               double s1, double s2, double b, const double* __restrict__ Y1,
                               double* __restrict__ Y2, int64_t ldy, const double* __restrict__ X,
@@ -966,7 +982,13 @@ __global__ void __launch_bounds__(768)
     int dst = 0, full = 0, off = 0;   // staged element, run length, first row relative to the tile
     int64_t lim = 0;                  // readable rows of the source column
     const double* base = nullptr;
+    // L2 policy: X and the matrix pairs are read again by every later step of the filter and
+    // never written (evict_last); the Y blocks take the default priority
+    bool keep = false;
+    uint64_t pol_keep = 0;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
     if (c == 0) {
+      keep = true;
       full = pair_d;
     } else if (c < 1 + G.nseg * R) {
       const int q = c - 1, j = q / R, k = q - j * R;
@@ -981,7 +1003,9 @@ __global__ void __launch_bounds__(768)
       full = T;
       lim = which ? x_rows : y_rows;
       base = which ? X + (int64_t)k * ldx : Y2 + (int64_t)k * ldy;
+      keep = which != 0;
     }
+    keep = keep && l2hint;
     int st = 0;
     uint32_t parity = 1;  // first pass over the ring: the stages are empty (wait falls through)
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
@@ -1014,8 +1038,11 @@ __global__ void __launch_bounds__(768)
         asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
                      "r"(total) : "memory");
       __syncwarp();
-      if (count > 0)
-        bulk_g2s(ring_s + (uint32_t)(st * stage_d + dst + lead) * 8u, src, bytes, bar);
+      if (count > 0) {
+        const uint32_t to = ring_s + (uint32_t)(st * stage_d + dst + lead) * 8u;
+        if (keep) bulk_g2s_hint(to, src, bytes, bar, pol_keep);
+        else bulk_g2s(to, src, bytes, bar);
+      }
       if (++st == nstages) { st = 0; parity ^= 1u; }
     }
     return;
@@ -1176,6 +1203,7 @@ bool launch_stencil_tma(flz_ctx* ctx, const SellView& A, double s1, double s2, d
   static const int want_prod = std::clamp(env_int("FLZ_ST_PRODUCERS", 4), 1, 8);
   const int ncopy = 1 + G.nseg * R + (MODE != 2 ? 2 * R : 0);
   const int nprod = std::max(want_prod, (ncopy + 31) / 32);
+  static const int l2hint = env_int("FLZ_ST_L2HINT", 1);
   static const int sms = [] {
     int dev = 0, n = 0;
     FLZ_CUDA(cudaGetDevice(&dev));
@@ -1197,7 +1225,7 @@ bool launch_stencil_tma(flz_ctx* ctx, const SellView& A, double s1, double s2, d
   const int64_t ntiles = (A.nslices + T / 32 - 1) / (T / 32);
   const unsigned grid = (unsigned)std::min<int64_t>(ntiles, (int64_t)sms * ctas);
   launch_k1_smem(ctx, clenshaw_step_stencil_tma<R, MODE>, grid, (unsigned)(T + 32 * nprod), smem, A, G,
-                 A.uv_pairs, A.nl, ntiles, stages, nprod, y_rows, x_rows, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo);
+                 A.uv_pairs, A.nl, ntiles, stages, nprod, l2hint, y_rows, x_rows, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo);
   return true;
 }
 
