@@ -211,7 +211,7 @@ def run_reference(args, wl):
         base["sample"] += "; block_steps unknown for this workload, assumed 100"
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": value * 1e3,
-            "higher_is_better": False, "scaling": "strong" if args.gpus > 1 else "n/a",
+            "higher_is_better": False, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{args.workload}: {wl['desc']}", "block_size": r,
                        "degree": degree, "block_steps": block_steps},
@@ -359,7 +359,7 @@ def run_flz(args, wl):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": value * 1e3, "higher_is_better": False,
-        "scaling": "strong" if world > 1 else "n/a", "vs_baseline": None, "dtype": "f64",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": f"{args.workload}: {wl['desc']}", "n": n, "nnz": nnz,
                    "interval": [a, b], "block_size": r, "degree": st["degree"],
