@@ -39,7 +39,7 @@ int main() {
   }
   // small-footprint copy like one K1 step (183 MB total traffic), cold-ish L2 by alternating buffers
   for (size_t m : {(size_t)12000000, (size_t)48000000}) {
-    cudaEventRecord(e0); for (int i=0;i<20;i++) copy_k<<<148*16, 512>>>((double2*)(a + (i%4)*m), (double2*)(b + (i%4)*m), m/2); cudaEventRecord(e1); cudaEventSynchronize(e1);
+    cudaEventRecord(e0); for (int i=0;i<20;i++) copy_k<<<148*16, 512>>>((double2*)(a + (i%(n/m))*m), (double2*)(b + (i%(n/m))*m), m/2); cudaEventRecord(e1); cudaEventSynchronize(e1);
     cudaEventElapsedTime(&ms, e0, e1); printf("copy of %zu MB per launch: %.1f us/launch %.0f GB/s\n", m*16/1000000, ms/20*1e3, 20*2.0*m*8/ms/1e6);
   }
   size_t rows = 1000000;
