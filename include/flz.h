@@ -98,6 +98,13 @@ int flz_matrix_stats(const flz_matrix* A, int64_t* stored_entries, int64_t* slic
  * layout for long ragged rows; the (value, mask) pairs alone for stencils with a tile plan)
  * and the number of true nonzeros held at uniform-offset positions */
 int flz_matrix_layout(const flz_matrix* A, int64_t* matrix_bytes, int64_t* uniform_entries);
+/* what one fused Clenshaw step of `r` block columns (1..4) runs and moves in fast mode on
+ * this matrix: name of the kernel (copied into kernel[cap]) and the bytes its layout has to
+ * stream per launch (compressed matrix + the block streams: gather source once, Y2 in,
+ * X in, result out), for the roofline record of bench.py.
+ * info[4] = {streamed bytes, dense blocks, nonzeros held in dense sections, block row stride
+ * (0 = planar)} */
+int flz_matrix_k1_info(const flz_matrix* A, int r, int64_t* info, char* kernel, int cap);
 /* launch-shape knobs of the fused Clenshaw-step kernels (0 = built-in default): slices per
  * CTA of the one-warp-per-slice kernel, tasks per CTA of the multi-warp kernel, positions
  * per pipeline stage of the one-warp-per-slice kernel (4 or 8) */
@@ -133,10 +140,13 @@ int flz_plan_arrays(const flz_plan* plan, int32_t* perm, int64_t* slice_ptr, int
 int flz_plan_ug(const flz_plan* plan, int64_t* sizes, int32_t* descriptors, double* ug_val,
                 int32_t* ug_col, int32_t* ug_uoff, int32_t* rest_rows);
 /* paired layout of the plan (long ragged rows; host/plan.hpp), for host-side checks:
- * sizes[4] = {used, 64-row slices, positions, interior slices}; ptr[slices + 1] first position
- * of every slice; col[positions * 32]; val[positions * 64] (two values per lane and position).
- * Any pointer may be NULL. */
-int flz_plan_p2(const flz_plan* plan, int64_t* sizes, int64_t* ptr, int32_t* col, double* val);
+ * sizes[8] = {used, slices, general positions, interior slices, dense positions, dense
+ * blocks, nonzeros in dense sections, 0}; ptr[slices + 1] first general position of every
+ * slice; col[positions * 32]; val[positions * 64] (two values per lane and position);
+ * desc[slices * 6] = {gpos, dpos, ng, nd, row0, nrows} per slice; dcol[dense positions]
+ * shared columns; dval[dense positions * 64].  Any pointer may be NULL. */
+int flz_plan_p2(const flz_plan* plan, int64_t* sizes, int64_t* ptr, int32_t* col, double* val,
+                int64_t* desc, int32_t* dcol, double* dval);
 /* tile plan of the TMA-staged stencil kernel (constant-coefficient stencils on one rank;
  * host/plan.hpp), for host-side checks: info[30] = {tile_rows, segments, seg_base[8],
  * seg_len[8], seg_start[8], staged elements per column, staged element of offset 0,

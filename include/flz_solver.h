@@ -76,6 +76,8 @@ int flz_hostmatrix_dims(const flz_hostmatrix* A, int64_t* n, int64_t* nnz);
  * index-compressed copy one fused Clenshaw step streams, true nonzeros at uniform positions */
 int flz_hostmatrix_layout(const flz_hostmatrix* A, int64_t* matrix_bytes,
                           int64_t* uniform_entries);
+/* flz_matrix_k1_info of the resident matrix (uploads it when needed) */
+int flz_hostmatrix_k1_info(const flz_hostmatrix* A, int r, int64_t* info, char* kernel, int cap);
 int flz_hostmatrix_csr(const flz_hostmatrix* A, int64_t* row_ptr, int32_t* col_idx,
                        double* values);
 /* SparseSymMatrix::spmm_block / ChebyshevFilter::apply through the C++ facade */

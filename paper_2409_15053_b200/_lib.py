@@ -93,7 +93,8 @@ _SIGS = {
     "flz_plan_set_give": (i32, [vp, i32, i64, i64p]),
     "flz_plan_arrays": (i32, [vp] + [vp] * 12),
     "flz_plan_ug": (i32, [vp, vp, vp, vp, vp, vp, vp]),
-    "flz_plan_p2": (i32, [vp, vp, vp, vp, vp]),
+    "flz_plan_p2": (i32, [vp, vp, vp, vp, vp, vp, vp, vp]),
+    "flz_matrix_k1_info": (i32, [vp, i32, vp, vp, i32]),
     "flz_plan_tiles": (i32, [vp, vp, vp]),
     "flz_matvec_count": (u64, []),
     "flz_reset_matvec_count": (None, []),
@@ -133,6 +134,7 @@ _SOLVER_SIGS = {
     "flz_hostmatrix_free": (None, [vp]),
     "flz_hostmatrix_dims": (i32, [vp, i64P, i64P]),
     "flz_hostmatrix_layout": (i32, [vp, i64P, i64P]),
+    "flz_hostmatrix_k1_info": (i32, [vp, i32, vp, vp, i32]),
     "flz_hostmatrix_csr": (i32, [vp, i64p, i32p, f64p]),
     "flz_hostmatrix_spmm": (i32, [vp, f64p, i64, i32, f64p]),
     "flz_hostmatrix_filter_apply": (i32, [vp, f64p, i32, d, d, f64p, i64, i32, f64p]),

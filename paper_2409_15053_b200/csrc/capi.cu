@@ -111,7 +111,8 @@ SellView make_view(const flz_matrix* A, const SliceTask* tasks, int64_t ntasks,
                   A->row_len.p, A->col.p,   A->val.p,      slice_ids,      nslices,
                   A->nl,        A->ug.p,    A->ug_val.p,   A->ug_col.p,    A->ug_uoff.p,
                   A->nl + A->nhalo, A->rest_rows.p, A->nslices,   A->w.p,
-                  A->uv_pairs.p,    false,          A->p2_ptr.p,  A->p2_col.p, A->p2_val.p,
+                  A->uv_pairs.p,    false,          A->p2_desc.p, A->p2_col.p, A->p2_val.p,
+                  A->p2_dcol.p,     A->p2_dval.p,
                   // the tile kernel covers whole-matrix launches only
                   (slice_ids == nullptr && nslices == A->nslices) ? A->tiles : StencilTiles{}};
 }
@@ -572,9 +573,17 @@ static void upload_plan(flz_ctx* ctx, HostPlan& P, flz_matrix* A) {
   std::memcpy(static_cast<void*>(&A->tiles), &P.tiles, sizeof(StencilTiles));
   A->p2 = P.p2;
   if (P.p2) {
-    up(A->p2_ptr, P.p2_ptr);
+    static_assert(sizeof(PlanP2Slice) == sizeof(P2Slice), "PlanP2Slice mirrors P2Slice");
+    A->p2_desc.reserve(std::max<size_t>(P.p2_desc.size(), 1));
+    if (!P.p2_desc.empty())
+      FLZ_CUDA(cudaMemcpyAsync(A->p2_desc.p, P.p2_desc.data(), P.p2_desc.size() * sizeof(P2Slice),
+                               cudaMemcpyHostToDevice, ctx->stream));
     up(A->p2_col, P.p2_col);
     up(A->p2_val, P.p2_val);
+    up(A->p2_dcol, P.p2_dcol);
+    up(A->p2_dval, P.p2_dval);
+    A->p2_blocks = P.p2_blocks;
+    A->p2_dense_entries = P.p2_dense_entries;
     auto up_p2 = [&](DevBuf<SliceTask>& buf, const std::vector<PlanTask>& host, int64_t& count) {
       count = (int64_t)host.size();
       buf.reserve(std::max<size_t>(host.size(), 1));
@@ -585,7 +594,8 @@ static void upload_plan(flz_ctx* ctx, HostPlan& P, flz_matrix* A) {
     up_p2(A->p2_tasks_all, P.p2_tasks_all, A->p2_nt_all);
     up_p2(A->p2_tasks_interior, P.p2_tasks_interior, A->p2_nt_interior);
     up_p2(A->p2_tasks_boundary, P.p2_tasks_boundary, A->p2_nt_boundary);
-    A->p2_bytes = (int64_t)(P.p2_col.size() * 4 + P.p2_val.size() * 8 + P.p2_ptr.size() * 8);
+    A->p2_bytes = (int64_t)(P.p2_col.size() * 4 + P.p2_val.size() * 8 + P.p2_dcol.size() * 4 +
+                            P.p2_dval.size() * 8 + P.p2_desc.size() * sizeof(P2Slice));
   }
   A->ug_bytes = (int64_t)(P.ug_val.size() * 8 + P.ug_col.size() * 4 + P.ug_uoff.size() * 4 +
                           P.ug_slice.size() * sizeof(UgSlice));
@@ -820,19 +830,34 @@ int flz_plan_ug(const flz_plan* plan, int64_t* sizes, int32_t* descriptors, doub
   return FLZ_OK;
 }
 
-int flz_plan_p2(const flz_plan* plan, int64_t* sizes, int64_t* ptr, int32_t* col, double* val) {
+int flz_plan_p2(const flz_plan* plan, int64_t* sizes, int64_t* ptr, int32_t* col, double* val,
+                int64_t* desc, int32_t* dcol, double* dval) {
   if (!plan) return FLZ_EINVAL;
   const HostPlan& P = plan->P;
+  const int64_t dense_positions =
+      P.p2 && !P.p2_desc.empty() ? P.p2_desc.back().dpos + P.p2_desc.back().nd : 0;
   if (sizes) {
+    std::fill(sizes, sizes + 8, (int64_t)0);
     sizes[0] = P.p2 ? 1 : 0;
     sizes[1] = P.p2_slices;
-    sizes[2] = P.p2 ? P.p2_ptr.back() : 0;   // positions
+    sizes[2] = P.p2 ? P.p2_ptr.back() : 0;   // general positions
     sizes[3] = (int64_t)P.p2_interior.size();
+    sizes[4] = dense_positions;
+    sizes[5] = P.p2_blocks;
+    sizes[6] = P.p2_dense_entries;
   }
   if (!P.p2) return FLZ_OK;
   if (ptr) std::copy(P.p2_ptr.begin(), P.p2_ptr.end(), ptr);
   if (col) std::copy(P.p2_col.begin(), P.p2_col.end(), col);
   if (val) std::copy(P.p2_val.begin(), P.p2_val.end(), val);
+  if (desc)
+    for (size_t s = 0; s < P.p2_desc.size(); ++s) {
+      const PlanP2Slice& D = P.p2_desc[s];
+      const int64_t row[6] = {D.gpos, D.dpos, D.ng, D.nd, D.row0, D.nrows};
+      std::copy(row, row + 6, desc + 6 * s);
+    }
+  if (dcol) std::copy_n(P.p2_dcol.begin(), dense_positions, dcol);
+  if (dval) std::copy_n(P.p2_dval.begin(), dense_positions * 64, dval);
   return FLZ_OK;
 }
 
@@ -882,6 +907,39 @@ int flz_matrix_layout(const flz_matrix* A, int64_t* matrix_bytes, int64_t* unifo
     *matrix_bytes = A->p2 ? A->p2_bytes
                           : (A->tiles.nseg > 0 ? (int64_t)A->uv_pairs.count * 8 : A->ug_bytes);
   if (uniform_entries) *uniform_entries = A->ug_uniform_entries;
+  return FLZ_OK;
+}
+int flz_matrix_k1_info(const flz_matrix* A, int r, int64_t* info, char* kernel, int cap) {
+  if (!A || r < 1 || r > kMaxFuse) return FLZ_EINVAL;
+  const int S = row_stride(A, r);
+  const char* name;
+  int64_t matrix_bytes;
+  if (A->ctx->exact) {
+    name = "clenshaw_step_sell<EXACT>";
+    matrix_bytes = A->stored * 12;
+  } else if (A->p2) {
+    name = A->p2_blocks > 0 ? "clenshaw_step_p2_tasks (paired + dense sections)"
+                            : "clenshaw_step_p2_tasks (paired)";
+    matrix_bytes = A->p2_bytes;
+  } else if (A->short_rows && A->lean) {
+    const bool tile = A->tiles.nseg > 0 && (S == 0 || (S == 1 && r == 1));
+    name = tile ? "clenshaw_step_stencil_tma" : "clenshaw_step_ug_warp";
+    matrix_bytes = tile ? (int64_t)A->uv_pairs.count * 8 : A->ug_bytes;
+  } else {
+    name = "clenshaw_step_ug_tasks";
+    matrix_bytes = A->ug_bytes;
+  }
+  const int64_t stride = S > 0 ? S : r;
+  if (info) {
+    info[0] = matrix_bytes + 8 * A->nl * (3 * stride + r);
+    info[1] = A->p2_blocks;
+    info[2] = A->p2_dense_entries;
+    info[3] = S;
+  }
+  if (kernel && cap > 0) {
+    std::strncpy(kernel, name, (size_t)cap - 1);
+    kernel[cap - 1] = 0;
+  }
   return FLZ_OK;
 }
 int flz_ctx_set_tuning(flz_ctx* ctx, int slices_per_cta, int tasks_per_cta, int batch) {

@@ -105,6 +105,13 @@ struct StencilTiles {
   int32_t y1_elems = 0, own_e = 0;
 };
 
+// Slice descriptor of the paired layout (mirrors PlanP2Slice, host/plan.hpp)
+struct P2Slice {
+  int64_t gpos, dpos;
+  int32_t ng, nd;
+  int32_t row0, nrows;
+};
+
 struct UgSlice {
   int64_t val_ptr;
   int64_t col_ptr;
@@ -176,9 +183,10 @@ struct flz_matrix {
   mutable unsigned long long tile_epoch = 0;
   // paired layout (host/plan.hpp)
   bool p2 = false;
-  flz::DevBuf<int64_t> p2_ptr;
-  flz::DevBuf<int32_t> p2_col;
-  flz::DevBuf<double> p2_val;
+  flz::DevBuf<flz::P2Slice> p2_desc;
+  flz::DevBuf<int32_t> p2_col, p2_dcol;
+  flz::DevBuf<double> p2_val, p2_dval;
+  int64_t p2_blocks = 0, p2_dense_entries = 0;
   flz::DevBuf<flz::SliceTask> p2_tasks_all, p2_tasks_interior, p2_tasks_boundary;
   int64_t p2_nt_all = 0, p2_nt_interior = 0, p2_nt_boundary = 0;
   int64_t p2_bytes = 0;
@@ -274,9 +282,11 @@ struct SellView {
   // paired layout (host/plan.hpp): 64-row slices, two adjacent rows per lane; `tasks` then
   // lists paired slices
   bool p2;
-  const int64_t* p2_ptr;
+  const P2Slice* p2_desc;
   const int32_t* p2_col;
   const double* p2_val;
+  const int32_t* p2_dcol;    // dense sections: shared columns, one value pair per lane
+  const double* p2_dval;
   StencilTiles tiles;        // nseg > 0: tile plan of the TMA-staged stencil kernel
 };
 

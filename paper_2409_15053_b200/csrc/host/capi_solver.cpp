@@ -166,6 +166,9 @@ int flz_hostmatrix_layout(const flz_hostmatrix* A, int64_t* matrix_bytes,
     throw_status(flz_matrix_layout(A->A.device(), matrix_bytes, uniform_entries));
   });
 }
+int flz_hostmatrix_k1_info(const flz_hostmatrix* A, int r, int64_t* info, char* kernel, int cap) {
+  return wrap([&] { throw_status(flz_matrix_k1_info(A->A.device(), r, info, kernel, cap)); });
+}
 int flz_hostmatrix_csr(const flz_hostmatrix* A, int64_t* row_ptr, int32_t* col_idx,
                        double* values) {
   std::copy(A->A.row_ptr().begin(), A->A.row_ptr().end(), row_ptr);

@@ -566,34 +566,152 @@ int64_t build_ug(HostPlan& P, const std::vector<uint8_t>& is_boundary, bool allo
   return (int64_t)rest_col.size();
 }
 
+// ---- dense blocks (plan.hpp) ---------------------------------------------------------------
+// Near-cliques among the LONG rows of the local diagonal block: rows much longer than the
+// median (the members of non-local projector balls on PARSEC-like Hamiltonians).  Greedy:
+// seeds in ascending row length (rows of a single ball first); candidate set K = the seed's
+// still uncovered long columns; two refinement passes keep the members adjacent to >= 80 % of
+// K; K is accepted when it has >= kDenseMin members and at least half of K x K is new.  All
+// entries (j, c), j and c in K, are then COVERED by the block.  Matrices without such blocks
+// cost a bounded number of failed seeds.
+struct DenseBlocks {
+  std::vector<std::vector<int32_t>> members;  // local row ids, ascending
+  std::vector<uint8_t> covered;               // per local CSR entry
+  std::vector<int32_t> count;                 // blocks a row belongs to
+  std::vector<int32_t> primary;               // the block of a row with count == 1, else -1
+  int64_t covered_entries = 0;
+  bool any() const { return !members.empty(); }
+};
+constexpr int kDenseMin = 32;
+
+DenseBlocks extract_dense_blocks(int64_t nl, int64_t row_begin, const int64_t* row_ptr,
+                                 const int32_t* col_idx, const std::vector<int32_t>& len,
+                                 int64_t nnz) {
+  DenseBlocks B;
+  if (nl < 1024) return B;
+  std::vector<int32_t> tmp(len);
+  std::nth_element(tmp.begin(), tmp.begin() + nl / 2, tmp.end());
+  const int32_t long_min = std::max<int32_t>(48, tmp[nl / 2] + tmp[nl / 2] / 2);
+  std::vector<uint8_t> is_long(nl, 0);
+  int64_t long_entries = 0;
+  std::vector<int32_t> seeds;
+  for (int64_t i = 0; i < nl; ++i)
+    if (len[i] > long_min) {
+      is_long[i] = 1;
+      long_entries += len[i];
+      seeds.push_back((int32_t)i);
+    }
+  if (5 * long_entries < nnz) return B;
+  const int64_t p0 = row_ptr[0];
+  auto local = [&](int64_t e) { return (int64_t)col_idx[e] - row_begin; };
+  std::vector<int32_t> uncov(nl, 0);
+  for (int32_t i : seeds)
+    for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
+      const int64_t c = local(e);
+      if (c >= 0 && c < nl && is_long[c]) ++uncov[i];
+    }
+  std::stable_sort(seeds.begin(), seeds.end(), [&](int32_t a, int32_t b) { return len[a] < len[b]; });
+  B.covered.assign((size_t)nnz, 0);
+  B.count.assign(nl, 0);
+  std::vector<uint8_t> mark(nl, 0);
+  std::vector<int32_t> K, keep;
+  int fails = 0;
+  for (int32_t seed : seeds) {
+    if (uncov[seed] < kDenseMin) continue;
+    K.clear();
+    bool has_seed = false;
+    for (int64_t e = row_ptr[seed]; e < row_ptr[seed + 1]; ++e) {
+      const int64_t c = local(e);
+      if (c < 0 || c >= nl || !is_long[c] || B.covered[e - p0]) continue;
+      K.push_back((int32_t)c);
+      has_seed = has_seed || c == seed;
+    }
+    if (!has_seed) K.push_back(seed);
+    for (int pass = 0; pass < 2 && (int)K.size() >= kDenseMin; ++pass) {
+      for (int32_t c : K) mark[c] = 1;
+      keep.clear();
+      for (int32_t j : K) {
+        int32_t d = 0;
+        for (int64_t e = row_ptr[j]; e < row_ptr[j + 1]; ++e) {
+          const int64_t c = local(e);
+          d += (c >= 0 && c < nl && mark[c]) ? 1 : 0;
+        }
+        if (5 * (int64_t)d >= 4 * (int64_t)K.size()) keep.push_back(j);
+      }
+      for (int32_t c : K) mark[c] = 0;
+      K.swap(keep);
+    }
+    bool ok = (int)K.size() >= kDenseMin;
+    if (ok) {  // at least half of K x K must be new entries
+      for (int32_t c : K) mark[c] = 1;
+      int64_t fresh = 0;
+      for (int32_t j : K)
+        for (int64_t e = row_ptr[j]; e < row_ptr[j + 1]; ++e) {
+          const int64_t c = local(e);
+          fresh += (c >= 0 && c < nl && mark[c] && !B.covered[e - p0]) ? 1 : 0;
+        }
+      ok = 2 * fresh >= (int64_t)K.size() * (int64_t)K.size();
+      if (ok) {
+        for (int32_t j : K)
+          for (int64_t e = row_ptr[j]; e < row_ptr[j + 1]; ++e) {
+            const int64_t c = local(e);
+            if (c >= 0 && c < nl && mark[c] && !B.covered[e - p0]) {
+              B.covered[e - p0] = 1;
+              --uncov[j];
+            }
+          }
+        B.covered_entries += fresh;
+      }
+      for (int32_t c : K) mark[c] = 0;
+    }
+    if (!ok) {
+      if (++fails > 64 + 4 * (int)B.members.size()) break;  // no block structure: give up
+      continue;
+    }
+    std::sort(K.begin(), K.end());
+    for (int32_t j : K) ++B.count[j];
+    B.members.push_back(K);
+  }
+  if (10 * B.covered_entries < nnz) return DenseBlocks{};  // not worth a second row order
+  B.primary.assign(nl, -1);
+  for (size_t b = 0; b < B.members.size(); ++b)
+    for (int32_t j : B.members[b])
+      if (B.count[j] == 1) B.primary[j] = (int32_t)b;
+  return B;
+}
+
 // ---- paired layout (plan.hpp) ------------------------------------------------------------
-void build_p2(HostPlan& P, const std::vector<uint8_t>& is_boundary32,
-              const std::vector<int32_t>& pair_ulen, bool frequency_order) {
+struct P2Spec {  // rows [row0, row0 + nrows) of the permuted order, block = dense block or -1
+  int32_t row0, nrows, block;
+};
+// `skip` (optional, parallel to P.col / P.val): entries that a dense section holds instead.
+void build_p2(HostPlan& P, const std::vector<P2Spec>& specs, const std::vector<uint8_t>* skip,
+              const DenseBlocks* blocks) {
   const int64_t nl = P.nl;
-  const int64_t ns = P.p2_slices = (nl + 63) / 64;
+  const int64_t ns = P.p2_slices = (int64_t)specs.size();
+  P.p2_desc.assign(ns, PlanP2Slice{});
   P.p2_ptr.assign(ns + 1, 0);
-  std::vector<int32_t> len(ns, 0);
   const int nchunks = (int)std::max<int64_t>(1, std::min<int64_t>(worker_count(), ns / 64));
   // merged (column, value A, value B) list of one lane, ascending column
   struct Entry {
     int32_t col;
     double a, b;
   };
-  auto merge_lane = [&](int64_t rowA, std::vector<Entry>& out, std::vector<Entry>& tmp) {
+  auto merge_lane = [&](int64_t rowA, int nrows, std::vector<Entry>& out, std::vector<Entry>& tmp) {
     out.clear();
-    for (int which = 0; which < 2; ++which) {
+    for (int which = 0; which < std::min(2, nrows); ++which) {
       const int64_t row = rowA + which;
-      if (row >= nl) continue;
       const int64_t s32 = row / kPlanSliceRows, l32 = row % kPlanSliceRows;
       const int64_t base = P.slice_ptr[s32] + l32;
       tmp.clear();
       for (int32_t p = 0; p < P.row_len[row]; ++p) {
         const int64_t e = base + (int64_t)p * kPlanSliceRows;
+        if (skip && (*skip)[e]) continue;
         tmp.push_back({P.col[e], which == 0 ? P.val[e] : 0.0, which == 1 ? P.val[e] : 0.0});
       }
       std::sort(tmp.begin(), tmp.end(), [](const Entry& x, const Entry& y) { return x.col < y.col; });
       if (which == 0) {
-        out = tmp;
+        out.swap(tmp);
       } else {  // merge into out
         std::vector<Entry> merged;
         merged.reserve(out.size() + tmp.size());
@@ -611,81 +729,54 @@ void build_p2(HostPlan& P, const std::vector<uint8_t>& is_boundary32,
       }
     }
   };
-  // slice lengths: the merged list sizes of the pairs were counted before the rows were sorted
-  // (pair_ulen, indexed by the pair's first row in the original order)
-  // — valid where the sort kept the pair together on an even position; a lone last row sorted
-  // in front of the others shifts the pairing, and those lanes are merged here instead
-  {
+  // pass 1: general positions per slice = the longest merged lane
+  std::vector<int32_t> ng(ns, 0);
+  run_chunks(nchunks, [&](int t) {
     std::vector<Entry> lane, tmp;
-    for (int64_t s = 0; s < ns; ++s) {
+    for (int64_t s = ns * t / nchunks; s < ns * (t + 1) / nchunks; ++s) {
       int32_t L = 0;
-      for (int l = 0; l < 32; ++l) {
-        const int64_t rowA = s * 64 + 2 * l;
-        if (rowA >= nl) break;
-        const int32_t origA = P.perm[rowA];
-        const bool lone = origA + 1 >= nl;
-        const bool kept = (origA % 2 == 0) &&
-                          (lone ? rowA + 1 >= nl : (rowA + 1 < nl && P.perm[rowA + 1] == origA + 1));
-        if (kept) {
-          L = std::max(L, pair_ulen[origA]);
-        } else {
-          merge_lane(rowA, lane, tmp);
-          L = std::max<int32_t>(L, (int32_t)lane.size());
-        }
+      for (int l = 0; 2 * l < specs[s].nrows; ++l) {
+        merge_lane(specs[s].row0 + 2 * l, specs[s].nrows - 2 * l, lane, tmp);
+        L = std::max<int32_t>(L, (int32_t)lane.size());
       }
-      len[s] = L;
+      ng[s] = L;
     }
+  });
+  int64_t gpos = 0, dpos = 0;
+  for (int64_t s = 0; s < ns; ++s) {
+    PlanP2Slice& D = P.p2_desc[s];
+    D.gpos = gpos;
+    D.dpos = dpos;
+    D.ng = ng[s];
+    D.nd = specs[s].block >= 0 ? (int32_t)blocks->members[specs[s].block].size() : 0;
+    D.row0 = specs[s].row0;
+    D.nrows = specs[s].nrows;
+    P.p2_ptr[s] = gpos;
+    gpos += D.ng;
+    dpos += D.nd;
   }
-  for (int64_t s = 0; s < ns; ++s) P.p2_ptr[s + 1] = P.p2_ptr[s] + len[s];
-  const int64_t positions = P.p2_ptr[ns];
-  P.p2_entries = positions * 32;
-  P.p2_col.assign(std::max<int64_t>(positions * 32, 1), 0);
-  P.p2_val.assign(std::max<int64_t>(positions * 64, 2), 0.0);
-  // pass 2: fill
-  // Entry order inside a lane, clustered row order only (frequency_order; otherwise ascending
-  // columns): columns that at least 8 lanes of the slice hold come first, most
-  // frequent first (ties ascending), the others follow in ascending order.  In a slice whose
-  // lanes sit in one dense block every lane then asks for the SAME column at the same position
-  // — one L1 line per warp-level gather instead of one per lane.  (Fast mode sums in layout
-  // order; the exact-mode kernel reads the CSR-order arrays.)  Padding entries repeat the
-  // column the lane below them asked for, so they add no line either.
-  constexpr int kSharedLanes = 8;
+  P.p2_ptr[ns] = gpos;
+  P.p2_entries = gpos * 32;
+  P.p2_col.assign(std::max<int64_t>(gpos * 32, 1), 0);
+  P.p2_val.assign(std::max<int64_t>(gpos * 64, 2), 0.0);
+  P.p2_dcol.assign(std::max<int64_t>(dpos, 1), 0);
+  P.p2_dval.assign(std::max<int64_t>(dpos * 64, 2), 0.0);
+  // pass 2: fill.  Padding entries of a general position repeat the column of the lane below
+  // (no extra line for the gather) with zero values.
+  std::vector<uint8_t> boundary(ns, 0);
+  std::vector<int64_t> dense_fill(nchunks, 0);
   run_chunks(nchunks, [&](int t) {
     std::vector<Entry> lanes[32], tmp;
-    std::vector<int32_t> all, ucol, ucnt;
     for (int64_t s = ns * t / nchunks; s < ns * (t + 1) / nchunks; ++s) {
-      int32_t* c = P.p2_col.data() + P.p2_ptr[s] * 32;
-      double* v = P.p2_val.data() + P.p2_ptr[s] * 64;
-      all.clear();
+      const PlanP2Slice& D = P.p2_desc[s];
+      int32_t* c = P.p2_col.data() + D.gpos * 32;
+      double* v = P.p2_val.data() + D.gpos * 64;
       for (int l = 0; l < 32; ++l) {
-        merge_lane(s * 64 + 2 * l, lanes[l], tmp);
-        if (frequency_order)
-          for (const Entry& e : lanes[l]) all.push_back(e.col);
+        if (2 * l < D.nrows) merge_lane(D.row0 + 2 * l, D.nrows - 2 * l, lanes[l], tmp);
+        else lanes[l].clear();
       }
-      std::sort(all.begin(), all.end());
-      ucol.clear();
-      ucnt.clear();
-      bool any_shared = false;
-      for (size_t i = 0; i < all.size();) {
-        size_t j = i;
-        while (j < all.size() && all[j] == all[i]) ++j;
-        ucol.push_back(all[i]);
-        ucnt.push_back((int32_t)(j - i));
-        any_shared = any_shared || (j - i) >= (size_t)kSharedLanes;
-        i = j;
-      }
-      if (any_shared && frequency_order) {
-        auto freq = [&](int32_t col) {
-          const int32_t f = ucnt[std::lower_bound(ucol.begin(), ucol.end(), col) - ucol.begin()];
-          return f >= kSharedLanes ? f : 0;
-        };
-        for (int l = 0; l < 32; ++l)
-          std::stable_sort(lanes[l].begin(), lanes[l].end(), [&](const Entry& x, const Entry& y) {
-            return freq(x.col) > freq(y.col);   // stable: ascending column inside a frequency
-          });
-      }
-      for (int32_t p = 0; p < len[s]; ++p) {
-        int32_t fill = (int32_t)std::min<int64_t>(s * 64, std::max<int64_t>(nl - 1, 0));
+      for (int32_t p = 0; p < D.ng; ++p) {
+        int32_t fill = (int32_t)std::min<int64_t>(D.row0, std::max<int64_t>(nl - 1, 0));
         for (int l = 0; l < 32; ++l)
           if (p < (int32_t)lanes[l].size()) {
             fill = lanes[l][p].col;
@@ -694,26 +785,49 @@ void build_p2(HostPlan& P, const std::vector<uint8_t>& is_boundary32,
         for (int l = 0; l < 32; ++l) {
           const bool on = p < (int32_t)lanes[l].size();
           if (on) fill = lanes[l][p].col;
+          if (fill >= nl) boundary[s] = 1;
           c[(int64_t)p * 32 + l] = fill;
           v[((int64_t)p * 32 + l) * 2] = on ? lanes[l][p].a : 0.0;
           v[((int64_t)p * 32 + l) * 2 + 1] = on ? lanes[l][p].b : 0.0;
         }
       }
+      if (D.nd > 0) {  // dense section: the block's columns once, a value pair per lane
+        const int32_t b = specs[s].block;
+        const std::vector<int32_t>& mem = blocks->members[b];   // old ids, ascending
+        int32_t* dc = P.p2_dcol.data() + D.dpos;
+        double* dv = P.p2_dval.data() + D.dpos * 64;
+        for (int32_t j = 0; j < D.nd; ++j) dc[j] = P.iperm[mem[j]];
+        for (int32_t r = 0; r < D.nrows; ++r) {
+          const int64_t row = D.row0 + r;
+          const int64_t s32 = row / kPlanSliceRows, l32 = row % kPlanSliceRows;
+          const int64_t base = P.slice_ptr[s32] + l32;
+          for (int32_t p = 0; p < P.row_len[row]; ++p) {
+            const int64_t e = base + (int64_t)p * kPlanSliceRows;
+            if (!(*skip)[e]) continue;
+            const int32_t old_col = P.perm[P.col[e]];
+            const int32_t j = (int32_t)(std::lower_bound(mem.begin(), mem.end(), old_col) - mem.begin());
+            dv[((int64_t)j * 32 + r / 2) * 2 + (r & 1)] = P.val[e];
+            ++dense_fill[t];
+          }
+        }
+      }
     }
   });
-  // interior / boundary: a 64-row slice covers two 32-row slices
+  P.p2_dense_entries = 0;
+  for (int64_t f : dense_fill) P.p2_dense_entries += f;
   P.p2_interior.clear();
   P.p2_boundary.clear();
-  std::vector<int32_t> all(ns);
+  std::vector<int32_t> all(ns), cost(ns);
   for (int64_t s = 0; s < ns; ++s) {
     all[s] = (int32_t)s;
-    const bool b = is_boundary32[2 * s] || (2 * s + 1 < (int64_t)is_boundary32.size() && is_boundary32[2 * s + 1]);
-    (b ? P.p2_boundary : P.p2_interior).push_back((int32_t)s);
+    (boundary[s] ? P.p2_boundary : P.p2_interior).push_back((int32_t)s);
+    // a dense position costs the kernel about 0.4 general ones
+    cost[s] = P.p2_desc[s].ng + (2 * P.p2_desc[s].nd + 4) / 5;
   }
-  choose_task_target(len);
-  P.p2_tasks_all = build_tasks(all, len);
-  P.p2_tasks_interior = build_tasks(P.p2_interior, len);
-  P.p2_tasks_boundary = build_tasks(P.p2_boundary, len);
+  choose_task_target(cost);
+  P.p2_tasks_all = build_tasks(all, cost);
+  P.p2_tasks_interior = build_tasks(P.p2_interior, cost);
+  P.p2_tasks_boundary = build_tasks(P.p2_boundary, cost);
 }
 
 struct PhaseTimer {  // FLZ_TRACE=1: phase timings of build_plan on stderr
@@ -943,140 +1057,95 @@ HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<in
     const char* e = std::getenv("FLZ_P2");
     return !(e && e[0] == '0');
   }();
-  std::vector<int32_t> pair_key, pair_ulen;
-  {
-    int32_t longest = 0;
-    for (int64_t i = 0; i < nl; ++i) longest = std::max(longest, len[i]);
-    if (want_p2_sort && !P.split && longest > 24) {
-      pair_key.assign(nl, 0);
-      pair_ulen.assign(nl, 0);
-      for (int64_t i = 0; i < nl; i += 2) {
-        int64_t a = row_ptr[i], a1 = row_ptr[i + 1];
-        int64_t b = i + 1 < nl ? row_ptr[i + 1] : 0, b1 = i + 1 < nl ? row_ptr[i + 2] : 0;
-        int32_t u = 0;
-        while (a < a1 || b < b1) {
-          if (b == b1 || (a < a1 && col_idx[a] < col_idx[b])) ++a;
-          else if (a == a1 || col_idx[b] < col_idx[a]) ++b;
-          else {
-            ++a;
-            ++b;
-          }
-          ++u;
-        }
-        pair_key[i] = (u + 1) / 2;
-        if (i + 1 < nl) pair_key[i + 1] = (u + 1) / 2;
-        pair_ulen[i] = u;
+  static const bool want_dense = [] {   // FLZ_P2_DENSE=0: no dense sections (experiments)
+    const char* e = std::getenv("FLZ_P2_DENSE");
+    return !(e && e[0] == '0');
+  }();
+  int32_t longest = 0;
+  for (int64_t i = 0; i < nl; ++i) longest = std::max(longest, len[i]);
+  const bool p2_candidate = want_p2_sort && !P.split && longest > 24 && nl > 0;
+  // size of the union of the (global, ascending) column lists of two local rows
+  auto union_size = [&](int64_t i, int64_t j) {
+    int64_t a = row_ptr[i], a1 = row_ptr[i + 1], b = row_ptr[j], b1 = row_ptr[j + 1];
+    int32_t u = 0;
+    while (a < a1 || b < b1) {
+      if (b == b1 || (a < a1 && col_idx[a] < col_idx[b])) ++a;
+      else if (a == a1 || col_idx[b] < col_idx[a]) ++b;
+      else {
+        ++a;
+        ++b;
       }
+      ++u;
+    }
+    return u;
+  };
+  std::vector<int32_t> pair_key;
+  DenseBlocks blocks;
+  std::vector<int32_t> block_order;   // new -> old when dense blocks order the rows
+  std::vector<P2Spec> specs;
+  if (p2_candidate && want_dense && sigma <= 0)
+    blocks = extract_dense_blocks(nl, P.row_begin, row_ptr, col_idx, len, P.nnz);
+  timer.lap("dense blocks");
+  if (blocks.any()) {
+    // row order: rows in several blocks (all entries general, longest first), then block by
+    // block the rows that belong to that block only, then the rows outside every block in
+    // natural order, pairs sorted by length class inside windows.  A slice never straddles
+    // two of these groups.
+    block_order.reserve(nl);
+    auto emit = [&](const std::vector<int32_t>& rows, int32_t block) {
+      for (size_t i = 0; i < rows.size(); i += 64) {
+        const int32_t cnt = (int32_t)std::min<size_t>(64, rows.size() - i);
+        specs.push_back({(int32_t)block_order.size(), cnt, block});
+        block_order.insert(block_order.end(), rows.begin() + i, rows.begin() + i + cnt);
+      }
+    };
+    std::vector<int32_t> rows;
+    for (int64_t i = 0; i < nl; ++i)
+      if (blocks.count[i] >= 2) rows.push_back((int32_t)i);
+    std::stable_sort(rows.begin(), rows.end(), [&](int32_t a, int32_t b) {
+      return length_class(len[a]) > length_class(len[b]);
+    });
+    emit(rows, -1);
+    for (size_t b = 0; b < blocks.members.size(); ++b) {
+      rows.clear();
+      for (int32_t j : blocks.members[b])
+        if (blocks.primary[j] == (int32_t)b) rows.push_back(j);
+      emit(rows, (int32_t)b);
+    }
+    rows.clear();
+    for (int64_t i = 0; i < nl; ++i)
+      if (blocks.count[i] == 0) rows.push_back((int32_t)i);
+    const int64_t npairs = ((int64_t)rows.size() + 1) / 2;
+    std::vector<int32_t> cls(npairs), pairs(npairs);
+    for (int64_t q = 0; q < npairs; ++q) {
+      pairs[q] = (int32_t)q;
+      const bool lone = 2 * q + 1 >= (int64_t)rows.size();
+      cls[q] = length_class(lone ? len[rows[2 * q]] : (union_size(rows[2 * q], rows[2 * q + 1]) + 1) / 2);
+    }
+    const int64_t window = 8192, whole = (int64_t)rows.size() / 2;   // a lone last row stays last
+    for (int64_t w0 = 0; w0 < whole; w0 += window)
+      std::stable_sort(pairs.begin() + w0, pairs.begin() + std::min(whole, w0 + window),
+                       [&](int32_t a, int32_t b) { return cls[a] > cls[b]; });
+    std::vector<int32_t> sorted;
+    sorted.reserve(rows.size());
+    for (int32_t q : pairs) {
+      sorted.push_back(rows[2 * q]);
+      if (2 * (int64_t)q + 1 < (int64_t)rows.size()) sorted.push_back(rows[2 * q + 1]);
+    }
+    emit(sorted, -1);
+    if (std::getenv("FLZ_TRACE"))
+      std::fprintf(stderr, "[flz]   plan dense blocks: %zu blocks cover %lld of %lld entries, "
+                           "%zu slices\n", blocks.members.size(), (long long)blocks.covered_entries,
+                   (long long)P.nnz, specs.size());
+  } else if (p2_candidate) {
+    pair_key.assign(nl, 0);
+    for (int64_t i = 0; i < nl; i += 2) {
+      const int32_t u = i + 1 < nl ? union_size(i, i + 1) : len[i];
+      pair_key[i] = (u + 1) / 2;
+      if (i + 1 < nl) pair_key[i + 1] = (u + 1) / 2;
     }
   }
   const std::vector<int32_t>* sort_key = pair_key.empty() ? nullptr : &pair_key;
-  // ---- clustered order for dense blocks (PARSEC non-local projectors: a ball of grid points
-  // coupled all-to-all).  Rows much longer than the median are "long"; a long pair's cluster is
-  // the min-hash of its long COLUMNS (columns whose own row is long: the block's members, not
-  // the stencil neighbours), so the rows of one dense block meet in one cluster.  Long pairs are
-  // sorted by (cluster, length class, row), short pairs keep the window sort.  With the lanes
-  // of a slice inside one block, build_p2 lines the block's columns up across the lanes and a
-  // warp-level gather touches ONE line instead of ~20 (scripts/analysis/p2_lines.py).
-  std::vector<int32_t> cluster_perm;
-  // Measured on B200 (PARSEC-shaped n = 113k): lines per gather 18.8 -> 12.8, time per step
-  // unchanged (28.2 vs 28.3 us): the kernel is bound by the BYTES a gather returns through the
-  // LSU data pipe (32 B per lane = 16 wavefronts even when every lane reads the same line),
-  // not by the lines it touches.  The order is therefore opt-in (FLZ_P2_CLUSTER=1): it is the
-  // groundwork for a kernel that stages a block's rows in shared memory once per slice.
-  static const bool want_cluster = [] {
-    const char* e = std::getenv("FLZ_P2_CLUSTER");
-    return e && e[0] == '1';
-  }();
-  if (sort_key && want_cluster && nl >= 4096) {
-    std::vector<int32_t> tmp(len);
-    std::nth_element(tmp.begin(), tmp.begin() + nl / 2, tmp.end());
-    const int32_t long_min = std::max<int32_t>(48, tmp[nl / 2] + tmp[nl / 2] / 2);
-    std::vector<uint8_t> is_long(nl, 0);
-    int64_t long_entries = 0;
-    for (int64_t i = 0; i < nl; ++i)
-      if (len[i] > long_min) {
-        is_long[i] = 1;
-        long_entries += len[i];
-      }
-    if (5 * long_entries >= P.nnz) {
-      const int64_t npairs = (nl + 1) / 2;
-      auto mix = [](int64_t c) { return ((uint64_t)c * 0x9E3779B97F4A7C15ull) >> 20; };
-      std::vector<int64_t> key(npairs, -1);
-      const int kc = (int)std::max<int64_t>(1, std::min<int64_t>(worker_count(), npairs / 1024));
-      run_chunks(kc, [&](int t) {
-        for (int64_t q = npairs * t / kc; q < npairs * (t + 1) / kc; ++q) {
-          const int64_t i0 = 2 * q, i1 = std::min(nl, i0 + 2);
-          bool any_long = false;
-          for (int64_t i = i0; i < i1; ++i) any_long = any_long || is_long[i];
-          if (!any_long) continue;
-          uint64_t best = ~0ull;
-          int64_t arg = -1;
-          for (int64_t i = i0; i < i1; ++i)
-            for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
-              const int64_t c = (int64_t)col_idx[e] - P.row_begin;
-              if (c < 0 || c >= nl || !is_long[c]) continue;
-              const uint64_t hsh = mix(c);
-              if (hsh < best) {
-                best = hsh;
-                arg = c;
-              }
-            }
-          key[q] = arg;
-        }
-      });
-      std::vector<int32_t> long_pairs, short_pairs;
-      const bool odd = nl % 2 != 0;  // the lone last row stays last: pairs keep even positions
-      for (int64_t q = 0; q < npairs - (odd ? 1 : 0); ++q)
-        (key[q] >= 0 ? long_pairs : short_pairs).push_back((int32_t)q);
-      std::vector<int32_t> cls(npairs);
-      for (int64_t q = 0; q < npairs; ++q) cls[q] = length_class(pair_key[2 * q]);
-      std::sort(long_pairs.begin(), long_pairs.end(), [&](int32_t a, int32_t b) {
-        if (key[a] != key[b]) return key[a] < key[b];
-        if (cls[a] != cls[b]) return cls[a] > cls[b];
-        return a < b;
-      });
-      // every second cluster runs shortest-first: a slice that straddles two clusters then
-      // holds the short ends (or the long ends) of both, which pads less
-      for (size_t i = 0, k = 0; i < long_pairs.size(); ++k) {
-        size_t j = i;
-        while (j < long_pairs.size() && key[long_pairs[j]] == key[long_pairs[i]]) ++j;
-        if (k % 2 == 1) std::reverse(long_pairs.begin() + i, long_pairs.begin() + j);
-        i = j;
-      }
-      const int64_t window = 8192;  // pairs (= the 16384-row window of the unclustered sort)
-      for (size_t w0 = 0; w0 < short_pairs.size(); w0 += window)
-        std::stable_sort(short_pairs.begin() + w0,
-                         short_pairs.begin() + std::min(short_pairs.size(), w0 + (size_t)window),
-                         [&](int32_t a, int32_t b) { return cls[a] > cls[b]; });
-      std::vector<int32_t> order(long_pairs);
-      order.insert(order.end(), short_pairs.begin(), short_pairs.end());
-      if (odd) order.push_back((int32_t)(npairs - 1));
-      // padded positions of this order against the window sort: clusters of unrelated long rows
-      // (no block structure) would only add padding
-      auto padded = [&](auto&& pair_at) {
-        int64_t total = 0;
-        for (int64_t s = 0; s < npairs; s += 32) {
-          int32_t mx = 0;
-          for (int64_t l = s; l < std::min(npairs, s + 32); ++l) mx = std::max(mx, pair_ulen[2 * pair_at(l)]);
-          total += mx;
-        }
-        return total;
-      };
-      sort_windows(len, 16384, P.perm, sort_key);
-      const int64_t base = padded([&](int64_t l) { return (int64_t)(P.perm[2 * l] / 2); });
-      const int64_t clustered = padded([&](int64_t l) { return (int64_t)order[l]; });
-      if (std::getenv("FLZ_TRACE"))
-        std::fprintf(stderr, "[flz]   plan clusters: %zu long pairs, positions %lld clustered vs %lld window-sorted\n",
-                     long_pairs.size(), (long long)clustered, (long long)base);
-      if ((double)clustered <= 1.1 * (double)base && long_pairs.size() >= 64) {
-        cluster_perm.reserve(nl);
-        for (int32_t q : order) {
-          cluster_perm.push_back(2 * q);
-          if (2 * (int64_t)q + 1 < nl) cluster_perm.push_back(2 * q + 1);
-        }
-      }
-    }
-  }
 
   // ---- sigma: smallest window whose padding overhead is <= 8 %
   int64_t chosen = sigma;
@@ -1102,9 +1171,8 @@ HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<in
       }
     }
   }
-  const bool clustered_order = !cluster_perm.empty() && sigma <= 0;
-  if (clustered_order) {
-    P.perm = cluster_perm;
+  if (blocks.any()) {
+    P.perm = block_order;
     chosen = std::max<int64_t>(nl, 2);
   } else {
     sort_windows(len, chosen, P.perm, sort_key);
@@ -1161,6 +1229,9 @@ HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<in
   P.col.assign(std::max<int64_t>(P.stored, 1), 0);
   P.val.assign(std::max<int64_t>(P.stored, 1), 0.0);
   std::vector<uint8_t> is_boundary(nslices, 0);
+  // entries the dense sections of the paired layout hold (rows that belong to one block only)
+  std::vector<uint8_t> skip;
+  if (blocks.any()) skip.assign(std::max<int64_t>(P.stored, 1), 0);
   const int fill_chunks = (int)std::max<int64_t>(1, std::min<int64_t>(worker_count(), nslices / 256));
   run_chunks(fill_chunks, [&](int t) {
   for (int64_t s = nslices * t / fill_chunks; s < nslices * (t + 1) / fill_chunks; ++s)
@@ -1183,6 +1254,8 @@ HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<in
           }
           P.col[base + (int64_t)cnt * kPlanSliceRows] = c;
           P.val[base + (int64_t)cnt * kPlanSliceRows] = values[p];
+          if (!skip.empty() && blocks.covered[p - p0] && blocks.count[iold] == 1)
+            skip[base + (int64_t)cnt * kPlanSliceRows] = 1;
         }
       }
       for (; cnt < P.slice_len[s]; ++cnt) {  // padding: zero value, harmless in-range column
@@ -1207,7 +1280,7 @@ HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<in
   {
     int32_t longest_slice = 0;
     for (int64_t s = 0; s < nslices; ++s) longest_slice = std::max(longest_slice, P.slice_len[s]);
-    P.ug_skipped = want_p2 && !P.split && nl > 0 && !pair_ulen.empty() && longest_slice > 256 &&
+    P.ug_skipped = want_p2 && !P.split && nl > 0 && p2_candidate && (longest_slice > 256 || blocks.any()) &&
                    std::getenv("FLZ_K1_T") == nullptr && std::getenv("FLZ_UG_ALWAYS") == nullptr;
   }
   if (P.ug_skipped) {
@@ -1218,8 +1291,16 @@ HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<in
   }
   timer.lap("UG layout");
   // long ragged rows: the paired layout feeds the fast kernel (FLZ_P2=0 keeps the UG tasks)
-  P.p2 = want_p2 && !P.split && !P.lean && nl > 0 && !pair_ulen.empty();
-  if (P.p2) build_p2(P, is_boundary, pair_ulen, clustered_order);
+  P.p2 = want_p2 && !P.split && !P.lean && nl > 0 && p2_candidate;
+  if (P.p2) {
+    if (!blocks.any()) {
+      specs.clear();
+      for (int64_t r0 = 0; r0 < nl; r0 += 64)
+        specs.push_back({(int32_t)r0, (int32_t)std::min<int64_t>(64, nl - r0), -1});
+    }
+    P.p2_blocks = (int64_t)blocks.members.size();
+    build_p2(P, specs, blocks.any() ? &skip : nullptr, blocks.any() ? &blocks : nullptr);
+  }
   timer.lap("paired layout");
   P.uv_pairs.clear();
   if (P.lean) {

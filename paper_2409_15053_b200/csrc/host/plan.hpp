@@ -61,6 +61,15 @@ struct PlanStencilTiles {
   int32_t own_e = 0;     // staged element of offset 0 (the tile's own rows)
 };
 
+// Slice descriptor of the paired layout (mirrors P2Slice, flz_internal.hpp): general positions
+// [gpos, gpos + ng) of p2_col / p2_val, dense positions [dpos, dpos + nd) of p2_dcol / p2_dval,
+// rows [row0, row0 + nrows), nrows <= 64.
+struct PlanP2Slice {
+  int64_t gpos, dpos;
+  int32_t ng, nd;
+  int32_t row0, nrows;
+};
+
 struct HostPlan {
   // partition
   int rank = 0, nranks = 1;
@@ -102,21 +111,35 @@ struct HostPlan {
   std::vector<int32_t> rest_rows;                    // [nrest * 32]
   std::vector<int32_t> rest_interior, rest_boundary; // slice ids (>= nslices)
   std::vector<PlanTask> tasks_rest_all, tasks_rest_interior, tasks_rest_boundary;
-  // PAIRED layout ("P2") for matrices with long ragged rows (not SPLIT, not lean): slices of
-  // 64 consecutive rows, lane l owns the ADJACENT rows 64 s + 2 l and + 1, and a position
-  // holds one column and TWO values (one per row, zero where a row lacks the entry).  The
-  // columns of a lane are the sorted union of its two rows' columns: neighbouring rows of the
-  // same dense block share almost all of them, so one 32-byte gather serves two matrix
-  // entries — the gathers, not HBM, bound this kernel.  p2_ptr[s] = first position
-  // of slice s (positions are [32 lanes] columns and [32 lanes][2] values).
+  // PAIRED layout ("P2") for matrices with long ragged rows (not SPLIT, not lean): slices of up
+  // to 64 consecutive rows, lane l owns the ADJACENT rows row0 + 2 l and + 1, and a GENERAL
+  // position holds one column and TWO values (one per row, zero where a row lacks the entry).
+  // The columns of a lane are the sorted union of its two rows' columns: neighbouring rows
+  // share many of them, so one 32-byte gather serves two matrix entries.
+  //
+  // DENSE sections.  Long rows of PARSEC-like Hamiltonians come from dense blocks (a ball of
+  // grid points coupled all-to-all by a non-local projector).  extract_dense_blocks() finds
+  // those near-cliques in the CSR structure; the rows that belong to exactly ONE block are
+  // ordered block by block, a slice never straddles two blocks, and the slice stores the
+  // block's columns ONCE (p2_dcol, shared by all lanes) with a value pair per lane and column
+  // (p2_dval, zero where the entry is absent).  The kernel stages the gathered rows of 32
+  // dense columns in shared memory and broadcasts them: a dense position costs the LSU ~10
+  // wavefronts instead of ~30 for a general one and 8 bytes per entry instead of 10-20.
+  // Rows in no block follow in (length-sorted) natural order; rows in several blocks keep all
+  // their entries as general positions.  p2_desc[s] describes slice s; p2_ptr[s] repeats gpos.
   bool p2 = false;
   int64_t p2_slices = 0;
-  std::vector<int64_t> p2_ptr;                  // [p2_slices + 1]
-  std::vector<int32_t> p2_col;                  // [positions * 32]
-  std::vector<double> p2_val;                   // [positions * 64]
+  std::vector<PlanP2Slice> p2_desc;             // [p2_slices]
+  std::vector<int64_t> p2_ptr;                  // [p2_slices + 1] first general position
+  std::vector<int32_t> p2_col;                  // [general positions * 32]
+  std::vector<double> p2_val;                   // [general positions * 64]
+  std::vector<int32_t> p2_dcol;                 // [dense positions]
+  std::vector<double> p2_dval;                  // [dense positions * 64]
   std::vector<int32_t> p2_interior, p2_boundary;
   std::vector<PlanTask> p2_tasks_all, p2_tasks_interior, p2_tasks_boundary;
-  int64_t p2_entries = 0;                       // positions * 32 (gathers per product)
+  int64_t p2_entries = 0;                       // general positions * 32 (gathers per product)
+  int64_t p2_blocks = 0;                        // dense blocks found
+  int64_t p2_dense_entries = 0;                 // true nonzeros stored in dense sections
   // halo: sorted unique remote global columns; slot h lives at row nl + h of a gather source
   std::vector<int64_t> halo;
   std::vector<int64_t> need_off, need_cnt;  // per owner rank: run of `halo` it must send us

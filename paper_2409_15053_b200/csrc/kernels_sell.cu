@@ -41,9 +41,6 @@ constexpr int kWarpsPerBlock = 4;
 #ifndef FLZ_K1_BATCH
 #define FLZ_K1_BATCH 4
 #endif
-#ifndef FLZ_K1_P2_STAGES
-#define FLZ_K1_P2_STAGES 3
-#endif
 constexpr int kBatch = FLZ_K1_BATCH;  // matrix entries per row requested per pipeline stage
 
 // Programmatic dependent launch: consecutive Clenshaw steps depend on each other through Y1/Y2
@@ -636,12 +633,15 @@ __global__ void __launch_bounds__(kTaskWarps * 32, FLZ_K1_TASK_CTAS)
   }
 }
 
-// Paired layout (host/plan.hpp): slices of 64 rows, lane l owns the adjacent rows 2l and
-// 2l+1 of the slice; a position is one column and two values.  One gathered block row feeds
-// two rows of the product: on the PARSEC-shaped matrices, where neighbouring rows of a dense
-// non-local block share their columns, this needs 25 % fewer gathers than entries — and the
-// gathers (L1 wavefronts), not HBM, bound this kernel.  Task list and multi-warp split as in
-// clenshaw_step_ug_tasks.
+// Paired layout (host/plan.hpp): slices of up to 64 rows, lane l owns the adjacent rows
+// row0 + 2l and + 1.  GENERAL positions: one column per lane and two values; one gathered block
+// row feeds two rows of the product.  DENSE positions (rows of one dense block, host/plan.hpp):
+// the column is shared by the whole slice, so a warp gathers the block rows of 32 dense
+// columns at once (one 32-byte gather per LANE instead of per lane and position), parks them
+// in its own shared-memory strip and every position then costs a broadcast shared load plus
+// the coalesced 512-byte value stream — about a third of the LSU wavefronts of a general
+// position.  Task list and multi-warp split as in clenshaw_step_ug_tasks: the W warps of a
+// slice share its general AND its dense positions evenly.
 template <int R, int S, int MODE>
 __global__ void __launch_bounds__(kTaskWarps * 32, FLZ_K1_TASK_CTAS)
     clenshaw_step_p2_tasks(SellView A, double s1, double s2, double b,
@@ -649,6 +649,7 @@ __global__ void __launch_bounds__(kTaskWarps * 32, FLZ_K1_TASK_CTAS)
                            const double* __restrict__ X, int64_t ldx, double* __restrict__ Out,
                            int64_t ldo) {
   __shared__ double part[kTaskWarps][2 * R][32];
+  __shared__ __align__(16) double strip[kTaskWarps][32][4];   // gathered rows of 32 dense columns
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   pdl_launch_dependents();
   const SliceTask task = A.tasks[blockIdx.x];
@@ -659,15 +660,23 @@ __global__ void __launch_bounds__(kTaskWarps * 32, FLZ_K1_TASK_CTAS)
 #pragma unroll
   for (int k = 0; k < R; ++k) acc[0][k] = acc[1][k] = 0.0;
   int64_t row = 0;
+  int row_end = 0;
   if (active) {
-    const int64_t slice = task.slice[sub];
-    row = slice * 64 + 2 * lane;
-    const int64_t pos0 = __ldg(A.p2_ptr + slice);
-    const int L = (int)(__ldg(A.p2_ptr + slice + 1) - pos0);
-    const int chunk = (((L + W - 1) / W) + kBatch - 1) / kBatch * kBatch;
-    const int p0 = piece * chunk, p1 = min(L, p0 + chunk);
-    const int32_t* __restrict__ col = A.p2_col + (pos0 + p0) * 32 + lane;
-    const double* __restrict__ val = A.p2_val + ((pos0 + p0) * 32 + lane) * 2;
+    const int4* hp = reinterpret_cast<const int4*>(A.p2_desc + task.slice[sub]);
+    const int4 h0 = __ldg(hp), h1 = __ldg(hp + 1);
+    const int64_t gpos = ((int64_t)(uint32_t)h0.y << 32) | (uint32_t)h0.x;
+    const int64_t dpos = ((int64_t)(uint32_t)h0.w << 32) | (uint32_t)h0.z;
+    const int ng = h1.x, nd = h1.y;
+    row = (int64_t)h1.z + 2 * lane;
+    row_end = h1.z + h1.w;
+    const int chunk = (((ng + W - 1) / W) + kBatch - 1) / kBatch * kBatch;
+    const int p0 = piece * chunk, p1 = min(ng, p0 + chunk);
+    const int dchunk = (((nd + W - 1) / W) + 31) / 32 * 32;
+    const int d0 = min(nd, piece * dchunk), d1 = min(nd, d0 + dchunk);
+    const int32_t* __restrict__ col = A.p2_col + (gpos + p0) * 32 + lane;
+    const double* __restrict__ val = A.p2_val + ((gpos + p0) * 32 + lane) * 2;
+    const int32_t* __restrict__ dcol = A.p2_dcol + dpos;
+    const double* __restrict__ dval = A.p2_dval + (dpos * 32 + lane) * 2;
     pdl_wait();
     for (int p = p0; p < p1; p += kBatch) {
       int c[kBatch];
@@ -693,6 +702,55 @@ __global__ void __launch_bounds__(kTaskWarps * 32, FLZ_K1_TASK_CTAS)
       col += kBatch * 32;
       val += kBatch * 64;
     }
+    // dense section: 32 columns per round
+    double (*mine)[4] = strip[warp];
+    for (int q = d0; q < d1; q += 32) {
+      const int cnt = min(32, d1 - q);
+      const double* __restrict__ v = dval + (int64_t)q * 64;
+      // the first value pairs are requested before the gather they do not depend on
+      double va[4], vb[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        va[u] = vb[u] = 0.0;
+        if (u < cnt)
+          asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];"
+                       : "=d"(va[u]), "=d"(vb[u]) : "l"(v + u * 64));
+      }
+      double g[R];
+      const int c = lane < cnt ? ld_stream_s32(dcol + q + lane) : 0;
+      gather_row<R, S>(Y1, ldy, c, lane < cnt, g);
+      __syncwarp();                      // the previous round's reads of the strip are done
+#pragma unroll
+      for (int k = 0; k < R; ++k) mine[lane][k] = g[k];
+      __syncwarp();
+      for (int j = 0; j < cnt; j += 4) {
+        double na[4], nb[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {    // next batch in flight while this one is consumed
+          na[u] = nb[u] = 0.0;
+          if (j + 4 + u < cnt)
+            asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];"
+                         : "=d"(na[u]), "=d"(nb[u]) : "l"(v + (j + 4 + u) * 64));
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int jj = min(j + u, 31);  // past cnt: zero values times a staged (finite) row
+#pragma unroll
+          for (int k = 0; k < R; ++k) {
+            const double y = mine[jj][k];
+            acc[0][k] = fma(va[u], y, acc[0][k]);
+            acc[1][k] = fma(vb[u], y, acc[1][k]);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          va[u] = na[u];
+          vb[u] = nb[u];
+        }
+      }
+    }
+  } else {
+    pdl_wait();
   }
   if (W > 1) {  // uniform across the CTA
     if (active && piece > 0) {
@@ -716,26 +774,14 @@ __global__ void __launch_bounds__(kTaskWarps * 32, FLZ_K1_TASK_CTAS)
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const int64_t r = row + h;
-    if (r >= A.nl) break;
+    if (r >= row_end) break;
     double y1o[R], y2o[R], xo[R];
     load_own<R, S, MODE>(A, r, Y1, Y2, ldy, X, ldx, y1o, y2o, xo);
     finish_row<R, S, MODE>(r, s1, s2, b, acc[h], y1o, y2o, xo, Y2, ldy, Out, ldo);
   }
 }
 
-// ---- paired layout, matrix stream staged by the TMA --------------------------------------
-// The (column, value pair) stream of a slice is contiguous per position (128 B of columns,
-// 512 B of values), so a warp's share of it moves global -> shared memory as bulk copies
-// (cp.async.bulk + mbarrier complete_tx) issued by one lane, kP2Stages batches ahead of the
-// lanes that consume it.  The stream then costs the LSU data pipe 5 shared-memory wavefronts
-// per position instead of 10 global ones (the gathers keep their 16), needs no registers
-// while in flight, and the first batches are requested before the previous Clenshaw step has
-// finished (programmatic dependent launch: the matrix never changes).
-constexpr int kP2Stages = FLZ_K1_P2_STAGES;
-constexpr int kP2StageBytes = kBatch * (32 * 16 + 32 * 4);       // values then columns
-constexpr int kP2WarpBytes = kP2Stages * kP2StageBytes + 64;      // + mbarriers (8 B each)
-constexpr int kP2SmemBytes = kTaskWarps * kP2WarpBytes;
-
+// ---- mbarrier / bulk-copy (TMA) primitives
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
@@ -771,115 +817,6 @@ __device__ __forceinline__ void bulk_g2s_hint(uint32_t dst, const void* src, uin
       "[%0], [%1], %2, [%3], %4;"
       ::"r"(dst), "l"(src), "r"(bytes), "r"(bar), "l"(policy) : "memory");
 }
-
-template <int R, int S, int MODE>
-__global__ void __launch_bounds__(kTaskWarps * 32, FLZ_K1_TASK_CTAS)
-    clenshaw_step_p2_tma(SellView A, double s1, double s2, double b,
-                         const double* __restrict__ Y1, double* __restrict__ Y2, int64_t ldy,
-                         const double* __restrict__ X, int64_t ldx, double* __restrict__ Out,
-                         int64_t ldo) {
-  extern __shared__ __align__(128) unsigned char p2_smem[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  pdl_launch_dependents();
-  unsigned char* ring = p2_smem + warp * kP2WarpBytes;
-  const uint32_t ring_s = smem_addr(ring);
-  const uint32_t bars = ring_s + kP2Stages * kP2StageBytes;
-  const SliceTask task = A.tasks[blockIdx.x];
-  const int W = task.warps_per_slice;
-  const int sub = warp / W, piece = warp - sub * W;
-  const bool active = sub < task.count;
-  double acc[2][R];
-#pragma unroll
-  for (int k = 0; k < R; ++k) acc[0][k] = acc[1][k] = 0.0;
-  int64_t row = 0;
-  if (active) {
-    const int64_t slice = task.slice[sub];
-    row = slice * 64 + 2 * lane;
-    const int64_t pos0 = __ldg(A.p2_ptr + slice);
-    const int L = (int)(__ldg(A.p2_ptr + slice + 1) - pos0);
-    const int chunk = (((L + W - 1) / W) + kBatch - 1) / kBatch * kBatch;
-    const int p0 = piece * chunk, p1 = min(L, p0 + chunk);
-    const int nbatch = p1 > p0 ? (p1 - p0 + kBatch - 1) / kBatch : 0;
-    const int32_t* __restrict__ col = A.p2_col + (pos0 + p0) * 32;
-    const double* __restrict__ val = A.p2_val + (pos0 + p0) * 64;
-    auto request = [&](int k) {  // lane 0: batch k -> stage k % kP2Stages
-      const int stage = k % kP2Stages;
-      const int npos = min(kBatch, p1 - p0 - k * kBatch);
-      const uint32_t dst = ring_s + stage * kP2StageBytes;
-      const uint32_t bar = bars + stage * 8;
-      mbar_expect_tx(bar, (uint32_t)npos * (512 + 128));
-      bulk_g2s(dst, val + (int64_t)k * kBatch * 64, (uint32_t)npos * 512, bar);
-      bulk_g2s(dst + kBatch * 512, col + (int64_t)k * kBatch * 32, (uint32_t)npos * 128, bar);
-    };
-    if (lane == 0) {
-      for (int st = 0; st < kP2Stages; ++st) mbar_init(bars + st * 8, 1);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      for (int k = 0; k < min(nbatch, kP2Stages); ++k) request(k);
-    }
-    __syncwarp();
-    pdl_wait();
-    for (int k = 0; k < nbatch; ++k) {
-      const int stage = k % kP2Stages;
-      mbar_wait(bars + stage * 8, (uint32_t)(k / kP2Stages) & 1u);
-      const double2* sv = reinterpret_cast<const double2*>(ring + stage * kP2StageBytes) + lane;
-      const int* sc = reinterpret_cast<const int*>(ring + stage * kP2StageBytes + kBatch * 512) + lane;
-      const int left = p1 - p0 - k * kBatch;
-      int c[kBatch];
-      double va[kBatch], vb[kBatch], g[kBatch][R];
-#pragma unroll
-      for (int u = 0; u < kBatch; ++u) {
-        const bool ok = u < left;
-        c[u] = ok ? sc[u * 32] : 0;
-        const double2 v = ok ? sv[u * 32] : make_double2(0.0, 0.0);
-        va[u] = v.x;
-        vb[u] = v.y;
-      }
-#pragma unroll
-      for (int u = 0; u < kBatch; ++u) gather_row<R, S>(Y1, ldy, c[u], u < left, g[u]);
-#pragma unroll
-      for (int u = 0; u < kBatch; ++u)
-#pragma unroll
-        for (int k2 = 0; k2 < R; ++k2) {
-          acc[0][k2] = fma(va[u], g[u][k2], acc[0][k2]);
-          acc[1][k2] = fma(vb[u], g[u][k2], acc[1][k2]);
-        }
-      __syncwarp();  // every lane has consumed the stage (its values fed the FMAs above)
-      if (lane == 0 && k + kP2Stages < nbatch) request(k + kP2Stages);
-    }
-  }
-  if (W > 1) {  // uniform across the CTA; a warp's partial sums reuse its own (drained) ring
-    double* part = reinterpret_cast<double*>(ring);
-    if (active && piece > 0) {
-#pragma unroll
-      for (int k = 0; k < R; ++k) {
-        part[k * 32 + lane] = acc[0][k];
-        part[(R + k) * 32 + lane] = acc[1][k];
-      }
-    }
-    __syncthreads();
-    if (active && piece == 0) {
-      for (int q = 1; q < W; ++q) {
-        const double* other = reinterpret_cast<const double*>(ring + q * kP2WarpBytes);
-#pragma unroll
-        for (int k = 0; k < R; ++k) {
-          acc[0][k] += other[k * 32 + lane];
-          acc[1][k] += other[(R + k) * 32 + lane];
-        }
-      }
-    }
-  }
-  if (!active || piece != 0) return;
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int64_t r = row + h;
-    if (r >= A.nl) break;
-    double y1o[R], y2o[R], xo[R];
-    load_own<R, S, MODE>(A, r, Y1, Y2, ldy, X, ldx, y1o, y2o, xo);
-    finish_row<R, S, MODE>(r, s1, s2, b, acc[h], y1o, y2o, xo, Y2, ldy, Out, ldo);
-  }
-}
-
 
 // ------------------------------------------------------------ TMA-staged stencil kernel
 // Constant-coefficient stencils on one GPU, planar blocks (host/plan.hpp, PlanStencilTiles).
@@ -1515,27 +1452,8 @@ void launch_ug(flz_ctx* ctx, const SellView& A, double s1, double s2, double b, 
   if constexpr (MODE != 3) {
     if (A.p2) {
       if (A.ntasks == 0) return;
-      // FLZ_K1_TMA=1 selects the TMA-staged stream.  Measured slower on B200 (PARSEC-shaped
-      // n = 113k: 35.1 vs 28.2 us per step; n = 268k: 60.2 vs 54.6): 186 KB of rings per SM
-      // leave the gathers ~60 KB of L1, and a 4-position batch is too little work per
-      // mbarrier round trip.  Kept as a tested alternative (tests/test_gpu_variants.py).
-      static const bool tma = [] {
-        const char* e = std::getenv("FLZ_K1_TMA");
-        return e && e[0] == '1';
-      }();
-      if (tma) {
-        static const bool configured = [] {
-          FLZ_CUDA(cudaFuncSetAttribute(clenshaw_step_p2_tma<R, S, MODE>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, kP2SmemBytes));
-          return true;
-        }();
-        (void)configured;
-        launch_k1_smem(ctx, clenshaw_step_p2_tma<R, S, MODE>, (unsigned)A.ntasks, kTaskWarps * 32,
-                       (size_t)kP2SmemBytes, A, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo);
-      } else {
-        launch_k1(ctx, clenshaw_step_p2_tasks<R, S, MODE>, (unsigned)A.ntasks, kTaskWarps * 32, A,
-                  s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo);
-      }
+      launch_k1(ctx, clenshaw_step_p2_tasks<R, S, MODE>, (unsigned)A.ntasks, kTaskWarps * 32, A,
+                s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo);
       ctx->launches++;
       return;
     }

@@ -163,18 +163,25 @@ class HaloPlan:
         return (y[:nl], np.array(done, np.int64)) if which != "all" else y[:nl]
 
     def p2_arrays(self):
-        """Paired layout (64-row slices, two rows per lane), or None when the plan has none."""
-        sizes = np.zeros(4, np.int64)
+        """Paired layout (slices of up to 64 rows, two rows per lane, optional dense section
+        per slice), or None when the plan has none."""
+        sizes = np.zeros(8, np.int64)
         vp = lambda a: a.ctypes.data_as(C.c_void_p)
-        check(lib().flz_plan_p2(self.handle, vp(sizes), None, None, None))
+        check(lib().flz_plan_p2(self.handle, vp(sizes), None, None, None, None, None, None))
         if not sizes[0]:
             return None
-        ptr = np.zeros(int(sizes[1]) + 1, np.int64)
-        col = np.zeros(max(int(sizes[2]) * 32, 1), np.int32)
-        val = np.zeros(max(int(sizes[2]) * 64, 2), np.float64)
-        check(lib().flz_plan_p2(self.handle, vp(sizes), vp(ptr), vp(col), vp(val)))
-        return dict(ptr=ptr, col=col, val=val, slices=int(sizes[1]), positions=int(sizes[2]),
-                    interior=int(sizes[3]))
+        ns, npos, nd = int(sizes[1]), int(sizes[2]), int(sizes[4])
+        ptr = np.zeros(ns + 1, np.int64)
+        col = np.zeros(max(npos * 32, 1), np.int32)
+        val = np.zeros(max(npos * 64, 2), np.float64)
+        desc = np.zeros((max(ns, 1), 6), np.int64)
+        dcol = np.zeros(max(nd, 1), np.int32)
+        dval = np.zeros(max(nd * 64, 2), np.float64)
+        check(lib().flz_plan_p2(self.handle, vp(sizes), vp(ptr), vp(col), vp(val), vp(desc),
+                                vp(dcol), vp(dval)))
+        return dict(ptr=ptr, col=col, val=val, slices=ns, positions=npos, interior=int(sizes[3]),
+                    desc=desc[:ns], dcol=dcol[:nd], dval=dval[:nd * 64], dense_positions=nd,
+                    blocks=int(sizes[5]), dense_entries=int(sizes[6]))
 
     def tile_plan(self):
         """Tile plan of the TMA-staged stencil kernel (flz_plan_tiles), or None."""
@@ -251,21 +258,33 @@ class HaloPlan:
         return y[:nl]
 
     def p2_product(self, x):
-        """y = A x evaluated from the paired layout as the kernel walks it."""
+        """y = A x evaluated from the paired layout as clenshaw_step_p2_tasks walks it: the
+        general positions of a slice (one column, two values per lane), then its dense section
+        (one shared column per position, two values per lane)."""
         p2 = self.p2_arrays()
         nl = self.info["rows_local"]
-        y = np.zeros(p2["slices"] * 64)
+        y = np.full(nl, np.nan)
         lanes = np.arange(32)
         for s in range(p2["slices"]):
+            gpos, dpos, ng, nd, row0, nrows = (int(v) for v in p2["desc"][s])
+            assert gpos == int(p2["ptr"][s]) and 0 < nrows <= 64
             accA, accB = np.zeros(32), np.zeros(32)
-            for p in range(int(p2["ptr"][s]), int(p2["ptr"][s + 1])):
+            for p in range(gpos, gpos + ng):
                 g = x[p2["col"][p * 32: p * 32 + 32]]
                 v = p2["val"][p * 64: p * 64 + 64].reshape(32, 2)
                 accA += v[:, 0] * g
                 accB += v[:, 1] * g
-            y[s * 64 + 2 * lanes] = accA
-            y[s * 64 + 2 * lanes + 1] = accB
-        return y[:nl]
+            for p in range(dpos, dpos + nd):
+                v = p2["dval"][p * 64: p * 64 + 64].reshape(32, 2)
+                g = x[p2["dcol"][p]]
+                accA += v[:, 0] * g
+                accB += v[:, 1] * g
+            ra, rb = row0 + 2 * lanes, row0 + 2 * lanes + 1
+            assert np.all(np.isnan(y[ra[ra < row0 + nrows]]))     # every row in one slice only
+            y[ra[ra < row0 + nrows]] = accA[ra < row0 + nrows]
+            y[rb[rb < row0 + nrows]] = accB[rb < row0 + nrows]
+        assert not np.isnan(y).any()
+        return y
 
     def __del__(self):
         try:

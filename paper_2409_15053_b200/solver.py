@@ -83,7 +83,16 @@ class SparseSymMatrix:
         for the matrix, and the nonzeros held at uniform-offset positions."""
         mb, ue = C.c_int64(), C.c_int64()
         check(lib().flz_hostmatrix_layout(self.handle, C.byref(mb), C.byref(ue)))
-        return {"matrix_bytes": mb.value, "uniform_entries": ue.value}
+        out = {"matrix_bytes": mb.value, "uniform_entries": ue.value, "step_bytes": []}
+        info = (C.c_int64 * 4)()
+        name = C.create_string_buffer(96)
+        for r in (1, 2, 3, 4):   # bytes one fused step of r columns streams, and its kernel
+            check(lib().flz_hostmatrix_k1_info(self.handle, r, info, name, 96))
+            out["step_bytes"].append(int(info[0]))
+            if r == 3:
+                out["kernel"] = name.value.decode()
+                out["dense_blocks"], out["dense_entries"] = int(info[1]), int(info[2])
+        return out
 
     def csr(self):
         rp = np.empty(self.n + 1, np.int64)

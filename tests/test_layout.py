@@ -4,11 +4,15 @@ positions with clamping, shared absolute columns of rest slices, general positio
 hand-over from rest slices to flagged main slices) and must reproduce A x.  Covers the SPLIT
 mode (rest slices), the unsplit sigma-sorted mode and the row-partitioned case where interior
 slices run before the halo arrives."""
+import os
+
 import numpy as np
 import pytest
 
 from paper_2409_15053_b200 import matrices as M
 from paper_2409_15053_b200.dist import HaloPlan, uniform_starts
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def reference(csr, x):
@@ -119,27 +123,115 @@ def test_partitioned_ug_product(monkeypatch, nranks, split):
         assert np.abs(out - want[starts[p]:starts[p + 1]]).max() <= 1e-12 * np.abs(want).max()
 
 
+def _check_p2_slices(p2, n):
+    """Slices tile the permuted rows: contiguous, in order, 1..64 rows each."""
+    d = p2["desc"]
+    assert d[0, 4] == 0 and d[-1, 4] + d[-1, 5] == n
+    assert np.all(d[1:, 4] == d[:-1, 4] + d[:-1, 5]) and np.all((d[:, 5] >= 1) & (d[:, 5] <= 64))
+    assert np.all(d[:, 0] == p2["ptr"][:-1]) and np.all(d[:, 2] == np.diff(p2["ptr"]))
+
+
 @pytest.mark.parametrize("gen", [lambda: M.parsec_like(radius=12.0, n_atoms=12),
                                  lambda: M.parsec_like(radius=10.0, n_atoms=30, ball_radius=3.6),
                                  lambda: M.random_sparse_sym(700, 0.06, 5)])
-def test_paired_layout_reproduces_product(gen):
-    """Long ragged rows: 64-row slices, two adjacent rows per lane, one column and two values
-    per position (host/plan.hpp).  The emulation walks it as clenshaw_step_p2_tasks does."""
+@pytest.mark.parametrize("dense", ["1", "0"])
+def test_paired_layout_reproduces_product(gen, dense):
+    """Long ragged rows: slices of up to 64 rows, two adjacent rows per lane, one column and
+    two values per general position, one shared column per dense position (host/plan.hpp).
+    The emulation walks it as clenshaw_step_p2_tasks does.  FLZ_P2_DENSE is read once per
+    process, hence the subprocess for the run without dense sections."""
     csr = gen()
     n, rp, ci, va = csr
+    if dense == "0":
+        import os, subprocess, sys
+        code = ("import sys; sys.path.insert(0, %r); import numpy as np\n"
+                "from paper_2409_15053_b200.dist import HaloPlan\n"
+                "d = np.load(sys.argv[1]); n = int(d['n'])\n"
+                "P = HaloPlan(n, 0, 1, [0, n], d['rp'], d['ci'], d['va']); p2 = P.p2_arrays()\n"
+                "perm = P.arrays()['perm']; x = np.random.default_rng(9).standard_normal(n)\n"
+                "y = P.p2_product(x[perm])\n"
+                "import scipy.sparse as sp\n"
+                "want = (sp.csr_matrix((d['va'], d['ci'], d['rp']), shape=(n, n)) @ x)[perm]\n"
+                "assert p2['blocks'] == 0 and p2['slices'] == (n + 63) // 64\n"
+                "even = perm[0:len(perm) - 1:2]\n"
+                "assert np.all((even %% 2 == 0) & (perm[1::2] == even + 1)[: len(even)])\n"
+                "assert np.abs(y - want).max() <= 1e-12 * np.abs(want).max()\n"
+                "assert p2['positions'] * 32 <= 1.15 * len(d['va'])\n" % ROOT)
+        import tempfile
+        with tempfile.NamedTemporaryFile(suffix=".npz") as f:
+            np.savez(f, n=n, rp=rp, ci=ci, va=va)
+            f.flush()
+            r = subprocess.run([sys.executable, "-c", code, f.name],
+                               env=dict(os.environ, FLZ_P2_DENSE="0"), capture_output=True,
+                               text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        return
     P = HaloPlan(n, 0, 1, [0, n], rp, ci, va)
     p2 = P.p2_arrays()
-    assert p2 is not None and p2["slices"] == (n + 63) // 64
-    a = P.arrays()
-    # pairs of adjacent rows stay adjacent (and even-aligned) under the permutation
-    perm = a["perm"]
-    even = perm[0:len(perm) - 1:2]
-    assert np.all((even % 2 == 0) & (perm[1::2] == even + 1)[: len(even)])
+    assert p2 is not None
+    _check_p2_slices(p2, n)
+    perm = P.arrays()["perm"]
+    assert np.array_equal(np.sort(perm), np.arange(n))
     x = np.random.default_rng(9).standard_normal(n)
     y = P.p2_product(x[perm])
     want = reference(csr, x)[perm]
     assert np.abs(y - want).max() <= 1e-12 * np.abs(want).max()
-    assert p2["positions"] * 32 <= 1.15 * len(va)       # at most the entries plus slice padding
+    # every nonzero is stored exactly once: general entries + dense-section entries
+    stored = np.count_nonzero(p2["val"]) + np.count_nonzero(p2["dval"])
+    assert stored == np.count_nonzero(va)
+    assert p2["dense_entries"] == np.count_nonzero(p2["dval"]) or np.any(va == 0.0)
+
+
+def test_dense_blocks_of_a_parsec_shaped_matrix_are_found():
+    """The non-local projector balls of a PARSEC-shaped Hamiltonian become dense sections: one
+    block per atom, most of the nonzeros leave the general positions, a dense section is shared
+    by rows of ONE block (its columns are exactly that block's members), and what is left per
+    row is the 37-point stencil."""
+    n_atoms = 24
+    csr = M.parsec_like(radius=14.0, n_atoms=n_atoms, ball_radius=3.4)
+    n, rp, ci, va = csr
+    P = HaloPlan(n, 0, 1, [0, n], rp, ci, va)
+    p2 = P.p2_arrays()
+    _check_p2_slices(p2, n)
+    assert p2["blocks"] == n_atoms
+    assert p2["dense_entries"] >= 0.3 * len(va)
+    d = p2["desc"]
+    dense = d[d[:, 3] > 0]
+    assert len(dense) >= n_atoms
+    perm = P.arrays()["perm"]
+    A = M.csr_to_scipy(n, rp, ci, va)
+    for gpos, dpos, ng, nd, row0, nrows in dense[:: max(1, len(dense) // 8)]:
+        cols_old = np.sort(perm[p2["dcol"][dpos: dpos + nd]])
+        rows_old = perm[row0: row0 + nrows]
+        assert np.all(np.isin(rows_old, cols_old))             # rows are members of the block
+        sub = A[rows_old][:, cols_old]
+        assert sub.nnz >= 0.9 * nrows * nd                      # and the block is dense
+        assert ng <= 64                                         # the stencil part is what is left
+    # general positions: fewer than half of what the layout without dense sections needs
+    assert p2["positions"] * 32 <= 0.65 * len(va)     # general positions left (0.78 without dense sections)
+    x = np.random.default_rng(4).standard_normal(n)
+    want = (A @ x)[perm]
+    assert np.abs(P.p2_product(x[perm]) - want).max() <= 1e-12 * np.abs(want).max()
+
+
+def test_matrices_without_dense_blocks_keep_the_plain_paired_layout():
+    """Long rows that are not cliques (random sparse, banded): the block search gives up after a
+    bounded number of seeds and the layout is the plain paired one."""
+    import scipy.sparse as sp
+    rng = np.random.default_rng(11)
+    n = 3000
+    B = sp.random(n, n, density=0.03, random_state=5, format="csr")
+    B = B + B.T + sp.diags(rng.uniform(1, 2, n))
+    csr = M._to_csr(B)
+    n, rp, ci, va = csr
+    P = HaloPlan(n, 0, 1, [0, n], rp, ci, va)
+    p2 = P.p2_arrays()
+    assert p2 is not None and p2["blocks"] == 0 and p2["dense_positions"] == 0
+    assert p2["slices"] == (n + 63) // 64
+    perm = P.arrays()["perm"]
+    x = rng.standard_normal(n)
+    want = (B @ x)[perm]
+    assert np.abs(P.p2_product(x[perm]) - want).max() <= 1e-12 * np.abs(want).max()
 
 
 def test_paired_layout_odd_row_count_lone_row_longest():
@@ -167,44 +259,6 @@ def test_paired_layout_odd_row_count_lone_row_longest():
     y = P.p2_product(x[perm])
     want = (dense @ x)[perm]
     assert np.abs(y[:n] - want).max() <= 1e-12 * np.abs(want).max()
-
-
-def test_clustered_pair_order_lines_up_dense_blocks():
-    """FLZ_P2_CLUSTER=1 (read once per process, hence the subprocess): long pairs sorted by the
-    min-hash of their long columns, lanes ordered by column frequency.  The product is unchanged,
-    pairs stay adjacent, and the lanes of a slice ask for far fewer distinct 128-byte lines."""
-    import json, os, subprocess, sys
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    code = r'''
-import sys, json
-sys.path.insert(0, %r)
-import numpy as np
-from paper_2409_15053_b200 import matrices as M
-from paper_2409_15053_b200.dist import HaloPlan
-n, rp, ci, va = M.parsec_like(radius=14.0, n_atoms=24, ball_radius=3.4)
-P = HaloPlan(n, 0, 1, [0, n], rp, ci, va)
-p2 = P.p2_arrays(); perm = P.arrays()["perm"]
-x = np.random.default_rng(2).standard_normal(n)
-import scipy.sparse as sp
-want = (sp.csr_matrix((va, ci, rp), shape=(n, n)) @ x)[perm]
-y = P.p2_product(x[perm])[:n]
-col = p2["col"].reshape(-1, 32)
-lines = 1 + (np.diff(np.sort(col // 4, axis=1), axis=1) != 0).sum(1)
-even = perm[0:len(perm) - 1:2]
-print(json.dumps(dict(err=float(np.abs(y - want).max() / np.abs(want).max()), lines=float(lines.mean()),
-                      positions=int(p2["positions"]),
-                      paired=bool(np.all((even %% 2 == 0) & (perm[1::2] == even + 1)[: len(even)])))))
-''' % root
-    out = {}
-    for flag in ("0", "1"):
-        env = dict(os.environ, FLZ_P2_CLUSTER=flag)
-        p = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
-        assert p.returncode == 0, p.stderr[-2000:]
-        out[flag] = json.loads(p.stdout.strip().splitlines()[-1])
-    assert out["0"]["err"] <= 1e-12 and out["1"]["err"] <= 1e-12
-    assert out["0"]["paired"] and out["1"]["paired"]
-    assert out["1"]["lines"] <= 0.8 * out["0"]["lines"]
-    assert out["1"]["positions"] <= 1.1 * out["0"]["positions"]
 
 
 def test_paired_layout_saves_gathers_on_dense_blocks():
