@@ -59,6 +59,9 @@ int flz_ctx_create_dist(int device, int rank, int nranks, const void* nccl_uniqu
 int flz_nccl_unique_id(void* out128);
 void flz_ctx_destroy(flz_ctx* ctx);
 int flz_ctx_sync(flz_ctx* ctx);
+/* binds the calling host thread to the context's device (worker threads that allocate
+ * page-locked memory or issue calls of their own) */
+int flz_ctx_make_current(const flz_ctx* ctx);
 int flz_ctx_rank(const flz_ctx* ctx);
 int flz_ctx_nranks(const flz_ctx* ctx);
 /* Launch counters: kernels of THIS library launched on the context since creation. */

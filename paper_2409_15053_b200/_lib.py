@@ -69,6 +69,7 @@ _SIGS = {
     "flz_nccl_unique_id": (i32, [vp]),
     "flz_ctx_destroy": (None, [vp]),
     "flz_ctx_sync": (i32, [vp]),
+    "flz_ctx_make_current": (i32, [vp]),
     "flz_ctx_rank": (i32, [vp]),
     "flz_ctx_nranks": (i32, [vp]),
     "flz_ctx_launch_count": (u64, [vp]),

@@ -112,7 +112,7 @@ SellView make_view(const flz_matrix* A, const SliceTask* tasks, int64_t ntasks,
                   A->nl,        A->ug.p,    A->ug_val.p,   A->ug_col.p,    A->ug_uoff.p,
                   A->nl + A->nhalo, A->rest_rows.p, A->nslices,   A->w.p,
                   A->uv_pairs.p,    false,          A->p2_desc.p, A->p2_col.p, A->p2_val.p,
-                  A->p2_dcol.p,     A->p2_dval.p,
+                  A->p2_dcol.p,     A->p2_dval.p,   nullptr,
                   // the tile kernel covers whole-matrix launches only
                   (slice_ids == nullptr && nslices == A->nslices) ? A->tiles : StencilTiles{}};
 }
@@ -120,6 +120,13 @@ SellView make_view(const flz_matrix* A, const SliceTask* tasks, int64_t ntasks,
 SellView paired(const flz_matrix* A, SellView v, int which) {
   if (!A->p2 || A->ctx->exact) return v;
   v.p2 = true;
+  // a fresh (zero) task counter per launch; the block of counters is cleared when it runs out
+  constexpr int kTicketSlots = 4096;
+  if (A->k1_tickets.count == 0 || A->ticket_cursor == kTicketSlots) {
+    A->k1_tickets.reserve_zero(kTicketSlots, A->ctx->stream);
+    A->ticket_cursor = 0;
+  }
+  v.tickets = A->k1_tickets.p + A->ticket_cursor++;
   v.tasks = which == 0 ? A->p2_tasks_all.p : (which == 1 ? A->p2_tasks_interior.p : A->p2_tasks_boundary.p);
   v.ntasks = which == 0 ? A->p2_nt_all : (which == 1 ? A->p2_nt_interior : A->p2_nt_boundary);
   return v;
@@ -508,6 +515,12 @@ int flz_flush_l2(flz_ctx* ctx, size_t bytes) {
 int flz_ctx_set_exact(flz_ctx* ctx, int exact) {
   ctx->exact = exact != 0;
   return FLZ_OK;
+}
+int flz_ctx_make_current(const flz_ctx* ctx) {
+  return guarded([&] {
+    FLZ_REQUIRE(ctx, FLZ_EINVAL, "make_current: null context");
+    use(ctx);
+  });
 }
 int flz_host_alloc(size_t bytes, void** out) {
   return guarded([&] { *out = pinned_alloc(bytes); });
@@ -1170,7 +1183,16 @@ int flz_lanczos_step(flz_ctx* ctx, const flz_matrix* A, flz_basis* B, const doub
     const SmallLayout L = small_layout(B->max_cols, r);
     double* sm = B->small.p;
 
-    B->k += 1;  // promote the pending block (lanczos.cpp:153)
+    // promote the pending block (lanczos.cpp:153); undone if anything below throws, so the
+    // device basis never runs ahead of the host's LanczosFactorization
+    struct Promote {
+      flz_basis* B;
+      bool committed = false;
+      ~Promote() {
+        if (!committed) B->k -= 1;
+      }
+    } promote{B};
+    B->k += 1;
     const int64_t cols = B->k * r, newest = cols - r;
 
     FLZ_CUDA(cudaEventRecord(B->e0, ctx->stream));
@@ -1243,6 +1265,7 @@ int flz_lanczos_step(flz_ctx* ctx, const flz_matrix* A, flz_basis* B, const doub
     FLZ_CUDA(cudaEventElapsedTime(&ms_orth, B->e1, B->e2));
     B->mv_s += 1e-3 * ms_mv;
     B->orth_s += 1e-3 * ms_orth;
+    promote.committed = true;
   });
 }
 
@@ -1329,16 +1352,15 @@ int flz_ritz_lift(flz_ctx* ctx, const flz_matrix* A, const flz_basis* Bc, int64_
     { Trace tr(ctx, "lift: reserve V, AV chunk");
     B->V.reserve_zero((size_t)ld * w, ctx->stream);
     B->AV.reserve_zero((size_t)ld * std::min(w, kRecoverChunk), ctx->stream); }
-    Trace* tr1 = new Trace(ctx, "lift: W transpose + H2D");
     // W (dim x w column-major) -> row-major [dim][ldw]
     std::vector<double> Wt((size_t)dim * ldw, 0.0);
+    DevBuf<double> dW;
+    { Trace tr(ctx, "lift: W transpose + H2D");
     for (int c = 0; c < w; ++c)
       for (int64_t j = 0; j < dim; ++j) Wt[(size_t)j * ldw + c] = W[(size_t)c * dim + j];
-    DevBuf<double> dW;
     dW.reserve(Wt.size() + 8);
     FLZ_CUDA(cudaMemcpyAsync(dW.p, Wt.data(), Wt.size() * sizeof(double), cudaMemcpyHostToDevice,
-                             ctx->stream));
-    delete tr1;
+                             ctx->stream)); }
     { Trace tr(ctx, "lift: V = Q W (gemm_nn)");
     launch_gemm_nn(ctx, B->Q.p, ld, dim, dW.p, ldw, w, nl, 1.0, false, B->V.p, ld); }
     DevBuf<double> dn;

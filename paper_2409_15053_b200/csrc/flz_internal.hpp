@@ -187,6 +187,9 @@ struct flz_matrix {
   flz::DevBuf<int32_t> p2_col, p2_dcol;
   flz::DevBuf<double> p2_val, p2_dval;
   int64_t p2_blocks = 0, p2_dense_entries = 0;
+  // task counters of the persistent paired kernel: one per launch, zeroed kTicketSlots at a time
+  mutable flz::DevBuf<unsigned> k1_tickets;
+  mutable int ticket_cursor = 0;
   flz::DevBuf<flz::SliceTask> p2_tasks_all, p2_tasks_interior, p2_tasks_boundary;
   int64_t p2_nt_all = 0, p2_nt_interior = 0, p2_nt_boundary = 0;
   int64_t p2_bytes = 0;
@@ -287,6 +290,7 @@ struct SellView {
   const double* p2_val;
   const int32_t* p2_dcol;    // dense sections: shared columns, one value pair per lane
   const double* p2_dval;
+  unsigned* tickets;         // this launch's task counter (starts at 0; persistent CTAs)
   StencilTiles tiles;        // nseg > 0: tile plan of the TMA-staged stencil kernel
 };
 

@@ -1112,26 +1112,100 @@ HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<in
         if (blocks.primary[j] == (int32_t)b) rows.push_back(j);
       emit(rows, (int32_t)b);
     }
+    // rows outside every block: CLUSTERS of `cluster_rows` rows that share gather targets
+    // (one CTA task each), grown greedily over the matrix graph — always add the frontier row
+    // with the most entries into the cluster.  On a 3D stencil a cluster is a compact brick, so
+    // the block rows its lanes gather are fetched from L2 once per CTA and then hit L1: the
+    // kernel is bound by L2 -> SM traffic, and in natural order a gathered row was
+    // fetched again by every x-line that needs it.
     rows.clear();
-    for (int64_t i = 0; i < nl; ++i)
-      if (blocks.count[i] == 0) rows.push_back((int32_t)i);
-    const int64_t npairs = ((int64_t)rows.size() + 1) / 2;
-    std::vector<int32_t> cls(npairs), pairs(npairs);
-    for (int64_t q = 0; q < npairs; ++q) {
-      pairs[q] = (int32_t)q;
-      const bool lone = 2 * q + 1 >= (int64_t)rows.size();
-      cls[q] = length_class(lone ? len[rows[2 * q]] : (union_size(rows[2 * q], rows[2 * q + 1]) + 1) / 2);
+    static const int cluster_rows = [] {
+      const char* e = std::getenv("FLZ_P2_CLUSTER_ROWS");
+      return e && *e ? std::max(64, std::atoi(e)) : 512;
+    }();
+    {
+      // units = the pairs a lane will own: two rows with consecutive indices (x-neighbours
+      // share 12 of 13 x-entries), or a single row where the neighbour is missing
+      std::vector<int32_t> unit_of(nl, -1), ua, ub;
+      for (int64_t i = 0; i < nl; ++i) {
+        if (blocks.count[i] != 0 || unit_of[i] >= 0) continue;
+        const bool pair = i + 1 < nl && blocks.count[i + 1] == 0;
+        unit_of[i] = (int32_t)ua.size();
+        if (pair) unit_of[i + 1] = (int32_t)ua.size();
+        ua.push_back((int32_t)i);
+        ub.push_back(pair ? (int32_t)(i + 1) : -1);
+      }
+      const int64_t nu = (int64_t)ua.size();
+      const int32_t maxdeg = 2 * longest;
+      std::vector<uint8_t> taken(nu, 0);
+      std::vector<std::vector<int32_t>> bucket(maxdeg + 1);
+      std::vector<int32_t> links(nu, 0), touched, cluster;
+      int64_t next_seed = 0;
+      while (true) {
+        while (next_seed < nu && taken[next_seed]) ++next_seed;
+        if (next_seed >= nu) break;
+        cluster.clear();
+        touched.clear();
+        int top = 0, nrows_in = 0;
+        auto add = [&](int32_t u) {
+          taken[u] = 1;
+          cluster.push_back(u);
+          for (int32_t i : {ua[u], ub[u]}) {
+            if (i < 0) continue;
+            ++nrows_in;
+            // STRONG connections only (|a_ij| >= 1/4 of the row's largest off-diagonal entry,
+            // as in algebraic multigrid): on a high-order stencil these are the nearest
+            // neighbours, so the cluster grows as a compact brick instead of along the arms
+            double big = 0.0;
+            for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e)
+              if ((int64_t)col_idx[e] - P.row_begin != i) big = std::max(big, std::abs(values[e]));
+            for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
+              const int64_t c = (int64_t)col_idx[e] - P.row_begin;
+              if (c < 0 || c >= nl || std::abs(values[e]) < 0.25 * big) continue;
+              const int32_t v = unit_of[c];
+              if (v < 0 || taken[v]) continue;
+              if (links[v] == 0) touched.push_back(v);
+              const int32_t k = std::min(++links[v], maxdeg);
+              bucket[k].push_back(v);
+              top = std::max(top, (int)k);
+            }
+          }
+        };
+        add((int32_t)next_seed);
+        while (nrows_in < cluster_rows) {
+          int32_t pick = -1;
+          while (top > 0 && pick < 0) {
+            auto& bk = bucket[top];
+            while (!bk.empty() && pick < 0) {
+              const int32_t v = bk.back();
+              bk.pop_back();
+              if (!taken[v] && std::min(links[v], maxdeg) == top) pick = v;  // else stale
+            }
+            if (pick < 0) --top;
+          }
+          if (pick < 0) break;  // component exhausted
+          add(pick);
+        }
+        for (int32_t v : touched) links[v] = 0;
+        for (int k = 1; k <= maxdeg; ++k) bucket[k].clear();
+        // inside a cluster: ascending index, then by length class so that the lanes of a
+        // slice pad little; single rows last (two of them share a lane)
+        std::sort(cluster.begin(), cluster.end());
+        std::vector<int32_t> cls(cluster.size());
+        for (size_t q = 0; q < cluster.size(); ++q) {
+          const int32_t u = cluster[q];
+          cls[q] = ub[u] < 0 ? -1 : length_class((union_size(ua[u], ub[u]) + 1) / 2);
+        }
+        std::vector<int32_t> pid(cluster.size());
+        std::iota(pid.begin(), pid.end(), 0);
+        std::stable_sort(pid.begin(), pid.end(), [&](int32_t a, int32_t b) { return cls[a] > cls[b]; });
+        for (int32_t q : pid) {
+          rows.push_back(ua[cluster[q]]);
+          if (ub[cluster[q]] >= 0) rows.push_back(ub[cluster[q]]);
+        }
+      }
     }
-    const int64_t window = 8192, whole = (int64_t)rows.size() / 2;   // a lone last row stays last
-    for (int64_t w0 = 0; w0 < whole; w0 += window)
-      std::stable_sort(pairs.begin() + w0, pairs.begin() + std::min(whole, w0 + window),
-                       [&](int32_t a, int32_t b) { return cls[a] > cls[b]; });
-    std::vector<int32_t> sorted;
-    sorted.reserve(rows.size());
-    for (int32_t q : pairs) {
-      sorted.push_back(rows[2 * q]);
-      if (2 * (int64_t)q + 1 < (int64_t)rows.size()) sorted.push_back(rows[2 * q + 1]);
-    }
+    const std::vector<int32_t>& sorted = rows;
     emit(sorted, -1);
     if (std::getenv("FLZ_TRACE"))
       std::fprintf(stderr, "[flz]   plan dense blocks: %zu blocks cover %lld of %lld entries, "

@@ -249,8 +249,13 @@ int expand(LanczosFactorization& st, int nblocks, ExpandTimes* times) {
           for (std::size_t i = 0; i < n; ++i) fresh[i] = gauss(rng);
           double rn = 0.0;
           double* mine = fresh.data() + row_b;  // this rank's rows; rn is the global norm
+          // against ALL cols + r columns: the device has already finished the intra-block QR
+          // of the live pending columns j+1.., so the replacement must be made orthogonal to
+          // them too (the reference removes the replacement from those columns instead,
+          // lanczos.cpp:208-218; either way the pending block ends up orthonormal).  Dead
+          // columns that are not replaced yet are exactly zero and contribute nothing.
           throw_status(flz_orthogonalize_column(ctx, st.dev_, static_cast<std::int64_t>(cols),
-                                                static_cast<int>(j), mine, &rn));
+                                                static_cast<int>(r), mine, &rn));
           if (rn > 1e-4) {
             const double inv = 1.0 / rn;
             for (std::size_t i = 0; i < row_e - row_b; ++i) mine[i] *= inv;
@@ -450,7 +455,12 @@ EigenResult recover_eigenpairs(const LanczosFactorization& st, const SparseSymMa
   // thread while the device lifts the Ritz vectors; at most w columns are needed
   std::future<DenseBlock> storage;
   if (return_vectors)
-    storage = std::async(std::launch::async, [n, w] { return DenseBlock::pinned(n, w); });
+    storage = std::async(std::launch::async, [n, w, ctx = Device::context()] {
+      // a new host thread starts on device 0: bind it to the rank's device before it
+      // page-locks memory, or every rank would create a context on GPU 0
+      throw_status(flz_ctx_make_current(ctx));
+      return DenseBlock::pinned(n, w);
+    });
 
   // Ritz vectors of T_k for the candidates only.
   const WallClock t_w;
@@ -673,7 +683,6 @@ EigenResult run_solve(const SparseSymMatrix& A, double alpha, double beta,
   };
   bool can_expand = true;
   int since_check = 0;
-  const WallClock loop_clock;
   double waited = 0.0;
   while (!converged && (can_expand || !queue.empty())) {
     // resolve finished checks, oldest first; block on the oldest when nothing else can be done
@@ -713,8 +722,7 @@ EigenResult run_solve(const SparseSymMatrix& A, double alpha, double beta,
     }
   }
   queue.clear();
-  time_check = overlap ? waited : waited;
-  (void)loop_clock;
+  time_check = waited;
   if (!converged) {  // budget or space exhausted: best pairs of the final state (:627-632)
     const WallClock chk;
     const RitzSet ritz = check_convergence(st, alpha, beta, cfg.tol, cfg.extra_ritz);

@@ -648,136 +648,164 @@ __global__ void __launch_bounds__(kTaskWarps * 32, FLZ_K1_TASK_CTAS)
                            const double* __restrict__ Y1, double* __restrict__ Y2, int64_t ldy,
                            const double* __restrict__ X, int64_t ldx, double* __restrict__ Out,
                            int64_t ldo) {
-  __shared__ double part[kTaskWarps][2 * R][32];
-  __shared__ __align__(16) double strip[kTaskWarps][32][4];   // gathered rows of 32 dense columns
+  // Persistent CTAs take tasks from a ticket counter (tasks are sorted longest first): an SM
+  // that was dealt long tasks simply takes fewer of them.  With one CTA per task the SMs were
+  // active 41k-83k cycles of a 90k-cycle launch (ncu, PARSEC-shaped n = 113k).
+  // One 1.5 KB strip per warp: the gathered rows of 32 dense columns ([32][4]) while the dense
+  // section runs, then the warp's partial sums ([2R][32]).  Shared memory is kept small on
+  // purpose: what the CTAs do not claim stays L1 for the gathered block rows.
+  __shared__ __align__(16) double scratch[kTaskWarps][2 * kMaxFuse * 32];
+  __shared__ int next_task;
+  auto part = [&](int w, int k) -> double* { return scratch[w] + k * 32; };
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   pdl_launch_dependents();
-  const SliceTask task = A.tasks[blockIdx.x];
-  const int W = task.warps_per_slice;
-  const int sub = warp / W, piece = warp - sub * W;
-  const bool active = sub < task.count;
-  double acc[2][R];
+  if (threadIdx.x == 0) next_task = (int)atomicAdd(A.tickets, 1u);
+  __syncthreads();
+  int t = next_task;
+  if (t >= A.ntasks) return;
+  pdl_wait();
+  for (;;) {
+    const int2 head = __ldg(reinterpret_cast<const int2*>(A.tasks + t));
+    const int W = head.x;   // warps per slice; head.y slices in this task
+    const int sub = warp / W, piece = warp - sub * W;
+    const bool active = sub < head.y;
+    double acc[2][R];
 #pragma unroll
-  for (int k = 0; k < R; ++k) acc[0][k] = acc[1][k] = 0.0;
-  int64_t row = 0;
-  int row_end = 0;
-  if (active) {
-    const int4* hp = reinterpret_cast<const int4*>(A.p2_desc + task.slice[sub]);
-    const int4 h0 = __ldg(hp), h1 = __ldg(hp + 1);
-    const int64_t gpos = ((int64_t)(uint32_t)h0.y << 32) | (uint32_t)h0.x;
-    const int64_t dpos = ((int64_t)(uint32_t)h0.w << 32) | (uint32_t)h0.z;
-    const int ng = h1.x, nd = h1.y;
-    row = (int64_t)h1.z + 2 * lane;
-    row_end = h1.z + h1.w;
-    const int chunk = (((ng + W - 1) / W) + kBatch - 1) / kBatch * kBatch;
-    const int p0 = piece * chunk, p1 = min(ng, p0 + chunk);
-    const int dchunk = (((nd + W - 1) / W) + 31) / 32 * 32;
-    const int d0 = min(nd, piece * dchunk), d1 = min(nd, d0 + dchunk);
-    const int32_t* __restrict__ col = A.p2_col + (gpos + p0) * 32 + lane;
-    const double* __restrict__ val = A.p2_val + ((gpos + p0) * 32 + lane) * 2;
-    const int32_t* __restrict__ dcol = A.p2_dcol + dpos;
-    const double* __restrict__ dval = A.p2_dval + (dpos * 32 + lane) * 2;
-    pdl_wait();
-    for (int p = p0; p < p1; p += kBatch) {
+    for (int k = 0; k < R; ++k) acc[0][k] = acc[1][k] = 0.0;
+    int64_t row = 0;
+    int row_end = 0;
+    if (active) {
+      const int4* hp = reinterpret_cast<const int4*>(A.p2_desc + __ldg(&A.tasks[t].slice[sub]));
+      const int4 h0 = __ldg(hp), h1 = __ldg(hp + 1);
+      const int64_t gpos = ((int64_t)(uint32_t)h0.y << 32) | (uint32_t)h0.x;
+      const int64_t dpos = ((int64_t)(uint32_t)h0.w << 32) | (uint32_t)h0.z;
+      const int ng = h1.x, nd = h1.y;
+      row = (int64_t)h1.z + 2 * lane;
+      row_end = h1.z + h1.w;
+      const int chunk = (((ng + W - 1) / W) + kBatch - 1) / kBatch * kBatch;
+      const int p0 = piece * chunk, p1 = min(ng, p0 + chunk);
+      const int dchunk = (((nd + W - 1) / W) + 31) / 32 * 32;
+      const int d0 = min(nd, piece * dchunk), d1 = min(nd, d0 + dchunk);
+      const int32_t* __restrict__ col = A.p2_col + (gpos + p0) * 32 + lane;
+      const double* __restrict__ val = A.p2_val + ((gpos + p0) * 32 + lane) * 2;
+      const int32_t* __restrict__ dcol = A.p2_dcol + dpos;
+      const double* __restrict__ dval = A.p2_dval + (dpos * 32 + lane) * 2;
+      // general positions, kBatch per round.  The columns of round i+1 are requested before
+      // the gathers of round i are consumed, so a round exposes ONE memory round trip (the
+      // gathers, with the values beside them), not two (columns, then gathers).
       int c[kBatch];
-      double va[kBatch], vb[kBatch], g[kBatch][R];
 #pragma unroll
-      for (int u = 0; u < kBatch; ++u) {
-        const bool ok = p + u < p1;
-        c[u] = ok ? ld_stream_s32(col + u * 32) : 0;
-        va[u] = vb[u] = 0.0;
-        if (ok)
-          asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];"
-                       : "=d"(va[u]), "=d"(vb[u]) : "l"(val + u * 64));
-      }
+      for (int u = 0; u < kBatch; ++u) c[u] = p0 + u < p1 ? ld_stream_s32(col + u * 32) : 0;
+      // first dense round: its column and gather do not depend on the general part
+      int dc = (d0 < d1 && lane < d1 - d0) ? ld_stream_s32(dcol + d0 + lane) : -1;
+      for (int p = p0; p < p1; p += kBatch) {
+        double va[kBatch], vb[kBatch], g[kBatch][R];
 #pragma unroll
-      for (int u = 0; u < kBatch; ++u) gather_row<R, S>(Y1, ldy, c[u], p + u < p1, g[u]);
+        for (int u = 0; u < kBatch; ++u) gather_row<R, S>(Y1, ldy, c[u], p + u < p1, g[u]);
 #pragma unroll
-      for (int u = 0; u < kBatch; ++u)
-#pragma unroll
-        for (int k = 0; k < R; ++k) {
-          acc[0][k] = fma(va[u], g[u][k], acc[0][k]);
-          acc[1][k] = fma(vb[u], g[u][k], acc[1][k]);
-        }
-      col += kBatch * 32;
-      val += kBatch * 64;
-    }
-    // dense section: 32 columns per round
-    double (*mine)[4] = strip[warp];
-    for (int q = d0; q < d1; q += 32) {
-      const int cnt = min(32, d1 - q);
-      const double* __restrict__ v = dval + (int64_t)q * 64;
-      // the first value pairs are requested before the gather they do not depend on
-      double va[4], vb[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        va[u] = vb[u] = 0.0;
-        if (u < cnt)
-          asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];"
-                       : "=d"(va[u]), "=d"(vb[u]) : "l"(v + u * 64));
-      }
-      double g[R];
-      const int c = lane < cnt ? ld_stream_s32(dcol + q + lane) : 0;
-      gather_row<R, S>(Y1, ldy, c, lane < cnt, g);
-      __syncwarp();                      // the previous round's reads of the strip are done
-#pragma unroll
-      for (int k = 0; k < R; ++k) mine[lane][k] = g[k];
-      __syncwarp();
-      for (int j = 0; j < cnt; j += 4) {
-        double na[4], nb[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {    // next batch in flight while this one is consumed
-          na[u] = nb[u] = 0.0;
-          if (j + 4 + u < cnt)
+        for (int u = 0; u < kBatch; ++u) {
+          va[u] = vb[u] = 0.0;
+          if (p + u < p1)
             asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];"
-                         : "=d"(na[u]), "=d"(nb[u]) : "l"(v + (j + 4 + u) * 64));
+                         : "=d"(va[u]), "=d"(vb[u]) : "l"(val + u * 64));
         }
+        col += kBatch * 32;
+        val += kBatch * 64;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int jj = min(j + u, 31);  // past cnt: zero values times a staged (finite) row
+        for (int u = 0; u < kBatch; ++u)
+          c[u] = p + kBatch + u < p1 ? ld_stream_s32(col + u * 32) : 0;
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u)
 #pragma unroll
           for (int k = 0; k < R; ++k) {
-            const double y = mine[jj][k];
-            acc[0][k] = fma(va[u], y, acc[0][k]);
-            acc[1][k] = fma(vb[u], y, acc[1][k]);
+            acc[0][k] = fma(va[u], g[u][k], acc[0][k]);
+            acc[1][k] = fma(vb[u], g[u][k], acc[1][k]);
           }
-        }
+      }
+      // dense section: 32 columns per round; the next round's column and gathered row are
+      // requested before this round's positions are consumed
+      double (*mine)[4] = reinterpret_cast<double (*)[4]>(scratch[warp]);
+      double g[R];
+      gather_row<R, S>(Y1, ldy, max(dc, 0), dc >= 0, g);
+      for (int q = d0; q < d1; q += 32) {
+        const int cnt = min(32, d1 - q);
+        const double* __restrict__ v = dval + (int64_t)q * 64;
+        double va[4], vb[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          va[u] = na[u];
-          vb[u] = nb[u];
+          va[u] = vb[u] = 0.0;
+          if (u < cnt)
+            asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];"
+                         : "=d"(va[u]), "=d"(vb[u]) : "l"(v + u * 64));
+        }
+        __syncwarp();                      // the previous round's reads of the strip are done
+#pragma unroll
+        for (int k = 0; k < R; ++k) mine[lane][k] = g[k];
+        __syncwarp();
+        dc = (q + 32 < d1 && lane < d1 - q - 32) ? ld_stream_s32(dcol + q + 32 + lane) : -1;
+        bool gathered = false;
+        for (int j = 0; j < cnt; j += 4) {
+          double na[4], nb[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {    // next batch in flight while this one is consumed
+            na[u] = nb[u] = 0.0;
+            if (j + 4 + u < cnt)
+              asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];"
+                           : "=d"(na[u]), "=d"(nb[u]) : "l"(v + (j + 4 + u) * 64));
+          }
+          if (!gathered && j >= 4) {       // the next round's column has had a batch to arrive
+            gather_row<R, S>(Y1, ldy, max(dc, 0), dc >= 0, g);
+            gathered = true;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int jj = min(j + u, 31);  // past cnt: zero values times a staged (finite) row
+#pragma unroll
+            for (int k = 0; k < R; ++k) {
+              const double y = mine[jj][k];
+              acc[0][k] = fma(va[u], y, acc[0][k]);
+              acc[1][k] = fma(vb[u], y, acc[1][k]);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            va[u] = na[u];
+            vb[u] = nb[u];
+          }
+        }
+        if (!gathered) gather_row<R, S>(Y1, ldy, max(dc, 0), dc >= 0, g);
+      }
+    }
+    if (W > 1) {  // uniform across the CTA
+      if (active && piece > 0) {
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+          part(warp, k)[lane] = acc[0][k];
+          part(warp, R + k)[lane] = acc[1][k];
         }
       }
     }
-  } else {
-    pdl_wait();
-  }
-  if (W > 1) {  // uniform across the CTA
-    if (active && piece > 0) {
-#pragma unroll
-      for (int k = 0; k < R; ++k) {
-        part[warp][k][lane] = acc[0][k];
-        part[warp][R + k][lane] = acc[1][k];
-      }
-    }
+    if (threadIdx.x == 0) next_task = (int)atomicAdd(A.tickets, 1u);
     __syncthreads();
+    t = next_task;
     if (active && piece == 0) {
       for (int q = 1; q < W; ++q)
 #pragma unroll
         for (int k = 0; k < R; ++k) {
-          acc[0][k] += part[warp + q][k][lane];
-          acc[1][k] += part[warp + q][R + k][lane];
+          acc[0][k] += part(warp + q, k)[lane];
+          acc[1][k] += part(warp + q, R + k)[lane];
         }
-    }
-  }
-  if (!active || piece != 0) return;
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int64_t r = row + h;
-    if (r >= row_end) break;
-    double y1o[R], y2o[R], xo[R];
-    load_own<R, S, MODE>(A, r, Y1, Y2, ldy, X, ldx, y1o, y2o, xo);
-    finish_row<R, S, MODE>(r, s1, s2, b, acc[h], y1o, y2o, xo, Y2, ldy, Out, ldo);
+      for (int h = 0; h < 2; ++h) {
+        const int64_t r = row + h;
+        if (r >= row_end) break;
+        double y1o[R], y2o[R], xo[R];
+        load_own<R, S, MODE>(A, r, Y1, Y2, ldy, X, ldx, y1o, y2o, xo);
+        finish_row<R, S, MODE>(r, s1, s2, b, acc[h], y1o, y2o, xo, Y2, ldy, Out, ldo);
+      }
+    }
+    if (t >= A.ntasks) break;
+    __syncthreads();   // `part` and next_task are reused by the next task
   }
 }
 
@@ -1452,8 +1480,17 @@ void launch_ug(flz_ctx* ctx, const SellView& A, double s1, double s2, double b, 
   if constexpr (MODE != 3) {
     if (A.p2) {
       if (A.ntasks == 0) return;
-      launch_k1(ctx, clenshaw_step_p2_tasks<R, S, MODE>, (unsigned)A.ntasks, kTaskWarps * 32, A,
-                s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo);
+      const unsigned grid =
+          (unsigned)std::min<int64_t>(A.ntasks, (int64_t)ctx->sm_count * FLZ_K1_TASK_CTAS);
+      static const bool configured = [] {   // smallest shared-memory carve-out that fits: rest is L1
+        const int pct = env_int("FLZ_K1_CARVEOUT", 25);
+        FLZ_CUDA(cudaFuncSetAttribute(clenshaw_step_p2_tasks<R, S, MODE>,
+                                      cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+        return true;
+      }();
+      (void)configured;
+      launch_k1(ctx, clenshaw_step_p2_tasks<R, S, MODE>, grid, kTaskWarps * 32, A, s1, s2, b, Y1,
+                Y2, ldy, X, ldx, Out, ldo);
       ctx->launches++;
       return;
     }

@@ -96,6 +96,51 @@ def test_identity_filter_breakdown_path():
     assert np.abs(Q.T @ Q - np.eye(6)).max() < 1e-12
 
 
+@pytest.mark.parametrize("which", [0, 1])
+def test_mixed_dead_and_live_pending_block_stays_orthonormal(best_oracle, which):
+    """A start block whose column `which` is an eigenvector, r = 3: that pending column dies in
+    the first step (p(A) v = p(lambda) v lies in the basis) while LATER columns stay alive.  The
+    replacement must be orthogonal to those later columns as well (lanczos.cpp:232-262 has it
+    in place before they are processed): Q^T Q = I, the factorization identity holds, and the
+    Ritz values of T_k agree with the reference's run from the same start block."""
+    g = 12
+    n, rp, ci, va = M.laplacian2d(g)
+    idx = np.arange(1, g + 1)
+    v = np.outer(np.sin(3 * np.pi * idx / (g + 1)), np.sin(5 * np.pi * idx / (g + 1))).ravel()
+    q = v / np.linalg.norm(v)
+    rest = np.random.default_rng(4).standard_normal((n, 2))
+    rest -= np.outer(q, q @ rest)
+    rest = np.linalg.qr(rest)[0]
+    cols = [rest[:, 0], rest[:, 1]]
+    cols.insert(which, q)                    # orthonormal start block, eigenvector at `which`
+    start = np.column_stack(cols)
+    A = S.SparseSymMatrix.from_csr(n, rp, ci, va)
+    lo, hi = -0.05, 8.05
+    cf = S.build_filter(lo, hi, 3.0, 4.0, 20)[0]
+    F = S.LanczosFactorization(A, start, 60, cf, (lo, hi), (3.0, 4.0))
+    k = F.expand(6)
+    assert k == 6 and F.flags() & 2                      # breakdown recorded, run continues
+    Q, D, S_, dead = F.get()
+    assert not dead.any()
+    assert np.abs(Q.T @ Q - np.eye(Q.shape[1])).max() < 1e-12
+    assert F.ortho_error() <= 1e-12
+    r = 3
+    Qk, Qp = Q[:, :k * r], Q[:, k * r:]
+    T = dense_T(D, S_, k, r)
+    OpQ = np.concatenate([A.filter_apply(cf, lo, hi, Qk[:, j:j + 3]) for j in range(0, k * r, 3)], 1)
+    E = np.zeros((k * r, r))
+    E[(k - 1) * r:, :] = np.eye(r)
+    assert np.abs(OpQ - Qk @ T - Qp @ S_[k - 1] @ E.T).max() < 1e-10
+    assert np.abs(Qk.T @ OpQ - T).max() < 1e-10
+    # the reference from the same start block: same orthonormality (its replacement vectors
+    # are drawn from the same stream, but it orthogonalises the other way round, so only
+    # basis-independent quantities are compared)
+    Ao = best_oracle.matrix_from_csr(n, rp, ci, va)
+    Fo = best_oracle.factorization(Ao, start, 60, cf, (lo, hi), (3.0, 4.0))
+    assert Fo.expand(6) == 6
+    assert Fo.ortho_error() <= 1e-12
+
+
 def test_space_exhaustion_on_tiny_matrix():
     # lanczos_test.cpp:207-224 / :297-308: the whole space gets spanned, columns go dead
     n, rp, ci, va = M.diag_matrix([1, 2, 3, 4, 5])
