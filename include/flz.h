@@ -150,6 +150,16 @@ int flz_plan_ug(const flz_plan* plan, int64_t* sizes, int32_t* descriptors, doub
  * shared columns; dval[dense positions * 64].  Any pointer may be NULL. */
 int flz_plan_p2(const flz_plan* plan, int64_t* sizes, int64_t* ptr, int32_t* col, double* val,
                 int64_t* desc, int32_t* dcol, double* dval);
+/* hybrid layout of the plan (stencil + dense blocks, natural row order; host/plan.hpp), for
+ * host-side checks: sizes[12] = {used, slices, dense tasks, ints in cols, doubles in uvval,
+ * doubles in gval, ints in dcols, doubles in dval, partial slots, dense blocks, nonzeros in
+ * dense tasks, nonzeros at uniform-value positions}; slices[slices * 6] = {col_off, uv_off,
+ * g_off, nuv, ng, np}; tasks[dense tasks * 5] = {val_off, col_off, ncols, slot_base, nrows};
+ * diag[rows]; sell_rows[SELL slices * 32] row of every lane of the exact-mode arrays.  Any
+ * pointer may be NULL. */
+int flz_plan_hy(const flz_plan* plan, int64_t* sizes, int64_t* slices, int32_t* cols,
+                double* uvval, double* gval, double* diag, int64_t* tasks, int32_t* dcols,
+                double* dval, int32_t* sell_rows);
 /* tile plan of the TMA-staged stencil kernel (constant-coefficient stencils on one rank;
  * host/plan.hpp), for host-side checks: info[30] = {tile_rows, segments, seg_base[8],
  * seg_len[8], seg_start[8], staged elements per column, staged element of offset 0,

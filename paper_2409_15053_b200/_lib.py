@@ -95,6 +95,7 @@ _SIGS = {
     "flz_plan_arrays": (i32, [vp] + [vp] * 12),
     "flz_plan_ug": (i32, [vp, vp, vp, vp, vp, vp, vp]),
     "flz_plan_p2": (i32, [vp, vp, vp, vp, vp, vp, vp, vp]),
+    "flz_plan_hy": (i32, [vp] * 11),
     "flz_matrix_k1_info": (i32, [vp, i32, vp, vp, i32]),
     "flz_plan_tiles": (i32, [vp, vp, vp]),
     "flz_matvec_count": (u64, []),

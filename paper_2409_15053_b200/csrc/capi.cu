@@ -114,7 +114,8 @@ SellView make_view(const flz_matrix* A, const SliceTask* tasks, int64_t ntasks,
                   A->uv_pairs.p,    false,          A->p2_desc.p, A->p2_col.p, A->p2_val.p,
                   A->p2_dcol.p,     A->p2_dval.p,   nullptr,
                   // the tile kernel covers whole-matrix launches only
-                  (slice_ids == nullptr && nslices == A->nslices) ? A->tiles : StencilTiles{}};
+                  (slice_ids == nullptr && nslices == A->nslices) ? A->tiles : StencilTiles{},
+                  A->hy ? A->sell_rows.p : nullptr};
 }
 // fast mode on a matrix with the paired layout: the launch walks the paired task lists
 SellView paired(const flz_matrix* A, SellView v, int which) {
@@ -150,8 +151,18 @@ SellView view_boundary(const flz_matrix* A) {
   return paired(A, make_view(A, A->tasks_boundary.p, A->nt_boundary, A->boundary.p, A->n_boundary), 2);
 }
 
-// leading dimension of the planar filter workspaces (local rows + halo rows, padded)
-int64_t planar_ld(const flz_matrix* A) { return round_up(A->nl + A->nhalo, kLdAlign); }
+// leading dimension of the planar filter workspaces (local rows + halo rows, padded); the
+// hybrid layout needs row nl as a zero row (the target of lanes without an entry)
+int64_t planar_ld(const flz_matrix* A) {
+  return round_up(A->nl + A->nhalo + (A->hy ? 1 : 0), kLdAlign);
+}
+
+HyView hybrid_view(const flz_matrix* A) {
+  if (A->hy_p.count == 0) A->hy_p.reserve_zero((size_t)A->hy_ldp * kMaxFuse + 8, A->ctx->stream);
+  return HyView{A->nl,         A->nslices,    (int)A->hy_ndtasks, A->hy_maxcols, A->hy_slice.p,
+                A->hy_cols.p,  A->hy_uvval.p, A->hy_gval.p,       A->hy_diag.p,  A->hy_dtasks.p,
+                A->hy_dcols.p, A->hy_dval.p,  A->hy_p.p,          A->hy_ldp};
+}
 
 void ensure_workspaces(const flz_matrix* A) {
   flz_ctx* ctx = A->ctx;
@@ -213,6 +224,10 @@ void sell_step(const flz_matrix* A, int R, int S, StepMode mode, double s1, doub
     launch_clenshaw_step(ctx, view_rest(A, which), R, S, StepMode::rest, false, 0.0, 0.0, 0.0, Y1,
                          Y2, ldy, nullptr, 0, nullptr, 0);
   };
+  if (A->hy && !ctx->exact) {   // hybrid layout: planar blocks, dense tasks + slices
+    launch_hybrid_step(ctx, hybrid_view(A), R, mode, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo);
+    return;
+  }
   if (ctx->nranks == 1 || A->peers.empty()) {
     rest(0, A->nt_rest_all);
     launch_clenshaw_step(ctx, view_all(A), R, S, mode, ctx->exact, s1, s2, b, Y1, Y2, ldy, X, ldx,
@@ -236,6 +251,7 @@ void sell_step(const flz_matrix* A, int R, int S, StepMode mode, double s1, doub
 // The exact-mode kernel always reads interleaved rows of stride R.
 int row_stride(const flz_matrix* A, int R) {
   if (A->ctx->exact || A->nl == 0) return R;
+  if (A->hy) return 0;   // the hybrid kernels read planar blocks
   static const char* force = std::getenv("FLZ_K1_LAYOUT");  // experiments: planar | interleaved
   // planar blocks pay for stencil matrices with 3 columns on one GPU (100^3 Laplacian: 23.0 vs
   // 25.0 us per step: a coalesced 8-byte warp load touches 2-3 lines, a 24-byte-stride one 7);
@@ -250,6 +266,16 @@ int row_stride(const flz_matrix* A, int R) {
   return (A->nnz >= 16 * A->nl) ? 4 : 3;
 }
 
+// Hybrid layout: row nl of every plane of the gather source is the zero row (the target of
+// lanes without an entry).  The workspaces are shared with the interleaved layouts of the
+// exact-mode kernel, so the pad rows [nl, ld) are cleared whenever a block is (re)built.
+void zero_pad_rows(const flz_matrix* A, int R, int S, double* Y) {
+  if (!A->hy || S != 0) return;
+  const int64_t ldy = planar_ld(A);
+  FLZ_CUDA(cudaMemset2DAsync(Y + A->nl, (size_t)ldy * sizeof(double), 0,
+                             (size_t)(ldy - A->nl) * sizeof(double), (size_t)R, A->ctx->stream));
+}
+
 // Z[:, 0..ncols) = A X[:, 0..ncols), device-resident column-major blocks (permuted rows).
 void spmm_device(const flz_matrix* A, const double* X, int64_t ldx, int ncols, double* Z,
                  int64_t ldz, bool counted) {
@@ -258,6 +284,7 @@ void spmm_device(const flz_matrix* A, const double* X, int64_t ldx, int ncols, d
   for (int c0 = 0; c0 < ncols; c0 += kMaxFuse) {
     const int R = std::min(kMaxFuse, ncols - c0);
     const int S = row_stride(A, R);
+    zero_pad_rows(A, R, S, A->y1.p);
     launch_interleave(ctx, A->nl, R, S, 1.0, X + (int64_t)c0 * ldx, ldx, A->y1.p, planar_ld(A));
     sell_step(A, R, S, StepMode::plain, 1.0, 0.0, 0.0, A->y1.p, A->y2.p, nullptr, 0,
               Z + (int64_t)c0 * ldz, ldz);
@@ -286,6 +313,7 @@ void filter_device(const flz_matrix* A, const double* coeffs, int m, double c, d
     }
     double* Y1 = A->y1.p;
     double* Y2 = A->y2.p;
+    zero_pad_rows(A, R, S, Y1);
     launch_interleave(ctx, A->nl, R, S, coeffs[m], Xc, ldx, Y1, planar_ld(A));   // :144
     FLZ_CUDA(cudaMemsetAsync(Y2, 0, (S > 0 ? (size_t)A->nl * S : (size_t)planar_ld(A) * R) *
                                             sizeof(double), ctx->stream));
@@ -610,6 +638,37 @@ static void upload_plan(flz_ctx* ctx, HostPlan& P, flz_matrix* A) {
     A->p2_bytes = (int64_t)(P.p2_col.size() * 4 + P.p2_val.size() * 8 + P.p2_dcol.size() * 4 +
                             P.p2_dval.size() * 8 + P.p2_desc.size() * sizeof(P2Slice));
   }
+  A->hy = P.hy;
+  if (P.hy) {
+    static_assert(sizeof(PlanHySlice) == sizeof(HySlice) && sizeof(PlanHyTask) == sizeof(HyTask),
+                  "PlanHySlice / PlanHyTask mirror HySlice / HyTask");
+    A->hy_slice.reserve(std::max<size_t>(P.hy_slice.size(), 1));
+    if (!P.hy_slice.empty())
+      FLZ_CUDA(cudaMemcpyAsync(A->hy_slice.p, P.hy_slice.data(), P.hy_slice.size() * sizeof(HySlice),
+                               cudaMemcpyHostToDevice, ctx->stream));
+    A->hy_dtasks.reserve(std::max<size_t>(P.hy_dtasks.size(), 1));
+    if (!P.hy_dtasks.empty())
+      FLZ_CUDA(cudaMemcpyAsync(A->hy_dtasks.p, P.hy_dtasks.data(),
+                               P.hy_dtasks.size() * sizeof(HyTask), cudaMemcpyHostToDevice,
+                               ctx->stream));
+    up(A->hy_cols, P.hy_cols);
+    up(A->hy_dcols, P.hy_dcols);
+    up(A->hy_uvval, P.hy_uvval);
+    up(A->hy_gval, P.hy_gval);
+    up(A->hy_diag, P.hy_diag);
+    up(A->hy_dval, P.hy_dval);
+    up(A->sell_rows, P.sell_rows);
+    A->hy_ndtasks = (int64_t)P.hy_dtasks.size();
+    A->hy_ldp = round_up(P.hy_nslots, kLdAlign);
+    A->hy_maxcols = P.hy_maxcols;
+    A->hy_blocks = P.hy_blocks;
+    A->hy_dense_entries = P.hy_dense_entries;
+    A->hy_uv_entries = P.hy_uv_entries;
+    A->hy_bytes = (int64_t)(P.hy_cols.size() * 4 + P.hy_dcols.size() * 4 +
+                            (P.hy_uvval.size() + P.hy_gval.size() + P.hy_diag.size() +
+                             P.hy_dval.size()) * 8 +
+                            P.hy_slice.size() * sizeof(HySlice) + P.hy_dtasks.size() * sizeof(HyTask));
+  }
   A->ug_bytes = (int64_t)(P.ug_val.size() * 8 + P.ug_col.size() * 4 + P.ug_uoff.size() * 4 +
                           P.ug_slice.size() * sizeof(UgSlice));
   A->ug_uniform_entries = P.ug_uniform_entries;
@@ -874,6 +933,45 @@ int flz_plan_p2(const flz_plan* plan, int64_t* sizes, int64_t* ptr, int32_t* col
   return FLZ_OK;
 }
 
+int flz_plan_hy(const flz_plan* plan, int64_t* sizes, int64_t* slices, int32_t* cols,
+                double* uvval, double* gval, double* diag, int64_t* tasks, int32_t* dcols,
+                double* dval, int32_t* sell_rows) {
+  if (!plan) return FLZ_EINVAL;
+  const HostPlan& P = plan->P;
+  if (sizes) {
+    std::fill(sizes, sizes + 12, (int64_t)0);
+    if (P.hy) {
+      const int64_t v[12] = {1, (int64_t)P.hy_slice.size(), (int64_t)P.hy_dtasks.size(),
+                             (int64_t)P.hy_cols.size(), (int64_t)P.hy_uvval.size(),
+                             (int64_t)P.hy_gval.size(), (int64_t)P.hy_dcols.size(),
+                             (int64_t)P.hy_dval.size(), P.hy_nslots, P.hy_blocks,
+                             P.hy_dense_entries, P.hy_uv_entries};
+      std::copy(v, v + 12, sizes);
+    }
+  }
+  if (!P.hy) return FLZ_OK;
+  if (slices)
+    for (size_t s = 0; s < P.hy_slice.size(); ++s) {
+      const PlanHySlice& H = P.hy_slice[s];
+      const int64_t row[6] = {H.col_off, H.uv_off, H.g_off, H.nuv, H.ng, H.np};
+      std::copy(row, row + 6, slices + 6 * s);
+    }
+  if (tasks)
+    for (size_t t = 0; t < P.hy_dtasks.size(); ++t) {
+      const PlanHyTask& T = P.hy_dtasks[t];
+      const int64_t row[5] = {T.val_off, T.col_off, T.ncols, T.slot_base, T.nrows};
+      std::copy(row, row + 5, tasks + 5 * t);
+    }
+  if (cols) std::copy(P.hy_cols.begin(), P.hy_cols.end(), cols);
+  if (uvval) std::copy(P.hy_uvval.begin(), P.hy_uvval.end(), uvval);
+  if (gval) std::copy(P.hy_gval.begin(), P.hy_gval.end(), gval);
+  if (diag) std::copy_n(P.hy_diag.begin(), P.nl, diag);
+  if (dcols) std::copy(P.hy_dcols.begin(), P.hy_dcols.end(), dcols);
+  if (dval) std::copy(P.hy_dval.begin(), P.hy_dval.end(), dval);
+  if (sell_rows) std::copy(P.sell_rows.begin(), P.sell_rows.end(), sell_rows);
+  return FLZ_OK;
+}
+
 int flz_plan_tiles(const flz_plan* plan, int64_t* info, double* pairs) {
   if (!plan || !info) return FLZ_EINVAL;
   const HostPlan& P = plan->P;
@@ -917,8 +1015,9 @@ int flz_matrix_layout(const flz_matrix* A, int64_t* matrix_bytes, int64_t* unifo
   if (!A) return FLZ_EINVAL;
   // stencils with a tile plan: the TMA-staged kernel streams the (value, mask) pairs only
   if (matrix_bytes)
-    *matrix_bytes = A->p2 ? A->p2_bytes
-                          : (A->tiles.nseg > 0 ? (int64_t)A->uv_pairs.count * 8 : A->ug_bytes);
+    *matrix_bytes = A->hy ? A->hy_bytes
+                          : (A->p2 ? A->p2_bytes
+                                   : (A->tiles.nseg > 0 ? (int64_t)A->uv_pairs.count * 8 : A->ug_bytes));
   if (uniform_entries) *uniform_entries = A->ug_uniform_entries;
   return FLZ_OK;
 }
@@ -930,6 +1029,10 @@ int flz_matrix_k1_info(const flz_matrix* A, int r, int64_t* info, char* kernel, 
   if (A->ctx->exact) {
     name = "clenshaw_step_sell<EXACT>";
     matrix_bytes = A->stored * 12;
+  } else if (A->hy) {
+    name = "hybrid_dense_tasks + hybrid_slices (dense blocks + value-grouped slices)";
+    // dense partials: written once and read once per row and block
+    matrix_bytes = A->hy_bytes + 16 * A->hy_ndtasks * 32 * r;
   } else if (A->p2) {
     name = A->p2_blocks > 0 ? "clenshaw_step_p2_tasks (paired + dense sections)"
                             : "clenshaw_step_p2_tasks (paired)";
@@ -945,8 +1048,8 @@ int flz_matrix_k1_info(const flz_matrix* A, int r, int64_t* info, char* kernel, 
   const int64_t stride = S > 0 ? S : r;
   if (info) {
     info[0] = matrix_bytes + 8 * A->nl * (3 * stride + r);
-    info[1] = A->p2_blocks;
-    info[2] = A->p2_dense_entries;
+    info[1] = A->hy ? A->hy_blocks : A->p2_blocks;
+    info[2] = A->hy ? A->hy_dense_entries : A->p2_dense_entries;
     info[3] = S;
   }
   if (kernel && cap > 0) {

@@ -112,6 +112,20 @@ struct P2Slice {
   int32_t row0, nrows;
 };
 
+// Hybrid layout (mirrors PlanHySlice / PlanHyTask, host/plan.hpp)
+struct HySlice {
+  int64_t col_off;
+  int32_t uv_off, g_off;
+  int32_t nuv, ng, np;
+  int32_t pad;
+};
+struct HyTask {
+  int64_t val_off;
+  int32_t col_off, ncols;
+  int32_t slot_base, nrows;
+  int32_t pad[2];
+};
+
 struct UgSlice {
   int64_t val_ptr;
   int64_t col_ptr;
@@ -187,6 +201,17 @@ struct flz_matrix {
   flz::DevBuf<int32_t> p2_col, p2_dcol;
   flz::DevBuf<double> p2_val, p2_dval;
   int64_t p2_blocks = 0, p2_dense_entries = 0;
+  // hybrid layout (host/plan.hpp): natural row order, dense tasks + value-grouped slices
+  bool hy = false;
+  flz::DevBuf<flz::HySlice> hy_slice;
+  flz::DevBuf<flz::HyTask> hy_dtasks;
+  flz::DevBuf<int32_t> hy_cols, hy_dcols;
+  flz::DevBuf<double> hy_uvval, hy_gval, hy_diag, hy_dval;
+  mutable flz::DevBuf<double> hy_p;      // partial sums of the dense tasks, planar [k][hy_ldp]
+  int64_t hy_ndtasks = 0, hy_ldp = 0, hy_blocks = 0, hy_dense_entries = 0, hy_uv_entries = 0;
+  int hy_maxcols = 0;
+  int64_t hy_bytes = 0;
+  flz::DevBuf<int32_t> sell_rows;        // exact-mode SELL lane -> row (hybrid only)
   // task counters of the persistent paired kernel: one per launch, zeroed kTicketSlots at a time
   mutable flz::DevBuf<unsigned> k1_tickets;
   mutable int ticket_cursor = 0;
@@ -292,6 +317,23 @@ struct SellView {
   const double* p2_dval;
   unsigned* tickets;         // this launch's task counter (starts at 0; persistent CTAs)
   StencilTiles tiles;        // nseg > 0: tile plan of the TMA-staged stencil kernel
+  const int32_t* sell_rows;  // exact-mode kernel: SELL lane -> row (nullptr: slice * 32 + lane)
+};
+
+// Hybrid layout (host/plan.hpp) as the kernels see it
+struct HyView {
+  int64_t nl, nslices;
+  int ndtasks, maxcols;
+  const HySlice* slice;
+  const int32_t* cols;
+  const double* uvval;
+  const double* gval;
+  const double* diag;
+  const HyTask* dtasks;
+  const int32_t* dcols;
+  const double* dval;
+  double* P;                 // partial slots, planar [k][ldp]
+  int64_t ldp;
 };
 
 enum class StepMode { step, final, plain, rest };
@@ -306,6 +348,11 @@ enum class StepMode { step, final, plain, rest };
 void launch_clenshaw_step(flz_ctx* ctx, const SellView& A, int R, int S, StepMode mode, bool exact,
                           double s1, double s2, double b, const double* Y1, double* Y2,
                           int64_t ldy, const double* X, int64_t ldx, double* Out, int64_t ldo);
+// The same step on a matrix with the hybrid layout: PLANAR blocks (column k of Y1/Y2 at
+// k * ldy, row nl of Y1 must be zero), two launches (dense tasks, then the slices).
+void launch_hybrid_step(flz_ctx* ctx, const HyView& A, int R, StepMode mode, double s1, double s2,
+                        double b, const double* Y1, double* Y2, int64_t ldy, const double* X,
+                        int64_t ldx, double* Out, int64_t ldo);
 // All nsteps Clenshaw steps of one filter application (planar blocks B0 = Y1, B1 = Y2; the last
 // step applies (f1, f2) and writes Out) in ONE persistent launch of the TMA-staged stencil
 // kernel; coef[i] (device) is the reference's coefficient array (step i uses coef[nsteps-1-i]).

@@ -571,7 +571,7 @@ int64_t build_ug(HostPlan& P, const std::vector<uint8_t>& is_boundary, bool allo
 // median (the members of non-local projector balls on PARSEC-like Hamiltonians).  Greedy:
 // seeds in ascending row length (rows of a single ball first); candidate set K = the seed's
 // still uncovered long columns; two refinement passes keep the members adjacent to >= 80 % of
-// K; K is accepted when it has >= kDenseMin members and at least half of K x K is new.  All
+// K; K is accepted when it has >= kDenseMin members and at least a quarter of K x K is new.  All
 // entries (j, c), j and c in K, are then COVERED by the block.  Matrices without such blocks
 // cost a bounded number of failed seeds.
 struct DenseBlocks {
@@ -650,7 +650,9 @@ DenseBlocks extract_dense_blocks(int64_t nl, int64_t row_begin, const int64_t* r
           const int64_t c = local(e);
           fresh += (c >= 0 && c < nl && mark[c] && !B.covered[e - p0]) ? 1 : 0;
         }
-      ok = 2 * fresh >= (int64_t)K.size() * (int64_t)K.size();
+      // (a quarter is enough: a ball that overlaps an earlier block is still worth a block —
+      // the hybrid layout drops the columns a task does not use, the paired layout stores zeros)
+      ok = 4 * fresh >= (int64_t)K.size() * (int64_t)K.size();
       if (ok) {
         for (int32_t j : K)
           for (int64_t e = row_ptr[j]; e < row_ptr[j + 1]; ++e) {
@@ -678,6 +680,273 @@ DenseBlocks extract_dense_blocks(int64_t nl, int64_t row_begin, const int64_t* r
     for (int32_t j : B.members[b])
       if (B.count[j] == 1) B.primary[j] = (int32_t)b;
   return B;
+}
+
+// ---- hybrid layout (plan.hpp) ------------------------------------------------------------
+// Dense tasks from the blocks, slices from everything else; natural row order.  An entry
+// (i, c) that blocks cover belongs to the FIRST block (in creation order) that holds both i
+// and c — the block that covered it in extract_dense_blocks.
+void require(bool ok, const char* msg);
+void build_hybrid(HostPlan& P, const DenseBlocks& blocks, const int64_t* row_ptr,
+                  const int32_t* col_idx, const double* values) {
+  const int64_t nl = P.nl;
+  const int64_t p0 = row_ptr[0];
+  const int32_t zero_row = (int32_t)nl;
+  auto local = [&](int64_t e) { return (int32_t)((int64_t)col_idx[e] - P.row_begin); };
+  // membership lists (block, index inside the block), ascending block id
+  std::vector<int32_t> mem_ptr(nl + 1, 0);
+  for (const auto& K : blocks.members)
+    for (int32_t j : K) ++mem_ptr[j + 1];
+  for (int64_t i = 0; i < nl; ++i) mem_ptr[i + 1] += mem_ptr[i];
+  std::vector<int32_t> mem_blk(mem_ptr[nl]), fill(mem_ptr.begin(), mem_ptr.end() - 1);
+  for (size_t b = 0; b < blocks.members.size(); ++b)
+    for (int32_t j : blocks.members[b]) mem_blk[fill[j]++] = (int32_t)b;
+  auto owner = [&](int32_t i, int32_t c) -> int32_t {
+    for (int32_t a = mem_ptr[i]; a < mem_ptr[i + 1]; ++a)
+      for (int32_t q = mem_ptr[c]; q < mem_ptr[c + 1]; ++q)
+        if (mem_blk[a] == mem_blk[q]) return mem_blk[a];
+    return -1;
+  };
+  // ---- dense tasks: block b x 32 of its rows x the columns those rows own entries in (a task
+  // whose rows sit in the overlap with an earlier block drops that block's columns)
+  P.hy_dtasks.clear();
+  P.hy_dcols.clear();
+  std::vector<int32_t> slot_ptr(nl + 1, 0);
+  for (int64_t i = 0; i < nl; ++i) slot_ptr[i + 1] = slot_ptr[i] + (mem_ptr[i + 1] - mem_ptr[i]);
+  std::vector<int32_t> slots(slot_ptr[nl], 0), slot_fill(slot_ptr.begin(), slot_ptr.end() - 1);
+  struct TaskSpec {
+    int32_t block, g0, nrows;
+  };
+  std::vector<TaskSpec> spec;
+  for (size_t b = 0; b < blocks.members.size(); ++b) {
+    const int32_t nb = (int32_t)blocks.members[b].size();
+    for (int32_t g0 = 0; g0 < nb; g0 += kPlanSliceRows)
+      spec.push_back({(int32_t)b, g0, std::min<int32_t>(kPlanSliceRows, nb - g0)});
+  }
+  const int64_t nt = (int64_t)spec.size();
+  // pass 1 (threaded): the columns every task uses
+  std::vector<std::vector<int32_t>> task_cols(nt);
+  const int dchunks = (int)std::max<int64_t>(1, std::min<int64_t>(worker_count(), nt / 8));
+  run_chunks(dchunks, [&](int w) {
+    std::vector<uint8_t> used;
+    for (int64_t t = nt * w / dchunks; t < nt * (w + 1) / dchunks; ++t) {
+      const auto& rows = blocks.members[spec[t].block];
+      used.assign(rows.size(), 0);
+      for (int32_t q = 0; q < spec[t].nrows; ++q) {
+        const int32_t i = rows[spec[t].g0 + q];
+        for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
+          if (!blocks.covered[e - p0]) continue;
+          const int32_t c = local(e);
+          if (c == i || owner(i, c) != spec[t].block) continue;
+          used[std::lower_bound(rows.begin(), rows.end(), c) - rows.begin()] = 1;
+        }
+      }
+      for (size_t j = 0; j < rows.size(); ++j)
+        if (used[j]) task_cols[t].push_back(rows[j]);
+    }
+  });
+  int64_t nslots = kPlanSliceRows, nvals = 0;
+  int32_t maxcols = 1;
+  for (int64_t t = 0; t < nt; ++t) {
+    if (task_cols[t].empty()) continue;   // every entry of these rows belongs to earlier blocks
+    const auto& rows = blocks.members[spec[t].block];
+    PlanHyTask T{};
+    T.val_off = nvals;
+    T.col_off = (int32_t)P.hy_dcols.size();
+    T.ncols = (int32_t)task_cols[t].size();
+    T.slot_base = (int32_t)nslots;
+    T.nrows = spec[t].nrows;
+    T.pad[0] = (int32_t)t;   // spec index (host only)
+    P.hy_dcols.insert(P.hy_dcols.end(), task_cols[t].begin(), task_cols[t].end());
+    for (int32_t q = 0; q < T.nrows; ++q) slots[slot_fill[rows[spec[t].g0 + q]]++] = T.slot_base + q;
+    nslots += kPlanSliceRows;
+    nvals += T.ncols;
+    maxcols = std::max(maxcols, T.ncols);
+    P.hy_dtasks.push_back(T);
+  }
+  // rows of skipped tasks consume fewer slots than blocks they belong to: compact the lists
+  std::vector<int32_t> slot_cnt(nl, 0);
+  for (int64_t i = 0; i < nl; ++i) slot_cnt[i] = slot_fill[i] - slot_ptr[i];
+  require(nslots < ((int64_t)1 << 31) && nvals * kPlanSliceRows < ((int64_t)1 << 40),
+          "plan: hybrid layout overflow");
+  P.hy_nslots = nslots;
+  P.hy_maxcols = maxcols;
+  P.hy_blocks = (int64_t)blocks.members.size();
+  P.hy_dval.assign((size_t)std::max<int64_t>(nvals, 1) * kPlanSliceRows, 0.0);
+  const int64_t ntask = (int64_t)P.hy_dtasks.size();
+  std::vector<int64_t> dense_part(dchunks, 0);
+  run_chunks(dchunks, [&](int w) {
+    for (int64_t t = ntask * w / dchunks; t < ntask * (w + 1) / dchunks; ++t) {
+      PlanHyTask& T = P.hy_dtasks[t];
+      const TaskSpec& S = spec[T.pad[0]];
+      const auto& rows = blocks.members[S.block];
+      const int32_t* tc = P.hy_dcols.data() + T.col_off;
+      double* v = P.hy_dval.data() + T.val_off * kPlanSliceRows;
+      for (int32_t q = 0; q < T.nrows; ++q) {
+        const int32_t i = rows[S.g0 + q];
+        for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
+          if (!blocks.covered[e - p0]) continue;
+          const int32_t c = local(e);
+          if (c == i || owner(i, c) != S.block) continue;
+          const int64_t j = std::lower_bound(tc, tc + T.ncols, c) - tc;
+          v[j * kPlanSliceRows + q] = values[e];
+          ++dense_part[w];
+        }
+      }
+    }
+  });
+  for (auto& T : P.hy_dtasks) T.pad[0] = 0;
+  P.hy_dense_entries = 0;
+  for (int64_t x : dense_part) P.hy_dense_entries += x;
+  // ---- slices
+  const int64_t ns = (nl + kPlanSliceRows - 1) / kPlanSliceRows;
+  P.hy_slice.assign(ns, PlanHySlice{});
+  P.hy_diag.assign(std::max<int64_t>(nl, 1), 0.0);
+  struct Chunk {
+    std::vector<int32_t> cols;
+    std::vector<double> uv, gv;
+    int64_t uv_entries = 0, g_entries = 0;
+  };
+  const int schunks = (int)std::max<int64_t>(1, std::min<int64_t>(worker_count(), ns / 64));
+  std::vector<Chunk> chunk(schunks);
+  run_chunks(schunks, [&](int w) {
+    Chunk& C = chunk[w];
+    struct Ent {
+      uint64_t bits;
+      int32_t lane, col;
+      double v;
+    };
+    std::vector<Ent> ents;
+    std::vector<std::vector<std::pair<int32_t, double>>> gen(kPlanSliceRows);
+    std::vector<std::vector<int32_t>> per(kPlanSliceRows);
+    for (int64_t s = ns * w / schunks; s < ns * (w + 1) / schunks; ++s) {
+      ents.clear();
+      for (auto& g : gen) g.clear();
+      for (int l = 0; l < kPlanSliceRows; ++l) {
+        const int64_t i = s * kPlanSliceRows + l;
+        if (i >= nl) break;
+        for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
+          const int32_t c = local(e);
+          if (c == (int32_t)i) {
+            P.hy_diag[i] = values[e];
+            continue;
+          }
+          if (blocks.covered[e - p0]) continue;
+          uint64_t bits;
+          std::memcpy(&bits, &values[e], 8);
+          ents.push_back({bits, l, c, values[e]});
+        }
+      }
+      std::sort(ents.begin(), ents.end(), [](const Ent& a, const Ent& b) {
+        if (a.bits != b.bits) return a.bits < b.bits;
+        if (a.lane != b.lane) return a.lane < b.lane;
+        return a.col < b.col;
+      });
+      PlanHySlice& H = P.hy_slice[s];
+      H.col_off = (int64_t)C.cols.size() / kPlanSliceRows;   // chunk-relative for now
+      H.uv_off = (int32_t)C.uv.size();
+      H.g_off = (int32_t)(C.gv.size() / kPlanSliceRows);
+      // uniform-value groups
+      std::vector<std::vector<int32_t>> pos_cols;   // per position: 32 columns
+      for (size_t a = 0; a < ents.size();) {
+        size_t z = a;
+        int lanes = 0, last = -1;
+        while (z < ents.size() && ents[z].bits == ents[a].bits) {
+          if (ents[z].lane != last) {
+            ++lanes;
+            last = ents[z].lane;
+          }
+          ++z;
+        }
+        if (lanes >= kHyMinLanes) {
+          for (auto& v : per) v.clear();
+          size_t cnt = 0;
+          for (size_t q = a; q < z; ++q) {
+            per[ents[q].lane].push_back(ents[q].col);
+            cnt = std::max(cnt, per[ents[q].lane].size());
+          }
+          for (size_t q = 0; q < cnt; ++q) {
+            C.uv.push_back(ents[a].v);
+            pos_cols.emplace_back(kPlanSliceRows, zero_row);
+            for (int l = 0; l < kPlanSliceRows; ++l)
+              if (q < per[l].size()) {
+                pos_cols.back()[l] = per[l][q];
+                ++C.uv_entries;
+              }
+          }
+        } else {
+          for (size_t q = a; q < z; ++q) gen[ents[q].lane].push_back({ents[q].col, ents[q].v});
+        }
+        a = z;
+      }
+      while (pos_cols.size() % 4) {
+        pos_cols.emplace_back(kPlanSliceRows, zero_row);
+        C.uv.push_back(0.0);
+      }
+      H.nuv = (int32_t)pos_cols.size();
+      for (size_t q = 0; q < pos_cols.size(); q += 4)
+        for (int l = 0; l < kPlanSliceRows; ++l)
+          for (int u = 0; u < 4; ++u) C.cols.push_back(pos_cols[q + u][l]);
+      // general positions (ascending column per lane)
+      size_t ng = 0;
+      for (auto& g : gen) {
+        std::sort(g.begin(), g.end());
+        ng = std::max(ng, g.size());
+      }
+      for (size_t q = 0; q < ng; ++q)
+        for (int l = 0; l < kPlanSliceRows; ++l) {
+          const bool has = q < gen[l].size();
+          C.cols.push_back(has ? gen[l][q].first : zero_row);
+          C.gv.push_back(has ? gen[l][q].second : 0.0);
+          C.g_entries += has;
+        }
+      H.ng = (int32_t)ng;
+      // partial positions
+      int32_t np = 0;
+      for (int l = 0; l < kPlanSliceRows; ++l) {
+        const int64_t i = s * kPlanSliceRows + l;
+        if (i < nl) np = std::max(np, slot_cnt[i]);
+      }
+      for (int32_t q = 0; q < np; ++q)
+        for (int l = 0; l < kPlanSliceRows; ++l) {
+          const int64_t i = s * kPlanSliceRows + l;
+          const bool has = i < nl && q < slot_cnt[i];
+          C.cols.push_back(has ? slots[slot_ptr[i] + q] : 0);
+        }
+      H.np = np;
+    }
+  });
+  // concatenate the chunks
+  int64_t ncols = 0, nuvv = 0, ngv = 0;
+  for (auto& C : chunk) {
+    ncols += (int64_t)C.cols.size();
+    nuvv += (int64_t)C.uv.size();
+    ngv += (int64_t)C.gv.size();
+  }
+  require(nuvv < ((int64_t)1 << 31) && ngv / kPlanSliceRows < ((int64_t)1 << 31),
+          "plan: hybrid layout overflow");
+  P.hy_cols.resize(std::max<int64_t>(ncols, 1));
+  P.hy_uvval.resize(std::max<int64_t>(nuvv, 1));
+  P.hy_gval.resize(std::max<int64_t>(ngv, 1));
+  P.hy_uv_entries = P.hy_g_entries = 0;
+  int64_t bc = 0, bu = 0, bg = 0;
+  for (int w = 0; w < schunks; ++w) {
+    Chunk& C = chunk[w];
+    std::copy(C.cols.begin(), C.cols.end(), P.hy_cols.begin() + bc);
+    std::copy(C.uv.begin(), C.uv.end(), P.hy_uvval.begin() + bu);
+    std::copy(C.gv.begin(), C.gv.end(), P.hy_gval.begin() + bg);
+    for (int64_t s = ns * w / schunks; s < ns * (w + 1) / schunks; ++s) {
+      P.hy_slice[s].col_off += bc / kPlanSliceRows;
+      P.hy_slice[s].uv_off += (int32_t)bu;
+      P.hy_slice[s].g_off += (int32_t)(bg / kPlanSliceRows);
+    }
+    bc += (int64_t)C.cols.size();
+    bu += (int64_t)C.uv.size();
+    bg += (int64_t)C.gv.size();
+    P.hy_uv_entries += C.uv_entries;
+    P.hy_g_entries += C.g_entries;
+  }
+  P.hy = true;
 }
 
 // ---- paired layout (plan.hpp) ------------------------------------------------------------
@@ -908,6 +1177,8 @@ void build_ug_section(HostPlan& P, const std::vector<uint8_t>& is_boundary) {
 
 void ensure_ug(HostPlan& P) {
   if (!P.ug_skipped) return;
+  if (P.hy)   // its SELL arrays group rows through sell_rows; no kernel reads a UG copy of them
+    throw std::invalid_argument("plan: a hybrid plan has no index-compressed (UG) layout");
   std::vector<uint8_t> is_boundary(P.nslices, 0);
   for (int32_t s : P.boundary) is_boundary[s] = 1;
   build_ug_section(P, is_boundary);
@@ -1086,7 +1357,35 @@ HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<in
   if (p2_candidate && want_dense && sigma <= 0)
     blocks = extract_dense_blocks(nl, P.row_begin, row_ptr, col_idx, len, P.nnz);
   timer.lap("dense blocks");
-  if (blocks.any()) {
+  // HYBRID layout (plan.hpp): natural row order, dense tasks + value-grouped slices.  One rank
+  // only (the slices gather local rows); FLZ_HY=0 keeps the paired layout (experiments).
+  const bool want_hy = [] {   // read per plan, so that tests can switch it
+    const char* e = std::getenv("FLZ_HY");
+    return !(e && e[0] == '0');
+  }();
+  bool hybrid = want_hy && blocks.any() && nranks == 1;
+  if (hybrid) {
+    size_t widest = 0;
+    for (const auto& K : blocks.members) widest = std::max(widest, K.size());
+    hybrid = widest <= 1400;   // the staged block rows of a task must fit 48 KB of shared memory
+  }
+  if (hybrid) {
+    // what the blocks leave of every row must be short (the stencil): long leftovers (balls
+    // the block search missed, heavily overlapping balls) would become hundreds of general
+    // positions per slice — such matrices keep the paired layout
+    std::vector<int32_t> tmp(len);   // "short" = twice the 10th percentile of the row lengths
+    std::nth_element(tmp.begin(), tmp.begin() + nl / 10, tmp.end());
+    const int64_t limit = 2 * (int64_t)tmp[nl / 10] + 8;
+    int64_t excess = 0;
+    const int64_t q0 = row_ptr[0];
+    for (int64_t i = 0; i < nl; ++i) {
+      int64_t left = 0;
+      for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) left += blocks.covered[e - q0] ? 0 : 1;
+      excess += std::max<int64_t>(0, left - limit);
+    }
+    hybrid = 20 * excess <= P.nnz;
+  }
+  if (blocks.any() && !hybrid) {
     // row order: rows in several blocks (all entries general, longest first), then block by
     // block the rows that belong to that block only, then the rows outside every block in
     // natural order, pairs sorted by length class inside windows.  A slice never straddles
@@ -1245,7 +1544,12 @@ HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<in
       }
     }
   }
-  if (blocks.any()) {
+  std::vector<int32_t> sell_order;   // hybrid: grouping of the exact-mode SELL arrays only
+  if (hybrid) {
+    chosen = 1;
+    sort_windows(len, chosen, P.perm, nullptr);   // identity: the device order is the natural one
+    sort_windows(len, std::max<int64_t>(nl, 2), sell_order, nullptr);
+  } else if (blocks.any()) {
     P.perm = block_order;
     chosen = std::max<int64_t>(nl, 2);
   } else {
@@ -1288,12 +1592,17 @@ HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<in
   P.slice_ptr.assign(nslices + 1, 0);
   P.slice_len.assign(nslices, 0);
   P.row_len.assign(nslices * kPlanSliceRows, 0);
+  const std::vector<int32_t>& sell_of = hybrid ? sell_order : P.perm;   // SELL lane -> old row
+  if (hybrid) {
+    P.sell_rows.assign(nslices * kPlanSliceRows, -1);
+    std::copy(sell_order.begin(), sell_order.end(), P.sell_rows.begin());
+  }
   for (int64_t s = 0; s < nslices; ++s) {
     int32_t mx = 0;
     for (int l = 0; l < kPlanSliceRows; ++l) {
       const int64_t inew = s * kPlanSliceRows + l;
       if (inew >= nl) break;
-      P.row_len[inew] = len[P.perm[inew]];
+      P.row_len[inew] = len[sell_of[inew]];
       mx = std::max(mx, P.row_len[inew]);
     }
     P.slice_len[s] = mx;
@@ -1305,7 +1614,7 @@ HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<in
   std::vector<uint8_t> is_boundary(nslices, 0);
   // entries the dense sections of the paired layout hold (rows that belong to one block only)
   std::vector<uint8_t> skip;
-  if (blocks.any()) skip.assign(std::max<int64_t>(P.stored, 1), 0);
+  if (blocks.any() && !hybrid) skip.assign(std::max<int64_t>(P.stored, 1), 0);
   const int fill_chunks = (int)std::max<int64_t>(1, std::min<int64_t>(worker_count(), nslices / 256));
   run_chunks(fill_chunks, [&](int t) {
   for (int64_t s = nslices * t / fill_chunks; s < nslices * (t + 1) / fill_chunks; ++s)
@@ -1315,7 +1624,7 @@ HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<in
       const int32_t self = (int32_t)std::min<int64_t>(inew, std::max<int64_t>(nl - 1, 0));
       int32_t cnt = 0;
       if (inew < nl) {
-        const int64_t iold = P.perm[inew];
+        const int64_t iold = sell_of[inew];
         for (int64_t p = row_ptr[iold]; p < row_ptr[iold + 1]; ++p, ++cnt) {  // CSR order kept
           const int64_t g = col_idx[p];
           int32_t c;
@@ -1356,6 +1665,7 @@ HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<in
     for (int64_t s = 0; s < nslices; ++s) longest_slice = std::max(longest_slice, P.slice_len[s]);
     P.ug_skipped = want_p2 && !P.split && nl > 0 && p2_candidate && (longest_slice > 256 || blocks.any()) &&
                    std::getenv("FLZ_K1_T") == nullptr && std::getenv("FLZ_UG_ALWAYS") == nullptr;
+    if (hybrid) P.ug_skipped = true;
   }
   if (P.ug_skipped) {
     P.short_rows = false;
@@ -1365,7 +1675,11 @@ HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<in
   }
   timer.lap("UG layout");
   // long ragged rows: the paired layout feeds the fast kernel (FLZ_P2=0 keeps the UG tasks)
-  P.p2 = want_p2 && !P.split && !P.lean && nl > 0 && p2_candidate;
+  P.p2 = want_p2 && !P.split && !P.lean && nl > 0 && p2_candidate && !hybrid;
+  if (hybrid) {
+    build_hybrid(P, blocks, row_ptr, col_idx, values);
+    timer.lap("hybrid layout");
+  }
   if (P.p2) {
     if (!blocks.any()) {
       specs.clear();

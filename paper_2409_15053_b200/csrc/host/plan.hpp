@@ -70,6 +70,39 @@ struct PlanP2Slice {
   int32_t row0, nrows;
 };
 
+// HYBRID layout ("HY") for matrices that are a short-row part (a stencil) plus dense blocks
+// (non-local projector balls of PARSEC-like Hamiltonians), single rank.  Rows keep their
+// NATURAL order (no permutation), so that the lanes of a slice — 32 consecutive rows, i.e. a
+// run of grid points — gather runs of consecutive block rows.  A product is two launches:
+//  (1) DENSE tasks: block b, 32 of its rows (one per lane), all its columns.  The block rows of
+//      the block's columns are staged in shared memory once per task, the values stream as
+//      [column][lane] (8 bytes per entry, no index).  A task leaves one partial sum per row in
+//      the slot array P (slot_base + lane); slots 0..31 stay zero.
+//  (2) SLICE tasks over every row: the entries no block covers, grouped by VALUE —
+//      UNIFORM-VALUE positions (>= kHyMinLanes lanes of the slice hold an entry with the same
+//      number, e.g. a stencil weight: one double for the position, one int32 column per lane,
+//      4 bytes per entry), GENERAL positions (per-lane value and column) and PARTIAL positions
+//      (per-lane slot of P, value 1).  The diagonal is an own-row operand of the epilogue.
+//      Lanes without an entry at a position point at the zero row nl of the gather source.
+// Columns of uniform-value positions are stored [position / 4][lane][4] (one 16-byte load per
+// lane for 4 positions; nuv is padded to a multiple of 4), all others [position][lane].
+constexpr int kHyMinLanes = 8;
+struct PlanHySlice {   // 32 bytes
+  int64_t col_off;     // first position of the slice in hy_cols (units of 32 ints)
+  int32_t uv_off;      // into hy_uvval (even)
+  int32_t g_off;       // into hy_gval, units of 32 doubles
+  int32_t nuv, ng, np;
+  int32_t pad;
+};
+struct PlanHyTask {    // 32 bytes
+  int64_t val_off;     // into hy_dval, units of 32 doubles (one column of the task)
+  int32_t col_off;     // into hy_dcols
+  int32_t ncols;
+  int32_t slot_base;   // the task's 32 partial slots
+  int32_t nrows;
+  int32_t pad[2];
+};
+
 struct HostPlan {
   // partition
   int rank = 0, nranks = 1;
@@ -140,6 +173,20 @@ struct HostPlan {
   int64_t p2_entries = 0;                       // general positions * 32 (gathers per product)
   int64_t p2_blocks = 0;                        // dense blocks found
   int64_t p2_dense_entries = 0;                 // true nonzeros stored in dense sections
+  // HYBRID layout (see PlanHySlice); when set the device order is the natural one (perm =
+  // identity) and the CSR-order SELL arrays of the exact-mode kernel group the rows by length
+  // through sell_rows (SELL lane -> row, -1 = none) instead of a permutation of the vectors.
+  bool hy = false;
+  std::vector<PlanHySlice> hy_slice;            // [nslices]
+  std::vector<int32_t> hy_cols;
+  std::vector<double> hy_uvval, hy_gval, hy_diag;
+  std::vector<PlanHyTask> hy_dtasks;
+  std::vector<int32_t> hy_dcols;
+  std::vector<double> hy_dval;
+  int64_t hy_nslots = 0;                        // partial slots (multiple of 32, >= 32)
+  int32_t hy_maxcols = 0;                       // widest dense block
+  int64_t hy_blocks = 0, hy_dense_entries = 0, hy_uv_entries = 0, hy_g_entries = 0;
+  std::vector<int32_t> sell_rows;               // [nslices * 32] when hy, else empty
   // halo: sorted unique remote global columns; slot h lives at row nl + h of a gather source
   std::vector<int64_t> halo;
   std::vector<int64_t> need_off, need_cnt;  // per owner rank: run of `halo` it must send us

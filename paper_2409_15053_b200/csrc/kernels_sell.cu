@@ -327,8 +327,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
   const int64_t widx = (int64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
   if (widx >= A.nslices) return;
   const int64_t slice = A.slice_ids ? (int64_t)A.slice_ids[widx] : widx;
-  const int64_t row = slice * kSliceRows + lane;
-  const int len = A.row_len[row];
+  const int64_t sell_lane = slice * kSliceRows + lane;
+  // hybrid matrices group the rows of a SELL slice by length without permuting the vectors
+  const int64_t row = A.sell_rows ? (int64_t)A.sell_rows[sell_lane] : sell_lane;
+  const int len = A.row_len[sell_lane];
   const int L = A.slice_len[slice];
   const int64_t base = A.slice_ptr[slice] + lane;
   const double* __restrict__ val = A.val + base;
@@ -346,7 +348,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
       for (int k = 0; k < R; ++k) acc[k] = mul_add<EXACT>(v, Y1[(int64_t)c * R + k], acc[k]);
     }
   }
-  if (row >= A.nl) return;
+  if (row < 0 || row >= A.nl) return;
   if constexpr (MODE == 2) {  // plain: Out = A*Y1
 #pragma unroll
     for (int k = 0; k < R; ++k) Out[(int64_t)k * ldo + row] = acc[k];
@@ -1337,6 +1339,237 @@ __global__ void combine_kernel(int64_t n, double s1, double s2, double b,
   out[i] = combine<EXACT>(s1, w[i], s2, y1[i], y2[i], b, x[i]);
 }
 
+// --------------------------------------------------------------------- hybrid layout
+// (host/plan.hpp) Matrices that are a stencil plus dense blocks, natural row order, PLANAR
+// blocks.  Two launches per product, chained by programmatic dependent launch; everything a
+// CTA reads before its grid-dependency wait is immutable matrix data (the value stream of a
+// dense task, the first column words of a slice), so it overlaps the previous launch's tail.
+__device__ __forceinline__ int4 ld_stream_s32x4(const int* p) {
+  int4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
+constexpr int kHyDenseWarps = 4;
+#ifndef FLZ_HY_DU
+#define FLZ_HY_DU 4
+#endif
+#ifndef FLZ_HY_SLICE_CTAS
+#define FLZ_HY_SLICE_CTAS 8
+#endif
+
+// Dense task: 4 warps share the columns of the block; the block rows of ALL its columns are
+// staged in shared memory once (ys[ncols][4]), a lane owns one row of the task and streams its
+// values ([column][lane], 256 coalesced bytes per column).  Partial sums meet in shared memory
+// in a fixed order; warp 0 stores the task's 32 partials.
+template <int R>
+__global__ void __launch_bounds__(kHyDenseWarps * 32)
+    hybrid_dense_tasks(HyView A, const double* __restrict__ Y1, int64_t ldy) {
+  extern __shared__ __align__(16) double hy_smem[];
+  double (*ys)[4] = reinterpret_cast<double (*)[4]>(hy_smem);
+  double (*part)[R][32] = reinterpret_cast<double (*)[R][32]>(hy_smem + 4 * A.maxcols);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  pdl_launch_dependents();
+  const int4* tp = reinterpret_cast<const int4*>(A.dtasks + blockIdx.x);
+  const int4 t0 = __ldg(tp), t1 = __ldg(tp + 1);
+  const int64_t val_off = ((int64_t)(uint32_t)t0.y << 32) | (uint32_t)t0.x;
+  const int col_off = t0.z, ncols = t0.w, slot_base = t1.x;
+  const int chunk = (ncols + kHyDenseWarps - 1) / kHyDenseWarps;
+  const int j0 = min(ncols, warp * chunk), j1 = min(ncols, j0 + chunk);
+  const double* __restrict__ v = A.dval + val_off * 32 + lane;
+  constexpr int U = FLZ_HY_DU;
+  double a[U], nx[U];
+  auto fetch = [&](double (&dst)[U], int j) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) dst[u] = j + u < j1 ? ld_stream_f64(v + (int64_t)(j + u) * 32) : 0.0;
+  };
+  fetch(a, j0);
+  fetch(nx, j0 + U);
+  {  // the rest of this warp's value chunk: into L2 while the previous launch drains
+    const char* base = reinterpret_cast<const char*>(v - lane + (int64_t)(j0 + 2 * U) * 32);
+    const int lines = max(0, j1 - j0 - 2 * U) * 2;
+    for (int l = lane; l < lines; l += 32) prefetch_l2(base + (size_t)l * 128);
+  }
+  pdl_wait();
+  for (int j = threadIdx.x; j < ncols; j += kHyDenseWarps * 32) {
+    const int c = __ldg(A.dcols + col_off + j);
+#pragma unroll
+    for (int k = 0; k < R; ++k) ys[j][k] = __ldg(Y1 + (int64_t)k * ldy + c);
+  }
+  __syncthreads();
+  double acc[R];
+#pragma unroll
+  for (int k = 0; k < R; ++k) acc[k] = 0.0;
+  for (int j = j0; j < j1; j += U) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int jj = min(j + u, ncols - 1);   // past j1: zero value times a staged (finite) row
+      if constexpr (R >= 2) {
+        const double2 y01 = *reinterpret_cast<const double2*>(&ys[jj][0]);
+        acc[0] = fma(a[u], y01.x, acc[0]);
+        acc[1] = fma(a[u], y01.y, acc[1]);
+        if constexpr (R >= 3) {
+          const double2 y23 = *reinterpret_cast<const double2*>(&ys[jj][2]);
+          acc[2] = fma(a[u], y23.x, acc[2]);
+          if constexpr (R == 4) acc[3] = fma(a[u], y23.y, acc[3]);
+        }
+      } else {
+        acc[0] = fma(a[u], ys[jj][0], acc[0]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) a[u] = nx[u];
+    fetch(nx, j + 2 * U);
+  }
+  if (warp > 0) {
+#pragma unroll
+    for (int k = 0; k < R; ++k) part[warp - 1][k][lane] = acc[k];
+  }
+  __syncthreads();
+  if (warp == 0) {
+    for (int q = 0; q < kHyDenseWarps - 1; ++q)
+#pragma unroll
+      for (int k = 0; k < R; ++k) acc[k] += part[q][k][lane];
+#pragma unroll
+    for (int k = 0; k < R; ++k) A.P[(int64_t)k * A.ldp + slot_base + lane] = acc[k];
+  }
+}
+
+// Slices: one warp per 32 consecutive rows.  MODE 0 step (planar Y2 in place), 1 final (Out,
+// column-major ldo), 2 plain (Out = A Y1).
+template <int R, int MODE>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, FLZ_HY_SLICE_CTAS)
+    hybrid_slices(HyView A, double s1, double s2, double b, const double* __restrict__ Y1,
+                  double* __restrict__ Y2, int64_t ldy, const double* __restrict__ X, int64_t ldx,
+                  double* __restrict__ Out, int64_t ldo) {
+  const int lane = threadIdx.x & 31;
+  const int64_t slice = (int64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  pdl_launch_dependents();
+  if (slice >= A.nslices) {
+    pdl_wait();
+    return;
+  }
+  const int4* hp = reinterpret_cast<const int4*>(A.slice + slice);
+  const int4 h0 = __ldg(hp), h1 = __ldg(hp + 1);
+  const int64_t col_off = ((int64_t)(uint32_t)h0.y << 32) | (uint32_t)h0.x;
+  const int uv_off = h0.z, g_off = h0.w, nuv = h1.x, ng = h1.y, np = h1.z;
+  const int zero_row = (int)A.nl;
+  const int64_t row = slice * kSliceRows + lane;
+  const int* __restrict__ col = A.cols + col_off * 32 + lane * 4;
+  const double2* __restrict__ uv = reinterpret_cast<const double2*>(A.uvval + uv_off);
+  double acc[R];
+#pragma unroll
+  for (int k = 0; k < R; ++k) acc[k] = 0.0;
+  int4 c = nuv > 0 ? ld_stream_s32x4(col) : make_int4(zero_row, zero_row, zero_row, zero_row);
+  {  // this slice's remaining column words and position values: into L2 ahead of their use
+    const char* base = reinterpret_cast<const char*>(A.cols + col_off * 32);
+    const int lines = nuv + ng + np;   // 128 bytes per position
+    for (int l = lane + 4; l < lines; l += 32) prefetch_l2(base + (size_t)l * 128);
+    if (lane * 16 < nuv) prefetch_l2(reinterpret_cast<const char*>(uv) + lane * 128);
+  }
+  pdl_wait();
+  // uniform-value positions, 4 per round; the columns of round i+1 are requested before the
+  // gathers of round i are consumed
+  for (int p = 0; p < nuv; p += 4) {
+    double g[4][R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      g[0][k] = __ldg(Y1 + (int64_t)k * ldy + c.x);
+      g[1][k] = __ldg(Y1 + (int64_t)k * ldy + c.y);
+      g[2][k] = __ldg(Y1 + (int64_t)k * ldy + c.z);
+      g[3][k] = __ldg(Y1 + (int64_t)k * ldy + c.w);
+    }
+    const double2 v01 = __ldg(uv + (p >> 1)), v23 = __ldg(uv + (p >> 1) + 1);
+    col += 128;
+    if (p + 4 < nuv) c = ld_stream_s32x4(col);
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      acc[k] = fma(v01.x, g[0][k], acc[k]);
+      acc[k] = fma(v01.y, g[1][k], acc[k]);
+      acc[k] = fma(v23.x, g[2][k], acc[k]);
+      acc[k] = fma(v23.y, g[3][k], acc[k]);
+    }
+  }
+  const int* __restrict__ gcol = A.cols + (col_off + nuv) * 32 + lane;
+  // general positions: per-lane value and column
+  if (ng > 0) {
+    const double* __restrict__ gv = A.gval + (int64_t)g_off * 32 + lane;
+    for (int p = 0; p < ng; p += 4) {
+      int cc[4];
+      double v[4], g[4][R];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        cc[u] = p + u < ng ? ld_stream_s32(gcol + (p + u) * 32) : zero_row;
+        v[u] = p + u < ng ? ld_stream_f64(gv + (int64_t)(p + u) * 32) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int k = 0; k < R; ++k) g[u][k] = __ldg(Y1 + (int64_t)k * ldy + cc[u]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int k = 0; k < R; ++k) acc[k] = fma(v[u], g[u][k], acc[k]);
+    }
+    gcol += ng * 32;
+  }
+  // partial positions: what the dense tasks of this product left for the row
+  for (int p = 0; p < np; ++p) {
+    const int sl = ld_stream_s32(gcol + p * 32);
+#pragma unroll
+    for (int k = 0; k < R; ++k) acc[k] += A.P[(int64_t)k * A.ldp + sl];
+  }
+  if (row >= A.nl) return;
+  const double d = ld_stream_f64(A.diag + row);
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    const double y1 = __ldg(Y1 + (int64_t)k * ldy + row);
+    const double w = fma(d, y1, acc[k]);
+    if constexpr (MODE == 2) {
+      Out[(int64_t)k * ldo + row] = w;
+    } else {
+      const double y2 = Y2[(int64_t)k * ldy + row];
+      const double x = ld_stream_f64(X + (int64_t)k * ldx + row);
+      const double o = combine<false>(s1, w, s2, y1, y2, b, x);
+      if constexpr (MODE == 0)
+        Y2[(int64_t)k * ldy + row] = o;
+      else
+        Out[(int64_t)k * ldo + row] = o;
+    }
+  }
+}
+
+template <int R>
+void launch_hybrid_r(flz_ctx* ctx, const HyView& A, StepMode mode, double s1, double s2, double b,
+                     const double* Y1, double* Y2, int64_t ldy, const double* X, int64_t ldx,
+                     double* Out, int64_t ldo) {
+  if (A.nslices == 0) return;
+  if (A.ndtasks > 0) {
+    const size_t smem = (size_t)A.maxcols * 32 + (size_t)(kHyDenseWarps - 1) * R * 32 * 8;
+    launch_k1_smem(ctx, hybrid_dense_tasks<R>, (unsigned)A.ndtasks, kHyDenseWarps * 32, smem, A, Y1, ldy);
+    ctx->launches++;
+  }
+  const unsigned grid = (unsigned)((A.nslices + kWarpsPerBlock - 1) / kWarpsPerBlock);
+  switch (mode) {
+    case StepMode::step:
+      launch_k1(ctx, hybrid_slices<R, 0>, grid, kWarpsPerBlock * 32, A, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo);
+      break;
+    case StepMode::final:
+      launch_k1(ctx, hybrid_slices<R, 1>, grid, kWarpsPerBlock * 32, A, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo);
+      break;
+    case StepMode::plain:
+      launch_k1(ctx, hybrid_slices<R, 2>, grid, kWarpsPerBlock * 32, A, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo);
+      break;
+    default:
+      throw ApiError(FLZ_EINVAL, "hybrid step: unsupported mode");
+  }
+  ctx->launches++;
+}
+
 template <int R, int MODE>
 void launch_simple(flz_ctx* ctx, const SellView& A, double s1, double s2, double b,
                    const double* Y1, double* Y2, const double* X, int64_t ldx, double* Out,
@@ -1567,6 +1800,19 @@ void launch_clenshaw_step(flz_ctx* ctx, const SellView& A, int R, int S, StepMod
     default: throw ApiError(FLZ_EINVAL, "clenshaw step: unsupported (columns, stride) pair");
   }
 #undef FLZ_K1_CASE
+  FLZ_CUDA(cudaGetLastError());
+}
+
+void launch_hybrid_step(flz_ctx* ctx, const HyView& A, int R, StepMode mode, double s1, double s2,
+                        double b, const double* Y1, double* Y2, int64_t ldy, const double* X,
+                        int64_t ldx, double* Out, int64_t ldo) {
+  switch (R) {
+    case 1: launch_hybrid_r<1>(ctx, A, mode, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo); break;
+    case 2: launch_hybrid_r<2>(ctx, A, mode, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo); break;
+    case 3: launch_hybrid_r<3>(ctx, A, mode, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo); break;
+    case 4: launch_hybrid_r<4>(ctx, A, mode, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo); break;
+    default: throw ApiError(FLZ_EINVAL, "hybrid step: unsupported column count");
+  }
   FLZ_CUDA(cudaGetLastError());
 }
 

@@ -183,6 +183,66 @@ class HaloPlan:
                     desc=desc[:ns], dcol=dcol[:nd], dval=dval[:nd * 64], dense_positions=nd,
                     blocks=int(sizes[5]), dense_entries=int(sizes[6]))
 
+    def hy_arrays(self):
+        """Hybrid layout (dense tasks + value-grouped slices, natural row order), or None."""
+        sizes = np.zeros(12, np.int64)
+        vp = lambda a: a.ctypes.data_as(C.c_void_p)
+        check(lib().flz_plan_hy(self.handle, vp(sizes), *([None] * 9)))
+        if not sizes[0]:
+            return None
+        ns, nt = int(sizes[1]), int(sizes[2])
+        nl = self.info["rows_local"]
+        slices = np.zeros((max(ns, 1), 6), np.int64)
+        tasks = np.zeros((max(nt, 1), 5), np.int64)
+        cols = np.zeros(max(int(sizes[3]), 1), np.int32)
+        uvval = np.zeros(max(int(sizes[4]), 1), np.float64)
+        gval = np.zeros(max(int(sizes[5]), 1), np.float64)
+        diag = np.zeros(max(nl, 1), np.float64)
+        dcols = np.zeros(max(int(sizes[6]), 1), np.int32)
+        dval = np.zeros(max(int(sizes[7]), 1), np.float64)
+        sell_rows = np.zeros(max(self.info["slices"] * 32, 1), np.int32)
+        check(lib().flz_plan_hy(self.handle, vp(sizes), vp(slices), vp(cols), vp(uvval), vp(gval),
+                                vp(diag), vp(tasks), vp(dcols), vp(dval), vp(sell_rows)))
+        return dict(slices=slices[:ns], tasks=tasks[:nt], cols=cols, uvval=uvval, gval=gval,
+                    diag=diag[:nl], dcols=dcols, dval=dval, nslots=int(sizes[8]),
+                    blocks=int(sizes[9]), dense_entries=int(sizes[10]),
+                    uv_entries=int(sizes[11]), sell_rows=sell_rows)
+
+    def hy_product(self, x):
+        """y = A x evaluated from the hybrid layout as hybrid_dense_tasks / hybrid_slices walk
+        it: the dense tasks leave partial sums in slots, a slice adds its uniform-value
+        positions ([position / 4][lane][4] columns), its general positions, the partial slots
+        of its rows and the diagonal.  Row nl of the gather source is the zero row."""
+        hy = self.hy_arrays()
+        nl = self.info["rows_local"]
+        xz = np.concatenate([np.asarray(x, np.float64), [0.0]])
+        P = np.zeros(hy["nslots"])
+        for val_off, col_off, ncols, slot_base, nrows in hy["tasks"]:
+            v = hy["dval"][val_off * 32:(val_off + ncols) * 32].reshape(ncols, 32)
+            g = xz[hy["dcols"][col_off:col_off + ncols]]
+            assert np.all(P[slot_base:slot_base + 32] == 0) and 0 < nrows <= 32
+            assert not v[:, nrows:].any()
+            P[slot_base:slot_base + 32] = g @ v
+        assert not P[:32].any()
+        y = np.zeros(nl)
+        for s, (col_off, uv_off, g_off, nuv, ng, npart) in enumerate(hy["slices"]):
+            assert nuv % 4 == 0 and uv_off % 2 == 0
+            acc = np.zeros(32)
+            base = col_off * 32
+            c = hy["cols"][base:base + nuv * 32].reshape(nuv // 4, 32, 4)
+            for p in range(nuv):
+                acc += hy["uvval"][uv_off + p] * xz[c[p // 4, :, p % 4]]
+            base += nuv * 32
+            for p in range(ng):
+                acc += hy["gval"][(g_off + p) * 32:(g_off + p + 1) * 32] * xz[hy["cols"][base:base + 32]]
+                base += 32
+            for p in range(npart):
+                acc += P[hy["cols"][base:base + 32]]
+                base += 32
+            rows = np.arange(s * 32, min(nl, s * 32 + 32))
+            y[rows] = acc[:len(rows)] + hy["diag"][rows] * xz[rows]
+        return y
+
     def tile_plan(self):
         """Tile plan of the TMA-staged stencil kernel (flz_plan_tiles), or None."""
         info = np.zeros(30, np.int64)

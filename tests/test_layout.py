@@ -33,7 +33,8 @@ CASES = {
 
 
 @pytest.mark.parametrize("name", list(CASES))
-def test_ug_layout_reproduces_product(name):
+def test_ug_layout_reproduces_product(name, monkeypatch):
+    monkeypatch.setenv("FLZ_HY", "0")     # this test is about the UG layout (parsec7k has blocks)
     gen, want_split = CASES[name]
     csr = gen()
     n, rp, ci, va = csr
@@ -135,7 +136,8 @@ def _check_p2_slices(p2, n):
                                  lambda: M.parsec_like(radius=10.0, n_atoms=30, ball_radius=3.6),
                                  lambda: M.random_sparse_sym(700, 0.06, 5)])
 @pytest.mark.parametrize("dense", ["1", "0"])
-def test_paired_layout_reproduces_product(gen, dense):
+def test_paired_layout_reproduces_product(gen, dense, monkeypatch):
+    monkeypatch.setenv("FLZ_HY", "0")     # the paired layout (multi-rank / no-blocks fallback)
     """Long ragged rows: slices of up to 64 rows, two adjacent rows per lane, one column and
     two values per general position, one shared column per dense position (host/plan.hpp).
     The emulation walks it as clenshaw_step_p2_tasks does.  FLZ_P2_DENSE is read once per
@@ -162,7 +164,7 @@ def test_paired_layout_reproduces_product(gen, dense):
             np.savez(f, n=n, rp=rp, ci=ci, va=va)
             f.flush()
             r = subprocess.run([sys.executable, "-c", code, f.name],
-                               env=dict(os.environ, FLZ_P2_DENSE="0"), capture_output=True,
+                               env=dict(os.environ, FLZ_P2_DENSE="0", FLZ_HY="0"), capture_output=True,
                                text=True, timeout=600)
         assert r.returncode == 0, r.stderr[-2000:]
         return
@@ -182,7 +184,8 @@ def test_paired_layout_reproduces_product(gen, dense):
     assert p2["dense_entries"] == np.count_nonzero(p2["dval"]) or np.any(va == 0.0)
 
 
-def test_dense_blocks_of_a_parsec_shaped_matrix_are_found():
+def test_dense_blocks_of_a_parsec_shaped_matrix_are_found(monkeypatch):
+    monkeypatch.setenv("FLZ_HY", "0")
     """The non-local projector balls of a PARSEC-shaped Hamiltonian become dense sections: one
     block per atom, most of the nonzeros leave the general positions, a dense section is shared
     by rows of ONE block (its columns are exactly that block's members), and what is left per
@@ -212,6 +215,78 @@ def test_dense_blocks_of_a_parsec_shaped_matrix_are_found():
     x = np.random.default_rng(4).standard_normal(n)
     want = (A @ x)[perm]
     assert np.abs(P.p2_product(x[perm]) - want).max() <= 1e-12 * np.abs(want).max()
+
+
+def test_hybrid_layout_not_used_when_the_blocks_leave_long_rows():
+    """Heavily overlapping balls: the block search finds only some of the cliques, the rest of
+    those rows would be hundreds of general positions per slice — the paired layout stays."""
+    n, rp, ci, va = M.parsec_like(radius=10.0, n_atoms=30, ball_radius=3.6)
+    P = HaloPlan(n, 0, 1, [0, n], rp, ci, va)
+    assert P.hy_arrays() is None and P.p2_arrays() is not None
+
+
+@pytest.mark.parametrize("gen", [lambda: M.parsec_like(radius=14.0, n_atoms=24, ball_radius=3.4),
+                                 lambda: M.parsec_like(radius=12.0, n_atoms=10, seed=3),
+                                 lambda: M.parsec_like(radius=16.0, n_atoms=30, ball_radius=3.0, seed=5)])
+def test_hybrid_layout_reproduces_product(gen):
+    """Stencil + dense blocks on one rank: natural row order, dense tasks (block x 32 rows, values
+    only) and slices whose entries are grouped by value (host/plan.hpp).  The emulation walks
+    the arrays as hybrid_dense_tasks / hybrid_slices do."""
+    csr = gen()
+    n, rp, ci, va = csr
+    P = HaloPlan(n, 0, 1, [0, n], rp, ci, va)
+    hy = P.hy_arrays()
+    assert hy is not None and P.p2_arrays() is None
+    assert np.array_equal(P.arrays()["perm"], np.arange(n))          # no permutation
+    x = np.random.default_rng(9).standard_normal(n)
+    want = reference(csr, x)
+    assert np.abs(P.hy_product(x) - want).max() <= 1e-12 * np.abs(want).max()
+    sl, tk = hy["slices"], hy["tasks"]
+    # every nonzero is stored exactly once: dense tasks + uniform-value + general + diagonal
+    general = sum(np.count_nonzero(hy["gval"][g * 32:(g + ng) * 32]) for g, ng in zip(sl[:, 2], sl[:, 4]))
+    assert hy["dense_entries"] == np.count_nonzero(hy["dval"])
+    assert hy["dense_entries"] + hy["uv_entries"] + general + np.count_nonzero(hy["diag"]) == len(va)
+    assert hy["dense_entries"] >= 0.3 * len(va)
+    # the stencil part sits at uniform-value positions, 4 bytes per entry (36 per interior row)
+    assert hy["uv_entries"] >= 0.75 * 30 * n
+    # tasks: 32 slots each, one task per 32 rows of a block, slots 0..31 stay free
+    assert np.all(tk[:, 3] % 32 == 0) and tk[:, 3].min() == 32 and len(set(tk[:, 3])) == len(tk)
+    assert hy["nslots"] == 32 * (len(tk) + 1)
+    # exact-mode SELL arrays: rows grouped by length, every row once
+    rows = hy["sell_rows"]
+    assert np.array_equal(np.sort(rows[rows >= 0]), np.arange(n))
+
+
+def test_hybrid_layout_exact_mode_arrays_follow_sell_rows():
+    """The CSR-order SELL arrays of a hybrid plan list the rows through sell_rows while their
+    columns stay in the natural order (the vectors are not permuted)."""
+    csr = M.parsec_like(radius=12.0, n_atoms=12)
+    n, rp, ci, va = csr
+    P = HaloPlan(n, 0, 1, [0, n], rp, ci, va)
+    a, hy = P.arrays(), P.hy_arrays()
+    x = np.random.default_rng(2).standard_normal(n)
+    y = np.zeros(n)
+    for s in range(P.info["slices"]):
+        base, L = int(a["slice_ptr"][s]), int(a["slice_len"][s])
+        for lane in range(32):
+            row = int(hy["sell_rows"][s * 32 + lane])
+            if row < 0:
+                continue
+            k = int(a["row_len"][s * 32 + lane])
+            idx = base + lane + 32 * np.arange(k)
+            y[row] = np.dot(a["val"][idx], x[a["col"][idx]])
+    want = reference(csr, x)
+    assert np.abs(y - want).max() <= 1e-13 * np.abs(want).max()
+    # grouping by length keeps the padding small although the row order is the natural one
+    assert P.info["stored"] <= 1.2 * len(va)
+
+
+def test_hybrid_layout_is_single_rank_only():
+    csr = M.parsec_like(radius=12.0, n_atoms=12)
+    n, rp, ci, va = csr
+    starts = [0, n // 2, n]
+    P = HaloPlan(n, 0, 2, starts, rp[: n // 2 + 1], ci[: rp[n // 2]], va[: rp[n // 2]])
+    assert P.hy_arrays() is None
 
 
 def test_matrices_without_dense_blocks_keep_the_plain_paired_layout():
@@ -261,7 +336,8 @@ def test_paired_layout_odd_row_count_lone_row_longest():
     assert np.abs(y[:n] - want).max() <= 1e-12 * np.abs(want).max()
 
 
-def test_paired_layout_saves_gathers_on_dense_blocks():
+def test_paired_layout_saves_gathers_on_dense_blocks(monkeypatch):
+    monkeypatch.setenv("FLZ_HY", "0")
     csr = M.parsec_like(radius=14.0, n_atoms=20, ball_radius=3.25)
     n, rp, ci, va = csr
     p2 = HaloPlan(n, 0, 1, [0, n], rp, ci, va).p2_arrays()
