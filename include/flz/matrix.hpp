@@ -197,8 +197,18 @@ class SparseSymMatrix {
   mutable std::shared_ptr<DeviceCopy> dev_;
 };
 
+// Matrix Market coordinate files (real / integer / pattern, general / symmetric), with the
+// reference's rules and error messages (sparse.cpp:119-291).  The file is parsed by all host
+// threads (csrc/host/mmio.cpp).  When the environment variable FLZ_MM_CACHE names a directory
+// (or is "1": next to the file), the validated CSR arrays are kept there as a binary image
+// keyed by the file's size and modification time and later loads read that instead.
 SparseSymMatrix load_matrix_market(const std::string& path);
 void save_matrix_market(const SparseSymMatrix& A, const std::string& path);
+// Binary CSR image (extension): header + row_ptr (int64) + col_idx (int32) + values (f64).
+// load_binary_csr trusts the image's symmetry (it was validated when the image was written)
+// but re-checks its structure.
+void save_binary_csr(const SparseSymMatrix& A, const std::string& path);
+SparseSymMatrix load_binary_csr(const std::string& path);
 void save_dense_matrix_market(const DenseBlock& X, const std::string& path);
 
 std::uint64_t matvec_count();

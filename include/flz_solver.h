@@ -70,6 +70,10 @@ int flz_hostmatrix_from_local_rows(int64_t n_global, int64_t row_begin, int64_t 
                                    const double* values, flz_hostmatrix** out);
 int flz_hostmatrix_load_mm(const char* path, flz_hostmatrix** out);
 int flz_hostmatrix_save_mm(const flz_hostmatrix* A, const char* path);
+/* binary CSR image (extension; csrc/host/mmio.cpp): header + row_ptr + col_idx + values.
+ * flz_hostmatrix_load_mm keeps such images itself when FLZ_MM_CACHE names a directory. */
+int flz_hostmatrix_save_bin(const flz_hostmatrix* A, const char* path);
+int flz_hostmatrix_load_bin(const char* path, flz_hostmatrix** out);
 void flz_hostmatrix_free(flz_hostmatrix* A);
 int flz_hostmatrix_dims(const flz_hostmatrix* A, int64_t* n, int64_t* nnz);
 /* device layout of the matrix (uploads it when it is not resident yet): bytes of the

@@ -252,6 +252,38 @@ class Oracle:
             raise OracleError(self.last_error())
         return Matrix(self, h)
 
+    def load_matrix_market(self, path):
+        """(n, row_ptr, col_idx, values) as the reference's own Matrix Market loader builds them
+        (reference build only).  Runs in a fresh interpreter without NumPy: the reference's
+        iostream-based loader crashes when it is called in a process that has loaded NumPy's
+        bundled runtime libraries first."""
+        import subprocess, sys, tempfile
+        code = (
+            "import ctypes as C, sys\n"
+            "L = C.CDLL(sys.argv[1])\n"
+            "f = L.ref_matrix_load_mm; f.restype = C.c_void_p; f.argtypes = [C.c_char_p]\n"
+            "h = f(sys.argv[2].encode())\n"
+            "e = L.ref_last_error; e.restype = C.c_char_p\n"
+            "if not h: sys.exit('ERR ' + e().decode())\n"
+            "d = L.ref_matrix_dim; d.restype = C.c_int64; d.argtypes = [C.c_void_p]\n"
+            "z = L.ref_matrix_nnz; z.restype = C.c_int64; z.argtypes = [C.c_void_p]\n"
+            "n, nnz = d(h), z(h)\n"
+            "rp = (C.c_int64 * (n + 1))(); ci = (C.c_int32 * max(nnz, 1))(); va = (C.c_double * max(nnz, 1))()\n"
+            "g = L.ref_matrix_csr; g.restype = None; g.argtypes = [C.c_void_p] * 4\n"
+            "g(h, rp, ci, va)\n"
+            "open(sys.argv[3], 'wb').write(bytes(C.c_int64(n)) + bytes(C.c_int64(nnz)) + bytes(rp) + bytes(ci)[:4 * nnz] + bytes(va)[:8 * nnz])\n")
+        with tempfile.NamedTemporaryFile(suffix=".bin") as out:
+            r = subprocess.run([sys.executable, "-S", "-c", code, self.path, str(path), out.name],
+                               capture_output=True, text=True, timeout=600)
+            if r.returncode != 0:
+                raise OracleError(r.stderr.strip()[-500:])
+            raw = open(out.name, "rb").read()
+        n, nnz = np.frombuffer(raw, np.int64, 2)
+        rp = np.frombuffer(raw, np.int64, n + 1, 16)
+        ci = np.frombuffer(raw, np.int32, nnz, 16 + 8 * (n + 1))
+        va = np.frombuffer(raw, np.float64, nnz, 16 + 8 * (n + 1) + 4 * nnz)
+        return int(n), rp, ci, va
+
     def matrix_from_triplets(self, n, rows, cols, values) -> Matrix:
         rows = np.ascontiguousarray(rows, np.int64)
         h = self._f("matrix_from_triplets")(n, len(rows), rows,

@@ -136,6 +136,13 @@ void* ref_matrix_from_csr(int64_t n, const int64_t* row_ptr, const int32_t* col_
     return nullptr;
   return out;
 }
+// reference-only extra (not part of oracle_abi.h): the reference's own Matrix Market loader
+// (sparse.cpp:172-291), the yardstick of the product's multi-threaded loader
+void* ref_matrix_load_mm(const char* path) {
+  SparseSymMatrix* out = nullptr;
+  if (guard([&] { out = new SparseSymMatrix(load_matrix_market(path)); })) return nullptr;
+  return out;
+}
 void ref_matrix_free(void* A) { delete static_cast<SparseSymMatrix*>(A); }
 int64_t ref_matrix_dim(void* A) { return static_cast<SparseSymMatrix*>(A)->dim(); }
 int64_t ref_matrix_nnz(void* A) { return static_cast<SparseSymMatrix*>(A)->nnz(); }

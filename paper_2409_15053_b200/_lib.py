@@ -132,6 +132,8 @@ _SOLVER_SIGS = {
     "flz_hostmatrix_from_csr": (i32, [i64, i64p, i32p, f64p, i32, C.POINTER(vp)]),
     "flz_hostmatrix_from_local_rows": (i32, [i64, i64, i64, i64p, i32p, f64p, C.POINTER(vp)]),
     "flz_hostmatrix_load_mm": (i32, [C.c_char_p, C.POINTER(vp)]),
+    "flz_hostmatrix_save_bin": (i32, [vp, C.c_char_p]),
+    "flz_hostmatrix_load_bin": (i32, [C.c_char_p, C.POINTER(vp)]),
     "flz_hostmatrix_save_mm": (i32, [vp, C.c_char_p]),
     "flz_hostmatrix_free": (None, [vp]),
     "flz_hostmatrix_dims": (i32, [vp, i64P, i64P]),

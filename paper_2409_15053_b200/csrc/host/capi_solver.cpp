@@ -154,6 +154,12 @@ int flz_hostmatrix_load_mm(const char* path, flz_hostmatrix** out) {
 int flz_hostmatrix_save_mm(const flz_hostmatrix* A, const char* path) {
   return wrap([&] { save_matrix_market(A->A, path); });
 }
+int flz_hostmatrix_save_bin(const flz_hostmatrix* A, const char* path) {
+  return wrap([&] { save_binary_csr(A->A, path); });
+}
+int flz_hostmatrix_load_bin(const char* path, flz_hostmatrix** out) {
+  return wrap([&] { *out = new flz_hostmatrix{load_binary_csr(path)}; });
+}
 void flz_hostmatrix_free(flz_hostmatrix* A) { delete A; }
 int flz_hostmatrix_dims(const flz_hostmatrix* A, int64_t* n, int64_t* nnz) {
   if (n) *n = static_cast<int64_t>(A->A.dim());

@@ -388,7 +388,11 @@ enum class Field { real, integer, pattern };
 
 }  // namespace
 
-SparseSymMatrix load_matrix_market(const std::string& path) {
+// The reference's loader, line by line (sparse.cpp:172-291): the fast loader in mmio.cpp
+// produces the same matrix for well-formed files and hands every file it finds anything wrong
+// with to this function, so that errors carry the reference's messages and line numbers.
+namespace detail {
+SparseSymMatrix load_matrix_market_sequential(const std::string& path) {
   std::ifstream in(path, std::ios::binary);
   if (!in) throw Error("cannot open '" + path + "'");
   std::string text((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
@@ -538,6 +542,7 @@ SparseSymMatrix load_matrix_market(const std::string& path) {
   }
   return SparseSymMatrix::from_entries(static_cast<std::size_t>(rows), std::move(entries));
 }
+}  // namespace detail
 
 void save_matrix_market(const SparseSymMatrix& A, const std::string& path) {
   std::FILE* fp = std::fopen(path.c_str(), "w");

@@ -78,6 +78,16 @@ class SparseSymMatrix:
     def save_matrix_market(self, path):
         check(lib().flz_hostmatrix_save_mm(self.handle, str(path).encode()))
 
+    @classmethod
+    def load_binary(cls, path):
+        """Binary CSR image written by save_binary (or by the FLZ_MM_CACHE of the loader)."""
+        h = C.c_void_p()
+        check(lib().flz_hostmatrix_load_bin(str(path).encode(), C.byref(h)))
+        return cls(h)
+
+    def save_binary(self, path):
+        check(lib().flz_hostmatrix_save_bin(self.handle, str(path).encode()))
+
     def layout(self):
         """Device layout (uploads the matrix if needed): bytes the fused Clenshaw step streams
         for the matrix, and the nonzeros held at uniform-offset positions."""

@@ -203,3 +203,74 @@ def test_matrix_market_errors(tmp_path, text, needle):
     assert needle in str(e.value)
     with pytest.raises(FlzError):
         S.SparseSymMatrix.load_matrix_market(tmp_path / "missing.mtx")
+
+
+def _write_mm(path, n, rows, cols, vals, symmetry="symmetric", shuffle=None, comments=True):
+    order = np.arange(len(rows)) if shuffle is None else np.random.default_rng(shuffle).permutation(len(rows))
+    with open(path, "w") as f:
+        f.write(f"%%MatrixMarket matrix coordinate real {symmetry}\n")
+        if comments:
+            f.write("% a comment\n\n%another\n")
+        f.write(f"{n} {n} {len(rows)}\n")
+        for k in order:
+            f.write(f"{rows[k] + 1} {cols[k] + 1} {vals[k]:.17g}\n")
+            if comments and k % 97 == 0:
+                f.write("   \n")
+
+
+def test_fast_matrix_market_loader_matches_the_reference_loader(tmp_path, best_oracle, monkeypatch):
+    """The multi-threaded loader (csrc/host/mmio.cpp) builds exactly the CSR arrays of the
+    reference's loader (sparse.cpp:172-291): symmetric files in shuffled order with blank and
+    comment lines, general files that get symmetrised, a file with duplicate entries, several
+    thread counts (pieces are cut at line ends)."""
+    n, rp, ci, va = M.parsec_like(radius=9.0, n_atoms=6)            # 3k rows, 250k entries
+    rows = np.repeat(np.arange(n), np.diff(rp))
+    low = ci <= rows
+    sym = tmp_path / "sym.mtx"
+    _write_mm(sym, n, rows[low], ci[low], va[low], shuffle=3)
+    gen = tmp_path / "gen.mtx"
+    noisy = va * (1.0 + 1e-14 * np.random.default_rng(1).standard_normal(len(va)))
+    _write_mm(gen, n, rows, ci, noisy, symmetry="general", shuffle=4)
+    dup = tmp_path / "dup.mtx"
+    k = low.nonzero()[0]
+    _write_mm(dup, n, np.concatenate([rows[k], rows[k[:50]]]), np.concatenate([ci[k], ci[k[:50]]]),
+              np.concatenate([va[k], 0.25 * va[k[:50]]]), shuffle=5)
+    for threads in ("1", "3", "16"):
+        monkeypatch.setenv("FLZ_HOST_THREADS", threads)
+        for path in (sym, gen, dup):
+            got = S.SparseSymMatrix.load_matrix_market(path).csr()
+            if best_oracle.kind == "reference":
+                want = best_oracle.load_matrix_market(str(path))
+                assert all(np.array_equal(x, y) for x, y in zip(got, want[1:])), (path, threads)
+        got = S.SparseSymMatrix.load_matrix_market(sym).csr()
+        assert np.array_equal(got[0], rp) and np.array_equal(got[1], ci) and np.array_equal(got[2], va)
+
+
+def test_binary_csr_image_and_cache(tmp_path, monkeypatch):
+    n, rp, ci, va = M.random_sparse_sym(300, 0.05, 2)
+    A = S.SparseSymMatrix.from_csr(n, rp, ci, va)
+    img = tmp_path / "a.flzcsr"
+    A.save_binary(img)
+    B = S.SparseSymMatrix.load_binary(img)
+    assert all(np.array_equal(x, y) for x, y in zip(A.csr(), B.csr()))
+    with open(img, "r+b") as f:                      # truncated image
+        f.truncate(os.path.getsize(img) - 8)
+    with pytest.raises(FlzError):
+        S.SparseSymMatrix.load_binary(img)
+    # cache of the text loader: keyed by size + mtime of the source
+    mtx = tmp_path / "a.mtx"
+    A.save_matrix_market(mtx)
+    cache = tmp_path / "cache"
+    cache.mkdir()
+    monkeypatch.setenv("FLZ_MM_CACHE", str(cache))
+    first = S.SparseSymMatrix.load_matrix_market(mtx).csr()
+    images = list(cache.iterdir())
+    assert len(images) == 1 and images[0].name.endswith(".flzcsr")
+    again = S.SparseSymMatrix.load_matrix_market(mtx).csr()      # served by the image
+    assert all(np.array_equal(x, y) for x, y in zip(first, again))
+    # a changed source invalidates the image
+    n2, rp2, ci2, va2 = M.random_sparse_sym(300, 0.05, 3)
+    S.SparseSymMatrix.from_csr(n2, rp2, ci2, va2).save_matrix_market(mtx)
+    os.utime(mtx, ns=(1, 10**18))
+    third = S.SparseSymMatrix.load_matrix_market(mtx).csr()
+    assert np.array_equal(third[2], va2)
