@@ -32,6 +32,9 @@ typedef struct {
    * recovery and return only eigenvalues and residuals (large runs: n x count doubles need
    * not cross PCIe); flz_config_default sets 1 */
   int32_t return_vectors;
+  /* extension: != 0 multiplies the filter coefficients by the Jackson kernel factors on the
+   * host (off by default: the reference has no damping) */
+  int32_t jackson_damping;
 } flz_config;
 
 /* speig::SolveStats (lanczos.hpp:136-155) + the GPU build's host buckets. */
@@ -94,6 +97,8 @@ int flz_hostmatrix_filter_apply(const flz_hostmatrix* A, const double* coeffs, i
 
 /* ---- filter scalars (filter.cpp:33-96, :163-184); host arithmetic ---- */
 int flz_indicator_coefficients(double alpha_s, double beta_s, int degree, double* out);
+/* Jackson kernel factors g_0..g_degree (extension; flz/chebyshev.hpp) */
+int flz_jackson_factors(int degree, double* out);
 int flz_select_degree(double alpha_s, double beta_s, double epsilon, int max_degree,
                       int* clamped); /* returns the degree, < 0 on error */
 double flz_clenshaw(const double* coeffs, int ncoeffs, double t);

@@ -41,7 +41,7 @@ class FlzConfig(C.Structure):
         ("check_every", C.c_int32), ("seed", C.c_uint64), ("extra_ritz", C.c_int32),
         ("bounds_steps", C.c_int32), ("degree", C.c_int32), ("epsilon", C.c_double),
         ("max_degree", C.c_int32), ("collect_diagnostics", C.c_int32),
-        ("return_vectors", C.c_int32),
+        ("return_vectors", C.c_int32), ("jackson_damping", C.c_int32),
     ]
 
 
@@ -143,6 +143,7 @@ _SOLVER_SIGS = {
     "flz_hostmatrix_spmm": (i32, [vp, f64p, i64, i32, f64p]),
     "flz_hostmatrix_filter_apply": (i32, [vp, f64p, i32, d, d, f64p, i64, i32, f64p]),
     "flz_indicator_coefficients": (i32, [d, d, i32, f64p]),
+    "flz_jackson_factors": (i32, [i32, f64p]),
     "flz_select_degree": (i32, [d, d, d, i32, iP]),
     "flz_clenshaw": (d, [f64p, i32, d]),
     "flz_build_filter": (i32, [d, d, d, d, i32, d, i32, vp, i32, dP, dP, iP]),

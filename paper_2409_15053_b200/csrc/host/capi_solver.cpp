@@ -72,6 +72,7 @@ LanczosConfig to_config(const flz_config& c) {
   k.max_degree = c.max_degree;
   k.collect_diagnostics = c.collect_diagnostics != 0;
   k.return_vectors = c.return_vectors != 0;
+  k.jackson_damping = c.jackson_damping != 0;
   return k;
 }
 
@@ -100,6 +101,7 @@ void flz_config_default(flz_config* cfg) {
   cfg->max_degree = k.max_degree;
   cfg->collect_diagnostics = 0;
   cfg->return_vectors = 1;
+  cfg->jackson_damping = 0;
 }
 
 int flz_set_default_ctx(flz_ctx* ctx) {
@@ -211,6 +213,12 @@ int flz_indicator_coefficients(double alpha_s, double beta_s, int degree, double
   return wrap([&] {
     const auto b = indicator_coefficients(alpha_s, beta_s, degree);
     std::copy(b.begin(), b.end(), out);
+  });
+}
+int flz_jackson_factors(int degree, double* out) {
+  return wrap([&] {
+    const auto g = jackson_factors(degree);
+    std::copy(g.begin(), g.end(), out);
   });
 }
 int flz_select_degree(double alpha_s, double beta_s, double epsilon, int max_degree,

@@ -634,8 +634,10 @@ EigenResult run_solve(const SparseSymMatrix& A, double alpha, double beta,
                         std::to_string(bounds.lambda_max()) + "]");
 
   std::optional<ChebyshevFilter> filter;
-  if (kind == OperatorKind::filtered)
+  if (kind == OperatorKind::filtered) {
     filter = build_filter(bounds, alpha, beta, cfg.degree, cfg.epsilon, cfg.max_degree);
+    if (cfg.jackson_damping) filter = filter->damped();   // opt-in, host side only
+  }
   const BlockOperator op =
       filter ? BlockOperator::filtered(A, *filter) : BlockOperator::plain(A);
 

@@ -15,12 +15,15 @@ from .device import _fcol, _from_fcol, _ptr
 
 def LanczosConfig(block_size=3, tol=1e-10, max_dim=0, check_every=10, seed=20177, extra_ritz=5,
                   bounds_steps=50, degree=0, epsilon=0.255, max_degree=1000,
-                  collect_diagnostics=False, return_vectors=True) -> FlzConfig:
+                  collect_diagnostics=False, return_vectors=True,
+                  jackson_damping=False) -> FlzConfig:
     """speig::LanczosConfig defaults (lanczos.hpp:14-29); degree<=0 / None = automatic.
-    ``return_vectors=False`` (extension) keeps the eigenvectors off the host."""
+    ``return_vectors=False`` (extension) keeps the eigenvectors off the host;
+    ``jackson_damping=True`` (extension, the reference has no damping) Jackson-damps the
+    filter coefficients on the host."""
     return FlzConfig(block_size, tol, max_dim, check_every, seed, extra_ritz, bounds_steps,
                      int(degree or 0), epsilon, max_degree, int(collect_diagnostics),
-                     int(return_vectors))
+                     int(return_vectors), int(jackson_damping))
 
 
 @dataclass
@@ -139,6 +142,13 @@ def matvec_count() -> int:
 def indicator_coefficients(a, b, degree):
     out = np.empty(degree + 1)
     check(lib().flz_indicator_coefficients(a, b, degree, out))
+    return out
+
+
+def jackson_factors(degree):
+    """Jackson kernel factors g_0..g_degree (extension: the reference has no damping)."""
+    out = np.empty(degree + 1)
+    check(lib().flz_jackson_factors(degree, out))
     return out
 
 

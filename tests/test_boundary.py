@@ -106,3 +106,31 @@ def test_product_never_touches_the_oracle():
     assert not offenders, offenders
     deps = subprocess.run(["ldd", _lib.LIB_PATH], capture_output=True, text=True).stdout
     assert "speig" not in deps and "oracle" not in deps
+
+
+EXT_SRC = os.path.join(ROOT, "tests", "ext", "speig_user.cpp")
+
+
+def _build_external_program(tmp_path):
+    """A program written against the reference's API (speig:: names via one alias line) is
+    compiled against include/flz/*.hpp and linked with libflz.so only."""
+    exe = str(tmp_path / "speig_user")
+    cmd = ["g++", "-std=c++20", "-O1", "-Wall", "-Wextra", "-I" + os.path.join(ROOT, "include"),
+           "-o", exe, EXT_SRC, "-L" + _lib.PKG_DIR, "-l:libflz.so", "-Wl,-rpath," + _lib.PKG_DIR,
+           "-L/usr/local/cuda/lib64", "-Wl,-rpath-link,/usr/local/cuda/lib64"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    return exe
+
+
+def test_external_program_compiles_against_the_drop_in_headers(tmp_path):
+    exe = _build_external_program(tmp_path)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)    # host-only part
+    assert r.returncode == 0 and r.stdout.strip() == "OK", r.stdout + r.stderr
+
+
+@pytest.mark.gpu
+def test_external_program_solves_and_pokes_the_kernel_seam(tmp_path):
+    exe = _build_external_program(tmp_path)
+    r = subprocess.run([exe, "solve"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and r.stdout.strip() == "OK", r.stdout + r.stderr

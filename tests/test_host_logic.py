@@ -274,3 +274,26 @@ def test_binary_csr_image_and_cache(tmp_path, monkeypatch):
     os.utime(mtx, ns=(1, 10**18))
     third = S.SparseSymMatrix.load_matrix_market(mtx).csr()
     assert np.array_equal(third[2], va2)
+
+
+def test_jackson_damping_is_an_opt_in_extension():
+    """Default = the reference's undamped coefficients (its degrees, tau cuts and iteration
+    counts depend on them); the Jackson factors are a host-side option.  Known properties of the
+    kernel: g_0 = 1, strictly decreasing to ~0, and the damped indicator series stays inside
+    [0, 1] (no Gibbs overshoot) while the undamped one does not."""
+    m = 80
+    g = S.jackson_factors(m)
+    assert len(g) == m + 1 and abs(g[0] - 1.0) < 1e-15
+    assert np.all(np.diff(g) < 0) and 0 <= g[-1] < 2e-3
+    N = m + 1.0
+    k = np.arange(m + 1)
+    q = np.pi / (N + 1)
+    want = ((N - k + 1) * np.cos(q * k) + np.sin(q * k) / np.tan(q)) / (N + 1)
+    assert np.abs(g - want).max() < 1e-15
+    cf = S.indicator_coefficients(0.1, 0.3, m)
+    t = np.linspace(-1, 1, 2001)
+    plain = np.array([S.clenshaw(cf, x) for x in t])
+    damped = np.array([S.clenshaw(cf * g, x) for x in t])
+    assert plain.min() < -0.02 and plain.max() > 1.02          # Gibbs oscillations
+    assert damped.min() > -1e-12 and damped.max() < 1.0 + 1e-12
+    assert S.LanczosConfig().jackson_damping == 0
