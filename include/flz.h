@@ -56,6 +56,14 @@ int flz_ctx_create(int device, flz_ctx** out);
  * and distributed by the caller (torch.distributed / MPI / file). */
 int flz_ctx_create_dist(int device, int rank, int nranks, const void* nccl_unique_id,
                         flz_ctx** out);
+/* LOOPBACK transport — TESTS ONLY.  NCCL refuses two ranks on one device; with a hub the ranks
+ * of a "distributed" run are host threads of this process that share one GPU, and halo
+ * send/recv, all-reduce and all-gather go through device-to-device copies ordered by CUDA
+ * events (csrc/comm.cu).  Every rank calls the library from its own thread with its own
+ * context; the row-partitioned device code that runs is exactly the NCCL build's. */
+int flz_loop_hub_create(int nranks, void** hub);
+void flz_loop_hub_destroy(void* hub);
+int flz_ctx_create_loopback(int device, int rank, int nranks, void* hub, flz_ctx** out);
 int flz_nccl_unique_id(void* out128);
 void flz_ctx_destroy(flz_ctx* ctx);
 int flz_ctx_sync(flz_ctx* ctx);

@@ -5,6 +5,6 @@ the C++ host solver mirroring the reference's ``speig`` API).  This package only
 """
 from . import _lib  # noqa: F401
 from ._lib import FlzConfig, FlzError, FlzStats, build, lib  # noqa: F401
-from .device import Basis, Context, DeviceMatrix  # noqa: F401
+from .device import Basis, Context, DeviceMatrix, LoopHub  # noqa: F401
 
-__all__ = ["Basis", "Context", "DeviceMatrix", "FlzConfig", "FlzError", "FlzStats", "build", "lib"]
+__all__ = ["Basis", "Context", "DeviceMatrix", "LoopHub", "FlzConfig", "FlzError", "FlzStats", "build", "lib"]

@@ -67,6 +67,9 @@ _SIGS = {
     "flz_ctx_create": (i32, [i32, C.POINTER(vp)]),
     "flz_ctx_create_dist": (i32, [i32, i32, i32, vp, C.POINTER(vp)]),
     "flz_nccl_unique_id": (i32, [vp]),
+    "flz_loop_hub_create": (i32, [i32, C.POINTER(vp)]),
+    "flz_loop_hub_destroy": (None, [vp]),
+    "flz_ctx_create_loopback": (i32, [i32, i32, i32, vp, C.POINTER(vp)]),
     "flz_ctx_destroy": (None, [vp]),
     "flz_ctx_sync": (i32, [vp]),
     "flz_ctx_make_current": (i32, [vp]),

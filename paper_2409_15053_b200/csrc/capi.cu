@@ -83,7 +83,7 @@ struct Pinned {  // small RAII pinned host array
 
 void allreduce(flz_ctx* ctx, double* buf, size_t count) {
   if (ctx->nranks == 1 || count == 0) return;
-  FLZ_NCCL(ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, ctx->comm, ctx->stream));
+  comm_allreduce_sum(ctx, buf, count, ctx->stream);
 }
 
 // The CSR-order SELL arrays serve the exact-mode kernel only: they stay on the host until
@@ -186,28 +186,28 @@ void halo_begin(const flz_matrix* A, int R, int S, double* Y1) {
   launch_pack_rows(ctx, ctx->stream, A->n_send, R, S, ldy, A->send_rows.p, Y1, A->send_buf.p);
   FLZ_CUDA(cudaEventRecord(ctx->ev_halo_ready, ctx->stream));
   FLZ_CUDA(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_halo_ready, 0));
-  FLZ_NCCL(ncclGroupStart());
+  constexpr size_t D = sizeof(double);
+  comm_group_start(ctx);
   for (const auto& p : A->peers) {
     if (S > 0) {
       if (p.send_count)
-        FLZ_NCCL(ncclSend(A->send_buf.p + p.send_off * S, (size_t)p.send_count * S, ncclDouble,
-                          p.rank, ctx->comm, ctx->comm_stream));
+        comm_send(ctx, A->send_buf.p + p.send_off * S, (size_t)p.send_count * S * D, p.rank,
+                  ctx->comm_stream);
       if (p.recv_count)
-        FLZ_NCCL(ncclRecv(Y1 + (A->nl + p.recv_off) * S, (size_t)p.recv_count * S, ncclDouble,
-                          p.rank, ctx->comm, ctx->comm_stream));
+        comm_recv(ctx, Y1 + (A->nl + p.recv_off) * S, (size_t)p.recv_count * S * D, p.rank,
+                  ctx->comm_stream);
     } else {
       for (int k = 0; k < R; ++k) {
         if (p.send_count)
-          FLZ_NCCL(ncclSend(A->send_buf.p + (int64_t)k * A->n_send + p.send_off,
-                            (size_t)p.send_count, ncclDouble, p.rank, ctx->comm,
-                            ctx->comm_stream));
+          comm_send(ctx, A->send_buf.p + (int64_t)k * A->n_send + p.send_off,
+                    (size_t)p.send_count * D, p.rank, ctx->comm_stream);
         if (p.recv_count)
-          FLZ_NCCL(ncclRecv(Y1 + (int64_t)k * ldy + A->nl + p.recv_off, (size_t)p.recv_count,
-                            ncclDouble, p.rank, ctx->comm, ctx->comm_stream));
+          comm_recv(ctx, Y1 + (int64_t)k * ldy + A->nl + p.recv_off, (size_t)p.recv_count * D,
+                    p.rank, ctx->comm_stream);
       }
     }
   }
-  FLZ_NCCL(ncclGroupEnd());
+  comm_group_end(ctx);
   FLZ_CUDA(cudaEventRecord(ctx->ev_halo_done, ctx->comm_stream));
 }
 
@@ -423,7 +423,8 @@ const char* flz_version(void) { return "flz 0.1 (sm_100a; SELL-32-sigma Clenshaw
 
 // ---------------------------------------------------------------- context
 
-static int ctx_create_common(int device, int rank, int nranks, const void* uid, flz_ctx** out) {
+static int ctx_create_common(int device, int rank, int nranks, const void* uid, flz_ctx** out,
+                             LoopHub* hub = nullptr) {
   return guarded([&] {
     FLZ_REQUIRE(out != nullptr, FLZ_EINVAL, "ctx_create: null output");
     int count = 0;
@@ -453,7 +454,8 @@ static int ctx_create_common(int device, int rank, int nranks, const void* uid, 
       FLZ_CUDA(cudaEventCreate(&ctx->t0[i]));
       FLZ_CUDA(cudaEventCreate(&ctx->t1[i]));
     }
-    if (nranks > 1) {
+    ctx->hub = hub;
+    if (nranks > 1 && !hub) {
       FLZ_REQUIRE(uid != nullptr, FLZ_EINVAL, "ctx_create_dist: null NCCL unique id");
       ncclUniqueId id;
       static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
@@ -473,6 +475,20 @@ int flz_ctx_create_dist(int device, int rank, int nranks, const void* uid, flz_c
     return FLZ_EINVAL;
   }
   return ctx_create_common(device, rank, nranks, uid, out);
+}
+int flz_loop_hub_create(int nranks, void** out) {
+  return guarded([&] {
+    FLZ_REQUIRE(out && nranks >= 1 && nranks <= 8, FLZ_EINVAL, "loop_hub_create: 1..8 ranks");
+    *out = loop_hub_create(nranks);
+  });
+}
+void flz_loop_hub_destroy(void* hub) { loop_hub_destroy(static_cast<LoopHub*>(hub)); }
+int flz_ctx_create_loopback(int device, int rank, int nranks, void* hub, flz_ctx** out) {
+  if (!hub || nranks < 1 || rank < 0 || rank >= nranks) {
+    set_last_error("ctx_create_loopback: bad hub/rank/nranks");
+    return FLZ_EINVAL;
+  }
+  return ctx_create_common(device, rank, nranks, nullptr, out, static_cast<LoopHub*>(hub));
 }
 int flz_nccl_unique_id(void* out128) {
   return guarded([&] {
@@ -730,7 +746,7 @@ int flz_matrix_upload(flz_ctx* ctx, int64_t n_global, int64_t row_begin, int64_t
       d.reserve(2 * (size_t)P + 2);
       FLZ_CUDA(cudaMemcpyAsync(d.p + P, &row_begin, sizeof(int64_t), cudaMemcpyHostToDevice,
                                ctx->stream));
-      FLZ_NCCL(ncclAllGather(d.p + P, d.p, 1, ncclInt64, ctx->comm, ctx->stream));
+      comm_allgather_i64(ctx, d.p + P, d.p, ctx->stream);
       FLZ_CUDA(cudaMemcpyAsync(starts.data(), d.p, P * sizeof(int64_t), cudaMemcpyDeviceToHost,
                                ctx->stream));
       FLZ_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -751,13 +767,13 @@ int flz_matrix_upload(flz_ctx* ctx, int64_t n_global, int64_t row_begin, int64_t
       d_cnt.reserve(2 * (size_t)P);
       FLZ_CUDA(cudaMemcpyAsync(d_cnt.p, plan.need_cnt.data(), P * sizeof(int64_t),
                                cudaMemcpyHostToDevice, ctx->stream));
-      FLZ_NCCL(ncclGroupStart());
+      comm_group_start(ctx);
       for (int p = 0; p < P; ++p) {
         if (p == ctx->rank) continue;
-        FLZ_NCCL(ncclSend(d_cnt.p + p, 1, ncclInt64, p, ctx->comm, ctx->stream));
-        FLZ_NCCL(ncclRecv(d_cnt.p + P + p, 1, ncclInt64, p, ctx->comm, ctx->stream));
+        comm_send(ctx, d_cnt.p + p, sizeof(int64_t), p, ctx->stream);
+        comm_recv(ctx, d_cnt.p + P + p, sizeof(int64_t), p, ctx->stream);
       }
-      FLZ_NCCL(ncclGroupEnd());
+      comm_group_end(ctx);
       std::vector<int64_t> give_cnt(P, 0), give_off(P, 0);
       FLZ_CUDA(cudaMemcpyAsync(give_cnt.data(), d_cnt.p + P, P * sizeof(int64_t),
                                cudaMemcpyDeviceToHost, ctx->stream));
@@ -773,17 +789,17 @@ int flz_matrix_upload(flz_ctx* ctx, int64_t n_global, int64_t row_begin, int64_t
       if (!plan.halo.empty())
         FLZ_CUDA(cudaMemcpyAsync(d_need.p, plan.halo.data(), plan.halo.size() * sizeof(int64_t),
                                  cudaMemcpyHostToDevice, ctx->stream));
-      FLZ_NCCL(ncclGroupStart());
+      comm_group_start(ctx);
       for (int p = 0; p < P; ++p) {
         if (p == ctx->rank) continue;
         if (plan.need_cnt[p])
-          FLZ_NCCL(ncclSend(d_need.p + plan.need_off[p], (size_t)plan.need_cnt[p], ncclInt64, p,
-                            ctx->comm, ctx->stream));
+          comm_send(ctx, d_need.p + plan.need_off[p], (size_t)plan.need_cnt[p] * sizeof(int64_t), p,
+                    ctx->stream);
         if (give_cnt[p])
-          FLZ_NCCL(ncclRecv(d_give.p + give_off[p], (size_t)give_cnt[p], ncclInt64, p, ctx->comm,
-                            ctx->stream));
+          comm_recv(ctx, d_give.p + give_off[p], (size_t)give_cnt[p] * sizeof(int64_t), p,
+                    ctx->stream);
       }
-      FLZ_NCCL(ncclGroupEnd());
+      comm_group_end(ctx);
       std::vector<int64_t> give(std::max<int64_t>(give_total, 1));
       if (give_total)
         FLZ_CUDA(cudaMemcpyAsync(give.data(), d_give.p, give_total * sizeof(int64_t),

@@ -137,6 +137,18 @@ struct UgSlice {
 
 }  // namespace flz
 
+// ---------------------------------------------------------------- transport (comm.cu)
+namespace flz {
+struct LoopHub;   // loopback transport: ranks are threads of one process on one GPU (tests)
+struct CommOp {
+  bool send;
+  void* buf;
+  size_t bytes;
+  int peer;
+  cudaStream_t stream;
+};
+}  // namespace flz
+
 // ---------------------------------------------------------------- context
 struct flz_ctx {
   int device = 0;
@@ -146,6 +158,9 @@ struct flz_ctx {
   cudaEvent_t ev_halo_done = nullptr;    // halo received (comm -> compute)
   int rank = 0, nranks = 1;
   ncclComm_t comm = nullptr;
+  flz::LoopHub* hub = nullptr;            // != nullptr: loopback transport instead of NCCL
+  std::vector<flz::CommOp> comm_ops;      // loopback: operations of the open group
+  bool comm_grouped = false;
   bool exact = false;
   int sm_count = 148;
   int refs = 1;                  // owner + every matrix/basis created on the context
@@ -278,6 +293,18 @@ struct flz_basis {
 };
 
 namespace flz {
+
+// --------------------------------------------------------------- transport
+// (comm.cu) NCCL, or the loopback hub when ctx->hub is set.  Sizes in bytes; a send/recv pair
+// outside a group is a group of one.
+LoopHub* loop_hub_create(int nranks);
+void loop_hub_destroy(LoopHub* hub);
+void comm_group_start(flz_ctx* ctx);
+void comm_group_end(flz_ctx* ctx);
+void comm_send(flz_ctx* ctx, const void* buf, size_t bytes, int peer, cudaStream_t stream);
+void comm_recv(flz_ctx* ctx, void* buf, size_t bytes, int peer, cudaStream_t stream);
+void comm_allreduce_sum(flz_ctx* ctx, double* buf, size_t count, cudaStream_t stream);
+void comm_allgather_i64(flz_ctx* ctx, const int64_t* d_in, int64_t* d_out, cudaStream_t stream);
 
 // --------------------------------------------------------- kernel launchers
 // (kernels_sell.cu)

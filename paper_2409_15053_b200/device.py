@@ -31,6 +31,20 @@ def _ptr(a: np.ndarray):
     return a.ctypes.data_as(C.c_void_p)
 
 
+class LoopHub:
+    """Shared state of the loopback transport (tests only; flz_loop_hub_create)."""
+
+    def __init__(self, nranks: int):
+        h = C.c_void_p()
+        check(lib().flz_loop_hub_create(nranks, C.byref(h)))
+        self.handle, self.nranks = h, nranks
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().flz_loop_hub_destroy(self.handle)
+            self.handle = None
+
+
 class Context:
     """flz_ctx: one GPU, one stream (+ NCCL communicator when nranks > 1)."""
 
@@ -43,6 +57,16 @@ class Context:
             check(lib().flz_ctx_create(device, C.byref(h)))
         self.handle = h
         self.rank, self.nranks = rank, nranks
+
+    @classmethod
+    def loopback(cls, hub: "LoopHub", rank: int, device: int = -1) -> "Context":
+        """TESTS ONLY: rank `rank` of a row-partitioned run whose ranks are threads of this
+        process sharing one GPU (csrc/comm.cu).  Call the library from one thread per rank."""
+        h = C.c_void_p()
+        check(lib().flz_ctx_create_loopback(device, rank, hub.nranks, hub.handle, C.byref(h)))
+        self = cls.__new__(cls)
+        self.handle, self.rank, self.nranks, self._hub = h, rank, hub.nranks, hub
+        return self
 
     @classmethod
     def default(cls) -> "Context":

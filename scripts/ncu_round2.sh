@@ -5,8 +5,8 @@ set -x
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 NCU="ncu --clock-control none"
-# (1) launch list of the bench command itself (headline c3, no extra workloads)
-$NCU --metrics gpu__time_duration.sum -s 200 -c 9000 --csv --log-file gpurun_out/r02_launches_bench_c3.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline --extra '' > gpurun_out/r02_launches_bench_c3.log 2>&1
+# (1) launch list of the bench command itself (headline c3, no extra workloads); SKIP_LIST=1 skips
+[ -n "$SKIP_LIST" ] || $NCU --metrics gpu__time_duration.sum -s 200 -c 9000 --csv --log-file gpurun_out/r02_launches_bench_c3.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline --extra '' > gpurun_out/r02_launches_bench_c3.log 2>&1
 # (2) full-set captures of the K1 kernels: cold (default cache control) and warm
 for w in c3 c4; do
   $NCU --set full --import-source on -k regex:"hybrid_" -s 200 -c 4 -o gpurun_out/r02_prof_k1_$w -f python scripts/profile_target.py $w 60 > gpurun_out/r02_prof_k1_$w.log 2>&1
