@@ -1441,8 +1441,9 @@ __global__ void __launch_bounds__(kHyDenseWarps * 32)
 
 // Slices: one warp per 32 consecutive rows.  MODE 0 step (planar Y2 in place), 1 final (Out,
 // column-major ldo), 2 plain (Out = A Y1).
-template <int R, int MODE>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, FLZ_HY_SLICE_CTAS)
+// CTAS = resident CTAs per SM the register budget is cut for: 8 (64 registers) or 6 (80).
+template <int R, int MODE, int CTAS>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, CTAS)
     hybrid_slices(HyView A, double s1, double s2, double b, const double* __restrict__ Y1,
                   double* __restrict__ Y2, int64_t ldy, const double* __restrict__ X, int64_t ldx,
                   double* __restrict__ Out, int64_t ldo) {
@@ -1554,19 +1555,27 @@ void launch_hybrid_r(flz_ctx* ctx, const HyView& A, StepMode mode, double s1, do
     ctx->launches++;
   }
   const unsigned grid = (unsigned)((A.nslices + kWarpsPerBlock - 1) / kWarpsPerBlock);
+  // Registers against waves: 6 CTAs per SM (80 registers, no spills) when that needs no more
+  // waves of CTAs than 8 per SM would (measured on B200: n = 113k, one wave either way, 24.2 ->
+  // 21.4 us per step; n = 268k, 2 waves against 3, 40.2 against 42.9 us)
+  const int64_t per8 = (int64_t)ctx->sm_count * 8, per6 = (int64_t)ctx->sm_count * 6;
+  const bool roomy = FLZ_HY_SLICE_CTAS != 8 ? FLZ_HY_SLICE_CTAS == 6
+                                            : (grid + per6 - 1) / per6 <= (grid + per8 - 1) / per8;
+#define FLZ_HY_LAUNCH(MODEV)                                                                       \
+  if (roomy)                                                                                       \
+    launch_k1(ctx, hybrid_slices<R, MODEV, 6>, grid, kWarpsPerBlock * 32, A, s1, s2, b, Y1, Y2, ldy, \
+              X, ldx, Out, ldo);                                                                   \
+  else                                                                                             \
+    launch_k1(ctx, hybrid_slices<R, MODEV, 8>, grid, kWarpsPerBlock * 32, A, s1, s2, b, Y1, Y2, ldy, \
+              X, ldx, Out, ldo)
   switch (mode) {
-    case StepMode::step:
-      launch_k1(ctx, hybrid_slices<R, 0>, grid, kWarpsPerBlock * 32, A, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo);
-      break;
-    case StepMode::final:
-      launch_k1(ctx, hybrid_slices<R, 1>, grid, kWarpsPerBlock * 32, A, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo);
-      break;
-    case StepMode::plain:
-      launch_k1(ctx, hybrid_slices<R, 2>, grid, kWarpsPerBlock * 32, A, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo);
-      break;
+    case StepMode::step: FLZ_HY_LAUNCH(0); break;
+    case StepMode::final: FLZ_HY_LAUNCH(1); break;
+    case StepMode::plain: FLZ_HY_LAUNCH(2); break;
     default:
       throw ApiError(FLZ_EINVAL, "hybrid step: unsupported mode");
   }
+#undef FLZ_HY_LAUNCH
   ctx->launches++;
 }
 

@@ -12,5 +12,7 @@ ctx = Context()
 A = DeviceMatrix(ctx, n, rp, ci, va)
 cf = S.indicator_coefficients(-0.3, -0.25, m)
 X = np.random.default_rng(0).standard_normal((n, 3))
-ms, _ = A.filter_bench(cf, 1.0, 2.0, X, reps=2)
-print(name, "us/step", ms / 2 / m * 1e3)
+A.filter_bench(cf, 1.0, 2.0, X, reps=2)          # warm-up: lazy allocations, clocks
+reps = 20
+ms, _ = A.filter_bench(cf, 1.0, 2.0, X, reps=reps, flush_l2=False)
+print(name, os.environ.get("FLZ_LIB", "default"), "us/step %.2f" % (ms / reps / m * 1e3))

@@ -6,11 +6,11 @@ CODE = r'''
 import sys, json, hashlib
 sys.path.insert(0, %r)
 import numpy as np
-import bench
+from paper_2409_15053_b200.workloads import workloads
 from paper_2409_15053_b200 import solver as S
 out = {}
 for name in sys.argv[1:]:
-    wl = bench.workloads()[name]
+    wl = workloads()[name]
     n, rp, ci, va = wl["gen"]()
     H = S.SparseSymMatrix.from_csr(n, rp, ci, va, check_symmetry=False)
     cfg = S.LanczosConfig(**wl["cfg"])

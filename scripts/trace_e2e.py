@@ -2,11 +2,11 @@
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
-import bench
+from paper_2409_15053_b200.workloads import workloads
 from paper_2409_15053_b200 import solver as S, Context
 ctx = Context.default()
 name = sys.argv[1] if len(sys.argv) > 1 else "c2"
-wl = bench.workloads()[name]
+wl = workloads()[name]
 n, rp, ci, va = wl["gen"]()
 cfg = S.LanczosConfig(**wl["cfg"])
 for rep in range(3):

@@ -3,11 +3,11 @@
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
-import bench
+from paper_2409_15053_b200.workloads import workloads
 from paper_2409_15053_b200 import solver as S, Context
 ctx = Context.default()
 for name in sys.argv[1:] or ["c2", "c3", "c4"]:
-    wl = bench.workloads()[name]
+    wl = workloads()[name]
     n, rp, ci, va = wl["gen"]()
     for rep in range(2):
         t0 = time.perf_counter()
