@@ -317,28 +317,6 @@ void filter_device(const flz_matrix* A, const double* coeffs, int m, double c, d
     launch_interleave(ctx, A->nl, R, S, coeffs[m], Xc, ldx, Y1, planar_ld(A));   // :144
     FLZ_CUDA(cudaMemsetAsync(Y2, 0, (S > 0 ? (size_t)A->nl * S : (size_t)planar_ld(A) * R) *
                                             sizeof(double), ctx->stream));
-    // stencils with a tile plan, FLZ_ST_FUSED=1: all m steps in one persistent launch.  Opt-in:
-    // correct (bit-identical, tests/test_gpu_variants.py) but measured SLOWER on B200 (100^3
-    // Laplacian: 27.9-29.6 vs 16.4 us per step) — the consumers' __threadfence() before each
-    // completion flag waits for their stores to reach L2, and every producer warp polls ~80
-    // counters and fences per tile (what it needs next).
-    static const bool fused = [] {
-      const char* e = std::getenv("FLZ_ST_FUSED");
-      return e && e[0] == '1';
-    }();
-    if (fused && !ctx->exact && A->tiles.nseg > 0 && (S == 0 || (S == 1 && R == 1))) {
-      const int64_t per = A->tiles.tile_rows / kSliceRows;
-      const int64_t ntiles = (A->nslices + per - 1) / per;
-      if (A->tile_done.count < (size_t)ntiles) A->tile_done.reserve_zero((size_t)ntiles, ctx->stream);
-      A->coef.reserve((size_t)m + 1);
-      FLZ_CUDA(cudaMemcpyAsync(A->coef.p, coeffs, ((size_t)m + 1) * sizeof(double),
-                               cudaMemcpyHostToDevice, ctx->stream));
-      if (launch_stencil_filter(ctx, view_all(A), R, m, s1, s2, f1, f2, A->coef.p, Y1, Y2,
-                                planar_ld(A), Xc, ldx, Zc, ldz, A->tile_done.p, &A->tile_epoch)) {
-        g_matvecs.fetch_add((uint64_t)R * (uint64_t)m, std::memory_order_relaxed);
-        continue;
-      }
-    }
     for (int j = m - 1; j >= 1; --j) {                                          // :146-151
       sell_step(A, R, S, StepMode::step, s1, s2, coeffs[j], Y1, Y2, Xc, ldx, nullptr, 0);
       std::swap(Y1, Y2);

@@ -205,11 +205,6 @@ struct flz_matrix {
   flz::DevBuf<int32_t> ug_col, ug_uoff;
   flz::DevBuf<double> uv_pairs;     // lean matrices: 16 doubles per slice (host/plan.hpp)
   flz::StencilTiles tiles;          // nseg > 0: the TMA-staged stencil kernel applies
-  // one-launch filter application: coefficients, per-tile completion counters (never reset;
-  // tile_epoch = arrivals per tile so far)
-  mutable flz::DevBuf<double> coef;
-  mutable flz::DevBuf<unsigned long long> tile_done;
-  mutable unsigned long long tile_epoch = 0;
   // paired layout (host/plan.hpp)
   bool p2 = false;
   flz::DevBuf<flz::P2Slice> p2_desc;
@@ -380,14 +375,6 @@ void launch_clenshaw_step(flz_ctx* ctx, const SellView& A, int R, int S, StepMod
 void launch_hybrid_step(flz_ctx* ctx, const HyView& A, int R, StepMode mode, double s1, double s2,
                         double b, const double* Y1, double* Y2, int64_t ldy, const double* X,
                         int64_t ldx, double* Out, int64_t ldo);
-// All nsteps Clenshaw steps of one filter application (planar blocks B0 = Y1, B1 = Y2; the last
-// step applies (f1, f2) and writes Out) in ONE persistent launch of the TMA-staged stencil
-// kernel; coef[i] (device) is the reference's coefficient array (step i uses coef[nsteps-1-i]).
-// false: not applicable (no tile plan, misaligned operands, distributed) — launch step by step.
-bool launch_stencil_filter(flz_ctx* ctx, const SellView& A, int R, int nsteps, double s1, double s2,
-                           double f1, double f2, const double* coef, double* B0, double* B1,
-                           int64_t ldy, const double* X, int64_t ldx, double* Out, int64_t ldo,
-                           unsigned long long* done, unsigned long long* epoch);
 // Y1 = scale * X  (column-major -> interleaved with row stride S >= R, or planar for S == 0)
 void launch_interleave(flz_ctx* ctx, int64_t nl, int R, int S, double scale, const double* X,
                        int64_t ldx, double* Y1, int64_t ldy);

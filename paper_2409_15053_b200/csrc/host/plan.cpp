@@ -1328,10 +1328,18 @@ HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<in
     const char* e = std::getenv("FLZ_P2");
     return !(e && e[0] == '0');
   }();
-  static const bool want_dense = [] {   // FLZ_P2_DENSE=0: no dense sections (experiments)
+  // Dense blocks are searched for when the hybrid layout can use them (one rank), or when the
+  // paired layout is asked to keep dense sections (FLZ_P2_DENSE=1, experiments: measured slower
+  // than the plain paired layout on the PARSEC shapes, 36.3 vs 30.0 us per step at n = 113k)
+  const bool p2_dense = [] {
     const char* e = std::getenv("FLZ_P2_DENSE");
+    return e && e[0] == '1';
+  }();
+  const bool hy_wanted = [] {
+    const char* e = std::getenv("FLZ_HY");
     return !(e && e[0] == '0');
   }();
+  const bool want_dense = p2_dense || (hy_wanted && nranks == 1);
   int32_t longest = 0;
   for (int64_t i = 0; i < nl; ++i) longest = std::max(longest, len[i]);
   const bool p2_candidate = want_p2_sort && !P.split && longest > 24 && nl > 0;
@@ -1359,11 +1367,7 @@ HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<in
   timer.lap("dense blocks");
   // HYBRID layout (plan.hpp): natural row order, dense tasks + value-grouped slices.  One rank
   // only (the slices gather local rows); FLZ_HY=0 keeps the paired layout (experiments).
-  const bool want_hy = [] {   // read per plan, so that tests can switch it
-    const char* e = std::getenv("FLZ_HY");
-    return !(e && e[0] == '0');
-  }();
-  bool hybrid = want_hy && blocks.any() && nranks == 1;
+  bool hybrid = hy_wanted && blocks.any() && nranks == 1;
   if (hybrid) {
     size_t widest = 0;
     for (const auto& K : blocks.members) widest = std::max(widest, K.size());
@@ -1385,6 +1389,7 @@ HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<in
     }
     hybrid = 20 * excess <= P.nnz;
   }
+  if (blocks.any() && !hybrid && !p2_dense) blocks = DenseBlocks{};   // plain paired layout
   if (blocks.any() && !hybrid) {
     // row order: rows in several blocks (all entries general, longest first), then block by
     // block the rows that belong to that block only, then the rows outside every block in

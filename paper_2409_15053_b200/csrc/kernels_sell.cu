@@ -876,8 +876,7 @@ template <int R>
 struct SliceAcc {
   double v[R];
 };
-// COHERENT: Y1 was written by other SMs during this launch (one-launch filter): L2 loads.
-template <int R, bool COHERENT = false>
+template <int R>
 __device__ __noinline__ SliceAcc<R> stencil_slice_rest(const SellView& A, int64_t slice, int lane,
                                                        int64_t row, const double* __restrict__ Y1,
                                                        int64_t ldy, SliceAcc<R> acc) {
@@ -891,14 +890,14 @@ __device__ __noinline__ SliceAcc<R> stencil_slice_rest(const SellView& A, int64_
     const double v = ld_stream_f64(val + (int64_t)(p - nuv) * kSliceRows);
     const int c = min(max((int)row + __ldg(desc + 8 + p), 0), cmax);
 #pragma unroll
-    for (int k = 0; k < R; ++k) acc.v[k] = fma(v, (COHERENT ? __ldcg(Y1 + (int64_t)k * ldy + c) : __ldg(Y1 + (int64_t)k * ldy + c)), acc.v[k]);
+    for (int k = 0; k < R; ++k) acc.v[k] = fma(v, __ldg(Y1 + (int64_t)k * ldy + c), acc.v[k]);
   }
   const int32_t* __restrict__ col = A.ug_col + H.col_ptr + lane;
   for (int q = 0; q < H.ng; ++q) {
     const double v = ld_stream_f64(val + (int64_t)(H.nu - nuv + q) * kSliceRows);
     const int c = ld_stream_s32(col + (int64_t)q * kSliceRows);
 #pragma unroll
-    for (int k = 0; k < R; ++k) acc.v[k] = fma(v, (COHERENT ? __ldcg(Y1 + (int64_t)k * ldy + c) : __ldg(Y1 + (int64_t)k * ldy + c)), acc.v[k]);
+    for (int k = 0; k < R; ++k) acc.v[k] = fma(v, __ldg(Y1 + (int64_t)k * ldy + c), acc.v[k]);
   }
   return acc;
 }
@@ -1084,221 +1083,6 @@ __global__ void __launch_bounds__(768)
 }
 
 
-// ------------------------------------------------ whole filter application in ONE launch
-// All Clenshaw steps of p(A) X in one persistent launch of the tile kernel above (same ring,
-// same arithmetic, bit-identical results).  A launch per step pays a ramp (no CTA can request
-// its first tile before the previous step has completed) and a tail (3 907 tiles over 296 CTAs)
-// — ~2-3 of 16.4 us on the 100^3 Laplacian.  Here the ring simply runs on into the next step:
-// tile t of step i+1 reads rows of the block step i wrote only inside its segments, i.e. from
-// tiles [t - h, t + h] (h = 40 for the 100^3 Laplacian), and overwrites rows those same tiles
-// read during step i, so ONE condition orders both: every tile in [t - h, t + h] has finished
-// step i.  done[t] counts the consumer warps that have stored (and fenced) their rows of tile
-// t, over all steps and launches (epoch0 = count before this launch); a producer warp polls
-// the range (relaxed loads, then one acquire fence) before it requests the tile.  CTAs walk (step, tile) in
-// lexicographic order and all CTAs are resident (the launcher sizes the grid by the occupancy
-// API and the launch is not a dependent launch), so the smallest unfinished (step, tile) can
-// always proceed: no deadlock.  Step i reads Y1 = B[i & 1], owns/writes B[(i + 1) & 1]; the
-// last step applies (f1, f2) and writes Out.  b of step i is coef[nsteps - 1 - i].
-__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-
-template <int R>
-__global__ void __launch_bounds__(768)
-    clenshaw_filter_stencil_tma(const __grid_constant__ SellView A,
-                                const __grid_constant__ StencilTiles G,
-                                const double* __restrict__ pairs, int64_t nl, int64_t ntiles,
-                                int nstages, int nprod, int64_t y_rows, int64_t x_rows, int nsteps,
-                                double s1, double s2, double f1, double f2,
-                                const double* __restrict__ coef, double* B0, double* B1,
-                                int64_t ldy, const double* __restrict__ X, int64_t ldx,
-                                double* __restrict__ Out, int64_t ldo, unsigned long long* done,
-                                unsigned long long epoch0) {
-  extern __shared__ __align__(128) unsigned char st_smem[];
-  const int T = (int)blockDim.x - 32 * nprod;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int spt = T >> 5;
-  const int pair_d = spt * 16;
-  const int y1e = G.y1_elems;
-  const int y1_d = R * y1e;
-  const int stage_d = pair_d + y1_d + 2 * R * T;
-  double* const ring = reinterpret_cast<double*>(st_smem);
-  const uint32_t ring_s = smem_addr(ring);
-  const uint32_t full_bars = ring_s + (uint32_t)nstages * stage_d * 8;
-  const uint32_t empty_bars = full_bars + (uint32_t)nstages * 8;
-  if (threadIdx.x == 0) {
-    for (int st = 0; st < nstages; ++st) {
-      mbar_init(full_bars + st * 8, nprod);
-      mbar_init(empty_bars + st * 8, spt);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  }
-  __syncthreads();
-
-  if (warp >= spt) {
-    // ---------------------------------------------------------------- producer warps
-    const int pw = warp - spt;
-    const int c = lane * nprod + pw;
-    const int ncopy = 1 + G.nseg * R + 2 * R;
-    int dst = 0, full = 0, off = 0, kind = 0, col = 0;  // kind: 0 pairs/none, 1 Y1 run, 2 own Y2, 3 own X
-    if (c == 0) {
-      full = pair_d;
-    } else if (c < 1 + G.nseg * R) {
-      const int q = c - 1, j = q / R;
-      col = q - j * R;
-      dst = pair_d + col * y1e + G.seg_start[j];
-      full = G.seg_len[j];
-      off = G.seg_base[j];
-      kind = 1;
-    } else if (c < ncopy) {
-      const int q = c - 1 - G.nseg * R, which = q / R;
-      col = q - which * R;
-      dst = pair_d + y1_d + q * T;
-      full = T;
-      kind = 2 + which;
-    }
-    // tiles whose rows the runs of tile t intersect: [t + dlo, t + dhi] (floor divisions)
-    const int lo_rows = G.seg_base[0];
-    const int hi_rows = G.seg_base[G.nseg - 1] + G.seg_len[G.nseg - 1] - 1;
-    const int dlo = lo_rows >= 0 ? lo_rows / T : -((-lo_rows + T - 1) / T);
-    const int dhi = hi_rows / T;
-    int st = 0;
-    uint32_t parity = 1;
-    for (int i = 0; i < nsteps; ++i) {
-      const double* y1 = (i & 1) ? B1 : B0;
-      const double* y2 = (i & 1) ? B0 : B1;
-      const double* base = kind == 1 ? y1 + (int64_t)col * ldy
-                                     : (kind == 2 ? y2 + (int64_t)col * ldy
-                                                  : (kind == 3 ? X + (int64_t)col * ldx : nullptr));
-      const int64_t lim = kind == 3 ? x_rows : y_rows;
-      const unsigned long long need = epoch0 + (unsigned long long)i * spt;
-      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        if (i > 0) {  // every tile this one reads from / writes under has finished step i-1
-          const int64_t t0 = max(t + dlo, (int64_t)0), t1 = min(t + dhi, ntiles - 1);
-          // all counters of the range are requested together (one L2 round trip when the
-          // range is done, which is the normal case: the polls must not throttle the producer)
-          for (;;) {
-            unsigned long long least = ~0ull;
-            for (int64_t u = t0 + lane; u <= t1; u += 32) least = min(least, ld_relaxed_u64(done + u));
-            if (__all_sync(0xffffffffu, least >= need)) break;
-            __nanosleep(64);
-          }
-          asm volatile("fence.acq_rel.gpu;" ::: "memory");
-          asm volatile("fence.proxy.async;" ::: "memory");  // acquired data -> visible to the TMA reads
-        }
-        mbar_wait(empty_bars + st * 8, parity);
-        double* sb = ring + (int64_t)st * stage_d;
-        const uint32_t bar = full_bars + st * 8;
-        int lead = 0, count = full;
-        const double* src = pairs + t * pair_d;
-        if (base) {
-          const int64_t g0 = t * T + off;
-          const int64_t a0 = max(g0, (int64_t)0), a1 = min(g0 + full, lim);
-          lead = (int)min(a0 - g0, (int64_t)full);
-          count = (int)max(a1 - a0, (int64_t)0);
-          src = base + a0;
-        }
-        unsigned clipped = __ballot_sync(0xffffffffu, count < full);
-        while (clipped) {
-          const int l = __ffs(clipped) - 1;
-          clipped &= clipped - 1;
-          const int zd = __shfl_sync(0xffffffffu, dst, l), zf = __shfl_sync(0xffffffffu, full, l);
-          const int zl = __shfl_sync(0xffffffffu, lead, l), zc = __shfl_sync(0xffffffffu, count, l);
-          for (int k = lane; k < zl; k += 32) sb[zd + k] = 0.0;
-          for (int k = zl + zc + lane; k < zf; k += 32) sb[zd + k] = 0.0;
-        }
-        const uint32_t bytes = (uint32_t)count * 8u;
-        const uint32_t total = __reduce_add_sync(0xffffffffu, bytes);
-        __syncwarp();
-        if (lane == 0)
-          asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
-                       "r"(total) : "memory");
-        __syncwarp();
-        if (count > 0)
-          bulk_g2s(ring_s + (uint32_t)(st * stage_d + dst + lead) * 8u, src, bytes, bar);
-        if (++st == nstages) { st = 0; parity ^= 1u; }
-      }
-    }
-    return;
-  }
-
-  // ------------------------------------------------------------------ consumer warps
-  int st = 0;
-  uint32_t parity = 0;
-  const uint32_t y1e8 = (uint32_t)y1e * 8u;
-  const uint32_t lanebit = 1u << lane;
-  const uint32_t own8 = (uint32_t)G.own_e * 8u;
-  const int64_t row0 = ((int64_t)blockIdx.x * spt + warp) * 32 + lane;
-  const int64_t row_step = (int64_t)gridDim.x * T;
-  for (int i = 0; i < nsteps; ++i) {
-    const bool last = i == nsteps - 1;
-    const double* y1g = (i & 1) ? B1 : B0;  // flagged slices gather from it
-    double* dst = (last ? Out : ((i & 1) ? B0 : B1)) + row0;
-    const int64_t ldd = last ? ldo : ldy;
-    const double c1 = last ? f1 : s1, c2 = last ? f2 : s2;
-    const double b = __ldg(coef + (nsteps - 1 - i));
-    int64_t row = row0;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, row += row_step, dst += row_step) {
-      mbar_wait(full_bars + st * 8, parity);
-      const double* sb = ring + (int64_t)st * stage_d;
-      const double2* sP = reinterpret_cast<const double2*>(sb + warp * 16);
-      const unsigned char* sY1 = reinterpret_cast<const unsigned char*>(sb + pair_d + threadIdx.x);
-      double acc[R];
-#pragma unroll
-      for (int k = 0; k < R; ++k) acc[k] = 0.0;
-      double2 pr[8];
-#pragma unroll
-      for (int p = 0; p < 8; ++p) pr[p] = sP[p];
-      const uint32_t word0 = (uint32_t)__double2hiint(pr[0].y);
-      const int nuv = (word0 >> 20) & 0xf;
-      auto position = [&](int p) {
-        const uint32_t e8 = (uint32_t)__double2hiint(pr[p].y) & 0xfffffu;
-        const double v = ((uint32_t)__double2loint(pr[p].y) & lanebit) ? pr[p].x : 0.0;
-#pragma unroll
-        for (int k = 0; k < R; ++k)
-          acc[k] = fma(v, *reinterpret_cast<const double*>(sY1 + k * y1e8 + e8), acc[k]);
-      };
-      position(0); position(1); position(2); position(3);
-      if (nuv > 4) { position(4); position(5); }
-      if (nuv > 6) { position(6); position(7); }
-      if ((word0 >> 24) & 1) {
-        SliceAcc<R> tmp;
-#pragma unroll
-        for (int k = 0; k < R; ++k) tmp.v[k] = acc[k];
-        tmp = stencil_slice_rest<R, true>(A, t * spt + warp, lane, row, y1g, ldy, tmp);
-#pragma unroll
-        for (int k = 0; k < R; ++k) acc[k] = tmp.v[k];
-      }
-      double o[R];
-      const double* sY2 = sb + pair_d + y1_d + threadIdx.x;
-      const double* sX = sY2 + R * T;
-#pragma unroll
-      for (int k = 0; k < R; ++k)
-        o[k] = combine<false>(c1, acc[k], c2,
-                              *reinterpret_cast<const double*>(sY1 + k * y1e8 + own8), sY2[k * T],
-                              b, sX[k * T]);
-      __syncwarp();
-      if (lane == 0)
-        asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(empty_bars + st * 8)
-                     : "memory");
-      if (row < nl) {
-#pragma unroll
-        for (int k = 0; k < R; ++k) dst[(int64_t)k * ldd] = o[k];
-      }
-      if (!last) {  // publish: this warp's rows of tile t, step i, are in global memory
-        __threadfence();
-        __syncwarp();
-        if (lane == 0) atomicAdd(done + t, 1ull);
-      }
-      if (++st == nstages) { st = 0; parity ^= 1u; }
-    }
-  }
-}
-
-// Y1[i*S+k] = scale * X[k*ldx+i], k < R; pad entries (R <= k < S) are zeroed
 template <int R, int S>
 __global__ void interleave_kernel(int64_t nl, double scale, const double* __restrict__ X,
                                   int64_t ldx, double* __restrict__ Y1, int64_t ldy) {
@@ -1654,63 +1438,6 @@ bool launch_stencil_tma(flz_ctx* ctx, const SellView& A, double s1, double s2, d
 }
 
 
-// The whole filter application (nsteps Clenshaw steps incl. the final one) in one launch of
-// clenshaw_filter_stencil_tma; false: not applicable, the caller launches step by step.
-// `coef` (device, nsteps + 1 doubles), `done` (device, one counter per tile, never reset) and
-// *epoch (arrivals per tile so far) belong to the matrix.
-template <int R>
-bool launch_stencil_filter_r(flz_ctx* ctx, const SellView& A, int nsteps, double s1, double s2,
-                             double f1, double f2, const double* coef, double* B0, double* B1,
-                             int64_t ldy, const double* X, int64_t ldx, double* Out, int64_t ldo,
-                             unsigned long long* done, unsigned long long* epoch) {
-  const StencilTiles& G = A.tiles;
-  if (G.nseg == 0 || A.nslices == 0 || nsteps < 1 || ctx->nranks != 1) return false;
-  auto aligned = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-  if (!aligned(B0) || !aligned(B1) || !aligned(X) || (ldy & 1) || (ldx & 1) || ldy < A.nl ||
-      ldx < A.nl)
-    return false;
-  const int T = G.tile_rows;
-  const size_t stage_bytes = 8 * ((size_t)(T / 32) * 16 + (size_t)R * G.y1_elems + 2 * (size_t)R * T);
-  static const int want_stages = std::clamp(env_int("FLZ_ST_STAGES", 3), 1, 8);
-  static const int want_ctas = std::clamp(env_int("FLZ_ST_CTAS", 2), 1, 8);
-  static const int want_prod = std::clamp(env_int("FLZ_ST_PRODUCERS", 4), 1, 8);
-  static const int sms = [] {
-    int dev = 0, n = 0;
-    FLZ_CUDA(cudaGetDevice(&dev));
-    FLZ_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
-    return n;
-  }();
-  const int ncopy = 1 + G.nseg * R + 2 * R;
-  const int nprod = std::max(want_prod, (ncopy + 31) / 32);
-  constexpr size_t kSmemPerSm = 227 * 1024, kMaxCta = 227 * 1024;
-  int ctas = want_ctas, stages = want_stages;
-  while (stages > 2 && (stages * (stage_bytes + 16) + 1024) * ctas > kSmemPerSm) --stages;
-  while (ctas > 1 && (stages * (stage_bytes + 16) + 1024) * ctas > kSmemPerSm) --ctas;
-  const size_t smem = stages * (stage_bytes + 16);
-  if (smem > kMaxCta) return false;
-  static const bool configured = [] {
-    FLZ_CUDA(cudaFuncSetAttribute(clenshaw_filter_stencil_tma<R>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxCta));
-    return true;
-  }();
-  (void)configured;
-  // every CTA must be resident (tiles wait for tiles of other CTAs)
-  int resident = 0;
-  FLZ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, clenshaw_filter_stencil_tma<R>,
-                                                         T + 32 * nprod, smem));
-  if (resident < 1) return false;
-  ctas = std::min(ctas, resident);
-  const int64_t ntiles = (A.nslices + T / 32 - 1) / (T / 32);
-  const unsigned grid = (unsigned)std::min<int64_t>(ntiles, (int64_t)sms * ctas);
-  clenshaw_filter_stencil_tma<R><<<grid, T + 32 * nprod, smem, ctx->stream>>>(
-      A, G, A.uv_pairs, A.nl, ntiles, stages, nprod, ldy, ldx, nsteps, s1, s2, f1, f2, coef, B0, B1,
-      ldy, X, ldx, Out, ldo, done, *epoch);
-  FLZ_CUDA(cudaGetLastError());
-  *epoch += (unsigned long long)(nsteps - 1) * (unsigned long long)(T / 32);
-  ctx->launches++;
-  return true;
-}
-
 template <int R, int S, int MODE>
 void launch_ug(flz_ctx* ctx, const SellView& A, double s1, double s2, double b, const double* Y1,
                double* Y2, int64_t ldy, const double* X, int64_t ldx, double* Out, int64_t ldo) {
@@ -1823,19 +1550,6 @@ void launch_hybrid_step(flz_ctx* ctx, const HyView& A, int R, StepMode mode, dou
     default: throw ApiError(FLZ_EINVAL, "hybrid step: unsupported column count");
   }
   FLZ_CUDA(cudaGetLastError());
-}
-
-bool launch_stencil_filter(flz_ctx* ctx, const SellView& A, int R, int nsteps, double s1, double s2,
-                           double f1, double f2, const double* coef, double* B0, double* B1,
-                           int64_t ldy, const double* X, int64_t ldx, double* Out, int64_t ldo,
-                           unsigned long long* done, unsigned long long* epoch) {
-  switch (R) {
-    case 1: return launch_stencil_filter_r<1>(ctx, A, nsteps, s1, s2, f1, f2, coef, B0, B1, ldy, X, ldx, Out, ldo, done, epoch);
-    case 2: return launch_stencil_filter_r<2>(ctx, A, nsteps, s1, s2, f1, f2, coef, B0, B1, ldy, X, ldx, Out, ldo, done, epoch);
-    case 3: return launch_stencil_filter_r<3>(ctx, A, nsteps, s1, s2, f1, f2, coef, B0, B1, ldy, X, ldx, Out, ldo, done, epoch);
-    case 4: return launch_stencil_filter_r<4>(ctx, A, nsteps, s1, s2, f1, f2, coef, B0, B1, ldy, X, ldx, Out, ldo, done, epoch);
-    default: return false;
-  }
 }
 
 void launch_interleave(flz_ctx* ctx, int64_t nl, int R, int S, double scale, const double* X,

@@ -17,7 +17,7 @@ def run(code, env_extra, args=()):
     env = dict(os.environ)
     for k in ("FLZ_SPLIT", "FLZ_K1_LAYOUT", "FLZ_SYNC_CHECK", "FLZ_K1_TMA", "FLZ_K1_PDL",
               "FLZ_P2_CLUSTER", "FLZ_ST_TILE", "FLZ_ST_STAGES", "FLZ_ST_CTAS",
-              "FLZ_ST_FUSED", "FLZ_ST_PRODUCERS"):
+              "FLZ_ST_PRODUCERS", "FLZ_HY"):
         env.pop(k, None)
     env.update(env_extra)
     p = subprocess.run([sys.executable, "-c", code, *args], env=env, capture_output=True,
@@ -122,8 +122,7 @@ def test_tile_kernel_bit_identical_to_warp_kernel():
     tile size / ring depth (boundary tiles: clipped runs, slices with per-lane positions)."""
     warp = run(TILE_CODE, {"FLZ_ST_TILE": "0", "FLZ_K1_LAYOUT": "planar"})
     for env in ({"FLZ_K1_LAYOUT": "planar"},                       # one launch per Clenshaw step
-                {"FLZ_K1_LAYOUT": "planar", "FLZ_ST_FUSED": "1"},  # one launch per filter application
-                {"FLZ_ST_TILE": "64", "FLZ_ST_PRODUCERS": "2", "FLZ_ST_FUSED": "1", "FLZ_K1_LAYOUT": "planar"},
+                {"FLZ_ST_TILE": "64", "FLZ_ST_PRODUCERS": "2", "FLZ_K1_LAYOUT": "planar"},
                 {"FLZ_ST_TILE": "32", "FLZ_ST_STAGES": "2", "FLZ_K1_LAYOUT": "planar"},
                 {"FLZ_ST_TILE": "256", "FLZ_ST_STAGES": "5", "FLZ_ST_CTAS": "1", "FLZ_K1_LAYOUT": "planar"}):
         assert run(TILE_CODE, env) == warp, env

@@ -138,6 +138,7 @@ def _check_p2_slices(p2, n):
 @pytest.mark.parametrize("dense", ["1", "0"])
 def test_paired_layout_reproduces_product(gen, dense, monkeypatch):
     monkeypatch.setenv("FLZ_HY", "0")     # the paired layout (multi-rank / no-blocks fallback)
+    monkeypatch.setenv("FLZ_P2_DENSE", "1")   # with its optional dense sections (experiments)
     """Long ragged rows: slices of up to 64 rows, two adjacent rows per lane, one column and
     two values per general position, one shared column per dense position (host/plan.hpp).
     The emulation walks it as clenshaw_step_p2_tasks does.  FLZ_P2_DENSE is read once per
@@ -186,6 +187,7 @@ def test_paired_layout_reproduces_product(gen, dense, monkeypatch):
 
 def test_dense_blocks_of_a_parsec_shaped_matrix_are_found(monkeypatch):
     monkeypatch.setenv("FLZ_HY", "0")
+    monkeypatch.setenv("FLZ_P2_DENSE", "1")
     """The non-local projector balls of a PARSEC-shaped Hamiltonian become dense sections: one
     block per atom, most of the nonzeros leave the general positions, a dense section is shared
     by rows of ONE block (its columns are exactly that block's members), and what is left per
@@ -338,6 +340,7 @@ def test_paired_layout_odd_row_count_lone_row_longest():
 
 def test_paired_layout_saves_gathers_on_dense_blocks(monkeypatch):
     monkeypatch.setenv("FLZ_HY", "0")
+    monkeypatch.setenv("FLZ_P2_DENSE", "1")
     csr = M.parsec_like(radius=14.0, n_atoms=20, ball_radius=3.25)
     n, rp, ci, va = csr
     p2 = HaloPlan(n, 0, 1, [0, n], rp, ci, va).p2_arrays()
