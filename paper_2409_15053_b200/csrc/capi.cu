@@ -159,9 +159,10 @@ int64_t planar_ld(const flz_matrix* A) {
 
 HyView hybrid_view(const flz_matrix* A) {
   if (A->hy_p.count == 0) A->hy_p.reserve_zero((size_t)A->hy_ldp * kMaxFuse + 8, A->ctx->stream);
+  if (A->hy_w.count == 0) A->hy_w.reserve_zero((size_t)planar_ld(A) * kMaxFuse + 8, A->ctx->stream);
   return HyView{A->nl,         A->nslices,    (int)A->hy_ndtasks, A->hy_maxcols, A->hy_slice.p,
                 A->hy_cols.p,  A->hy_uvval.p, A->hy_gval.p,       A->hy_diag.p,  A->hy_dtasks.p,
-                A->hy_dcols.p, A->hy_dval.p,  A->hy_p.p,          A->hy_ldp};
+                A->hy_dcols.p, A->hy_dval.p,  A->hy_p.p,          A->hy_ldp,     A->hy_w.p};
 }
 
 void ensure_workspaces(const flz_matrix* A) {
@@ -1024,9 +1025,12 @@ int flz_matrix_k1_info(const flz_matrix* A, int r, int64_t* info, char* kernel, 
     name = "clenshaw_step_sell<EXACT>";
     matrix_bytes = A->stored * 12;
   } else if (A->hy) {
-    name = "hybrid_dense_tasks + hybrid_slices (dense blocks + value-grouped slices)";
-    // dense partials: written once and read once per row and block
-    matrix_bytes = A->hy_bytes + 16 * A->hy_ndtasks * 32 * r;
+    const bool overlap = hybrid_overlaps(A->ctx, A->nslices, A->hy_ndtasks);
+    name = overlap ? "hybrid_gather + hybrid_finish (dense tasks and slices overlapped)"
+                   : "hybrid_dense_tasks + hybrid_slices (dense blocks + value-grouped slices)";
+    // dense partials: written once and read once per row and block; the overlapped variant
+    // also writes and reads the slices' sums once
+    matrix_bytes = A->hy_bytes + 16 * A->hy_ndtasks * 32 * r + (overlap ? 16 * A->nl * r : 0);
   } else if (A->p2) {
     name = A->p2_blocks > 0 ? "clenshaw_step_p2_tasks (paired + dense sections)"
                             : "clenshaw_step_p2_tasks (paired)";

@@ -218,6 +218,7 @@ struct flz_matrix {
   flz::DevBuf<int32_t> hy_cols, hy_dcols;
   flz::DevBuf<double> hy_uvval, hy_gval, hy_diag, hy_dval;
   mutable flz::DevBuf<double> hy_p;      // partial sums of the dense tasks, planar [k][hy_ldp]
+  mutable flz::DevBuf<double> hy_w;      // overlapped variant: slice sums, planar like y1
   int64_t hy_ndtasks = 0, hy_ldp = 0, hy_blocks = 0, hy_dense_entries = 0, hy_uv_entries = 0;
   int hy_maxcols = 0;
   int64_t hy_bytes = 0;
@@ -356,6 +357,7 @@ struct HyView {
   const double* dval;
   double* P;                 // partial slots, planar [k][ldp]
   int64_t ldp;
+  double* W;                 // overlapped variant: the slices' sums before the finish launch
 };
 
 enum class StepMode { step, final, plain, rest };
@@ -372,6 +374,9 @@ void launch_clenshaw_step(flz_ctx* ctx, const SellView& A, int R, int S, StepMod
                           int64_t ldy, const double* X, int64_t ldx, double* Out, int64_t ldo);
 // The same step on a matrix with the hybrid layout: PLANAR blocks (column k of Y1/Y2 at
 // k * ldy, row nl of Y1 must be zero), two launches (dense tasks, then the slices).
+// true: the overlapped variant runs (hybrid_gather + hybrid_finish), else hybrid_dense_tasks +
+// hybrid_slices
+bool hybrid_overlaps(const flz_ctx* ctx, int64_t nslices, int64_t ndtasks);
 void launch_hybrid_step(flz_ctx* ctx, const HyView& A, int R, StepMode mode, double s1, double s2,
                         double b, const double* Y1, double* Y2, int64_t ldy, const double* X,
                         int64_t ldx, double* Out, int64_t ldo);

@@ -52,6 +52,12 @@ __device__ __forceinline__ void pdl_launch_dependents() {
 }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+// integer environment switch (experiments: FLZ_ST_STAGES, FLZ_ST_CTAS, FLZ_HY_OVERLAP, ...)
+inline int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e && *e ? std::atoi(e) : dflt;
+}
+
 // FLZ_K1_PDL=0 restores plain stream-ordered launches (experiments)
 inline bool pdl_enabled() {
   static const bool on = [] {
@@ -1145,6 +1151,9 @@ constexpr int kHyDenseWarps = 4;
 #ifndef FLZ_HY_SLICE_CTAS
 #define FLZ_HY_SLICE_CTAS 8
 #endif
+#ifndef FLZ_HY_OVERLAP_DEFAULT
+#define FLZ_HY_OVERLAP_DEFAULT -1
+#endif
 
 // Dense task: 4 warps share the columns of the block; the block rows of ALL its columns are
 // staged in shared memory once (ys[ncols][4]), a lane owns one row of the task and streams its
@@ -1328,17 +1337,247 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, CTAS)
   }
 }
 
+// ---- overlapped variant: ONE launch holds the dense tasks and the slices' gather work, CTA
+// roles interleaved by blockIdx (Bresenham: of every nd + ns consecutive CTAs, nd are dense
+// tasks), so that every SM runs DRAM-bound dense CTAs next to LSU-bound slice CTAs.  No CTA
+// waits for another: the slices leave their sums in W, and a second, small launch adds the
+// partial sums of the dense tasks and applies the Clenshaw combine (same order of additions as
+// hybrid_slices: bit-identical results).
+template <int R, int CTAS>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, CTAS)
+    hybrid_gather(HyView A, const double* __restrict__ Y1, int64_t ldy) {
+  extern __shared__ __align__(16) double hy_smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t total = gridDim.x, nd = A.ndtasks, bid = blockIdx.x;
+  const int64_t d0 = bid * nd / total, d1 = (bid + 1) * nd / total;
+  pdl_launch_dependents();
+  if (d1 > d0) {   // ---- dense task d0 (as hybrid_dense_tasks)
+    double (*ys)[4] = reinterpret_cast<double (*)[4]>(hy_smem);
+    double (*part)[R][32] = reinterpret_cast<double (*)[R][32]>(hy_smem + 4 * A.maxcols);
+    const int4* tp = reinterpret_cast<const int4*>(A.dtasks + d0);
+    const int4 t0 = __ldg(tp), t1 = __ldg(tp + 1);
+    const int64_t val_off = ((int64_t)(uint32_t)t0.y << 32) | (uint32_t)t0.x;
+    const int col_off = t0.z, ncols = t0.w, slot_base = t1.x;
+    const int chunk = (ncols + kHyDenseWarps - 1) / kHyDenseWarps;
+    const int j0 = min(ncols, warp * chunk), j1 = min(ncols, j0 + chunk);
+    const double* __restrict__ v = A.dval + val_off * 32 + lane;
+    constexpr int U = FLZ_HY_DU;
+    double a[U], nx[U];
+    auto fetch = [&](double (&dst)[U], int j) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) dst[u] = j + u < j1 ? ld_stream_f64(v + (int64_t)(j + u) * 32) : 0.0;
+    };
+    fetch(a, j0);
+    fetch(nx, j0 + U);
+    {
+      const char* base = reinterpret_cast<const char*>(v - lane + (int64_t)(j0 + 2 * U) * 32);
+      const int lines = max(0, j1 - j0 - 2 * U) * 2;
+      for (int l = lane; l < lines; l += 32) prefetch_l2(base + (size_t)l * 128);
+    }
+    pdl_wait();
+    for (int j = threadIdx.x; j < ncols; j += kHyDenseWarps * 32) {
+      const int c = __ldg(A.dcols + col_off + j);
+#pragma unroll
+      for (int k = 0; k < R; ++k) ys[j][k] = __ldg(Y1 + (int64_t)k * ldy + c);
+    }
+    __syncthreads();
+    double acc[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) acc[k] = 0.0;
+    for (int j = j0; j < j1; j += U) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int jj = min(j + u, ncols - 1);
+        if constexpr (R >= 2) {
+          const double2 y01 = *reinterpret_cast<const double2*>(&ys[jj][0]);
+          acc[0] = fma(a[u], y01.x, acc[0]);
+          acc[1] = fma(a[u], y01.y, acc[1]);
+          if constexpr (R >= 3) {
+            const double2 y23 = *reinterpret_cast<const double2*>(&ys[jj][2]);
+            acc[2] = fma(a[u], y23.x, acc[2]);
+            if constexpr (R == 4) acc[3] = fma(a[u], y23.y, acc[3]);
+          }
+        } else {
+          acc[0] = fma(a[u], ys[jj][0], acc[0]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) a[u] = nx[u];
+      fetch(nx, j + 2 * U);
+    }
+    if (warp > 0) {
+#pragma unroll
+      for (int k = 0; k < R; ++k) part[warp - 1][k][lane] = acc[k];
+    }
+    __syncthreads();
+    if (warp == 0) {
+      for (int q = 0; q < kHyDenseWarps - 1; ++q)
+#pragma unroll
+        for (int k = 0; k < R; ++k) acc[k] += part[q][k][lane];
+#pragma unroll
+      for (int k = 0; k < R; ++k) A.P[(int64_t)k * A.ldp + slot_base + lane] = acc[k];
+    }
+    return;
+  }
+  // ---- slice CTA (bid - d0): uniform-value and general positions into W
+  const int64_t slice = (bid - d0) * kWarpsPerBlock + warp;
+  if (slice >= A.nslices) {
+    pdl_wait();
+    return;
+  }
+  const int4* hp = reinterpret_cast<const int4*>(A.slice + slice);
+  const int4 h0 = __ldg(hp), h1 = __ldg(hp + 1);
+  const int64_t col_off = ((int64_t)(uint32_t)h0.y << 32) | (uint32_t)h0.x;
+  const int uv_off = h0.z, g_off = h0.w, nuv = h1.x, ng = h1.y;
+  const int zero_row = (int)A.nl;
+  const int64_t row = slice * kSliceRows + lane;
+  const int* __restrict__ col = A.cols + col_off * 32 + lane * 4;
+  const double2* __restrict__ uv = reinterpret_cast<const double2*>(A.uvval + uv_off);
+  double acc[R];
+#pragma unroll
+  for (int k = 0; k < R; ++k) acc[k] = 0.0;
+  int4 c = nuv > 0 ? ld_stream_s32x4(col) : make_int4(zero_row, zero_row, zero_row, zero_row);
+  {
+    const char* base = reinterpret_cast<const char*>(A.cols + col_off * 32);
+    const int lines = nuv + ng;
+    for (int l = lane + 4; l < lines; l += 32) prefetch_l2(base + (size_t)l * 128);
+    if (lane * 16 < nuv) prefetch_l2(reinterpret_cast<const char*>(uv) + lane * 128);
+  }
+  pdl_wait();
+  for (int p = 0; p < nuv; p += 4) {
+    double g[4][R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      g[0][k] = __ldg(Y1 + (int64_t)k * ldy + c.x);
+      g[1][k] = __ldg(Y1 + (int64_t)k * ldy + c.y);
+      g[2][k] = __ldg(Y1 + (int64_t)k * ldy + c.z);
+      g[3][k] = __ldg(Y1 + (int64_t)k * ldy + c.w);
+    }
+    const double2 v01 = __ldg(uv + (p >> 1)), v23 = __ldg(uv + (p >> 1) + 1);
+    col += 128;
+    if (p + 4 < nuv) c = ld_stream_s32x4(col);
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      acc[k] = fma(v01.x, g[0][k], acc[k]);
+      acc[k] = fma(v01.y, g[1][k], acc[k]);
+      acc[k] = fma(v23.x, g[2][k], acc[k]);
+      acc[k] = fma(v23.y, g[3][k], acc[k]);
+    }
+  }
+  if (ng > 0) {
+    const int* __restrict__ gcol = A.cols + (col_off + nuv) * 32 + lane;
+    const double* __restrict__ gv = A.gval + (int64_t)g_off * 32 + lane;
+    for (int p = 0; p < ng; p += 4) {
+      int cc[4];
+      double v[4], g[4][R];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        cc[u] = p + u < ng ? ld_stream_s32(gcol + (p + u) * 32) : zero_row;
+        v[u] = p + u < ng ? ld_stream_f64(gv + (int64_t)(p + u) * 32) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int k = 0; k < R; ++k) g[u][k] = __ldg(Y1 + (int64_t)k * ldy + cc[u]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int k = 0; k < R; ++k) acc[k] = fma(v[u], g[u][k], acc[k]);
+    }
+  }
+  if (row < A.nl) {
+#pragma unroll
+    for (int k = 0; k < R; ++k) A.W[(int64_t)k * ldy + row] = acc[k];
+  }
+}
+
+// Second launch of the overlapped variant: W + partial sums + diagonal, then the combine.
+template <int R, int MODE>
+__global__ void __launch_bounds__(256)
+    hybrid_finish(HyView A, double s1, double s2, double b, const double* __restrict__ Y1,
+                  double* __restrict__ Y2, int64_t ldy, const double* __restrict__ X, int64_t ldx,
+                  double* __restrict__ Out, int64_t ldo) {
+  const int lane = threadIdx.x & 31;
+  const int64_t slice = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  pdl_launch_dependents();
+  if (slice >= A.nslices) {
+    pdl_wait();
+    return;
+  }
+  const int4* hp = reinterpret_cast<const int4*>(A.slice + slice);
+  const int4 h0 = __ldg(hp), h1 = __ldg(hp + 1);
+  const int64_t col_off = ((int64_t)(uint32_t)h0.y << 32) | (uint32_t)h0.x;
+  const int nuv = h1.x, ng = h1.y, np = h1.z;
+  const int64_t row = slice * kSliceRows + lane;
+  const int* __restrict__ pcol = A.cols + (col_off + nuv + ng) * 32 + lane;
+  const bool live = row < A.nl;
+  const double d = live ? ld_stream_f64(A.diag + row) : 0.0;
+  double x[R];
+  int sl[4];
+#pragma unroll
+  for (int p = 0; p < 4; ++p) sl[p] = p < np ? ld_stream_s32(pcol + p * 32) : 0;
+  if constexpr (MODE != 2) {
+#pragma unroll
+    for (int k = 0; k < R; ++k) x[k] = live ? ld_stream_f64(X + (int64_t)k * ldx + row) : 0.0;
+  }
+  pdl_wait();
+  if (!live) return;
+  double acc[R];
+#pragma unroll
+  for (int k = 0; k < R; ++k) acc[k] = A.W[(int64_t)k * ldy + row];
+  for (int p = 0; p < np; ++p) {
+    const int s = p < 4 ? sl[p] : ld_stream_s32(pcol + p * 32);
+#pragma unroll
+    for (int k = 0; k < R; ++k) acc[k] += A.P[(int64_t)k * A.ldp + s];
+  }
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    const double y1 = __ldg(Y1 + (int64_t)k * ldy + row);
+    const double w = fma(d, y1, acc[k]);
+    if constexpr (MODE == 2) {
+      Out[(int64_t)k * ldo + row] = w;
+    } else {
+      const double y2 = Y2[(int64_t)k * ldy + row];
+      const double o = combine<false>(s1, w, s2, y1, y2, b, x[k]);
+      if constexpr (MODE == 0)
+        Y2[(int64_t)k * ldy + row] = o;
+      else
+        Out[(int64_t)k * ldo + row] = o;
+    }
+  }
+}
+
 template <int R>
 void launch_hybrid_r(flz_ctx* ctx, const HyView& A, StepMode mode, double s1, double s2, double b,
                      const double* Y1, double* Y2, int64_t ldy, const double* X, int64_t ldx,
                      double* Out, int64_t ldo) {
   if (A.nslices == 0) return;
+  const size_t smem = (size_t)A.maxcols * 32 + (size_t)(kHyDenseWarps - 1) * R * 32 * 8;
+  const unsigned grid = (unsigned)((A.nslices + kWarpsPerBlock - 1) / kWarpsPerBlock);
+  if (hybrid_overlaps(ctx, A.nslices, A.ndtasks)) {
+    const unsigned total = grid + (unsigned)A.ndtasks;
+    launch_k1_smem(ctx, hybrid_gather<R, 6>, total, kWarpsPerBlock * 32, smem, A, Y1, ldy);
+    const unsigned fgrid = (unsigned)((A.nslices + 7) / 8);
+    switch (mode) {
+      case StepMode::step:
+        launch_k1(ctx, hybrid_finish<R, 0>, fgrid, 256, A, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo);
+        break;
+      case StepMode::final:
+        launch_k1(ctx, hybrid_finish<R, 1>, fgrid, 256, A, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo);
+        break;
+      case StepMode::plain:
+        launch_k1(ctx, hybrid_finish<R, 2>, fgrid, 256, A, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo);
+        break;
+      default:
+        throw ApiError(FLZ_EINVAL, "hybrid step: unsupported mode");
+    }
+    ctx->launches += 2;
+    return;
+  }
   if (A.ndtasks > 0) {
-    const size_t smem = (size_t)A.maxcols * 32 + (size_t)(kHyDenseWarps - 1) * R * 32 * 8;
     launch_k1_smem(ctx, hybrid_dense_tasks<R>, (unsigned)A.ndtasks, kHyDenseWarps * 32, smem, A, Y1, ldy);
     ctx->launches++;
   }
-  const unsigned grid = (unsigned)((A.nslices + kWarpsPerBlock - 1) / kWarpsPerBlock);
   // Registers against waves: 6 CTAs per SM (80 registers, no spills) when that needs no more
   // waves of CTAs than 8 per SM would (measured on B200: n = 113k, one wave either way, 24.2 ->
   // 21.4 us per step; n = 268k, 2 waves against 3, 40.2 against 42.9 us)
@@ -1385,11 +1624,6 @@ void launch_simple(flz_ctx* ctx, const SellView& A, double s1, double s2, double
 #endif
 
 
-// FLZ_ST_STAGES / FLZ_ST_CTAS: ring depth and CTAs per SM of the TMA-staged stencil kernel
-inline int env_int(const char* name, int dflt) {
-  const char* e = std::getenv(name);
-  return e && *e ? std::atoi(e) : dflt;
-}
 
 // Launches the TMA-staged stencil kernel when the matrix has a tile plan and the operands
 // allow 16-byte bulk copies; false: the caller falls back to the one-warp-per-slice kernel.
@@ -1537,6 +1771,17 @@ void launch_clenshaw_step(flz_ctx* ctx, const SellView& A, int R, int S, StepMod
   }
 #undef FLZ_K1_CASE
   FLZ_CUDA(cudaGetLastError());
+}
+
+// Overlapping pays for its second launch once a product is several waves of CTAs (measured on
+// B200: n = 268k, 3.7 waves, 40.2 -> 37.3 us per step; n = 113k, 2.3 waves, 21.4 -> 22.0).
+// FLZ_HY_OVERLAP=0|1 forces a variant.
+bool hybrid_overlaps(const flz_ctx* ctx, int64_t nslices, int64_t ndtasks) {
+  static const int forced = env_int("FLZ_HY_OVERLAP", FLZ_HY_OVERLAP_DEFAULT);
+  if (ndtasks <= 0) return false;
+  if (forced >= 0) return forced != 0;
+  const int64_t ctas = (nslices + kWarpsPerBlock - 1) / kWarpsPerBlock + ndtasks;
+  return ctas >= 3 * (int64_t)ctx->sm_count * 6;
 }
 
 void launch_hybrid_step(flz_ctx* ctx, const HyView& A, int R, StepMode mode, double s1, double s2,

@@ -179,6 +179,14 @@ class DeviceMatrix:
                 "fill": a.value / max(self.nnz, 1), "matrix_bytes": mb.value,
                 "uniform_entries": ue.value}
 
+    def k1_info(self, r=3):
+        """Kernel a fused Clenshaw step of r columns runs and the bytes it streams."""
+        info = (C.c_int64 * 4)()
+        name = C.create_string_buffer(96)
+        check(lib().flz_matrix_k1_info(self.handle, r, info, name, 96))
+        return {"kernel": name.value.decode(), "step_bytes": int(info[0]),
+                "dense_blocks": int(info[1]), "dense_entries": int(info[2])}
+
     def close(self):
         if getattr(self, "handle", None):
             lib().flz_matrix_destroy(self.handle)

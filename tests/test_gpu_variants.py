@@ -17,7 +17,7 @@ def run(code, env_extra, args=()):
     env = dict(os.environ)
     for k in ("FLZ_SPLIT", "FLZ_K1_LAYOUT", "FLZ_SYNC_CHECK", "FLZ_K1_TMA", "FLZ_K1_PDL",
               "FLZ_P2_CLUSTER", "FLZ_ST_TILE", "FLZ_ST_STAGES", "FLZ_ST_CTAS",
-              "FLZ_ST_PRODUCERS", "FLZ_HY"):
+              "FLZ_ST_PRODUCERS", "FLZ_HY", "FLZ_HY_OVERLAP"):
         env.pop(k, None)
     env.update(env_extra)
     p = subprocess.run([sys.executable, "-c", code, *args], env=env, capture_output=True,
@@ -32,6 +32,8 @@ def run(code, env_extra, args=()):
                                  {"FLZ_K1_PDL": "0"},          # plain stream-ordered launches
                                  {"FLZ_P2_CLUSTER": "1"},      # dense-block row clustering
                                  {"FLZ_ST_TILE": "0"},         # stencils: one-warp-per-slice kernel
+                                 {"FLZ_HY_OVERLAP": "1"},      # hybrid layout: gather + finish launches
+                                 {"FLZ_HY_OVERLAP": "0"},
                                  {"FLZ_ST_TILE": "64", "FLZ_ST_STAGES": "2", "FLZ_ST_CTAS": "3"},
                                  {"FLZ_ST_TILE": "256", "FLZ_ST_STAGES": "4", "FLZ_ST_CTAS": "1"},
                                  {"FLZ_ST_TILE": "512", "FLZ_K1_LAYOUT": "planar"}])
@@ -126,3 +128,38 @@ def test_tile_kernel_bit_identical_to_warp_kernel():
                 {"FLZ_ST_TILE": "32", "FLZ_ST_STAGES": "2", "FLZ_K1_LAYOUT": "planar"},
                 {"FLZ_ST_TILE": "256", "FLZ_ST_STAGES": "5", "FLZ_ST_CTAS": "1", "FLZ_K1_LAYOUT": "planar"}):
         assert run(TILE_CODE, env) == warp, env
+
+
+HY_CODE = r'''
+import sys, json, hashlib
+sys.path.insert(0, %r)
+import numpy as np
+from paper_2409_15053_b200 import Context, DeviceMatrix, matrices as M, solver as S
+ctx = Context(0)
+out = {}
+for name, gen in (("parsec7k", lambda: M.parsec_like(radius=12.0, n_atoms=12)),
+                  ("parsec_overlap", lambda: M.parsec_like(radius=10.0, n_atoms=30, ball_radius=3.6)),
+                  ("parsec20k", lambda: M.parsec_like(radius=17.0, n_atoms=40))):
+    n, rp, ci, va = gen()
+    A = DeviceMatrix(ctx, n, rp, ci, va)
+    out[name + "_kernel"] = A.k1_info(3)["kernel"] if hasattr(A, "k1_info") else ""
+    cf = S.indicator_coefficients(-0.3, 0.25, 25)
+    for r in (1, 2, 3, 4, 7):
+        X = np.random.default_rng(r).standard_normal((n, r))
+        Y = A.filter_apply(cf, 4.0, 4.5, X)
+        Z = A.spmm(X)
+        out["%%s_r%%d" %% (name, r)] = [hashlib.sha1(np.ascontiguousarray(Y).tobytes()).hexdigest(),
+                                      hashlib.sha1(np.ascontiguousarray(Z).tobytes()).hexdigest()]
+print(json.dumps(out))
+''' % ROOT
+
+
+def test_hybrid_overlapped_variant_bit_identical():
+    """hybrid_gather + hybrid_finish (dense tasks and slices in one launch, sums combined by a
+    second one) add in the same order as hybrid_dense_tasks + hybrid_slices."""
+    two = run(HY_CODE, {"FLZ_HY_OVERLAP": "0"})
+    one = run(HY_CODE, {"FLZ_HY_OVERLAP": "1"})
+    assert any("hybrid_gather" in v for k, v in one.items() if k.endswith("_kernel")), one
+    assert all("hybrid_gather" not in v for k, v in two.items() if k.endswith("_kernel"))
+    strip = lambda d: {k: v for k, v in d.items() if not k.endswith("_kernel")}
+    assert strip(one) == strip(two)
