@@ -81,6 +81,16 @@ struct Pinned {  // small RAII pinned host array
   Pinned& operator=(const Pinned&) = delete;
 };
 
+// FLZ_ORTH_FUSED=0: the multi-launch orthogonalization of the row-partitioned path on one
+// rank too (experiments, A/B tests)
+bool fused_orth_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("FLZ_ORTH_FUSED");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 void allreduce(flz_ctx* ctx, double* buf, size_t count) {
   if (ctx->nranks == 1 || count == 0) return;
   comm_allreduce_sum(ctx, buf, count, ctx->stream);
@@ -1301,44 +1311,59 @@ int flz_lanczos_step(flz_ctx* ctx, const flz_matrix* A, flz_basis* B, const doub
     // (lanczos.cpp:161-164) — it keeps the filter's X operand at a fixed address.
     FLZ_CUDA(cudaMemcpyAsync(B->X.p, B->col(newest), (size_t)ld * r * sizeof(double),
                              cudaMemcpyDeviceToDevice, ctx->stream));
+    double* Zout = (ctx->nranks == 1 && fused_orth_enabled()) ? B->col(cols) : B->Z.p;
     if (m >= 0)
-      filter_device(A, coeffs, m, c, e, B->X.p, ld, r, B->Z.p, ld);
+      filter_device(A, coeffs, m, c, e, B->X.p, ld, r, Zout, ld);
     else
-      spmm_device(A, B->X.p, ld, r, B->Z.p, ld, true);
+      spmm_device(A, B->X.p, ld, r, Zout, ld, true);
     FLZ_CUDA(cudaEventRecord(B->e1, ctx->stream));
 
-    // op_scale = max(op_scale, ||Z_j||) (lanczos.cpp:169-170)
-    launch_coldot(ctx, B->Z.p, ld, B->Z.p, ld, r, nl, sm + L.normsq);
-    allreduce(ctx, sm + L.normsq, r);
-    launch_update_scale(ctx, sm + L.normsq, r, 0, sm + L.scale);
+    const bool fused = ctx->nranks == 1 && fused_orth_enabled();
+    if (fused) {
+      // One rank: Z already sits in the pending block's storage, so [Q_k Z]^T Z gives the
+      // projection coefficients AND Z^T Z (op_scale) in one sweep; the intra-block QR is one
+      // cooperative launch that normalises the pending block in place.
+      double* P = B->col(cols);
+      launch_gemm_tn(ctx, B->Q.p, ld, cols + r, P, ld, r, nl, sm + L.C1, L.ldc);
+      launch_gemm_nn(ctx, B->Q.p, ld, cols, sm + L.C1, L.ldc, r, nl, -1.0, true, P, ld);
+      launch_gemm_tn(ctx, B->Q.p, ld, cols, P, ld, r, nl, sm + L.C2, L.ldc);
+      launch_gemm_nn(ctx, B->Q.p, ld, cols, sm + L.C2, L.ldc, r, nl, -1.0, true, P, ld);
+      launch_block_qr(ctx, P, ld, nl, r, sm + L.C1 + cols * L.ldc, L.ldc + 1, sm + L.scale,
+                      sm + L.Sk, sm + L.dead);
+    } else {
+      // op_scale = max(op_scale, ||Z_j||) (lanczos.cpp:169-170)
+      launch_coldot(ctx, B->Z.p, ld, B->Z.p, ld, r, nl, sm + L.normsq);
+      allreduce(ctx, sm + L.normsq, r);
+      launch_update_scale(ctx, sm + L.normsq, r, 0, sm + L.scale);
 
-    // two full Gram-Schmidt sweeps in GEMM form (lanczos.cpp:177-182)
-    launch_gemm_tn(ctx, B->Q.p, ld, cols, B->Z.p, ld, r, nl, sm + L.C1, L.ldc);
-    allreduce(ctx, sm + L.C1, (size_t)cols * L.ldc);
-    launch_gemm_nn(ctx, B->Q.p, ld, cols, sm + L.C1, L.ldc, r, nl, -1.0, true, B->Z.p, ld);
-    launch_gemm_tn(ctx, B->Q.p, ld, cols, B->Z.p, ld, r, nl, sm + L.C2, L.ldc);
-    allreduce(ctx, sm + L.C2, (size_t)cols * L.ldc);
-    launch_gemm_nn(ctx, B->Q.p, ld, cols, sm + L.C2, L.ldc, r, nl, -1.0, true, B->Z.p, ld);
+      // two full Gram-Schmidt sweeps in GEMM form (lanczos.cpp:177-182)
+      launch_gemm_tn(ctx, B->Q.p, ld, cols, B->Z.p, ld, r, nl, sm + L.C1, L.ldc);
+      allreduce(ctx, sm + L.C1, (size_t)cols * L.ldc);
+      launch_gemm_nn(ctx, B->Q.p, ld, cols, sm + L.C1, L.ldc, r, nl, -1.0, true, B->Z.p, ld);
+      launch_gemm_tn(ctx, B->Q.p, ld, cols, B->Z.p, ld, r, nl, sm + L.C2, L.ldc);
+      allreduce(ctx, sm + L.C2, (size_t)cols * L.ldc);
+      launch_gemm_nn(ctx, B->Q.p, ld, cols, sm + L.C2, L.ldc, r, nl, -1.0, true, B->Z.p, ld);
 
-    // intra-block QR, two sweeps against the finished pending columns (lanczos.cpp:205-230)
-    FLZ_CUDA(cudaMemsetAsync(sm + L.Sk, 0, (size_t)(L.normsq - L.Sk) * sizeof(double),
-                             ctx->stream));
-    double* P = B->col(cols);
-    for (int j = 0; j < r; ++j) {
-      double* zj = B->Z.p + (int64_t)j * ld;
-      if (j > 0) {
-        for (int pass = 0; pass < 2; ++pass) {
-          double* t = sm + (pass == 0 ? L.t1 : L.t2) + (int64_t)j * kRMax * 8;
-          launch_gemm_tn(ctx, P, ld, j, zj, ld, 1, nl, t, 8);
-          allreduce(ctx, t, (size_t)j * 8);
-          launch_gemm_nn(ctx, P, ld, j, t, 8, 1, nl, -1.0, true, zj, ld);
+      // intra-block QR, two sweeps against the finished pending columns (lanczos.cpp:205-230)
+      FLZ_CUDA(cudaMemsetAsync(sm + L.Sk, 0, (size_t)(L.normsq - L.Sk) * sizeof(double),
+                               ctx->stream));
+      double* P = B->col(cols);
+      for (int j = 0; j < r; ++j) {
+        double* zj = B->Z.p + (int64_t)j * ld;
+        if (j > 0) {
+          for (int pass = 0; pass < 2; ++pass) {
+            double* t = sm + (pass == 0 ? L.t1 : L.t2) + (int64_t)j * kRMax * 8;
+            launch_gemm_tn(ctx, P, ld, j, zj, ld, 1, nl, t, 8);
+            allreduce(ctx, t, (size_t)j * 8);
+            launch_gemm_nn(ctx, P, ld, j, t, 8, 1, nl, -1.0, true, zj, ld);
+          }
         }
+        launch_coldot(ctx, zj, ld, zj, ld, 1, nl, sm + L.normsq + j);
+        allreduce(ctx, sm + L.normsq + j, 1);
+        launch_finish_col(ctx, sm + L.normsq + j, sm + L.scale, sm + L.Sk, r, j, sm + L.inv + j,
+                          sm + L.dead + j);
+        launch_scale_copy(ctx, zj, sm + L.inv + j, P + (int64_t)j * ld, nl);
       }
-      launch_coldot(ctx, zj, ld, zj, ld, 1, nl, sm + L.normsq + j);
-      allreduce(ctx, sm + L.normsq + j, 1);
-      launch_finish_col(ctx, sm + L.normsq + j, sm + L.scale, sm + L.Sk, r, j, sm + L.inv + j,
-                        sm + L.dead + j);
-      launch_scale_copy(ctx, zj, sm + L.inv + j, P + (int64_t)j * ld, nl);
     }
     FLZ_CUDA(cudaEventRecord(B->e2, ctx->stream));
 
@@ -1354,8 +1379,9 @@ int flz_lanczos_step(flz_ctx* ctx, const flz_matrix* A, flz_basis* B, const doub
     for (int i = 0; i < r * r; ++i) Sk[i] = 0.0;
     for (int j = 0; j < r; ++j) {
       for (int i = 0; i < j; ++i)
-        Sk[i * r + j] = h[L.t1 + (int64_t)j * kRMax * 8 + i * 8] +
-                        h[L.t2 + (int64_t)j * kRMax * 8 + i * 8];
+        Sk[i * r + j] = fused ? h[L.Sk + i * r + j]
+                              : h[L.t1 + (int64_t)j * kRMax * 8 + i * 8] +
+                                    h[L.t2 + (int64_t)j * kRMax * 8 + i * 8];
       Sk[j * r + j] = h[L.Sk + j * r + j];
       dead[j] = h[L.dead + j] != 0.0 ? 1 : 0;
     }

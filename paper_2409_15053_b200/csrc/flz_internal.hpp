@@ -172,6 +172,9 @@ struct flz_ctx {
   flz::DevBuf<double> stage;     // host<->device staging of blocks
   flz::DevBuf<double> stage2;
   flz::DevBuf<char> flush;       // L2 flush target
+  flz::DevBuf<double> qr_scratch;              // block_qr_kernel: per-phase, per-CTA partial sums
+  flz::DevBuf<unsigned long long> qr_barrier;  // its grid-barrier counter (monotone)
+  unsigned long long qr_arrivals = 0;          // arrivals issued so far
 };
 
 // ----------------------------------------------------------------- matrix
@@ -421,6 +424,9 @@ void launch_permute_in(flz_ctx* ctx, const double* src, int64_t lds, double* dst
 void launch_permute_out(flz_ctx* ctx, const double* src, int64_t lds, double* dst, int64_t ldd,
                         int N, int64_t rows, const int32_t* perm);
 // block-step scalar logic (single thread kernels)
+void launch_block_qr(flz_ctx* ctx, double* Z, int64_t ld, int64_t rows, int r,
+                     const double* normsq0, int64_t stride, double* scale, double* Sk,
+                     double* dead);
 void launch_update_scale(flz_ctx* ctx, const double* gram, int r, int ldg, double* op_scale);
 void launch_finish_col(flz_ctx* ctx, const double* normsq, const double* op_scale, double* Sk,
                        int r, int j, double* inv, double* dead_flag);

@@ -216,6 +216,275 @@ __global__ void __launch_bounds__(256)
     }
 }
 
+// ---------------------------------------------------------------- ts_update (K4, N <= 8)
+// Out[i, 0..N) += alpha * sum_j A[i, j] * Bs[j][0..N): the Gram-Schmidt update of a block of
+// N <= 8 columns against K basis columns, gemm_nn_kernel<1, true>'s fragment mapping (a warp
+// owns 16 rows as two interleaved 8-row tiles, one k-step = 4 columns) with two changes the
+// small-n shapes need:
+//  * U = 8 k-steps are requested together (volatile loads, 8 x 512 B per warp in flight; the
+//    compiler had interleaved loads and DMMAs of the unrolled loop);
+//  * the 8 warps of a CTA are RW = 8 / KW row groups x KW column sets, so that a 40k-row basis
+//    still gives several waves of CTAs (gemm_nn: 313 CTAs = 0.42 waves, 3.5 TB/s at
+//    40k x 1700; 864 CTAs = 1.17 waves, 4.2 TB/s at 110k x 630 with a quarter of the time in
+//    the tail).  The KW partial fragments of a row group meet in shared memory in warp order:
+//    deterministic.
+template <int KW>
+__global__ void __launch_bounds__(256)
+    ts_update_kernel(const double* __restrict__ A, int64_t lda, int64_t K,
+                     const double* __restrict__ Bs, int64_t ldbs, int N, int64_t rows,
+                     double alpha, double* __restrict__ Out, int64_t ldo) {
+  constexpr int RW = 8 / KW, U = 8;
+  __shared__ double part[KW > 1 ? KW - 1 : 1][RW][4][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int rg = warp / KW, kw = warp % KW;
+  const int64_t i0 = ((int64_t)blockIdx.x * RW + rg) * 16;
+  const bool live = i0 < rows;
+  double ce0 = 0.0, ce1 = 0.0, co0 = 0.0, co1 = 0.0;
+  const double* ap = A + (live ? i0 : 0) + 2 * g;
+  const double* bp = Bs + g;
+  const int64_t ngroups = (K + 3) / 4, full = K / 4;   // groups with all four columns < K
+  const int64_t step_a = 4 * (int64_t)KW * lda, step_b = 4 * (int64_t)KW * ldbs;
+  const double* pa = ap + (4 * (int64_t)kw + t) * lda;
+  const double* pb = bp + (4 * (int64_t)kw + t) * ldbs;
+  int64_t q0 = kw;
+  if (live) {
+    for (; q0 + (int64_t)(U - 1) * KW < full; q0 += (int64_t)KW * U) {   // whole batches: no checks
+      double2 a2[U];
+      double b[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        a2[u] = ld_stream_f64x2(pa + u * step_a);
+        b[u] = __ldg(pb + u * step_b);
+      }
+      pa += U * step_a;
+      pb += U * step_b;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        dmma(ce0, ce1, a2[u].x, b[u]);
+        dmma(co0, co1, a2[u].y, b[u]);
+      }
+    }
+  }
+  for (; q0 < ngroups; q0 += KW) {   // the last, partial batch
+    const int64_t j = 4 * q0 + t;
+    const bool ok = live && j < K;
+    const double2 a2 = ok ? ld_stream_f64x2(ap + j * lda) : make_double2(0.0, 0.0);
+    const double b = ok ? __ldg(bp + j * ldbs) : 0.0;
+    dmma(ce0, ce1, a2.x, b);
+    dmma(co0, co1, a2.y, b);
+  }
+  if constexpr (KW > 1) {
+    if (kw > 0) {
+      part[kw - 1][rg][0][lane] = ce0;
+      part[kw - 1][rg][1][lane] = ce1;
+      part[kw - 1][rg][2][lane] = co0;
+      part[kw - 1][rg][3][lane] = co1;
+    }
+    __syncthreads();
+    if (kw > 0) return;
+#pragma unroll
+    for (int w = 0; w < KW - 1; ++w) {
+      ce0 += part[w][rg][0][lane];
+      ce1 += part[w][rg][1][lane];
+      co0 += part[w][rg][2][lane];
+      co1 += part[w][rg][3][lane];
+    }
+  }
+  // fragment (row g of the even/odd tile, columns 2t, 2t+1) -> rows i0+2g, i0+2g+1
+  const int64_t i = i0 + 2 * g;
+  if (!live || i >= rows) return;
+  const bool second = (i + 1) < rows;
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    const int n = 2 * t + e;
+    if (n >= N) continue;
+    double* o = Out + (int64_t)n * ldo + i;
+    const double2 old = *reinterpret_cast<const double2*>(o);
+    const double v0 = fma(alpha, e == 0 ? ce0 : ce1, old.x);
+    const double v1 = fma(alpha, e == 0 ? co0 : co1, old.y);
+    if (second)
+      *reinterpret_cast<double2*>(o) = make_double2(v0, v1);
+    else
+      o[0] = v0;
+  }
+}
+
+// ---------------------------------------------------------------- block QR (one rank)
+// Intra-block QR of the r twice-projected columns (lanczos.cpp:205-230) in ONE cooperative
+// launch: CTA c owns a fixed range of rows; a reduction is per-CTA partials (fixed tree) ->
+// scratch slot -> grid barrier -> every CTA adds the slots in the same order.  Column j:
+//   [scale column j-1 +] dots against P_0..P_{j-1}   | reduce
+//   first update + second-pass dots                    | reduce
+//   second update + sum of squares                     | reduce
+//   norm -> S_k(j,j), dead flag; the scaling is folded into the next column's first phase.
+// 1 + 3 (r - 1) reductions instead of ~6 launches per column.  Columns are normalised in
+// place (Z is the pending block's storage in the basis).
+struct QrArgs {
+  double* Z;            // r columns, leading dimension ld, normalised in place
+  int64_t ld, rows;
+  int r;
+  const double* normsq0;  // z_j . z_j BEFORE the Gram-Schmidt sweeps at normsq0[j * stride] (op_scale)
+  int64_t stride;
+  double* scale;        // op_scale, in/out
+  double* Sk;           // r x r row-major, written whole
+  double* dead;         // r flags (0.0 / 1.0)
+  double* scratch;      // [phases][gridDim.x][RQ] partial sums
+  unsigned long long* barrier;
+  unsigned long long base;   // arrivals before this launch
+};
+
+__device__ __forceinline__ void grid_barrier(unsigned long long* ctr, unsigned long long target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(ctr, 1ULL);
+    unsigned long long seen;
+    do {
+      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(seen) : "l"(ctr) : "memory");
+    } while (seen < target);
+  }
+  __syncthreads();
+}
+
+template <int RQ>
+__global__ void __launch_bounds__(256) block_qr_kernel(QrArgs a) {
+  __shared__ double red[8][RQ];
+  __shared__ double tot[RQ];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int G = gridDim.x, r = a.r;
+  const int64_t per = ((a.rows + G - 1) / G + 1) & ~(int64_t)1;
+  const int64_t r0 = min(a.rows, (int64_t)blockIdx.x * per), r1 = min(a.rows, r0 + per);
+  int phase = 0;
+  unsigned long long arrived = a.base;
+  // sum `v[0..count)` over the grid; every thread of every CTA receives the totals in tot[]
+  auto reduce = [&](double (&v)[RQ], int count) {
+#pragma unroll
+    for (int q = 0; q < RQ; ++q) {
+      if (q < count) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) v[q] += __shfl_down_sync(0xffffffffu, v[q], off);
+        if (lane == 0) red[warp][q] = v[q];
+      }
+    }
+    __syncthreads();
+    double* slot = a.scratch + ((int64_t)phase * G + blockIdx.x) * RQ;
+    if (threadIdx.x < count) {
+      double s = 0.0;
+      for (int w = 0; w < 8; ++w) s += red[w][threadIdx.x];
+      slot[threadIdx.x] = s;
+    }
+    arrived += (unsigned long long)G;
+    grid_barrier(a.barrier, arrived);
+    if (warp < count && warp < 8) {   // warp q adds slot q of every CTA: lanes stride, fixed tree
+      double s = 0.0;
+      for (int c = lane; c < G; c += 32) s += __ldcg(a.scratch + ((int64_t)phase * G + c) * RQ + warp);
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off);
+      if (lane == 0) tot[warp] = s;
+    }
+    if constexpr (RQ > 8) {
+      if (warp == 0)
+        for (int q = 8; q < count; ++q) {
+          double s = 0.0;
+          for (int c = lane; c < G; c += 32) s += __ldcg(a.scratch + ((int64_t)phase * G + c) * RQ + q);
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off);
+          if (lane == 0) tot[q] = s;
+        }
+    }
+    __syncthreads();
+    ++phase;
+  };
+  // op_scale = max(op_scale, ||z_j||) over the block, before the sweeps (lanczos.cpp:169-170)
+  double scale = *a.scale;
+  for (int j = 0; j < r; ++j) scale = fmax(scale, sqrt(fmax(a.normsq0[j * a.stride], 0.0)));
+  const double dead_tol = 1e-10 * fmax(scale, 1e-300);
+  double inv_prev = 1.0;   // scaling still owed to column j - 1
+  for (int j = 0; j < r; ++j) {
+    double* zj = a.Z + (int64_t)j * a.ld;
+    double coeff[RQ], d[RQ];
+#pragma unroll
+    for (int q = 0; q < RQ; ++q) coeff[q] = d[q] = 0.0;
+    if (j > 0) {
+      // phase A: scale column j-1 (owed), first-pass dots
+      double* zp = a.Z + (int64_t)(j - 1) * a.ld;
+      for (int64_t i = r0 + threadIdx.x; i < r1; i += 256) {
+        const double p = zp[i] * inv_prev;
+        zp[i] = p;
+        const double z = zj[i];
+#pragma unroll
+        for (int q = 0; q < RQ; ++q)
+          if (q < j) d[q] = fma(q == j - 1 ? p : a.Z[(int64_t)q * a.ld + i], z, d[q]);
+      }
+      reduce(d, j);
+#pragma unroll
+      for (int q = 0; q < RQ; ++q)
+        if (q < j) coeff[q] = tot[q];
+      // phase B: first update, second-pass dots
+      double c1[RQ];
+#pragma unroll
+      for (int q = 0; q < RQ; ++q) {
+        c1[q] = q < j ? tot[q] : 0.0;
+        d[q] = 0.0;
+      }
+      for (int64_t i = r0 + threadIdx.x; i < r1; i += 256) {
+        double z = zj[i];
+        double pq[RQ];
+#pragma unroll
+        for (int q = 0; q < RQ; ++q)
+          if (q < j) {
+            pq[q] = a.Z[(int64_t)q * a.ld + i];
+            z = fma(-c1[q], pq[q], z);
+          }
+        zj[i] = z;
+#pragma unroll
+        for (int q = 0; q < RQ; ++q)
+          if (q < j) d[q] = fma(pq[q], z, d[q]);
+      }
+      reduce(d, j);
+#pragma unroll
+      for (int q = 0; q < RQ; ++q)
+        if (q < j) {
+          c1[q] = tot[q];
+          coeff[q] += tot[q];
+        }
+      // phase C: second update, sum of squares
+      double ss[RQ];
+#pragma unroll
+      for (int q = 0; q < RQ; ++q) ss[q] = 0.0;
+      for (int64_t i = r0 + threadIdx.x; i < r1; i += 256) {
+        double z = zj[i];
+#pragma unroll
+        for (int q = 0; q < RQ; ++q)
+          if (q < j) z = fma(-c1[q], a.Z[(int64_t)q * a.ld + i], z);
+        zj[i] = z;
+        ss[0] = fma(z, z, ss[0]);
+      }
+      reduce(ss, 1);
+    } else {
+      double ss[RQ];
+#pragma unroll
+      for (int q = 0; q < RQ; ++q) ss[q] = 0.0;
+      for (int64_t i = r0 + threadIdx.x; i < r1; i += 256) ss[0] = fma(zj[i], zj[i], ss[0]);
+      reduce(ss, 1);
+    }
+    const double norm = sqrt(fmax(tot[0], 0.0));
+    const bool alive = norm > dead_tol;
+    inv_prev = alive ? 1.0 / norm : 0.0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      for (int q = 0; q < r; ++q) a.Sk[q * r + j] = q < j ? coeff[q] : 0.0;
+      a.Sk[j * r + j] = alive ? norm : 0.0;
+      a.dead[j] = alive ? 0.0 : 1.0;
+    }
+    __syncthreads();   // tot[] is rewritten by the next reduction
+  }
+  // the last column's scaling
+  double* zl = a.Z + (int64_t)(r - 1) * a.ld;
+  for (int64_t i = r0 + threadIdx.x; i < r1; i += 256) zl[i] *= inv_prev;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *a.scale = scale;
+}
+
 // ---------------------------------------------------------------- helpers
 // out[c] = sum_i A[i,c]*B[i,c]: one block row-chunk per (chunk, c), fixed-order tree
 __global__ void __launch_bounds__(256)
@@ -321,6 +590,15 @@ __global__ void finish_col_kernel(const double* normsq, const double* op_scale, 
 
 // --------------------------------------------------------------- launchers
 
+// FLZ_TS_UPDATE=0: the DMMA gemm_nn for the Gram-Schmidt updates too (experiments)
+static bool ts_update_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("FLZ_TS_UPDATE");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 void launch_gemm_tn(flz_ctx* ctx, const double* A, int64_t lda, int64_t M, const double* B,
                     int64_t ldb, int N, int64_t rows, double* C, int64_t ldc) {
   if (M <= 0 || N <= 0) return;
@@ -369,6 +647,26 @@ void launch_gemm_nn(flz_ctx* ctx, const double* A, int64_t lda, int64_t K, const
   if (rows <= 0 || N <= 0) return;
   FLZ_REQUIRE(round_up(rows, 2) <= lda && round_up(rows, 2) <= ldo, FLZ_EDIM,
               "gemm_nn: leading dimension too small");
+  if (accumulate && N <= 8 && K > 0 && ldbs >= 8 && ts_update_enabled()) {
+    // tall-skinny update: as many column sets per CTA as it takes to have ~4 waves of CTAs
+    // (4 resident CTAs per SM)
+    const int64_t want = (int64_t)ctx->sm_count * 16;
+    int rw = 8;
+    while (rw > 1 && (rows + 16 * rw - 1) / (16 * rw) < want) rw >>= 1;
+    const unsigned grid = (unsigned)((rows + 16 * rw - 1) / (16 * rw));
+#define FLZ_TSU(KWV)                                                                          \
+  ts_update_kernel<KWV><<<grid, 256, 0, ctx->stream>>>(A, lda, K, Bs, ldbs, N, rows, alpha, Out, ldo)
+    switch (rw) {
+      case 8: FLZ_TSU(1); break;
+      case 4: FLZ_TSU(2); break;
+      case 2: FLZ_TSU(4); break;
+      default: FLZ_TSU(8); break;
+    }
+#undef FLZ_TSU
+    ctx->launches++;
+    FLZ_CUDA(cudaGetLastError());
+    return;
+  }
   const int NT = N > 32 ? 8 : (N > 16 ? 4 : (N > 8 ? 2 : 1));
   FLZ_REQUIRE(ldbs >= round_up(N, 8 * NT), FLZ_EDIM, "gemm_nn: Bs row stride too small");
   dim3 grid((unsigned)((rows + 127) / 128), (unsigned)((N + 8 * NT - 1) / (8 * NT)));
@@ -388,6 +686,33 @@ void launch_gemm_nn(flz_ctx* ctx, const double* A, int64_t lda, int64_t K, const
 #undef FLZ_NN
   ctx->launches++;
   FLZ_CUDA(cudaGetLastError());
+}
+
+// Intra-block QR in one cooperative launch (one rank).  normsq0: z_j . z_j before the sweeps at
+// stride `stride`.  Sk (r x r row-major), dead (r flags) and *scale are device pointers.
+void launch_block_qr(flz_ctx* ctx, double* Z, int64_t ld, int64_t rows, int r,
+                     const double* normsq0, int64_t stride, double* scale, double* Sk,
+                     double* dead) {
+  FLZ_REQUIRE(r >= 1 && r <= 16, FLZ_EINVAL, "block_qr: block size out of range");
+  const int G = (int)std::max<int64_t>(1, std::min<int64_t>(ctx->sm_count, (rows + 511) / 512));
+  const int RQ = r <= 4 ? 4 : 16;
+  const int phases = 1 + 3 * (r - 1);
+  if (ctx->qr_scratch.count == 0) {
+    ctx->qr_scratch.reserve((size_t)(1 + 3 * 15) * ctx->sm_count * 16);
+    ctx->qr_barrier.reserve_zero(1, ctx->stream);
+    ctx->qr_arrivals = 0;
+  }
+  QrArgs a{Z, ld, rows, r, normsq0, stride, scale, Sk, dead, ctx->qr_scratch.p,
+           reinterpret_cast<unsigned long long*>(ctx->qr_barrier.p), ctx->qr_arrivals};
+  void* args[] = {&a};
+  if (RQ == 4)
+    FLZ_CUDA(cudaLaunchCooperativeKernel((const void*)block_qr_kernel<4>, dim3(G), dim3(256), args,
+                                         0, ctx->stream));
+  else
+    FLZ_CUDA(cudaLaunchCooperativeKernel((const void*)block_qr_kernel<16>, dim3(G), dim3(256),
+                                         args, 0, ctx->stream));
+  ctx->qr_arrivals += (unsigned long long)phases * G;
+  ctx->launches++;
 }
 
 void launch_coldot(flz_ctx* ctx, const double* A, int64_t lda, const double* B, int64_t ldb, int N,
