@@ -288,6 +288,20 @@ struct flz_basis {
   double op_scale = 0.0;
   double mv_s = 0.0, orth_s = 0.0;
   cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr;
+  // Speculative operator application (one rank, fused orthogonalization): the step that has
+  // just queued its small D2H copies also queues op(pending block) for the NEXT step, so the
+  // device works while the host waits for and digests the step's results.  The next
+  // flz_lanczos_step consumes it when its arguments match and nothing touched the basis in
+  // between (basis_set / truncate / orthogonalize_column drop it and take its matvecs back).
+  cudaEvent_t s0[2] = {nullptr, nullptr}, s1[2] = {nullptr, nullptr};   // around the speculative
+  int spec_slot = 0;                        // application (two pairs: one read, one recorded)
+  cudaEvent_t e1b = nullptr, e_done = nullptr;
+  bool spec_valid = false;
+  std::vector<double> spec_coeffs;          // the coefficients it was queued with (by value)
+  int spec_m = 0;
+  double spec_c = 0.0, spec_e = 0.0;
+  uint64_t spec_matvecs = 0;
+  float last_mv_ms = 0.f;
   double* col(int64_t j) const { return Q.p + j * ld; }
 };
 
