@@ -135,6 +135,11 @@ int flz_plan_create(int64_t n_global, int rank, int nranks, const int64_t* start
                     const int64_t* row_ptr, const int32_t* col_idx, const double* values,
                     int sigma, flz_plan** out);
 void flz_plan_destroy(flz_plan* plan);
+/* Device copy of a finished single-rank plan (nranks == 1 on both sides): what
+ * flz_matrix_upload does after building the plan itself.  Lets a caller build the layout on
+ * host threads ahead of time (SparseSymMatrix::from_csr builds it beside its symmetry check).
+ * The plan is consumed: its arrays move into the matrix, a second upload is refused. */
+int flz_matrix_upload_plan(flz_ctx* ctx, flz_plan* plan, flz_matrix** out);
 int flz_plan_info(const flz_plan* plan, int64_t* info);
 int64_t flz_plan_need(const flz_plan* plan, int peer, int64_t* rows);
 int flz_plan_set_give(flz_plan* plan, int peer, int64_t count, const int64_t* rows);

@@ -195,6 +195,10 @@ class SparseSymMatrix {
   double max_abs_ = 0.0;
   struct DeviceCopy;
   mutable std::shared_ptr<DeviceCopy> dev_;
+  // Device layout built ahead of the first use: from_csr plans a large matrix on host threads
+  // beside its symmetry check (single-GPU contexts); device() uploads it and drops it.
+  struct Planned;
+  mutable std::shared_ptr<Planned> planned_;
 };
 
 // Matrix Market coordinate files (real / integer / pattern, general / symmetric), with the

@@ -92,6 +92,7 @@ _SIGS = {
     "flz_ctx_set_tuning": (i32, [vp, i32, i32, i32]),
     "flz_plan_create": (i32, [i64, i32, i32, i64p, i64p, i32p, f64p, i32, C.POINTER(vp)]),
     "flz_plan_destroy": (None, [vp]),
+    "flz_matrix_upload_plan": (i32, [vp, vp, C.POINTER(vp)]),
     "flz_plan_info": (i32, [vp, i64p]),
     "flz_plan_need": (i64, [vp, i32, vp]),
     "flz_plan_set_give": (i32, [vp, i32, i64, i64p]),

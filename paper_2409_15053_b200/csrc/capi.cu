@@ -812,6 +812,7 @@ int flz_matrix_upload(flz_ctx* ctx, int64_t n_global, int64_t row_begin, int64_t
 // ---- host-only view of the plan (no GPU needed): used to test the multi-GPU logic on CPUs
 struct flz_plan {
   HostPlan P;
+  bool consumed = false;
 };
 
 int flz_plan_create(int64_t n_global, int rank, int nranks, const int64_t* starts,
@@ -831,6 +832,21 @@ int flz_plan_create(int64_t n_global, int rank, int nranks, const int64_t* start
   });
 }
 void flz_plan_destroy(flz_plan* plan) { delete plan; }
+int flz_matrix_upload_plan(flz_ctx* ctx, flz_plan* plan, flz_matrix** out) {
+  return guarded([&] {
+    FLZ_REQUIRE(ctx && plan && out, FLZ_EINVAL, "matrix_upload_plan: null argument");
+    FLZ_REQUIRE(ctx->nranks == 1 && plan->P.nranks == 1, FLZ_EINVAL,
+                "matrix_upload_plan: single-rank plans and contexts only");
+    FLZ_REQUIRE(!plan->consumed, FLZ_EINVAL, "matrix_upload_plan: the plan was uploaded before");
+    use(ctx);
+    const Trace t(ctx, "upload of the prebuilt plan");
+    auto A = std::make_unique<flz_matrix>();
+    plan->consumed = true;
+    upload_plan(ctx, plan->P, A.get());
+    ctx->refs += 1;
+    *out = A.release();
+  });
+}
 int flz_plan_info(const flz_plan* plan, int64_t* info) {
   const HostPlan& P = plan->P;
   const int64_t v[10] = {P.nl, (int64_t)P.halo.size(), P.nslices, P.stored,

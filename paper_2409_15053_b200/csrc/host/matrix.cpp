@@ -45,6 +45,15 @@ bool g_ctx_owned = false;
 int g_dev_index = -1;
 }  // namespace
 
+// FLZ_PLAN_AHEAD=0: the device layout is built at the first product (experiments)
+static bool g_plan_ahead_off() {
+  static const bool off = [] {
+    const char* e = std::getenv("FLZ_PLAN_AHEAD");
+    return e && e[0] == '0';
+  }();
+  return off;
+}
+
 flz_ctx* Device::context() {
   std::lock_guard<std::mutex> lock(g_dev_mutex);
   if (!g_ctx) {
@@ -84,6 +93,13 @@ struct SparseSymMatrix::DeviceCopy {
   flz_ctx* ctx = nullptr;
   ~DeviceCopy() {
     if (handle) flz_matrix_destroy(handle);
+  }
+};
+
+struct SparseSymMatrix::Planned {
+  flz_plan* plan = nullptr;
+  ~Planned() {
+    if (plan) flz_plan_destroy(plan);
   }
 };
 
@@ -199,7 +215,31 @@ SparseSymMatrix SparseSymMatrix::from_csr(std::size_t n, std::vector<std::int64_
   });
   if (bad_msg) throw Error(bad_msg);
   A.max_abs_ = max_abs;
+  // Large matrices headed for a single-GPU context: the device layout (csrc/host/plan.cpp, host
+  // threads only) is built now, beside the symmetry check, instead of at the first product.
+  // The arrays are structurally valid at this point, which is all the planner needs; a
+  // planning failure is not an error here — device() then plans again and reports it.
+  const bool plan_now = A.col_idx_.size() >= (std::size_t(1) << 20) && !g_plan_ahead_off() &&
+                        (g_ctx == nullptr || flz_ctx_nranks(g_ctx) == 1);
+  std::shared_ptr<Planned> planned;
+  std::thread planner;
+  if (plan_now)
+    planner = std::thread([&] {
+      const std::int64_t starts[2] = {0, static_cast<std::int64_t>(n)};
+      auto P = std::make_shared<Planned>();
+      if (flz_plan_create(static_cast<std::int64_t>(n), 0, 1, starts, A.row_ptr_.data(),
+                          A.col_idx_.data(), A.values_.data(), 0, &P->plan) == FLZ_OK)
+        planned = std::move(P);
+    });
+  struct Join {
+    std::thread& t;
+    ~Join() {
+      if (t.joinable()) t.join();
+    }
+  } join{planner};
   if (check) A.verify_symmetry();
+  if (planner.joinable()) planner.join();
+  A.planned_ = std::move(planned);
   return A;
 }
 
@@ -233,21 +273,51 @@ SparseSymMatrix SparseSymMatrix::from_local_rows(std::size_t n_global, std::size
 // runs, so the entry the reference would report is the one reported.
 void SparseSymMatrix::verify_symmetry() const {
   std::atomic<bool> ok{true};
-  parallel_rows(n_, [&](std::size_t r0, std::size_t r1) {
-    for (std::size_t i = r0; i < r1 && ok.load(std::memory_order_relaxed); ++i)
-      for (std::int64_t p = row_ptr_[i]; p < row_ptr_[i + 1]; ++p) {
-        const auto j = static_cast<std::size_t>(col_idx_[p]);
-        if (j <= i) continue;
-        const std::int32_t* first = col_idx_.data() + row_ptr_[j];
-        const std::int32_t* last = col_idx_.data() + row_ptr_[j + 1];
-        const std::int32_t* hit = std::lower_bound(first, last, static_cast<std::int32_t>(i));
-        if (hit == last || *hit != static_cast<std::int32_t>(i) ||
-            values_[p] != values_[row_ptr_[j] + (hit - first)]) {
+  // Thread t owns the mirror rows j in [J0, J1).  It walks the rows i < J1 in ascending order
+  // and, for every upper entry (i, j) with j in its range, advances row j's cursor to column
+  // i: the mirrors of one row are asked for in ascending column order, so a cursor per row
+  // replaces the reference's binary search per entry (one random access instead of ~7).
+  // Lower entries without an upper partner are skipped, as the reference never looks them up.
+  unsigned workers = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  if (const char* e = std::getenv("FLZ_HOST_THREADS")) workers = std::max(1, std::atoi(e));
+  workers = (unsigned)std::min<std::size_t>(workers, n_ / 4096 + 1);
+  // ranges of mirror rows with equal shares of the nonzeros
+  std::vector<std::size_t> cut(workers + 1, n_);
+  cut[0] = 0;
+  for (unsigned t = 1; t < workers; ++t) {
+    const std::int64_t want = row_ptr_[n_] / workers * t;
+    cut[t] = std::lower_bound(row_ptr_.begin(), row_ptr_.end(), want) - row_ptr_.begin();
+    cut[t] = std::min(std::max(cut[t], cut[t - 1]), n_);
+  }
+  auto body = [&](unsigned t) {
+    const std::size_t J0 = cut[t], J1 = cut[t + 1];
+    if (J0 >= J1) return;
+    std::vector<std::int64_t> cursor(row_ptr_.begin() + J0, row_ptr_.begin() + J1);
+    const std::int32_t lo = static_cast<std::int32_t>(J0), hi = static_cast<std::int32_t>(J1);
+    for (std::size_t i = 0; i + 1 < J1 && ok.load(std::memory_order_relaxed); ++i) {
+      const std::int32_t* first = col_idx_.data() + row_ptr_[i];
+      const std::int32_t* last = col_idx_.data() + row_ptr_[i + 1];
+      const std::int32_t from = std::max<std::int32_t>(lo, static_cast<std::int32_t>(i) + 1);
+      for (const std::int32_t* q = std::lower_bound(first, last, from); q < last && *q < hi; ++q) {
+        const std::size_t j = static_cast<std::size_t>(*q);
+        std::int64_t& c = cursor[j - J0];
+        const std::int64_t end = row_ptr_[j + 1];
+        while (c < end && col_idx_[c] < static_cast<std::int32_t>(i)) ++c;
+        if (c == end || col_idx_[c] != static_cast<std::int32_t>(i) ||
+            values_[q - col_idx_.data()] != values_[c]) {
           ok.store(false, std::memory_order_relaxed);
-          break;
+          return;
         }
       }
-  });
+    }
+  };
+  if (workers <= 1) {
+    body(0);
+  } else {
+    std::vector<std::thread> pool;
+    for (unsigned t = 0; t < workers; ++t) pool.emplace_back(body, t);
+    for (auto& th : pool) th.join();
+  }
   if (ok) return;
   for (std::size_t i = 0; i < n_; ++i)
     for (std::int64_t p = row_ptr_[i]; p < row_ptr_[i + 1]; ++p) {
@@ -304,9 +374,14 @@ flz_matrix* SparseSymMatrix::device() const {
     } else {
       rp += b;  // replicated global matrix: this rank's rows, absolute offsets
     }
-    throw_status(flz_matrix_upload(ctx, static_cast<std::int64_t>(n_),
-                                   static_cast<std::int64_t>(b), static_cast<std::int64_t>(e), rp,
-                                   col_idx_.data(), values_.data(), 0, &copy->handle));
+    std::shared_ptr<Planned> planned = std::move(planned_);   // single use
+    planned_.reset();
+    if (planned && planned->plan && !slab_ && flz_ctx_nranks(ctx) == 1)
+      throw_status(flz_matrix_upload_plan(ctx, planned->plan, &copy->handle));
+    else
+      throw_status(flz_matrix_upload(ctx, static_cast<std::int64_t>(n_),
+                                     static_cast<std::int64_t>(b), static_cast<std::int64_t>(e),
+                                     rp, col_idx_.data(), values_.data(), 0, &copy->handle));
     dev_ = std::move(copy);
   }
   return dev_->handle;

@@ -1525,6 +1525,26 @@ HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<in
   }
   const std::vector<int32_t>* sort_key = pair_key.empty() ? nullptr : &pair_key;
 
+  // The hybrid layout depends on the blocks only (natural row order): it is built on its own
+  // thread while this one sorts the rows and fills the CSR-order SELL arrays.  build_hybrid
+  // writes the hy_* members of P and nothing else.
+  std::thread hybrid_thread;
+  std::exception_ptr hybrid_error;
+  if (hybrid)
+    hybrid_thread = std::thread([&] {
+      try {
+        build_hybrid(P, blocks, row_ptr, col_idx, values);
+      } catch (...) {
+        hybrid_error = std::current_exception();
+      }
+    });
+  struct JoinGuard {   // an exception on this thread must not leave the worker running
+    std::thread& t;
+    ~JoinGuard() {
+      if (t.joinable()) t.join();
+    }
+  } hybrid_guard{hybrid_thread};
+
   // ---- sigma: smallest window whose padding overhead is <= 8 %
   int64_t chosen = sigma;
   if (P.split) {
@@ -1682,8 +1702,9 @@ HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<in
   // long ragged rows: the paired layout feeds the fast kernel (FLZ_P2=0 keeps the UG tasks)
   P.p2 = want_p2 && !P.split && !P.lean && nl > 0 && p2_candidate && !hybrid;
   if (hybrid) {
-    build_hybrid(P, blocks, row_ptr, col_idx, values);
-    timer.lap("hybrid layout");
+    hybrid_thread.join();
+    if (hybrid_error) std::rethrow_exception(hybrid_error);
+    timer.lap("hybrid layout (rest; built beside the SELL arrays)");
   }
   if (P.p2) {
     if (!blocks.any()) {

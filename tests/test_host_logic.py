@@ -297,3 +297,49 @@ def test_jackson_damping_is_an_opt_in_extension():
     assert plain.min() < -0.02 and plain.max() > 1.02          # Gibbs oscillations
     assert damped.min() > -1e-12 and damped.max() < 1.0 + 1e-12
     assert S.LanczosConfig().jackson_damping == 0
+
+
+@pytest.mark.parametrize("threads", ["1", "5"])
+def test_symmetry_check_reports_what_the_reference_reports(threads, best_oracle):
+    """The threaded cursor-per-row symmetry check (matrix.cpp) accepts and rejects the same
+    matrices as the reference's binary search per upper entry (sparse.cpp:65-83), with the
+    same message: the FIRST offending upper entry in row-major order.  Lower entries without
+    an upper partner are not looked up by either."""
+    import subprocess, sys, json
+    code = r'''
+import sys, json
+sys.path.insert(0, %r)
+import numpy as np, scipy.sparse as sp
+from paper_2409_15053_b200 import FlzError, matrices as M, solver as S
+n, rp, ci, va = M.laplacian2d(150)          # n = 22 500: several worker ranges
+A = sp.csr_matrix((va, ci, rp), shape=(n, n)).tolil()
+def attempt(edits):
+    B = A.copy()
+    for i, j, v in edits:
+        B[i, j] = v
+    B = B.tocsr(); B.eliminate_zeros(); B.sort_indices()
+    try:
+        S.SparseSymMatrix.from_csr(n, B.indptr.astype(np.int64), B.indices.astype(np.int32), B.data)
+        return "ok"
+    except FlzError as e:
+        return str(e)
+out = {
+  "clean": attempt([]),
+  "lower_only": attempt([(9000, 17, 2.5), (22499, 3, 1.0)]),        # extra LOWER entries: accepted
+  "missing_mirror": attempt([(20000, 20001, 0.0)]),                  # upper (20000,20001) has no... deleted upper: lower left alone
+  "structural": attempt([(20001, 20000, 0.0)]),                      # mirror of upper (20000, 20001) deleted
+  "numerical": attempt([(151, 1, -1.25)]),                           # mirror of upper (1, 151) differs
+  "two": attempt([(22000, 21999, 0.0), (4001, 4000, 7.0), (13000, 12999, 0.0)]),
+  "far_upper": attempt([(5, 22000, 3.0)]),                           # upper entry without a mirror
+}
+print(json.dumps(out))
+''' % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, FLZ_HOST_THREADS=threads)
+    p = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert p.returncode == 0, p.stderr[-2000:]
+    got = json.loads(p.stdout.strip().splitlines()[-1])
+    assert got["clean"] == "ok" and got["lower_only"] == "ok" and got["missing_mirror"] == "ok"
+    assert "structurally asymmetric at (20000,20001)" in got["structural"]
+    assert "numerically asymmetric at (1,151)" in got["numerical"]
+    assert "numerically asymmetric at (4000,4001)" in got["two"]
+    assert "structurally asymmetric at (5,22000)" in got["far_upper"]
