@@ -110,8 +110,8 @@ void ensure_exact_arrays(const flz_matrix* A) {
                              cudaMemcpyHostToDevice, ctx->stream));
     FLZ_CUDA(cudaStreamSynchronize(ctx->stream));
   }
-  std::vector<int32_t>().swap(A->h_col);
-  std::vector<double>().swap(A->h_val);
+  flz::BigVec<int32_t>().swap(A->h_col);
+  flz::BigVec<double>().swap(A->h_val);
 }
 
 SellView make_view(const flz_matrix* A, const SliceTask* tasks, int64_t ntasks,

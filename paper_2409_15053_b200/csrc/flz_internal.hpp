@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "flz.h"
+#include "host/plan.hpp"   // BigVec
 
 namespace flz {
 
@@ -200,8 +201,8 @@ struct flz_matrix {
   // from the host copies below
   mutable flz::DevBuf<int32_t> col; // [stored] permuted local col or nl + halo slot
   mutable flz::DevBuf<double> val;  // [stored]
-  mutable std::vector<int32_t> h_col;
-  mutable std::vector<double> h_val;
+  mutable flz::BigVec<int32_t> h_col;
+  mutable flz::BigVec<double> h_val;
   // index-compressed layout read by the fast kernels
   flz::DevBuf<flz::UgSlice> ug;     // [nslices]
   flz::DevBuf<double> ug_val;

@@ -117,12 +117,31 @@ void sort_windows(const std::vector<int32_t>& len, int64_t sigma, std::vector<in
   perm.resize(nl);
   std::iota(perm.begin(), perm.end(), 0);
   if (sigma <= 1) return;
+  // classes through a table (two logarithms per row otherwise); large windows by a stable
+  // counting sort over the few dozen classes, descending — the order std::stable_sort gives
+  const std::vector<int32_t>& k = key ? *key : len;
+  int32_t kmax = 0;
+  for (int64_t i = 0; i < nl; ++i) kmax = std::max(kmax, k[i]);
+  std::vector<int32_t> table((size_t)kmax + 1);
+  for (int32_t v = 0; v <= kmax; ++v) table[v] = length_class(v);
   std::vector<int32_t> cls(nl);
-  for (int64_t i = 0; i < nl; ++i) cls[i] = length_class(key ? (*key)[i] : len[i]);
+  for (int64_t i = 0; i < nl; ++i) cls[i] = table[std::max(k[i], 0)];
+  const int32_t ncls = table.empty() ? 1 : *std::max_element(table.begin(), table.end()) + 1;
+  std::vector<int64_t> start;
+  std::vector<int32_t> sorted;
   for (int64_t w0 = 0; w0 < nl; w0 += sigma) {
     const int64_t w1 = std::min(nl, w0 + sigma);
-    std::stable_sort(perm.begin() + w0, perm.begin() + w1,
-                     [&](int32_t a, int32_t b) { return cls[a] > cls[b]; });
+    if (w1 - w0 < 4096) {
+      std::stable_sort(perm.begin() + w0, perm.begin() + w1,
+                       [&](int32_t a, int32_t b) { return cls[a] > cls[b]; });
+      continue;
+    }
+    start.assign((size_t)ncls + 1, 0);
+    for (int64_t i = w0; i < w1; ++i) ++start[ncls - 1 - cls[perm[i]] + 1];   // descending class
+    for (int32_t c = 0; c < ncls; ++c) start[c + 1] += start[c];
+    sorted.resize(w1 - w0);
+    for (int64_t i = w0; i < w1; ++i) sorted[start[ncls - 1 - cls[perm[i]]]++] = perm[i];
+    std::copy(sorted.begin(), sorted.end(), perm.begin() + w0);
   }
 }
 
@@ -566,6 +585,18 @@ int64_t build_ug(HostPlan& P, const std::vector<uint8_t>& is_boundary, bool allo
   return (int64_t)rest_col.size();
 }
 
+struct PhaseTimer {  // FLZ_TRACE=1: phase timings of build_plan on stderr
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  bool on = std::getenv("FLZ_TRACE") != nullptr;
+  void lap(const char* what) {
+    if (!on) return;
+    const auto t1 = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[flz]   plan %-22s %9.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(t1 - t0).count());
+    t0 = t1;
+  }
+};
+
 // ---- dense blocks (plan.hpp) ---------------------------------------------------------------
 // Near-cliques among the LONG rows of the local diagonal block: rows much longer than the
 // median (the members of non-local projector balls on PARSEC-like Hamiltonians).  Greedy:
@@ -589,6 +620,7 @@ DenseBlocks extract_dense_blocks(int64_t nl, int64_t row_begin, const int64_t* r
                                  int64_t nnz) {
   DenseBlocks B;
   if (nl < 1024) return B;
+  PhaseTimer sub;
   std::vector<int32_t> tmp(len);
   std::nth_element(tmp.begin(), tmp.begin() + nl / 2, tmp.end());
   const int32_t long_min = std::max<int32_t>(48, tmp[nl / 2] + tmp[nl / 2] / 2);
@@ -605,13 +637,25 @@ DenseBlocks extract_dense_blocks(int64_t nl, int64_t row_begin, const int64_t* r
   const int64_t p0 = row_ptr[0];
   auto local = [&](int64_t e) { return (int64_t)col_idx[e] - row_begin; };
   std::vector<int32_t> uncov(nl, 0);
-  for (int32_t i : seeds)
-    for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
-      const int64_t c = local(e);
-      if (c >= 0 && c < nl && is_long[c]) ++uncov[i];
-    }
+  {
+    const int64_t ns = (int64_t)seeds.size();
+    const int chunks = (int)std::max<int64_t>(1, std::min<int64_t>(worker_count(), ns / 2048));
+    run_chunks(chunks, [&](int t) {
+      for (int64_t q = ns * t / chunks; q < ns * (t + 1) / chunks; ++q) {
+        const int32_t i = seeds[q];
+        int32_t u = 0;
+        for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
+          const int64_t c = local(e);
+          u += (c >= 0 && c < nl && is_long[c]) ? 1 : 0;
+        }
+        uncov[i] = u;
+      }
+    });
+  }
+  sub.lap("  blocks: long rows, uncov");
   std::stable_sort(seeds.begin(), seeds.end(), [&](int32_t a, int32_t b) { return len[a] < len[b]; });
   B.covered.assign((size_t)nnz, 0);
+  sub.lap("  blocks: seed sort");
   B.count.assign(nl, 0);
   std::vector<uint8_t> mark(nl, 0);
   std::vector<int32_t> K, keep;
@@ -627,29 +671,40 @@ DenseBlocks extract_dense_blocks(int64_t nl, int64_t row_begin, const int64_t* r
       has_seed = has_seed || c == seed;
     }
     if (!has_seed) K.push_back(seed);
-    for (int pass = 0; pass < 2 && (int)K.size() >= kDenseMin; ++pass) {
+    // (a pass that keeps every member leaves K as it was: a second pass would find the same
+    // counts, and the new entries of K x K counted during that pass are the final ones)
+    int64_t fresh_seen = -1;
+    for (int pass = 0; pass < 2 && (int)K.size() >= kDenseMin && fresh_seen < 0; ++pass) {
       for (int32_t c : K) mark[c] = 1;
       keep.clear();
+      int64_t fresh_pass = 0;
       for (int32_t j : K) {
         int32_t d = 0;
         for (int64_t e = row_ptr[j]; e < row_ptr[j + 1]; ++e) {
           const int64_t c = local(e);
-          d += (c >= 0 && c < nl && mark[c]) ? 1 : 0;
+          const bool in = c >= 0 && c < nl && mark[c];
+          d += in ? 1 : 0;
+          fresh_pass += (in && !B.covered[e - p0]) ? 1 : 0;
         }
         if (5 * (int64_t)d >= 4 * (int64_t)K.size()) keep.push_back(j);
       }
       for (int32_t c : K) mark[c] = 0;
+      if (keep.size() == K.size()) fresh_seen = fresh_pass;
       K.swap(keep);
     }
     bool ok = (int)K.size() >= kDenseMin;
     if (ok) {  // at least half of K x K must be new entries
       for (int32_t c : K) mark[c] = 1;
       int64_t fresh = 0;
-      for (int32_t j : K)
-        for (int64_t e = row_ptr[j]; e < row_ptr[j + 1]; ++e) {
-          const int64_t c = local(e);
-          fresh += (c >= 0 && c < nl && mark[c] && !B.covered[e - p0]) ? 1 : 0;
-        }
+      if (fresh_seen >= 0) {
+        fresh = fresh_seen;
+      } else {
+        for (int32_t j : K)
+          for (int64_t e = row_ptr[j]; e < row_ptr[j + 1]; ++e) {
+            const int64_t c = local(e);
+            fresh += (c >= 0 && c < nl && mark[c] && !B.covered[e - p0]) ? 1 : 0;
+          }
+      }
       // (a quarter is enough: a ball that overlaps an earlier block is still worth a block —
       // the hybrid layout drops the columns a task does not use, the paired layout stores zeros)
       ok = 4 * fresh >= (int64_t)K.size() * (int64_t)K.size();
@@ -674,6 +729,7 @@ DenseBlocks extract_dense_blocks(int64_t nl, int64_t row_begin, const int64_t* r
     for (int32_t j : K) ++B.count[j];
     B.members.push_back(K);
   }
+  sub.lap("  blocks: greedy search");
   if (10 * B.covered_entries < nnz) return DenseBlocks{};  // not worth a second row order
   B.primary.assign(nl, -1);
   for (size_t b = 0; b < B.members.size(); ++b)
@@ -692,6 +748,7 @@ void build_hybrid(HostPlan& P, const DenseBlocks& blocks, const int64_t* row_ptr
   const int64_t nl = P.nl;
   const int64_t p0 = row_ptr[0];
   const int32_t zero_row = (int32_t)nl;
+  PhaseTimer sub;
   auto local = [&](int64_t e) { return (int32_t)((int64_t)col_idx[e] - P.row_begin); };
   // membership lists (block, index inside the block), ascending block id
   std::vector<int32_t> mem_ptr(nl + 1, 0);
@@ -729,8 +786,14 @@ void build_hybrid(HostPlan& P, const DenseBlocks& blocks, const int64_t* row_ptr
   const int dchunks = (int)std::max<int64_t>(1, std::min<int64_t>(worker_count(), nt / 8));
   run_chunks(dchunks, [&](int w) {
     std::vector<uint8_t> used;
+    std::vector<int32_t> pos(nl, 0);   // member index of a row inside the current block
+    int32_t pos_block = -1;
     for (int64_t t = nt * w / dchunks; t < nt * (w + 1) / dchunks; ++t) {
       const auto& rows = blocks.members[spec[t].block];
+      if (pos_block != spec[t].block) {
+        for (size_t j = 0; j < rows.size(); ++j) pos[rows[j]] = (int32_t)j;
+        pos_block = spec[t].block;
+      }
       used.assign(rows.size(), 0);
       for (int32_t q = 0; q < spec[t].nrows; ++q) {
         const int32_t i = rows[spec[t].g0 + q];
@@ -738,13 +801,14 @@ void build_hybrid(HostPlan& P, const DenseBlocks& blocks, const int64_t* row_ptr
           if (!blocks.covered[e - p0]) continue;
           const int32_t c = local(e);
           if (c == i || owner(i, c) != spec[t].block) continue;
-          used[std::lower_bound(rows.begin(), rows.end(), c) - rows.begin()] = 1;
+          used[pos[c]] = 1;   // c is a member: owner() found the block among c's blocks
         }
       }
       for (size_t j = 0; j < rows.size(); ++j)
         if (used[j]) task_cols[t].push_back(rows[j]);
     }
   });
+  sub.lap("  hybrid: task columns");
   int64_t nslots = kPlanSliceRows, nvals = 0;
   int32_t maxcols = 1;
   for (int64_t t = 0; t < nt; ++t) {
@@ -772,29 +836,34 @@ void build_hybrid(HostPlan& P, const DenseBlocks& blocks, const int64_t* row_ptr
   P.hy_nslots = nslots;
   P.hy_maxcols = maxcols;
   P.hy_blocks = (int64_t)blocks.members.size();
-  P.hy_dval.assign((size_t)std::max<int64_t>(nvals, 1) * kPlanSliceRows, 0.0);
+  P.hy_dval.resize((size_t)std::max<int64_t>(nvals, 1) * kPlanSliceRows);   // zeroed per task below
+  if (nvals == 0) std::fill(P.hy_dval.begin(), P.hy_dval.end(), 0.0);
   const int64_t ntask = (int64_t)P.hy_dtasks.size();
   std::vector<int64_t> dense_part(dchunks, 0);
   run_chunks(dchunks, [&](int w) {
+    std::vector<int32_t> pos(nl, 0);   // index of a row among the current task's columns
     for (int64_t t = ntask * w / dchunks; t < ntask * (w + 1) / dchunks; ++t) {
       PlanHyTask& T = P.hy_dtasks[t];
       const TaskSpec& S = spec[T.pad[0]];
       const auto& rows = blocks.members[S.block];
       const int32_t* tc = P.hy_dcols.data() + T.col_off;
+      for (int32_t j = 0; j < T.ncols; ++j) pos[tc[j]] = j;
       double* v = P.hy_dval.data() + T.val_off * kPlanSliceRows;
+      std::fill(v, v + (int64_t)T.ncols * kPlanSliceRows, 0.0);
       for (int32_t q = 0; q < T.nrows; ++q) {
         const int32_t i = rows[S.g0 + q];
         for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
           if (!blocks.covered[e - p0]) continue;
           const int32_t c = local(e);
           if (c == i || owner(i, c) != S.block) continue;
-          const int64_t j = std::lower_bound(tc, tc + T.ncols, c) - tc;
+          const int64_t j = pos[c];   // c is one of the task's columns (pass 1 marked it)
           v[j * kPlanSliceRows + q] = values[e];
           ++dense_part[w];
         }
       }
     }
   });
+  sub.lap("  hybrid: dense values");
   for (auto& T : P.hy_dtasks) T.pad[0] = 0;
   P.hy_dense_entries = 0;
   for (int64_t x : dense_part) P.hy_dense_entries += x;
@@ -916,6 +985,7 @@ void build_hybrid(HostPlan& P, const DenseBlocks& blocks, const int64_t* row_ptr
       H.np = np;
     }
   });
+  sub.lap("  hybrid: slices");
   // concatenate the chunks
   int64_t ncols = 0, nuvv = 0, ngv = 0;
   for (auto& C : chunk) {
@@ -926,6 +996,7 @@ void build_hybrid(HostPlan& P, const DenseBlocks& blocks, const int64_t* row_ptr
   require(nuvv < ((int64_t)1 << 31) && ngv / kPlanSliceRows < ((int64_t)1 << 31),
           "plan: hybrid layout overflow");
   P.hy_cols.resize(std::max<int64_t>(ncols, 1));
+  if (ncols == 0) P.hy_cols[0] = 0;
   P.hy_uvval.resize(std::max<int64_t>(nuvv, 1));
   P.hy_gval.resize(std::max<int64_t>(ngv, 1));
   P.hy_uv_entries = P.hy_g_entries = 0;
@@ -946,6 +1017,7 @@ void build_hybrid(HostPlan& P, const DenseBlocks& blocks, const int64_t* row_ptr
     P.hy_uv_entries += C.uv_entries;
     P.hy_g_entries += C.g_entries;
   }
+  sub.lap("  hybrid: concatenate");
   P.hy = true;
 }
 
@@ -1098,18 +1170,6 @@ void build_p2(HostPlan& P, const std::vector<P2Spec>& specs, const std::vector<u
   P.p2_tasks_interior = build_tasks(P.p2_interior, cost);
   P.p2_tasks_boundary = build_tasks(P.p2_boundary, cost);
 }
-
-struct PhaseTimer {  // FLZ_TRACE=1: phase timings of build_plan on stderr
-  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
-  bool on = std::getenv("FLZ_TRACE") != nullptr;
-  void lap(const char* what) {
-    if (!on) return;
-    const auto t1 = std::chrono::steady_clock::now();
-    std::fprintf(stderr, "[flz]   plan %-22s %9.3f ms\n", what,
-                 std::chrono::duration<double, std::milli>(t1 - t0).count());
-    t0 = t1;
-  }
-};
 
 void require(bool ok, const char* msg) {
   if (!ok) throw std::invalid_argument(msg);
@@ -1380,13 +1440,20 @@ HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<in
     std::vector<int32_t> tmp(len);   // "short" = twice the 10th percentile of the row lengths
     std::nth_element(tmp.begin(), tmp.begin() + nl / 10, tmp.end());
     const int64_t limit = 2 * (int64_t)tmp[nl / 10] + 8;
-    int64_t excess = 0;
     const int64_t q0 = row_ptr[0];
-    for (int64_t i = 0; i < nl; ++i) {
-      int64_t left = 0;
-      for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) left += blocks.covered[e - q0] ? 0 : 1;
-      excess += std::max<int64_t>(0, left - limit);
-    }
+    const int echunks = (int)std::max<int64_t>(1, std::min<int64_t>(worker_count(), nl / 4096));
+    std::vector<int64_t> part(echunks, 0);
+    run_chunks(echunks, [&](int t) {
+      int64_t sum = 0;
+      for (int64_t i = nl * t / echunks; i < nl * (t + 1) / echunks; ++i) {
+        int64_t left = 0;
+        for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) left += blocks.covered[e - q0] ? 0 : 1;
+        sum += std::max<int64_t>(0, left - limit);
+      }
+      part[t] = sum;
+    });
+    int64_t excess = 0;
+    for (int64_t v : part) excess += v;
     hybrid = 20 * excess <= P.nnz;
   }
   if (blocks.any() && !hybrid && !p2_dense) blocks = DenseBlocks{};   // plain paired layout
@@ -1634,8 +1701,12 @@ HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<in
     P.slice_ptr[s + 1] = P.slice_ptr[s] + (int64_t)mx * kPlanSliceRows;
   }
   P.stored = P.slice_ptr[nslices];
-  P.col.assign(std::max<int64_t>(P.stored, 1), 0);
-  P.val.assign(std::max<int64_t>(P.stored, 1), 0.0);
+  P.col.resize(std::max<int64_t>(P.stored, 1));   // uninitialised: every stored entry is written
+  P.val.resize(std::max<int64_t>(P.stored, 1));   // by the fill below (real entries + padding)
+  if (P.stored == 0) {
+    P.col[0] = 0;
+    P.val[0] = 0.0;
+  }
   std::vector<uint8_t> is_boundary(nslices, 0);
   // entries the dense sections of the paired layout hold (rows that belong to one block only)
   std::vector<uint8_t> skip;

@@ -10,8 +10,34 @@
 
 #include <cstdint>
 #include <vector>
+#include <memory>
+#include <type_traits>
+#include <utility>
 
 namespace flz {
+
+// std::vector whose resize() leaves trivially-constructible elements uninitialised: the big
+// layout arrays (tens of MB) are then first touched by the threads that fill them instead of
+// being zero-filled by one thread first (a third of the layout time on an 8M-nonzero matrix).
+template <class T>
+struct DefaultInitAllocator : std::allocator<T> {
+  template <class U>
+  struct rebind {
+    using other = DefaultInitAllocator<U>;
+  };
+  using std::allocator<T>::allocator;
+  template <class U>
+  void construct(U* p) noexcept(std::is_nothrow_default_constructible<U>::value) {
+    ::new (static_cast<void*>(p)) U;
+  }
+  template <class U, class... Args>
+  void construct(U* p, Args&&... args) {
+    ::new (static_cast<void*>(p)) U(std::forward<Args>(args)...);
+  }
+};
+template <class T>
+using BigVec = std::vector<T, DefaultInitAllocator<T>>;
+
 
 constexpr int kPlanSliceRows = 32;
 constexpr int kPlanTaskWarps = 8;
@@ -113,8 +139,9 @@ struct HostPlan {
   int64_t nslices = 0, stored = 0;
   std::vector<int32_t> perm, iperm;      // new -> old, old -> new (local rows)
   std::vector<int64_t> slice_ptr;
-  std::vector<int32_t> slice_len, row_len, col;
-  std::vector<double> val;
+  std::vector<int32_t> slice_len, row_len;
+  BigVec<int32_t> col;
+  BigVec<double> val;
   std::vector<int32_t> interior, boundary;  // slice ids
   std::vector<PlanTask> tasks_all, tasks_interior, tasks_boundary;
   bool short_rows = false;
@@ -178,11 +205,11 @@ struct HostPlan {
   // through sell_rows (SELL lane -> row, -1 = none) instead of a permutation of the vectors.
   bool hy = false;
   std::vector<PlanHySlice> hy_slice;            // [nslices]
-  std::vector<int32_t> hy_cols;
+  BigVec<int32_t> hy_cols;
   std::vector<double> hy_uvval, hy_gval, hy_diag;
   std::vector<PlanHyTask> hy_dtasks;
   std::vector<int32_t> hy_dcols;
-  std::vector<double> hy_dval;
+  BigVec<double> hy_dval;
   int64_t hy_nslots = 0;                        // partial slots (multiple of 32, >= 32)
   int32_t hy_maxcols = 0;                       // widest dense block
   int64_t hy_blocks = 0, hy_dense_entries = 0, hy_uv_entries = 0, hy_g_entries = 0;
