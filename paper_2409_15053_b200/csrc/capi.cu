@@ -172,7 +172,8 @@ HyView hybrid_view(const flz_matrix* A) {
   if (A->hy_w.count == 0) A->hy_w.reserve_zero((size_t)planar_ld(A) * kMaxFuse + 8, A->ctx->stream);
   return HyView{A->nl,         A->nslices,    (int)A->hy_ndtasks, A->hy_maxcols, A->hy_slice.p,
                 A->hy_cols.p,  A->hy_uvval.p, A->hy_gval.p,       A->hy_diag.p,  A->hy_dtasks.p,
-                A->hy_dcols.p, A->hy_dval.p,  A->hy_p.p,          A->hy_ldp,     A->hy_w.p};
+                A->hy_dcols.p, A->hy_dval.p,  A->hy_p.p,          A->hy_ldp,     A->hy_w.p,
+                (int)(A->nl + A->nhalo)};
 }
 
 void ensure_workspaces(const flz_matrix* A) {
@@ -236,7 +237,16 @@ void sell_step(const flz_matrix* A, int R, int S, StepMode mode, double s1, doub
                          Y2, ldy, nullptr, 0, nullptr, 0);
   };
   if (A->hy && !ctx->exact) {   // hybrid layout: planar blocks, dense tasks + slices
-    launch_hybrid_step(ctx, hybrid_view(A), R, mode, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo);
+    if (ctx->nranks == 1 || A->peers.empty()) {
+      launch_hybrid_step(ctx, hybrid_view(A), R, mode, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo);
+    } else {
+      // row-partitioned: the dense blocks lie inside the local diagonal block, so their tasks
+      // run while the halo rows travel; the slices (the only readers of halo rows) follow
+      halo_begin(A, R, S, Y1);
+      launch_hybrid_step(ctx, hybrid_view(A), R, mode, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo, 1);
+      FLZ_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_halo_done, 0));
+      launch_hybrid_step(ctx, hybrid_view(A), R, mode, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo, 2);
+    }
     return;
   }
   if (ctx->nranks == 1 || A->peers.empty()) {
@@ -274,7 +284,7 @@ int row_stride(const flz_matrix* A, int R) {
   if (planar) return 0;
   if (R != 3) return R;
   if (force && force[0] == '4') return 4;  // experiments: padded rows for every matrix
-  return (A->nnz >= 16 * A->nl) ? 4 : 3;
+  return A->dense_rows ? 4 : 3;   // (nonzeros per row of the WHOLE matrix: all ranks agree)
 }
 
 // Hybrid layout: row nl of every plane of the gather source is the zero row (the target of
@@ -584,6 +594,7 @@ static void upload_plan(flz_ctx* ctx, HostPlan& P, flz_matrix* A) {
   A->nl = P.nl;
   A->ld = std::max<int64_t>(round_up(P.nl, kLdAlign), kLdAlign);
   A->nnz = P.nnz;
+  A->dense_rows = P.nnz >= 16 * P.nl;
   A->stored = P.stored;
   A->nslices = P.nslices;
   A->nhalo = (int64_t)P.halo.size();
@@ -750,6 +761,35 @@ int flz_matrix_upload(flz_ctx* ctx, int64_t n_global, int64_t row_begin, int64_t
     } catch (const std::invalid_argument& e) {
       throw ApiError(FLZ_EINVAL, std::string("matrix_upload: ") + e.what());
     }
+    bool dense_rows_global = plan.nnz >= 16 * plan.nl;
+    if (P > 1) {
+      // Halo rows travel in the block layout of the filter workspaces, so every rank must pick
+      // the same one: the hybrid layout (planar blocks) only if EVERY rank found its dense
+      // blocks, and the interleaved stride from the global nonzeros per row.
+      DevBuf<int64_t> d;
+      d.reserve(2 * (size_t)P + 2);
+      std::vector<int64_t> all(P);
+      auto gather = [&](int64_t mine) {
+        FLZ_CUDA(cudaMemcpyAsync(d.p + P, &mine, sizeof(int64_t), cudaMemcpyHostToDevice,
+                                 ctx->stream));
+        comm_allgather_i64(ctx, d.p + P, d.p, ctx->stream);
+        FLZ_CUDA(cudaMemcpyAsync(all.data(), d.p, P * sizeof(int64_t), cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+        FLZ_CUDA(cudaStreamSynchronize(ctx->stream));
+      };
+      gather(plan.hy ? 1 : 0);
+      const bool all_hybrid = std::all_of(all.begin(), all.end(), [](int64_t v) { return v != 0; });
+      gather(plan.nnz);
+      const int64_t nnz_all = std::accumulate(all.begin(), all.end(), (int64_t)0);
+      dense_rows_global = nnz_all >= 16 * n_global;
+      if (plan.hy && !all_hybrid) {
+        try {
+          plan = build_plan(n_global, ctx->rank, P, starts, row_ptr, col_idx, values, sigma, false);
+        } catch (const std::invalid_argument& e) {
+          throw ApiError(FLZ_EINVAL, std::string("matrix_upload: ") + e.what());
+        }
+      }
+    }
     if (P > 1) {
       // tell every owner which of its rows we gather: counts first, then the row lists
       DevBuf<int64_t> d_cnt, d_need, d_give;
@@ -804,6 +844,7 @@ int flz_matrix_upload(flz_ctx* ctx, int64_t n_global, int64_t row_begin, int64_t
     }
     auto A = std::make_unique<flz_matrix>();
     upload_plan(ctx, plan, A.get());
+    A->dense_rows = dense_rows_global;
     ctx->refs += 1;
     *out = A.release();
   });

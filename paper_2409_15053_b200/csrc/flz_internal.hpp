@@ -189,6 +189,7 @@ struct flz_matrix {
   int64_t nl = 0;         // local rows
   int64_t ld = 0;         // padded local rows (multiple of kLdAlign)
   int64_t nnz = 0;        // true local nonzeros
+  bool dense_rows = false; // >= 16 nonzeros per row over the whole matrix (interleaved stride 4)
   int64_t stored = 0;     // stored entries incl. padding
   int64_t nslices = 0;
   int64_t nhalo = 0;      // halo rows appended after the nl local rows of a gather source
@@ -376,6 +377,7 @@ struct HyView {
   double* P;                 // partial slots, planar [k][ldp]
   int64_t ldp;
   double* W;                 // overlapped variant: the slices' sums before the finish launch
+  int zero_row;              // row of the gather source that is always zero (nl + halo rows)
 };
 
 enum class StepMode { step, final, plain, rest };
@@ -395,9 +397,11 @@ void launch_clenshaw_step(flz_ctx* ctx, const SellView& A, int R, int S, StepMod
 // true: the overlapped variant runs (hybrid_gather + hybrid_finish), else hybrid_dense_tasks +
 // hybrid_slices
 bool hybrid_overlaps(const flz_ctx* ctx, int64_t nslices, int64_t ndtasks);
+// phase 0: the whole step; 1: the dense tasks only (they gather LOCAL rows: a partitioned run
+// launches them while the halo rows travel); 2: the slices only
 void launch_hybrid_step(flz_ctx* ctx, const HyView& A, int R, StepMode mode, double s1, double s2,
                         double b, const double* Y1, double* Y2, int64_t ldy, const double* X,
-                        int64_t ldx, double* Out, int64_t ldo);
+                        int64_t ldx, double* Out, int64_t ldo, int phase = 0);
 // Y1 = scale * X  (column-major -> interleaved with row stride S >= R, or planar for S == 0)
 void launch_interleave(flz_ctx* ctx, int64_t nl, int R, int S, double scale, const double* X,
                        int64_t ldx, double* Y1, int64_t ldy);

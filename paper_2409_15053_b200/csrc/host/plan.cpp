@@ -747,9 +747,14 @@ void build_hybrid(HostPlan& P, const DenseBlocks& blocks, const int64_t* row_ptr
                   const int32_t* col_idx, const double* values) {
   const int64_t nl = P.nl;
   const int64_t p0 = row_ptr[0];
-  const int32_t zero_row = (int32_t)nl;
+  // gather-source index: local rows first, then the halo slots, then the zero row
+  const int32_t zero_row = (int32_t)(nl + (int64_t)P.halo.size());
   PhaseTimer sub;
-  auto local = [&](int64_t e) { return (int32_t)((int64_t)col_idx[e] - P.row_begin); };
+  auto local = [&](int64_t e) {
+    const int64_t g = col_idx[e];
+    if (g >= P.row_begin && g < P.row_end) return (int32_t)(g - P.row_begin);
+    return (int32_t)(nl + (std::lower_bound(P.halo.begin(), P.halo.end(), g) - P.halo.begin()));
+  };
   // membership lists (block, index inside the block), ascending block id
   std::vector<int32_t> mem_ptr(nl + 1, 0);
   for (const auto& K : blocks.members)
@@ -1319,7 +1324,7 @@ static void build_stencil_tiles(HostPlan& P) {
 
 HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<int64_t>& starts,
                     const int64_t* row_ptr, const int32_t* col_idx, const double* values,
-                    int sigma) {
+                    int sigma, bool allow_hybrid) {
   require(nranks >= 1 && rank >= 0 && rank < nranks, "plan: bad rank/nranks");
   require((int)starts.size() == nranks + 1 && starts.front() == 0 && starts.back() == n_global,
           "plan: rank row ranges must cover [0, n)");
@@ -1395,11 +1400,11 @@ HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<in
     const char* e = std::getenv("FLZ_P2_DENSE");
     return e && e[0] == '1';
   }();
-  const bool hy_wanted = [] {
+  const bool hy_wanted = allow_hybrid && [] {
     const char* e = std::getenv("FLZ_HY");
     return !(e && e[0] == '0');
   }();
-  const bool want_dense = p2_dense || (hy_wanted && nranks == 1);
+  const bool want_dense = p2_dense || hy_wanted;
   int32_t longest = 0;
   for (int64_t i = 0; i < nl; ++i) longest = std::max(longest, len[i]);
   const bool p2_candidate = want_p2_sort && !P.split && longest > 24 && nl > 0;
@@ -1427,7 +1432,7 @@ HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<in
   timer.lap("dense blocks");
   // HYBRID layout (plan.hpp): natural row order, dense tasks + value-grouped slices.  One rank
   // only (the slices gather local rows); FLZ_HY=0 keeps the paired layout (experiments).
-  bool hybrid = hy_wanted && blocks.any() && nranks == 1;
+  bool hybrid = hy_wanted && blocks.any();
   if (hybrid) {
     size_t widest = 0;
     for (const auto& K : blocks.members) widest = std::max(widest, K.size());
@@ -1592,6 +1597,29 @@ HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<in
   }
   const std::vector<int32_t>* sort_key = pair_key.empty() ? nullptr : &pair_key;
 
+  // ---- halo columns: sorted unique remote global ids, grouped by owner
+  if (nranks > 1) {
+    for (int64_t p = 0; p < P.nnz; ++p) {
+      const int64_t g = col_idx[p0 + p];
+      if (g < P.row_begin || g >= P.row_end) P.halo.push_back(g);
+    }
+    std::sort(P.halo.begin(), P.halo.end());
+    P.halo.erase(std::unique(P.halo.begin(), P.halo.end()), P.halo.end());
+  }
+  require(nl + (int64_t)P.halo.size() < ((int64_t)1 << 31), "plan: index overflow");
+  P.need_off.assign(nranks, 0);
+  P.need_cnt.assign(nranks, 0);
+  {
+    size_t h = 0;
+    for (int p = 0; p < nranks; ++p) {
+      P.need_off[p] = (int64_t)h;
+      while (h < P.halo.size() && P.halo[h] < starts[p + 1]) ++h;
+      P.need_cnt[p] = (int64_t)h - P.need_off[p];
+    }
+  }
+  P.give_off.assign(nranks, 0);
+  P.give_cnt.assign(nranks, 0);
+
   // The hybrid layout depends on the blocks only (natural row order): it is built on its own
   // thread while this one sorts the rows and fills the CSR-order SELL arrays.  build_hybrid
   // writes the hy_* members of P and nothing else.
@@ -1655,29 +1683,6 @@ HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<in
   for (int64_t i = 0; i < nl; ++i) P.iperm[P.perm[i]] = (int32_t)i;
 
   timer.lap("sigma / perm");
-  // ---- halo columns: sorted unique remote global ids, grouped by owner
-  if (nranks > 1) {
-    for (int64_t p = 0; p < P.nnz; ++p) {
-      const int64_t g = col_idx[p0 + p];
-      if (g < P.row_begin || g >= P.row_end) P.halo.push_back(g);
-    }
-    std::sort(P.halo.begin(), P.halo.end());
-    P.halo.erase(std::unique(P.halo.begin(), P.halo.end()), P.halo.end());
-  }
-  require(nl + (int64_t)P.halo.size() < ((int64_t)1 << 31), "plan: index overflow");
-  P.need_off.assign(nranks, 0);
-  P.need_cnt.assign(nranks, 0);
-  {
-    size_t h = 0;
-    for (int p = 0; p < nranks; ++p) {
-      P.need_off[p] = (int64_t)h;
-      while (h < P.halo.size() && P.halo[h] < starts[p + 1]) ++h;
-      P.need_cnt[p] = (int64_t)h - P.need_off[p];
-    }
-  }
-  P.give_off.assign(nranks, 0);
-  P.give_cnt.assign(nranks, 0);
-
   timer.lap("halo");
   // ---- SELL-32 storage
   const int64_t nslices = P.nslices = (nl + kPlanSliceRows - 1) / kPlanSliceRows;

@@ -225,9 +225,11 @@ struct HostPlan {
 // row_ptr holds absolute offsets into col_idx/values for local rows [row_begin,row_end);
 // col_idx are GLOBAL column ids.  sigma <= 0 selects the sorting window automatically.
 // Throws std::invalid_argument on malformed input.
+// allow_hybrid = false: no hybrid layout (a row-partitioned upload rebuilds with it when not
+// every rank found dense blocks: all ranks must exchange halo rows in the same block layout).
 HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<int64_t>& starts,
                     const int64_t* row_ptr, const int32_t* col_idx, const double* values,
-                    int sigma);
+                    int sigma, bool allow_hybrid = true);
 
 // Peer `p` asks for `count` of our rows (global ids); call once per peer, any order.
 void plan_set_give(HostPlan& plan, int peer, int64_t count, const int64_t* global_rows);

@@ -1251,7 +1251,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, CTAS)
   const int4 h0 = __ldg(hp), h1 = __ldg(hp + 1);
   const int64_t col_off = ((int64_t)(uint32_t)h0.y << 32) | (uint32_t)h0.x;
   const int uv_off = h0.z, g_off = h0.w, nuv = h1.x, ng = h1.y, np = h1.z;
-  const int zero_row = (int)A.nl;
+  const int zero_row = A.zero_row;
   const int64_t row = slice * kSliceRows + lane;
   const int* __restrict__ col = A.cols + col_off * 32 + lane * 4;
   const double2* __restrict__ uv = reinterpret_cast<const double2*>(A.uvval + uv_off);
@@ -1429,7 +1429,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, CTAS)
   const int4 h0 = __ldg(hp), h1 = __ldg(hp + 1);
   const int64_t col_off = ((int64_t)(uint32_t)h0.y << 32) | (uint32_t)h0.x;
   const int uv_off = h0.z, g_off = h0.w, nuv = h1.x, ng = h1.y;
-  const int zero_row = (int)A.nl;
+  const int zero_row = A.zero_row;
   const int64_t row = slice * kSliceRows + lane;
   const int* __restrict__ col = A.cols + col_off * 32 + lane * 4;
   const double2* __restrict__ uv = reinterpret_cast<const double2*>(A.uvval + uv_off);
@@ -1550,11 +1550,11 @@ __global__ void __launch_bounds__(256)
 template <int R>
 void launch_hybrid_r(flz_ctx* ctx, const HyView& A, StepMode mode, double s1, double s2, double b,
                      const double* Y1, double* Y2, int64_t ldy, const double* X, int64_t ldx,
-                     double* Out, int64_t ldo) {
+                     double* Out, int64_t ldo, int phase) {
   if (A.nslices == 0) return;
   const size_t smem = (size_t)A.maxcols * 32 + (size_t)(kHyDenseWarps - 1) * R * 32 * 8;
   const unsigned grid = (unsigned)((A.nslices + kWarpsPerBlock - 1) / kWarpsPerBlock);
-  if (hybrid_overlaps(ctx, A.nslices, A.ndtasks)) {
+  if (phase == 0 && hybrid_overlaps(ctx, A.nslices, A.ndtasks)) {
     const unsigned total = grid + (unsigned)A.ndtasks;
     launch_k1_smem(ctx, hybrid_gather<R, 6>, total, kWarpsPerBlock * 32, smem, A, Y1, ldy);
     const unsigned fgrid = (unsigned)((A.nslices + 7) / 8);
@@ -1574,10 +1574,11 @@ void launch_hybrid_r(flz_ctx* ctx, const HyView& A, StepMode mode, double s1, do
     ctx->launches += 2;
     return;
   }
-  if (A.ndtasks > 0) {
+  if (A.ndtasks > 0 && phase != 2) {
     launch_k1_smem(ctx, hybrid_dense_tasks<R>, (unsigned)A.ndtasks, kHyDenseWarps * 32, smem, A, Y1, ldy);
     ctx->launches++;
   }
+  if (phase == 1) return;
   // Registers against waves: 6 CTAs per SM (80 registers, no spills) when that needs no more
   // waves of CTAs than 8 per SM would (measured on B200: n = 113k, one wave either way, 24.2 ->
   // 21.4 us per step; n = 268k, 2 waves against 3, 40.2 against 42.9 us)
@@ -1778,7 +1779,7 @@ void launch_clenshaw_step(flz_ctx* ctx, const SellView& A, int R, int S, StepMod
 // FLZ_HY_OVERLAP=0|1 forces a variant.
 bool hybrid_overlaps(const flz_ctx* ctx, int64_t nslices, int64_t ndtasks) {
   static const int forced = env_int("FLZ_HY_OVERLAP", FLZ_HY_OVERLAP_DEFAULT);
-  if (ndtasks <= 0) return false;
+  if (ndtasks <= 0 || ctx->nranks > 1) return false;   // partitioned: the dense launch hides the halo exchange
   if (forced >= 0) return forced != 0;
   const int64_t ctas = (nslices + kWarpsPerBlock - 1) / kWarpsPerBlock + ndtasks;
   return ctas >= 3 * (int64_t)ctx->sm_count * 6;
@@ -1786,12 +1787,12 @@ bool hybrid_overlaps(const flz_ctx* ctx, int64_t nslices, int64_t ndtasks) {
 
 void launch_hybrid_step(flz_ctx* ctx, const HyView& A, int R, StepMode mode, double s1, double s2,
                         double b, const double* Y1, double* Y2, int64_t ldy, const double* X,
-                        int64_t ldx, double* Out, int64_t ldo) {
+                        int64_t ldx, double* Out, int64_t ldo, int phase) {
   switch (R) {
-    case 1: launch_hybrid_r<1>(ctx, A, mode, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo); break;
-    case 2: launch_hybrid_r<2>(ctx, A, mode, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo); break;
-    case 3: launch_hybrid_r<3>(ctx, A, mode, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo); break;
-    case 4: launch_hybrid_r<4>(ctx, A, mode, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo); break;
+    case 1: launch_hybrid_r<1>(ctx, A, mode, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo, phase); break;
+    case 2: launch_hybrid_r<2>(ctx, A, mode, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo, phase); break;
+    case 3: launch_hybrid_r<3>(ctx, A, mode, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo, phase); break;
+    case 4: launch_hybrid_r<4>(ctx, A, mode, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo, phase); break;
     default: throw ApiError(FLZ_EINVAL, "hybrid step: unsupported column count");
   }
   FLZ_CUDA(cudaGetLastError());

@@ -208,14 +208,17 @@ class HaloPlan:
                     blocks=int(sizes[9]), dense_entries=int(sizes[10]),
                     uv_entries=int(sizes[11]), sell_rows=sell_rows)
 
-    def hy_product(self, x):
+    def hy_product(self, x, x_halo=None):
         """y = A x evaluated from the hybrid layout as hybrid_dense_tasks / hybrid_slices walk
         it: the dense tasks leave partial sums in slots, a slice adds its uniform-value
         positions ([position / 4][lane][4] columns), its general positions, the partial slots
-        of its rows and the diagonal.  Row nl of the gather source is the zero row."""
+        of its rows and the diagonal.  The gather source is [local rows | halo rows | zero row];
+        x_halo: the values of the halo rows (order of need()), for row-partitioned plans."""
         hy = self.hy_arrays()
         nl = self.info["rows_local"]
-        xz = np.concatenate([np.asarray(x, np.float64), [0.0]])
+        halo = np.zeros(0) if x_halo is None else np.asarray(x_halo, np.float64)
+        assert len(halo) == self.info["halo_rows"]
+        xz = np.concatenate([np.asarray(x, np.float64), halo, [0.0]])
         P = np.zeros(hy["nslots"])
         for val_off, col_off, ncols, slot_base, nrows in hy["tasks"]:
             v = hy["dval"][val_off * 32:(val_off + ncols) * 32].reshape(ncols, 32)

@@ -136,3 +136,50 @@ def test_partitioned_lanczos_steps_match_single_context(name):
     assert np.abs(Q.T @ Q - np.eye(Q.shape[1])).max() <= 1e-12
     assert np.abs(np.abs(np.sum(Q * Q0, axis=0)) - 1.0).max() <= 1e-9     # same basis vectors
     assert max(parts[0][2], parts[1][2]) <= 1e-12
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_partitioned_hybrid_layout_matches_single_context(nranks):
+    """Stencil + dense-block matrices keep the hybrid layout on row slabs: dense tasks of the
+    local diagonal block run while the halo rows travel, the slices read the halo slots behind
+    the local rows.  Filter and product agree with the single-context result (exact mode bit
+    for bit; fast mode to rounding — the blocks of a slab differ from the global ones)."""
+    csr = M.parsec_like(radius=17.0, n_atoms=40)
+    n, rp, ci, va = csr
+    r = 3
+    X = np.random.default_rng(7).standard_normal((n, r))
+    cf = S.indicator_coefficients(-0.4, 0.1, 24)
+    c, e = 3.0, 3.5
+    ctx0 = Context()
+    A0 = DeviceMatrix(ctx0, n, rp, ci, va)
+    assert "hybrid" in A0.k1_info(r)["kernel"]
+    ctx0.set_exact(True)
+    want_exact = A0.filter_apply(cf, c, e, X)
+    ctx0.set_exact(False)
+    want_fast = A0.filter_apply(cf, c, e, X)
+    want_spmm = A0.spmm(X, counted=False)
+    starts = [n * k // nranks for k in range(nranks + 1)]
+
+    def body(rank, ctx):
+        b, e_ = starts[rank], starts[rank + 1]
+        lrp, lci, lva = slab(csr, b, e_)
+        A = DeviceMatrix(ctx, n, lrp, lci, lva, row_begin=b, row_end=e_)
+        kernel = A.k1_info(r)["kernel"]
+        ctx.set_exact(True)
+        ye = A.filter_apply(cf, c, e, X[b:e_])
+        ctx.set_exact(False)
+        yf = A.filter_apply(cf, c, e, X[b:e_])
+        zf = A.spmm(X[b:e_], counted=False)
+        return ye, yf, zf, kernel, A.stats()
+
+    parts = run_ranks(nranks, body)
+    # all ranks or none: the halo rows travel in the block layout of the filter workspaces, so
+    # a rank whose slab has dense blocks gives the hybrid layout up when another rank's has not
+    # (3 ranks here: only the last slab has them)
+    kinds = ["hybrid" in p[3] for p in parts]
+    assert all(kinds) if nranks == 2 else not any(kinds), [p[3] for p in parts]
+    assert sum(p[4]["halo_rows"] for p in parts) > 0
+    assert np.array_equal(np.vstack([p[0] for p in parts]), want_exact)
+    scale = np.abs(want_fast).max()
+    assert np.abs(np.vstack([p[1] for p in parts]) - want_fast).max() <= 1e-13 * scale
+    assert np.abs(np.vstack([p[2] for p in parts]) - want_spmm).max() <= 1e-13 * np.abs(want_spmm).max()

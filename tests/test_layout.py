@@ -283,12 +283,32 @@ def test_hybrid_layout_exact_mode_arrays_follow_sell_rows():
     assert P.info["stored"] <= 1.2 * len(va)
 
 
-def test_hybrid_layout_is_single_rank_only():
-    csr = M.parsec_like(radius=12.0, n_atoms=12)
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_hybrid_layout_on_row_slabs(nranks):
+    """Row-partitioned plans take the hybrid layout too: the dense blocks are searched inside
+    the local diagonal block, halo columns stay in the slices and point at the halo slots
+    behind the local rows, the zero row moves behind the halo.  Every rank's product, evaluated
+    from the arrays as the kernels walk them, is its slab of A x."""
+    csr = M.parsec_like(radius=17.0, n_atoms=40)
     n, rp, ci, va = csr
-    starts = [0, n // 2, n]
-    P = HaloPlan(n, 0, 2, starts, rp[: n // 2 + 1], ci[: rp[n // 2]], va[: rp[n // 2]])
-    assert P.hy_arrays() is None
+    x = np.random.default_rng(3).standard_normal(n)
+    want = reference(csr, x)
+    starts = [n * k // nranks for k in range(nranks + 1)]
+    hybrids = 0
+    for rank in range(nranks):
+        b, e = starts[rank], starts[rank + 1]
+        P = HaloPlan(n, rank, nranks, starts, rp[b:e + 1], ci, va)
+        hy = P.hy_arrays()
+        if hy is None:
+            continue
+        hybrids += 1
+        need = np.concatenate([P.need(p) for p in range(nranks)]).astype(np.int64)
+        assert len(need) == P.info["halo_rows"] > 0
+        y = P.hy_product(x[b:e], x[need])
+        assert np.abs(y - want[b:e]).max() <= 1e-12 * np.abs(want).max()
+        # dense tasks gather local rows only: they can run while the halo rows travel
+        assert hy["dcols"].max() < e - b
+    assert hybrids >= 1
 
 
 def test_matrices_without_dense_blocks_keep_the_plain_paired_layout():
