@@ -608,6 +608,7 @@ void launch_gemm_tn(flz_ctx* ctx, const double* A, int64_t lda, int64_t M, const
   const int64_t mtiles = (M + 7) / 8;
   const int nblocks = (N + 8 * NT - 1) / (8 * NT);
   // ~4 CTAs (32 warps) per SM over the whole grid, chunks of at least 2048 rows
+  // (3 to 16 work items per SM measured the same on B200 for 40k x 1740, 110k x 630, 1M x 210)
   const int64_t want_ctas = (int64_t)ctx->sm_count * 6;
   int64_t nchunks = (want_ctas + mtiles * nblocks - 1) / (mtiles * nblocks);
   const int64_t max_chunks = (rows8 + 2047) / 2048;
@@ -648,11 +649,18 @@ void launch_gemm_nn(flz_ctx* ctx, const double* A, int64_t lda, int64_t K, const
   FLZ_REQUIRE(round_up(rows, 2) <= lda && round_up(rows, 2) <= ldo, FLZ_EDIM,
               "gemm_nn: leading dimension too small");
   if (accumulate && N <= 8 && K > 0 && ldbs >= 8 && ts_update_enabled()) {
-    // tall-skinny update: as many column sets per CTA as it takes to have ~4 waves of CTAs
-    // (4 resident CTAs per SM)
-    const int64_t want = (int64_t)ctx->sm_count * 16;
+    // tall-skinny update: as many column sets per CTA as it takes to have ~2 waves of CTAs
+    // (4 resident CTAs per SM).  Measured on B200 (orthogonalization time of a whole
+    // factorization, row groups per CTA 8 / 4 / 2 / 1): 110k rows 56.8 / 53.6 / 57.2 / 62.9 ms,
+    // 40k rows 434 / 438 / 421 / 420 ms, 1M rows 52.9 / 58.3 ms, 262k rows 85.6 / 85.6 ms.
+    const int64_t want = (int64_t)ctx->sm_count * 8;
     int rw = 8;
     while (rw > 1 && (rows + 16 * rw - 1) / (16 * rw) < want) rw >>= 1;
+    static const int forced_rw = [] {   // experiments: FLZ_TSU_RW = 8 | 4 | 2 | 1 row groups per CTA
+      const char* e = std::getenv("FLZ_TSU_RW");
+      return e && *e ? std::atoi(e) : 0;
+    }();
+    if (forced_rw == 8 || forced_rw == 4 || forced_rw == 2 || forced_rw == 1) rw = forced_rw;
     const unsigned grid = (unsigned)((rows + 16 * rw - 1) / (16 * rw));
 #define FLZ_TSU(KWV)                                                                          \
   ts_update_kernel<KWV><<<grid, 256, 0, ctx->stream>>>(A, lda, K, Bs, ldbs, N, rows, alpha, Out, ldo)
