@@ -17,7 +17,8 @@ def run(code, env_extra, args=()):
     env = dict(os.environ)
     for k in ("FLZ_SPLIT", "FLZ_K1_LAYOUT", "FLZ_SYNC_CHECK", "FLZ_K1_TMA", "FLZ_K1_PDL",
               "FLZ_P2_CLUSTER", "FLZ_ST_TILE", "FLZ_ST_STAGES", "FLZ_ST_CTAS",
-              "FLZ_ST_PRODUCERS", "FLZ_HY", "FLZ_HY_OVERLAP"):
+              "FLZ_ST_PRODUCERS", "FLZ_HY", "FLZ_HY_OVERLAP", "FLZ_SPECULATE", "FLZ_ORTH_FUSED",
+              "FLZ_TS_UPDATE", "FLZ_PLAN_AHEAD"):
         env.pop(k, None)
     env.update(env_extra)
     p = subprocess.run([sys.executable, "-c", code, *args], env=env, capture_output=True,
@@ -163,3 +164,62 @@ def test_hybrid_overlapped_variant_bit_identical():
     assert all("hybrid_gather" not in v for k, v in two.items() if k.endswith("_kernel"))
     strip = lambda d: {k: v for k, v in d.items() if not k.endswith("_kernel")}
     assert strip(one) == strip(two)
+
+
+def test_speculative_application_changes_nothing():
+    """The operator application queued ahead of the host's wait (flz_lanczos_step) is the
+    application the next step would have run: eigenpairs, block counts, matvec counts and check
+    counts are bit-identical with FLZ_SPECULATE=0, with the pipelined and the sequential
+    checks (rollbacks drop a queued application), and with the layout planned at the first
+    product instead of inside from_csr."""
+    base = run(SOLVE_CODE, {"FLZ_SPECULATE": "0"})
+    assert run(SOLVE_CODE, {}) == base
+    assert run(SOLVE_CODE, {"FLZ_SYNC_CHECK": "1", "FLZ_SPECULATE": "0"}) == base
+    assert run(SOLVE_CODE, {"FLZ_PLAN_AHEAD": "0"}) == base
+    assert all(v["conv"] == 1 for v in base.values())
+
+
+ORTH_CODE = r'''
+import sys, json
+sys.path.insert(0, %r)
+import numpy as np
+from paper_2409_15053_b200 import Context, DeviceMatrix, matrices as M, solver as S
+from paper_2409_15053_b200.device import Basis
+ctx = Context(0)
+out = {}
+for name, gen in (("lap3d20", lambda: M.laplacian3d(20)), ("parsec7k", lambda: M.parsec_like(radius=12.0, n_atoms=12))):
+    n, rp, ci, va = gen()
+    A = DeviceMatrix(ctx, n, rp, ci, va)
+    cf = S.indicator_coefficients(-0.4, 0.1, 12)
+    for r in (1, 2, 3, 4, 5, 8):
+        start = S.init_block(n, r, 20177)
+        B = Basis(ctx, A, start, 10 * r)
+        res = [B.step(cf, 3.0, 3.5) for _ in range(8)]
+        out["%%s_r%%d" %% (name, r)] = dict(
+            D=[x[0].tolist() for x in res], S=[x[1].tolist() for x in res],
+            scale=[x[2] for x in res], dead=[x[3].tolist() for x in res],
+            ortho=B.ortho_error(), Q=B.get(0, 9 * r).tolist() if r <= 2 and n < 9000 else None)
+        B.close()
+print(json.dumps(out))
+''' % ROOT
+
+
+def test_fused_orthogonalization_agrees_with_the_multi_launch_path():
+    """One rank: [Q Z]^T Z in one sweep, the tall-skinny update kernel and the cooperative block
+    QR (r <= 4: block_qr_kernel<4>, r = 5, 8: <16>) against the multi-launch path of the
+    row-partitioned runs — same D_k, S_k, op_scale and dead flags to rounding, basis
+    orthonormal to 1e-13 either way."""
+    fused = run(ORTH_CODE, {})
+    plain = run(ORTH_CODE, {"FLZ_ORTH_FUSED": "0"})
+    old_update = run(ORTH_CODE, {"FLZ_TS_UPDATE": "0"})
+    for other in (plain, old_update):
+        for key, a in fused.items():
+            b = other[key]
+            assert a["ortho"] <= 1e-13 and b["ortho"] <= 1e-13, key
+            assert a["dead"] == b["dead"], key
+            for k in range(len(a["D"])):
+                Da, Db = np.array(a["D"][k]), np.array(b["D"][k])
+                Sa, Sb = np.array(a["S"][k]), np.array(b["S"][k])
+                tol = 1e-10 * max(1.0, np.abs(Da).max(), np.abs(Sa).max())
+                assert np.abs(Da - Db).max() <= tol and np.abs(Sa - Sb).max() <= tol, (key, k)
+                assert abs(a["scale"][k] - b["scale"][k]) <= 1e-12 * a["scale"][k]
