@@ -15,8 +15,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def run(code, env_extra, args=()):
     env = dict(os.environ)
-    for k in ("FLZ_SPLIT", "FLZ_K1_LAYOUT", "FLZ_SYNC_CHECK", "FLZ_K1_TMA", "FLZ_K1_PDL",
-              "FLZ_P2_CLUSTER", "FLZ_ST_TILE", "FLZ_ST_STAGES", "FLZ_ST_CTAS",
+    for k in ("FLZ_SPLIT", "FLZ_K1_LAYOUT", "FLZ_SYNC_CHECK", "FLZ_K1_PDL", "FLZ_P2_DENSE",
+              "FLZ_ST_TILE", "FLZ_ST_STAGES", "FLZ_ST_CTAS",
               "FLZ_ST_PRODUCERS", "FLZ_HY", "FLZ_HY_OVERLAP", "FLZ_SPECULATE", "FLZ_ORTH_FUSED",
               "FLZ_TS_UPDATE", "FLZ_PLAN_AHEAD"):
         env.pop(k, None)
@@ -29,9 +29,9 @@ def run(code, env_extra, args=()):
 
 @pytest.mark.parametrize("env", [{"FLZ_SPLIT": "1"}, {"FLZ_SPLIT": "0"}, {"FLZ_K1_LAYOUT": "planar"},
                                  {"FLZ_SPLIT": "1", "FLZ_K1_LAYOUT": "planar"},
-                                 {"FLZ_K1_TMA": "1"},          # paired layout, TMA-staged matrix stream
                                  {"FLZ_K1_PDL": "0"},          # plain stream-ordered launches
-                                 {"FLZ_P2_CLUSTER": "1"},      # dense-block row clustering
+                                 {"FLZ_P2_DENSE": "1", "FLZ_HY": "0"},   # paired layout with dense sections
+                                 {"FLZ_HY": "0"},              # plain paired layout for block matrices
                                  {"FLZ_ST_TILE": "0"},         # stencils: one-warp-per-slice kernel
                                  {"FLZ_HY_OVERLAP": "1"},      # hybrid layout: gather + finish launches
                                  {"FLZ_HY_OVERLAP": "0"},
