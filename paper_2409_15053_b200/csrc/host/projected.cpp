@@ -14,6 +14,7 @@
 #include "flz/projected.hpp"
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 #include <limits>
@@ -155,6 +156,29 @@ void reduce_band(const SymBandMatrix& M, std::vector<double>& d, std::vector<dou
 }
 
 // Householder tridiagonalization of the dense embedding (wide bands).
+// Team of host threads stepping through the reflectors of reduce_householder together: a
+// sense-reversing spin barrier (the per-reflector work is a few microseconds, far below what a
+// condition variable costs).
+class SpinBarrier {
+ public:
+  explicit SpinBarrier(unsigned count) : count_(count) {}
+  void wait() {
+    const unsigned gen = generation_.load(std::memory_order_acquire);
+    if (arrived_.fetch_add(1, std::memory_order_acq_rel) + 1 == count_) {
+      arrived_.store(0, std::memory_order_relaxed);
+      generation_.store(gen + 1, std::memory_order_release);
+    } else {
+      unsigned spins = 0;
+      while (generation_.load(std::memory_order_acquire) == gen)
+        if (++spins > 4096) std::this_thread::yield();
+    }
+  }
+
+ private:
+  const unsigned count_;
+  std::atomic<unsigned> arrived_{0}, generation_{0};
+};
+
 void reduce_householder(const SymBandMatrix& M, std::vector<double>& d, std::vector<double>& e,
                         DenseBlock& G) {
   const std::size_t n = M.dim();
@@ -162,43 +186,89 @@ void reduce_householder(const SymBandMatrix& M, std::vector<double>& d, std::vec
   std::vector<double> v(n), p(n), w(n), vstore;
   std::vector<std::size_t> reflectors;
   vstore.reserve(n * n / 2 + n);
-  for (std::size_t k = 0; k + 2 < n; ++k) {
-    const std::size_t len = n - k - 1;
-    double sq = 0.0;
-    for (std::size_t i = 0; i < len; ++i) {
-      v[i] = A(k + 1 + i, k);
-      sq += v[i] * v[i];
+  // The trailing block's two passes per reflector (p = A22 v, then the rank-2 update) are split
+  // over the columns of A22 by a team of threads: every element is computed by exactly the
+  // operations of the sequential loops, so the result does not depend on the team size.
+  unsigned team = 1;
+  if (n >= 192) {
+    unsigned hw = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+    if (const char* env = std::getenv("FLZ_HOST_THREADS")) hw = (unsigned)std::max(1, std::atoi(env));
+    team = std::min(hw, 8u);
+  }
+  SpinBarrier barrier(team);
+  // shared per-reflector state, written by member 0 between barriers
+  struct Step {
+    std::size_t len = 0;
+    double alpha = 0.0;
+    bool apply = false, done = false;
+  } step;
+  auto member = [&](unsigned me) {
+    for (std::size_t k = 0; k + 2 < n; ++k) {
+      const std::size_t len = n - k - 1;
+      if (me == 0) {
+        step.len = len;
+        step.apply = false;
+        double sq = 0.0;
+        for (std::size_t i = 0; i < len; ++i) {
+          v[i] = A(k + 1 + i, k);
+          sq += v[i] * v[i];
+        }
+        if (sq - v[0] * v[0] > 0.0) {  // something below the sub-diagonal
+          const double norm = std::sqrt(sq);
+          const double alpha = v[0] >= 0.0 ? -norm : norm;
+          v[0] -= alpha;
+          double vn = 0.0;
+          for (std::size_t i = 0; i < len; ++i) vn += v[i] * v[i];
+          vn = std::sqrt(vn);
+          if (vn != 0.0) {
+            for (std::size_t i = 0; i < len; ++i) v[i] /= vn;
+            step.alpha = alpha;
+            step.apply = true;
+          }
+        }
+      }
+      if (team > 1) barrier.wait();   // v and step are published
+      if (!step.apply) {
+        if (team > 1) barrier.wait();   // nobody reads `step` while member 0 rewrites it
+        continue;
+      }
+      const std::size_t c0 = len * me / team, c1 = len * (me + 1) / team;
+      // trailing block: A22 <- H A22 H with H = I - 2 v v^T
+      for (std::size_t i = c0; i < c1; ++i) {
+        double acc = 0.0;
+        // A22 stays bitwise symmetric under the rank-2 update below, so row i is read as the
+        // (contiguous) column i: same values, same summation order
+        for (std::size_t j = 0; j < len; ++j) acc += A(k + 1 + j, k + 1 + i) * v[j];
+        p[i] = acc;
+      }
+      if (team > 1) barrier.wait();   // p complete
+      double vp = 0.0;                // every member: the same sum in the same order
+      for (std::size_t i = 0; i < len; ++i) vp += v[i] * p[i];
+      if (me == 0)
+        for (std::size_t i = 0; i < len; ++i) w[i] = p[i] - vp * v[i];
+      if (team > 1) barrier.wait();   // w complete
+      for (std::size_t j = c0; j < c1; ++j)
+        for (std::size_t i = 0; i < len; ++i)
+          A(k + 1 + i, k + 1 + j) -= 2.0 * (v[i] * w[j] + w[i] * v[j]);
+      if (team > 1) barrier.wait();   // update complete: member 0 may touch column k and v
+      if (me == 0) {
+        A(k + 1, k) = A(k, k + 1) = step.alpha;
+        for (std::size_t i = k + 2; i < n; ++i) A(i, k) = A(k, i) = 0.0;
+        reflectors.push_back(k);
+        vstore.insert(vstore.end(), v.begin(), v.begin() + len);
+      }
     }
-    if (sq - v[0] * v[0] <= 0.0) continue;  // nothing below the sub-diagonal
-    const double norm = std::sqrt(sq);
-    const double alpha = v[0] >= 0.0 ? -norm : norm;
-    v[0] -= alpha;
-    double vn = 0.0;
-    for (std::size_t i = 0; i < len; ++i) vn += v[i] * v[i];
-    vn = std::sqrt(vn);
-    if (vn == 0.0) continue;
-    for (std::size_t i = 0; i < len; ++i) v[i] /= vn;
-    // trailing block: A22 <- H A22 H with H = I - 2 v v^T
-    for (std::size_t i = 0; i < len; ++i) {
-      double acc = 0.0;
-      // A22 stays bitwise symmetric under the rank-2 update below, so row i is read as the
-      // (contiguous) column i: same values, same summation order
-      for (std::size_t j = 0; j < len; ++j) acc += A(k + 1 + j, k + 1 + i) * v[j];
-      p[i] = acc;
-    }
-    double vp = 0.0;
-    for (std::size_t i = 0; i < len; ++i) vp += v[i] * p[i];
-    for (std::size_t i = 0; i < len; ++i) w[i] = p[i] - vp * v[i];
-    for (std::size_t j = 0; j < len; ++j)
-      for (std::size_t i = 0; i < len; ++i)
-        A(k + 1 + i, k + 1 + j) -= 2.0 * (v[i] * w[j] + w[i] * v[j]);
-    A(k + 1, k) = A(k, k + 1) = alpha;
-    for (std::size_t i = k + 2; i < n; ++i) A(i, k) = A(k, i) = 0.0;
-    // accumulator: G <- G diag(I, H), applied after the loop (rows in parallel)
-    reflectors.push_back(k);
-    vstore.insert(vstore.end(), v.begin(), v.begin() + len);
+  };
+  if (team <= 1) {
+    member(0);
+  } else {
+    std::vector<std::thread> pool;
+    for (unsigned t = 1; t < team; ++t) pool.emplace_back(member, t);
+    member(0);
+    for (auto& th : pool) th.join();
   }
   {
+    // accumulator: G <- G diag(I, H), applied after the loop (rows in parallel)
     const std::size_t rows = G.rows();
     parallel_rows(rows, n * n, [&](std::size_t r0, std::size_t r1) {
       std::vector<double> gv(r1 - r0);
