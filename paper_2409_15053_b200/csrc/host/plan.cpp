@@ -1,6 +1,7 @@
 // host/plan.cpp — see plan.hpp.  Pure host code, no CUDA.
 
 #include "plan.hpp"
+#include "spin_barrier.hpp"
 
 #include <algorithm>
 #include <chrono>
@@ -242,7 +243,7 @@ int64_t build_ug(HostPlan& P, const std::vector<uint8_t>& is_boundary, bool allo
     uint8_t spill = 0, own_first = 0;
     int64_t uni_begin = 0;  // into the chunk's offset pool (UV offsets first, each run sorted)
   };
-  struct Chunk {
+  struct alignas(128) Chunk {   // own cache lines (vector headers change on every push_back)
     int64_t s0 = 0, s1 = 0;
     std::vector<int64_t> uni_pool;
     std::vector<double> uv_value;   // per pooled offset: the common value (UV offsets only)
@@ -658,7 +659,66 @@ DenseBlocks extract_dense_blocks(int64_t nl, int64_t row_begin, const int64_t* r
   sub.lap("  blocks: seed sort");
   B.count.assign(nl, 0);
   std::vector<uint8_t> mark(nl, 0);
-  std::vector<int32_t> K, keep;
+  std::vector<int32_t> K, keep, dcount;
+  // team of scanning threads (member 0 is this thread); they live for the whole search and
+  // meet at a spin barrier before and after every scan — a scan is ~50 us of work
+  const unsigned team = (unsigned)std::max(1, std::min(8, worker_count()));
+  struct alignas(128) FreshList {   // one cache line pair per member: the list headers are
+    std::vector<std::pair<int64_t, int32_t>> v;   // written on every push_back
+    void clear() { v.clear(); }
+    size_t size() const { return v.size(); }
+    void push_back(std::pair<int64_t, int32_t> x) { v.push_back(x); }
+    auto begin() const { return v.begin(); }
+    auto end() const { return v.end(); }
+  };
+  std::vector<FreshList> fresh_at(team);
+  SpinBarrier barrier(team);
+  bool team_stop = false;
+  int team_job = 0;   // 0: scan a share of K; 1: mark a share's new entries as covered
+  auto cover_share = [&](unsigned me) {   // shares hold disjoint rows: no two members touch
+    for (const auto& f : fresh_at[me]) {  // the same entry or the same uncov counter
+      B.covered[f.first] = 1;
+      --uncov[f.second];
+    }
+  };
+  auto scan_share = [&](unsigned me) {
+    auto& mine = fresh_at[me];
+    mine.clear();   // (entry, row) of the new entries of K x K in this share
+    const size_t q0 = K.size() * me / team, q1 = K.size() * (me + 1) / team;
+    for (size_t q = q0; q < q1; ++q) {
+      const int32_t j = K[q];
+      int32_t d = 0;
+      for (int64_t e = row_ptr[j]; e < row_ptr[j + 1]; ++e) {
+        const int64_t c = local(e);
+        const bool in = c >= 0 && c < nl && mark[c];
+        d += in ? 1 : 0;
+        if (in && !B.covered[e - p0]) mine.push_back({e - p0, j});
+      }
+      dcount[q] = d;
+    }
+  };
+  std::vector<std::thread> scanners;
+  for (unsigned m = 1; m < team; ++m)
+    scanners.emplace_back([&, m] {
+      while (true) {
+        barrier.wait();
+        if (team_stop) return;
+        if (team_job == 0) scan_share(m);
+        else cover_share(m);
+        barrier.wait();
+      }
+    });
+  struct StopTeam {   // also on an exception: release and join the scanners
+    std::vector<std::thread>& pool;
+    SpinBarrier& barrier;
+    bool& stop;
+    ~StopTeam() {
+      if (pool.empty()) return;
+      stop = true;
+      barrier.wait();
+      for (auto& t : pool) t.join();
+    }
+  } stop_team{scanners, barrier, team_stop};
   int fails = 0;
   for (int32_t seed : seeds) {
     if (uncov[seed] < kDenseMin) continue;
@@ -676,18 +736,23 @@ DenseBlocks extract_dense_blocks(int64_t nl, int64_t row_begin, const int64_t* r
     int64_t fresh_seen = -1;
     for (int pass = 0; pass < 2 && (int)K.size() >= kDenseMin && fresh_seen < 0; ++pass) {
       for (int32_t c : K) mark[c] = 1;
+      // the rows of K are scanned by the team (member m: a contiguous share of K, its new
+      // entries in its own list); counts and lists are put together in K order, so the result
+      // is the sequential scan's
+      dcount.resize(K.size());
+      if (team > 1) {
+        team_job = 0;
+        barrier.wait();   // job published (K, mark)
+        scan_share(0);
+        barrier.wait();   // all shares done
+      } else {
+        scan_share(0);
+      }
       keep.clear();
       int64_t fresh_pass = 0;
-      for (int32_t j : K) {
-        int32_t d = 0;
-        for (int64_t e = row_ptr[j]; e < row_ptr[j + 1]; ++e) {
-          const int64_t c = local(e);
-          const bool in = c >= 0 && c < nl && mark[c];
-          d += in ? 1 : 0;
-          fresh_pass += (in && !B.covered[e - p0]) ? 1 : 0;
-        }
-        if (5 * (int64_t)d >= 4 * (int64_t)K.size()) keep.push_back(j);
-      }
+      for (size_t q = 0; q < K.size(); ++q)
+        if (5 * (int64_t)dcount[q] >= 4 * (int64_t)K.size()) keep.push_back(K[q]);
+      for (unsigned m = 0; m < team; ++m) fresh_pass += (int64_t)fresh_at[m].size();
       for (int32_t c : K) mark[c] = 0;
       if (keep.size() == K.size()) fresh_seen = fresh_pass;
       K.swap(keep);
@@ -708,7 +773,18 @@ DenseBlocks extract_dense_blocks(int64_t nl, int64_t row_begin, const int64_t* r
       // (a quarter is enough: a ball that overlaps an earlier block is still worth a block —
       // the hybrid layout drops the columns a task does not use, the paired layout stores zeros)
       ok = 4 * fresh >= (int64_t)K.size() * (int64_t)K.size();
-      if (ok) {
+      if (ok && fresh_seen >= 0) {
+        // the last pass kept every member: its lists of new entries are the block's
+        if (team > 1) {
+          team_job = 1;
+          barrier.wait();
+          cover_share(0);
+          barrier.wait();
+        } else {
+          cover_share(0);
+        }
+        B.covered_entries += fresh;
+      } else if (ok) {
         for (int32_t j : K)
           for (int64_t e = row_ptr[j]; e < row_ptr[j + 1]; ++e) {
             const int64_t c = local(e);
@@ -847,6 +923,7 @@ void build_hybrid(HostPlan& P, const DenseBlocks& blocks, const int64_t* row_ptr
   std::vector<int64_t> dense_part(dchunks, 0);
   run_chunks(dchunks, [&](int w) {
     std::vector<int32_t> pos(nl, 0);   // index of a row among the current task's columns
+    int64_t filled = 0;   // (a local count: the shared array would bounce between the cores)
     for (int64_t t = ntask * w / dchunks; t < ntask * (w + 1) / dchunks; ++t) {
       PlanHyTask& T = P.hy_dtasks[t];
       const TaskSpec& S = spec[T.pad[0]];
@@ -863,10 +940,11 @@ void build_hybrid(HostPlan& P, const DenseBlocks& blocks, const int64_t* row_ptr
           if (c == i || owner(i, c) != S.block) continue;
           const int64_t j = pos[c];   // c is one of the task's columns (pass 1 marked it)
           v[j * kPlanSliceRows + q] = values[e];
-          ++dense_part[w];
+          ++filled;
         }
       }
     }
+    dense_part[w] = filled;
   });
   sub.lap("  hybrid: dense values");
   for (auto& T : P.hy_dtasks) T.pad[0] = 0;
@@ -876,7 +954,7 @@ void build_hybrid(HostPlan& P, const DenseBlocks& blocks, const int64_t* row_ptr
   const int64_t ns = (nl + kPlanSliceRows - 1) / kPlanSliceRows;
   P.hy_slice.assign(ns, PlanHySlice{});
   P.hy_diag.assign(std::max<int64_t>(nl, 1), 0.0);
-  struct Chunk {
+  struct alignas(128) Chunk {   // own cache lines: the vector headers change on every push_back
     std::vector<int32_t> cols;
     std::vector<double> uv, gv;
     int64_t uv_entries = 0, g_entries = 0;
@@ -890,7 +968,11 @@ void build_hybrid(HostPlan& P, const DenseBlocks& blocks, const int64_t* row_ptr
       int32_t lane, col;
       double v;
     };
-    std::vector<Ent> ents;
+    std::vector<Ent> ents, sorted_ents;
+    std::vector<uint64_t> gkeys;
+    std::vector<size_t> gcount, goffset;
+    std::vector<int> gorder;
+    std::vector<int16_t> gid_of;
     std::vector<std::vector<std::pair<int32_t, double>>> gen(kPlanSliceRows);
     std::vector<std::vector<int32_t>> per(kPlanSliceRows);
     for (int64_t s = ns * w / schunks; s < ns * (w + 1) / schunks; ++s) {
@@ -911,11 +993,57 @@ void build_hybrid(HostPlan& P, const DenseBlocks& blocks, const int64_t* row_ptr
           ents.push_back({bits, l, c, values[e]});
         }
       }
-      std::sort(ents.begin(), ents.end(), [](const Ent& a, const Ent& b) {
-        if (a.bits != b.bits) return a.bits < b.bits;
-        if (a.lane != b.lane) return a.lane < b.lane;
-        return a.col < b.col;
-      });
+      // order (value bits, lane, column).  The entries arrive by lane and, inside a lane, by
+      // column, so a STABLE distribution over the distinct values (a few dozen on a stencil)
+      // sorted by their bits gives that order without a comparison sort of the entries
+      {
+        constexpr int kTab = 256;
+        uint64_t tkey[kTab];
+        int16_t tgid[kTab];
+        std::fill(tgid, tgid + kTab, (int16_t)-1);
+        gkeys.clear();
+        gcount.clear();
+        gid_of.resize(ents.size());
+        bool small = true;
+        for (size_t q = 0; q < ents.size() && small; ++q) {
+          uint64_t h = ents[q].bits * 0x9E3779B97F4A7C15ULL;
+          int slot = (int)(h >> 56);
+          while (tgid[slot] >= 0 && tkey[slot] != ents[q].bits) slot = (slot + 1) & (kTab - 1);
+          if (tgid[slot] < 0) {
+            if (gkeys.size() >= 160) {   // many distinct values: no stencil, sort instead
+              small = false;
+              break;
+            }
+            tkey[slot] = ents[q].bits;
+            tgid[slot] = (int16_t)gkeys.size();
+            gkeys.push_back(ents[q].bits);
+            gcount.push_back(0);
+          }
+          gid_of[q] = tgid[slot];
+          ++gcount[tgid[slot]];
+        }
+        if (small) {
+          const int ng_keys = (int)gkeys.size();
+          gorder.resize(ng_keys);
+          std::iota(gorder.begin(), gorder.end(), 0);
+          std::sort(gorder.begin(), gorder.end(), [&](int a, int b) { return gkeys[a] < gkeys[b]; });
+          goffset.assign(ng_keys, 0);
+          size_t run = 0;
+          for (int r = 0; r < ng_keys; ++r) {
+            goffset[gorder[r]] = run;
+            run += gcount[gorder[r]];
+          }
+          sorted_ents.resize(ents.size());
+          for (size_t q = 0; q < ents.size(); ++q) sorted_ents[goffset[gid_of[q]]++] = ents[q];
+          ents.swap(sorted_ents);
+        } else {
+          std::sort(ents.begin(), ents.end(), [](const Ent& a, const Ent& b) {
+            if (a.bits != b.bits) return a.bits < b.bits;
+            if (a.lane != b.lane) return a.lane < b.lane;
+            return a.col < b.col;
+          });
+        }
+      }
       PlanHySlice& H = P.hy_slice[s];
       H.col_off = (int64_t)C.cols.size() / kPlanSliceRows;   // chunk-relative for now
       H.uv_off = (int32_t)C.uv.size();
@@ -1005,9 +1133,17 @@ void build_hybrid(HostPlan& P, const DenseBlocks& blocks, const int64_t* row_ptr
   P.hy_uvval.resize(std::max<int64_t>(nuvv, 1));
   P.hy_gval.resize(std::max<int64_t>(ngv, 1));
   P.hy_uv_entries = P.hy_g_entries = 0;
-  int64_t bc = 0, bu = 0, bg = 0;
+  std::vector<int64_t> base_c(schunks + 1, 0), base_u(schunks + 1, 0), base_g(schunks + 1, 0);
   for (int w = 0; w < schunks; ++w) {
+    base_c[w + 1] = base_c[w] + (int64_t)chunk[w].cols.size();
+    base_u[w + 1] = base_u[w] + (int64_t)chunk[w].uv.size();
+    base_g[w + 1] = base_g[w] + (int64_t)chunk[w].gv.size();
+    P.hy_uv_entries += chunk[w].uv_entries;
+    P.hy_g_entries += chunk[w].g_entries;
+  }
+  run_chunks(schunks, [&](int w) {   // every chunk moves to its place on its own thread
     Chunk& C = chunk[w];
+    const int64_t bc = base_c[w], bu = base_u[w], bg = base_g[w];
     std::copy(C.cols.begin(), C.cols.end(), P.hy_cols.begin() + bc);
     std::copy(C.uv.begin(), C.uv.end(), P.hy_uvval.begin() + bu);
     std::copy(C.gv.begin(), C.gv.end(), P.hy_gval.begin() + bg);
@@ -1016,12 +1152,7 @@ void build_hybrid(HostPlan& P, const DenseBlocks& blocks, const int64_t* row_ptr
       P.hy_slice[s].uv_off += (int32_t)bu;
       P.hy_slice[s].g_off += (int32_t)(bg / kPlanSliceRows);
     }
-    bc += (int64_t)C.cols.size();
-    bu += (int64_t)C.uv.size();
-    bg += (int64_t)C.gv.size();
-    P.hy_uv_entries += C.uv_entries;
-    P.hy_g_entries += C.g_entries;
-  }
+  });
   sub.lap("  hybrid: concatenate");
   P.hy = true;
 }
@@ -1348,9 +1479,14 @@ HostPlan build_plan(int64_t n_global, int rank, int nranks, const std::vector<in
     len[i] = (int32_t)l;
   }
   const int64_t p0 = nl > 0 ? row_ptr[0] : 0;
-  for (int64_t p = 0; p < P.nnz; ++p)
-    require(col_idx[p0 + p] >= 0 && col_idx[p0 + p] < n_global,
-            "plan: column index out of range");
+  {
+    const int vchunks = (int)std::max<int64_t>(1, std::min<int64_t>(worker_count(), P.nnz >> 18));
+    run_chunks(vchunks, [&](int t) {
+      for (int64_t p = P.nnz * t / vchunks; p < P.nnz * (t + 1) / vchunks; ++p)
+        require(col_idx[p0 + p] >= 0 && col_idx[p0 + p] < n_global,
+                "plan: column index out of range");
+    });
+  }
 
   PhaseTimer timer;
   timer.lap("validate");

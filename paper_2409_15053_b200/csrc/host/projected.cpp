@@ -12,6 +12,7 @@
 // dim x dim embedding.
 
 #include "flz/projected.hpp"
+#include "spin_barrier.hpp"
 
 #include <algorithm>
 #include <atomic>
@@ -156,29 +157,6 @@ void reduce_band(const SymBandMatrix& M, std::vector<double>& d, std::vector<dou
 }
 
 // Householder tridiagonalization of the dense embedding (wide bands).
-// Team of host threads stepping through the reflectors of reduce_householder together: a
-// sense-reversing spin barrier (the per-reflector work is a few microseconds, far below what a
-// condition variable costs).
-class SpinBarrier {
- public:
-  explicit SpinBarrier(unsigned count) : count_(count) {}
-  void wait() {
-    const unsigned gen = generation_.load(std::memory_order_acquire);
-    if (arrived_.fetch_add(1, std::memory_order_acq_rel) + 1 == count_) {
-      arrived_.store(0, std::memory_order_relaxed);
-      generation_.store(gen + 1, std::memory_order_release);
-    } else {
-      unsigned spins = 0;
-      while (generation_.load(std::memory_order_acquire) == gen)
-        if (++spins > 4096) std::this_thread::yield();
-    }
-  }
-
- private:
-  const unsigned count_;
-  std::atomic<unsigned> arrived_{0}, generation_{0};
-};
-
 void reduce_householder(const SymBandMatrix& M, std::vector<double>& d, std::vector<double>& e,
                         DenseBlock& G) {
   const std::size_t n = M.dim();
