@@ -173,6 +173,10 @@ struct flz_ctx {
   flz::DevBuf<double> stage;     // host<->device staging of blocks
   flz::DevBuf<double> stage2;
   flz::DevBuf<char> flush;       // L2 flush target
+  // staged downloads into pageable host memory (capi.cu download_block): two page-locked
+  // buffers filled by the copy engine and emptied by host threads
+  void* dl_pinned[2] = {nullptr, nullptr};
+  cudaEvent_t dl_event[2] = {nullptr, nullptr};
   flz::DevBuf<double> qr_scratch;              // block_qr_kernel: per-phase, per-CTA partial sums
   flz::DevBuf<unsigned long long> qr_barrier;  // its grid-barrier counter (monotone)
   unsigned long long qr_arrivals = 0;          // arrivals issued so far
