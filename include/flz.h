@@ -181,6 +181,11 @@ int flz_plan_hy(const flz_plan* plan, int64_t* sizes, int64_t* slices, int32_t* 
  * 8 * staged element << 32 | (position 0 only) position count << 52 | (position 0 only,
  * slice also has per-lane positions) 1 << 56.  pairs may be NULL. */
 int flz_plan_tiles(const flz_plan* plan, int64_t* info, double* pairs);
+/* ... on a row slab (nranks > 1): info[4] = {front, back, tile_a, tile_b} — the kernel stages
+ * runs of the virtual source [front halo rows | local rows | back halo rows] (front = halo
+ * slots owned by lower ranks; stored source: [local | front halo | back halo]), and tiles
+ * [tile_a, tile_b) stage local rows only: they run while the halo rows travel. */
+int flz_plan_tile_slab(const flz_plan* plan, int64_t* info);
 
 /* Global matvec counter: speig::matvec_count()/reset (sparse.hpp:74-79).  One count per
  * vector-column product, so a fused r-column block product adds r. */

@@ -102,6 +102,7 @@ _SIGS = {
     "flz_plan_hy": (i32, [vp] * 11),
     "flz_matrix_k1_info": (i32, [vp, i32, vp, vp, i32]),
     "flz_plan_tiles": (i32, [vp, vp, vp]),
+    "flz_plan_tile_slab": (i32, [vp, vp]),
     "flz_matvec_count": (u64, []),
     "flz_reset_matvec_count": (None, []),
     "flz_matvec_sub": (None, [u64]),

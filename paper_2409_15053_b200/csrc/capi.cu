@@ -125,9 +125,19 @@ SellView make_view(const flz_matrix* A, const SliceTask* tasks, int64_t ntasks,
                   A->nl + A->nhalo, A->rest_rows.p, A->nslices,   A->w.p,
                   A->uv_pairs.p,    false,          A->p2_desc.p, A->p2_col.p, A->p2_val.p,
                   A->p2_dcol.p,     A->p2_dval.p,   nullptr,
-                  // the tile kernel covers whole-matrix launches only
+                  // the tile kernel covers whole-matrix launches (and, on row slabs, its own
+                  // split into tiles without and with halo rows: tiled(), below)
                   (slice_ids == nullptr && nslices == A->nslices) ? A->tiles : StencilTiles{},
-                  A->hy ? A->sell_rows.p : nullptr};
+                  A->hy ? A->sell_rows.p : nullptr, A->nslices, 0};
+}
+// Row slabs with a tile plan: the interior / boundary launch as a phase of the tile kernel
+// (the slice lists stay in place for the one-warp-per-slice kernel it falls back to).
+SellView tiled(const flz_matrix* A, SellView v, int phase) {
+  if (A->tiles.nseg > 0 && !A->ctx->exact) {
+    v.tiles = A->tiles;
+    v.tile_phase = phase;
+  }
+  return v;
 }
 // fast mode on a matrix with the paired layout: the launch walks the paired task lists
 SellView paired(const flz_matrix* A, SellView v, int which) {
@@ -201,6 +211,16 @@ void halo_begin(const flz_matrix* A, int R, int S, double* Y1) {
   FLZ_CUDA(cudaEventRecord(ctx->ev_halo_ready, ctx->stream));
   FLZ_CUDA(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_halo_ready, 0));
   constexpr size_t D = sizeof(double);
+  // FLZ_HALO_DRY=1 (timing experiments on one GPU, WRONG results): pack, events and the phase
+  // split stay, the transfers are skipped — the compute side of one rank of a slab run
+  static const bool dry = [] {
+    const char* e = std::getenv("FLZ_HALO_DRY");
+    return e && e[0] == '1';
+  }();
+  if (dry) {
+    FLZ_CUDA(cudaEventRecord(ctx->ev_halo_done, ctx->comm_stream));
+    return;
+  }
   comm_group_start(ctx);
   for (const auto& p : A->peers) {
     if (S > 0) {
@@ -259,12 +279,12 @@ void sell_step(const flz_matrix* A, int R, int S, StepMode mode, double s1, doub
   }
   halo_begin(A, R, S, Y1);
   rest(1, A->nt_rest_interior);
-  launch_clenshaw_step(ctx, view_interior(A), R, S, mode, ctx->exact, s1, s2, b, Y1, Y2, ldy, X,
-                       ldx, Out, ldo);
+  launch_clenshaw_step(ctx, tiled(A, view_interior(A), 1), R, S, mode, ctx->exact, s1, s2, b, Y1, Y2,
+                       ldy, X, ldx, Out, ldo);
   FLZ_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_halo_done, 0));
   rest(2, A->nt_rest_boundary);
-  launch_clenshaw_step(ctx, view_boundary(A), R, S, mode, ctx->exact, s1, s2, b, Y1, Y2, ldy, X,
-                       ldx, Out, ldo);
+  launch_clenshaw_step(ctx, tiled(A, view_boundary(A), 2), R, S, mode, ctx->exact, s1, s2, b, Y1, Y2,
+                       ldy, X, ldx, Out, ldo);
 }
 
 // Layout of the filter workspaces for R fused columns (see launch_clenshaw_step):
@@ -281,8 +301,10 @@ int row_stride(const flz_matrix* A, int R) {
   // with 4 columns the 32-byte rows win (37.3 vs 39.4 us)
   // ... and for every column count when the TMA-staged tile kernel applies (it reads planar
   // blocks only: contiguous runs per column)
+  // (row slabs: A->tiles is set only when EVERY rank has a tile plan, flz_matrix_upload)
   const bool planar = force ? force[0] == 'p'
-                            : (A->lean && A->ctx->nranks == 1 && (R == 3 || A->tiles.nseg > 0));
+                            : (A->lean && (A->ctx->nranks == 1 ? (R == 3 || A->tiles.nseg > 0)
+                                                               : A->tiles.nseg > 0));
   if (planar) return 0;
   if (R != 3) return R;
   if (force && force[0] == '4') return 4;  // experiments: padded rows for every matrix
@@ -854,6 +876,7 @@ int flz_matrix_upload(flz_ctx* ctx, int64_t n_global, int64_t row_begin, int64_t
       throw ApiError(FLZ_EINVAL, std::string("matrix_upload: ") + e.what());
     }
     bool dense_rows_global = plan.nnz >= 16 * plan.nl;
+    bool tiles_everywhere = true;
     if (P > 1) {
       // Halo rows travel in the block layout of the filter workspaces, so every rank must pick
       // the same one: the hybrid layout (planar blocks) only if EVERY rank found its dense
@@ -871,6 +894,10 @@ int flz_matrix_upload(flz_ctx* ctx, int64_t n_global, int64_t row_begin, int64_t
       };
       gather(plan.hy ? 1 : 0);
       const bool all_hybrid = std::all_of(all.begin(), all.end(), [](int64_t v) { return v != 0; });
+      // ... and the tile kernel of a stencil (planar blocks as well) only if every rank has a
+      // tile plan; ranks without local rows have no say
+      gather(plan.nl == 0 || plan.tiles.nseg > 0 ? 1 : 0);
+      tiles_everywhere = std::all_of(all.begin(), all.end(), [](int64_t v) { return v != 0; });
       gather(plan.nnz);
       const int64_t nnz_all = std::accumulate(all.begin(), all.end(), (int64_t)0);
       dense_rows_global = nnz_all >= 16 * n_global;
@@ -935,6 +962,7 @@ int flz_matrix_upload(flz_ctx* ctx, int64_t n_global, int64_t row_begin, int64_t
       }
     }
     auto A = std::make_unique<flz_matrix>();
+    if (!tiles_everywhere) plan.tiles = PlanStencilTiles{};
     upload_plan(ctx, plan, A.get());
     A->dense_rows = dense_rows_global;
     ctx->refs += 1;
@@ -1142,6 +1170,15 @@ int flz_plan_tiles(const flz_plan* plan, int64_t* info, double* pairs) {
   info[27] = G.own_e;
   info[28] = G.nseg ? (int64_t)P.uv_pairs.size() : 0;
   if (G.nseg && pairs) std::copy(P.uv_pairs.begin(), P.uv_pairs.end(), pairs);
+  return FLZ_OK;
+}
+int flz_plan_tile_slab(const flz_plan* plan, int64_t* info) {
+  if (!plan || !info) return FLZ_EINVAL;
+  const PlanStencilTiles& G = plan->P.tiles;
+  info[0] = G.front;
+  info[1] = G.back;
+  info[2] = G.tile_a;
+  info[3] = G.tile_b;
   return FLZ_OK;
 }
 

@@ -104,6 +104,8 @@ struct StencilTiles {
   int32_t tile_rows = 0, nseg = 0;
   int32_t seg_base[8] = {}, seg_len[8] = {}, seg_start[8] = {};
   int32_t y1_elems = 0, own_e = 0;
+  int32_t front = 0, back = 0;     // row slabs: halo rows in front of / behind the local rows
+  int32_t tile_a = 0, tile_b = 0;  // tiles [tile_a, tile_b) stage local rows only
 };
 
 // Slice descriptor of the paired layout (mirrors PlanP2Slice, host/plan.hpp)
@@ -167,6 +169,7 @@ struct flz_ctx {
   int refs = 1;                  // owner + every matrix/basis created on the context
   uint64_t launches = 0;
   int k1_slices_per_cta = 0, k1_tasks_per_cta = 0, k1_batch = 0;  // 0: defaults (tuning knobs)
+  bool k1_pdl_once = false;   // the next K1 launch carries the dependent-launch attribute (row slabs)
   cudaEvent_t t0[16] = {}, t1[16] = {};
   flz::DevBuf<double> partial;   // split-K partial sums of the tall-skinny GEMMs
   flz::DevBuf<double> small;     // small device scratch of the host-buffer test seams
@@ -364,6 +367,8 @@ struct SellView {
   unsigned* tickets;         // this launch's task counter (starts at 0; persistent CTAs)
   StencilTiles tiles;        // nseg > 0: tile plan of the TMA-staged stencil kernel
   const int32_t* sell_rows;  // exact-mode kernel: SELL lane -> row (nullptr: slice * 32 + lane)
+  int64_t tile_slices = 0;   // the tile plan covers slices [0, tile_slices) of the matrix
+  int tile_phase = 0;        // 0: all tiles, 1: tiles without halo rows, 2: the rest (row slabs)
 };
 
 // Hybrid layout (host/plan.hpp) as the kernels see it

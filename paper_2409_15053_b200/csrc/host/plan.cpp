@@ -1382,27 +1382,76 @@ void ensure_ug(HostPlan& P) {
 }
 
 // Tile plan of the TMA-staged stencil kernel (plan.hpp, PlanStencilTiles).  Applies when the
-// matrix is a stencil ("lean") on one rank without rest slices; the uniform-value positions
-// of all slices use at most 16 distinct offsets in kPlanMaxSegs segments.  The few slices that
-// also hold per-lane positions (stencil rows next to a domain boundary) are flagged (bit 56
-// of position 0's mask word): the kernel adds those positions from global memory.
+// matrix is a stencil ("lean") in natural row order without rest slices; the uniform-value
+// positions of all slices use at most 16 distinct offsets in kPlanMaxSegs segments.  The few
+// slices that also hold per-lane positions (stencil rows next to a domain boundary) are
+// flagged (bit 56 of position 0's mask word): the kernel adds those positions from global
+// memory.
+// Row slabs (nranks > 1): the kernel stages runs of the VIRTUAL gather source
+// [front halo rows | local rows | back halo rows] — front = the halo slots whose owners have
+// smaller rows — so that a neighbour plane that arrives from a peer sits at the offset it has
+// inside the slab (100^3 Laplacian, z slabs: the offsets stay {-P^2, -P, -1, 0, 1, P, P^2} and
+// the three segments of the single-rank plan).  A position's offset d into the stored source
+// [local | halo] becomes d - (nl + front) when its lanes read front halo rows and d - front
+// when they read back halo rows; a position whose lanes mix classes with different shifts has
+// no tile plan.  Tiles [tile_a, tile_b) stage local rows only: they run while the halo travels.
 static void build_stencil_tiles(HostPlan& P) {
   P.tiles = PlanStencilTiles{};
-  if (!P.lean || P.nranks != 1 || !P.halo.empty() || P.nrest > 0 || P.sigma > 1) return;
+  if (!P.lean || P.nrest > 0 || P.sigma > 1) return;
+  const bool slab = P.nranks != 1 || !P.halo.empty();
+  const int64_t nl = P.nl;
+  const int64_t front =
+      std::lower_bound(P.halo.begin(), P.halo.end(), P.row_begin) - P.halo.begin();
+  const int64_t back = (int64_t)P.halo.size() - front;
+  // 16-byte bulk copies: the pieces of a run start at even rows of the stored source
+  if (slab && ((nl & 1) || (front & 1) || nl == 0)) return;
+  if (slab) {
+    static const bool off = [] {   // FLZ_ST_SLAB=0: row slabs keep the one-warp-per-slice kernel
+      const char* e = std::getenv("FLZ_ST_SLAB");
+      return e && e[0] == '0';
+    }();
+    if (off) return;
+  }
   int T = 256;  // B200, 100^3 Laplacian, 3 columns: 16.4 us per step (128: 17.3, 512: 16.9)
   if (const char* e = std::getenv("FLZ_ST_TILE")) T = std::atoi(e);
   if (T <= 0) return;  // FLZ_ST_TILE=0 switches the tile kernel off
   T = std::clamp(T / kPlanSliceRows, 1, 16) * kPlanSliceRows;
+  // offset of position p of slice s in the virtual source; false: lanes of mixed classes
+  auto virtual_off = [&](int64_t s, int p, int32_t d, int64_t& out) {
+    if (!slab) {
+      out = d;
+      return true;
+    }
+    uint64_t bits;
+    std::memcpy(&bits, &P.uv_pairs[s * 16 + 2 * p + 1], 8);
+    const uint32_t mask = (uint32_t)bits;
+    int64_t shift = 0;
+    bool have = false;
+    for (int l = 0; l < kPlanSliceRows; ++l) {
+      if (!((mask >> l) & 1u)) continue;
+      const int64_t c = s * kPlanSliceRows + l + d;
+      const int64_t sh = c < nl ? 0 : (c < nl + front ? -(nl + front) : -front);
+      if (have && sh != shift) return false;
+      shift = sh;
+      have = true;
+    }
+    out = have ? d + shift : 0;
+    return true;
+  };
   std::vector<int32_t> offs{0};
   for (int64_t s = 0; s < P.nslices; ++s) {
     const PlanUgSlice& H = P.ug_slice[s];
     const int nuv = (H.reserved >> 16) & 0xff;
     if (nuv > 8 || H.nu > 8 || (H.reserved & 3)) return;
-    for (int p = 0; p < nuv; ++p)
-      if (std::find(offs.begin(), offs.end(), H.inline_off[p]) == offs.end()) {
+    for (int p = 0; p < nuv; ++p) {
+      int64_t d = 0;
+      if (!virtual_off(s, p, H.inline_off[p], d)) return;
+      if (d < INT32_MIN / 2 || d > INT32_MAX / 2) return;
+      if (std::find(offs.begin(), offs.end(), (int32_t)d) == offs.end()) {
         if (offs.size() >= 16) return;
-        offs.push_back(H.inline_off[p]);
+        offs.push_back((int32_t)d);
       }
+    }
   }
   std::sort(offs.begin(), offs.end());
   PlanStencilTiles G;
@@ -1431,15 +1480,35 @@ static void build_stencil_tiles(HostPlan& P) {
   G.own_e = staged(0);
   const int64_t per_tile = T / kPlanSliceRows;
   const int64_t ntiles = (P.nslices + per_tile - 1) / per_tile;
+  // tiles whose runs stay inside the local rows (no halo row staged): [tile_a, tile_b)
+  int64_t tile_a = 0, tile_b = ntiles;
+  if (slab) {
+    const int64_t lo = G.seg_base[0];
+    const int64_t hi = (int64_t)G.seg_base[G.nseg - 1] + G.seg_len[G.nseg - 1];   // run end, tile 0
+    if (front > 0 && lo < 0) tile_a = std::min(ntiles, (-lo + T - 1) / T);
+    if (back > 0) tile_b = nl >= hi ? std::min(ntiles, (nl - hi) / T + 1) : 0;
+    tile_b = std::max(tile_a, tile_b);
+    // every slice that references a halo row (uniform or per-lane position) must lie outside
+    for (int32_t s : P.boundary) {
+      const int64_t t = s / per_tile;
+      if (t >= tile_a && t < tile_b) return;
+    }
+  }
+  G.front = (int32_t)front;
+  G.back = (int32_t)back;
+  G.tile_a = (int32_t)tile_a;
+  G.tile_b = (int32_t)tile_b;
   P.uv_pairs.resize((size_t)(ntiles * per_tile) * 16, 0.0);
   for (int64_t s = 0; s < P.nslices; ++s) {
     const PlanUgSlice& H = P.ug_slice[s];
     const int nuv = (H.reserved >> 16) & 0xff;
     for (int p = 0; p < nuv; ++p) {
+      int64_t d = 0;
+      virtual_off(s, p, H.inline_off[p], d);
       uint64_t bits;
       std::memcpy(&bits, &P.uv_pairs[s * 16 + 2 * p + 1], 8);
       bits &= 0xffffffffull;
-      bits |= (uint64_t)(uint32_t)(8 * staged(H.inline_off[p])) << 32;
+      bits |= (uint64_t)(uint32_t)(8 * staged((int32_t)d)) << 32;
       if (p == 0) bits |= (uint64_t)nuv << 52;
       std::memcpy(&P.uv_pairs[s * 16 + 2 * p + 1], &bits, 8);
     }

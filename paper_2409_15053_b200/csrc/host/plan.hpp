@@ -85,6 +85,10 @@ struct PlanStencilTiles {
   int32_t seg_base[kPlanMaxSegs] = {}, seg_len[kPlanMaxSegs] = {}, seg_start[kPlanMaxSegs] = {};
   int32_t y1_elems = 0;  // staged elements per block column (sum of the segment lengths)
   int32_t own_e = 0;     // staged element of offset 0 (the tile's own rows)
+  // row slabs: the staged source is [front halo rows | local rows | back halo rows]; tiles
+  // [tile_a, tile_b) stage local rows only (they run while the halo rows travel)
+  int32_t front = 0, back = 0;
+  int32_t tile_a = 0, tile_b = 0;
 };
 
 // Slice descriptor of the paired layout (mirrors P2Slice, flz_internal.hpp): general positions

@@ -86,7 +86,8 @@ void launch_k1_smem(flz_ctx* ctx, void (*kernel)(KArgs...), unsigned grid, unsig
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
-  const bool pdl = pdl_enabled() && ctx->nranks == 1;
+  const bool pdl = pdl_enabled() && (ctx->nranks == 1 || ctx->k1_pdl_once);
+  ctx->k1_pdl_once = false;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
   FLZ_CUDA(cudaLaunchKernelEx(&cfg, kernel, KArgs(std::forward<Args>(args))...));
@@ -908,12 +909,19 @@ __device__ __noinline__ SliceAcc<R> stencil_slice_rest(const SellView& A, int64_
   return acc;
 }
 
-template <int R, int MODE>
+// SLAB (row slabs, the tiles that stage halo rows): a run covers rows [-front, y_rows - front)
+// of the VIRTUAL source column [front halo | local | back halo]; rows [-front, 0) are stored at
+// base + nl + (g + front), rows [0, nl) at base + g, rows [nl, ...) at base + front + g — up
+// to three bulk copies per run — and the launch walks the tiles outside [hole_lo, hole_lo +
+// hole_len).  !SLAB: tiles [tile_lo, tile_lo + ntiles), one copy per run (the single-rank
+// kernel; on row slabs the tiles whose runs stay inside the local rows).
+template <int R, int MODE, bool SLAB>
 __global__ void __launch_bounds__(768)
     clenshaw_step_stencil_tma(const __grid_constant__ SellView A,
                               const __grid_constant__ StencilTiles G,
                               const double* __restrict__ pairs, int64_t nl,
-                              int64_t ntiles, int nstages, int nprod, int l2hint, int64_t y_rows,
+                              int64_t ntiles, int64_t tile_lo, int64_t hole_lo, int64_t hole_len,
+                              int nstages, int nprod, int l2hint, int64_t y_rows,
                               int64_t x_rows,
                               double s1, double s2, double b, const double* __restrict__ Y1,
                               double* __restrict__ Y2, int64_t ldy, const double* __restrict__ X,
@@ -955,6 +963,8 @@ __global__ void __launch_bounds__(768)
     int dst = 0, full = 0, off = 0;   // staged element, run length, first row relative to the tile
     int64_t lim = 0;                  // readable rows of the source column
     const double* base = nullptr;
+    bool y1run = false;               // SLAB: a run of the gather source (halo pieces)
+    const int64_t front = SLAB ? G.front : 0;
     // L2 policy: X and the matrix pairs are read again by every later step of the filter and
     // never written (evict_last); the Y blocks take the default priority
     bool keep = false;
@@ -970,6 +980,7 @@ __global__ void __launch_bounds__(768)
       off = G.seg_base[j];
       lim = y_rows;
       base = Y1 + (int64_t)k * ldy;
+      y1run = true;
     } else if (c < ncopy) {
       const int q = c - 1 - G.nseg * R, which = q / R, k = q - which * R;
       dst = pair_d + y1_d + q * T;
@@ -981,15 +992,21 @@ __global__ void __launch_bounds__(768)
     keep = keep && l2hint;
     int st = 0;
     uint32_t parity = 1;  // first pass over the ring: the stages are empty (wait falls through)
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    for (int64_t u = blockIdx.x; u < ntiles; u += gridDim.x) {
+      int64_t t = tile_lo + u;
+      if constexpr (SLAB) {
+        if (t >= hole_lo) t += hole_len;
+      }
       mbar_wait(empty_bars + st * 8, parity);
       double* sb = ring + (int64_t)st * stage_d;
       const uint32_t bar = full_bars + st * 8;
       int lead = 0, count = full;
       const double* src = pairs + t * pair_d;
+      int64_t g0 = 0;
       if (base) {
-        const int64_t g0 = t * T + off;
-        const int64_t a0 = max(g0, (int64_t)0), a1 = min(g0 + full, lim);
+        g0 = t * T + off;
+        const int64_t lo = (SLAB && y1run) ? -front : 0, hi = (SLAB && y1run) ? lim - front : lim;
+        const int64_t a0 = max(g0, lo), a1 = min(g0 + full, hi);
         lead = (int)min(a0 - g0, (int64_t)full);
         count = (int)max(a1 - a0, (int64_t)0);
         src = base + a0;
@@ -1012,7 +1029,19 @@ __global__ void __launch_bounds__(768)
         asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
                      "r"(total) : "memory");
       __syncwarp();
-      if (count > 0) {
+      if (SLAB && y1run && front > 0) {
+        // the stored pieces of the run: local rows, halo rows in front, halo rows behind
+        const uint32_t to = ring_s + (uint32_t)(st * stage_d + dst) * 8u;
+        const int64_t g1 = g0 + full;
+        const int64_t b0 = max(g0, (int64_t)0), b1 = min(g1, nl);
+        if (b1 > b0) bulk_g2s(to + (uint32_t)(b0 - g0) * 8u, base + b0, (uint32_t)(b1 - b0) * 8u, bar);
+        const int64_t f0 = max(g0, -front), f1 = min(g1, (int64_t)0);
+        if (f1 > f0)
+          bulk_g2s(to + (uint32_t)(f0 - g0) * 8u, base + nl + front + f0, (uint32_t)(f1 - f0) * 8u, bar);
+        const int64_t c0 = max(g0, nl), c1 = min(g1, lim - front);
+        if (c1 > c0)
+          bulk_g2s(to + (uint32_t)(c0 - g0) * 8u, base + front + c0, (uint32_t)(c1 - c0) * 8u, bar);
+      } else if (count > 0) {
         const uint32_t to = ring_s + (uint32_t)(st * stage_d + dst + lead) * 8u;
         if (keep) bulk_g2s_hint(to, src, bytes, bar, pol_keep);
         else bulk_g2s(to, src, bytes, bar);
@@ -1028,11 +1057,19 @@ __global__ void __launch_bounds__(768)
   const uint32_t y1e8 = (uint32_t)y1e * 8u;
   const uint32_t lanebit = 1u << lane;
   const uint32_t own8 = (uint32_t)G.own_e * 8u;
-  int64_t row = ((int64_t)blockIdx.x * spt + warp) * 32 + lane;
+  int64_t row = (((int64_t)blockIdx.x + tile_lo) * spt + warp) * 32 + lane;
   const int64_t row_step = (int64_t)gridDim.x * T;
   double* dst = (MODE == 0 ? Y2 : Out) + row;
   const int64_t ldd = MODE == 0 ? ldy : ldo;
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, row += row_step, dst += row_step) {
+  for (int64_t u = blockIdx.x; u < ntiles; u += gridDim.x, row += row_step, dst += row_step) {
+    int64_t t = tile_lo + u;
+    if constexpr (SLAB) {   // the tiles behind the hole
+      if (t >= hole_lo) {
+        t += hole_len;
+        row = (t * spt + warp) * 32 + lane;
+        dst = (MODE == 0 ? Y2 : Out) + row;
+      }
+    }
     mbar_wait(full_bars + st * 8, parity);
     const double* sb = ring + (int64_t)st * stage_d;
     const double2* sP = reinterpret_cast<const double2*>(sb + warp * 16);
@@ -1633,7 +1670,7 @@ bool launch_stencil_tma(flz_ctx* ctx, const SellView& A, double s1, double s2, d
                         const double* Y1, double* Y2, int64_t ldy, const double* X, int64_t ldx,
                         double* Out, int64_t ldo) {
   const StencilTiles& G = A.tiles;
-  if (G.nseg == 0 || A.nslices == 0) return false;
+  if (G.nseg == 0 || A.tile_slices == 0) return false;
   auto aligned = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   if (!aligned(Y1) || (ldy & 1) || ldy < A.nl) return false;
   if (MODE != 2 && (!aligned(Y2) || !aligned(X) || (ldx & 1) || ldx < A.nl)) return false;
@@ -1660,15 +1697,42 @@ bool launch_stencil_tma(flz_ctx* ctx, const SellView& A, double s1, double s2, d
   const size_t smem = stages * (stage_bytes + 16);
   if (smem > kMaxCta) return false;
   static const bool configured = [] {
-    FLZ_CUDA(cudaFuncSetAttribute(clenshaw_step_stencil_tma<R, MODE>,
+    FLZ_CUDA(cudaFuncSetAttribute(clenshaw_step_stencil_tma<R, MODE, false>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxCta));
+    FLZ_CUDA(cudaFuncSetAttribute(clenshaw_step_stencil_tma<R, MODE, true>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxCta));
     return true;
   }();
   (void)configured;
-  const int64_t ntiles = (A.nslices + T / 32 - 1) / (T / 32);
+  // tile_phase 0: every tile; 1: the tiles that stage local rows only; 2: the others (row
+  // slabs: the halo rows have arrived)
+  const int64_t all = (A.tile_slices + T / 32 - 1) / (T / 32);
+  int64_t ntiles = all, tile_lo = 0, hole_lo = all, hole_len = 0;
+  if (A.tile_phase == 1) {
+    tile_lo = G.tile_a;
+    ntiles = G.tile_b - G.tile_a;
+  } else if (A.tile_phase == 2) {
+    hole_lo = G.tile_a;
+    hole_len = G.tile_b - G.tile_a;
+    ntiles = all - hole_len;
+  }
+  if (ntiles <= 0) return true;
+  // row slabs: the two phases of a step are chained by programmatic dependent launch as the
+  // steps of a single-rank run are (the pack kernel in between has no early trigger, the
+  // event waits of the stream serialise as usual)
+  static const int slab_pdl = env_int("FLZ_SLAB_PDL", 1);
+  ctx->k1_pdl_once = A.tile_phase != 0 && slab_pdl != 0;
   const unsigned grid = (unsigned)std::min<int64_t>(ntiles, (int64_t)sms * ctas);
-  launch_k1_smem(ctx, clenshaw_step_stencil_tma<R, MODE>, grid, (unsigned)(T + 32 * nprod), smem, A, G,
-                 A.uv_pairs, A.nl, ntiles, stages, nprod, l2hint, y_rows, x_rows, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo);
+  // the halo-aware instantiation only where a tile can stage halo rows
+  const bool slab = (G.front > 0 || G.back > 0) && A.tile_phase != 1;
+  if (slab)
+    launch_k1_smem(ctx, clenshaw_step_stencil_tma<R, MODE, true>, grid, (unsigned)(T + 32 * nprod), smem,
+                   A, G, A.uv_pairs, A.nl, ntiles, tile_lo, hole_lo, hole_len, stages, nprod, l2hint,
+                   y_rows, x_rows, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo);
+  else
+    launch_k1_smem(ctx, clenshaw_step_stencil_tma<R, MODE, false>, grid, (unsigned)(T + 32 * nprod), smem,
+                   A, G, A.uv_pairs, A.nl, ntiles, tile_lo, hole_lo, hole_len, stages, nprod, l2hint,
+                   y_rows, x_rows, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo);
   return true;
 }
 
@@ -1821,7 +1885,19 @@ void launch_pack_rows(flz_ctx* ctx, cudaStream_t stream, int64_t count, int R, i
   if (count == 0) return;
   const unsigned grid = (unsigned)((count + 255) / 256);
   switch (S) {
-    case 0: pack_rows_planar_kernel<<<grid, 256, 0, stream>>>(count, R, rows, Y1, ldy, buf); break;
+    case 0: {
+      // planar halo rows belong to the tile kernel's steps: same shared-memory carve-out, so
+      // that the SMs are not reconfigured twice per step
+      static const bool configured = [] {
+        if (env_int("FLZ_PACK_CARVEOUT", 1))
+          FLZ_CUDA(cudaFuncSetAttribute(pack_rows_planar_kernel,
+                                        cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        return true;
+      }();
+      (void)configured;
+      pack_rows_planar_kernel<<<grid, 256, 0, stream>>>(count, R, rows, Y1, ldy, buf);
+      break;
+    }
     case 1: pack_rows_kernel<1><<<grid, 256, 0, stream>>>(count, rows, Y1, buf); break;
     case 2: pack_rows_kernel<2><<<grid, 256, 0, stream>>>(count, rows, Y1, buf); break;
     case 3: pack_rows_kernel<3><<<grid, 256, 0, stream>>>(count, rows, Y1, buf); break;

@@ -256,34 +256,55 @@ class HaloPlan:
         pairs = np.zeros(int(info[28]), np.float64)
         check(lib().flz_plan_tiles(self.handle, vp(info), vp(pairs)))
         ns = int(info[1])
+        slab = np.zeros(4, np.int64)
+        check(lib().flz_plan_tile_slab(self.handle, vp(slab)))
         return dict(tile_rows=int(info[0]), nseg=ns, seg_base=info[2:2 + ns].copy(),
                     seg_len=info[10:10 + ns].copy(), seg_start=info[18:18 + ns].copy(),
-                    y1_elems=int(info[26]), own_e=int(info[27]), pairs=pairs)
+                    y1_elems=int(info[26]), own_e=int(info[27]), pairs=pairs,
+                    front=int(slab[0]), back=int(slab[1]), tile_a=int(slab[2]),
+                    tile_b=int(slab[3]))
 
-    def tile_product(self, x, y_rows=None):
+    def tile_product(self, x, y_rows=None, x_halo=None, phase=0, poison_halo=False):
         """y = A x evaluated tile by tile as clenshaw_step_stencil_tma does: the runs of x a
         tile's segments reach are staged (clipped to [0, y_rows), zero filled), every position
-        reads staged element + row-in-tile, masked by its lane bit."""
+        reads staged element + row-in-tile, masked by its lane bit.  Row slabs: x_halo holds the
+        halo rows in slot order; the runs are pieces of the stored source [local | halo] that
+        make up the virtual source [front halo | local | back halo].  phase 1 / 2: only the
+        tiles that stage local rows / the others (rows of the other tiles stay NaN);
+        poison_halo: the halo rows are NaN (phase 1 must not read them)."""
         G = self.tile_plan()
         u = self.ug_arrays()
         nl = self.info["rows_local"]
         T = G["tile_rows"]
-        y_rows = y_rows or (nl + 31) // 32 * 32
+        nh = 0 if x_halo is None else len(x_halo)
+        front = G["front"]
+        assert front + G["back"] == nh
+        y_rows = y_rows or (nl + nh + 31) // 32 * 32
         xs = np.zeros(y_rows)
         xs[:nl] = x
+        if nh:
+            xs[nl:nl + nh] = np.nan if poison_halo else x_halo
+        lo, split, hi = -front, (nl if front > 0 else y_rows), y_rows - front
         words = G["pairs"].view(np.uint64)
         ntiles = len(G["pairs"]) // 16 // (T // 32)
-        y = np.zeros(ntiles * T)
+        y = np.full(ntiles * T, np.nan)
         lanes = np.arange(32)
         for t in range(ntiles):
+            inner = G["tile_a"] <= t < G["tile_b"]
+            if (phase == 1 and not inner) or (phase == 2 and inner):
+                continue
             r0 = t * T
             stage = np.full(G["y1_elems"], np.nan)     # unfilled elements must never be read
             for j in range(G["nseg"]):
                 g0 = r0 + int(G["seg_base"][j]); g1 = g0 + int(G["seg_len"][j])
-                a0, a1 = max(g0, 0), min(g1, y_rows)
                 seg = np.zeros(g1 - g0)
-                if a1 > a0:
-                    seg[a0 - g0:a1 - g0] = xs[a0:a1]
+                pieces = [(max(g0, 0), min(g1, split), 0),               # local rows
+                          (max(g0, lo), min(g1, 0), split - lo),         # front halo rows
+                          (max(g0, split), min(g1, hi), front)]          # back halo rows
+                for a0, a1, shift in pieces:
+                    if a1 > a0:
+                        assert a0 % 2 == 0 and a1 % 2 == 0 and (a0 + shift) % 2 == 0
+                        seg[a0 - g0:a1 - g0] = xs[a0 + shift:a1 + shift]
                 assert g0 % 2 == 0 and len(seg) % 2 == 0 and int(G["seg_start"][j]) % 2 == 0
                 stage[int(G["seg_start"][j]):int(G["seg_start"][j]) + len(seg)] = seg
             for w in range(T // 32):
@@ -307,7 +328,7 @@ class HaloPlan:
                     lane_rows = val_ptr + (2 * nuv + 15) // 16 * 16
                     rows = s * 32 + lanes
                     for p in range(nuv, nu):
-                        c = np.clip(rows + int(d[8 + p]), 0, nl - 1)
+                        c = np.clip(rows + int(d[8 + p]), 0, nl + nh - 1)
                         q = lane_rows + (p - nuv) * 32
                         acc += u["val"][q: q + 32] * xs[c]
                     for q in range(ng):

@@ -18,7 +18,7 @@ def run(code, env_extra, args=()):
     for k in ("FLZ_SPLIT", "FLZ_K1_LAYOUT", "FLZ_SYNC_CHECK", "FLZ_K1_PDL", "FLZ_P2_DENSE",
               "FLZ_ST_TILE", "FLZ_ST_STAGES", "FLZ_ST_CTAS",
               "FLZ_ST_PRODUCERS", "FLZ_HY", "FLZ_HY_OVERLAP", "FLZ_SPECULATE", "FLZ_ORTH_FUSED",
-              "FLZ_TS_UPDATE", "FLZ_PLAN_AHEAD"):
+              "FLZ_TS_UPDATE", "FLZ_PLAN_AHEAD", "FLZ_ST_SLAB"):
         env.pop(k, None)
     env.update(env_extra)
     p = subprocess.run([sys.executable, "-c", code, *args], env=env, capture_output=True,
@@ -129,6 +129,80 @@ def test_tile_kernel_bit_identical_to_warp_kernel():
                 {"FLZ_ST_TILE": "32", "FLZ_ST_STAGES": "2", "FLZ_K1_LAYOUT": "planar"},
                 {"FLZ_ST_TILE": "256", "FLZ_ST_STAGES": "5", "FLZ_ST_CTAS": "1", "FLZ_K1_LAYOUT": "planar"}):
         assert run(TILE_CODE, env) == warp, env
+
+
+SLAB_CODE = r'''
+import sys, json, hashlib, threading
+sys.path.insert(0, %r)
+import numpy as np
+from paper_2409_15053_b200 import Context, DeviceMatrix, LoopHub, matrices as M, solver as S
+out = {}
+cf = S.indicator_coefficients(-0.3, 0.25, 24)
+for name, gen, nranks in (("lap3d24x3", lambda: M.laplacian3d(24), 3),
+                          ("lap3d32x2", lambda: M.laplacian3d(32), 2),
+                          ("lap3d16x8", lambda: M.laplacian3d(16), 8),
+                          ("lap3d12x3", lambda: M.laplacian3d(12), 3),      # slices across planes
+                          ("lap2d96x4", lambda: M.laplacian2d(96), 4),
+                          ("lap3d40x2", lambda: M.laplacian3d(40), 2)):
+    n, rp, ci, va = gen()
+    starts = [n * k // nranks // 2 * 2 for k in range(nranks + 1)]
+    hub = LoopHub(nranks)
+    res, err = [None] * nranks, [None] * nranks
+    def work(rank):
+        try:
+            ctx = Context.loopback(hub, rank)
+            b, e = starts[rank], starts[rank + 1]
+            A = DeviceMatrix(ctx, n, rp[b:e + 1] - rp[b], ci[rp[b]:rp[e]], va[rp[b]:rp[e]],
+                             row_begin=b, row_end=e)
+            got = {"kernel": A.k1_info(3)["kernel"]}
+            for r in (1, 3, 4):
+                X = np.random.default_rng(r).standard_normal((n, r))
+                Y = A.filter_apply(cf, 4.0, 4.5, X[b:e])
+                Z = A.spmm(X[b:e], counted=False)
+                got[r] = (Y, Z)
+            ctx.sync()
+            res[rank] = got
+        except BaseException as ex:
+            err[rank] = ex
+    th = [threading.Thread(target=work, args=(k,)) for k in range(nranks)]
+    [t.start() for t in th]
+    [t.join(timeout=300) for t in th]
+    assert not any(t.is_alive() for t in th), "a rank hangs"
+    for ex in err:
+        if ex is not None:
+            raise ex
+    out[name + "_kernel"] = sorted(set(p["kernel"] for p in res))
+    ctx0 = Context(0)
+    A0 = DeviceMatrix(ctx0, n, rp, ci, va)
+    for r in (1, 3, 4):
+        Y = np.vstack([p[r][0] for p in res]); Z = np.vstack([p[r][1] for p in res])
+        X = np.random.default_rng(r).standard_normal((n, r))
+        Y0 = A0.filter_apply(cf, 4.0, 4.5, X); Z0 = A0.spmm(X, counted=False)
+        out["%%s_r%%d" %% (name, r)] = [hashlib.sha1(np.ascontiguousarray(Y).tobytes()).hexdigest(),
+                                      hashlib.sha1(np.ascontiguousarray(Z).tobytes()).hexdigest()]
+        out["%%s_r%%d_dev" %% (name, r)] = max(float(np.abs(Y - Y0).max() / np.abs(Y0).max()),
+                                             float(np.abs(Z - Z0).max() / np.abs(Z0).max()))
+print(json.dumps(out))
+''' % ROOT
+
+
+def test_tile_kernel_on_row_slabs_bit_identical_to_warp_kernel():
+    """Row slabs through the loopback transport: the TMA-staged tile kernel (runs of the
+    virtual source [front halo | local | back halo], tiles without halo rows launched while
+    the halo travels) against the one-warp-per-slice kernel on the same slabs — same order of
+    additions, bit-identical filter outputs and products; both within 1e-13 of one context."""
+    tile = run(SLAB_CODE, {})
+    warp = run(SLAB_CODE, {"FLZ_ST_SLAB": "0"})
+    small = run(SLAB_CODE, {"FLZ_ST_TILE": "64", "FLZ_ST_STAGES": "2"})
+    for k, v in tile.items():
+        if k.endswith("_kernel"):
+            assert v == ["clenshaw_step_stencil_tma"], (k, v)
+            assert warp[k] == ["clenshaw_step_ug_warp"], (k, warp[k])
+        elif k.endswith("_dev"):
+            assert v <= 1e-13 and warp[k] <= 1e-13, (k, v, warp[k])
+        else:
+            assert v == warp[k], k
+            assert v == small[k], k
 
 
 HY_CODE = r'''

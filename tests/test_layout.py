@@ -387,12 +387,71 @@ def test_stencil_tile_plan_reproduces_product(monkeypatch, gen, tile):
 
 
 def test_stencil_tile_plan_absent_where_it_does_not_apply(monkeypatch):
-    """No tile plan for ragged matrices, for row-partitioned stencils (halo rows are not
-    contiguous runs) or when switched off."""
+    """No tile plan for ragged matrices, for row slabs with an odd number of rows (16-byte
+    bulk copies) or when switched off."""
     n, rp, ci, va = M.parsec_like(radius=10.0, n_atoms=8)
     assert HaloPlan(n, 0, 1, uniform_starts(n, 1), rp, ci, va).tile_plan() is None
     n, rp, ci, va = M.laplacian3d(16)
-    st = uniform_starts(n, 2)
+    st = [0, 2049, n]
     assert HaloPlan(n, 0, 2, st, rp[: st[1] + 1], ci, va).tile_plan() is None
+    monkeypatch.setenv("FLZ_ST_SLAB", "0")
+    st = uniform_starts(n, 2)
+    # (FLZ_ST_SLAB is read once per process: only checked when set before the first slab plan)
+    monkeypatch.delenv("FLZ_ST_SLAB")
     monkeypatch.setenv("FLZ_ST_TILE", "0")
     assert HaloPlan(n, 0, 1, uniform_starts(n, 1), rp, ci, va).tile_plan() is None
+    assert HaloPlan(n, 0, 2, st, rp[: st[1] + 1], ci, va).tile_plan() is None
+
+
+def slab_csr(csr, b, e):
+    n, rp, ci, va = csr
+    return rp[b:e + 1] - rp[b], ci[rp[b]:rp[e]], va[rp[b]:rp[e]]
+
+
+@pytest.mark.parametrize("tile", [32, 256])
+@pytest.mark.parametrize("case", [
+    ("lap3d z slabs", lambda: M.laplacian3d(24), 3, None),
+    ("lap3d 8 slabs", lambda: M.laplacian3d(16), 8, None),
+    ("aniso", lambda: M.laplacian3d(16, (1.0, 0.5, 0.25)), 2, None),
+    ("lap2d", lambda: M.laplacian2d(64), 4, None),
+    ("cut inside a plane", lambda: M.laplacian3d(16), 3, [0, 1400, 2900, 4096]),
+    ("slices across planes", lambda: M.laplacian3d(12), 3, None),
+], ids=lambda c: c[0])
+def test_stencil_tile_plan_on_row_slabs(monkeypatch, case, tile):
+    """Row slabs: the tile kernel stages runs of the virtual source [front halo | local | back
+    halo] (a neighbour plane from a peer sits at the offset it has inside the slab), every rank's
+    product from its plan equals its rows of A x; the tiles of phase 1 read no halo row (the
+    emulation poisons them) and the two phases together cover every row once."""
+    monkeypatch.setenv("FLZ_ST_TILE", str(tile))
+    _, gen, nranks, starts = case
+    csr = gen()
+    n, rp, ci, va = csr
+    starts = starts or [n * k // nranks for k in range(nranks + 1)]
+    x = np.random.default_rng(7).standard_normal(n)
+    want = reference(csr, x)
+    for rank in range(nranks):
+        b, e = starts[rank], starts[rank + 1]
+        lrp, lci, lva = slab_csr(csr, b, e)
+        P = HaloPlan(n, rank, nranks, starts, lrp, lci, lva)
+        G = P.tile_plan()
+        assert G is not None, f"rank {rank} has no tile plan"
+        need = np.concatenate([P.need(p) for p in range(nranks)]).astype(np.int64)
+        assert G["front"] == int((need < b).sum()) and G["back"] == int((need >= e).sum())
+        assert G["front"] + G["back"] == len(need) > 0
+        single = HaloPlan(n, 0, 1, [0, n], rp, ci, va).tile_plan()
+        if case[0] in ("lap3d z slabs", "lap3d 8 slabs", "aniso", "lap2d"):
+            # whole planes per rank: the offsets (and segments) of the single-rank plan
+            assert G["nseg"] == single["nseg"] and list(G["seg_base"]) == list(single["seg_base"])
+        y = P.tile_product(x[b:e], x_halo=x[need])
+        assert np.abs(y - want[b:e]).max() <= 1e-13 * np.abs(want).max()
+        y1 = P.tile_product(x[b:e], x_halo=x[need], phase=1, poison_halo=True)
+        y2 = P.tile_product(x[b:e], x_halo=x[need], phase=2)
+        inner = ~np.isnan(y1)
+        assert not np.isnan(y1[inner]).any() and np.isnan(y2[inner]).all()
+        assert not np.isnan(y2[~inner]).any()
+        assert np.array_equal(np.where(inner, y1, y2), y)
+        T = G["tile_rows"]
+        assert inner.sum() == max(0, min(e - b, G["tile_b"] * T) - G["tile_a"] * T)
+        # every slice that touches a halo row lies outside the phase-1 tiles
+        bnd = P.arrays()["boundary"]
+        assert all(not (G["tile_a"] <= s // (T // 32) < G["tile_b"]) for s in bnd)
