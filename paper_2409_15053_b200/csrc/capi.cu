@@ -128,7 +128,7 @@ SellView make_view(const flz_matrix* A, const SliceTask* tasks, int64_t ntasks,
                   // the tile kernel covers whole-matrix launches (and, on row slabs, its own
                   // split into tiles without and with halo rows: tiled(), below)
                   (slice_ids == nullptr && nslices == A->nslices) ? A->tiles : StencilTiles{},
-                  A->hy ? A->sell_rows.p : nullptr, A->nslices, 0};
+                  A->hy ? A->sell_rows.p : nullptr, nullptr, nullptr, 0, A->nslices, 0};
 }
 // Row slabs with a tile plan: the interior / boundary launch as a phase of the tile kernel
 // (the slice lists stay in place for the one-warp-per-slice kernel it falls back to).
@@ -136,6 +136,11 @@ SellView tiled(const flz_matrix* A, SellView v, int phase) {
   if (A->tiles.nseg > 0 && !A->ctx->exact) {
     v.tiles = A->tiles;
     v.tile_phase = phase;
+    if (phase == 2 && A->send_slots.count > 0) {
+      v.send_slots = A->send_slots.p;
+      v.send_buf = A->send_buf.p;
+      v.n_send = A->n_send;
+    }
   }
   return v;
 }
@@ -207,7 +212,10 @@ void ensure_workspaces(const flz_matrix* A) {
 void halo_begin(const flz_matrix* A, int R, int S, double* Y1) {
   flz_ctx* ctx = A->ctx;
   const int64_t ldy = planar_ld(A);
-  launch_pack_rows(ctx, ctx->stream, A->n_send, R, S, ldy, A->send_rows.p, Y1, A->send_buf.p);
+  // (the tile kernel's last phase-2 launch may have left Y1's halo rows in send_buf already)
+  if (A->packed_from != Y1)
+    launch_pack_rows(ctx, ctx->stream, A->n_send, R, S, ldy, A->send_rows.p, Y1, A->send_buf.p);
+  A->packed_from = nullptr;
   FLZ_CUDA(cudaEventRecord(ctx->ev_halo_ready, ctx->stream));
   FLZ_CUDA(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_halo_ready, 0));
   constexpr size_t D = sizeof(double);
@@ -283,8 +291,13 @@ void sell_step(const flz_matrix* A, int R, int S, StepMode mode, double s1, doub
                        ldy, X, ldx, Out, ldo);
   FLZ_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_halo_done, 0));
   rest(2, A->nt_rest_boundary);
-  launch_clenshaw_step(ctx, tiled(A, view_boundary(A), 2), R, S, mode, ctx->exact, s1, s2, b, Y1, Y2,
-                       ldy, X, ldx, Out, ldo);
+  const SellView vb = tiled(A, view_boundary(A), 2);
+  launch_clenshaw_step(ctx, vb, R, S, mode, ctx->exact, s1, s2, b, Y1, Y2, ldy, X, ldx, Out, ldo);
+  // a Clenshaw step through the tile kernel packed the halo rows of its result on the way
+  if (mode == StepMode::step && S == 0 && vb.send_slots && vb.tiles.nseg > 0 && ctx->k1_packed) {
+    A->packed_from = Y2;
+  }
+  ctx->k1_packed = false;
 }
 
 // Layout of the filter workspaces for R fused columns (see launch_clenshaw_step):
@@ -326,6 +339,7 @@ void spmm_device(const flz_matrix* A, const double* X, int64_t ldx, int ncols, d
                  int64_t ldz, bool counted) {
   flz_ctx* ctx = A->ctx;
   ensure_workspaces(A);
+  A->packed_from = nullptr;
   for (int c0 = 0; c0 < ncols; c0 += kMaxFuse) {
     const int R = std::min(kMaxFuse, ncols - c0);
     const int S = row_stride(A, R);
@@ -358,6 +372,7 @@ void filter_device(const flz_matrix* A, const double* coeffs, int m, double c, d
     }
     double* Y1 = A->y1.p;
     double* Y2 = A->y2.p;
+    A->packed_from = nullptr;   // Y1 is rebuilt: nothing of it is packed yet
     zero_pad_rows(A, R, S, Y1);
     launch_interleave(ctx, A->nl, R, S, coeffs[m], Xc, ldx, Y1, planar_ld(A));   // :144
     FLZ_CUDA(cudaMemsetAsync(Y2, 0, (S > 0 ? (size_t)A->nl * S : (size_t)planar_ld(A) * R) *
@@ -839,6 +854,33 @@ static void upload_plan(flz_ctx* ctx, HostPlan& P, flz_matrix* A) {
   A->n_send = (int64_t)P.send_rows.size();
   up(A->send_rows, P.send_rows);
   A->send_buf.reserve(std::max<size_t>(P.send_rows.size() * kMaxFuse, 1));
+  if (P.tiles.nseg > 0 && (P.tiles.front > 0 || P.tiles.back > 0) && !P.send_rows.empty()) {
+    // fused halo pack: every send row must lie in a halo-staging tile and go to <= 2 peers
+    static const bool fused = [] {
+      const char* e = std::getenv("FLZ_SLAB_PACK");   // 0: always the pack launch
+      return !(e && e[0] == '0');
+    }();
+    const int64_t T = P.tiles.tile_rows;
+    const int64_t hole0 = (int64_t)P.tiles.tile_a * T, hole1 = (int64_t)P.tiles.tile_b * T;
+    const int64_t ntiles = (P.nslices * kPlanSliceRows + T - 1) / T;
+    const int64_t rows = ntiles * T - (hole1 - hole0);
+    std::vector<int2> slots((size_t)std::max<int64_t>(rows, 1), int2{-1, -1});
+    bool ok = fused;
+    for (size_t q = 0; ok && q < P.send_rows.size(); ++q) {
+      const int64_t r = P.send_rows[q];
+      if (r >= hole0 && r < hole1) { ok = false; break; }
+      int2& e = slots[(size_t)(r < hole0 ? r : r - (hole1 - hole0))];
+      if (e.x < 0) e.x = (int)q;
+      else if (e.y < 0) e.y = (int)q;
+      else ok = false;
+    }
+    if (ok) {
+      A->send_slots.reserve(slots.size());
+      FLZ_CUDA(cudaMemcpyAsync(A->send_slots.p, slots.data(), slots.size() * sizeof(int2),
+                               cudaMemcpyHostToDevice, ctx->stream));
+      FLZ_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
+  }
   FLZ_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 

@@ -169,6 +169,7 @@ struct flz_ctx {
   int refs = 1;                  // owner + every matrix/basis created on the context
   uint64_t launches = 0;
   int k1_slices_per_cta = 0, k1_tasks_per_cta = 0, k1_batch = 0;  // 0: defaults (tuning knobs)
+  bool k1_packed = false;     // the last tile-kernel launch packed halo rows into send_buf
   bool k1_pdl_once = false;   // the next K1 launch carries the dependent-launch attribute (row slabs)
   cudaEvent_t t0[16] = {}, t1[16] = {};
   flz::DevBuf<double> partial;   // split-K partial sums of the tall-skinny GEMMs
@@ -270,6 +271,11 @@ struct flz_matrix {
   flz::DevBuf<int32_t> send_rows;   // concatenated per-peer send lists
   int64_t n_send = 0;
   flz::DevBuf<double> send_buf;     // n_send * kMaxFuse doubles
+  // tile kernel on row slabs: send slots of the rows of the halo-staging tiles (two per row,
+  // -1: none; rows behind the hole [tile_a, tile_b) indexed minus the hole) — those tiles
+  // write their results into send_buf as well, so the next step needs no pack launch
+  flz::DevBuf<int2> send_slots;
+  mutable const double* packed_from = nullptr;   // the block whose halo rows send_buf holds
   // filter workspaces (interleaved (nl+nhalo) x R), created on first use
   mutable flz::DevBuf<double> y1, y2, xs, zs;
 };
@@ -367,6 +373,9 @@ struct SellView {
   unsigned* tickets;         // this launch's task counter (starts at 0; persistent CTAs)
   StencilTiles tiles;        // nseg > 0: tile plan of the TMA-staged stencil kernel
   const int32_t* sell_rows;  // exact-mode kernel: SELL lane -> row (nullptr: slice * 32 + lane)
+  const int2* send_slots = nullptr;   // tile kernel, phase 2 of a Clenshaw step: fused halo pack
+  double* send_buf = nullptr;
+  int64_t n_send = 0;
   int64_t tile_slices = 0;   // the tile plan covers slices [0, tile_slices) of the matrix
   int tile_phase = 0;        // 0: all tiles, 1: tiles without halo rows, 2: the rest (row slabs)
 };

@@ -1120,6 +1120,17 @@ __global__ void __launch_bounds__(768)
     if (row < nl) {
 #pragma unroll
       for (int k = 0; k < R; ++k) dst[(int64_t)k * ldd] = o[k];
+      if constexpr (SLAB && MODE == 0) {
+        // fused halo pack: the rows the peers gather from go to the send buffer as well
+        if (A.send_slots) {
+          const int2 sl = __ldg(A.send_slots + (row < hole_lo * T ? row : row - hole_len * T));
+#pragma unroll
+          for (int k = 0; k < R; ++k) {
+            if (sl.x >= 0) A.send_buf[(int64_t)k * A.n_send + sl.x] = o[k];
+            if (sl.y >= 0) A.send_buf[(int64_t)k * A.n_send + sl.y] = o[k];
+          }
+        }
+      }
     }
     if (++st == nstages) { st = 0; parity ^= 1u; }
   }
@@ -1725,6 +1736,7 @@ bool launch_stencil_tma(flz_ctx* ctx, const SellView& A, double s1, double s2, d
   const unsigned grid = (unsigned)std::min<int64_t>(ntiles, (int64_t)sms * ctas);
   // the halo-aware instantiation only where a tile can stage halo rows
   const bool slab = (G.front > 0 || G.back > 0) && A.tile_phase != 1;
+  ctx->k1_packed = slab && MODE == 0 && A.send_slots != nullptr;
   if (slab)
     launch_k1_smem(ctx, clenshaw_step_stencil_tma<R, MODE, true>, grid, (unsigned)(T + 32 * nprod), smem,
                    A, G, A.uv_pairs, A.nl, ntiles, tile_lo, hole_lo, hole_len, stages, nprod, l2hint,

@@ -18,7 +18,7 @@ def run(code, env_extra, args=()):
     for k in ("FLZ_SPLIT", "FLZ_K1_LAYOUT", "FLZ_SYNC_CHECK", "FLZ_K1_PDL", "FLZ_P2_DENSE",
               "FLZ_ST_TILE", "FLZ_ST_STAGES", "FLZ_ST_CTAS",
               "FLZ_ST_PRODUCERS", "FLZ_HY", "FLZ_HY_OVERLAP", "FLZ_SPECULATE", "FLZ_ORTH_FUSED",
-              "FLZ_TS_UPDATE", "FLZ_PLAN_AHEAD", "FLZ_ST_SLAB"):
+              "FLZ_TS_UPDATE", "FLZ_PLAN_AHEAD", "FLZ_ST_SLAB", "FLZ_SLAB_PACK", "FLZ_SLAB_PDL"):
         env.pop(k, None)
     env.update(env_extra)
     p = subprocess.run([sys.executable, "-c", code, *args], env=env, capture_output=True,
@@ -194,6 +194,7 @@ def test_tile_kernel_on_row_slabs_bit_identical_to_warp_kernel():
     tile = run(SLAB_CODE, {})
     warp = run(SLAB_CODE, {"FLZ_ST_SLAB": "0"})
     small = run(SLAB_CODE, {"FLZ_ST_TILE": "64", "FLZ_ST_STAGES": "2"})
+    plain = run(SLAB_CODE, {"FLZ_SLAB_PACK": "0", "FLZ_SLAB_PDL": "0"})   # pack launch, no PDL
     for k, v in tile.items():
         if k.endswith("_kernel"):
             assert v == ["clenshaw_step_stencil_tma"], (k, v)
@@ -203,6 +204,7 @@ def test_tile_kernel_on_row_slabs_bit_identical_to_warp_kernel():
         else:
             assert v == warp[k], k
             assert v == small[k], k
+            assert v == plain[k], k
 
 
 HY_CODE = r'''
