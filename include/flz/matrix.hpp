@@ -46,6 +46,8 @@ class Device {
   static flz_ctx* context();
   // Adopt an externally created context (e.g. a distributed one from flz_ctx_create_dist).
   static void adopt(flz_ctx* ctx);
+  // tests only: the calling thread uses `ctx` (loopback ranks are threads); nullptr: undo
+  static void adopt_thread(flz_ctx* ctx);
   static void set_device(int index);  // before first use
   static void shutdown();
   // Multi-GPU (one process per GPU): rank / size of the active context and the contiguous

@@ -57,6 +57,9 @@ void flz_config_default(flz_config* cfg); /* lanczos.hpp:14-29 defaults */
 /* The host layer runs on the process-wide default context; adopt a caller-made one
  * (e.g. a distributed context) with this call.  ctx == NULL restores the lazy default. */
 int flz_set_default_ctx(flz_ctx* ctx);
+/* TESTS ONLY: the calling THREAD's host-layer calls run on `ctx` (NULL: back to the
+ * process-wide one) — the ranks of a loopback run (flz_ctx_create_loopback) are threads. */
+int flz_set_thread_ctx(flz_ctx* ctx);
 /* The context the host layer is using (created on first use). */
 int flz_default_ctx(flz_ctx** out);
 

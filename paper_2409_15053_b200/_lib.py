@@ -132,6 +132,7 @@ _SIGS = {
 _SOLVER_SIGS = {
     "flz_config_default": (None, [C.POINTER(FlzConfig)]),
     "flz_set_default_ctx": (i32, [vp]),
+    "flz_set_thread_ctx": (i32, [vp]),
     "flz_default_ctx": (i32, [C.POINTER(vp)]),
     "flz_hostmatrix_from_triplets": (i32, [i64, i64, i64p, i64p, f64p, C.POINTER(vp)]),
     "flz_hostmatrix_from_csr": (i32, [i64, i64p, i32p, f64p, i32, C.POINTER(vp)]),

@@ -145,6 +145,10 @@ int flz_set_default_ctx(flz_ctx* ctx) {
   });
 }
 
+int flz_set_thread_ctx(flz_ctx* ctx) {
+  return wrap([&] { Device::adopt_thread(ctx); });
+}
+
 int flz_default_ctx(flz_ctx** out) {
   return wrap([&] { *out = Device::context(); });
 }

@@ -43,6 +43,7 @@ std::mutex g_dev_mutex;
 flz_ctx* g_ctx = nullptr;
 bool g_ctx_owned = false;
 int g_dev_index = -1;
+thread_local flz_ctx* t_ctx = nullptr;   // tests: per-thread override (loopback ranks)
 }  // namespace
 
 // FLZ_PLAN_AHEAD=0: the device layout is built at the first product (experiments)
@@ -54,7 +55,9 @@ static bool g_plan_ahead_off() {
   return off;
 }
 
+void Device::adopt_thread(flz_ctx* ctx) { t_ctx = ctx; }
 flz_ctx* Device::context() {
+  if (t_ctx) return t_ctx;
   std::lock_guard<std::mutex> lock(g_dev_mutex);
   if (!g_ctx) {
     throw_status(flz_ctx_create(g_dev_index, &g_ctx));

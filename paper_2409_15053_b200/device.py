@@ -82,6 +82,15 @@ class Context:
         """Make the host solver layer (filtered_lanczos & co.) run on this context."""
         check(lib().flz_set_default_ctx(self.handle))
 
+    def adopt_for_thread(self):
+        """TESTS ONLY: the calling thread's host-layer calls run on this context (the ranks of
+        a loopback run are threads of one process)."""
+        check(lib().flz_set_thread_ctx(self.handle))
+
+    @staticmethod
+    def release_thread():
+        check(lib().flz_set_thread_ctx(None))
+
     @staticmethod
     def nccl_unique_id() -> bytes:
         buf = C.create_string_buffer(128)
