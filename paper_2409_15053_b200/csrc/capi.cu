@@ -351,6 +351,31 @@ void spmm_device(const flz_matrix* A, const double* X, int64_t ldx, int ncols, d
   if (counted) g_matvecs.fetch_add((uint64_t)ncols, std::memory_order_relaxed);
 }
 
+// Several Clenshaw steps per launch (clenshaw_multistep_stencil): constant-coefficient stencils
+// on one rank with planar blocks and no per-lane positions, where a step is launch-bound
+// (rows x columns below FLZ_MS_ROWS, default 2^17; FLZ_MS=0 never, FLZ_MS=1 whenever the window
+// fits).  Allocates the second pair of workspaces on first use.
+bool multistep_applies(const flz_matrix* A, int R, int S, bool allocate = true) {
+  static const int mode = [] {
+    const char* e = std::getenv("FLZ_MS");
+    return e ? std::atoi(e) : -1;
+  }();
+  static const int64_t max_rows = [] {
+    const char* e = std::getenv("FLZ_MS_ROWS");
+    return e ? (int64_t)std::atoll(e) : ((int64_t)1 << 17);
+  }();
+  flz_ctx* ctx = A->ctx;
+  if (mode == 0 || !A->multistep || ctx->exact || S != 0 || ctx->nranks != 1) return false;
+  if (mode != 1 && A->nl * R > max_rows) return false;
+  if (!allocate) return true;
+  const size_t need = (size_t)planar_ld(A) * kMaxFuse + 8;
+  if (A->y3.count < need) {
+    A->y3.reserve_zero(need, ctx->stream);
+    A->y4.reserve_zero(need, ctx->stream);
+  }
+  return true;
+}
+
 // Z = p((A - cI)/e) X by block Clenshaw (filter.cpp:122-155), device-resident blocks.
 void filter_device(const flz_matrix* A, const double* coeffs, int m, double c, double e,
                    const double* X, int64_t ldx, int ncols, double* Z, int64_t ldz) {
@@ -377,9 +402,28 @@ void filter_device(const flz_matrix* A, const double* coeffs, int m, double c, d
     launch_interleave(ctx, A->nl, R, S, coeffs[m], Xc, ldx, Y1, planar_ld(A));   // :144
     FLZ_CUDA(cudaMemsetAsync(Y2, 0, (S > 0 ? (size_t)A->nl * S : (size_t)planar_ld(A) * R) *
                                             sizeof(double), ctx->stream));
-    for (int j = m - 1; j >= 1; --j) {                                          // :146-151
+    // short-reach stencils: several steps per launch while at least two are left (the state
+    // after K steps is (y_K, y_{K-1}) in the second pair of workspaces)
+    const bool multi = multistep_applies(A, R, S);
+    double* O1 = multi ? A->y3.p : nullptr;
+    double* O2 = multi ? A->y4.p : nullptr;
+    for (int j = m - 1; j >= 1;) {                                              // :146-151
+      if (multi && j >= 2) {
+        double bs[8];
+        const int avail = std::min(8, j);
+        for (int q = 0; q < avail; ++q) bs[q] = coeffs[j - q];
+        const int done = launch_multistep(ctx, view_all(A), R, avail, bs, s1, s2, Y1, Y2,
+                                          planar_ld(A), Xc, ldx, O1, O2);
+        if (done > 0) {
+          std::swap(Y1, O1);
+          std::swap(Y2, O2);
+          j -= done;
+          continue;
+        }
+      }
       sell_step(A, R, S, StepMode::step, s1, s2, coeffs[j], Y1, Y2, Xc, ldx, nullptr, 0);
       std::swap(Y1, Y2);
+      --j;
     }
     sell_step(A, R, S, StepMode::final, f1, f2, coeffs[0], Y1, Y2, Xc, ldx, Zc, ldz);  // :152-154
     g_matvecs.fetch_add((uint64_t)R * (uint64_t)m, std::memory_order_relaxed);
@@ -757,6 +801,13 @@ static void upload_plan(flz_ctx* ctx, HostPlan& P, flz_matrix* A) {
   up(A->uv_pairs, P.uv_pairs);
   static_assert(sizeof(PlanStencilTiles) == sizeof(StencilTiles), "PlanStencilTiles mirrors StencilTiles");
   std::memcpy(static_cast<void*>(&A->tiles), &P.tiles, sizeof(StencilTiles));
+  // multi-step launches: every position of every slice must be a (value, mask) pair
+  A->multistep = P.tiles.nseg > 0 && P.nranks == 1 && P.halo.empty();
+  for (size_t sl = 0; A->multistep && sl * 16 + 1 < P.uv_pairs.size(); ++sl) {
+    uint64_t bits;
+    std::memcpy(&bits, &P.uv_pairs[sl * 16 + 1], 8);
+    if ((bits >> 56) & 1) A->multistep = false;
+  }
   A->p2 = P.p2;
   if (P.p2) {
     static_assert(sizeof(PlanP2Slice) == sizeof(P2Slice), "PlanP2Slice mirrors P2Slice");
@@ -1275,7 +1326,11 @@ int flz_matrix_k1_info(const flz_matrix* A, int r, int64_t* info, char* kernel, 
     matrix_bytes = A->p2_bytes;
   } else if (A->short_rows && A->lean) {
     const bool tile = A->tiles.nseg > 0 && (S == 0 || (S == 1 && r == 1));
-    name = tile ? "clenshaw_step_stencil_tma" : "clenshaw_step_ug_warp";
+    name = tile ? (multistep_applies(A, r, S, false)
+                       ? "clenshaw_multistep_stencil (several Clenshaw steps per launch) + "
+                         "clenshaw_step_stencil_tma"
+                       : "clenshaw_step_stencil_tma")
+                : "clenshaw_step_ug_warp";
     matrix_bytes = tile ? (int64_t)A->uv_pairs.count * 8 : A->ug_bytes;
   } else {
     name = "clenshaw_step_ug_tasks";

@@ -278,6 +278,8 @@ struct flz_matrix {
   mutable const double* packed_from = nullptr;   // the block whose halo rows send_buf holds
   // filter workspaces (interleaved (nl+nhalo) x R), created on first use
   mutable flz::DevBuf<double> y1, y2, xs, zs;
+  mutable flz::DevBuf<double> y3, y4;   // second pair of filter workspaces (multi-step launches)
+  bool multistep = false;               // short-reach stencil without per-lane positions
 };
 
 // ------------------------------------------------------------------ basis
@@ -421,6 +423,10 @@ void launch_hybrid_step(flz_ctx* ctx, const HyView& A, int R, StepMode mode, dou
                         double b, const double* Y1, double* Y2, int64_t ldy, const double* X,
                         int64_t ldx, double* Out, int64_t ldo, int phase = 0);
 // Y1 = scale * X  (column-major -> interleaved with row stride S >= R, or planar for S == 0)
+// several Clenshaw steps of a short-reach stencil in one launch (0: not applicable)
+int launch_multistep(flz_ctx* ctx, const SellView& A, int R, int max_steps, const double* b,
+                     double s1, double s2, const double* Y1, const double* Y2, int64_t ldy,
+                     const double* X, int64_t ldx, double* O1, double* O2);
 void launch_interleave(flz_ctx* ctx, int64_t nl, int R, int S, double scale, const double* X,
                        int64_t ldx, double* Y1, int64_t ldy);
 // halo packing: buf[s*S+k] = Y1[rows[s]*S+k]; planar (S == 0): buf[k*count+s] = Y1[k*ldy+rows[s]]

@@ -1137,6 +1137,125 @@ __global__ void __launch_bounds__(768)
 }
 
 
+// ------------------------------------------------ several Clenshaw steps per launch (stencils)
+// Temporal blocking for stencils with a short reach (2-D grids: reach = one grid line).  A CTA
+// owns `core` consecutive rows and loads the window [r0 - K*reach, r0 + core + K*reach) of Y1,
+// Y2 and X into shared memory; step s of the launch updates the rows that are still s*reach
+// inside the window (their neighbours were updated by step s-1 in this CTA), so after K steps
+// the core rows hold the state a sequence of K one-step launches would have produced — the halo
+// rows are recomputed by the neighbouring CTAs.  The recurrence state after K steps is two
+// blocks (y_K, y_{K-1}); they go to O1 / O2 (not in place: other CTAs still read the old
+// state of these rows as their halo).  Positions are added in the order of
+// clenshaw_step_stencil_tma (same masked values, same fma chain, same combine): bit-identical
+// to K launches of it.  One launch replaces K dependent launches where a step is launch-bound
+// (200 x 200 grid: 2.9 us per launch) and divides the DRAM traffic of a step by ~K where it
+// is bandwidth-bound.
+struct StepCoeffs {
+  double b[8];
+};
+template <int R>
+__global__ void __launch_bounds__(1024)
+    clenshaw_multistep_stencil(const __grid_constant__ StencilTiles G,
+                               const double* __restrict__ pairs, int64_t nl, int64_t npair_slices,
+                               int core, int reach, int K, const __grid_constant__ StepCoeffs cf,
+                               double s1, double s2, const double* __restrict__ Y1,
+                               const double* __restrict__ Y2, int64_t ldy,
+                               const double* __restrict__ X, int64_t ldx, double* __restrict__ O1,
+                               double* __restrict__ O2) {
+  extern __shared__ __align__(16) unsigned char ms_smem[];
+  const int W = core + 2 * K * reach;            // window rows (multiple of 32)
+  const int nq = W >> 5;                         // slices of the window
+  double* ybuf = reinterpret_cast<double*>(ms_smem);          // [3][R][W]
+  double* xs = ybuf + 3 * R * W;                              // [R][W]
+  // per slice and position: (value, lane mask | row offset << 32) — one 16-byte broadcast load
+  double2* prs = reinterpret_cast<double2*>(xs + R * W);      // [nq][8]
+  int* pnuv = reinterpret_cast<int*>(prs + nq * 8);           // [nq]
+  const int64_t w0 = (int64_t)blockIdx.x * core - (int64_t)K * reach;   // first row of the window
+  pdl_launch_dependents();
+  // the slices' (value, mask, offset) triples: immutable, read before the dependency wait
+  for (int e = threadIdx.x; e < nq * 8; e += blockDim.x) {
+    const int q = e >> 3, p = e & 7;
+    const int64_t sl = (w0 >> 5) + q;
+    double v = 0.0;
+    unsigned mask = 0;
+    int off = 0, nuv = 0;
+    if (sl >= 0 && sl < npair_slices) {
+      const double2 pr = __ldg(reinterpret_cast<const double2*>(pairs + sl * 16) + p);
+      const unsigned hi = (unsigned)__double2hiint(pr.y);
+      const int elem = (int)((hi & 0xfffffu) >> 3);          // staged element of the tile kernel
+      v = pr.x;
+      mask = (unsigned)__double2loint(pr.y);
+      nuv = (int)((hi >> 20) & 0xf);
+      off = G.seg_base[0] + elem;                            // ... back to a row offset
+      for (int j = 1; j < G.nseg; ++j)
+        if (elem >= G.seg_start[j]) off = G.seg_base[j] + (elem - G.seg_start[j]);
+    }
+    prs[e] = make_double2(v, __hiloint2double(off, (int)mask));
+    if (p == 0) pnuv[q] = nuv;
+  }
+  pdl_wait();
+  for (int i = threadIdx.x; i < W; i += blockDim.x) {
+    const int64_t row = w0 + i;
+    const bool in = row >= 0 && row < nl;
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      ybuf[(0 * R + k) * W + i] = in ? Y2[(int64_t)k * ldy + row] : 0.0;   // y_{j+1}
+      ybuf[(1 * R + k) * W + i] = in ? Y1[(int64_t)k * ldy + row] : 0.0;   // y_j
+      ybuf[(2 * R + k) * W + i] = 0.0;
+      xs[k * W + i] = in ? X[(int64_t)k * ldx + row] : 0.0;
+    }
+  }
+  __syncthreads();
+  int prev = 0, cur = 1, next = 2;
+  for (int s = 1; s <= K; ++s) {
+    const double b = cf.b[s - 1];
+    const double* yc = ybuf + cur * R * W;
+    const double* yp = ybuf + prev * R * W;
+    double* yn = ybuf + next * R * W;
+    for (int i = s * reach + threadIdx.x; i < W - s * reach; i += blockDim.x) {
+      const int64_t row = w0 + i;
+      if (row < 0 || row >= nl) {
+#pragma unroll
+        for (int k = 0; k < R; ++k) yn[k * W + i] = 0.0;
+        continue;
+      }
+      const int q = i >> 5;
+      const unsigned lanebit = 1u << (i & 31);
+      const int nuv = pnuv[q];
+      double acc[R];
+#pragma unroll
+      for (int k = 0; k < R; ++k) acc[k] = 0.0;
+      auto position = [&](int p) {
+        const double2 pr = prs[q * 8 + p];
+        const double v = ((unsigned)__double2loint(pr.y) & lanebit) ? pr.x : 0.0;
+        const int at = i + __double2hiint(pr.y);
+#pragma unroll
+        for (int k = 0; k < R; ++k) acc[k] = fma(v, yc[k * W + at], acc[k]);
+      };
+      position(0); position(1); position(2); position(3);
+      if (nuv > 4) { position(4); position(5); }
+      if (nuv > 6) { position(6); position(7); }
+#pragma unroll
+      for (int k = 0; k < R; ++k)
+        yn[k * W + i] = combine<false>(s1, acc[k], s2, yc[k * W + i], yp[k * W + i], b, xs[k * W + i]);
+    }
+    __syncthreads();
+    const int t = prev;
+    prev = cur;
+    cur = next;
+    next = t;
+  }
+  for (int i = K * reach + threadIdx.x; i < K * reach + core; i += blockDim.x) {
+    const int64_t row = w0 + i;
+    if (row >= nl) break;
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      O1[(int64_t)k * ldy + row] = ybuf[(cur * R + k) * W + i];
+      O2[(int64_t)k * ldy + row] = ybuf[(prev * R + k) * W + i];
+    }
+  }
+}
+
 template <int R, int S>
 __global__ void interleave_kernel(int64_t nl, double scale, const double* __restrict__ X,
                                   int64_t ldx, double* __restrict__ Y1, int64_t ldy) {
@@ -1872,6 +1991,73 @@ void launch_hybrid_step(flz_ctx* ctx, const HyView& A, int R, StepMode mode, dou
     default: throw ApiError(FLZ_EINVAL, "hybrid step: unsupported column count");
   }
   FLZ_CUDA(cudaGetLastError());
+}
+
+// K Clenshaw steps (StepMode::step, coefficients b[0..K)) of a short-reach stencil in one
+// launch; planar blocks.  0: not applicable (the caller runs single steps); else the number
+// of steps done.  Geometry: reach = the largest |offset| rounded up to 32 rows, K steps, core
+// rows per CTA such that the window fits the shared memory and the grid is about one CTA per
+// SM (FLZ_MS_K, FLZ_MS_CORE override).  Measured on B200, 200 x 200 grid, us per step of a
+// degree-50 filter application (one launch per step: 4.07 with one column, 4.0 with three):
+// K = 3, core = K * reach: 2.08 (K = 2: 2.22-2.42, K = 4: 2.14, K = 6: 3.6; core = 2 K reach:
+// 2.5; K = 6 / 8 with small cores: 1.98-2.3 — the fixed cost of an application, ~1.2 us per
+// step at degree 50, is in all of these); three columns: K = 3, core = 2 * reach 2.84
+// (K = 2: 3.04, core = 3 * reach: 3.29).
+template <int R>
+int launch_multistep_r(flz_ctx* ctx, const SellView& A, int max_steps, const double* b, double s1,
+                       double s2, const double* Y1, const double* Y2, int64_t ldy, const double* X,
+                       int64_t ldx, double* O1, double* O2) {
+  const StencilTiles& G = A.tiles;
+  static const int forced_k = std::clamp(env_int("FLZ_MS_K", 0), 0, 8);
+  const int want_k = forced_k > 0 ? forced_k : 3;
+  static const int want_core = env_int("FLZ_MS_CORE", 0);
+  if (G.nseg == 0 || want_k < 2 || max_steps < 2) return 0;
+  const int lo = -G.seg_base[0];
+  const int hi = G.seg_base[G.nseg - 1] + G.seg_len[G.nseg - 1] - G.tile_rows;
+  const int reach = (std::max(lo, hi) + 31) / 32 * 32;
+  if (reach <= 0) return 0;
+  const int K = std::min(want_k, max_steps);
+  constexpr size_t kMaxCta = 227 * 1024;
+  auto smem_for = [&](int core) {
+    const size_t W = (size_t)core + 2 * (size_t)K * reach, nq = W / 32;
+    return 8 * (4 * (size_t)R * W) + 16 * (nq * 8) + 4 * nq + 64;
+  };
+  // as many core rows as halo rows on one side (the window is 3x the core), more when the
+  // matrix has more rows than that per SM
+  int core = want_core > 0 ? (want_core + 31) / 32 * 32
+                           : (int)std::max<int64_t>((int64_t)(R == 1 ? K : 2) * reach,
+                                                    ((A.nl + ctx->sm_count - 1) / ctx->sm_count + 31) / 32 * 32);
+  while (core > 32 && smem_for(core) > kMaxCta) core -= 32;
+  if (smem_for(core) > kMaxCta || (want_core <= 0 && core < 2 * reach)) return 0;   // halo would dominate
+  static const bool configured = [] {
+    FLZ_CUDA(cudaFuncSetAttribute(clenshaw_multistep_stencil<R>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxCta));
+    return true;
+  }();
+  (void)configured;
+  StepCoeffs cf{};
+  for (int s = 0; s < K; ++s) cf.b[s] = b[s];
+  const unsigned grid = (unsigned)((A.nl + core - 1) / core);
+  const int64_t npair_slices = (A.tile_slices + G.tile_rows / 32 - 1) / (G.tile_rows / 32) * (G.tile_rows / 32);
+  launch_k1_smem(ctx, clenshaw_multistep_stencil<R>, grid, 1024u, smem_for(core), G, A.uv_pairs, A.nl,
+                 npair_slices, core, reach, K, cf, s1, s2, Y1, Y2, ldy, X, ldx, O1, O2);
+  ctx->launches++;
+  return K;
+}
+
+int launch_multistep(flz_ctx* ctx, const SellView& A, int R, int max_steps, const double* b,
+                     double s1, double s2, const double* Y1, const double* Y2, int64_t ldy,
+                     const double* X, int64_t ldx, double* O1, double* O2) {
+  int done = 0;
+  switch (R) {
+    case 1: done = launch_multistep_r<1>(ctx, A, max_steps, b, s1, s2, Y1, Y2, ldy, X, ldx, O1, O2); break;
+    case 2: done = launch_multistep_r<2>(ctx, A, max_steps, b, s1, s2, Y1, Y2, ldy, X, ldx, O1, O2); break;
+    case 3: done = launch_multistep_r<3>(ctx, A, max_steps, b, s1, s2, Y1, Y2, ldy, X, ldx, O1, O2); break;
+    case 4: done = launch_multistep_r<4>(ctx, A, max_steps, b, s1, s2, Y1, Y2, ldy, X, ldx, O1, O2); break;
+    default: break;
+  }
+  if (done) FLZ_CUDA(cudaGetLastError());
+  return done;
 }
 
 void launch_interleave(flz_ctx* ctx, int64_t nl, int R, int S, double scale, const double* X,

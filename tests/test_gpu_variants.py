@@ -18,7 +18,8 @@ def run(code, env_extra, args=()):
     for k in ("FLZ_SPLIT", "FLZ_K1_LAYOUT", "FLZ_SYNC_CHECK", "FLZ_K1_PDL", "FLZ_P2_DENSE",
               "FLZ_ST_TILE", "FLZ_ST_STAGES", "FLZ_ST_CTAS",
               "FLZ_ST_PRODUCERS", "FLZ_HY", "FLZ_HY_OVERLAP", "FLZ_SPECULATE", "FLZ_ORTH_FUSED",
-              "FLZ_TS_UPDATE", "FLZ_PLAN_AHEAD", "FLZ_ST_SLAB", "FLZ_SLAB_PACK", "FLZ_SLAB_PDL"):
+              "FLZ_TS_UPDATE", "FLZ_PLAN_AHEAD", "FLZ_ST_SLAB", "FLZ_SLAB_PACK", "FLZ_SLAB_PDL",
+              "FLZ_MS", "FLZ_MS_K", "FLZ_MS_CORE", "FLZ_MS_ROWS"):
         env.pop(k, None)
     env.update(env_extra)
     p = subprocess.run([sys.executable, "-c", code, *args], env=env, capture_output=True,
@@ -205,6 +206,43 @@ def test_tile_kernel_on_row_slabs_bit_identical_to_warp_kernel():
             assert v == warp[k], k
             assert v == small[k], k
             assert v == plain[k], k
+
+
+MS_CODE = r'''
+import sys, json, hashlib
+sys.path.insert(0, %r)
+import numpy as np
+from paper_2409_15053_b200 import Context, DeviceMatrix, matrices as M, solver as S
+ctx = Context(0)
+out = {}
+for name, gen in (("lap2d200", lambda: M.laplacian2d(200)), ("lap2d77", lambda: M.laplacian2d(77)),
+                  ("lap2d33", lambda: M.laplacian2d(33)), ("lap2d300", lambda: M.laplacian2d(300)),
+                  ("lap3d12", lambda: M.laplacian3d(12))):
+    n, rp, ci, va = gen()
+    A = DeviceMatrix(ctx, n, rp, ci, va)
+    for m in (1, 2, 3, 4, 5, 6, 9, 10, 50):
+        cf = S.indicator_coefficients(-0.3, 0.25, m)
+        for r in (1, 3, 4, 6):
+            X = np.random.default_rng(r + m).standard_normal((n, r))
+            Y = A.filter_apply(cf, 4.0, 4.5, X)
+            out["%%s_m%%d_r%%d" %% (name, m, r)] = hashlib.sha1(np.ascontiguousarray(Y).tobytes()).hexdigest()
+out["launches"] = ctx.launches
+print(json.dumps(out))
+''' % ROOT
+
+
+def test_multistep_stencil_launches_bit_identical_to_single_steps():
+    """clenshaw_multistep_stencil (K Clenshaw steps of a short-reach stencil per launch, halo
+    rows recomputed per CTA) against one launch per step: bit-identical filter outputs for every
+    degree (leftover steps, m < K), column count, K and core size; fewer launches."""
+    one = run(MS_CODE, {"FLZ_MS": "0"})
+    for env in ({}, {"FLZ_MS": "1"}, {"FLZ_MS": "1", "FLZ_MS_K": "2"}, {"FLZ_MS": "1", "FLZ_MS_K": "8"},
+                {"FLZ_MS": "1", "FLZ_MS_K": "3", "FLZ_MS_CORE": "1024"}):
+        got = run(MS_CODE, env)
+        assert got["launches"] < one["launches"], env
+        for k, v in one.items():
+            if k != "launches":
+                assert got[k] == v, (env, k)
 
 
 HY_CODE = r'''
