@@ -173,7 +173,7 @@ int flz_plan_p2(const flz_plan* plan, int64_t* sizes, int64_t* ptr, int32_t* col
 int flz_plan_hy(const flz_plan* plan, int64_t* sizes, int64_t* slices, int32_t* cols,
                 double* uvval, double* gval, double* diag, int64_t* tasks, int32_t* dcols,
                 double* dval, int32_t* sell_rows);
-/* tile plan of the TMA-staged stencil kernel (constant-coefficient stencils on one rank;
+/* tile plan of the TMA-staged stencil kernel (constant-coefficient stencils, one rank or row slabs;
  * host/plan.hpp), for host-side checks: info[30] = {tile_rows, segments, seg_base[8],
  * seg_len[8], seg_start[8], staged elements per column, staged element of offset 0,
  * doubles in pairs, 0}; info[1] == 0: the matrix has no tile plan.  pairs: 16 doubles per
