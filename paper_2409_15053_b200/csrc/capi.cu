@@ -219,13 +219,14 @@ void halo_begin(const flz_matrix* A, int R, int S, double* Y1) {
   FLZ_CUDA(cudaEventRecord(ctx->ev_halo_ready, ctx->stream));
   FLZ_CUDA(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_halo_ready, 0));
   constexpr size_t D = sizeof(double);
-  // FLZ_HALO_DRY=1 (timing experiments on one GPU, WRONG results): pack, events and the phase
-  // split stay, the transfers are skipped — the compute side of one rank of a slab run
+  // FLZ_HALO_DRY=1 (timing experiments on one GPU through the loopback transport, WRONG
+  // results): pack, events and the phase split stay, the transfers are skipped — the compute
+  // side of one rank of a slab run
   static const bool dry = [] {
     const char* e = std::getenv("FLZ_HALO_DRY");
     return e && e[0] == '1';
   }();
-  if (dry) {
+  if (dry && ctx->hub) {   // loopback contexts only: never on a production (NCCL) context
     FLZ_CUDA(cudaEventRecord(ctx->ev_halo_done, ctx->comm_stream));
     return;
   }
