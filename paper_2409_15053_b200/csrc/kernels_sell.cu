@@ -1153,6 +1153,11 @@ __global__ void __launch_bounds__(768)
 struct StepCoeffs {
   double b[8];
 };
+__device__ __forceinline__ void ms_cp_async8(double* dst_smem, const double* src, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst_smem);
+  const int bytes = valid ? 8 : 0;   // 0: the destination is zero filled
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(bytes) : "memory");
+}
 template <int R>
 __global__ void __launch_bounds__(1024)
     clenshaw_multistep_stencil(const __grid_constant__ StencilTiles G,
@@ -1194,17 +1199,22 @@ __global__ void __launch_bounds__(1024)
     if (p == 0) pnuv[q] = nuv;
   }
   pdl_wait();
+  // the window: 8-byte cp.async (zero fill outside the matrix) — every element of the window
+  // is in flight at once, no registers staged
   for (int i = threadIdx.x; i < W; i += blockDim.x) {
     const int64_t row = w0 + i;
     const bool in = row >= 0 && row < nl;
+    const int64_t at = in ? row : 0;
 #pragma unroll
     for (int k = 0; k < R; ++k) {
-      ybuf[(0 * R + k) * W + i] = in ? Y2[(int64_t)k * ldy + row] : 0.0;   // y_{j+1}
-      ybuf[(1 * R + k) * W + i] = in ? Y1[(int64_t)k * ldy + row] : 0.0;   // y_j
+      ms_cp_async8(ybuf + (0 * R + k) * W + i, Y2 + (int64_t)k * ldy + at, in);   // y_{j+1}
+      ms_cp_async8(ybuf + (1 * R + k) * W + i, Y1 + (int64_t)k * ldy + at, in);   // y_j
+      ms_cp_async8(xs + k * W + i, X + (int64_t)k * ldx + at, in);
       ybuf[(2 * R + k) * W + i] = 0.0;
-      xs[k * W + i] = in ? X[(int64_t)k * ldx + row] : 0.0;
     }
   }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncthreads();
   int prev = 0, cur = 1, next = 2;
   for (int s = 1; s <= K; ++s) {
